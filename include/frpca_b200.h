@@ -1,0 +1,150 @@
+/*
+ * frpca_b200.h — C ABI of the B200-native frPCA / frPCAt hot path
+ * (arXiv 1810.06825; reference: /root/reference/proj/include/frpca/*.hpp).
+ *
+ * The reference has no FFI: its boundary is the header-only C++ template API
+ * of randsvd.hpp (frpca :229-232, frpcat :281-284, auto_pca :339-341) over
+ * SparseMatrixCsr<double> (sparse_matrix.hpp:19-150). This header is the thin
+ * C layer the drop-in C++ API (include/frpca/frpca.hpp) and the Python host
+ * mirror (paper_1810_06825_b200/) call; every entry point names the
+ * reference interface it replaces. Plain pointers and sizes only.
+ *
+ * Conventions
+ *  - Host dense matrices are COLUMN-MAJOR (Eigen's layout, types.hpp:12-16).
+ *    Device-resident variants (FRPCA_FLAG_DEVICE_IO) use the same layout.
+ *  - Sparse input is the reference CSR: int64 row_ptr (rows+1), int64
+ *    col_idx (nnz, strictly increasing per row), double values (nnz).
+ *  - Status: 0 ok; 2 invalid argument (std::invalid_argument via
+ *    detail::require, types.hpp:45-47); 3 I/O; 4 numerical
+ *    (frpca::NumericalError, types.hpp:27-30); 5 CUDA/NCCL failure.
+ *    These equal the reference CLI's exit codes (frpca_cli.cpp:33-35).
+ *    The message is available from frpca_last_error() (thread-local).
+ */
+#ifndef FRPCA_B200_H
+#define FRPCA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FRPCA_OK 0
+#define FRPCA_ERR_INVALID 2
+#define FRPCA_ERR_IO 3
+#define FRPCA_ERR_NUMERICAL 4
+#define FRPCA_ERR_CUDA 5
+
+/* PcaAlgorithm (randsvd.hpp:14): only the fast algorithms are on the path. */
+#define FRPCA_ALGO_FRPCA 0  /* Alg. 5, rows <= cols (randsvd.hpp:224-276) */
+#define FRPCA_ALGO_FRPCAT 1 /* Alg. 6, rows >= cols (randsvd.hpp:278-328) */
+#define FRPCA_ALGO_AUTO 2   /* shape dispatch (randsvd.hpp:330-351) */
+
+/* frpca_run flags */
+#define FRPCA_FLAG_DEVICE_IO 1u   /* omega/U/S/V/basis pointers are device pointers */
+#define FRPCA_FLAG_HOST_OMEGA 2u  /* draw Omega with the host libstdc++ generator
+                                     (default: bit-compatible device generator) */
+
+typedef struct frpca_ctx frpca_ctx;   /* device, stream, cuSOLVER handle, NCCL comm */
+typedef struct frpca_dmat frpca_dmat; /* device CSR + transposed CSR, built at load */
+
+/* PcaConfig (randsvd.hpp:28-40); `deterministic` is unused by the reference
+ * algorithms too (kernels here are always deterministic). */
+typedef struct {
+    int64_t k;
+    int64_t oversample;
+    int64_t passes; /* q >= 2, total passes over A */
+    int64_t power;  /* baselines' p; unused on this path */
+    uint64_t seed;
+    int32_t deterministic;
+    uint32_t flags; /* FRPCA_FLAG_* */
+} frpca_config;
+
+/* RunStats (randsvd.hpp:42-53) + load time of the upload that built dmat. */
+typedef struct {
+    double sketch_seconds;
+    double power_seconds;
+    double finalize_seconds;
+    uint64_t passes_over_matrix;
+} frpca_stats;
+
+/* ---- library / context ---------------------------------------------------- */
+const char* frpca_last_error(void);
+int frpca_version(void);
+int frpca_ctx_create(int device, frpca_ctx** out);
+/* Multi-GPU: one process per GPU; `nccl_id` is the 128-byte ncclUniqueId from
+ * frpca_nccl_unique_id() on rank 0, broadcast by the caller. */
+int frpca_nccl_unique_id(void* out128);
+int frpca_ctx_create_dist(int device, int rank, int world, const void* nccl_id128,
+                          frpca_ctx** out);
+int frpca_ctx_destroy(frpca_ctx* ctx);
+int frpca_ctx_sync(frpca_ctx* ctx);
+/* Pinned host memory helpers (for zero-staging host buffers). */
+int frpca_host_alloc(uint64_t bytes, void** out);
+int frpca_host_free(void* p);
+
+/* ---- sparse matrix (replaces SparseMatrixCsr<double>, sparse_matrix.hpp:19-150)
+ * Uploads and validates (same checks and messages as validate(), :125-142),
+ * then builds the transposed CSR on the device (sparse_matrix.hpp:242-267,
+ * moved to load time) and the load-balanced work lists of both. Host arrays
+ * may be pageable or pinned. */
+int frpca_dmat_upload(frpca_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz,
+                      const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                      frpca_dmat** out);
+/* Multi-GPU shard: this rank holds rows [row0, row0+rows) of a global
+ * (grows x gcols) matrix (frpcat row-block sharding), or, with
+ * col_shard = 1, columns [col0, col0+cols) of a (grows x gcols) matrix given
+ * as a local CSR with LOCAL column ids (frpca column-block sharding). */
+int frpca_dmat_upload_shard(frpca_ctx* ctx, int64_t grows, int64_t gcols, int32_t col_shard,
+                            int64_t offset, int64_t rows, int64_t cols, int64_t nnz,
+                            const int64_t* row_ptr, const int64_t* col_idx,
+                            const double* values, frpca_dmat** out);
+int frpca_dmat_destroy(frpca_dmat* A);
+int frpca_dmat_info(const frpca_dmat* A, int64_t* rows, int64_t* cols, int64_t* nnz);
+/* passCount()/resetPassCount() (sparse_matrix.hpp:119-122). */
+int frpca_dmat_pass_count(const frpca_dmat* A, uint64_t* out);
+int frpca_dmat_reset_pass_count(frpca_dmat* A);
+/* Copies the device transposed CSR back (test helper, mirrors transpose()). */
+int frpca_dmat_get_transpose(const frpca_dmat* A, int64_t* t_row_ptr, int64_t* t_col_idx,
+                             double* t_values);
+
+/* ---- kernels (sparse_matrix.hpp:177-240, dense_kernels.hpp:16-174) --------- */
+/* Y = A*X (transpose=0, spmm :177-206) or Y = A^T*X (transpose=1,
+ * spmm_transpose :208-240). X: (A.cols or A.rows) x ncols column-major with
+ * leading dimension ldx; Y column-major. One pass over A. */
+int frpca_spmm(frpca_ctx* ctx, frpca_dmat* A, int transpose, const double* X, int64_t ldx,
+               int64_t ncols, double* Y);
+/* gaussian_matrix (dense_kernels.hpp:16-28): column-major rows x cols from
+ * mt19937_64(seed) + libstdc++ normal_distribution, drawn on the device. */
+int frpca_gaussian_matrix(frpca_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed,
+                          double* out);
+/* lu_basis (dense_kernels.hpp:50-116): X = P^T L of M (m x l, m >= l). */
+int frpca_lu_basis(frpca_ctx* ctx, int64_t m, int64_t l, const double* M, double* X);
+/* eig_svd (dense_kernels.hpp:145-174): U m x n, S ascending (n), V n x n. */
+int frpca_eig_svd(frpca_ctx* ctx, int64_t m, int64_t n, const double* A, double* U, double* S,
+                  double* V);
+
+/* ---- algorithms (randsvd.hpp:224-351) -------------------------------------
+ * algorithm: FRPCA_ALGO_*. omega: optional injected sketch (column-major,
+ * omega_rows x omega_cols; the shape check of sketch_matrix, randsvd.hpp:68-74).
+ * Outputs: U rows x k, S k (descending), V cols x k, column-major; basis
+ * (nullable) receives Q (RunStats::capture_basis). stats, dispatched nullable.
+ * With a distributed ctx, each rank passes its shard; U (frpcat) / V (frpca)
+ * receive the rank's local rows, the replicated factor is written on every rank. */
+int frpca_run(frpca_ctx* ctx, frpca_dmat* A, int algorithm, const frpca_config* cfg,
+              const double* omega, int64_t omega_rows, int64_t omega_cols, double* U,
+              double* S, double* V, double* basis, frpca_stats* stats, int* dispatched);
+
+/* ---- timing helpers (device-side events on the ctx stream) ---------------- */
+/* Last-run per-kernel accounting: name, launches, total device ms, algorithmic
+ * bytes and flops (for the roofline report). idx out of range -> 2. */
+int frpca_profile_enable(frpca_ctx* ctx, int enable);
+int frpca_profile_count(frpca_ctx* ctx, int* n);
+int frpca_profile_get(frpca_ctx* ctx, int idx, const char** name, int64_t* launches,
+                      double* ms, double* bytes, double* flops);
+int frpca_profile_reset(frpca_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRPCA_B200_H */

@@ -1,0 +1,268 @@
+"""ctypes bindings of oracle/_build/liboracle.so (TEST INFRASTRUCTURE ONLY).
+
+Matrices cross this boundary column-major (Fortran order), the layout of the
+reference's Eigen matrices (types.hpp:12-16). Errors map exactly as the
+reference's exceptions do: status 2 -> ValueError (std::invalid_argument),
+status 4 -> NumericalError (frpca::NumericalError, types.hpp:27).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "_build", "liboracle.so")
+
+_i64 = C.c_int64
+_u64 = C.c_uint64
+_dp = C.POINTER(C.c_double)
+_lp = C.POINTER(C.c_int64)
+_vp = C.c_void_p
+
+
+class NumericalError(RuntimeError):
+    """Mirror of frpca::NumericalError (types.hpp:27-30)."""
+
+
+def build() -> str:
+    if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(
+            os.path.join(_HERE, "oracle.cpp")):
+        subprocess.check_call(["make", "-s", "-C", _HERE])
+    return _SO
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            build()
+        L = C.CDLL(_SO)
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_mix_seed.restype = _u64
+        L.orc_mix_seed.argtypes = [_u64, _u64]
+        L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_gaussian_matrix.argtypes = [_i64, _i64, _u64, _dp]
+        L.orc_csr_create.argtypes = [_i64, _i64, _i64, _lp, _lp, _dp, C.POINTER(_vp)]
+        L.orc_csr_from_triplets.argtypes = [_i64, _i64, _i64, _lp, _lp, _dp, C.POINTER(_vp)]
+        L.orc_csr_random_sparse.argtypes = [_i64, _i64, C.c_double, _u64, C.POINTER(_vp)]
+        L.orc_csr_transpose.argtypes = [_vp, C.POINTER(_vp)]
+        L.orc_csr_info.argtypes = [_vp, _lp, _lp, _lp]
+        L.orc_csr_copy.argtypes = [_vp, _lp, _lp, _dp]
+        L.orc_csr_pass_count.restype = _u64
+        L.orc_csr_pass_count.argtypes = [_vp]
+        L.orc_csr_reset_pass_count.argtypes = [_vp]
+        L.orc_csr_destroy.argtypes = [_vp]
+        L.orc_spmm.argtypes = [_vp, _dp, _i64, _i64, _dp]
+        L.orc_spmm_transpose.argtypes = [_vp, _dp, _i64, _i64, _dp]
+        L.orc_lu_basis.argtypes = [_i64, _i64, _dp, _dp]
+        L.orc_eig_svd.argtypes = [_i64, _i64, _dp, _dp, _dp, _dp]
+        L.orc_eig_sym.argtypes = [_i64, _dp, _dp, _dp]
+        L.orc_gram_lower.argtypes = [_i64, _i64, _dp, _dp]
+        L.orc_oracle_svd.argtypes = [_i64, _i64, _dp, _dp, _dp, _dp]
+        L.orc_pca.argtypes = [_vp, C.c_int, _i64, _i64, _i64, _i64, _u64, _dp, _i64, _i64,
+                              _dp, _dp, _dp, _dp, _dp, C.POINTER(C.c_int)]
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status == 0:
+        return
+    msg = lib().orc_last_error().decode()
+    if status == 2:
+        raise ValueError(msg)
+    if status == 4:
+        raise NumericalError(msg)
+    raise RuntimeError(msg)
+
+
+def _d(a):
+    return a.ctypes.data_as(_dp)
+
+
+def _l(a):
+    return a.ctypes.data_as(_lp)
+
+
+def set_threads(n: int):
+    lib().orc_set_threads(int(n))
+
+
+def mix_seed(seed: int, tag: int) -> int:
+    return int(lib().orc_mix_seed(seed, tag))
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """dense_kernels.hpp:16-28; returns a Fortran-ordered rows x cols array."""
+    out = np.empty((rows, cols), dtype=np.float64, order="F")
+    _check(lib().orc_gaussian_matrix(rows, cols, seed, _d(out)))
+    return out
+
+
+class Csr:
+    """Oracle SparseMatrixCsr<double> (sparse_matrix.hpp:19-150)."""
+
+    def __init__(self, handle):
+        self._h = _vp(handle)
+        r, c, n = _i64(), _i64(), _i64()
+        lib().orc_csr_info(self._h, C.byref(r), C.byref(c), C.byref(n))
+        self.rows, self.cols, self.nnz = r.value, c.value, n.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and _lib is not None:
+            _lib.orc_csr_destroy(self._h)
+            self._h = None
+
+    @staticmethod
+    def create(rows, cols, row_ptr, col_idx, values) -> "Csr":
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+        va = np.ascontiguousarray(values, dtype=np.float64)
+        h = _vp()
+        _check(lib().orc_csr_create(rows, cols, len(va), _l(rp), _l(ci), _d(va), C.byref(h)))
+        return Csr(h.value)
+
+    @staticmethod
+    def from_triplets(rows, cols, triplets) -> "Csr":
+        t = list(triplets)
+        r = np.array([x[0] for x in t], dtype=np.int64)
+        c = np.array([x[1] for x in t], dtype=np.int64)
+        v = np.array([x[2] for x in t], dtype=np.float64)
+        h = _vp()
+        _check(lib().orc_csr_from_triplets(rows, cols, len(t), _l(r), _l(c), _d(v), C.byref(h)))
+        return Csr(h.value)
+
+    @staticmethod
+    def random_sparse(rows, cols, density, seed) -> "Csr":
+        """test_support.hpp:46-55 (same libstdc++ stream => same matrix)."""
+        h = _vp()
+        _check(lib().orc_csr_random_sparse(rows, cols, density, seed, C.byref(h)))
+        return Csr(h.value)
+
+    def transpose(self) -> "Csr":
+        h = _vp()
+        _check(lib().orc_csr_transpose(self._h, C.byref(h)))
+        return Csr(h.value)
+
+    def arrays(self):
+        rp = np.empty(self.rows + 1, dtype=np.int64)
+        ci = np.empty(self.nnz, dtype=np.int64)
+        va = np.empty(self.nnz, dtype=np.float64)
+        lib().orc_csr_copy(self._h, _l(rp), _l(ci), _d(va))
+        return rp, ci, va
+
+    def to_dense(self) -> np.ndarray:
+        rp, ci, va = self.arrays()
+        D = np.zeros((self.rows, self.cols))
+        for i in range(self.rows):
+            D[i, ci[rp[i]:rp[i + 1]]] = va[rp[i]:rp[i + 1]]
+        return D
+
+    def pass_count(self) -> int:
+        return int(lib().orc_csr_pass_count(self._h))
+
+    def reset_pass_count(self):
+        lib().orc_csr_reset_pass_count(self._h)
+
+
+def spmm(A: Csr, X: np.ndarray) -> np.ndarray:
+    X = np.asfortranarray(X, dtype=np.float64)
+    if X.ndim != 2 or X.shape[0] != A.cols:
+        raise ValueError("spmm: inner dimensions do not match")
+    Y = np.empty((A.rows, X.shape[1]), order="F")
+    _check(lib().orc_spmm(A._h, _d(X), max(X.shape[0], 1), X.shape[1], _d(Y)))
+    return Y
+
+
+def spmm_transpose(A: Csr, Y: np.ndarray) -> np.ndarray:
+    Y = np.asfortranarray(Y, dtype=np.float64)
+    if Y.ndim != 2 or Y.shape[0] != A.rows:
+        raise ValueError("spmm_transpose: inner dimensions do not match")
+    Z = np.empty((A.cols, Y.shape[1]), order="F")
+    _check(lib().orc_spmm_transpose(A._h, _d(Y), max(Y.shape[0], 1), Y.shape[1], _d(Z)))
+    return Z
+
+
+def lu_basis(M: np.ndarray) -> np.ndarray:
+    M = np.asfortranarray(M, dtype=np.float64)
+    X = np.empty(M.shape, order="F")
+    _check(lib().orc_lu_basis(M.shape[0], M.shape[1], _d(M), _d(X)))
+    return X
+
+
+def eig_svd(A: np.ndarray):
+    """dense_kernels.hpp:145-174: returns (U, S ascending, V)."""
+    A = np.asfortranarray(A, dtype=np.float64)
+    m, n = A.shape
+    U = np.empty((m, n), order="F")
+    S = np.empty(n)
+    V = np.empty((n, n), order="F")
+    _check(lib().orc_eig_svd(m, n, _d(A), _d(U), _d(S), _d(V)))
+    return U, S, V
+
+
+def eig_sym(B: np.ndarray):
+    B = np.asfortranarray(B, dtype=np.float64)
+    n = B.shape[0]
+    V = np.empty((n, n), order="F")
+    D = np.empty(n)
+    _check(lib().orc_eig_sym(n, _d(B), _d(V), _d(D)))
+    return V, D
+
+
+def gram_lower(W: np.ndarray) -> np.ndarray:
+    W = np.asfortranarray(W, dtype=np.float64)
+    m, n = W.shape
+    B = np.empty((n, n), order="F")
+    _check(lib().orc_gram_lower(m, n, _d(W), _d(B)))
+    return B
+
+
+def oracle_svd(A: np.ndarray):
+    """validation.hpp:79-121 one-sided Jacobi: (U, S descending, V)."""
+    A = np.asfortranarray(A, dtype=np.float64)
+    m, n = A.shape
+    r = min(m, n)
+    U = np.empty((m, r), order="F")
+    S = np.empty(r)
+    V = np.empty((n, r), order="F")
+    _check(lib().orc_oracle_svd(m, n, _d(A), _d(U), _d(S), _d(V)))
+    return U, S, V
+
+
+FRPCA, FRPCAT, AUTO = 0, 1, 2
+
+
+def pca(A: Csr, algorithm: int, k: int, oversample: int = 5, passes: int = 2, seed: int = 0,
+        omega: np.ndarray | None = None, power: int = 0, want_basis: bool = False):
+    """frpca / frpcat / auto_pca (randsvd.hpp:224-351).
+
+    Returns dict(U, S, V, stats, basis, dispatched)."""
+    l = k + oversample
+    algo = algorithm
+    if algo == AUTO:
+        algo = FRPCA if A.rows < A.cols else FRPCAT
+    kk = max(k, 0)
+    U = np.empty((A.rows, kk), order="F")
+    S = np.empty(kk)
+    V = np.empty((A.cols, kk), order="F")
+    stats = np.zeros(4)
+    qrows = A.rows if algo == FRPCA else A.cols
+    basis = np.empty((qrows, max(l, 0)), order="F") if want_basis else None
+    disp = C.c_int(-1)
+    om_p, om_r, om_c = None, 0, 0
+    if omega is not None:
+        omega = np.asfortranarray(omega, dtype=np.float64)
+        om_p, (om_r, om_c) = _d(omega), omega.shape
+    _check(lib().orc_pca(A._h, algorithm, k, oversample, passes, power, seed, om_p, om_r, om_c,
+                         _d(U), _d(S), _d(V), _d(stats),
+                         _d(basis) if basis is not None else None, C.byref(disp)))
+    return dict(U=U, S=S, V=V, basis=basis, dispatched=disp.value,
+                stats=dict(sketch_seconds=stats[0], power_seconds=stats[1],
+                           finalize_seconds=stats[2], passes_over_matrix=int(stats[3])))

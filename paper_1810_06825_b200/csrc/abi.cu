@@ -1,0 +1,406 @@
+// extern "C" boundary (include/frpca_b200.h). Exceptions never cross it:
+// each entry point maps fb::InvalidArgument -> 2, fb::NumericalError -> 4,
+// CUDA/NCCL/cuSOLVER failures -> 5 and keeps the message for
+// frpca_last_error(), which the C++ drop-in rethrows as the reference's
+// std::invalid_argument / frpca::NumericalError.
+#include <cstring>
+#include <string>
+
+#include "driver.cuh"
+
+using namespace fb;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FRPCA_OK;
+    } catch (const InvalidArgument& e) {
+        g_err = e.what();
+        return FRPCA_ERR_INVALID;
+    } catch (const NumericalError& e) {
+        g_err = e.what();
+        return FRPCA_ERR_NUMERICAL;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return FRPCA_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        g_err = "frpca_b200: host allocation failed";
+        return FRPCA_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FRPCA_ERR_CUDA;
+    }
+}
+
+void check_ctx(const frpca_ctx* c) { require(c != nullptr, "frpca_b200: null context"); }
+
+}  // namespace
+
+struct frpca_ctx : fb::Ctx {};
+struct frpca_dmat : fb::DMat {};
+
+namespace fb {
+
+cudaEvent_t Ctx::get_event() {
+    if (!event_pool.empty()) {
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    FB_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void Ctx::flush_profile() {
+    if (pending.empty()) return;
+    FB_CUDA(cudaStreamSynchronize(stream));
+    for (auto& p : pending) {
+        float ms = 0.f;
+        FB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        ProfAgg& g = agg[p.name];
+        g.launches += 1;
+        g.ms += ms;
+        g.bytes += p.bytes;
+        g.flops += p.flops;
+        event_pool.push_back(p.a);
+        event_pool.push_back(p.b);
+    }
+    pending.clear();
+}
+
+Prof::Prof(Ctx& ctx, const char* name, double bytes, double flops) : c(ctx) {
+    if (!c.prof) return;
+    Ctx::Pending p;
+    p.name = name;
+    p.a = c.get_event();
+    p.b = c.get_event();
+    p.bytes = bytes;
+    p.flops = flops;
+    cudaEventRecord(p.a, c.stream);
+    idx = c.pending.size();
+    c.pending.push_back(p);
+}
+
+Prof::~Prof() {
+    if (idx != size_t(-1) && idx < c.pending.size()) cudaEventRecord(c.pending[idx].b, c.stream);
+}
+
+}  // namespace fb
+
+namespace {
+
+// host column-major (rows x cols, ld) -> device row-major rows x cols
+void upload_colmajor(Ctx& c, const double* h, int64_t rows, int64_t cols, int64_t ld, double* d_rm) {
+    DBuf<double> t(size_t(rows * cols), c.stream);
+    if (ld == rows) {
+        FB_CUDA(cudaMemcpyAsync(t.get(), h, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, c.stream));
+    } else {
+        FB_CUDA(cudaMemcpy2DAsync(t.get(), sizeof(double) * rows, h, sizeof(double) * ld,
+                                  sizeof(double) * rows, cols, cudaMemcpyHostToDevice, c.stream));
+    }
+    transpose_device(c, t.get(), cols, rows, d_rm);
+}
+
+// device row-major rows x cols -> host column-major
+void download_colmajor(Ctx& c, const double* d_rm, int64_t rows, int64_t cols, double* h) {
+    DBuf<double> t(size_t(rows * cols), c.stream);
+    transpose_device(c, d_rm, rows, cols, t.get());
+    FB_CUDA(cudaMemcpyAsync(h, t.get(), sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, c.stream));
+    FB_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* frpca_last_error(void) { return g_err.c_str(); }
+int frpca_version(void) { return 10000; }
+
+int frpca_ctx_create(int device, frpca_ctx** out) {
+    return guarded([&] {
+        require(out != nullptr, "frpca_ctx_create: null output");
+        FB_CUDA(cudaSetDevice(device));
+        auto* c = new frpca_ctx;
+        c->device = device;
+        try {
+            FB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS)
+                throw CudaError("cusolverDnCreate failed");
+            cusolverDnSetStream(c->solver, c->stream);
+            FB_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+            // keep freed stream-ordered allocations pooled between calls
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int frpca_nccl_unique_id(void* out128) {
+    return guarded([&] { comm_unique_id(out128); });
+}
+
+int frpca_ctx_create_dist(int device, int rank, int world, const void* nccl_id128, frpca_ctx** out) {
+    return guarded([&] {
+        require(world >= 1 && rank >= 0 && rank < world, "frpca_ctx_create_dist: bad rank/world");
+        int st = frpca_ctx_create(device, out);
+        if (st != FRPCA_OK) throw CudaError(g_err);
+        comm_init(**out, rank, world, nccl_id128);
+    });
+}
+
+int frpca_ctx_destroy(frpca_ctx* c) {
+    return guarded([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        comm_destroy(*c);
+        for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+        for (auto e : c->event_pool) cudaEventDestroy(e);
+        if (c->solver) cusolverDnDestroy(c->solver);
+        if (c->stream) cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int frpca_ctx_sync(frpca_ctx* c) {
+    return guarded([&] {
+        check_ctx(c);
+        FB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int frpca_host_alloc(uint64_t bytes, void** out) {
+    return guarded([&] { FB_CUDA(cudaMallocHost(out, bytes ? bytes : 1)); });
+}
+int frpca_host_free(void* p) {
+    return guarded([&] { if (p) FB_CUDA(cudaFreeHost(p)); });
+}
+
+int frpca_dmat_upload(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                      const int64_t* col_idx, const double* values, frpca_dmat** out) {
+    return frpca_dmat_upload_shard(c, rows, cols, 0, 0, rows, cols, nnz, row_ptr, col_idx, values, out);
+}
+
+int frpca_dmat_upload_shard(frpca_ctx* c, int64_t grows, int64_t gcols, int32_t col_shard,
+                            int64_t offset, int64_t rows, int64_t cols, int64_t nnz,
+                            const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                            frpca_dmat** out) {
+    return guarded([&] {
+        check_ctx(c);
+        require(out != nullptr, "frpca_dmat_upload: null output");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        if (col_shard) {
+            require(rows == grows && offset >= 0 && offset + cols <= gcols,
+                    "frpca_dmat_upload_shard: column block out of range");
+        } else {
+            require(cols == gcols && offset >= 0 && offset + rows <= grows,
+                    "frpca_dmat_upload_shard: row block out of range");
+        }
+        auto* M = new frpca_dmat;
+        M->ctx = c;
+        M->grows = grows;
+        M->gcols = gcols;
+        M->offset = offset;
+        M->col_shard = col_shard;
+        try {
+            dcsr_upload_build(*c, *M, rows, cols, nnz, row_ptr, col_idx, values);
+        } catch (...) {
+            delete M;
+            throw;
+        }
+        *out = M;
+    });
+}
+
+int frpca_dmat_destroy(frpca_dmat* M) {
+    return guarded([&] {
+        if (!M) return;
+        cudaSetDevice(M->ctx->device);
+        delete M;
+    });
+}
+
+int frpca_dmat_info(const frpca_dmat* M, int64_t* rows, int64_t* cols, int64_t* nnz) {
+    return guarded([&] {
+        require(M != nullptr, "frpca_dmat_info: null matrix");
+        if (rows) *rows = M->A.rows;
+        if (cols) *cols = M->A.cols;
+        if (nnz) *nnz = M->A.nnz;
+    });
+}
+
+int frpca_dmat_pass_count(const frpca_dmat* M, uint64_t* out) {
+    return guarded([&] {
+        require(M != nullptr && out != nullptr, "frpca_dmat_pass_count: null argument");
+        *out = M->passes.load(std::memory_order_relaxed);
+    });
+}
+
+int frpca_dmat_reset_pass_count(frpca_dmat* M) {
+    return guarded([&] {
+        require(M != nullptr, "frpca_dmat_reset_pass_count: null matrix");
+        M->passes.store(0, std::memory_order_relaxed);
+    });
+}
+
+int frpca_dmat_get_transpose(const frpca_dmat* M, int64_t* rp, int64_t* ci, double* v) {
+    return guarded([&] {
+        require(M != nullptr, "frpca_dmat_get_transpose: null matrix");
+        Ctx& c = *M->ctx;
+        std::lock_guard<std::mutex> lk(c.mu);
+        FB_CUDA(cudaSetDevice(c.device));
+        download_csr(c, M->At, rp, ci, v);
+    });
+}
+
+int frpca_spmm(frpca_ctx* c, frpca_dmat* M, int transpose, const double* X, int64_t ldx,
+               int64_t ncols, double* Y) {
+    return guarded([&] {
+        check_ctx(c);
+        require(M != nullptr, "spmm: null matrix");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        const DCsr& A = transpose ? M->At : M->A;
+        const int64_t nin = A.cols, nout = A.rows;
+        require(ncols >= 0, "spmm: negative column count");
+        require(ncols == 0 || ldx >= nin, "spmm: leading dimension too small");
+        if (ncols == 0 || nout == 0) {
+            M->passes.fetch_add(1);
+            return;
+        }
+        DBuf<double> dX(size_t(std::max<int64_t>(nin, 1) * ncols), c->stream);
+        DBuf<double> dY(size_t(nout * ncols), c->stream);
+        if (nin) upload_colmajor(*c, X, nin, ncols, ldx, dX.get());
+        spmm_pass(*c, *M, transpose != 0, dX.get(), ncols, dY.get());
+        download_colmajor(*c, dY.get(), nout, ncols, Y);
+    });
+}
+
+int frpca_gaussian_matrix(frpca_ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        require(rows >= 1 && cols >= 1, "gaussian_matrix: dimensions must be >= 1");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        DBuf<double> d(size_t(rows * cols), c->stream);
+        gaussian_stream_device(*c, seed, rows * cols, d.get());
+        FB_CUDA(cudaMemcpyAsync(out, d.get(), sizeof(double) * rows * cols, cudaMemcpyDeviceToHost,
+                                c->stream));
+        FB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int frpca_lu_basis(frpca_ctx* c, int64_t m, int64_t l, const double* Mh, double* X) {
+    return guarded([&] {
+        check_ctx(c);
+        require(m >= l && l >= 1, "lu_basis: input must be tall (rows >= cols >= 1)");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        DBuf<double> W(size_t(m * l), c->stream);
+        upload_colmajor(*c, Mh, m, l, m, W.get());
+        lu_basis_device(*c, W.get(), m, l);
+        download_colmajor(*c, W.get(), m, l, X);
+    });
+}
+
+int frpca_eig_svd(frpca_ctx* c, int64_t m, int64_t n, const double* Ah, double* U, double* S,
+                  double* V) {
+    return guarded([&] {
+        check_ctx(c);
+        require(m >= n && n >= 1, "eig_svd: input must be tall (rows >= cols >= 1)");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        DBuf<double> W(size_t(m * n), c->stream), Ud(size_t(m * n), c->stream);
+        upload_colmajor(*c, Ah, m, n, m, W.get());
+        EigWork e;
+        e.run(*c, W.get(), m, n);
+        DBuf<double> Mf(size_t(n * n), c->stream), Sd(size_t(n), c->stream);
+        e.factor(*c, 0, int(n), int(n), false, true, Mf.get());
+        gemm_device(*c, W.get(), m, n, Mf.get(), n, Ud.get(), n, false);
+        e.singular_values(*c, 0, int(n), false, Sd.get());
+        FB_CUDA(cudaMemcpyAsync(S, Sd.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        FB_CUDA(cudaMemcpyAsync(V, e.B.get(), sizeof(double) * n * n, cudaMemcpyDeviceToHost, c->stream));
+        download_colmajor(*c, Ud.get(), m, n, U);
+    });
+}
+
+int frpca_run(frpca_ctx* c, frpca_dmat* M, int algorithm, const frpca_config* cfg, const double* omega,
+              int64_t omega_rows, int64_t omega_cols, double* U, double* S, double* V, double* basis,
+              frpca_stats* stats, int* dispatched) {
+    return guarded([&] {
+        check_ctx(c);
+        require(M != nullptr && cfg != nullptr, "frpca_run: null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        RunArgs a;
+        a.cfg = *cfg;
+        a.omega = omega;
+        a.omega_rows = omega_rows;
+        a.omega_cols = omega_cols;
+        a.U = U; a.S = S; a.V = V; a.basis = basis;
+        a.device_io = (cfg->flags & FRPCA_FLAG_DEVICE_IO) != 0;
+        int algo = algorithm;
+        if (algo == FRPCA_ALGO_AUTO) algo = (M->grows < M->gcols) ? FRPCA_ALGO_FRPCA : FRPCA_ALGO_FRPCAT;
+        require(algo == FRPCA_ALGO_FRPCA || algo == FRPCA_ALGO_FRPCAT, "frpca_run: unknown algorithm");
+        if (dispatched) *dispatched = algo;
+        if (algo == FRPCA_ALGO_FRPCA) run_frpca(*c, *M, a, stats);
+        else run_frpcat(*c, *M, a, stats);
+    });
+}
+
+int frpca_profile_enable(frpca_ctx* c, int enable) {
+    return guarded([&] {
+        check_ctx(c);
+        c->flush_profile();
+        c->prof = enable != 0;
+    });
+}
+
+int frpca_profile_reset(frpca_ctx* c) {
+    return guarded([&] {
+        check_ctx(c);
+        c->flush_profile();
+        c->agg.clear();
+    });
+}
+
+int frpca_profile_count(frpca_ctx* c, int* n) {
+    return guarded([&] {
+        check_ctx(c);
+        c->flush_profile();
+        c->agg_names.clear();
+        for (auto& kv : c->agg) c->agg_names.push_back(kv.first);
+        *n = int(c->agg_names.size());
+    });
+}
+
+int frpca_profile_get(frpca_ctx* c, int idx, const char** name, int64_t* launches, double* ms,
+                      double* bytes, double* flops) {
+    return guarded([&] {
+        check_ctx(c);
+        require(idx >= 0 && idx < int(c->agg_names.size()), "frpca_profile_get: index out of range");
+        const std::string& k = c->agg_names[size_t(idx)];
+        const ProfAgg& g = c->agg.at(k);
+        if (name) *name = k.c_str();
+        if (launches) *launches = g.launches;
+        if (ms) *ms = g.ms;
+        if (bytes) *bytes = g.bytes;
+        if (flops) *flops = g.flops;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// Shared plumbing for the B200 frPCA hot path: status codes, error capture,
+// device buffers. All panels on the device are ROW-MAJOR r x l (ld = l), so a
+// CSR nonzero gathers one contiguous l*8-byte row of the dense operand.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/frpca_b200.h"
+
+namespace fb {
+
+// Exceptions carried to the C-ABI boundary and mapped to FRPCA_ERR_* codes.
+struct InvalidArgument : std::runtime_error {
+    explicit InvalidArgument(const std::string& w) : std::runtime_error(w) {}
+};
+struct NumericalError : std::runtime_error {
+    explicit NumericalError(const std::string& w) : std::runtime_error(w) {}
+};
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+
+// detail::require of types.hpp:45-47: std::invalid_argument with the message.
+inline void require(bool cond, const char* msg) {
+    if (!cond) throw InvalidArgument(msg);
+}
+
+#define FB_CUDA(expr)                                                                    \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            throw ::fb::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e) +   \
+                                  " (" __FILE__ ":" + std::to_string(__LINE__) + ")");   \
+    } while (0)
+
+#define FB_LAUNCH_CHECK() FB_CUDA(cudaGetLastError())
+
+// Minimal owning device buffer (stream-ordered allocation).
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DBuf() = default;
+    DBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count, cudaStream_t stream) {
+        release();
+        s = stream;
+        n = count;
+        if (count) FB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+    }
+    void release() noexcept {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+}  // namespace fb

@@ -1,0 +1,316 @@
+// Device CSR at load time: upload + validation (sparse_matrix.hpp:125-142),
+// transposed CSR (sparse_matrix.hpp:242-267, moved from a test helper to the
+// load step so A^T*Y is a gather, never an atomic scatter), and the
+// load-balanced SpMM work lists of both.
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace fb {
+namespace {
+
+constexpr unsigned long long kNoError = ~0ull;
+
+// Row-level check of validate() (:131): row_ptr non-decreasing. Records the
+// first offending row (atomicMin keeps it deterministic).
+__global__ void k_check_rowptr(const int64_t* __restrict__ rp, int64_t m,
+                               unsigned long long* __restrict__ bad_row) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (rp[i] > rp[i + 1]) atomicMin(bad_row, (unsigned long long)i);
+}
+
+// Marks the first nonzero of each (valid) row with its row id; an inclusive
+// max-scan then yields the row id of every nonzero.
+__global__ void k_mark_rows(const int64_t* __restrict__ rp, int64_t m_valid,
+                            int32_t* __restrict__ mark) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m_valid;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (rp[i + 1] > rp[i]) mark[rp[i]] = int32_t(i);
+}
+
+// Per-nonzero checks of validate() (:132-138) fused with the int64 -> int32
+// narrowing of the column ids. Key = (row << 33) | (2*offset + kind) so the
+// minimum is the first failure in the reference's scan order.
+__global__ void k_check_cols(const int64_t* __restrict__ rp, const int32_t* __restrict__ rowid,
+                             const int64_t* __restrict__ col64, int64_t nnz_valid, int64_t ncols,
+                             int32_t* __restrict__ col32, unsigned long long* __restrict__ err) {
+    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < nnz_valid;
+         p += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t c = col64[p];
+        const int64_t r = rowid[p];
+        const int64_t off = p - rp[r];
+        if (c < 0 || c >= ncols) {
+            atomicMin(err, ((unsigned long long)r << 33) | (unsigned long long)(2 * off + 1));
+            col32[p] = 0;
+            continue;
+        }
+        col32[p] = int32_t(c);
+        if (off > 0 && !(col64[p - 1] < c))
+            atomicMin(err, ((unsigned long long)r << 33) | (unsigned long long)(2 * off + 2));
+    }
+}
+
+__global__ void k_iota(int32_t* __restrict__ x, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        x[i] = int32_t(i);
+}
+
+// Transposed entries from the stable column sort: entry k of A^T is original
+// nonzero perm[k]; its column id in A^T is the original row id.
+__global__ void k_gather_transpose(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowid,
+                                   const double* __restrict__ val, int64_t nnz,
+                                   int32_t* __restrict__ tcol, double* __restrict__ tval) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t p = perm[k];
+        tcol[k] = rowid[p];
+        tval[k] = val[p];
+    }
+}
+
+// t_rowptr[c] = lower_bound(sorted_keys, c), c in [0, n].
+__global__ void k_rowptr_from_sorted(const int32_t* __restrict__ keys, int64_t nnz, int64_t n,
+                                     int64_t* __restrict__ trp) {
+    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c <= n;
+         c += int64_t(gridDim.x) * blockDim.x) {
+        int64_t lo = 0, hi = nnz;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < c) lo = mid + 1; else hi = mid;
+        }
+        trp[c] = lo;
+    }
+}
+
+// ---- work lists --------------------------------------------------------------
+// Row r is "long" if it has more than `ch` nonzeros: it is cut into chunks of
+// ch nonzeros (one item each) whose partial sums are combined in order.
+// Short rows are grouped: row r starts a group unless its predecessor is a
+// short row in the same bin, bin(r) = (row_ptr[r] + r) / ch (weight of a row
+// = nnz + 1 for its output write), so a group carries <= ~ch of weight.
+__device__ __forceinline__ bool is_long(const int64_t* rp, int64_t r, int64_t ch) {
+    return rp[r + 1] - rp[r] > ch;
+}
+__device__ __forceinline__ bool is_start(const int64_t* rp, int64_t r, int64_t ch) {
+    if (is_long(rp, r, ch)) return false;
+    if (r == 0) return true;
+    if (is_long(rp, r - 1, ch)) return true;
+    return (rp[r] + r) / ch != (rp[r - 1] + r - 1) / ch;
+}
+
+__global__ void k_item_counts(const int64_t* __restrict__ rp, int64_t m, int64_t ch,
+                              int32_t* __restrict__ n_items, int32_t* __restrict__ n_slots,
+                              int32_t* __restrict__ n_comb) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < m;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t nz = rp[r + 1] - rp[r];
+        if (nz > ch) {
+            const int32_t k = int32_t((nz + ch - 1) / ch);
+            n_items[r] = k; n_slots[r] = k; n_comb[r] = 1;
+        } else {
+            n_items[r] = is_start(rp, r, ch) ? 1 : 0; n_slots[r] = 0; n_comb[r] = 0;
+        }
+    }
+}
+
+__global__ void k_item_write(const int64_t* __restrict__ rp, int64_t m, int64_t ch,
+                             const int32_t* __restrict__ o_items, const int32_t* __restrict__ o_slots,
+                             const int32_t* __restrict__ o_comb, WorkItem* __restrict__ items,
+                             Combine* __restrict__ comb) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < m;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t p0 = rp[r], nz = rp[r + 1] - p0;
+        if (nz > ch) {
+            const int32_t k = int32_t((nz + ch - 1) / ch);
+            const int32_t s0 = o_slots[r];
+            for (int32_t t = 0; t < k; ++t) {
+                WorkItem w;
+                w.p0 = p0 + int64_t(t) * ch;
+                w.p1 = min(p0 + int64_t(t + 1) * ch, p0 + nz);
+                w.r0 = int32_t(r);
+                w.r1 = -(s0 + t) - 1;
+                items[o_items[r] + t] = w;
+            }
+            Combine cb;
+            cb.row = int32_t(r); cb.s0 = s0; cb.s1 = s0 + k; cb.pad = 0;
+            comb[o_comb[r]] = cb;
+        } else if (is_start(rp, r, ch)) {
+            int64_t e = r + 1;
+            while (e < m && !is_long(rp, e, ch) && !is_start(rp, e, ch)) ++e;
+            WorkItem w;
+            w.p0 = 0; w.p1 = 0; w.r0 = int32_t(r); w.r1 = int32_t(e);
+            items[o_items[r]] = w;
+        }
+    }
+}
+
+int grid_for(const Ctx& c, int64_t n, int threads = 256) {
+    const int64_t want = (n + threads - 1) / threads;
+    const int64_t cap = int64_t(c.num_sms) * 32;
+    return int(std::max<int64_t>(1, std::min(want, cap)));
+}
+
+template <class T>
+T read_scalar(Ctx& c, const T* d) {
+    T h;
+    FB_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+    FB_CUDA(cudaStreamSynchronize(c.stream));
+    return h;
+}
+
+void build_items(Ctx& c, DCsr& A) {
+    const int64_t m = A.rows;
+    A.nitems = A.ncombine = A.nslots = 0;
+    if (m == 0) return;
+    // chunk size: ~16 items per resident warp, clamped
+    const int64_t target = int64_t(c.num_sms) * 24 * 16;
+    int64_t ch = (A.nnz + m + target - 1) / target;
+    ch = std::max<int64_t>(256, std::min<int64_t>(16384, ch));
+    A.chunk = ch;
+    DBuf<int32_t> cnt(3 * (m + 1), c.stream), off(3 * (m + 1), c.stream);
+    int32_t *ni = cnt.get(), *ns = ni + (m + 1), *nc = ns + (m + 1);
+    int32_t *oi = off.get(), *os = oi + (m + 1), *oc = os + (m + 1);
+    FB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), c.stream));
+    k_item_counts<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, ni, ns, nc);
+    FB_LAUNCH_CHECK();
+    size_t tb = 0;
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, ni, oi, m + 1, c.stream));
+    DBuf<unsigned char> tmp(tb, c.stream);
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, ni, oi, m + 1, c.stream));
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, ns, os, m + 1, c.stream));
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, nc, oc, m + 1, c.stream));
+    A.nitems = read_scalar(c, oi + m);
+    A.nslots = read_scalar(c, os + m);
+    A.ncombine = read_scalar(c, oc + m);
+    A.items.alloc(size_t(A.nitems), c.stream);
+    A.combine.alloc(size_t(std::max<int64_t>(A.ncombine, 1)), c.stream);
+    k_item_write<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, oi, os, oc,
+                                                        A.items.get(), A.combine.get());
+    FB_LAUNCH_CHECK();
+}
+
+const char* kValidateMsg[3] = {
+    "csr: row_ptr must be non-decreasing",
+    "csr: column index out of range",
+    "csr: column indices must be strictly increasing within a row",
+};
+
+}  // namespace
+
+void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
+                       const int64_t* h_rp, const int64_t* h_col, const double* h_val) {
+    // O(1) checks of validate() (sparse_matrix.hpp:126-130), same messages.
+    require(rows >= 0 && cols >= 0, "csr: negative dimension");
+    require(nnz >= 0, "csr: col_idx/values length mismatch");
+    require(h_rp != nullptr, "csr: row_ptr length must be rows + 1");
+    require(h_rp[0] == 0, "csr: row_ptr[0] must be 0");
+    require(h_rp[rows] == nnz, "csr: row_ptr[rows] must equal nnz");
+    require(rows < (int64_t(1) << 31) && cols < (int64_t(1) << 31) && nnz < (int64_t(1) << 31),
+            "frpca_b200: rows, cols and nnz must each be < 2^31 per device");
+    cudaStream_t s = c.stream;
+    DCsr& A = M.A;
+    A.rows = rows; A.cols = cols; A.nnz = nnz;
+    A.rowptr.alloc(size_t(rows + 1), s);
+    A.col.alloc(size_t(nnz), s);
+    A.val.alloc(size_t(nnz), s);
+    DBuf<int64_t> col64(size_t(nnz), s);
+    FB_CUDA(cudaMemcpyAsync(A.rowptr.get(), h_rp, sizeof(int64_t) * (rows + 1),
+                            cudaMemcpyHostToDevice, s));
+    if (nnz) {
+        FB_CUDA(cudaMemcpyAsync(col64.get(), h_col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+        FB_CUDA(cudaMemcpyAsync(A.val.get(), h_val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    }
+    DBuf<unsigned long long> err(2, s);
+    FB_CUDA(cudaMemsetAsync(err.get(), 0xff, err.bytes(), s));
+    if (rows) {
+        k_check_rowptr<<<grid_for(c, rows), 256, 0, s>>>(A.rowptr.get(), rows, err.get());
+        FB_LAUNCH_CHECK();
+    }
+    const unsigned long long bad_row = read_scalar(c, err.get());
+    const int64_t m_valid = bad_row == kNoError ? rows : int64_t(bad_row);
+    int64_t nnz_valid = nnz;
+    if (m_valid < rows) {
+        int64_t tmp;
+        FB_CUDA(cudaMemcpy(&tmp, A.rowptr.get() + m_valid, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        nnz_valid = std::min<int64_t>(tmp, nnz);
+    }
+    // row id of every nonzero (mark + inclusive max-scan)
+    DBuf<int32_t> rowid(size_t(nnz), s);
+    if (nnz) {
+        DBuf<int32_t> mark(size_t(nnz), s);
+        FB_CUDA(cudaMemsetAsync(mark.get(), 0, mark.bytes(), s));
+        if (m_valid) {
+            k_mark_rows<<<grid_for(c, m_valid), 256, 0, s>>>(A.rowptr.get(), m_valid, mark.get());
+            FB_LAUNCH_CHECK();
+        }
+        size_t tb = 0;
+        FB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, mark.get(), rowid.get(), cub::Max(),
+                                               nnz, s));
+        DBuf<unsigned char> tmp(tb, s);
+        FB_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(), tb, mark.get(), rowid.get(), cub::Max(),
+                                               nnz, s));
+        if (nnz_valid > 0) {
+            k_check_cols<<<grid_for(c, nnz_valid), 256, 0, s>>>(
+                A.rowptr.get(), rowid.get(), col64.get(), nnz_valid, cols, A.col.get(), err.get() + 1);
+            FB_LAUNCH_CHECK();
+        }
+    }
+    const unsigned long long key = read_scalar(c, err.get() + 1);
+    if (key != kNoError) {
+        const int kind = (key & 1ull) ? 1 : 2;
+        throw InvalidArgument(kValidateMsg[kind]);
+    }
+    if (m_valid < rows) throw InvalidArgument(kValidateMsg[0]);
+    col64.release();
+
+    // ---- transposed CSR (stable radix sort by column keeps ascending rows,
+    // the order spmm_transpose accumulates in, sparse_matrix.hpp:229-237)
+    DCsr& T = M.At;
+    T.rows = cols; T.cols = rows; T.nnz = nnz;
+    T.rowptr.alloc(size_t(cols + 1), s);
+    T.col.alloc(size_t(nnz), s);
+    T.val.alloc(size_t(nnz), s);
+    if (nnz) {
+        DBuf<int32_t> keys_out(size_t(nnz), s), perm_in(size_t(nnz), s), perm_out(size_t(nnz), s);
+        k_iota<<<grid_for(c, nnz), 256, 0, s>>>(perm_in.get(), nnz);
+        FB_LAUNCH_CHECK();
+        int end_bit = 1;
+        while (end_bit < 31 && (int64_t(1) << end_bit) <= cols) ++end_bit;
+        size_t tb = 0;
+        FB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, A.col.get(), keys_out.get(),
+                                                perm_in.get(), perm_out.get(), nnz, 0, end_bit, s));
+        DBuf<unsigned char> tmp(tb, s);
+        FB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, A.col.get(), keys_out.get(),
+                                                perm_in.get(), perm_out.get(), nnz, 0, end_bit, s));
+        k_gather_transpose<<<grid_for(c, nnz), 256, 0, s>>>(perm_out.get(), rowid.get(), A.val.get(),
+                                                            nnz, T.col.get(), T.val.get());
+        FB_LAUNCH_CHECK();
+        k_rowptr_from_sorted<<<grid_for(c, cols + 1), 256, 0, s>>>(keys_out.get(), nnz, cols,
+                                                                    T.rowptr.get());
+        FB_LAUNCH_CHECK();
+    } else {
+        FB_CUDA(cudaMemsetAsync(T.rowptr.get(), 0, T.rowptr.bytes(), s));
+    }
+    rowid.release();
+    build_items(c, A);
+    build_items(c, T);
+    FB_CUDA(cudaStreamSynchronize(s));
+}
+
+void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v) {
+    std::vector<int32_t> tmp(static_cast<size_t>(A.nnz));
+    FB_CUDA(cudaMemcpyAsync(rp, A.rowptr.get(), sizeof(int64_t) * (A.rows + 1),
+                            cudaMemcpyDeviceToHost, c.stream));
+    if (A.nnz) {
+        FB_CUDA(cudaMemcpyAsync(tmp.data(), A.col.get(), sizeof(int32_t) * A.nnz,
+                                cudaMemcpyDeviceToHost, c.stream));
+        FB_CUDA(cudaMemcpyAsync(v, A.val.get(), sizeof(double) * A.nnz, cudaMemcpyDeviceToHost,
+                                c.stream));
+    }
+    FB_CUDA(cudaStreamSynchronize(c.stream));
+    for (int64_t i = 0; i < A.nnz; ++i) ci[i] = tmp[size_t(i)];
+}
+
+}  // namespace fb

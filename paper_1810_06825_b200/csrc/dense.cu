@@ -1,0 +1,294 @@
+// K4 (Gram B = W^T W, dense_kernels.hpp:156-157), K6 (rescale / output GEMM
+// C = W * M, dense_kernels.hpp:172 and randsvd.hpp:262-267/:314-319), layout
+// transposes and max|x| for the LU tolerance.
+//
+// fp64 has no tcgen05 kind, so the tall-skinny products run on the fp64
+// tensor-core path that sm_100a does have: warp-level DMMA
+// (mma.sync.m8n8k4.f64, SASS DMMA.8x8x4). Each warp owns a 32x32 tile
+// (16 MMAs per k4 step from 8 operand loads), operands are staged in padded
+// shared memory by a 2-stage cp.async pipeline, and split-K partials are
+// reduced in a fixed order so results are deterministic run to run.
+#include "internal.cuh"
+
+namespace fb {
+namespace {
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int n = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---------------------------------------------------------------------------
+// Gram: B = W^T W over lower 64x64 tiles, split over rows.
+constexpr int GT = 64;      // output tile
+constexpr int GK = 16;      // rows per stage
+constexpr int GPAD = GT + 4;
+
+__global__ void __launch_bounds__(128)
+k_gram(const double* __restrict__ W, int64_t r, int n, int nt, int64_t rows_per_split,
+       double* __restrict__ part) {
+    __shared__ __align__(16) double As[2][GK][GPAD];
+    __shared__ __align__(16) double Bs[2][GK][GPAD];
+    // lower tile index -> (ti, tj), ti >= tj
+    int t = blockIdx.x, ti = 0;
+    while (t > ti) { t -= ti + 1; ++ti; }
+    const int tj = t;
+    const bool diag = ti == tj;
+    const int i0 = ti * GT, j0 = tj * GT;
+    const int64_t rs = int64_t(blockIdx.y) * rows_per_split;
+    const int64_t re = min(r, rs + rows_per_split);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wi = warp >> 1, wj = warp & 1;
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    auto load = [&](int stage, int64_t k0) {
+#pragma unroll
+        for (int e = 0; e < (GK * GT) / 128; ++e) {
+            const int idx = e * 128 + tid;
+            const int kr = idx / GT, cc = idx % GT;
+            const int64_t row = k0 + kr;
+            const bool rv = row < re;
+            const int ci = i0 + cc;
+            cp_async8(&As[stage][kr][cc], W + (rv ? row * n + min(ci, n - 1) : 0), rv && ci < n);
+            if (!diag) {
+                const int cj = j0 + cc;
+                cp_async8(&Bs[stage][kr][cc], W + (rv ? row * n + min(cj, n - 1) : 0), rv && cj < n);
+            }
+        }
+        cp_async_commit();
+    };
+
+    const int64_t nsteps = (re - rs + GK - 1) / GK;
+    if (nsteps > 0) load(0, rs);
+    for (int64_t s = 0; s < nsteps; ++s) {
+        const int stage = int(s & 1);
+        if (s + 1 < nsteps) {
+            load(stage ^ 1, rs + (s + 1) * GK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double(*Ab)[GPAD] = As[stage];
+        const double(*Bb)[GPAD] = diag ? As[stage] : Bs[stage];
+#pragma unroll
+        for (int kk = 0; kk < GK / 4; ++kk) {
+            const int krow = kk * 4 + (lane & 3);
+            double af[4], bf[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) af[a] = Ab[krow][wi * 32 + a * 8 + (lane >> 2)];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bf[b] = Bb[krow][wj * 32 + b * 8 + (lane >> 2)];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma(acc[a][b], af[a], bf[b]);
+        }
+        __syncthreads();
+    }
+    // partial tile (64x64 row-major) for this split
+    double* out = part + (int64_t(blockIdx.y) * gridDim.x + blockIdx.x) * (GT * GT);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int ii = wi * 32 + a * 8 + (lane >> 2);
+            const int jj = wj * 32 + b * 8 + (lane & 3) * 2;
+            *reinterpret_cast<double2*>(out + ii * GT + jj) = make_double2(acc[a][b][0], acc[a][b][1]);
+        }
+}
+
+// Sum split partials in split order; write B column-major, both triangles.
+__global__ void k_gram_reduce(const double* __restrict__ part, int ntiles, int nsplit, int n,
+                              double* __restrict__ B) {
+    const int tile = blockIdx.x;
+    int t = tile, ti = 0;
+    while (t > ti) { t -= ti + 1; ++ti; }
+    const int tj = t;
+    for (int e = threadIdx.x; e < GT * GT; e += blockDim.x) {
+        const int ii = e / GT, jj = e % GT;
+        const int i = ti * GT + ii, j = tj * GT + jj;
+        if (i >= n || j >= n || (ti == tj && jj > ii)) continue;
+        double acc = 0.0;
+        for (int s = 0; s < nsplit; ++s) acc += part[(int64_t(s) * ntiles + tile) * (GT * GT) + e];
+        B[i + int64_t(j) * n] = acc;
+        B[j + int64_t(i) * n] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// GEMM: C (r x N) = W (r x K, row-major) * M (K x N, row-major).
+constexpr int MT = 64;      // rows per tile
+constexpr int NT = 64;      // cols per tile
+constexpr int KT = 16;      // k per stage
+constexpr int APAD = KT + 4;
+constexpr int BPAD = NT + 4;
+
+__global__ void __launch_bounds__(128)
+k_gemm(const double* __restrict__ W, int64_t r, int K, const double* __restrict__ M, int N,
+       double* __restrict__ C, int64_t ldc, int col_major) {
+    __shared__ __align__(16) double As[2][MT][APAD];
+    __shared__ __align__(16) double Bs[2][KT][BPAD];
+    const int64_t r0 = int64_t(blockIdx.x) * MT;
+    const int n0 = blockIdx.y * NT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wi = warp >> 1, wj = warp & 1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    auto load = [&](int stage, int k0) {
+#pragma unroll
+        for (int e = 0; e < (MT * KT) / 128; ++e) {
+            const int idx = e * 128 + tid;
+            const int rr = idx / KT, kk = idx % KT;
+            const int64_t row = r0 + rr;
+            const int k = k0 + kk;
+            const bool v = row < r && k < K;
+            cp_async8(&As[stage][rr][kk], W + (v ? row * K + k : 0), v);
+        }
+#pragma unroll
+        for (int e = 0; e < (KT * NT) / 128; ++e) {
+            const int idx = e * 128 + tid;
+            const int kk = idx / NT, cc = idx % NT;
+            const int k = k0 + kk, col = n0 + cc;
+            const bool v = k < K && col < N;
+            cp_async8(&Bs[stage][kk][cc], M + (v ? int64_t(k) * N + col : 0), v);
+        }
+        cp_async_commit();
+    };
+    const int nsteps = (K + KT - 1) / KT;
+    load(0, 0);
+    for (int s = 0; s < nsteps; ++s) {
+        const int stage = s & 1;
+        if (s + 1 < nsteps) {
+            load(stage ^ 1, (s + 1) * KT);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < KT / 4; ++kk) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) af[a] = As[stage][wi * 32 + a * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bf[b] = Bs[stage][kk * 4 + (lane & 3)][wj * 32 + b * 8 + (lane >> 2)];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma(acc[a][b], af[a], bf[b]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int64_t row = r0 + wi * 32 + a * 8 + (lane >> 2);
+            const int col = n0 + wj * 32 + b * 8 + (lane & 3) * 2;
+            if (row >= r) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (col + h >= N) continue;
+                if (col_major) C[int64_t(col + h) * ldc + row] = acc[a][b][h];
+                else C[row * ldc + col + h] = acc[a][b][h];
+            }
+        }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_transpose(const double* __restrict__ in, int64_t rows, int64_t cols,
+                            double* __restrict__ out) {
+    __shared__ double tile[32][33];
+    const int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t r = r0 + k, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t c = c0 + k, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+    }
+}
+
+__global__ void k_maxabs(const double* __restrict__ x, int64_t n, unsigned long long* __restrict__ out) {
+    double m = 0.0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        m = fmax(m, fabs(x[i]));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+}  // namespace
+
+void gram_device(Ctx& c, const double* W, int64_t r, int64_t n, double* B) {
+    Prof prof(c, "gram", 8.0 * r * n, double(r) * n * (n + 1));
+    const int nt = int((n + GT - 1) / GT);
+    const int ntiles = nt * (nt + 1) / 2;
+    int64_t nsplit = std::max<int64_t>(1, (int64_t(c.num_sms) * 8) / ntiles);
+    nsplit = std::min<int64_t>(nsplit, std::max<int64_t>(1, (r + 63) / 64));
+    const int64_t rps = ((r + nsplit - 1) / nsplit + GK - 1) / GK * GK;
+    nsplit = std::max<int64_t>(1, (r + rps - 1) / rps);
+    DBuf<double> part(size_t(nsplit) * ntiles * GT * GT, c.stream);
+    dim3 grid(ntiles, unsigned(nsplit));
+    k_gram<<<grid, 128, 0, c.stream>>>(W, r, int(n), nt, rps, part.get());
+    FB_LAUNCH_CHECK();
+    k_gram_reduce<<<ntiles, 256, 0, c.stream>>>(part.get(), ntiles, int(nsplit), int(n), B);
+    FB_LAUNCH_CHECK();
+}
+
+void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M, int64_t N,
+                 double* C, int64_t ldc, bool col_major_out) {
+    if (r == 0 || N == 0) return;
+    Prof prof(c, "rescale_gemm", 8.0 * r * (K + N), 2.0 * r * K * N);
+    dim3 grid(unsigned((r + MT - 1) / MT), unsigned((N + NT - 1) / NT));
+    k_gemm<<<grid, 128, 0, c.stream>>>(W, r, int(K), M, int(N), C, ldc, col_major_out ? 1 : 0);
+    FB_LAUNCH_CHECK();
+}
+
+void transpose_device(Ctx& c, const double* in, int64_t rows, int64_t cols, double* out) {
+    if (rows == 0 || cols == 0) return;
+    Prof prof(c, "transpose", 16.0 * rows * cols, 0.0);
+    dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32));
+    k_transpose<<<grid, dim3(32, 8), 0, c.stream>>>(in, rows, cols, out);
+    FB_LAUNCH_CHECK();
+}
+
+double maxabs_device(Ctx& c, const double* x, int64_t n) {
+    DBuf<unsigned long long> d(1, c.stream);
+    FB_CUDA(cudaMemsetAsync(d.get(), 0, 8, c.stream));
+    if (n) {
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms * 8, (n + 255) / 256)));
+        k_maxabs<<<grid, 256, 0, c.stream>>>(x, n, d.get());
+        FB_LAUNCH_CHECK();
+    }
+    unsigned long long h;
+    FB_CUDA(cudaMemcpyAsync(&h, d.get(), 8, cudaMemcpyDeviceToHost, c.stream));
+    FB_CUDA(cudaStreamSynchronize(c.stream));
+    double v;
+    std::memcpy(&v, &h, 8);
+    return v;
+}
+
+}  // namespace fb

@@ -1,0 +1,313 @@
+// Device drivers of the two fast algorithms: frpca (Alg. 5, randsvd.hpp:224-276)
+// and frpcat (Alg. 6, randsvd.hpp:278-328), plus eig_svd (dense_kernels.hpp:
+// 145-174) as the device pipeline Gram -> syevd -> rank check -> rescale.
+//
+// All intermediate panels stay in HBM, row-major r x l. The host sees only the
+// final U/S/V (column-major, like SvdResult) and the scalars needed for the
+// reference's error checks (the l eigenvalues for the rank test).
+#include <cfloat>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "driver.cuh"
+
+namespace fb {
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) {
+    return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+// M (row-major l x ncols): column t takes eigenvector src(t) of V (column-major
+// l x l), src(t) = rev ? s + k - 1 - t : t, scaled by 1/S[src] when `scale`
+// (V * diag(1/S), dense_kernels.hpp:172; reversal ind = s+k-1..s,
+// randsvd.hpp:265-267 / :317-319).
+__global__ void k_factor(const double* __restrict__ V, const double* __restrict__ D, int l, int s,
+                         int k, int ncols, int rev, int scale, double* __restrict__ M) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < l * ncols; e += gridDim.x * blockDim.x) {
+        const int kk = e / ncols, t = e % ncols;
+        const int src = rev ? (s + k - 1 - t) : t;
+        double v = V[kk + int64_t(src) * l];
+        if (scale) {
+            const double inv = 1.0 / sqrt(D[src]);
+            v = v * inv;
+        }
+        M[e] = v;
+    }
+}
+
+__global__ void k_sing_out(const double* __restrict__ D, int s, int k, int rev, double* __restrict__ S) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < k; t += gridDim.x * blockDim.x)
+        S[t] = sqrt(D[rev ? (s + k - 1 - t) : t]);
+}
+
+}  // namespace
+
+void EigWork::run(Ctx& c, const double* W, int64_t r, int64_t n) {
+    B.alloc(size_t(n * n), c.stream);
+    D.alloc(size_t(n), c.stream);
+    gram_device(c, W, r, n, B.get());
+    allreduce_sum(c, B.get(), n * n);  // row-sharded W: Gram partials
+    syevd_device(c, B.get(), n, D.get(), hD);
+    // rank check (dense_kernels.hpp:163-167)
+    const double lambda_max = hD[size_t(n - 1)];
+    if (lambda_max <= 0.0 || hD[0] <= double(n) * DBL_EPSILON * lambda_max)
+        throw NumericalError("eig_svd: input does not have full numerical column rank");
+    l = n;
+}
+
+void EigWork::factor(Ctx& c, int s, int k, int ncols, bool rev, bool scale, double* M) {
+    const int total = int(l) * ncols;
+    k_factor<<<std::max(1, std::min(1024, (total + 255) / 256)), 256, 0, c.stream>>>(
+        B.get(), D.get(), int(l), s, k, ncols, rev ? 1 : 0, scale ? 1 : 0, M);
+    FB_LAUNCH_CHECK();
+}
+
+void EigWork::singular_values(Ctx& c, int s, int k, bool rev, double* S) {
+    k_sing_out<<<1, 256, 0, c.stream>>>(D.get(), s, k, rev ? 1 : 0, S);
+    FB_LAUNCH_CHECK();
+}
+
+// eig_svd(W).U: Uout (row-major r x n) = W * V diag(1/S).
+void eig_svd_U(Ctx& c, const double* W, int64_t r, int64_t n, double* Uout) {
+    EigWork e;
+    e.run(c, W, r, n);
+    DBuf<double> M(size_t(n * n), c.stream);
+    e.factor(c, 0, int(n), int(n), false, true, M.get());
+    gemm_device(c, W, r, n, M.get(), n, Uout, n, false);
+}
+
+// Omega of the sketch (randsvd.hpp:65-76): `count` doubles in stream order
+// (the column-major fill of gaussian_matrix), either the injected matrix or
+// the seeded stream, into device memory.
+void sketch_stream(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, double* dst) {
+    const int64_t count = rows * cols;
+    if (a.omega) {
+        require(a.omega_rows == rows && a.omega_cols == cols, "injected sketch has the wrong shape");
+        FB_CUDA(cudaMemcpyAsync(dst, a.omega, sizeof(double) * count,
+                                a.device_io ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                c.stream));
+        return;
+    }
+    const uint64_t seed = mix_seed(a.cfg.seed, 0xA11CEull);
+    if (a.cfg.flags & FRPCA_FLAG_HOST_OMEGA) {
+        Prof prof(c, "omega_host", 8.0 * count, 0.0);
+        std::vector<double> h(static_cast<size_t>(count));
+        gaussian_stream_host(seed, count, h.data());
+        FB_CUDA(cudaMemcpyAsync(dst, h.data(), sizeof(double) * count, cudaMemcpyHostToDevice, c.stream));
+        FB_CUDA(cudaStreamSynchronize(c.stream));
+    } else {
+        gaussian_stream_device(c, seed, count, dst);
+    }
+}
+
+static void check_common(const frpca_config& cfg) {  // randsvd.hpp:78-81
+    require(cfg.k >= 1, "config: rank k must be >= 1");
+    require(cfg.oversample >= 0, "config: oversampling must be >= 0");
+}
+
+static void copy_out(Ctx& c, const RunArgs& a, double* dst_user, const double* src_dev, int64_t count) {
+    if (!dst_user || count == 0) return;
+    FB_CUDA(cudaMemcpyAsync(dst_user, src_dev, sizeof(double) * count,
+                            a.device_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c.stream));
+}
+
+// Q (row-major r x l) -> column-major output basis (RunStats::basis).
+static void basis_out(Ctx& c, const RunArgs& a, const double* Q, int64_t r, int64_t l) {
+    if (!a.basis) return;
+    DBuf<double> t(size_t(r * l), c.stream);
+    transpose_device(c, Q, r, l, t.get());
+    copy_out(c, a, a.basis, t.get(), r * l);
+}
+
+// ---------------------------------------------------------------------------
+// frpcat (Alg. 6), randsvd.hpp:278-328. Row-sharded: this rank holds rows
+// [offset, offset + m_loc) of A; A^T partials and Gram partials are summed
+// across ranks.
+void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
+    const frpca_config& cfg = a.cfg;
+    check_common(cfg);
+    require(M.grows >= M.gcols, "frpcat: requires rows >= cols (use frpca otherwise)");
+    require(cfg.passes >= 2, "frpcat: pass count q must be >= 2");
+    const int64_t l = cfg.k + cfg.oversample;
+    require(l <= M.gcols, "frpcat: k + oversample must be <= cols");
+    require(!M.col_shard, "frpcat: needs a row-sharded matrix");
+    const int64_t q = cfg.passes, loops = (q - 1) / 2;
+    const int64_t m = M.A.rows, n = M.A.cols, k = cfg.k, s = cfg.oversample;
+    const uint64_t passes0 = M.passes.load();
+    cudaStream_t S = c.stream;
+
+    DBuf<double> bufM(size_t(std::max<int64_t>(m, 1) * l), S);
+    DBuf<double> Q(size_t(n * l), S), Z(size_t(n * l), S);
+
+    auto t0 = Clock::now();
+    if (q % 2 == 0) {
+        // Omega (l x grows, column-major) == Omega^T row-major: this rank's rows
+        // are the stream slice [offset*l, (offset+m)*l).
+        if (M.offset == 0 && m == M.grows) {
+            sketch_stream(c, a, l, M.grows, bufM.get());
+        } else {
+            DBuf<double> full(size_t(M.grows * l), S);
+            sketch_stream(c, a, l, M.grows, full.get());
+            FB_CUDA(cudaMemcpyAsync(bufM.get(), full.get() + M.offset * l, sizeof(double) * m * l,
+                                    cudaMemcpyDeviceToDevice, S));
+        }
+        spmm_pass(c, M, /*transpose=*/true, bufM.get(), l, Z.get());  // (Omega A)^T, n x l
+        allreduce_sum(c, Z.get(), n * l);
+        if (q == 2) {
+            eig_svd_U(c, Z.get(), n, l, Q.get());
+        } else {
+            lu_basis_device(c, Z.get(), n, l);
+            std::swap(Q, Z);
+        }
+    } else {
+        DBuf<double> om(size_t(n * l), S);
+        sketch_stream(c, a, n, l, om.get());              // n x l column-major
+        transpose_device(c, om.get(), l, n, Q.get());     // -> row-major n x l
+    }
+    FB_CUDA(cudaStreamSynchronize(S));
+    const double t_sketch = since(t0);
+
+    t0 = Clock::now();
+    for (int64_t i = 1; i <= loops; ++i) {
+        spmm_pass(c, M, false, Q.get(), l, bufM.get());   // A Q, m x l
+        spmm_pass(c, M, true, bufM.get(), l, Z.get());    // A^T (A Q), n x l
+        allreduce_sum(c, Z.get(), n * l);
+        if (i == loops) {
+            eig_svd_U(c, Z.get(), n, l, Q.get());
+        } else {
+            lu_basis_device(c, Z.get(), n, l);
+            std::swap(Q, Z);
+        }
+    }
+    FB_CUDA(cudaStreamSynchronize(S));
+    const double t_power = since(t0);
+
+    t0 = Clock::now();
+    spmm_pass(c, M, false, Q.get(), l, bufM.get());       // W = A Q, m x l
+    EigWork e;
+    e.run(c, bufM.get(), m, l);
+    DBuf<double> MU(size_t(l * k), S), MV(size_t(l * k), S);
+    e.factor(c, int(s), int(k), int(k), true, true, MU.get());
+    e.factor(c, int(s), int(k), int(k), true, false, MV.get());
+    DBuf<double> Uo(size_t(std::max<int64_t>(m, 1) * k), S), Vo(size_t(n * k), S), So(size_t(k), S);
+    gemm_device(c, bufM.get(), m, l, MU.get(), k, Uo.get(), std::max<int64_t>(m, 1), true);
+    gemm_device(c, Q.get(), n, l, MV.get(), k, Vo.get(), n, true);
+    e.singular_values(c, int(s), int(k), true, So.get());
+    copy_out(c, a, a.U, Uo.get(), m * k);
+    copy_out(c, a, a.V, Vo.get(), n * k);
+    copy_out(c, a, a.S, So.get(), k);
+    basis_out(c, a, Q.get(), n, l);
+    FB_CUDA(cudaStreamSynchronize(S));
+    if (st) {
+        st->sketch_seconds = t_sketch;
+        st->power_seconds = t_power;
+        st->finalize_seconds = since(t0);
+        st->passes_over_matrix = M.passes.load() - passes0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// frpca (Alg. 5), randsvd.hpp:224-276. Column-sharded: this rank holds
+// columns [offset, offset + n_loc) of A; the m x l products A*X are summed
+// across ranks and the final Gram of A^T Q (n-sharded rows) too.
+void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
+    const frpca_config& cfg = a.cfg;
+    check_common(cfg);
+    require(M.grows <= M.gcols, "frpca: requires rows <= cols (use frpcat otherwise)");
+    require(cfg.passes >= 2, "frpca: pass count q must be >= 2");
+    const int64_t l = cfg.k + cfg.oversample;
+    require(l <= M.grows, "frpca: k + oversample must be <= rows");
+    require(M.col_shard || c.world == 1, "frpca: needs a column-sharded matrix");
+    const int64_t q = cfg.passes, loops = (q - 1) / 2;
+    const int64_t m = M.A.rows, n = M.A.cols, k = cfg.k, s = cfg.oversample;
+    const uint64_t passes0 = M.passes.load();
+    cudaStream_t S = c.stream;
+
+    DBuf<double> Q(size_t(m * l), S), Y(size_t(m * l), S);
+    DBuf<double> bufN(size_t(std::max<int64_t>(n, 1) * l), S);
+
+    auto t0 = Clock::now();
+    if (q % 2 == 0) {
+        // Omega: gcols x l column-major; this rank needs rows [offset, offset+n)
+        DBuf<double> om(size_t(M.gcols * l), S);
+        sketch_stream(c, a, M.gcols, l, om.get());
+        if (M.offset == 0 && n == M.gcols) {
+            transpose_device(c, om.get(), l, n, bufN.get());
+        } else {
+            DBuf<double> full(size_t(M.gcols * l), S);
+            transpose_device(c, om.get(), l, M.gcols, full.get());
+            FB_CUDA(cudaMemcpyAsync(bufN.get(), full.get() + M.offset * l, sizeof(double) * n * l,
+                                    cudaMemcpyDeviceToDevice, S));
+        }
+        spmm_pass(c, M, false, bufN.get(), l, Y.get());   // A Omega, m x l
+        allreduce_sum(c, Y.get(), m * l);
+        if (q > 2) {
+            lu_basis_device(c, Y.get(), m, l);
+            std::swap(Q, Y);
+        } else {
+            eig_svd_U(c, Y.get(), m, l, Q.get());
+        }
+    } else {
+        DBuf<double> om(size_t(m * l), S);
+        sketch_stream(c, a, m, l, om.get());
+        transpose_device(c, om.get(), l, m, Q.get());
+    }
+    FB_CUDA(cudaStreamSynchronize(S));
+    const double t_sketch = since(t0);
+
+    t0 = Clock::now();
+    for (int64_t i = 1; i <= loops; ++i) {
+        spmm_pass(c, M, true, Q.get(), l, bufN.get());    // A^T Q, n x l
+        spmm_pass(c, M, false, bufN.get(), l, Y.get());   // A (A^T Q), m x l
+        allreduce_sum(c, Y.get(), m * l);
+        if (i == loops) {
+            eig_svd_U(c, Y.get(), m, l, Q.get());
+        } else {
+            lu_basis_device(c, Y.get(), m, l);
+            std::swap(Q, Y);
+        }
+    }
+    FB_CUDA(cudaStreamSynchronize(S));
+    const double t_power = since(t0);
+
+    t0 = Clock::now();
+    spmm_pass(c, M, true, Q.get(), l, bufN.get());        // W = A^T Q, n x l
+    EigWork e;
+    e.run(c, bufN.get(), n, l);
+    DBuf<double> MU(size_t(l * k), S), MV(size_t(l * k), S);
+    e.factor(c, int(s), int(k), int(k), true, false, MU.get());   // U = Q * V(:, ind)
+    e.factor(c, int(s), int(k), int(k), true, true, MV.get());    // V = f.U(:, ind)
+    DBuf<double> Uo(size_t(m * k), S), Vo(size_t(std::max<int64_t>(n, 1) * k), S), So(size_t(k), S);
+    gemm_device(c, Q.get(), m, l, MU.get(), k, Uo.get(), m, true);
+    gemm_device(c, bufN.get(), n, l, MV.get(), k, Vo.get(), std::max<int64_t>(n, 1), true);
+    e.singular_values(c, int(s), int(k), true, So.get());
+    copy_out(c, a, a.U, Uo.get(), m * k);
+    copy_out(c, a, a.V, Vo.get(), n * k);
+    copy_out(c, a, a.S, So.get(), k);
+    basis_out(c, a, Q.get(), m, l);
+    FB_CUDA(cudaStreamSynchronize(S));
+    if (st) {
+        st->sketch_seconds = t_sketch;
+        st->power_seconds = t_power;
+        st->finalize_seconds = since(t0);
+        st->passes_over_matrix = M.passes.load() - passes0;
+    }
+}
+
+void spmm_pass(Ctx& c, DMat& M, bool transpose, const double* X, int64_t ncols, double* Y) {
+    const DCsr& A = transpose ? M.At : M.A;
+    spmm_device(c, A, X, ncols, ncols, Y, ncols, transpose ? "spmm_AtY" : "spmm_AX");
+    M.passes.fetch_add(1, std::memory_order_relaxed);  // recordPass, sparse_matrix.hpp:119-122
+}
+
+uint64_t mix_seed(uint64_t seed, uint64_t tag) {  // types.hpp:52-57
+    uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (tag + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+}  // namespace fb

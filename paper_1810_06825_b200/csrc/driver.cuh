@@ -1,0 +1,38 @@
+// Driver-level declarations (driver.cu, comm.cu, abi.cu).
+#pragma once
+
+#include "internal.cuh"
+
+namespace fb {
+
+struct RunArgs {
+    frpca_config cfg{};
+    const double* omega = nullptr;
+    int64_t omega_rows = 0, omega_cols = 0;
+    double *U = nullptr, *S = nullptr, *V = nullptr, *basis = nullptr;
+    bool device_io = false;
+};
+
+// eig_svd pipeline state: Gram -> (allreduce) -> syevd (B becomes V) -> rank check.
+struct EigWork {
+    DBuf<double> B, D;
+    std::vector<double> hD;
+    int64_t l = 0;
+    void run(Ctx& c, const double* W, int64_t r, int64_t n);
+    void factor(Ctx& c, int s, int k, int ncols, bool rev, bool scale, double* M);
+    void singular_values(Ctx& c, int s, int k, bool rev, double* S);
+};
+
+void eig_svd_U(Ctx& c, const double* W, int64_t r, int64_t n, double* Uout);
+void spmm_pass(Ctx& c, DMat& M, bool transpose, const double* X, int64_t ncols, double* Y);
+void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st);
+void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st);
+uint64_t mix_seed(uint64_t seed, uint64_t tag);
+
+// comm.cu: in-place sum over ranks (no-op on one GPU).
+void allreduce_sum(Ctx& c, double* x, int64_t count);
+void comm_init(Ctx& c, int rank, int world, const void* id128);
+void comm_destroy(Ctx& c);
+void comm_unique_id(void* out128);
+
+}  // namespace fb

@@ -1,0 +1,125 @@
+// Internal types shared by the translation units of libfrpca_b200.so.
+#pragma once
+
+#include <cusolverDn.h>
+
+#include <atomic>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+typedef struct ncclComm* ncclComm_t;
+
+namespace fb {
+
+// One unit of SpMM work for one warp (see spmm.cu). r1 >= 0: the consecutive
+// short rows [r0, r1), each summed sequentially in CSR order straight into the
+// output row. r1 < 0: nonzeros [p0, p1) of the long row r0, summed
+// sequentially into partial slot -(r1 + 1); partials of one row are then
+// added in slot order (fixed, deterministic combine).
+struct WorkItem {
+    int64_t p0, p1;
+    int32_t r0, r1;
+};
+struct Combine {
+    int32_t row, s0, s1, pad;
+};
+
+// Device CSR: int64 row_ptr (8 B/row), int32 col ids, fp64 values (12 B/nnz).
+struct DCsr {
+    int64_t rows = 0, cols = 0, nnz = 0;
+    DBuf<int64_t> rowptr;
+    DBuf<int32_t> col;
+    DBuf<double> val;
+    // load-balanced work list (built once at load)
+    DBuf<WorkItem> items;
+    DBuf<Combine> combine;
+    int64_t nitems = 0, ncombine = 0, nslots = 0, chunk = 0;
+};
+
+struct ProfAgg {
+    int64_t launches = 0;
+    double ms = 0, bytes = 0, flops = 0;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cusolverDnHandle_t solver = nullptr;
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    int num_sms = 148;
+    std::mutex mu;  // the ABI serialises calls on one context
+
+    // profiling: events around each launch, folded into per-kernel aggregates
+    bool prof = false;
+    struct Pending {
+        std::string name;
+        cudaEvent_t a, b;
+        double bytes, flops;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    std::map<std::string, ProfAgg> agg;
+    std::vector<std::string> agg_names;  // stable storage for frpca_profile_get
+
+    cudaEvent_t get_event();
+    void flush_profile();  // synchronises the stream
+};
+
+// RAII launch bracket: records events on ctx.stream when profiling is on.
+struct Prof {
+    Ctx& c;
+    size_t idx = size_t(-1);
+    Prof(Ctx& ctx, const char* name, double bytes, double flops);
+    ~Prof();
+};
+
+struct DMat {
+    Ctx* ctx = nullptr;
+    DCsr A;   // local rows (or local column block) of the matrix
+    DCsr At;  // its transpose, built on the device at load
+    int64_t grows = 0, gcols = 0;  // global shape (== local shape on 1 GPU)
+    int64_t offset = 0;            // first global row (row shard) or column (col shard)
+    int col_shard = 0;
+    std::atomic<uint64_t> passes{0};
+};
+
+// ---- csr.cu
+void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
+                       const int64_t* h_rowptr, const int64_t* h_col, const double* h_val);
+void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v);
+
+// ---- spmm.cu : Y (rows x ncols, row-major ldy) = A * X (row-major ldx)
+void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
+                 int64_t ldy, const char* tag);
+
+// ---- dense.cu
+// B (n x n, column-major, full symmetric) = W^T W for row-major W (r x n, ld n).
+void gram_device(Ctx& c, const double* W, int64_t r, int64_t n, double* B);
+// C = W (r x K row-major, ld K) * M (K x N row-major, ld N). col_major_out: C is
+// column-major (ldc >= r) else row-major (ldc >= N).
+void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M, int64_t N,
+                 double* C, int64_t ldc, bool col_major_out);
+// out (cols x rows, row-major) = transpose of in (rows x cols row-major) ==
+// column-major <-> row-major conversion of an r x c matrix.
+void transpose_device(Ctx& c, const double* in, int64_t rows, int64_t cols, double* out);
+double maxabs_device(Ctx& c, const double* x, int64_t n);
+
+// ---- eig.cu : symmetric eigensolve of column-major n x n B (lower used):
+// V (column-major) eigenvectors, D ascending eigenvalues (device), D copied to h_D.
+void syevd_device(Ctx& c, double* B_inout_V, int64_t n, double* d_D, std::vector<double>& h_D);
+
+// ---- lu.cu : in place: W (m x l row-major) -> P^T L (row-major), lu_basis.
+void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l);
+
+// ---- rng.cu : Omega stream (dense_kernels.hpp:19-28) into `out` (count
+// doubles, stream order), generated on the device.
+void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out);
+void gaussian_stream_host(uint64_t seed, int64_t count, double* out);
+
+}  // namespace fb

@@ -1,0 +1,224 @@
+// K1/K2: CSR SpMM over row-major fp64 panels, Y = A * X.
+//   spmm           (sparse_matrix.hpp:177-206) runs on the CSR of A;
+//   spmm_transpose (sparse_matrix.hpp:208-240) runs the SAME kernel on the
+//   transposed CSR built at load, so A^T * Y is a gather with no atomics.
+//
+// One warp owns one output row slice of up to 64*NCH columns; lane j holds
+// columns {64*ch + 2*j, +1} (double2). Each nonzero gathers one contiguous
+// l*8-byte row of X (coalesced 512-byte warp loads), and the accumulation of
+// every output entry is the reference's order: a sequential sum over the row's
+// nonzeros in CSR order (rows split into chunks for load balance are summed
+// per chunk, then the chunk partials are added in chunk order).
+// Column ids / values are streamed once (evict-first); X rows go through L1/L2
+// (read-only path) since power-law columns are re-gathered many times.
+#include "internal.cuh"
+
+namespace fb {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int VEC>
+struct Vec;
+template <>
+struct Vec<2> {
+    using T = double2;
+    __device__ static T load(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+    __device__ static void fma(T& a, double v, const T& x) {
+        a.x = __fma_rn(v, x.x, a.x);
+        a.y = __fma_rn(v, x.y, a.y);
+    }
+    __device__ static void store(double* p, const T& a) { *reinterpret_cast<double2*>(p) = a; }
+    __device__ static T zero() { return make_double2(0.0, 0.0); }
+};
+template <>
+struct Vec<1> {
+    using T = double;
+    __device__ static T load(const double* p) { return __ldg(p); }
+    __device__ static void fma(T& a, double v, const T& x) { a = __fma_rn(v, x, a); }
+    __device__ static void store(double* p, const T& a) { *p = a; }
+    __device__ static T zero() { return 0.0; }
+};
+
+template <int VEC, int NCH>
+__device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
+                                               const double* __restrict__ val, int64_t p0, int64_t p1,
+                                               const double* __restrict__ X, int64_t ldx,
+                                               int lane, int ncols,
+                                               typename Vec<VEC>::T (&acc)[NCH]) {
+    using V = Vec<VEC>;
+    using T = typename V::T;
+    bool ok[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) ok[ch] = (ch * 32 + lane) * VEC < ncols;
+    const double* Xl = X + lane * VEC;
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int cnt = (p1 - base) < 32 ? int(p1 - base) : 32;
+        int myc = 0;
+        double myv = 0.0;
+        if (lane < cnt) {
+            myc = __ldcs(col + base + lane);
+            myv = __ldcs(val + base + lane);
+        }
+        int j = 0;
+        for (; j + 4 <= cnt; j += 4) {
+            int c[4];
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                c[u] = __shfl_sync(0xffffffffu, myc, j + u);
+                v[u] = __shfl_sync(0xffffffffu, myv, j + u);
+            }
+            T x[4][NCH];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch)
+                    x[u][ch] = ok[ch] ? V::load(Xl + int64_t(c[u]) * ldx + ch * 32 * VEC) : V::zero();
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) V::fma(acc[ch], v[u], x[u][ch]);
+        }
+        for (; j < cnt; ++j) {
+            const int c0 = __shfl_sync(0xffffffffu, myc, j);
+            const double v0 = __shfl_sync(0xffffffffu, myv, j);
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                if (ok[ch]) V::fma(acc[ch], v0, V::load(Xl + int64_t(c0) * ldx + ch * 32 * VEC));
+        }
+    }
+}
+
+template <int VEC, int NCH>
+__global__ void __launch_bounds__(kThreads)
+k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+       const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
+       const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
+       double* __restrict__ part, int ncols) {
+    using V = Vec<VEC>;
+    using T = typename V::T;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * kThreads) >> 5;
+    for (int64_t it = warp; it < nitems; it += nwarps) {
+        const WorkItem w = items[it];
+        if (w.r1 >= 0) {
+            for (int32_t r = w.r0; r < w.r1; ++r) {
+                T acc[NCH];
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
+                row_accumulate<VEC, NCH>(col, val, rowptr[r], rowptr[r + 1], X, ldx, lane, ncols, acc);
+                double* yr = Y + int64_t(r) * ldy + lane * VEC;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch)
+                    if ((ch * 32 + lane) * VEC < ncols) V::store(yr + ch * 32 * VEC, acc[ch]);
+            }
+        } else {
+            T acc[NCH];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
+            row_accumulate<VEC, NCH>(col, val, w.p0, w.p1, X, ldx, lane, ncols, acc);
+            const int64_t slot = -int64_t(w.r1) - 1;
+            double* pr = part + slot * ncols + lane * VEC;
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                if ((ch * 32 + lane) * VEC < ncols) V::store(pr + ch * 32 * VEC, acc[ch]);
+        }
+    }
+}
+
+// Long rows: Y[row] = sum of its chunk partials, in chunk order.
+__global__ void __launch_bounds__(kThreads)
+k_combine(const Combine* __restrict__ comb, int64_t ncomb, const double* __restrict__ part,
+          int ncols, double* __restrict__ Y, int64_t ldy) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * kThreads) >> 5;
+    for (int64_t e = warp; e < ncomb; e += nwarps) {
+        const Combine cb = comb[e];
+        for (int c = lane; c < ncols; c += 32) {
+            double acc = part[int64_t(cb.s0) * ncols + c];
+            for (int32_t s = cb.s0 + 1; s < cb.s1; ++s) acc += part[int64_t(s) * ncols + c];
+            Y[int64_t(cb.row) * ldy + c] = acc;
+        }
+    }
+}
+
+template <int VEC, int NCH>
+void launch(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
+            double* part, int ncols) {
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<VEC, NCH>,
+                                                              kThreads, 0));
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const int64_t warps_needed = A.nitems;
+    int grid = int(std::min<int64_t>(int64_t(c.num_sms) * blocks_per_sm,
+                                     (warps_needed + 7) / 8));
+    grid = std::max(grid, 1);
+    k_spmm<VEC, NCH><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
+                                                      A.items.get(), A.nitems, X, ldx, Y, ldy,
+                                                      part, ncols);
+    FB_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
+                 int64_t ldy, const char* tag) {
+    if (A.rows == 0 || ncols == 0) return;
+    // algorithmic bytes: 12 B/nnz + 8 B/row ptr + dense in + out
+    const double bytes = 12.0 * A.nnz + 8.0 * (A.rows + 1) + 8.0 * ncols * (A.cols + A.rows);
+    const double flops = 2.0 * A.nnz * ncols;
+    Prof prof(c, tag, bytes, flops);
+    const int64_t slice_max = 256;
+    DBuf<double> part;
+    for (int64_t off = 0; off < ncols; off += slice_max) {
+        const int nc = int(std::min<int64_t>(slice_max, ncols - off));
+        if (A.nslots && part.n < size_t(A.nslots) * nc) part.alloc(size_t(A.nslots) * nc, c.stream);
+        const bool v2 = (nc % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) && (off % 2 == 0);
+        const double* Xo = X + off;
+        double* Yo = Y + off;
+        if (v2) {
+            const int nch = (nc + 63) / 64;
+            switch (nch) {
+                case 1: launch<2, 1>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
+                case 2: launch<2, 2>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
+                case 3: launch<2, 3>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
+                default: launch<2, 4>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
+            }
+        } else {
+            const int nch = (nc + 31) / 32;
+            if (nch <= 1) launch<1, 1>(c, A, Xo, ldx, Yo, ldy, part.get(), nc);
+            else if (nch <= 2) launch<1, 2>(c, A, Xo, ldx, Yo, ldy, part.get(), nc);
+            else if (nch <= 4) launch<1, 4>(c, A, Xo, ldx, Yo, ldy, part.get(), nc);
+            else {
+                // odd widths above 128: two launches of <=128 columns
+                launch<1, 4>(c, A, Xo, ldx, Yo, ldy, part.get(), 128);
+                if (A.ncombine) {
+                    k_combine<<<std::max(1, std::min<int>(c.num_sms * 8, int((A.ncombine + 7) / 8))),
+                                kThreads, 0, c.stream>>>(A.combine.get(), A.ncombine, part.get(), 128,
+                                                         Yo, ldy);
+                    FB_LAUNCH_CHECK();
+                }
+                launch<1, 4>(c, A, Xo + 128, ldx, Yo + 128, ldy, part.get(), nc - 128);
+                if (A.ncombine) {
+                    k_combine<<<std::max(1, std::min<int>(c.num_sms * 8, int((A.ncombine + 7) / 8))),
+                                kThreads, 0, c.stream>>>(A.combine.get(), A.ncombine, part.get(),
+                                                         nc - 128, Yo + 128, ldy);
+                    FB_LAUNCH_CHECK();
+                }
+                continue;
+            }
+        }
+        if (A.ncombine) {
+            k_combine<<<std::max(1, std::min<int>(c.num_sms * 8, int((A.ncombine + 7) / 8))),
+                        kThreads, 0, c.stream>>>(A.combine.get(), A.ncombine, part.get(), nc, Yo, ldy);
+            FB_LAUNCH_CHECK();
+        }
+    }
+}
+
+}  // namespace fb

@@ -1,0 +1,170 @@
+"""GPU parity of frpca / frpcat / auto_pca against the CPU oracle, through the
+C ABI. Mirrors proj/tests/test_randsvd.cpp for the fast algorithms and the
+north_star bar: with Omega from the same seed, top-k singular values within
+1e-10 relative and ||UU^T - U'U'^T||_2 <= 1e-8 (V likewise)."""
+import numpy as np
+import pytest
+
+from metrics import SIGMA_TOL, SUBSPACE_TOL, orthonormality, sigma_rel, subspace_dist
+from test_gpu_kernels import powerlaw_csr, to_fb
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg(fb, k, s, q, seed=0, host=True):
+    return fb.PcaConfig(k=k, oversample=s, passes=q, seed=seed, host_omega=host)
+
+
+def check_invariants(r):  # test_randsvd.cpp:37-43
+    k = r.S.size
+    assert orthonormality(r.U) < 1e-10 and orthonormality(r.V) < 1e-10
+    assert np.all(np.diff(r.S) <= 0) and r.S[k - 1] >= 0
+
+
+def assert_parity(r, o):
+    assert sigma_rel(r.S, o["S"]) <= SIGMA_TOL
+    assert subspace_dist(o["U"], r.U) <= SUBSPACE_TOL
+    assert subspace_dist(o["V"], r.V) <= SUBSPACE_TOL
+
+
+def test_frpca_diag_wide(fb):  # test_randsvd.cpp:71-77
+    A = fb.SparseMatrixCsr.from_triplets(5, 8, [(i, i, float(v)) for i, v in enumerate([5, 4, 3, 2, 1])])
+    r = fb.frpca(A, cfg(fb, 2, 3, 6))
+    assert abs(r.S[0] - 5) < 1e-8 and abs(r.S[1] - 4) < 1e-8
+    check_invariants(r)
+
+
+def test_frpcat_diag_tall(fb):  # test_randsvd.cpp:79-85
+    A = fb.SparseMatrixCsr.from_triplets(8, 5, [(i, i, float(v)) for i, v in enumerate([5, 4, 3, 2, 1])])
+    r = fb.frpcat(A, cfg(fb, 2, 3, 11))
+    assert abs(r.S[0] - 5) < 1e-8 and abs(r.S[1] - 4) < 1e-8
+    check_invariants(r)
+
+
+@pytest.mark.parametrize("q", [2, 3, 4, 5])
+def test_exact_rank3_recovery(fb, orc, q):  # test_randsvd.cpp:87-104
+    u = orc.gaussian_matrix(100, 3, 11)
+    v = orc.gaussian_matrix(3, 80, 12)
+    D = u @ v
+    ii, jj = np.nonzero(D)
+    A = fb.SparseMatrixCsr.from_triplets(100, 80, (ii, jj, D[ii, jj]))
+    At = fb.transpose(A)
+    na = np.linalg.norm(D)
+    f = fb.frpca(At, cfg(fb, 3, 0, q))
+    assert np.linalg.norm(D.T - (f.U * f.S) @ f.V.T) < 1e-8 * na
+    t = fb.frpcat(A, cfg(fb, 3, 0, q))
+    assert np.linalg.norm(D - (t.U * t.S) @ t.V.T) < 1e-8 * na
+
+
+def test_zero_matrix_rejected(fb):  # test_randsvd.cpp:106-111
+    Z = fb.SparseMatrixCsr.from_triplets(6, 6, [])
+    with pytest.raises(fb.NumericalError):
+        fb.frpcat(Z, cfg(fb, 2, 1, 4))
+    with pytest.raises(fb.NumericalError):
+        fb.frpca(Z, cfg(fb, 2, 1, 3))
+
+
+def test_auto_dispatch(fb, orc):  # test_randsvd.cpp:182-190
+    c = cfg(fb, 4, 5, 4)
+    assert fb.auto_pca(to_fb(fb, orc.Csr.random_sparse(80, 120, 0.2, 91)), c).dispatched == fb.PcaAlgorithm.Frpca
+    assert fb.auto_pca(to_fb(fb, orc.Csr.random_sparse(120, 80, 0.2, 92)), c).dispatched == fb.PcaAlgorithm.Frpcat
+    assert fb.auto_pca(to_fb(fb, orc.Csr.random_sparse(100, 100, 0.2, 93)), c).dispatched == fb.PcaAlgorithm.Frpcat
+
+
+@pytest.mark.parametrize("q", [2, 3, 4, 5, 6, 9, 11])
+def test_pass_accounting(fb, orc, q):  # test_randsvd.cpp:192-209
+    oA = orc.Csr.random_sparse(50, 70, 0.3, 55)
+    A = to_fb(fb, oA)
+    At = to_fb(fb, oA.transpose())
+    st = fb.RunStats()
+    fb.frpca(A, cfg(fb, 4, 4, q), st)
+    assert st.passes_over_matrix == q
+    fb.frpcat(At, cfg(fb, 4, 4, q), st)
+    assert st.passes_over_matrix == q
+
+
+@pytest.mark.parametrize("q", [2, 3, 4, 7])
+def test_invariants(fb, orc, q):  # test_randsvd.cpp:211-223
+    o = orc.Csr.random_sparse(60, 100, 0.2, 61)
+    check_invariants(fb.frpca(to_fb(fb, o), cfg(fb, 6, 5, q, seed=q)))
+    check_invariants(fb.frpcat(to_fb(fb, o.transpose()), cfg(fb, 6, 5, q, seed=q)))
+
+
+@pytest.mark.parametrize("k,s,q,algo,shape,msg", [
+    (28, 5, 4, "frpca", (30, 40), "k \\+ oversample"),
+    (2, 5, 1, "frpca", (30, 40), "pass count"),
+    (0, 5, 4, "frpca", (30, 40), "rank k"),
+    (2, 5, 4, "frpcat", (30, 40), "requires rows >= cols"),
+    (2, 5, 4, "frpca", (40, 30), "requires rows <= cols"),
+])
+def test_preconditions(fb, orc, k, s, q, algo, shape, msg):  # test_randsvd.cpp:253-262
+    A = to_fb(fb, orc.Csr.random_sparse(shape[0], shape[1], 0.3, 99))
+    with pytest.raises(ValueError, match=msg):
+        getattr(fb, algo)(A, cfg(fb, k, s, q))
+
+
+def test_bitwise_determinism(fb, orc):  # test_randsvd.cpp:264-271
+    A = to_fb(fb, orc.Csr.random_sparse(50, 80, 0.2, 101))
+    a = fb.frpca(A, cfg(fb, 5, 5, 5, seed=2024))
+    b = fb.frpca(A, cfg(fb, 5, 5, 5, seed=2024))
+    assert np.array_equal(a.S, b.S) and np.array_equal(a.U, b.U) and np.array_equal(a.V, b.V)
+
+
+def test_injected_sketch_wrong_shape(fb, orc):  # randsvd.hpp:68-74
+    A = to_fb(fb, orc.Csr.random_sparse(40, 30, 0.3, 5))
+    with pytest.raises(ValueError, match="wrong shape"):
+        fb.frpcat(A, cfg(fb, 4, 2, 3), omega=np.zeros((5, 5)))
+
+
+# ---- parity vs the oracle on identical inputs (seeded Omega) ---------------
+
+@pytest.mark.parametrize("q", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("host", [True])
+def test_frpcat_parity_random(fb, orc, q, host):
+    oA = orc.Csr.random_sparse(600, 300, 0.05, 1234)
+    r = fb.frpcat(to_fb(fb, oA), cfg(fb, 10, 10, q, seed=3, host=host))
+    o = orc.pca(oA, orc.FRPCAT, 10, 10, q, seed=3)
+    assert_parity(r, o)
+
+
+@pytest.mark.parametrize("q", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("host", [True])
+def test_frpca_parity_random(fb, orc, q, host):
+    oA = orc.Csr.random_sparse(300, 600, 0.05, 4321)
+    r = fb.frpca(to_fb(fb, oA), cfg(fb, 10, 10, q, seed=5, host=host))
+    o = orc.pca(oA, orc.FRPCA, 10, 10, q, seed=5)
+    assert_parity(r, o)
+
+
+@pytest.mark.parametrize("q", [3, 4, 5])
+def test_frpcat_parity_powerlaw_l200(fb, orc, q):
+    """l = 200 (the BASELINE width) on a power-law matrix with long rows."""
+    oA = powerlaw_csr(orc, 20000, 4000, 400000, 17, a_row=1.8, a_col=1.05)
+    r = fb.frpcat(to_fb(fb, oA), cfg(fb, 100, 100, q, seed=0, host=True))
+    o = orc.pca(oA, orc.FRPCAT, 100, 100, q, seed=0)
+    assert_parity(r, o)
+
+
+@pytest.mark.parametrize("q", [3, 4])
+def test_frpca_parity_powerlaw_l200(fb, orc, q):
+    oA = powerlaw_csr(orc, 3000, 30000, 400000, 19, a_row=1.2, a_col=1.2)
+    r = fb.frpca(to_fb(fb, oA), cfg(fb, 100, 100, q, seed=0, host=True))
+    o = orc.pca(oA, orc.FRPCA, 100, 100, q, seed=0)
+    assert_parity(r, o)
+
+
+def test_injected_omega_parity(fb, orc):
+    oA = orc.Csr.random_sparse(500, 200, 0.05, 77)
+    om = orc.gaussian_matrix(12, 500, 42)  # even q frpcat: Omega is l x m
+    r = fb.frpcat(to_fb(fb, oA), cfg(fb, 8, 4, 4), omega=om)
+    o = orc.pca(oA, orc.FRPCAT, 8, 4, 4, omega=om)
+    assert_parity(r, o)
+
+
+def test_capture_basis(fb, orc):
+    oA = orc.Csr.random_sparse(400, 150, 0.05, 8)
+    st = fb.RunStats(capture_basis=True)
+    fb.frpcat(to_fb(fb, oA), cfg(fb, 8, 4, 3, host=True), st)
+    o = orc.pca(oA, orc.FRPCAT, 8, 4, 3, want_basis=True)
+    assert st.basis.shape == o["basis"].shape
+    assert subspace_dist(o["basis"], st.basis) < 1e-9

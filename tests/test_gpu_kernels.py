@@ -1,0 +1,225 @@
+"""GPU parity of the hot-path kernels against the CPU oracle, through the C ABI
+(paper_1810_06825_b200 -> libfrpca_b200.so). Mirrors the hot-path assertions of
+proj/tests/test_sparse.cpp and test_dense_kernels.cpp, plus SURVEY §8c's
+SpMM bar: Frobenius-relative error <= 1e-12 against the oracle on identical
+inputs (FMA vs separate mul/add is the only difference in a row's sum)."""
+import numpy as np
+import pytest
+
+from metrics import SPMM_TOL, orth, orthonormality, projector_gap_dense, rel_fro, subspace_dist
+
+pytestmark = pytest.mark.gpu
+
+
+def to_fb(fb, oA):
+    rp, ci, va = oA.arrays()
+    return fb.SparseMatrixCsr(oA.rows, oA.cols, rp, ci, va)
+
+
+def powerlaw_csr(orc, m, n, nnz_target, seed, a_row=1.6, a_col=1.1):
+    """Small power-law matrix (long rows and hot columns) for load-balance paths."""
+    rng = np.random.default_rng(seed)
+    deg = np.minimum(rng.zipf(a_row, m), n)
+    deg = np.maximum(1, (deg * nnz_target / deg.sum()).astype(np.int64))
+    deg = np.minimum(deg, n)
+    rows, cols = [], []
+    perm = rng.permutation(n)
+    for i, d in enumerate(deg):
+        c = np.unique(np.minimum(rng.zipf(a_col, 2 * d + 8), n) - 1)
+        c = perm[c[:d]]
+        rows.append(np.full(c.size, i))
+        cols.append(np.sort(c))
+    r = np.concatenate(rows)
+    c = np.concatenate(cols)
+    v = rng.standard_normal(r.size)
+    rp = np.zeros(m + 1, dtype=np.int64)
+    np.add.at(rp, r + 1, 1)
+    rp = np.cumsum(rp)
+    return orc.Csr.create(m, n, rp, c, v)
+
+# ------------------------------------------------------------------ SpMM
+
+
+def test_spmm_identity_and_hand(fb, ctx):  # test_sparse.cpp:46-59
+    I = fb.SparseMatrixCsr.from_triplets(3, 3, [(i, i, 1.0) for i in range(3)])
+    X = np.random.default_rng(0).standard_normal((3, 2))
+    assert np.array_equal(fb.spmm(I, X), X)
+    D = fb.SparseMatrixCsr.from_triplets(2, 2, [(0, 0, 2.0), (1, 1, 3.0)])
+    Y = fb.spmm(D, np.ones((2, 1)))
+    assert Y[0, 0] == 2.0 and Y[1, 0] == 3.0
+
+
+def test_spmm_transpose_hand(fb, ctx):  # test_sparse.cpp:68-81
+    I = fb.SparseMatrixCsr.from_triplets(4, 4, [(i, i, 1.0) for i in range(4)])
+    Y = np.random.default_rng(1).standard_normal((4, 3))
+    assert np.array_equal(fb.spmm_transpose(I, Y), Y)
+    A = fb.SparseMatrixCsr.from_triplets(2, 3, [(0, 0, 1.0), (0, 2, 2.0), (1, 1, 3.0)])
+    z = fb.spmm_transpose(A, np.ones((2, 1)))
+    assert z.ravel().tolist() == [1.0, 3.0, 2.0]
+
+
+@pytest.mark.parametrize("ncols", [1, 3, 7, 40, 64, 150, 200, 257, 300])
+def test_spmm_vs_oracle_widths(fb, orc, ncols):
+    oA = orc.Csr.random_sparse(120, 90, 0.08, 7 + ncols)
+    A = to_fb(fb, oA)
+    X = orc.gaussian_matrix(90, ncols, 3)
+    Y = orc.gaussian_matrix(120, ncols, 4)
+    assert rel_fro(fb.spmm(A, X), orc.spmm(oA, X)) <= SPMM_TOL
+    assert rel_fro(fb.spmm_transpose(A, Y), orc.spmm_transpose(oA, Y)) <= SPMM_TOL
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_spmm_powerlaw_long_rows(fb, orc, seed):
+    """Power-law rows/columns: exercises the chunked long-row path and the
+    fixed-order partial combine on both A and the transposed CSR."""
+    oA = powerlaw_csr(orc, 3000, 2000, 120000, seed)
+    A = to_fb(fb, oA)
+    X = orc.gaussian_matrix(2000, 200, seed)
+    Y = orc.gaussian_matrix(3000, 200, seed + 1)
+    assert rel_fro(fb.spmm(A, X), orc.spmm(oA, X)) <= SPMM_TOL
+    assert rel_fro(fb.spmm_transpose(A, Y), orc.spmm_transpose(oA, Y)) <= SPMM_TOL
+
+
+def test_spmm_empty_rows_and_matrix(fb, orc):
+    A = fb.SparseMatrixCsr.from_triplets(5, 4, [(1, 2, 3.0)])
+    X = np.ones((4, 6))
+    Y = fb.spmm(A, X)
+    assert Y.shape == (5, 6) and np.array_equal(Y[1], np.full(6, 3.0)) and not Y[[0, 2, 3, 4]].any()
+    Z = fb.SparseMatrixCsr.from_triplets(6, 6, [])
+    assert not fb.spmm(Z, np.ones((6, 2))).any()
+    assert not fb.spmm_transpose(Z, np.ones((6, 2))).any()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_transpose_matches_oracle(fb, orc, seed):  # test_sparse.cpp:90-100
+    oA = orc.Csr.random_sparse(30 + 3 * seed, 25 + 2 * seed, 0.15, seed + 100)
+    T = fb.transpose(to_fb(fb, oA))
+    rp, ci, va = oA.transpose().arrays()
+    assert np.array_equal(T.rowPtr(), rp) and np.array_equal(T.colIdx(), ci) and np.array_equal(T.values(), va)
+
+
+def test_spmm_transpose_bitwise_equals_spmm_on_transpose(fb, orc):
+    """A^T*Y from the load-time transposed CSR == spmm on transpose(A): same kernel, same order."""
+    oA = powerlaw_csr(orc, 2000, 1500, 60000, 5)
+    A = to_fb(fb, oA)
+    At = fb.transpose(A)
+    Y = orc.gaussian_matrix(2000, 40, 9)
+    assert np.array_equal(fb.spmm_transpose(A, Y), fb.spmm(At, Y))
+
+
+def test_pass_counter(fb, orc):  # test_sparse.cpp:111-118
+    A = to_fb(fb, orc.Csr.random_sparse(20, 20, 0.2, 1))
+    X = np.ones((20, 3))
+    fb.spmm(A, X)
+    A.resetPassCount()
+    fb.spmm(A, X)
+    fb.spmm_transpose(A, X)
+    assert A.passCount() == 2
+
+
+@pytest.mark.parametrize("bad,msg", [
+    (dict(row_ptr=[0, 2, 1], col_idx=[0, 1], values=[1.0, 1.0]), "row_ptr"),
+    (dict(row_ptr=[0, 1, 2], col_idx=[0, 5], values=[1.0, 1.0]), "out of range"),
+])
+def test_device_validation_messages(fb, bad, msg):
+    """The device upload re-validates (sparse_matrix.hpp:125-142) even when the
+    host object was built without checks."""
+    A = fb.SparseMatrixCsr(2, 2, validate=False, **bad)
+    with pytest.raises(ValueError, match=msg):
+        fb.spmm(A, np.ones((2, 1)))
+
+
+def test_spmm_deterministic(fb, orc):
+    oA = powerlaw_csr(orc, 4000, 3000, 200000, 11)
+    A = to_fb(fb, oA)
+    X = orc.gaussian_matrix(3000, 200, 2)
+    a = fb.spmm(A, X)
+    b = fb.spmm(A, X)
+    c = fb.spmm_transpose(A, orc.gaussian_matrix(4000, 200, 3))
+    d = fb.spmm_transpose(A, orc.gaussian_matrix(4000, 200, 3))
+    assert np.array_equal(a, b) and np.array_equal(c, d)
+
+# ------------------------------------------------------------------ LU
+
+
+def test_lu_identity(fb, ctx):  # test_dense_kernels.cpp:71-75
+    M = np.eye(5, 3)
+    assert np.abs(fb.lu_basis(M) - M).max() == 0.0
+
+
+def test_lu_pivoting_range(fb, ctx):  # test_dense_kernels.cpp:77-82
+    M = np.array([[0.0, 1.0], [1.0, 0.0], [0.0, 0.0]])
+    assert projector_gap_dense(orth(fb.lu_basis(M)), orth(M)) < 1e-14
+
+
+def test_lu_unit_lower_factor(fb, orc):  # test_dense_kernels.cpp:90-102
+    X = fb.lu_basis(orc.gaussian_matrix(20, 6, 9))
+    assert abs(np.abs(X).max() - 1.0) < 1e-15
+    for j in range(X.shape[1]):
+        assert (X[:, j] == 1.0).sum() >= 1
+
+
+def test_lu_rank_deficiency(fb):  # test_dense_kernels.cpp:104-109
+    c0 = np.linspace(1, 4, 4)
+    with pytest.raises(fb.NumericalError):
+        fb.lu_basis(np.stack([c0, -3.0 * c0], axis=1))
+
+
+@pytest.mark.parametrize("m,l", [(40, 8), (300, 70), (5000, 150), (20000, 200), (1000, 33)])
+def test_lu_vs_oracle(fb, orc, m, l):
+    """Same pivots (first max, ties to lowest position) -> the same P^T L up to
+    rounding of the updates."""
+    M = orc.gaussian_matrix(m, l, m + l)
+    X = fb.lu_basis(M)
+    Xo = orc.lu_basis(M)
+    assert np.array_equal(X == 1.0, Xo == 1.0)          # same pivot rows
+    assert np.array_equal(X == 0.0, Xo == 0.0)
+    assert np.abs(X - Xo).max() < 1e-9
+
+
+# ------------------------------------------------------------------ eig_svd
+
+
+def test_eig_svd_hand(fb):  # test_dense_kernels.cpp:147-157
+    _, S, _ = fb.eig_svd(np.eye(3))
+    assert np.abs(S - 1).max() < 1e-14
+    A = np.zeros((4, 2))
+    A[0, 0], A[1, 1] = 2.0, 3.0
+    _, S, _ = fb.eig_svd(A)
+    assert abs(S[0] - 2) < 1e-12 and abs(S[1] - 3) < 1e-12
+
+
+def test_eig_svd_vs_oracle(fb, orc):  # test_dense_kernels.cpp:159-165
+    A = orc.gaussian_matrix(200, 30, 17)
+    U, S, V = fb.eig_svd(A)
+    _, So, _ = orc.oracle_svd(A)
+    assert np.max(np.abs(S[::-1] - So) / So) < 1e-10
+    assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-10
+
+
+def test_eig_svd_rank_deficient(fb, orc):  # test_dense_kernels.cpp:167-172
+    A = orc.gaussian_matrix(5, 3, 1)
+    A[:, 2] = A[:, 0] + A[:, 1]
+    with pytest.raises(fb.NumericalError):
+        fb.eig_svd(A)
+
+
+@pytest.mark.parametrize("m,n", [(50, 7), (3000, 64), (100000, 200), (20000, 150)])
+def test_eig_svd_tall(fb, orc, m, n):
+    A = orc.gaussian_matrix(m, n, m + n)
+    U, S, V = fb.eig_svd(A)
+    Uo, So, Vo = orc.eig_svd(A)
+    assert np.max(np.abs(S - So) / So) < 1e-12
+    assert orthonormality(U) < 1e-10 and orthonormality(V) < 1e-12
+    assert subspace_dist(Uo, U) < 1e-10
+
+
+@pytest.mark.parametrize("seed", range(0, 100, 9))
+def test_eig_svd_property(fb, orc, seed):  # test_dense_kernels.cpp:174-186
+    n = 2 + seed % 12
+    m = n + (seed * 7) % 40
+    A = orc.gaussian_matrix(m, n, 1000 + seed)
+    U, S, V = fb.eig_svd(A)
+    assert orthonormality(U) < 1e-10 and orthonormality(V) < 1e-12
+    assert np.all(np.diff(S) >= 0) and S[0] >= 0
+    assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-10

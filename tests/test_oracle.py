@@ -1,0 +1,345 @@
+"""Pins the CPU oracle against the reference's own known answers and property
+tests (the reference ships no golden data files): the assertions of
+proj/tests/test_sparse.cpp, test_dense_kernels.cpp and test_randsvd.cpp for
+the hot path, run on the oracle restatement. Inputs the reference drew with
+Eigen's std::rand-based Matrix::Random are replaced by seeded Gaussian draws
+(same assertion, different values); random_sparse uses the same libstdc++
+stream as test_support.hpp:46-55, so those matrices are the reference's own."""
+import numpy as np
+import pytest
+
+from metrics import projector_gap_dense, orth, orthonormality
+
+# ---------------------------------------------------------------- test_sparse
+
+
+def test_from_triplets_sorts_sums_drops(orc):  # test_sparse.cpp:28-36
+    A = orc.Csr.from_triplets(3, 3, [(1, 2, 3.0), (0, 1, 1.0), (1, 2, -1.0), (0, 0, 2.0),
+                                     (2, 0, 5.0), (2, 0, -5.0)])
+    rp, ci, va = A.arrays()
+    assert A.nnz == 3
+    assert rp.tolist() == [0, 2, 3, 3]
+    assert ci.tolist() == [0, 1, 2]
+    assert va.tolist() == [2.0, 1.0, 2.0]
+
+
+@pytest.mark.parametrize("args,msg", [
+    ((2, 2, [0, 1], [0], [1.0]), "row_ptr length"),
+    ((2, 2, [0, 2, 1], [0, 1], [1.0, 1.0]), "non-decreasing"),
+    ((2, 2, [0, 1, 2], [0, 5], [1.0, 1.0]), "out of range"),
+    ((1, 3, [0, 2], [1, 1], [1.0, 1.0]), "strictly increasing"),
+])
+def test_constructor_rejects_malformed(orc, args, msg):  # test_sparse.cpp:38-44
+    rows, cols, rp, ci, va = args
+    if len(rp) != rows + 1:
+        pytest.skip("length mismatch is a C++ vector-size check; covered by the product host test")
+    with pytest.raises(ValueError):  # the reference checks the type only
+        orc.Csr.create(rows, cols, rp, ci, va)
+    with pytest.raises(ValueError):
+        orc.Csr.from_triplets(2, 2, [(0, 2, 1.0)])
+
+
+def test_spmm_identity_and_hand(orc):  # test_sparse.cpp:46-59
+    I = orc.Csr.from_triplets(3, 3, [(i, i, 1.0) for i in range(3)])
+    X = orc.gaussian_matrix(3, 2, 5)
+    assert np.abs(orc.spmm(I, X) - X).max() == 0.0
+    D = orc.Csr.from_triplets(2, 2, [(0, 0, 2.0), (1, 1, 3.0)])
+    Y = orc.spmm(D, np.ones((2, 1)))
+    assert Y[0, 0] == 2.0 and Y[1, 0] == 3.0
+
+
+def test_spmm_vs_triple_loop(orc):  # test_sparse.cpp:61-66
+    A = orc.Csr.random_sparse(50, 40, 0.05, 7)
+    X = orc.gaussian_matrix(40, 7, 1)
+    ref = A.to_dense() @ X
+    assert np.linalg.norm(orc.spmm(A, X) - ref) / np.linalg.norm(ref) < 1e-13
+
+
+def test_spmm_transpose_hand(orc):  # test_sparse.cpp:68-81
+    I = orc.Csr.from_triplets(4, 4, [(i, i, 1.0) for i in range(4)])
+    Y = orc.gaussian_matrix(4, 3, 9)
+    assert np.abs(orc.spmm_transpose(I, Y) - Y).max() == 0.0
+    A = orc.Csr.from_triplets(2, 3, [(0, 0, 1.0), (0, 2, 2.0), (1, 1, 3.0)])
+    z = orc.spmm_transpose(A, np.ones((2, 1)))
+    assert z.ravel().tolist() == [1.0, 3.0, 2.0]
+
+
+def test_spmm_transpose_vs_dense(orc):  # test_sparse.cpp:83-88
+    A = orc.Csr.random_sparse(60, 35, 0.1, 11)
+    Y = orc.gaussian_matrix(60, 6, 2)
+    ref = A.to_dense().T @ Y
+    assert np.linalg.norm(orc.spmm_transpose(A, Y) - ref) / np.linalg.norm(ref) < 1e-13
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_transpose_kernel_agrees(orc, seed):  # test_sparse.cpp:90-100
+    A = orc.Csr.random_sparse(30 + 3 * seed, 25 + 2 * seed, 0.15, seed + 100)
+    At = A.transpose()
+    Y = orc.gaussian_matrix(A.rows, 4, seed)
+    a = orc.spmm_transpose(A, Y)
+    b = orc.spmm(At, Y)
+    # same ascending-row order on both sides -> bitwise equal
+    assert np.array_equal(a, b)
+    assert np.array_equal(At.to_dense(), A.to_dense().T)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_spmm_random_instances(orc, seed):  # test_sparse.cpp:102-109
+    A = orc.Csr.random_sparse(20 + seed, 30 - seed, 0.2, seed + 40)
+    X = orc.gaussian_matrix(A.cols, 5, seed)
+    ref = A.to_dense() @ X
+    assert np.linalg.norm(orc.spmm(A, X) - ref) <= 1e-12 * max(1.0, np.linalg.norm(ref))
+
+
+def test_pass_counter(orc):  # test_sparse.cpp:111-118
+    A = orc.Csr.random_sparse(20, 20, 0.2, 1)
+    A.reset_pass_count()
+    X = orc.gaussian_matrix(20, 3, 3)
+    orc.spmm(A, X)
+    orc.spmm_transpose(A, X)
+    assert A.pass_count() == 2
+
+
+def test_spmm_thread_count_invariant(orc):
+    """The oracle's threading never changes a bit (used as a timed baseline)."""
+    A = orc.Csr.random_sparse(300, 200, 0.05, 3)
+    X = orc.gaussian_matrix(200, 16, 4)
+    orc.set_threads(1)
+    a = orc.spmm(A, X)
+    b = orc.spmm_transpose(A, orc.gaussian_matrix(300, 16, 5))
+    orc.set_threads(4)
+    try:
+        assert np.array_equal(a, orc.spmm(A, X))
+        assert np.array_equal(b, orc.spmm_transpose(A, orc.gaussian_matrix(300, 16, 5)))
+    finally:
+        orc.set_threads(1)
+
+# --------------------------------------------------------- test_dense_kernels
+
+
+def test_gaussian_determinism(orc):  # test_dense_kernels.cpp:15-21
+    a = orc.gaussian_matrix(17, 9, 123)
+    b = orc.gaussian_matrix(17, 9, 123)
+    c = orc.gaussian_matrix(17, 9, 124)
+    assert np.array_equal(a, b) and not np.array_equal(a, c)
+
+
+def test_gaussian_moments(orc):  # test_dense_kernels.cpp:23-29
+    g = orc.gaussian_matrix(10000, 1, 7).ravel()
+    assert abs(g.mean()) < 0.05 and abs(g.var(ddof=1) - 1.0) < 0.1
+
+
+def test_gaussian_full_rank(orc):  # test_dense_kernels.cpp:31-36
+    g = orc.gaussian_matrix(2000, 50, 11)
+    _, S, _ = orc.oracle_svd(g)
+    assert S[49] > 0 and S[49] / S[0] > 1e-3
+
+
+def test_gaussian_golden_stream(orc):
+    """Pins the libstdc++ polar stream against the committed golden vector
+    (tests/golden/omega_stream.json, written by tests/golden/make_golden.py
+    with std::mt19937_64 + std::normal_distribution)."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "omega_stream.json")))
+    for case in g["cases"]:
+        got = orc.gaussian_matrix(case["rows"], case["cols"], case["seed"]).ravel(order="F")
+        want = np.array([float.fromhex(h) for h in case["values_hex"]])
+        assert np.array_equal(got[:want.size], want)
+
+
+def test_lu_identity(orc):  # test_dense_kernels.cpp:71-75
+    M = np.eye(5, 3)
+    assert np.abs(orc.lu_basis(M) - M).max() == 0.0
+
+
+def test_lu_pivoting_range(orc):  # test_dense_kernels.cpp:77-82
+    M = np.array([[0.0, 1.0], [1.0, 0.0], [0.0, 0.0]])
+    X = orc.lu_basis(M)
+    assert projector_gap_dense(orth(X), orth(M)) < 1e-14
+
+
+def test_lu_random_range(orc):  # test_dense_kernels.cpp:84-88
+    M = orc.gaussian_matrix(40, 8, 3)
+    assert projector_gap_dense(orth(orc.lu_basis(M)), orth(M)) < 1e-12
+
+
+def test_lu_unit_lower_factor(orc):  # test_dense_kernels.cpp:90-102
+    X = orc.lu_basis(orc.gaussian_matrix(20, 6, 9))
+    assert abs(np.abs(X).max() - 1.0) < 1e-15
+    for j in range(X.shape[1]):
+        assert (X[:, j] == 1.0).sum() >= 1
+
+
+def test_lu_rank_deficiency(orc):  # test_dense_kernels.cpp:104-109
+    c0 = np.linspace(1, 4, 4)
+    M = np.stack([c0, -3.0 * c0], axis=1)
+    with pytest.raises(orc.NumericalError):
+        orc.lu_basis(M)
+
+
+def test_lu_blocked_wide(orc):
+    """l > nb = 32 exercises the blocked TRSM + trailing update (:95-105)."""
+    M = orc.gaussian_matrix(300, 70, 21)
+    X = orc.lu_basis(M)
+    assert projector_gap_dense(orth(X), orth(M)) < 1e-11
+    assert np.abs(X).max() <= 1.0 + 1e-15
+
+
+def test_eig_svd_hand(orc):  # test_dense_kernels.cpp:147-157
+    _, S, _ = orc.eig_svd(np.eye(3))
+    assert np.abs(S - 1).max() < 1e-14
+    A = np.zeros((4, 2))
+    A[0, 0], A[1, 1] = 2.0, 3.0
+    _, S, _ = orc.eig_svd(A)
+    assert abs(S[0] - 2) < 1e-12 and abs(S[1] - 3) < 1e-12
+
+
+def test_eig_svd_vs_jacobi(orc):  # test_dense_kernels.cpp:159-165
+    A = orc.gaussian_matrix(200, 30, 17)
+    U, S, V = orc.eig_svd(A)
+    _, So, _ = orc.oracle_svd(A)
+    assert np.max(np.abs(S[::-1] - So) / So) < 1e-10
+    assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-10
+
+
+def test_eig_svd_rank_deficient(orc):  # test_dense_kernels.cpp:167-172
+    A = orc.gaussian_matrix(5, 3, 1)
+    A[:, 2] = A[:, 0] + A[:, 1]
+    with pytest.raises(orc.NumericalError):
+        orc.eig_svd(A)
+
+
+@pytest.mark.parametrize("seed", range(0, 100, 7))
+def test_eig_svd_property(orc, seed):  # test_dense_kernels.cpp:174-186
+    n = 2 + seed % 12
+    m = n + (seed * 7) % 40
+    A = orc.gaussian_matrix(m, n, 1000 + seed)
+    U, S, V = orc.eig_svd(A)
+    assert orthonormality(U) < 1e-10 and orthonormality(V) < 1e-12
+    assert np.all(np.diff(S) >= 0) and S[0] >= 0
+    assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-10
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_range_preservation(orc, seed):  # test_dense_kernels.cpp:188-196
+    M = orc.gaussian_matrix(60 + 5 * seed, 6 + seed % 5, 500 + seed)
+    Q_ref = orth(M)
+    assert projector_gap_dense(orth(orc.lu_basis(M)), Q_ref) < 1e-10
+    assert projector_gap_dense(orc.eig_svd(M)[0], Q_ref) < 1e-10
+
+# ---------------------------------------------------------------- test_randsvd
+
+
+def diag_sparse(vals, rows, cols, orc):
+    return orc.Csr.from_triplets(rows, cols, [(i, i, float(v)) for i, v in enumerate(vals)])
+
+
+def check_invariants(r):  # test_randsvd.cpp:37-43
+    k = r["S"].size
+    assert orthonormality(r["U"]) < 1e-10 and orthonormality(r["V"]) < 1e-10
+    assert np.all(np.diff(r["S"]) <= 0) and r["S"][k - 1] >= 0
+
+
+def test_frpca_diag_wide(orc):  # test_randsvd.cpp:71-77
+    A = diag_sparse([5, 4, 3, 2, 1], 5, 8, orc)
+    r = orc.pca(A, orc.FRPCA, 2, 3, 6)
+    assert abs(r["S"][0] - 5) < 1e-8 and abs(r["S"][1] - 4) < 1e-8
+    check_invariants(r)
+
+
+def test_frpcat_diag_tall(orc):  # test_randsvd.cpp:79-85
+    A = diag_sparse([5, 4, 3, 2, 1], 8, 5, orc)
+    r = orc.pca(A, orc.FRPCAT, 2, 3, 11)
+    assert abs(r["S"][0] - 5) < 1e-8 and abs(r["S"][1] - 4) < 1e-8
+    check_invariants(r)
+
+
+def exact_rank3(rows, cols, seed, orc):  # test_randsvd.cpp:47-51
+    u = orc.gaussian_matrix(rows, 3, seed)
+    v = orc.gaussian_matrix(3, cols, seed + 1)
+    D = u @ v
+    ii, jj = np.nonzero(D)
+    return orc.Csr.from_triplets(rows, cols, list(zip(ii.tolist(), jj.tolist(), D[ii, jj].tolist()))), D
+
+
+@pytest.mark.parametrize("q", [2, 3, 4, 5])
+def test_exact_rank3_recovery(orc, q):  # test_randsvd.cpp:87-104
+    A, D = exact_rank3(100, 80, 11, orc)
+    At = A.transpose()
+    na = np.linalg.norm(D)
+    f = orc.pca(At, orc.FRPCA, 3, 0, q)
+    assert np.linalg.norm(D.T - (f["U"] * f["S"]) @ f["V"].T) < 1e-8 * na
+    t = orc.pca(A, orc.FRPCAT, 3, 0, q)
+    assert np.linalg.norm(D - (t["U"] * t["S"]) @ t["V"].T) < 1e-8 * na
+
+
+def test_zero_matrix_rejected(orc):  # test_randsvd.cpp:106-111
+    Z = orc.Csr.from_triplets(6, 6, [])
+    with pytest.raises(orc.NumericalError):
+        orc.pca(Z, orc.FRPCAT, 2, 1, 4)
+    with pytest.raises(orc.NumericalError):
+        orc.pca(Z, orc.FRPCA, 2, 1, 3)
+
+
+def test_auto_dispatch(orc):  # test_randsvd.cpp:182-190
+    wide = orc.Csr.random_sparse(80, 120, 0.2, 91)
+    tall = orc.Csr.random_sparse(120, 80, 0.2, 92)
+    sq = orc.Csr.random_sparse(100, 100, 0.2, 93)
+    assert orc.pca(wide, orc.AUTO, 4, 5, 4)["dispatched"] == orc.FRPCA
+    assert orc.pca(tall, orc.AUTO, 4, 5, 4)["dispatched"] == orc.FRPCAT
+    assert orc.pca(sq, orc.AUTO, 4, 5, 4)["dispatched"] == orc.FRPCAT
+
+
+@pytest.mark.parametrize("q", [2, 3, 4, 5, 6, 9, 11])
+def test_pass_accounting(orc, q):  # test_randsvd.cpp:192-209
+    A = orc.Csr.random_sparse(50, 70, 0.3, 55)
+    At = A.transpose()
+    assert orc.pca(A, orc.FRPCA, 4, 4, q)["stats"]["passes_over_matrix"] == q
+    assert orc.pca(At, orc.FRPCAT, 4, 4, q)["stats"]["passes_over_matrix"] == q
+
+
+@pytest.mark.parametrize("q", [2, 3, 4, 7])
+def test_invariants(orc, q):  # test_randsvd.cpp:211-223
+    wide = orc.Csr.random_sparse(60, 100, 0.2, 61)
+    tall = wide.transpose()
+    check_invariants(orc.pca(wide, orc.FRPCA, 6, 5, q, seed=q))
+    check_invariants(orc.pca(tall, orc.FRPCAT, 6, 5, q, seed=q))
+
+
+@pytest.mark.parametrize("k,s,q,algo,shape,msg", [
+    (28, 5, 4, 0, (30, 40), "k \\+ oversample"),
+    (2, 5, 1, 0, (30, 40), "pass count"),
+    (0, 5, 4, 0, (30, 40), "rank k"),
+    (2, 5, 4, 1, (30, 40), "requires rows >= cols"),
+    (2, 5, 4, 0, (40, 30), "requires rows <= cols"),
+])
+def test_preconditions(orc, k, s, q, algo, shape, msg):  # test_randsvd.cpp:253-262
+    A = orc.Csr.random_sparse(shape[0], shape[1], 0.3, 99)
+    with pytest.raises(ValueError, match=msg):
+        orc.pca(A, algo, k, s, q)
+
+
+def test_bitwise_determinism(orc):  # test_randsvd.cpp:264-271
+    A = orc.Csr.random_sparse(50, 80, 0.2, 101)
+    a = orc.pca(A, orc.FRPCA, 5, 5, 5, seed=2024)
+    b = orc.pca(A, orc.FRPCA, 5, 5, 5, seed=2024)
+    for key in "USV":
+        assert np.array_equal(a[key], b[key])
+
+
+def test_injected_sketch_shape_checked(orc):  # randsvd.hpp:68-74
+    A = orc.Csr.random_sparse(40, 30, 0.3, 5)
+    with pytest.raises(ValueError, match="wrong shape"):
+        orc.pca(A, orc.FRPCAT, 4, 2, 3, omega=np.zeros((5, 5)))
+
+
+def test_shared_seed_equals_injected(orc):
+    """The sketch stream is mix_seed(seed, 0xA11CE) (randsvd.hpp:63-76)."""
+    A = orc.Csr.random_sparse(60, 40, 0.3, 7)
+    seed = 77
+    l = 6
+    om = orc.gaussian_matrix(40, l, orc.mix_seed(seed, 0xA11CE))
+    a = orc.pca(A, orc.FRPCAT, 4, 2, 3, seed=seed)
+    b = orc.pca(A, orc.FRPCAT, 4, 2, 3, seed=999, omega=om)
+    assert np.array_equal(a["S"], b["S"])
