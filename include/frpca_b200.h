@@ -143,6 +143,12 @@ int frpca_profile_count(frpca_ctx* ctx, int* n);
 int frpca_profile_get(frpca_ctx* ctx, int idx, const char** name, int64_t* launches,
                       double* ms, double* bytes, double* flops);
 int frpca_profile_reset(frpca_ctx* ctx);
+/* Device-time bracket on the ctx stream (CUDA events): begin, then end returns
+ * the elapsed milliseconds between the two events. */
+int frpca_timer_begin(frpca_ctx* ctx);
+int frpca_timer_end(frpca_ctx* ctx, double* ms);
+/* Number of kernels this library has launched in this process (all contexts). */
+int frpca_launch_count(uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,9 @@ SIGNATURES = {
     "frpca_profile_get": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_char_p), _lp,
                                     _dp, _dp, _dp]),
     "frpca_profile_reset": (C.c_int, [_vp]),
+    "frpca_timer_begin": (C.c_int, [_vp]),
+    "frpca_timer_end": (C.c_int, [_vp, _dp]),
+    "frpca_launch_count": (C.c_int, [C.POINTER(_u64)]),
 }
 
 _lib = None

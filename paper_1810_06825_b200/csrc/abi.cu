@@ -46,6 +46,9 @@ struct frpca_dmat : fb::DMat {};
 
 namespace fb {
 
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 cudaEvent_t Ctx::get_event() {
     if (!event_pool.empty()) {
         cudaEvent_t e = event_pool.back();
@@ -169,6 +172,8 @@ int frpca_ctx_destroy(frpca_ctx* c) {
         comm_destroy(*c);
         for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
         for (auto e : c->event_pool) cudaEventDestroy(e);
+        if (c->timer_a) cudaEventDestroy(c->timer_a);
+        if (c->timer_b) cudaEventDestroy(c->timer_b);
         if (c->solver) cusolverDnDestroy(c->solver);
         if (c->stream) cudaStreamDestroy(c->stream);
         delete c;
@@ -401,6 +406,31 @@ int frpca_profile_get(frpca_ctx* c, int idx, const char** name, int64_t* launche
         if (bytes) *bytes = g.bytes;
         if (flops) *flops = g.flops;
     });
+}
+
+int frpca_timer_begin(frpca_ctx* c) {
+    return guarded([&] {
+        check_ctx(c);
+        if (!c->timer_a) FB_CUDA(cudaEventCreate(&c->timer_a));
+        if (!c->timer_b) FB_CUDA(cudaEventCreate(&c->timer_b));
+        FB_CUDA(cudaEventRecord(c->timer_a, c->stream));
+    });
+}
+
+int frpca_timer_end(frpca_ctx* c, double* ms) {
+    return guarded([&] {
+        check_ctx(c);
+        require(c->timer_a != nullptr, "frpca_timer_end: no frpca_timer_begin");
+        FB_CUDA(cudaEventRecord(c->timer_b, c->stream));
+        FB_CUDA(cudaEventSynchronize(c->timer_b));
+        float f = 0.f;
+        FB_CUDA(cudaEventElapsedTime(&f, c->timer_a, c->timer_b));
+        *ms = f;
+    });
+}
+
+int frpca_launch_count(uint64_t* out) {
+    return guarded([&] { *out = g_launches.load(std::memory_order_relaxed); });
 }
 
 }  // extern "C"

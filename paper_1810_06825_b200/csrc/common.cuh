@@ -41,7 +41,14 @@ inline void require(bool cond, const char* msg) {
                                   " (" __FILE__ ":" + std::to_string(__LINE__) + ")");   \
     } while (0)
 
-#define FB_LAUNCH_CHECK() FB_CUDA(cudaGetLastError())
+// Every kernel launch in this library is followed by FB_LAUNCH_CHECK(), which
+// also counts it (frpca_launch_count, reported by bench.py as gpu_launches).
+void count_launch();
+#define FB_LAUNCH_CHECK()        \
+    do {                         \
+        ::fb::count_launch();    \
+        FB_CUDA(cudaGetLastError()); \
+    } while (0)
 
 // Minimal owning device buffer (stream-ordered allocation).
 template <class T>

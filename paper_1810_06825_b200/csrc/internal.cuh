@@ -54,6 +54,7 @@ struct Ctx {
     ncclComm_t comm = nullptr;
     int num_sms = 148;
     std::mutex mu;  // the ABI serialises calls on one context
+    cudaEvent_t timer_a = nullptr, timer_b = nullptr;
 
     // profiling: events around each launch, folded into per-kernel aggregates
     bool prof = false;

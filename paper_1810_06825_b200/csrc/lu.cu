@@ -259,16 +259,18 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
         for (int j = jb; j < jb + bw; ++j) {
             k_pivot<<<1, 1024, 0, s>>>(cand.get(), ncand, j, tol, pos.get(), perm.get(), pivrow.get(),
                                       err.get());
+            FB_LAUNCH_CHECK();
             k_panel_update<<<nblk, kT, 0, s>>>(P.get(), m, jb, bw, j, pos.get(), pivrow.get(), err.get(),
                                               cand.get());
+            FB_LAUNCH_CHECK();
             ncand = nblk;
         }
-        FB_LAUNCH_CHECK();
         k_panel_store<<<nblk, kT, 0, s>>>(W, m, L, jb, bw, P.get());
         FB_LAUNCH_CHECK();
         const int tcols = L - jb - bw;
         if (tcols > 0) {
             k_trsm<<<1, 256, 0, s>>>(W, L, jb, bw, pivrow.get(), err.get());
+            FB_LAUNCH_CHECK();
             const size_t sm = sizeof(double) * size_t(bw) * tcols;
             if (sm > 48 * 1024)
                 FB_CUDA(cudaFuncSetAttribute(k_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize,
