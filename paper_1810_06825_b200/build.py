@@ -26,7 +26,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                   "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-I" + os.path.join(ROOT, "include")]
 CXXFLAGS = ["-std=c++17", "-O3", "-ffp-contract=off", "-fPIC"]
-LDFLAGS = ["-L" + os.path.join(CUDA, "lib64"), "-lcusolver", "-lcublas", "-lnccl",
+LDFLAGS = ["-L" + os.path.join(CUDA, "lib64"), "-lcusolver", "-lcublas", "-ldl",
            "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64")]
 
 

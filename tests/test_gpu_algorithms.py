@@ -11,7 +11,7 @@ from test_gpu_kernels import powerlaw_csr, to_fb
 pytestmark = pytest.mark.gpu
 
 
-def cfg(fb, k, s, q, seed=0, host=True):
+def cfg(fb, k, s, q, seed=0, host=False):
     return fb.PcaConfig(k=k, oversample=s, passes=q, seed=seed, host_omega=host)
 
 
@@ -119,7 +119,7 @@ def test_injected_sketch_wrong_shape(fb, orc):  # randsvd.hpp:68-74
 # ---- parity vs the oracle on identical inputs (seeded Omega) ---------------
 
 @pytest.mark.parametrize("q", [2, 3, 4, 5, 6])
-@pytest.mark.parametrize("host", [True])
+@pytest.mark.parametrize("host", [False, True])
 def test_frpcat_parity_random(fb, orc, q, host):
     oA = orc.Csr.random_sparse(600, 300, 0.05, 1234)
     r = fb.frpcat(to_fb(fb, oA), cfg(fb, 10, 10, q, seed=3, host=host))
@@ -128,7 +128,7 @@ def test_frpcat_parity_random(fb, orc, q, host):
 
 
 @pytest.mark.parametrize("q", [2, 3, 4, 5, 6])
-@pytest.mark.parametrize("host", [True])
+@pytest.mark.parametrize("host", [False, True])
 def test_frpca_parity_random(fb, orc, q, host):
     oA = orc.Csr.random_sparse(300, 600, 0.05, 4321)
     r = fb.frpca(to_fb(fb, oA), cfg(fb, 10, 10, q, seed=5, host=host))
@@ -140,7 +140,7 @@ def test_frpca_parity_random(fb, orc, q, host):
 def test_frpcat_parity_powerlaw_l200(fb, orc, q):
     """l = 200 (the BASELINE width) on a power-law matrix with long rows."""
     oA = powerlaw_csr(orc, 20000, 4000, 400000, 17, a_row=1.8, a_col=1.05)
-    r = fb.frpcat(to_fb(fb, oA), cfg(fb, 100, 100, q, seed=0, host=True))
+    r = fb.frpcat(to_fb(fb, oA), cfg(fb, 100, 100, q, seed=0))
     o = orc.pca(oA, orc.FRPCAT, 100, 100, q, seed=0)
     assert_parity(r, o)
 
@@ -148,7 +148,7 @@ def test_frpcat_parity_powerlaw_l200(fb, orc, q):
 @pytest.mark.parametrize("q", [3, 4])
 def test_frpca_parity_powerlaw_l200(fb, orc, q):
     oA = powerlaw_csr(orc, 3000, 30000, 400000, 19, a_row=1.2, a_col=1.2)
-    r = fb.frpca(to_fb(fb, oA), cfg(fb, 100, 100, q, seed=0, host=True))
+    r = fb.frpca(to_fb(fb, oA), cfg(fb, 100, 100, q, seed=0))
     o = orc.pca(oA, orc.FRPCA, 100, 100, q, seed=0)
     assert_parity(r, o)
 

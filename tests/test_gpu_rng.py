@@ -1,0 +1,52 @@
+"""Device Omega generator vs the libstdc++ stream the reference draws
+(dense_kernels.hpp:19-28): golden vectors (tests/golden/omega_stream.json, made
+by g++ from std::mt19937_64 + std::normal_distribution) and the oracle's
+gaussian_matrix at sizes that cross many jump-ahead segments. Accept/reject
+decisions are exact (they only use r2); values may differ from glibc's log()
+by at most 1 ulp, and almost all are bitwise equal."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "omega_stream.json")))
+
+
+def ulp_diff(a, b):
+    ia = a.view(np.int64)
+    ib = b.view(np.int64)
+    return np.abs(ia - ib)
+
+
+@pytest.mark.parametrize("case", range(len(GOLD["cases"])))
+def test_device_stream_matches_golden(fb, ctx, case):
+    c = GOLD["cases"][case]
+    got = fb.gaussian_matrix(c["rows"], c["cols"], c["seed"]).ravel(order="F")
+    want = np.array([float.fromhex(h) for h in c["values_hex"]])
+    d = ulp_diff(got, want)
+    assert d.max() <= 1
+    assert (d == 0).mean() >= 0.9
+
+
+@pytest.mark.parametrize("rows,cols,seed", [(1000, 7, 1), (100000, 40, 2), (2000000, 3, 3),
+                                            (12345, 200, 0xA11CE)])
+def test_device_stream_matches_host(fb, orc, rows, cols, seed):
+    got = fb.gaussian_matrix(rows, cols, seed)
+    want = orc.gaussian_matrix(rows, cols, seed)
+    d = ulp_diff(got.ravel(order="F"), want.ravel(order="F"))
+    assert d.max() <= 1, f"max ulp diff {d.max()}"
+    assert (d == 0).mean() >= 0.9
+
+
+def test_device_stream_deterministic(fb, ctx):
+    a = fb.gaussian_matrix(50000, 10, 99)
+    b = fb.gaussian_matrix(50000, 10, 99)
+    assert np.array_equal(a, b)
+
+
+def test_device_stream_moments(fb, ctx):  # test_dense_kernels.cpp:23-29
+    g = fb.gaussian_matrix(10000, 1, 7).ravel()
+    assert abs(g.mean()) < 0.05 and abs(g.var(ddof=1) - 1.0) < 0.1
