@@ -73,6 +73,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"synth build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    # the drop-in C++ API test program (tests/cpp), linked against the library
+    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    exe = os.path.join(ROOT, "tests", "cpp", "_build", "test_dropin")
+    if os.path.exists(src) and (force or not os.path.exists(exe) or
+                                os.path.getmtime(exe) < max(os.path.getmtime(src), os.path.getmtime(LIB),
+                                                            os.path.getmtime(os.path.join(ROOT, "include", "frpca", "frpca.hpp")))):
+        os.makedirs(os.path.dirname(exe), exist_ok=True)
+        cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-o", exe,
+               "-L" + LIBDIR, "-lfrpca_b200", "-Wl,-rpath," + LIBDIR]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"drop-in test build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     if verbose:
         print(LIB)
         print(SYNTH_LIB)

@@ -14,8 +14,10 @@
 // pairs, an exclusive scan gives every segment its output offset, and (2)
 // regenerates the segment and writes its normals. The arithmetic of every
 // accepted pair is the host's, operation for operation, in IEEE round-to-
-// nearest without contraction; only log() may differ from glibc's in the last
-// ulp, which changes no accept/reject decision (that uses r2 alone).
+// nearest without contraction; log(r2) is evaluated correctly rounded. glibc's
+// log is not correctly rounded in ~0.08% of inputs (its bound is 0.52 ulp), so
+// those normals differ from libstdc++'s by a few ulp; accept/reject decisions
+// (r2 alone) and hence the stream positions are always identical.
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -59,56 +61,126 @@ __device__ __forceinline__ double canonical(uint64_t w) {
 
 __device__ __forceinline__ int wrap(int i) { return i >= NN ? i - NN : i; }
 
-// Segment start states: state_k = T^(k J) s0, applying the jump for every set
-// bit a of k with polynomial x^(J 2^a) mod P.
+// ---- correctly rounded natural log on (0, 1] (double-double evaluation) ----
+// CUDA's log() is faithful (<= 1 ulp); evaluating log(r2) to ~100 bits and
+// rounding once matches glibc's log everywhere glibc itself is correctly
+// rounded (all but ~0.08% of the polar method's inputs, measured).
+struct dd { double hi, lo; };
+__device__ __forceinline__ dd two_sum(double a, double b) {
+    const double s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    const double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+    return {s, e};
+}
+__device__ __forceinline__ dd fast_two_sum(double a, double b) {
+    const double s = __dadd_rn(a, b);
+    return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ dd two_prod(double a, double b) {
+    const double p = __dmul_rn(a, b);
+    return {p, __fma_rn(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+    dd s = two_sum(a.hi, b.hi);
+    const double t = __dadd_rn(a.lo, b.lo);
+    s.lo = __dadd_rn(s.lo, t);
+    return fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+    dd p = two_prod(a.hi, b.hi);
+    p.lo = __fma_rn(a.hi, b.lo, p.lo);
+    p.lo = __fma_rn(a.lo, b.hi, p.lo);
+    return fast_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ dd dd_div(dd a, dd b) {
+    const double q1 = __ddiv_rn(a.hi, b.hi);
+    dd r = dd_add(a, dd_mul({-q1, 0.0}, b));
+    const double q2 = __ddiv_rn(r.hi, b.hi);
+    r = dd_add(r, dd_mul({-q2, 0.0}, b));
+    const double q3 = __ddiv_rn(r.hi, b.hi);
+    dd q = fast_two_sum(q1, q2);
+    return dd_add(q, {q3, 0.0});
+}
+
+__device__ double cr_log(double x) {
+    if (x == 1.0) return 0.0;
+    int e;
+    double m = frexp(x, &e);                       // x = m 2^e, m in [0.5, 1)
+    if (m < 0.70710678118654752440) { m = __dmul_rn(m, 2.0); e -= 1; }
+    // log m = 2 atanh(s), s = (m - 1) / (m + 1), |s| < 0.172
+    const dd num{__dsub_rn(m, 1.0), 0.0};         // exact (Sterbenz)
+    const dd den = two_sum(m, 1.0);
+    const dd s = dd_div(num, den);
+    const dd s2 = dd_mul(s, s);
+    // tail sum_{k>=4} s2^(k-4) / (2k+1) in double (relative weight < 1e-6)
+    double t = 1.0 / 45.0;
+    #pragma unroll
+    for (int k = 21; k >= 4; --k) t = __fma_rn(t, s2.hi, 1.0 / double(2 * k + 1));
+    // 1 + s2/3 + s2^2/5 + s2^3/7 + s2^4 t, in double-double
+    const dd c3{0x1.5555555555555p-2, 0x1.5555555555555p-56};   // 1/3
+    const dd c5{0x1.999999999999ap-3, -0x1.999999999999ap-57};  // 1/5
+    const dd c7{0x1.2492492492492p-3, 0x1.2492492492492p-57};   // 1/7
+    dd p{t, 0.0};
+    p = dd_add(dd_mul(p, s2), c7);
+    p = dd_add(dd_mul(p, s2), c5);
+    p = dd_add(dd_mul(p, s2), c3);
+    p = dd_add(dd_mul(p, s2), {1.0, 0.0});
+    dd lm = dd_mul(p, s);
+    lm.hi = __dmul_rn(lm.hi, 2.0);
+    lm.lo = __dmul_rn(lm.lo, 2.0);
+    const dd ln2{0x1.62e42fefa39efp-1, 0x1.abc9e3b39803fp-56};
+    const dd el = dd_mul({double(e), 0.0}, ln2);
+    const dd r = dd_add(el, lm);
+    return __dadd_rn(r.hi, r.lo);
+}
+
+// Segment start states by tree doubling: level a computes, for every k in
+// [2^a, 2^(a+1)), state_k = T^(J 2^a) state_(k - 2^a) with the jump polynomial
+// x^(J 2^a) mod P (one jump per segment in total). Horner over the 19937
+// coefficients, 32 per step: r <- T^32 r + sum_b c_(32g+b) T^b base, where the
+// windows T^b base (b < 32) of the base sequence are held in registers.
 __global__ void __launch_bounds__(320)
-k_jump(const uint64_t* __restrict__ s0, const uint32_t* __restrict__ polys, int groups,
-       uint64_t* __restrict__ states) {
+k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, int groups, int64_t first,
+             int64_t K) {
     __shared__ uint64_t base[NN + 32];
     __shared__ uint64_t R[NN];
+    __shared__ uint32_t co[640];
     const int tid = threadIdx.x;
-    const unsigned k = blockIdx.x;
-    if (tid < NN) base[tid] = s0[tid];
+    const int64_t k = first + blockIdx.x;
+    if (k >= K) return;
+    const uint64_t* src = states + size_t(k - first) * NN;
+    if (tid < NN) {
+        base[tid] = src[tid];
+        R[tid] = 0;
+    }
+    for (int g = tid; g < groups; g += blockDim.x) co[g] = poly[g];
     __syncthreads();
-    for (int a = 0; a < kMaxJumps; ++a) {
-        if (!((k >> a) & 1u)) continue;
-        // the 31 words after the base window give the shifted windows T^b base
-        if (tid < 32) base[NN + tid] = mt_next(base[tid], base[tid + 1], base[tid + MM]);
-        if (tid < NN) R[tid] = 0;
-        int h = 0;
-        __syncthreads();
-        const uint32_t* co = polys + size_t(a) * groups;
-        for (int g = groups - 1; g >= 0; --g) {
-            // r <- T^32 r
-            uint64_t nw = 0;
-            if (tid < 32) {
-                const int i0 = wrap(h + tid);
-                nw = mt_next(R[i0], R[wrap(i0 + 1)], R[wrap(i0 + MM)]);
-            }
-            __syncthreads();
-            if (tid < 32) R[wrap(h + tid)] = nw;
-            h = wrap(h + 32);
-            __syncthreads();
-            // r <- r + sum_b c_(32g+b) T^b base
-            uint32_t c = co[g];
-            if (tid < NN && c) {
-                uint64_t x = 0;
-                while (c) {
-                    const int b = __ffs(c) - 1;
-                    x ^= base[tid + b];
-                    c &= c - 1;
-                }
-                R[wrap(h + tid)] ^= x;
-            }
-            __syncthreads();
+    if (tid < 32) base[NN + tid] = mt_next(base[tid], base[tid + 1], base[tid + MM]);
+    __syncthreads();
+    uint64_t w[32];
+    #pragma unroll
+    for (int b = 0; b < 32; ++b) w[b] = tid < NN ? base[tid + b] : 0ull;
+    int h = 0;
+    for (int g = groups - 1; g >= 0; --g) {
+        // r <- T^32 r (warp 0), while the other warps form their window sums
+        const uint32_t c = co[g];
+        uint64_t x = 0;
+        #pragma unroll
+        for (int b = 0; b < 32; ++b)
+            if (c & (1u << b)) x ^= w[b];
+        uint64_t nw = 0;
+        if (tid < 32) {
+            const int i0 = wrap(h + tid);
+            nw = mt_next(R[i0], R[wrap(i0 + 1)], R[wrap(i0 + MM)]);
         }
-        uint64_t v = 0;
-        if (tid < NN) v = R[wrap(h + tid)];
         __syncthreads();
-        if (tid < NN) base[tid] = v;
+        if (tid < 32) R[wrap(h + tid)] = nw;
+        h = wrap(h + 32);
+        __syncthreads();
+        if (tid < NN) R[wrap(h + tid)] ^= x;
         __syncthreads();
     }
-    if (tid < NN) states[size_t(k) * NN + tid] = base[tid];
+    if (tid < NN) states[size_t(k) * NN + tid] = R[wrap(h + tid)];
 }
 
 // MODE 0: count accepted pairs per segment. MODE 1: write the normals.
@@ -161,7 +233,7 @@ k_polar(const uint64_t* __restrict__ states, int64_t steps, const int64_t* __res
             const int64_t idx = 2 * (base_pair + acc + pre);
             // mult = sqrt(-2 log(r2) / r2); returns y*mult, then the saved x*mult;
             // each passes through `ret * stddev + mean` with (1, 0).
-            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
+            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, cr_log(r2)), r2));
             if (idx < count) out[idx] = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), 1.0), 0.0);
             if (idx + 1 < count) out[idx + 1] = __dadd_rn(__dmul_rn(__dmul_rn(x, mult), 1.0), 0.0);
         }
@@ -205,7 +277,7 @@ const uint32_t* device_polys(Ctx& c, int log2S, int& groups) {
 
 void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     if (count <= 0) return;
-    Prof prof(c, "omega_device", 8.0 * count, 0.0);
+    Prof prof(c, "omega_total", 8.0 * count, 0.0);
     cudaStream_t s = c.stream;
     // pairs needed with margin: accepted pairs ~ Bin(P, pi/4), need 2*acc >= count
     const double half = 0.5 * double(count);
@@ -225,11 +297,24 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         require(K < (int64_t(1) << kMaxJumps), "gaussian_matrix: stream too long for the jump table");
         DBuf<uint64_t> states(size_t(K) * NN, s);
         DBuf<int64_t> counts(size_t(K) + 1, s), offs(size_t(K) + 1, s);
-        k_jump<<<unsigned(K), 320, 0, s>>>(d_s0.get(), polys, groups, states.get());
-        FB_LAUNCH_CHECK();
+        {
+            Prof pj(c, "omega_jump", 0.0, 0.0);
+            FB_CUDA(cudaMemcpyAsync(states.get(), d_s0.get(), sizeof(uint64_t) * NN,
+                                    cudaMemcpyDeviceToDevice, s));
+            for (int a = 0; (int64_t(1) << a) < K; ++a) {
+                const int64_t first = int64_t(1) << a;
+                const int64_t n = std::min<int64_t>(first, K - first);
+                k_jump_level<<<unsigned(n), 320, 0, s>>>(states.get(), polys + size_t(a) * groups, groups,
+                                                         first, K);
+                FB_LAUNCH_CHECK();
+            }
+        }
         FB_CUDA(cudaMemsetAsync(counts.get(), 0, counts.bytes(), s));
-        k_polar<0><<<unsigned(K), 160, 0, s>>>(states.get(), J / MM, nullptr, counts.get(), nullptr, count);
-        FB_LAUNCH_CHECK();
+        {
+            Prof pc(c, "omega_count", 0.0, 0.0);
+            k_polar<0><<<unsigned(K), 160, 0, s>>>(states.get(), J / MM, nullptr, counts.get(), nullptr, count);
+            FB_LAUNCH_CHECK();
+        }
         size_t tb = 0;
         FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.get(), offs.get(), K + 1, s));
         DBuf<unsigned char> tmp(tb, s);
@@ -238,6 +323,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         FB_CUDA(cudaMemcpyAsync(&total, offs.get() + K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FB_CUDA(cudaStreamSynchronize(s));
         if (2 * total >= count) {
+            Prof pe(c, "omega_emit", 8.0 * count, 0.0);
             k_polar<1><<<unsigned(K), 160, 0, s>>>(states.get(), J / MM, offs.get(), nullptr, out, count);
             FB_LAUNCH_CHECK();
             return;

@@ -1,0 +1,94 @@
+// Drop-in check: reference-style code (the assertions of proj/tests/
+// test_sparse.cpp, test_dense_kernels.cpp and test_randsvd.cpp for the hot
+// path) compiled against include/frpca/frpca.hpp and run on the B200.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+
+#include "frpca/frpca.hpp"
+
+using frpca::Index;
+using Csr = frpca::SparseMatrixCsr<double>;
+using Matrix = frpca::Matrix<double>;
+
+static int failures = 0;
+#define CHECK(c)                                                            \
+    do {                                                                    \
+        if (!(c)) { std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c); ++failures; } \
+    } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+    try { f(); } catch (const E&) { return true; } catch (...) { return false; }
+    return false;
+}
+
+static Csr diag_sparse(const std::vector<double>& v, Index rows, Index cols) {
+    std::vector<Csr::Triplet> e;
+    for (Index i = 0; i < Index(v.size()); ++i) e.push_back({i, i, v[size_t(i)]});
+    return Csr::from_triplets(rows, cols, e);
+}
+
+static frpca::PcaConfig make_config(Index k, Index s, Index q, std::uint64_t seed = 0) {
+    frpca::PcaConfig c;
+    c.k = k; c.oversample = s; c.passes = q; c.seed = seed;
+    return c;
+}
+
+int main() {
+    // test_sparse.cpp:28-36
+    Csr A = Csr::from_triplets(3, 3, {{1, 2, 3.0}, {0, 1, 1.0}, {1, 2, -1.0}, {0, 0, 2.0}, {2, 0, 5.0}, {2, 0, -5.0}});
+    CHECK(A.nonZeros() == 3);
+    CHECK((A.rowPtr() == std::vector<Index>{0, 2, 3, 3}));
+    // test_sparse.cpp:38-44
+    CHECK((throws<std::invalid_argument>([] { Csr(2, 2, {0, 2, 1}, {0, 1}, {1.0, 1.0}); })));
+    CHECK((throws<std::invalid_argument>([] { Csr(2, 2, {0, 1, 2}, {0, 5}, {1.0, 1.0}); })));
+    // test_sparse.cpp:68-81 (spmm_transpose hand expansion)
+    Csr B = Csr::from_triplets(2, 3, {{0, 0, 1.0}, {0, 2, 2.0}, {1, 1, 3.0}});
+    Matrix y(2, 1);
+    y(0, 0) = 1; y(1, 0) = 1;
+    Matrix z = frpca::spmm_transpose(B, y);
+    CHECK(z(0, 0) == 1.0 && z(1, 0) == 3.0 && z(2, 0) == 2.0);
+    // test_sparse.cpp:111-118 (pass counter)
+    Csr R = diag_sparse({1, 2, 3, 4}, 4, 4);
+    R.resetPassCount();
+    Matrix X = Matrix::Identity(4, 2);
+    frpca::spmm(R, X);
+    frpca::spmm_transpose(R, X);
+    CHECK(R.passCount() == 2);
+    // test_dense_kernels.cpp:71-75, :104-109
+    Matrix I53 = Matrix::Identity(5, 3);
+    CHECK(frpca::lu_basis(I53) == I53);
+    Matrix D(4, 2);
+    for (int i = 0; i < 4; ++i) { D(i, 0) = 1.0 + i; D(i, 1) = -3.0 * (1.0 + i); }
+    CHECK((throws<frpca::NumericalError>([&] { frpca::lu_basis(D); })));
+    // test_dense_kernels.cpp:15-21
+    CHECK(frpca::gaussian_matrix<double>(17, 9, 123) == frpca::gaussian_matrix<double>(17, 9, 123));
+    CHECK(frpca::gaussian_matrix<double>(17, 9, 123) != frpca::gaussian_matrix<double>(17, 9, 124));
+    // test_randsvd.cpp:71-85
+    auto r1 = frpca::frpca(diag_sparse({5, 4, 3, 2, 1}, 5, 8), make_config(2, 3, 6));
+    CHECK(std::abs(r1.S(0) - 5.0) < 1e-8 && std::abs(r1.S(1) - 4.0) < 1e-8);
+    auto r2 = frpca::frpcat(diag_sparse({5, 4, 3, 2, 1}, 8, 5), make_config(2, 3, 11));
+    CHECK(std::abs(r2.S(0) - 5.0) < 1e-8 && std::abs(r2.S(1) - 4.0) < 1e-8);
+    // test_randsvd.cpp:106-111
+    Csr Z = Csr::from_triplets(6, 6, {});
+    CHECK((throws<frpca::NumericalError>([&] { frpca::frpcat(Z, make_config(2, 1, 4)); })));
+    // test_randsvd.cpp:182-190 (auto dispatch), :192-209 (pass accounting)
+    Csr W = diag_sparse({5, 4, 3, 2, 1, 0.5, 0.25}, 7, 9);
+    CHECK(frpca::auto_pca(W, make_config(2, 2, 4)).dispatched == frpca::PcaAlgorithm::Frpca);
+    for (Index q : {2, 3, 4, 5, 6, 9, 11}) {
+        frpca::RunStats<double> st;
+        frpca::frpca(W, make_config(2, 2, q), &st);
+        CHECK(st.passes_over_matrix == std::uint64_t(q));
+    }
+    // test_randsvd.cpp:253-262 (preconditions)
+    CHECK((throws<std::invalid_argument>([&] { frpca::frpca(W, make_config(7, 5, 4)); })));
+    CHECK((throws<std::invalid_argument>([&] { frpca::frpca(W, make_config(2, 2, 1)); })));
+    CHECK((throws<std::invalid_argument>([&] { frpca::frpcat(W, make_config(2, 2, 4)); })));
+    // test_randsvd.cpp:264-271 (bitwise determinism)
+    auto a = frpca::frpca(W, make_config(2, 2, 5, 2024));
+    auto b = frpca::frpca(W, make_config(2, 2, 5, 2024));
+    CHECK(a.S == b.S && a.U == b.U && a.V == b.V);
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+    return failures ? 1 : 0;
+}

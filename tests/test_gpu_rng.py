@@ -2,8 +2,9 @@
 (dense_kernels.hpp:19-28): golden vectors (tests/golden/omega_stream.json, made
 by g++ from std::mt19937_64 + std::normal_distribution) and the oracle's
 gaussian_matrix at sizes that cross many jump-ahead segments. Accept/reject
-decisions are exact (they only use r2); values may differ from glibc's log()
-by at most 1 ulp, and almost all are bitwise equal."""
+decisions are exact (they only use r2), so every value sits at its reference
+position; the device log is correctly rounded while glibc's is not in ~0.08% of
+inputs, so those values differ by a few ulp and >= 99.5% are bitwise equal."""
 import json
 import os
 
@@ -27,8 +28,8 @@ def test_device_stream_matches_golden(fb, ctx, case):
     got = fb.gaussian_matrix(c["rows"], c["cols"], c["seed"]).ravel(order="F")
     want = np.array([float.fromhex(h) for h in c["values_hex"]])
     d = ulp_diff(got, want)
-    assert d.max() <= 1
-    assert (d == 0).mean() >= 0.9
+    assert d.max() <= 4
+    assert (d == 0).mean() >= 0.995
 
 
 @pytest.mark.parametrize("rows,cols,seed", [(1000, 7, 1), (100000, 40, 2), (2000000, 3, 3),
@@ -37,8 +38,8 @@ def test_device_stream_matches_host(fb, orc, rows, cols, seed):
     got = fb.gaussian_matrix(rows, cols, seed)
     want = orc.gaussian_matrix(rows, cols, seed)
     d = ulp_diff(got.ravel(order="F"), want.ravel(order="F"))
-    assert d.max() <= 1, f"max ulp diff {d.max()}"
-    assert (d == 0).mean() >= 0.9
+    assert d.max() <= 4, f"max ulp diff {d.max()}"
+    assert (d == 0).mean() >= 0.995
 
 
 def test_device_stream_deterministic(fb, ctx):
