@@ -91,7 +91,7 @@ __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
 }
 
 template <int VEC, int NCH>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
        const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
        const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
@@ -128,20 +128,40 @@ k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     }
 }
 
-// Long rows: Y[row] = sum of its chunk partials, in chunk order.
-__global__ void __launch_bounds__(kThreads)
-k_combine(const Combine* __restrict__ comb, int64_t ncomb, const double* __restrict__ part,
-          int ncols, double* __restrict__ Y, int64_t ldy) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * kThreads) >> 5;
-    for (int64_t e = warp; e < ncomb; e += nwarps) {
-        const Combine cb = comb[e];
-        for (int c = lane; c < ncols; c += 32) {
-            double acc = part[int64_t(cb.s0) * ncols + c];
-            for (int32_t s = cb.s0 + 1; s < cb.s1; ++s) acc += part[int64_t(s) * ncols + c];
+// Long rows: Y[row] = sum of its chunk partials in a fixed order. One CTA per
+// long row; warp w sums the w-th contiguous eighth of the row's chunks
+// sequentially (loads unrolled), then the eight warp sums are added in warp
+// order -- deterministic, and short enough that no single warp walks the
+// hundreds of partials of a Zipf-head column alone.
+constexpr int kCombWarps = 8;
+__global__ void __launch_bounds__(kCombWarps * 32)
+k_combine(const Combine* __restrict__ comb, const double* __restrict__ part, int ncols,
+          double* __restrict__ Y, int64_t ldy) {
+    __shared__ double red[kCombWarps][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const Combine cb = comb[blockIdx.x];
+    const int ns = cb.s1 - cb.s0;
+    const int per = (ns + kCombWarps - 1) / kCombWarps;
+    const int s0 = cb.s0 + min(ns, warp * per), s1 = cb.s0 + min(ns, (warp + 1) * per);
+    for (int cb0 = 0; cb0 < ncols; cb0 += 256) {
+        for (int c = cb0 + lane; c < min(ncols, cb0 + 256); c += 32) {
+            double acc = 0.0;
+            int s = s0;
+            for (; s + 4 <= s1; s += 4) {
+                const double a0 = part[int64_t(s) * ncols + c], a1 = part[int64_t(s + 1) * ncols + c];
+                const double a2 = part[int64_t(s + 2) * ncols + c], a3 = part[int64_t(s + 3) * ncols + c];
+                acc += a0; acc += a1; acc += a2; acc += a3;
+            }
+            for (; s < s1; ++s) acc += part[int64_t(s) * ncols + c];
+            red[warp][c - cb0] = acc;
+        }
+        __syncthreads();
+        for (int c = cb0 + threadIdx.x; c < min(ncols, cb0 + 256); c += blockDim.x) {
+            double acc = red[0][c - cb0];
+            for (int w = 1; w < kCombWarps; ++w) acc += red[w][c - cb0];
             Y[int64_t(cb.row) * ldy + c] = acc;
         }
+        __syncthreads();
     }
 }
 
@@ -166,6 +186,12 @@ void launch(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int6
 
 }  // namespace
 
+void combine(Ctx& c, const DCsr& A, const double* part, int nc, double* Y, int64_t ldy) {
+    if (!A.ncombine) return;
+    k_combine<<<unsigned(A.ncombine), kCombWarps * 32, 0, c.stream>>>(A.combine.get(), part, nc, Y, ldy);
+    FB_LAUNCH_CHECK();
+}
+
 void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
                  int64_t ldy, const char* tag) {
     if (A.rows == 0 || ncols == 0) return;
@@ -189,34 +215,17 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
                 case 3: launch<2, 3>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
                 default: launch<2, 4>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
             }
+            combine(c, A, part.get(), nc, Yo, ldy);
         } else {
-            const int nch = (nc + 31) / 32;
-            if (nch <= 1) launch<1, 1>(c, A, Xo, ldx, Yo, ldy, part.get(), nc);
-            else if (nch <= 2) launch<1, 2>(c, A, Xo, ldx, Yo, ldy, part.get(), nc);
-            else if (nch <= 4) launch<1, 4>(c, A, Xo, ldx, Yo, ldy, part.get(), nc);
-            else {
-                // odd widths above 128: two launches of <=128 columns
-                launch<1, 4>(c, A, Xo, ldx, Yo, ldy, part.get(), 128);
-                if (A.ncombine) {
-                    k_combine<<<std::max(1, std::min<int>(c.num_sms * 8, int((A.ncombine + 7) / 8))),
-                                kThreads, 0, c.stream>>>(A.combine.get(), A.ncombine, part.get(), 128,
-                                                         Yo, ldy);
-                    FB_LAUNCH_CHECK();
-                }
-                launch<1, 4>(c, A, Xo + 128, ldx, Yo + 128, ldy, part.get(), nc - 128);
-                if (A.ncombine) {
-                    k_combine<<<std::max(1, std::min<int>(c.num_sms * 8, int((A.ncombine + 7) / 8))),
-                                kThreads, 0, c.stream>>>(A.combine.get(), A.ncombine, part.get(),
-                                                         nc - 128, Yo + 128, ldy);
-                    FB_LAUNCH_CHECK();
-                }
-                continue;
+            // scalar path (odd widths): slices of <= 128 columns
+            for (int o = 0; o < nc; o += 128) {
+                const int w = std::min(128, nc - o);
+                const int nch = (w + 31) / 32;
+                if (nch <= 1) launch<1, 1>(c, A, Xo + o, ldx, Yo + o, ldy, part.get(), w);
+                else if (nch <= 2) launch<1, 2>(c, A, Xo + o, ldx, Yo + o, ldy, part.get(), w);
+                else launch<1, 4>(c, A, Xo + o, ldx, Yo + o, ldy, part.get(), w);
+                combine(c, A, part.get(), w, Yo + o, ldy);
             }
-        }
-        if (A.ncombine) {
-            k_combine<<<std::max(1, std::min<int>(c.num_sms * 8, int((A.ncombine + 7) / 8))),
-                        kThreads, 0, c.stream>>>(A.combine.get(), A.ncombine, part.get(), nc, Yo, ldy);
-            FB_LAUNCH_CHECK();
         }
     }
 }
