@@ -137,13 +137,15 @@ __device__ double cr_log(double x) {
 // Segment start states by tree doubling: level a computes, for every k in
 // [2^a, 2^(a+1)), state_k = T^(J 2^a) state_(k - 2^a) with the jump polynomial
 // x^(J 2^a) mod P (one jump per segment in total). Horner over the 19937
-// coefficients, 32 per step: r <- T^32 r + sum_b c_(32g+b) T^b base, where the
-// windows T^b base (b < 32) of the base sequence are held in registers.
+// coefficients, 32 per step: r <- T^32 r + sum_b c_(32g+b) T^b base, with the
+// windows T^b base (b < 32) of the base sequence held in registers. The window
+// r is ping-ponged between two shared buffers, so a step is one barrier:
+// thread j writes r'[j] = (j < 280 ? r[j+32] : next word j-280) ^ x_j.
 __global__ void __launch_bounds__(320)
 k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, int groups, int64_t first,
              int64_t K) {
     __shared__ uint64_t base[NN + 32];
-    __shared__ uint64_t R[NN];
+    __shared__ uint64_t R[2][NN];
     __shared__ uint32_t co[640];
     const int tid = threadIdx.x;
     const int64_t k = first + blockIdx.x;
@@ -151,7 +153,7 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, i
     const uint64_t* src = states + size_t(k - first) * NN;
     if (tid < NN) {
         base[tid] = src[tid];
-        R[tid] = 0;
+        R[0][tid] = 0;
     }
     for (int g = tid; g < groups; g += blockDim.x) co[g] = poly[g];
     __syncthreads();
@@ -160,37 +162,40 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, i
     uint64_t w[32];
     #pragma unroll
     for (int b = 0; b < 32; ++b) w[b] = tid < NN ? base[tid + b] : 0ull;
-    int h = 0;
+    int cur = 0;
     for (int g = groups - 1; g >= 0; --g) {
-        // r <- T^32 r (warp 0), while the other warps form their window sums
         const uint32_t c = co[g];
         uint64_t x = 0;
         #pragma unroll
-        for (int b = 0; b < 32; ++b)
-            if (c & (1u << b)) x ^= w[b];
-        uint64_t nw = 0;
-        if (tid < 32) {
-            const int i0 = wrap(h + tid);
-            nw = mt_next(R[i0], R[wrap(i0 + 1)], R[wrap(i0 + MM)]);
+        for (int b = 0; b < 32; ++b) x ^= (c & (1u << b)) ? w[b] : 0ull;
+        if (tid < NN) {
+            const uint64_t* r = R[cur];
+            uint64_t v;
+            if (tid < NN - 32) {
+                v = r[tid + 32];
+            } else {
+                const int t = tid - (NN - 32);
+                v = mt_next(r[t], r[t + 1], r[t + MM]);
+            }
+            R[cur ^ 1][tid] = v ^ x;
         }
-        __syncthreads();
-        if (tid < 32) R[wrap(h + tid)] = nw;
-        h = wrap(h + 32);
-        __syncthreads();
-        if (tid < NN) R[wrap(h + tid)] ^= x;
+        cur ^= 1;
         __syncthreads();
     }
-    if (tid < NN) states[size_t(k) * NN + tid] = R[wrap(h + tid)];
+    if (tid < NN) states[size_t(k) * NN + tid] = R[cur][tid];
 }
 
 // MODE 0: count accepted pairs per segment. MODE 1: write the normals.
+// One barrier per 156-word step: the window is ping-ponged (thread j < 156
+// shifts X[j+156] down, thread 156+t computes and tempers new word t), the
+// attempt (t, t+1) for even t lives in adjacent lanes of one warp, and the
+// per-warp accept counts of step k go to slot k&1, read after the barrier.
 template <int MODE>
-__global__ void __launch_bounds__(160)
+__global__ void __launch_bounds__(320)
 k_polar(const uint64_t* __restrict__ states, int64_t steps, const int64_t* __restrict__ pair_off,
         int64_t* __restrict__ counts, double* __restrict__ out, int64_t count) {
-    __shared__ uint64_t X[NN];
-    __shared__ uint64_t O[MM];
-    __shared__ int wsum[4];
+    __shared__ uint64_t X[2][NN];
+    __shared__ int wcnt[2][10];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const size_t k = blockIdx.x;
     int64_t base_pair = 0;
@@ -198,38 +203,45 @@ k_polar(const uint64_t* __restrict__ states, int64_t steps, const int64_t* __res
         base_pair = pair_off[k];
         if (2 * base_pair >= count) return;
     }
-    for (int i = tid; i < NN; i += blockDim.x) X[i] = states[k * NN + i];
+    if (tid < NN) X[0][tid] = states[k * NN + tid];
     __syncthreads();
-    int h = 0;
+    int cur = 0;
     int64_t acc = 0;
     for (int64_t st = 0; st < steps; ++st) {
-        uint64_t nw = 0;
+        const int slot = int(st & 1);
+        uint64_t o = 0;
         if (tid < MM) {
-            const int i0 = wrap(h + tid);
-            nw = mt_next(X[i0], X[wrap(i0 + 1)], X[wrap(i0 + MM)]);
+            X[cur ^ 1][tid] = X[cur][tid + MM];
+        } else if (tid < NN) {
+            const int t = tid - MM;
+            const uint64_t* x = X[cur];
+            const uint64_t nw = mt_next(x[t], x[t + 1], x[t + MM]);
+            X[cur ^ 1][tid] = nw;
+            o = temper(nw);
         }
-        __syncthreads();
-        if (tid < MM) {
-            X[wrap(h + tid)] = nw;
-            O[tid] = temper(nw);
-        }
-        h = wrap(h + MM);
-        __syncthreads();
+        const uint64_t o1 = __shfl_down_sync(0xffffffffu, o, 1);
+        const bool mine = tid >= MM && tid < NN && ((tid - MM) & 1) == 0;
         bool ok = false;
         double x = 0, y = 0, r2 = 0;
-        if (tid < MM / 2) {
-            x = __dsub_rn(__dmul_rn(2.0, canonical(O[2 * tid])), 1.0);
-            y = __dsub_rn(__dmul_rn(2.0, canonical(O[2 * tid + 1])), 1.0);
+        if (mine) {
+            x = __dsub_rn(__dmul_rn(2.0, canonical(o)), 1.0);
+            y = __dsub_rn(__dmul_rn(2.0, canonical(o1)), 1.0);
             r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
             ok = !(r2 > 1.0 || r2 == 0.0);
         }
         const unsigned bal = __ballot_sync(0xffffffffu, ok);
-        if (lane == 0 && warp < 3) wsum[warp] = __popc(bal);
+        if (lane == 0) wcnt[slot][warp] = __popc(bal);
+        cur ^= 1;
         __syncthreads();
-        const int tot = wsum[0] + wsum[1] + wsum[2];
+        int tot = 0, pre = 0;
+        #pragma unroll
+        for (int w = 4; w < 10; ++w) {
+            const int cw = wcnt[slot][w];
+            tot += cw;
+            if (w < warp) pre += cw;
+        }
         if (MODE == 1 && ok) {
-            int pre = __popc(bal & ((1u << lane) - 1u));
-            for (int w = 0; w < warp; ++w) pre += wsum[w];
+            pre += __popc(bal & ((1u << lane) - 1u));
             const int64_t idx = 2 * (base_pair + acc + pre);
             // mult = sqrt(-2 log(r2) / r2); returns y*mult, then the saved x*mult;
             // each passes through `ret * stddev + mean` with (1, 0).
@@ -239,7 +251,6 @@ k_polar(const uint64_t* __restrict__ states, int64_t steps, const int64_t* __res
         }
         acc += tot;
         if (MODE == 1 && 2 * (base_pair + acc) >= count) break;
-        __syncthreads();
     }
     if (MODE == 0 && tid == 0) counts[k] = acc;
 }
@@ -312,7 +323,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         FB_CUDA(cudaMemsetAsync(counts.get(), 0, counts.bytes(), s));
         {
             Prof pc(c, "omega_count", 0.0, 0.0);
-            k_polar<0><<<unsigned(K), 160, 0, s>>>(states.get(), J / MM, nullptr, counts.get(), nullptr, count);
+            k_polar<0><<<unsigned(K), 320, 0, s>>>(states.get(), J / MM, nullptr, counts.get(), nullptr, count);
             FB_LAUNCH_CHECK();
         }
         size_t tb = 0;
@@ -324,7 +335,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         FB_CUDA(cudaStreamSynchronize(s));
         if (2 * total >= count) {
             Prof pe(c, "omega_emit", 8.0 * count, 0.0);
-            k_polar<1><<<unsigned(K), 160, 0, s>>>(states.get(), J / MM, offs.get(), nullptr, out, count);
+            k_polar<1><<<unsigned(K), 320, 0, s>>>(states.get(), J / MM, offs.get(), nullptr, out, count);
             FB_LAUNCH_CHECK();
             return;
         }
