@@ -5,16 +5,29 @@
 // :72-80), tol = l * eps * max|M| (:64-65, :81), TRSM for U12 (:98-100),
 // trailing update (:101-104), P^T L assembly (:108-115).
 //
-// B200 layout: rows never move. A position array pos[] (and its inverse perm[])
-// records the interchanges, so a "row swap" is two integer writes instead of
-// two l*8-byte row copies. Each 32-column panel is factored out of a
-// column-major copy P (coalesced thread-per-row access, L2-resident for the
-// configs' panel heights); every column step is a tiny pivot kernel (argmax of
-// the per-CTA candidates) plus one grid-wide update kernel that also emits the
-// next column's candidates.
+// B200 design: ONE cooperative persistent kernel for the whole factorisation.
+//  * Rows never move. Each thread owns a fixed set of rows for the whole run
+//    and keeps their current positions (pos[]); a row interchange at step j
+//    is resolved locally: the pivot row takes position j and the row that
+//    held position j takes the pivot's old position, which travels with the
+//    pivot candidate. No bookkeeping kernel, no race.
+//  * The active 32-column panel lives in a column-major copy P (coalesced
+//    thread-per-row access; L2-resident at the configs' heights).
+//  * Column step = one grid barrier: every CTA reduces all per-CTA candidates
+//    (deterministic: max |v|, ties to the lowest position), reads the pivot
+//    row from P, updates its rows and publishes its best candidate for the
+//    next column.
+//  * After a panel, every CTA solves U12 = L11^{-1} A12 redundantly in shared
+//    memory (U12 is never part of the output P^T L, so it is not stored), then
+//    updates its own rows' trailing columns, stages the next panel into P and
+//    publishes candidates for its first column.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 
 #include "internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace fb {
 namespace {
@@ -31,189 +44,162 @@ __device__ __forceinline__ bool better(double v, int32_t p, double bv, int32_t b
     return v > bv || (v == bv && p < bp);
 }
 
-// block-wide reduction of (v, pos, row); result valid in thread 0
-__device__ Cand block_best(Cand c) {
-    __shared__ Cand sh[32];
+__device__ __forceinline__ void cand_merge(Cand& c, const Cand& o) {
+    if (better(o.v, o.pos, c.v, c.pos)) c = o;
+}
+
+// block-wide reduction; the result is returned to every thread
+__device__ Cand block_best(Cand c, Cand* sh) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int o = 16; o; o >>= 1) {
-        const double v = __shfl_xor_sync(0xffffffffu, c.v, o);
-        const int32_t p = __shfl_xor_sync(0xffffffffu, c.pos, o);
-        const int32_t r = __shfl_xor_sync(0xffffffffu, c.row, o);
-        if (better(v, p, c.v, c.pos)) { c.v = v; c.pos = p; c.row = r; }
+        Cand x;
+        x.v = __shfl_xor_sync(0xffffffffu, c.v, o);
+        x.pos = __shfl_xor_sync(0xffffffffu, c.pos, o);
+        x.row = __shfl_xor_sync(0xffffffffu, c.row, o);
+        cand_merge(c, x);
     }
     if (lane == 0) sh[warp] = c;
     __syncthreads();
-    if (warp == 0) {
-        const int nw = blockDim.x >> 5;
-        c = lane < nw ? sh[lane] : Cand{-1.0, INT32_MAX, -1};
-        for (int o = 16; o; o >>= 1) {
-            const double v = __shfl_xor_sync(0xffffffffu, c.v, o);
-            const int32_t p = __shfl_xor_sync(0xffffffffu, c.pos, o);
-            const int32_t r = __shfl_xor_sync(0xffffffffu, c.row, o);
-            if (better(v, p, c.v, c.pos)) { c.v = v; c.pos = p; c.row = r; }
-        }
-    }
+    Cand r = sh[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) cand_merge(r, sh[w]);
     __syncthreads();
-    return c;
-}
-
-__global__ void k_init(int32_t* pos, int32_t* perm, int64_t m) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
-         i += int64_t(gridDim.x) * blockDim.x)
-        pos[i] = perm[i] = int32_t(i);
-}
-
-// P (column-major m x bw) <- W[:, jb:jb+bw]; candidates for column jb.
-__global__ void __launch_bounds__(kT)
-k_panel_load(const double* __restrict__ W, int64_t m, int l, int jb, int bw, double* __restrict__ P,
-             const int32_t* __restrict__ pos, Cand* __restrict__ cand) {
-    const int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x;
-    Cand c{-1.0, INT32_MAX, -1};
-    if (i < m) {
-        const double* wr = W + i * l + jb;
-        for (int t = 0; t < bw; ++t) P[int64_t(t) * m + i] = wr[t];
-        const int32_t p = pos[i];
-        if (p >= jb) c = Cand{fabs(wr[0]), p, int32_t(i)};
-    }
-    c = block_best(c);
-    if (threadIdx.x == 0) cand[blockIdx.x] = c;
+    return r;
 }
 
 __global__ void __launch_bounds__(kT)
-k_panel_store(double* __restrict__ W, int64_t m, int l, int jb, int bw, const double* __restrict__ P) {
-    const int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x;
-    if (i >= m) return;
-    double* wr = W + i * l + jb;
-    for (int t = 0; t < bw; ++t) wr[t] = P[int64_t(t) * m + i];
-}
+k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ P,
+     int32_t* __restrict__ pos, Cand* __restrict__ cand, int* __restrict__ err) {
+    extern __shared__ double smem[];
+    double* U12 = smem;                     // NB x l (trailing part used)
+    double* L11 = U12 + NB * l;             // NB x NB
+    double* u = L11 + NB * (NB + 1);        // NB
+    __shared__ Cand shc[kT / 32];
+    __shared__ int32_t prow[NB];
+    cg::grid_group grid = cg::this_grid();
+    const int64_t gtid = int64_t(blockIdx.x) * kT + threadIdx.x;
+    const int64_t nthr = int64_t(gridDim.x) * kT;
+    const int nblk = gridDim.x;
 
-// Reduce candidates -> pivot of step j; zero-pivot check (:81); interchange
-// bookkeeping (:82-85) on pos/perm.
-__global__ void __launch_bounds__(1024)
-k_pivot(const Cand* __restrict__ cand, int ncand, int j, double tol, int32_t* __restrict__ pos,
-        int32_t* __restrict__ perm, int32_t* __restrict__ pivrow, int* __restrict__ err) {
-    Cand c{-1.0, INT32_MAX, -1};
-    for (int k = threadIdx.x; k < ncand; k += blockDim.x) {
-        const Cand o = cand[k];
-        if (better(o.v, o.pos, c.v, c.pos)) c = o;
-    }
-    c = block_best(c);
-    if (threadIdx.x == 0) {
-        if (*err) return;
-        if (!(c.v > tol) || c.row < 0) {  // best <= tol
-            *err = 1;
-            return;
+    // prologue: positions, panel 0, candidates of column 0
+    {
+        const int bw = min(NB, l);
+        Cand c{-1.0, INT32_MAX, -1};
+        for (int64_t i = gtid; i < m; i += nthr) {
+            pos[i] = int32_t(i);
+            const double* wr = W + i * l;
+            for (int t = 0; t < bw; ++t) P[int64_t(t) * m + i] = wr[t];
+            cand_merge(c, Cand{fabs(wr[0]), int32_t(i), int32_t(i)});
         }
-        const int32_t pr = c.row;
-        const int32_t a = perm[j];
-        const int32_t pb = pos[pr];
-        perm[j] = pr;
-        perm[pb] = a;
-        pos[pr] = j;
-        pos[a] = pb;
-        pivrow[j] = pr;
-    }
-}
-
-// Step j of the unblocked panel factorisation (:86-93) + candidates of j+1.
-__global__ void __launch_bounds__(kT)
-k_panel_update(double* __restrict__ P, int64_t m, int jb, int bw, int j,
-               const int32_t* __restrict__ pos, const int32_t* __restrict__ pivrow,
-               const int* __restrict__ err, Cand* __restrict__ cand) {
-    if (*err) return;
-    __shared__ double u[NB];
-    const int cl = j - jb;
-    const int32_t pr = pivrow[j];
-    if (threadIdx.x < bw) u[threadIdx.x] = P[int64_t(threadIdx.x) * m + pr];
-    __syncthreads();
-    const double d = u[cl];
-    const int64_t i = int64_t(blockIdx.x) * kT + threadIdx.x;
-    Cand c{-1.0, INT32_MAX, -1};
-    if (i < m) {
-        const int32_t p = pos[i];
-        if (p > j) {
-            const double mi = P[int64_t(cl) * m + i] / d;
-            P[int64_t(cl) * m + i] = mi;
-            for (int t = cl + 1; t < bw; ++t) {
-                double* e = P + int64_t(t) * m + i;
-                *e = *e - mi * u[t];
-            }
-            if (cl + 1 < bw) c = Cand{fabs(P[int64_t(cl + 1) * m + i]), p, int32_t(i)};
-        }
-    }
-    if (cl + 1 < bw) {
-        c = block_best(c);
+        c = block_best(c, shc);
         if (threadIdx.x == 0) cand[blockIdx.x] = c;
     }
-}
 
-// U12 = L11^{-1} A12 on the bw pivot rows (:98-100); one thread per column.
-__global__ void k_trsm(double* __restrict__ W, int l, int jb, int bw, const int32_t* __restrict__ pivrow,
-                       const int* __restrict__ err) {
-    if (*err) return;
-    __shared__ double L[NB][NB + 1];
-    __shared__ int32_t rows[NB];
-    if (threadIdx.x < bw) rows[threadIdx.x] = pivrow[jb + threadIdx.x];
-    __syncthreads();
-    for (int e = threadIdx.x; e < bw * bw; e += blockDim.x) {
-        const int t = e / bw, s = e % bw;
-        L[t][s] = W[int64_t(rows[t]) * l + jb + s];
-    }
-    __syncthreads();
-    for (int c = jb + bw + blockIdx.x * blockDim.x + threadIdx.x; c < l; c += gridDim.x * blockDim.x) {
-        double x[NB];
-        for (int t = 0; t < bw; ++t) {
-            double acc = W[int64_t(rows[t]) * l + c];
-            for (int s = 0; s < t; ++s) acc -= L[t][s] * x[s];
-            x[t] = acc;
-            W[int64_t(rows[t]) * l + c] = acc;
-        }
-    }
-}
-
-// A22 -= L21 * U12 (:101-104) for non-pivot rows; candidates for column jb+bw.
-// One warp per row; lanes over the trailing columns (coalesced row-major).
-__global__ void __launch_bounds__(kT)
-k_trailing(double* __restrict__ W, int64_t m, int l, int jb, int bw, const int32_t* __restrict__ pos,
-           const int32_t* __restrict__ pivrow, const int* __restrict__ err, Cand* __restrict__ cand) {
-    if (*err) return;
-    extern __shared__ double U[];  // bw x tcols
-    const int c0 = jb + bw, tcols = l - c0;
-    for (int e = threadIdx.x; e < bw * tcols; e += blockDim.x) {
-        const int t = e / tcols, cc = e % tcols;
-        U[e] = W[int64_t(pivrow[jb + t]) * l + c0 + cc];
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t(blockIdx.x) * kT + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * kT) >> 5;
-    Cand best{-1.0, INT32_MAX, -1};
-    for (int64_t i = warp; i < m; i += nwarps) {
-        const int32_t p = pos[i];
-        if (p < c0) continue;
-        double* wr = W + i * l;
-        const double lv = lane < bw ? wr[jb + lane] : 0.0;
-        for (int cb = 0; cb < tcols; cb += 32) {
-            const int cc = cb + lane;
-            const bool on = cc < tcols;
-            double acc = on ? wr[c0 + cc] : 0.0;
-            for (int t = 0; t < bw; ++t) {
-                const double lt = __shfl_sync(0xffffffffu, lv, t);
-                if (on) acc -= lt * U[t * tcols + cc];
+    for (int jb = 0; jb < l; jb += NB) {
+        const int bw = min(NB, l - jb);
+        for (int jj = 0; jj < bw; ++jj) {
+            const int j = jb + jj;
+            grid.sync();
+            // every CTA reduces the candidates identically
+            Cand c{-1.0, INT32_MAX, -1};
+            for (int k = threadIdx.x; k < nblk; k += kT) cand_merge(c, cand[k]);
+            const Cand best = block_best(c, shc);
+            if (!(best.v > tol) || best.row < 0) {  // zero pivot (:81)
+                if (blockIdx.x == 0 && threadIdx.x == 0) *err = 1;
+                return;  // uniform across the grid
             }
-            if (on) wr[c0 + cc] = acc;
-            if (cc == 0) {
-                const double v = fabs(acc);
-                if (better(v, p, best.v, best.pos)) best = Cand{v, p, int32_t(i)};
+            const int32_t pr = best.row, pb = best.pos;
+            if (threadIdx.x < bw) u[threadIdx.x] = P[int64_t(threadIdx.x) * m + pr];
+            if (threadIdx.x == 0) prow[jj] = pr;
+            __syncthreads();
+            const double d = u[jj];
+            Cand nc{-1.0, INT32_MAX, -1};
+            for (int64_t i = gtid; i < m; i += nthr) {
+                int32_t p = pos[i];
+                if (i == pr) {
+                    pos[i] = j;
+                    continue;
+                }
+                if (p == j) {  // displaced by the interchange (:82-85)
+                    p = pb;
+                    pos[i] = p;
+                }
+                if (p > j) {
+                    const double mi = P[int64_t(jj) * m + i] / d;   // :88
+                    P[int64_t(jj) * m + i] = mi;
+                    for (int t = jj + 1; t < bw; ++t) {             // :89-92
+                        double* e = P + int64_t(t) * m + i;
+                        *e = *e - mi * u[t];
+                    }
+                    if (jj + 1 < bw) cand_merge(nc, Cand{fabs(P[int64_t(jj + 1) * m + i]), p, int32_t(i)});
+                }
+            }
+            if (jj + 1 < bw) {
+                nc = block_best(nc, shc);
+                if (threadIdx.x == 0) cand[blockIdx.x] = nc;
             }
         }
+        const int c0 = jb + bw, tcols = l - c0;
+        grid.sync();  // the last column's update of every pivot row is visible
+        if (tcols > 0) {
+            // L11 (unit lower) of the bw pivot rows and A12 = their trailing columns
+            for (int e = threadIdx.x; e < bw * bw; e += kT) {
+                const int t = e / bw, s = e % bw;
+                L11[t * (NB + 1) + s] = P[int64_t(s) * m + prow[t]];
+            }
+            for (int e = threadIdx.x; e < bw * tcols; e += kT) {
+                const int t = e / tcols, cc = e % tcols;
+                U12[t * tcols + cc] = W[int64_t(prow[t]) * l + c0 + cc];
+            }
+            __syncthreads();
+            // U12 = L11^{-1} A12 (forward substitution, one column per thread)
+            for (int cc = threadIdx.x; cc < tcols; cc += kT)
+                for (int t = 1; t < bw; ++t) {
+                    double acc = U12[t * tcols + cc];
+                    for (int s = 0; s < t; ++s) acc -= L11[t * (NB + 1) + s] * U12[s * tcols + cc];
+                    U12[t * tcols + cc] = acc;
+                }
+            __syncthreads();
+        }
+        // own rows: write the finished panel back to W, trailing update
+        // A22 -= L21 U12 (:101-104), stage the next panel, candidates.
+        const int nbw = min(NB, tcols);
+        Cand nc{-1.0, INT32_MAX, -1};
+        for (int64_t i = gtid; i < m; i += nthr) {
+            const int32_t p = pos[i];
+            if (p < jb) continue;  // pivot of an earlier panel: finished
+            double* wr = W + i * l;
+            double Lr[NB];
+#pragma unroll
+            for (int t = 0; t < NB; ++t) {
+                if (t < bw) {
+                    Lr[t] = P[int64_t(t) * m + i];
+                    wr[jb + t] = Lr[t];
+                }
+            }
+            // rows pivoted in this panel keep their P entries (other CTAs read
+            // L11 from them) and their trailing columns (A12 of the TRSM)
+            if (tcols > 0 && p >= c0) {
+                for (int cc = 0; cc < tcols; ++cc) {
+                    double acc = wr[c0 + cc];
+#pragma unroll
+                    for (int t = 0; t < NB; ++t)
+                        if (t < bw) acc -= Lr[t] * U12[t * tcols + cc];
+                    wr[c0 + cc] = acc;
+                    if (cc < nbw) P[int64_t(cc) * m + i] = acc;
+                }
+                cand_merge(nc, Cand{fabs(wr[c0]), p, int32_t(i)});
+            }
+        }
+        if (tcols > 0) {
+            nc = block_best(nc, shc);
+            if (threadIdx.x == 0) cand[blockIdx.x] = nc;
+        }
+        __syncthreads();
     }
-    best = block_best(best);
-    if (threadIdx.x == 0) cand[blockIdx.x] = best;
 }
 
-// Output assembly (:108-115): X[r][j] = (j == pos) ? 1 : (j < pos ? W[r][j] : 0).
 __global__ void k_assemble(double* __restrict__ W, int64_t m, int l, const int32_t* __restrict__ pos) {
+    // (:108-115) X[r][j] = (j == pos) ? 1 : (j < pos ? W[r][j] : 0)
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m * l;
          e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / l;
@@ -233,53 +219,30 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
     cudaStream_t s = c.stream;
     const double maxabs = maxabs_device(c, W, m * l);
     const double tol = double(l) * DBL_EPSILON * maxabs;
-    DBuf<int32_t> pos(size_t(m), s), perm(size_t(m), s), pivrow(size_t(l), s);
-    DBuf<int> err(1, s);
-    FB_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(int), s));
-    const int nblk = int((m + kT - 1) / kT);
-    const int tgrid = std::max(1, std::min(nblk, c.num_sms * 8));
-    DBuf<Cand> cand(size_t(std::max(nblk, tgrid)), s);
-    DBuf<double> P(size_t(m) * NB, s);
-    k_init<<<std::min(nblk, c.num_sms * 16), kT, 0, s>>>(pos.get(), perm.get(), m);
-    FB_LAUNCH_CHECK();
-    const int L = int(l);
-    for (int jb = 0; jb < L; jb += NB) {
-        const int bw = std::min(NB, L - jb);
-        // candidates for column jb come from the panel load (jb == 0) or the
-        // previous trailing update
-        int ncand = nblk;
-        if (jb == 0) {
-            k_panel_load<<<nblk, kT, 0, s>>>(W, m, L, jb, bw, P.get(), pos.get(), cand.get());
-        } else {
-            DBuf<Cand> dummy(size_t(nblk), s);
-            k_panel_load<<<nblk, kT, 0, s>>>(W, m, L, jb, bw, P.get(), pos.get(), dummy.get());
-            ncand = tgrid;
-        }
-        FB_LAUNCH_CHECK();
-        for (int j = jb; j < jb + bw; ++j) {
-            k_pivot<<<1, 1024, 0, s>>>(cand.get(), ncand, j, tol, pos.get(), perm.get(), pivrow.get(),
-                                      err.get());
-            FB_LAUNCH_CHECK();
-            k_panel_update<<<nblk, kT, 0, s>>>(P.get(), m, jb, bw, j, pos.get(), pivrow.get(), err.get(),
-                                              cand.get());
-            FB_LAUNCH_CHECK();
-            ncand = nblk;
-        }
-        k_panel_store<<<nblk, kT, 0, s>>>(W, m, L, jb, bw, P.get());
-        FB_LAUNCH_CHECK();
-        const int tcols = L - jb - bw;
-        if (tcols > 0) {
-            k_trsm<<<1, 256, 0, s>>>(W, L, jb, bw, pivrow.get(), err.get());
-            FB_LAUNCH_CHECK();
-            const size_t sm = sizeof(double) * size_t(bw) * tcols;
-            if (sm > 48 * 1024)
-                FB_CUDA(cudaFuncSetAttribute(k_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(sm)));
-            k_trailing<<<tgrid, kT, sm, s>>>(W, m, L, jb, bw, pos.get(), pivrow.get(), err.get(),
-                                            cand.get());
-            FB_LAUNCH_CHECK();
-        }
+    const size_t smem = sizeof(double) * (size_t(NB) * size_t(l) + NB * (NB + 1) + NB);
+    static int attr_set = 0;
+    if (smem > 48 * 1024 || !attr_set) {
+        FB_CUDA(cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(std::max<size_t>(smem, 48 * 1024))));
+        attr_set = 1;
     }
+    int per_sm = 0;
+    FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu, kT, smem));
+    require(per_sm >= 1, "lu_basis: panel width too large for one CTA's shared memory");
+    int grid = std::max(1, std::min<int>(per_sm * c.num_sms, int((m + kT - 1) / kT)));
+    DBuf<int32_t> pos(size_t(m), s);
+    DBuf<int> err(1, s);
+    DBuf<Cand> cand(size_t(grid), s);
+    DBuf<double> P(size_t(m) * NB, s);
+    FB_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(int), s));
+    int L = int(l);
+    double* Pp = P.get();
+    int32_t* posp = pos.get();
+    Cand* candp = cand.get();
+    int* errp = err.get();
+    void* args[] = {&W, &m, &L, const_cast<double*>(&tol), &Pp, &posp, &candp, &errp};
+    FB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_lu), dim3(grid), dim3(kT), args, smem, s));
+    count_launch();
     int h_err = 0;
     FB_CUDA(cudaMemcpyAsync(&h_err, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     FB_CUDA(cudaStreamSynchronize(s));

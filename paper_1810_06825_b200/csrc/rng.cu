@@ -108,9 +108,14 @@ __device__ double cr_log(double x) {
     double m = frexp(x, &e);                       // x = m 2^e, m in [0.5, 1)
     if (m < 0.70710678118654752440) { m = __dmul_rn(m, 2.0); e -= 1; }
     // log m = 2 atanh(s), s = (m - 1) / (m + 1), |s| < 0.172
-    const dd num{__dsub_rn(m, 1.0), 0.0};         // exact (Sterbenz)
+    const double num = __dsub_rn(m, 1.0);         // exact (Sterbenz)
     const dd den = two_sum(m, 1.0);
-    const dd s = dd_div(num, den);
+    // s = num / den to ~2^-104: one division, residual by FMA
+    const double rcp = __ddiv_rn(1.0, den.hi);
+    const double q1 = __dmul_rn(num, rcp);
+    const double rem = __dsub_rn(__fma_rn(-q1, den.hi, num), __dmul_rn(q1, den.lo));
+    const double q2 = __dmul_rn(rem, rcp);
+    const dd s = fast_two_sum(q1, q2);
     const dd s2 = dd_mul(s, s);
     // tail sum_{k>=4} s2^(k-4) / (2k+1) in double (relative weight < 1e-6)
     double t = 1.0 / 45.0;
@@ -186,17 +191,19 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, i
 }
 
 // MODE 0: count accepted pairs per segment. MODE 1: write the normals.
-// One barrier per 156-word step: the window is ping-ponged (thread j < 156
-// shifts X[j+156] down, thread 156+t computes and tempers new word t), the
-// attempt (t, t+1) for even t lives in adjacent lanes of one warp, and the
-// per-warp accept counts of step k go to slot k&1, read after the barrier.
+// One barrier per 156-word step. Threads 0..155 shift the window
+// (ping-ponged X), threads 156..311 compute and temper the 156 new words into
+// O[step & 1]. Warp 0 evaluates the 78 attempts of the PREVIOUS step (lane q
+// takes attempts q, q+32, q+64), so attempt evaluation overlaps generation;
+// its in-order prefix over attempts is warp-local (ballots), no cross-warp sum.
 template <int MODE>
 __global__ void __launch_bounds__(320)
 k_polar(const uint64_t* __restrict__ states, int64_t steps, const int64_t* __restrict__ pair_off,
         int64_t* __restrict__ counts, double* __restrict__ out, int64_t count) {
     __shared__ uint64_t X[2][NN];
-    __shared__ int wcnt[2][10];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ uint64_t O[2][MM];
+    __shared__ int64_t acc_sh;
+    const int tid = threadIdx.x, lane = tid & 31;
     const size_t k = blockIdx.x;
     int64_t base_pair = 0;
     if (MODE == 1) {
@@ -204,53 +211,53 @@ k_polar(const uint64_t* __restrict__ states, int64_t steps, const int64_t* __res
         if (2 * base_pair >= count) return;
     }
     if (tid < NN) X[0][tid] = states[k * NN + tid];
+    if (tid == 0) acc_sh = 0;
     __syncthreads();
     int cur = 0;
-    int64_t acc = 0;
-    for (int64_t st = 0; st < steps; ++st) {
-        const int slot = int(st & 1);
-        uint64_t o = 0;
-        if (tid < MM) {
-            X[cur ^ 1][tid] = X[cur][tid + MM];
-        } else if (tid < NN) {
-            const int t = tid - MM;
-            const uint64_t* x = X[cur];
-            const uint64_t nw = mt_next(x[t], x[t + 1], x[t + MM]);
-            X[cur ^ 1][tid] = nw;
-            o = temper(nw);
+    int64_t acc = 0;  // accepted attempts so far (warp 0)
+    for (int64_t st = 0; st <= steps; ++st) {
+        if (st < steps) {
+            if (tid < MM) {
+                X[cur ^ 1][tid] = X[cur][tid + MM];
+            } else if (tid < NN) {
+                const int t = tid - MM;
+                const uint64_t* x = X[cur];
+                const uint64_t nw = mt_next(x[t], x[t + 1], x[t + MM]);
+                X[cur ^ 1][tid] = nw;
+                O[st & 1][t] = temper(nw);
+            }
         }
-        const uint64_t o1 = __shfl_down_sync(0xffffffffu, o, 1);
-        const bool mine = tid >= MM && tid < NN && ((tid - MM) & 1) == 0;
-        bool ok = false;
-        double x = 0, y = 0, r2 = 0;
-        if (mine) {
-            x = __dsub_rn(__dmul_rn(2.0, canonical(o)), 1.0);
-            y = __dsub_rn(__dmul_rn(2.0, canonical(o1)), 1.0);
-            r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
-            ok = !(r2 > 1.0 || r2 == 0.0);
+        if (tid < 32 && st > 0) {
+            const uint64_t* o = O[(st - 1) & 1];
+            int run = 0;
+            #pragma unroll
+            for (int rnd = 0; rnd < 3; ++rnd) {
+                const int q = rnd * 32 + lane;
+                bool ok = false;
+                double x = 0, y = 0, r2 = 0;
+                if (q < MM / 2) {
+                    x = __dsub_rn(__dmul_rn(2.0, canonical(o[2 * q])), 1.0);
+                    y = __dsub_rn(__dmul_rn(2.0, canonical(o[2 * q + 1])), 1.0);
+                    r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+                    ok = !(r2 > 1.0 || r2 == 0.0);
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                if (MODE == 1 && ok) {
+                    const int64_t idx = 2 * (base_pair + acc + run + __popc(bal & ((1u << lane) - 1u)));
+                    // mult = sqrt(-2 log(r2) / r2); y*mult first, then the saved x*mult;
+                    // each passes through `ret * stddev + mean` with (1, 0).
+                    const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, cr_log(r2)), r2));
+                    if (idx < count) out[idx] = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), 1.0), 0.0);
+                    if (idx + 1 < count) out[idx + 1] = __dadd_rn(__dmul_rn(__dmul_rn(x, mult), 1.0), 0.0);
+                }
+                run += __popc(bal);
+            }
+            acc += run;
+            if (lane == 0) acc_sh = acc;
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, ok);
-        if (lane == 0) wcnt[slot][warp] = __popc(bal);
         cur ^= 1;
         __syncthreads();
-        int tot = 0, pre = 0;
-        #pragma unroll
-        for (int w = 4; w < 10; ++w) {
-            const int cw = wcnt[slot][w];
-            tot += cw;
-            if (w < warp) pre += cw;
-        }
-        if (MODE == 1 && ok) {
-            pre += __popc(bal & ((1u << lane) - 1u));
-            const int64_t idx = 2 * (base_pair + acc + pre);
-            // mult = sqrt(-2 log(r2) / r2); returns y*mult, then the saved x*mult;
-            // each passes through `ret * stddev + mean` with (1, 0).
-            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, cr_log(r2)), r2));
-            if (idx < count) out[idx] = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), 1.0), 0.0);
-            if (idx + 1 < count) out[idx + 1] = __dadd_rn(__dmul_rn(__dmul_rn(x, mult), 1.0), 0.0);
-        }
-        acc += tot;
-        if (MODE == 1 && 2 * (base_pair + acc) >= count) break;
+        if (MODE == 1 && 2 * (base_pair + acc_sh) >= count) break;
     }
     if (MODE == 0 && tid == 0) counts[k] = acc;
 }
