@@ -162,31 +162,6 @@ def ncu_traffic(config: str):
     return None if e is None else e.get("dram_bytes_per_launch")
 
 
-# --------------------------------------------------------------------------- shards
-
-def shard_rows(row_ptr: np.ndarray, world: int, rank: int):
-    """Contiguous row block of this rank, balanced by nnz + rows."""
-    m = row_ptr.size - 1
-    w = row_ptr.astype(np.float64) + np.arange(m + 1)
-    total = w[-1]
-    cuts = [0] + [int(np.searchsorted(w, total * r / world)) for r in range(1, world)] + [m]
-    return cuts[rank], cuts[rank + 1]
-
-
-def shard_cols(row_ptr, col_idx, values, ncols: int, world: int, rank: int):
-    """Column block [c0, c1) of the matrix as a local CSR (frpca)."""
-    counts = np.bincount(col_idx, minlength=ncols).astype(np.float64) + 1.0
-    pref = np.concatenate([[0.0], np.cumsum(counts)])
-    cuts = [0] + [int(np.searchsorted(pref, pref[-1] * r / world)) for r in range(1, world)] + [ncols]
-    c0, c1 = cuts[rank], cuts[rank + 1]
-    keep = (col_idx >= c0) & (col_idx < c1)
-    rowid = np.repeat(np.arange(row_ptr.size - 1), np.diff(row_ptr))
-    rp = np.zeros(row_ptr.size, dtype=np.int64)
-    np.add.at(rp, rowid[keep] + 1, 1)
-    rp = np.cumsum(rp)
-    return c0, c1, rp, np.ascontiguousarray(col_idx[keep] - c0), np.ascontiguousarray(values[keep])
-
-
 # --------------------------------------------------------------------------- arms
 
 def cpu_reference_seconds(cfg, A_arrays, threads: int, budget_s: float = 30.0):
@@ -237,7 +212,7 @@ def run_reference_arm(args, cfg):
 def run_gpu_arm(args, cfg):
     import ctypes as C
     import paper_1810_06825_b200 as fb
-    from paper_1810_06825_b200 import _lib, synth
+    from paper_1810_06825_b200 import _lib, shard, synth
 
     rank, world, local = dist_env()
     dist = Dist(rank, world)
@@ -261,28 +236,26 @@ def run_gpu_arm(args, cfg):
     log(f"[rank {rank}] generated {cfg.name}: {m}x{n}, nnz={int(rp[-1])} in {time.perf_counter() - t0:.1f}s")
     algo = _lib.ALGO_FRPCA if cfg.algorithm == "frpca" else _lib.ALGO_FRPCAT
     if world == 1:
-        shard = dict(grows=m, gcols=n, col_shard=0, off=0, rows=m, cols=n, rp=rp, ci=ci, va=va)
+        shard_ = dict(grows=m, gcols=n, col_shard=0, off=0, rows=m, cols=n, rp=rp, ci=ci, va=va)
     elif algo == _lib.ALGO_FRPCAT:
-        r0, r1 = shard_rows(rp, world, rank)
-        lrp = np.ascontiguousarray(rp[r0:r1 + 1] - rp[r0])
-        shard = dict(grows=m, gcols=n, col_shard=0, off=r0, rows=r1 - r0, cols=n, rp=lrp,
-                     ci=np.ascontiguousarray(ci[rp[r0]:rp[r1]]), va=np.ascontiguousarray(va[rp[r0]:rp[r1]]))
+        r0, r1, lrp, lci, lva = shard.shard_rows(rp, ci, va, world, rank)
+        shard_ = dict(grows=m, gcols=n, col_shard=0, off=r0, rows=r1 - r0, cols=n, rp=lrp, ci=lci, va=lva)
     else:
-        c0, c1, lrp, lci, lva = shard_cols(rp, ci, va, n, world, rank)
-        shard = dict(grows=m, gcols=n, col_shard=1, off=c0, rows=m, cols=c1 - c0, rp=lrp, ci=lci, va=lva)
-    nnz_loc = int(shard["rp"][-1])
+        c0, c1, lrp, lci, lva = shard.shard_cols(rp, ci, va, n, world, rank)
+        shard_ = dict(grows=m, gcols=n, col_shard=1, off=c0, rows=m, cols=c1 - c0, rp=lrp, ci=lci, va=lva)
+    nnz_loc = int(shard_["rp"][-1])
 
     def upload():
         h = C.c_void_p()
         _lib.check(L.frpca_dmat_upload_shard(
-            ctx._h, shard["grows"], shard["gcols"], shard["col_shard"], shard["off"], shard["rows"],
-            shard["cols"], nnz_loc, shard["rp"].ctypes.data, shard["ci"].ctypes.data,
-            shard["va"].ctypes.data, C.byref(h)))
+            ctx._h, shard_["grows"], shard_["gcols"], shard_["col_shard"], shard_["off"], shard_["rows"],
+            shard_["cols"], nnz_loc, shard_["rp"].ctypes.data, shard_["ci"].ctypes.data,
+            shard_["va"].ctypes.data, C.byref(h)))
         return h
 
     k, l = cfg.k, cfg.k + cfg.s
-    m_loc = shard["rows"]
-    n_loc = shard["cols"]
+    m_loc = shard_["rows"]
+    n_loc = shard_["cols"]
     import torch  # device buffers for the device-resident outputs (plumbing only)
     dU = torch.empty(max(1, m_loc * k), dtype=torch.float64, device=f"cuda:{local}")
     dS = torch.empty(k, dtype=torch.float64, device=f"cuda:{local}")
@@ -358,7 +331,7 @@ def run_gpu_arm(args, cfg):
         _lib.check(L.frpca_timer_end(ctx._h, C.byref(ms)))
         dist.barrier()
         e2e_ms.append(dist.max(ms.value))
-    h2d = (shard["rp"].nbytes + shard["ci"].nbytes + shard["va"].nbytes)
+    h2d = (shard_["rp"].nbytes + shard_["ci"].nbytes + shard_["va"].nbytes)
     d2h = 8 * (m_loc * k + k + n_loc * k)
 
     # ---- roofline of the SpMM kernels (algorithmic bytes / measured launch time)

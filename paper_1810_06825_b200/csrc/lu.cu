@@ -124,13 +124,26 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
                     pos[i] = p;
                 }
                 if (p > j) {
-                    const double mi = P[int64_t(jj) * m + i] / d;   // :88
+                    // the row's remaining panel entries: independent loads first
+                    double v[NB];
+#pragma unroll
+                    for (int t = 0; t < NB; ++t)
+                        if (t >= jj && t < bw) v[t] = P[int64_t(t) * m + i];
+                    const double mi = v[jj] / d;                      // :88
                     P[int64_t(jj) * m + i] = mi;
-                    for (int t = jj + 1; t < bw; ++t) {             // :89-92
-                        double* e = P + int64_t(t) * m + i;
-                        *e = *e - mi * u[t];
+#pragma unroll
+                    for (int t = 0; t < NB; ++t)                      // :89-92
+                        if (t > jj && t < bw) {
+                            v[t] = v[t] - mi * u[t];
+                            P[int64_t(t) * m + i] = v[t];
+                        }
+                    if (jj + 1 < bw) {
+                        double nv = 0.0;
+#pragma unroll
+                        for (int t = 1; t < NB; ++t)
+                            if (t == jj + 1) nv = v[t];
+                        cand_merge(nc, Cand{fabs(nv), p, int32_t(i)});
                     }
-                    if (jj + 1 < bw) cand_merge(nc, Cand{fabs(P[int64_t(jj + 1) * m + i]), p, int32_t(i)});
                 }
             }
             if (jj + 1 < bw) {
@@ -179,13 +192,25 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
             // rows pivoted in this panel keep their P entries (other CTAs read
             // L11 from them) and their trailing columns (A12 of the TRSM)
             if (tcols > 0 && p >= c0) {
-                for (int cc = 0; cc < tcols; ++cc) {
-                    double acc = wr[c0 + cc];
+                // 8 trailing columns at a time: independent loads, then FMAs
+                for (int cb = 0; cb < tcols; cb += 8) {
+                    double a[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (cb + e < tcols) a[e] = wr[c0 + cb + e];
 #pragma unroll
                     for (int t = 0; t < NB; ++t)
-                        if (t < bw) acc -= Lr[t] * U12[t * tcols + cc];
-                    wr[c0 + cc] = acc;
-                    if (cc < nbw) P[int64_t(cc) * m + i] = acc;
+                        if (t < bw) {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e)
+                                if (cb + e < tcols) a[e] -= Lr[t] * U12[t * tcols + cb + e];
+                        }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (cb + e < tcols) {
+                            wr[c0 + cb + e] = a[e];
+                            if (cb + e < nbw) P[int64_t(cb + e) * m + i] = a[e];
+                        }
                 }
                 cand_merge(nc, Cand{fabs(wr[c0]), p, int32_t(i)});
             }

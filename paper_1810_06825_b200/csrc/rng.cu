@@ -146,7 +146,7 @@ __device__ double cr_log(double x) {
 // windows T^b base (b < 32) of the base sequence held in registers. The window
 // r is ping-ponged between two shared buffers, so a step is one barrier:
 // thread j writes r'[j] = (j < 280 ? r[j+32] : next word j-280) ^ x_j.
-__global__ void __launch_bounds__(320)
+__global__ void __launch_bounds__(320, 2)
 k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, int groups, int64_t first,
              int64_t K) {
     __shared__ uint64_t base[NN + 32];
@@ -170,9 +170,16 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, i
     int cur = 0;
     for (int g = groups - 1; g >= 0; --g) {
         const uint32_t c = co[g];
-        uint64_t x = 0;
+        // XOR of the selected windows as a 5-level tree (not a 32-long chain)
+        uint64_t t16[16];
         #pragma unroll
-        for (int b = 0; b < 32; ++b) x ^= (c & (1u << b)) ? w[b] : 0ull;
+        for (int b = 0; b < 16; ++b)
+            t16[b] = ((c & (1u << (2 * b))) ? w[2 * b] : 0ull) ^ ((c & (2u << (2 * b))) ? w[2 * b + 1] : 0ull);
+        #pragma unroll
+        for (int h2 = 8; h2 >= 1; h2 >>= 1)
+            #pragma unroll
+            for (int b = 0; b < h2; ++b) t16[b] ^= t16[b + h2];
+        const uint64_t x = t16[0];
         if (tid < NN) {
             const uint64_t* r = R[cur];
             uint64_t v;
