@@ -197,76 +197,104 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, i
     if (tid < NN) states[size_t(k) * NN + tid] = R[cur][tid];
 }
 
-// MODE 0: count accepted pairs per segment. MODE 1: write the normals.
-// One barrier per 156-word step. Threads 0..155 shift the window
-// (ping-ponged X), threads 156..311 compute and temper the 156 new words into
-// O[step & 1]. Warp 0 evaluates the 78 attempts of the PREVIOUS step (lane q
-// takes attempts q, q+32, q+64), so attempt evaluation overlaps generation;
-// its in-order prefix over attempts is warp-local (ballots), no cross-warp sum.
-template <int MODE>
+// Raw stream of a segment: 156 new words per step, one barrier per step
+// (ping-ponged window); the tempered outputs go straight to global memory.
 __global__ void __launch_bounds__(320)
-k_polar(const uint64_t* __restrict__ states, int64_t steps, const int64_t* __restrict__ pair_off,
-        int64_t* __restrict__ counts, double* __restrict__ out, int64_t count) {
+k_gen(const uint64_t* __restrict__ states, int64_t seg0, int64_t steps, uint64_t* __restrict__ raw) {
     __shared__ uint64_t X[2][NN];
-    __shared__ uint64_t O[2][MM];
-    __shared__ int64_t acc_sh;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const size_t k = blockIdx.x;
-    int64_t base_pair = 0;
-    if (MODE == 1) {
-        base_pair = pair_off[k];
-        if (2 * base_pair >= count) return;
-    }
-    if (tid < NN) X[0][tid] = states[k * NN + tid];
-    if (tid == 0) acc_sh = 0;
+    const int tid = threadIdx.x;
+    const int64_t seg = seg0 + blockIdx.x;
+    if (tid < NN) X[0][tid] = states[seg * NN + tid];
     __syncthreads();
+    uint64_t* dst = raw + int64_t(blockIdx.x) * steps * MM;
     int cur = 0;
-    int64_t acc = 0;  // accepted attempts so far (warp 0)
-    for (int64_t st = 0; st <= steps; ++st) {
-        if (st < steps) {
-            if (tid < MM) {
-                X[cur ^ 1][tid] = X[cur][tid + MM];
-            } else if (tid < NN) {
-                const int t = tid - MM;
-                const uint64_t* x = X[cur];
-                const uint64_t nw = mt_next(x[t], x[t + 1], x[t + MM]);
-                X[cur ^ 1][tid] = nw;
-                O[st & 1][t] = temper(nw);
-            }
-        }
-        if (tid < 32 && st > 0) {
-            const uint64_t* o = O[(st - 1) & 1];
-            int run = 0;
-            #pragma unroll
-            for (int rnd = 0; rnd < 3; ++rnd) {
-                const int q = rnd * 32 + lane;
-                bool ok = false;
-                double x = 0, y = 0, r2 = 0;
-                if (q < MM / 2) {
-                    x = __dsub_rn(__dmul_rn(2.0, canonical(o[2 * q])), 1.0);
-                    y = __dsub_rn(__dmul_rn(2.0, canonical(o[2 * q + 1])), 1.0);
-                    r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
-                    ok = !(r2 > 1.0 || r2 == 0.0);
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, ok);
-                if (MODE == 1 && ok) {
-                    const int64_t idx = 2 * (base_pair + acc + run + __popc(bal & ((1u << lane) - 1u)));
-                    // mult = sqrt(-2 log(r2) / r2); y*mult first, then the saved x*mult;
-                    // each passes through `ret * stddev + mean` with (1, 0).
-                    const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, cr_log(r2)), r2));
-                    if (idx < count) out[idx] = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), 1.0), 0.0);
-                    if (idx + 1 < count) out[idx + 1] = __dadd_rn(__dmul_rn(__dmul_rn(x, mult), 1.0), 0.0);
-                }
-                run += __popc(bal);
-            }
-            acc += run;
-            if (lane == 0) acc_sh = acc;
+    for (int64_t st = 0; st < steps; ++st) {
+        if (tid < MM) {
+            X[cur ^ 1][tid] = X[cur][tid + MM];
+        } else if (tid < NN) {
+            const int t = tid - MM;
+            const uint64_t* x = X[cur];
+            const uint64_t nw = mt_next(x[t], x[t + 1], x[t + MM]);
+            X[cur ^ 1][tid] = nw;
+            dst[st * MM + t] = temper(nw);
         }
         cur ^= 1;
         __syncthreads();
-        if (MODE == 1 && 2 * (base_pair + acc_sh) >= count) break;
     }
-    if (MODE == 0 && tid == 0) counts[k] = acc;
+}
+
+// polar attempt on raw words (w0, w1): x = 2u1 - 1, y = 2u2 - 1, r2 = x^2 + y^2
+__device__ __forceinline__ bool attempt(uint64_t w0, uint64_t w1, double& x, double& y, double& r2) {
+    x = __dsub_rn(__dmul_rn(2.0, canonical(w0)), 1.0);
+    y = __dsub_rn(__dmul_rn(2.0, canonical(w1)), 1.0);
+    r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+    return !(r2 > 1.0 || r2 == 0.0);
+}
+
+constexpr int PT = 256;      // threads per chunk CTA
+constexpr int PPT = 4;       // attempts per thread
+constexpr int CHUNK = PT * PPT;
+
+// accepted attempts per chunk of CHUNK consecutive attempts
+__global__ void __launch_bounds__(PT)
+k_count(const uint64_t* __restrict__ raw, int64_t npairs, int64_t* __restrict__ cnt) {
+    __shared__ int red[PT / 32];
+    const int64_t p0 = int64_t(blockIdx.x) * CHUNK + threadIdx.x * PPT;
+    int c = 0;
+    #pragma unroll
+    for (int e = 0; e < PPT; ++e) {
+        const int64_t q = p0 + e;
+        if (q < npairs) {
+            const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(raw + 2 * q);
+            double x, y, r2;
+            c += attempt(w.x, w.y, x, y, r2) ? 1 : 0;
+        }
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < PT / 32; ++w) t += red[w];
+        cnt[blockIdx.x] = t;
+    }
+}
+
+// normals of the accepted attempts, written at their stream positions
+__global__ void __launch_bounds__(PT)
+k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restrict__ off,
+       double* __restrict__ out, int64_t count) {
+    using Scan = cub::BlockScan<int, PT>;
+    __shared__ typename Scan::TempStorage tmp;
+    const int64_t base = off[blockIdx.x];
+    if (2 * base >= count) return;
+    const int64_t p0 = int64_t(blockIdx.x) * CHUNK + threadIdx.x * PPT;
+    double xs[PPT], ys[PPT], rs[PPT];
+    bool ok[PPT];
+    int c = 0;
+    #pragma unroll
+    for (int e = 0; e < PPT; ++e) {
+        const int64_t q = p0 + e;
+        ok[e] = false;
+        if (q < npairs) {
+            const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(raw + 2 * q);
+            ok[e] = attempt(w.x, w.y, xs[e], ys[e], rs[e]);
+        }
+        c += ok[e] ? 1 : 0;
+    }
+    int pre = 0;
+    Scan(tmp).ExclusiveSum(c, pre);
+    int64_t idx = 2 * (base + pre);
+    #pragma unroll
+    for (int e = 0; e < PPT; ++e) {
+        if (!ok[e]) continue;
+        // mult = sqrt(-2 log(r2) / r2); y*mult first, then the saved x*mult; each
+        // passes through `ret * stddev + mean` with (1, 0) (random.tcc).
+        const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, cr_log(rs[e])), rs[e]));
+        if (idx < count) out[idx] = __dadd_rn(__dmul_rn(__dmul_rn(ys[e], mult), 1.0), 0.0);
+        if (idx + 1 < count) out[idx + 1] = __dadd_rn(__dmul_rn(__dmul_rn(xs[e], mult), 1.0), 0.0);
+        idx += 2;
+    }
 }
 
 struct PolyCache {
@@ -304,58 +332,80 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     if (count <= 0) return;
     Prof prof(c, "omega_total", 8.0 * count, 0.0);
     cudaStream_t s = c.stream;
-    // pairs needed with margin: accepted pairs ~ Bin(P, pi/4), need 2*acc >= count
+    // attempts needed with margin: accepted ~ Bin(P, pi/4), need 2*acc >= count
     const double half = 0.5 * double(count);
-    int64_t P = int64_t(half / (M_PI / 4.0) + 8.0 * std::sqrt(half / (M_PI / 4.0)) + 64.0);
-    // segments of J = 156 * 2^e words (~2k segments at most per 2^e step)
+    const int64_t P = int64_t(half / (M_PI / 4.0) + 8.0 * std::sqrt(half / (M_PI / 4.0)) + 64.0);
+    // segments of J = 156 * 2^e words, at most ~2048 of them per level of 2^e
     int log2S = 6;
     while (log2S < 14 && (2 * P) / (int64_t(MM) << log2S) > 2048) ++log2S;
-    const int64_t J = int64_t(MM) << log2S;
+    const int64_t steps = int64_t(1) << log2S, J = int64_t(MM) << log2S;
     int groups = 0;
     const uint32_t* polys = device_polys(c, log2S, groups);
     uint64_t s0[NN];
     mt64_seed_state(seed, s0);
-    DBuf<uint64_t> d_s0(NN, s);
-    FB_CUDA(cudaMemcpyAsync(d_s0.get(), s0, sizeof(s0), cudaMemcpyHostToDevice, s));
-    for (int attempt = 0; attempt < 4; ++attempt) {
-        const int64_t K = (2 * P + J - 1) / J;
-        require(K < (int64_t(1) << kMaxJumps), "gaussian_matrix: stream too long for the jump table");
-        DBuf<uint64_t> states(size_t(K) * NN, s);
-        DBuf<int64_t> counts(size_t(K) + 1, s), offs(size_t(K) + 1, s);
-        {
-            Prof pj(c, "omega_jump", 0.0, 0.0);
-            FB_CUDA(cudaMemcpyAsync(states.get(), d_s0.get(), sizeof(uint64_t) * NN,
-                                    cudaMemcpyDeviceToDevice, s));
-            for (int a = 0; (int64_t(1) << a) < K; ++a) {
+    int64_t K = (2 * P + J - 1) / J;
+    // segment start states (tree doubling), computed for up to 2K segments
+    // so that the rare shortfall never needs a recomputation
+    const int64_t Kmax = 2 * K + 1;
+    require(Kmax < (int64_t(1) << kMaxJumps), "gaussian_matrix: stream too long for the jump table");
+    DBuf<uint64_t> states(size_t(Kmax) * NN, s);
+    {
+        Prof pj(c, "omega_jump", 0.0, 0.0);
+        FB_CUDA(cudaMemcpyAsync(states.get(), s0, sizeof(s0), cudaMemcpyHostToDevice, s));
+        for (int a = 0; (int64_t(1) << a) < K; ++a) {
+            const int64_t first = int64_t(1) << a;
+            const int64_t n = std::min<int64_t>(first, K - first);
+            k_jump_level<<<unsigned(n), 320, 0, s>>>(states.get(), polys + size_t(a) * groups, groups,
+                                                     first, K);
+            FB_LAUNCH_CHECK();
+        }
+    }
+    // batches of segments: raw words -> per-chunk counts -> scan -> normals
+    const int64_t seg_per_batch = std::max<int64_t>(1, (int64_t(1) << 28) / J);
+    DBuf<uint64_t> raw(size_t(std::min(K, seg_per_batch) * J), s);
+    int64_t pairs_done = 0;  // accepted attempts emitted so far
+    for (int64_t seg0 = 0; 2 * pairs_done < count; seg0 += seg_per_batch) {
+        if (seg0 >= K) {
+            // shortfall (probability ~ 1e-15): extend the jump table to Kmax
+            require(seg0 < Kmax, "gaussian_matrix: device stream generation did not converge");
+            for (int a = 0; (int64_t(1) << a) < Kmax; ++a) {
                 const int64_t first = int64_t(1) << a;
-                const int64_t n = std::min<int64_t>(first, K - first);
-                k_jump_level<<<unsigned(n), 320, 0, s>>>(states.get(), polys + size_t(a) * groups, groups,
-                                                         first, K);
+                if (first + std::min<int64_t>(first, Kmax - first) <= K) continue;
+                k_jump_level<<<unsigned(std::min<int64_t>(first, Kmax - first)), 320, 0, s>>>(
+                    states.get(), polys + size_t(a) * groups, groups, first, Kmax);
                 FB_LAUNCH_CHECK();
             }
+            K = Kmax;
         }
-        FB_CUDA(cudaMemsetAsync(counts.get(), 0, counts.bytes(), s));
+        const int64_t nseg = std::min(seg_per_batch, K - seg0);
+        const int64_t npairs = nseg * J / 2;
+        const int64_t nchunks = (npairs + CHUNK - 1) / CHUNK;
         {
-            Prof pc(c, "omega_count", 0.0, 0.0);
-            k_polar<0><<<unsigned(K), 320, 0, s>>>(states.get(), J / MM, nullptr, counts.get(), nullptr, count);
+            Prof pg(c, "omega_gen", 8.0 * nseg * J, 0.0);
+            k_gen<<<unsigned(nseg), 320, 0, s>>>(states.get(), seg0, steps, raw.get());
             FB_LAUNCH_CHECK();
         }
-        size_t tb = 0;
-        FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.get(), offs.get(), K + 1, s));
-        DBuf<unsigned char> tmp(tb, s);
-        FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, counts.get(), offs.get(), K + 1, s));
-        int64_t total = 0;
-        FB_CUDA(cudaMemcpyAsync(&total, offs.get() + K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        DBuf<int64_t> cnt(size_t(nchunks) + 1, s), off(size_t(nchunks) + 1, s);
+        {
+            Prof pc(c, "omega_count", 8.0 * nseg * J, 0.0);
+            FB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+            k_count<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, cnt.get());
+            FB_LAUNCH_CHECK();
+            size_t tb = 0;
+            FB_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tb, cnt.get(), off.get(), cub::Sum(),
+                                                   pairs_done, nchunks + 1, s));
+            DBuf<unsigned char> tmp(tb, s);
+            FB_CUDA(cub::DeviceScan::ExclusiveScan(tmp.get(), tb, cnt.get(), off.get(), cub::Sum(),
+                                                   pairs_done, nchunks + 1, s));
+        }
+        {
+            Prof pe(c, "omega_emit", 8.0 * nseg * J + 8.0 * count, 0.0);
+            k_emit<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, off.get(), out, count);
+            FB_LAUNCH_CHECK();
+        }
+        FB_CUDA(cudaMemcpyAsync(&pairs_done, off.get() + nchunks, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FB_CUDA(cudaStreamSynchronize(s));
-        if (2 * total >= count) {
-            Prof pe(c, "omega_emit", 8.0 * count, 0.0);
-            k_polar<1><<<unsigned(K), 320, 0, s>>>(states.get(), J / MM, offs.get(), nullptr, out, count);
-            FB_LAUNCH_CHECK();
-            return;
-        }
-        P = P + P / 8 + 1024;
     }
-    throw CudaError("gaussian_matrix: device stream generation did not converge");
 }
 
 }  // namespace fb
