@@ -142,14 +142,21 @@ __device__ double cr_log(double x) {
 // Segment start states by tree doubling: level a computes, for every k in
 // [2^a, 2^(a+1)), state_k = T^(J 2^a) state_(k - 2^a) with the jump polynomial
 // x^(J 2^a) mod P (one jump per segment in total). Horner over the 19937
-// coefficients, 32 per step: r <- T^32 r + sum_b c_(32g+b) T^b base, with the
-// windows T^b base (b < 32) of the base sequence held in registers. The window
-// r is ping-ponged between two shared buffers, so a step is one barrier:
-// thread j writes r'[j] = (j < 280 ? r[j+32] : next word j-280) ^ x_j.
+// coefficients, 32 per step: r <- T^32 r + sum_b c_(32g+b) T^b base.
+// The window T^b base is the base sequence shifted by b, so one shared table
+// serves every thread: N[v][j] = XOR of ext[j + i] over the set bits i of the
+// nibble v, and the 32-coefficient sum for thread j is
+//   XOR_q N[nibble_q(c)][j + 4q], q = 0..7  (8 shared loads, conflict-free).
+// The window r is ping-ponged, so a step is one barrier.
+constexpr int NTAB = NN + 32;  // table row length (j + 4q + 3 < NN + 31)
+constexpr size_t kNibBytes = sizeof(uint64_t) * 16 * NTAB;
+
 __global__ void __launch_bounds__(320, 2)
 k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, int groups, int64_t first,
              int64_t K) {
-    __shared__ uint64_t base[NN + 32];
+    __shared__ uint64_t ext[NN + 32];
+    extern __shared__ uint64_t nib_dyn[];  // [16][NTAB]
+    uint64_t (*nib)[NTAB] = reinterpret_cast<uint64_t (*)[NTAB]>(nib_dyn);
     __shared__ uint64_t R[2][NN];
     __shared__ uint32_t co[640];
     const int tid = threadIdx.x;
@@ -157,30 +164,29 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, i
     if (k >= K) return;
     const uint64_t* src = states + size_t(k - first) * NN;
     if (tid < NN) {
-        base[tid] = src[tid];
+        ext[tid] = src[tid];
         R[0][tid] = 0;
     }
     for (int g = tid; g < groups; g += blockDim.x) co[g] = poly[g];
     __syncthreads();
-    if (tid < 32) base[NN + tid] = mt_next(base[tid], base[tid + 1], base[tid + MM]);
+    if (tid < 32) ext[NN + tid] = mt_next(ext[tid], ext[tid + 1], ext[tid + MM]);
     __syncthreads();
-    uint64_t w[32];
-    #pragma unroll
-    for (int b = 0; b < 32; ++b) w[b] = tid < NN ? base[tid + b] : 0ull;
+    for (int e = tid; e < 16 * NTAB; e += blockDim.x) {
+        const int v = e / NTAB, j = e % NTAB;
+        uint64_t x = 0;
+        #pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (((v >> i) & 1) && j + i < NN + 32) x ^= ext[j + i];
+        nib[v][j] = x;
+    }
+    __syncthreads();
     int cur = 0;
     for (int g = groups - 1; g >= 0; --g) {
         const uint32_t c = co[g];
-        // XOR of the selected windows as a 5-level tree (not a 32-long chain)
-        uint64_t t16[16];
-        #pragma unroll
-        for (int b = 0; b < 16; ++b)
-            t16[b] = ((c & (1u << (2 * b))) ? w[2 * b] : 0ull) ^ ((c & (2u << (2 * b))) ? w[2 * b + 1] : 0ull);
-        #pragma unroll
-        for (int h2 = 8; h2 >= 1; h2 >>= 1)
-            #pragma unroll
-            for (int b = 0; b < h2; ++b) t16[b] ^= t16[b + h2];
-        const uint64_t x = t16[0];
         if (tid < NN) {
+            uint64_t x = 0;
+            #pragma unroll
+            for (int q = 0; q < 8; ++q) x ^= nib[(c >> (4 * q)) & 15u][tid + 4 * q];
             const uint64_t* r = R[cur];
             uint64_t v;
             if (tid < NN - 32) {
@@ -341,6 +347,11 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     const int64_t steps = int64_t(1) << log2S, J = int64_t(MM) << log2S;
     int groups = 0;
     const uint32_t* polys = device_polys(c, log2S, groups);
+    static bool attr = false;
+    if (!attr) {
+        FB_CUDA(cudaFuncSetAttribute(k_jump_level, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNibBytes)));
+        attr = true;
+    }
     uint64_t s0[NN];
     mt64_seed_state(seed, s0);
     int64_t K = (2 * P + J - 1) / J;
@@ -355,8 +366,8 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         for (int a = 0; (int64_t(1) << a) < K; ++a) {
             const int64_t first = int64_t(1) << a;
             const int64_t n = std::min<int64_t>(first, K - first);
-            k_jump_level<<<unsigned(n), 320, 0, s>>>(states.get(), polys + size_t(a) * groups, groups,
-                                                     first, K);
+            k_jump_level<<<unsigned(n), 320, kNibBytes, s>>>(states.get(), polys + size_t(a) * groups,
+                                                             groups, first, K);
             FB_LAUNCH_CHECK();
         }
     }
@@ -371,7 +382,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
             for (int a = 0; (int64_t(1) << a) < Kmax; ++a) {
                 const int64_t first = int64_t(1) << a;
                 if (first + std::min<int64_t>(first, Kmax - first) <= K) continue;
-                k_jump_level<<<unsigned(std::min<int64_t>(first, Kmax - first)), 320, 0, s>>>(
+                k_jump_level<<<unsigned(std::min<int64_t>(first, Kmax - first)), 320, kNibBytes, s>>>(
                     states.get(), polys + size_t(a) * groups, groups, first, Kmax);
                 FB_LAUNCH_CHECK();
             }
