@@ -191,6 +191,55 @@ void build_items(Ctx& c, DCsr& A) {
     FB_LAUNCH_CHECK();
 }
 
+__global__ void k_col_counts(const int64_t* __restrict__ trp, int64_t n, int32_t* __restrict__ cnt,
+                             int32_t* __restrict__ ids) {
+    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n;
+         c += int64_t(gridDim.x) * blockDim.x) {
+        cnt[c] = int32_t(trp[c + 1] - trp[c]);
+        ids[c] = int32_t(c);
+    }
+}
+
+__global__ void k_rank_map(const int32_t* __restrict__ hot, int nhot, int32_t* __restrict__ rank_of) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nhot; r += gridDim.x * blockDim.x)
+        rank_of[hot[r]] = r;
+}
+
+__global__ void k_encode_hot(int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ rank_of) {
+    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < nnz;
+         p += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t r = rank_of[col[p]];
+        if (r >= 0) col[p] = -(r + 1);
+    }
+}
+
+// Rank the columns of A by popularity (nnz, ties to the lower id) and encode
+// the top kHot in A's column ids, for the shared-memory staging of A*X.
+void build_hot(Ctx& c, DCsr& A, const DCsr& T) {
+    const int64_t n = A.cols;
+    A.nhot = 0;
+    if (n == 0 || A.nnz == 0) return;
+    cudaStream_t s = c.stream;
+    DBuf<int32_t> cnt(size_t(n), s), ids(size_t(n), s), cnt_s(size_t(n), s), ids_s(size_t(n), s);
+    k_col_counts<<<grid_for(c, n), 256, 0, s>>>(T.rowptr.get(), n, cnt.get(), ids.get());
+    FB_LAUNCH_CHECK();
+    size_t tb = 0;
+    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.get(), cnt_s.get(), ids.get(),
+                                                      ids_s.get(), n, 0, 32, s));
+    DBuf<unsigned char> tmp(tb, s);
+    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), tb, cnt.get(), cnt_s.get(), ids.get(),
+                                                      ids_s.get(), n, 0, 32, s));
+    A.nhot = std::min<int64_t>(kHot, n);
+    A.hot_cols.alloc(size_t(A.nhot), s);
+    FB_CUDA(cudaMemcpyAsync(A.hot_cols.get(), ids_s.get(), sizeof(int32_t) * A.nhot, cudaMemcpyDeviceToDevice, s));
+    DBuf<int32_t> rank_of(size_t(n), s);
+    FB_CUDA(cudaMemsetAsync(rank_of.get(), 0xff, rank_of.bytes(), s));
+    k_rank_map<<<grid_for(c, A.nhot), 256, 0, s>>>(A.hot_cols.get(), int(A.nhot), rank_of.get());
+    FB_LAUNCH_CHECK();
+    k_encode_hot<<<grid_for(c, A.nnz), 256, 0, s>>>(A.col.get(), A.nnz, rank_of.get());
+    FB_LAUNCH_CHECK();
+}
+
 const char* kValidateMsg[3] = {
     "csr: row_ptr must be non-decreasing",
     "csr: column index out of range",
@@ -294,6 +343,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         FB_CUDA(cudaMemsetAsync(T.rowptr.get(), 0, T.rowptr.bytes(), s));
     }
     rowid.release();
+    build_hot(c, A, T);
     build_items(c, A);
     build_items(c, T);
     FB_CUDA(cudaStreamSynchronize(s));

@@ -39,7 +39,12 @@ struct DCsr {
     DBuf<WorkItem> items;
     DBuf<Combine> combine;
     int64_t nitems = 0, ncombine = 0, nslots = 0, chunk = 0;
+    // Hot columns (A only): the kHot most popular columns, by nnz, are encoded
+    // in `col` as -(rank+1); hot_cols[rank] is the original column id.
+    DBuf<int32_t> hot_cols;
+    int64_t nhot = 0;
 };
+constexpr int kHot = 4096;
 
 struct ProfAgg {
     int64_t launches = 0;

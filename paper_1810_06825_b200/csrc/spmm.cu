@@ -40,11 +40,42 @@ struct Vec<1> {
     __device__ static T zero() { return 0.0; }
 };
 
-template <int VEC, int NCH>
+// Hot-column staging (A * X only): the most popular columns of A are encoded
+// as -(rank+1); ranks below H are served from the CTA's shared copy Xs of
+// those X rows, higher ranks are decoded through hot_cols and gathered from
+// global memory like any other column.
+struct Hot {
+    const double* Xs;        // H x ncols in shared memory (nullptr when H == 0)
+    int H;
+    const int32_t* cols;     // rank -> original column id
+};
+
+template <int VEC, int NCH, bool HOT>
+__device__ __forceinline__ void gather(typename Vec<VEC>::T (&x)[NCH], int c, const double* __restrict__ Xl,
+                                       int64_t ldx, const bool (&ok)[NCH], int lane, int ncols,
+                                       const Hot& hot) {
+    using V = Vec<VEC>;
+    if (HOT && c < 0) {
+        const int slot = -c - 1;
+        if (slot < hot.H) {
+            const double* src = hot.Xs + size_t(slot) * ncols + lane * VEC;
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                x[ch] = ok[ch] ? *reinterpret_cast<const typename V::T*>(src + ch * 32 * VEC) : V::zero();
+            return;
+        }
+        c = __ldg(hot.cols + slot);
+    }
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+        x[ch] = ok[ch] ? V::load(Xl + int64_t(c) * ldx + ch * 32 * VEC) : V::zero();
+}
+
+template <int VEC, int NCH, bool HOT>
 __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
                                                const double* __restrict__ val, int64_t p0, int64_t p1,
                                                const double* __restrict__ X, int64_t ldx,
-                                               int lane, int ncols,
+                                               int lane, int ncols, const Hot& hot,
                                                typename Vec<VEC>::T (&acc)[NCH]) {
     using V = Vec<VEC>;
     using T = typename V::T;
@@ -71,10 +102,7 @@ __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
             }
             T x[4][NCH];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int ch = 0; ch < NCH; ++ch)
-                    x[u][ch] = ok[ch] ? V::load(Xl + int64_t(c[u]) * ldx + ch * 32 * VEC) : V::zero();
+            for (int u = 0; u < 4; ++u) gather<VEC, NCH, HOT>(x[u], c[u], Xl, ldx, ok, lane, ncols, hot);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -83,24 +111,26 @@ __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
         for (; j < cnt; ++j) {
             const int c0 = __shfl_sync(0xffffffffu, myc, j);
             const double v0 = __shfl_sync(0xffffffffu, myv, j);
+            T x[NCH];
+            gather<VEC, NCH, HOT>(x, c0, Xl, ldx, ok, lane, ncols, hot);
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch)
-                if (ok[ch]) V::fma(acc[ch], v0, V::load(Xl + int64_t(c0) * ldx + ch * 32 * VEC));
+                if (ok[ch]) V::fma(acc[ch], v0, x[ch]);
         }
     }
 }
 
-template <int VEC, int NCH>
-__global__ void __launch_bounds__(kThreads, 4)
-k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-       const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
-       const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
-       double* __restrict__ part, int ncols) {
+template <int VEC, int NCH, bool HOT>
+__device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                           const double* __restrict__ val, const WorkItem* __restrict__ items,
+                                           int64_t nitems, const double* __restrict__ X, int64_t ldx,
+                                           double* __restrict__ Y, int64_t ldy, double* __restrict__ part,
+                                           int ncols, const Hot& hot) {
     using V = Vec<VEC>;
     using T = typename V::T;
     const int lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * kThreads) >> 5;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t it = warp; it < nitems; it += nwarps) {
         const WorkItem w = items[it];
         if (w.r1 >= 0) {
@@ -108,7 +138,7 @@ k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                 T acc[NCH];
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
-                row_accumulate<VEC, NCH>(col, val, rowptr[r], rowptr[r + 1], X, ldx, lane, ncols, acc);
+                row_accumulate<VEC, NCH, HOT>(col, val, rowptr[r], rowptr[r + 1], X, ldx, lane, ncols, hot, acc);
                 double* yr = Y + int64_t(r) * ldy + lane * VEC;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch)
@@ -118,7 +148,7 @@ k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
             T acc[NCH];
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
-            row_accumulate<VEC, NCH>(col, val, w.p0, w.p1, X, ldx, lane, ncols, acc);
+            row_accumulate<VEC, NCH, HOT>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc);
             const int64_t slot = -int64_t(w.r1) - 1;
             double* pr = part + slot * ncols + lane * VEC;
 #pragma unroll
@@ -126,6 +156,39 @@ k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                 if ((ch * 32 + lane) * VEC < ncols) V::store(pr + ch * 32 * VEC, acc[ch]);
         }
     }
+}
+
+// Plain kernel (A^T * Y, and A * X when no column is hot enough to stage).
+// HOT = true here only decodes hot ids through the rank table (H = 0).
+template <int VEC, int NCH, bool HOT>
+__global__ void __launch_bounds__(kThreads, 4)
+k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+       const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
+       const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
+       double* __restrict__ part, int ncols, const int32_t* __restrict__ hot_cols) {
+    const Hot hot{nullptr, 0, HOT ? hot_cols : nullptr};
+    spmm_items<VEC, NCH, HOT>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot);
+}
+
+// A * X with the H most popular columns' X rows staged in shared memory: one
+// 768-thread CTA per SM (24 resident warps, 85 registers per thread).
+constexpr int kHotThreads = 768;
+template <int NCH>
+__global__ void __launch_bounds__(kHotThreads, 1)
+k_spmm_hot(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+           const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
+           const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
+           double* __restrict__ part, int ncols, const int32_t* __restrict__ hot_cols, int H) {
+    extern __shared__ __align__(16) double Xs[];
+    const int half = ncols / 2;
+    for (int e = threadIdx.x; e < H * half; e += blockDim.x) {
+        const int r = e / half, c2 = e % half;
+        reinterpret_cast<double2*>(Xs)[e] =
+            __ldg(reinterpret_cast<const double2*>(X + int64_t(hot_cols[r]) * ldx) + c2);
+    }
+    __syncthreads();
+    const Hot hot{Xs, H, hot_cols};
+    spmm_items<2, NCH, true>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot);
 }
 
 // Long rows: Y[row] = sum of its chunk partials in a fixed order. One CTA per
@@ -165,23 +228,49 @@ k_combine(const Combine* __restrict__ comb, const double* __restrict__ part, int
     }
 }
 
-template <int VEC, int NCH>
-void launch(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
-            double* part, int ncols) {
+template <int VEC, int NCH, bool HOT>
+void launch_plain(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                  double* part, int ncols) {
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
-        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<VEC, NCH>,
+        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<VEC, NCH, HOT>,
                                                               kThreads, 0));
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    const int64_t warps_needed = A.nitems;
-    int grid = int(std::min<int64_t>(int64_t(c.num_sms) * blocks_per_sm,
-                                     (warps_needed + 7) / 8));
+    int grid = int(std::min<int64_t>(int64_t(c.num_sms) * blocks_per_sm, (A.nitems + 7) / 8));
     grid = std::max(grid, 1);
-    k_spmm<VEC, NCH><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
-                                                      A.items.get(), A.nitems, X, ldx, Y, ldy,
-                                                      part, ncols);
+    k_spmm<VEC, NCH, HOT><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
+                                                           A.items.get(), A.nitems, X, ldx, Y, ldy, part,
+                                                           ncols, A.hot_cols.get());
     FB_LAUNCH_CHECK();
+}
+
+constexpr size_t kHotSmem = 200 * 1024;
+
+template <int NCH>
+void launch_hot(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                double* part, int ncols) {
+    const int H = int(std::min<int64_t>(A.nhot, int64_t(kHotSmem / (sizeof(double) * ncols))));
+    static bool attr = false;
+    if (!attr) {
+        FB_CUDA(cudaFuncSetAttribute(k_spmm_hot<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kHotSmem)));
+        attr = true;
+    }
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, (A.nitems + 31) / 32)));
+    k_spmm_hot<NCH><<<grid, kHotThreads, sizeof(double) * size_t(H) * ncols, c.stream>>>(
+        A.rowptr.get(), A.col.get(), A.val.get(), A.items.get(), A.nitems, X, ldx, Y, ldy, part, ncols,
+        A.hot_cols.get(), H);
+    FB_LAUNCH_CHECK();
+}
+
+template <int VEC, int NCH>
+void launch(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
+            double* part, int ncols) {
+    if (A.nhot == 0) return launch_plain<VEC, NCH, false>(c, A, X, ldx, Y, ldy, part, ncols);
+    if (VEC == 2 && ncols % 2 == 0 && A.nitems >= 32 * c.num_sms)
+        return launch_hot<NCH>(c, A, X, ldx, Y, ldy, part, ncols);
+    launch_plain<VEC, NCH, true>(c, A, X, ldx, Y, ldy, part, ncols);
 }
 
 }  // namespace
