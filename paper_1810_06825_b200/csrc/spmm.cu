@@ -55,16 +55,21 @@ __device__ __forceinline__ void gather(typename Vec<VEC>::T (&x)[NCH], int c, co
                                        int64_t ldx, const bool (&ok)[NCH], int lane, int ncols,
                                        const Hot& hot) {
     using V = Vec<VEC>;
-    if (HOT && c < 0) {
-        const int slot = -c - 1;
-        if (slot < hot.H) {
-            const double* src = hot.Xs + size_t(slot) * ncols + lane * VEC;
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch)
-                x[ch] = ok[ch] ? *reinterpret_cast<const typename V::T*>(src + ch * 32 * VEC) : V::zero();
-            return;
+    using T = typename V::T;
+    if (HOT) {
+        // one generic pointer for both sources: shared copy or global row
+        const double* src;
+        if (c < 0) {
+            const int slot = -c - 1;
+            src = slot < hot.H ? hot.Xs + size_t(slot) * ncols + lane * VEC
+                               : Xl + int64_t(__ldg(hot.cols + slot)) * ldx;
+        } else {
+            src = Xl + int64_t(c) * ldx;
         }
-        c = __ldg(hot.cols + slot);
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+            x[ch] = ok[ch] ? *reinterpret_cast<const T*>(src + ch * 32 * VEC) : V::zero();
+        return;
     }
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch)
@@ -171,8 +176,9 @@ k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
 }
 
 // A * X with the H most popular columns' X rows staged in shared memory: one
-// 768-thread CTA per SM (24 resident warps, 85 registers per thread).
-constexpr int kHotThreads = 768;
+// 512-thread CTA per SM (16 resident warps; 128 registers keep the four
+// in-flight nonzeros of every warp unspilled).
+constexpr int kHotThreads = 512;
 template <int NCH>
 __global__ void __launch_bounds__(kHotThreads, 1)
 k_spmm_hot(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
