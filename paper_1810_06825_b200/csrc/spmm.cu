@@ -11,6 +11,8 @@
 // per chunk, then the chunk partials are added in chunk order).
 // Column ids / values are streamed once (evict-first); X rows go through L1/L2
 // (read-only path) since power-law columns are re-gathered many times.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace fb {
@@ -274,7 +276,11 @@ template <int VEC, int NCH>
 void launch(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
             double* part, int ncols) {
     if (A.nhot == 0) return launch_plain<VEC, NCH, false>(c, A, X, ldx, Y, ldy, part, ncols);
-    if (VEC == 2 && ncols % 2 == 0 && A.nitems >= 32 * c.num_sms)
+    static const bool use_hot = [] {
+        const char* e = std::getenv("FRPCA_HOT_STAGING");
+        return e && e[0] == '1';
+    }();
+    if (use_hot && VEC == 2 && ncols % 2 == 0 && A.nitems >= 32 * c.num_sms)
         return launch_hot<NCH>(c, A, X, ldx, Y, ldy, part, ncols);
     launch_plain<VEC, NCH, true>(c, A, X, ldx, Y, ldy, part, ncols);
 }
