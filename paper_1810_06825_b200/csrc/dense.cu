@@ -359,6 +359,114 @@ k_gemm(const double* __restrict__ W, int64_t r, int K, const double* __restrict_
 }
 
 // ---------------------------------------------------------------------------
+// Tall-skinny GEMM with the full output width per CTA (N <= 256): C (r x N) =
+// W (r x K) * M (K x N). Each warp owns 2 row tiles x NT column tiles of 8x8
+// (per k4 step: 2 + NT fragment loads for 2*NT DMMAs), so the only padding is
+// N up to a multiple of 8 (no 64-wide tile waste). Warps: 8 per CTA, WC
+// column groups; the CTA covers 16 * 8 / WC rows. K is staged 16 at a time
+// (2-stage cp.async) into rows of stride 20 (W) and NP + pad (M), both
+// = 4 or 12 mod 16 doubles: conflict-free fragment loads.
+constexpr int TK = 16;
+constexpr int TSA = TK + 4;
+
+template <int NT>
+__global__ void __launch_bounds__(256, (NT <= 8 ? 2 : 1))
+k_gemm_tall(const double* __restrict__ W, int64_t r, int K, const double* __restrict__ M, int N,
+            double* __restrict__ C, int64_t ldc, int col_major, int WC, int SB) {
+    extern __shared__ __align__(16) double sm[];
+    const int BM = 16 * (8 / WC);
+    const int ntiles = (N + 7) / 8;
+    const int NP = 8 * ntiles;
+    double* Ws = sm;                                  // [2][BM][TSA]
+    double* Ms = sm + 2 * BM * TSA;                   // [2][TK][SB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rg = warp / WC, cgp = warp % WC;
+    const int64_t r0 = int64_t(blockIdx.x) * BM;
+    double acc[2][NT][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[a][t][0] = acc[a][t][1] = 0.0;
+
+    auto load = [&](int stage, int k0) {
+        double* wd = Ws + stage * BM * TSA;
+        for (int e = tid; e < BM * TK; e += 256) {
+            const int rr = e / TK, kk = e % TK;
+            const int64_t row = r0 + rr;
+            const int k = k0 + kk;
+            const bool v = row < r && k < K;
+            cp_async8(wd + rr * TSA + kk, W + (v ? row * K + k : 0), v);
+        }
+        double* md = Ms + stage * TK * SB;
+        for (int e = tid; e < TK * NP; e += 256) {
+            const int kk = e / NP, cc = e % NP;
+            const int k = k0 + kk;
+            const bool v = k < K && cc < N;
+            cp_async8(md + kk * SB + cc, M + (v ? int64_t(k) * N + cc : 0), v);
+        }
+        cp_async_commit();
+    };
+    const int nsteps = (K + TK - 1) / TK;
+    load(0, 0);
+    for (int st = 0; st < nsteps; ++st) {
+        const int stage = st & 1;
+        if (st + 1 < nsteps) {
+            load(stage ^ 1, (st + 1) * TK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* wd = Ws + stage * BM * TSA + (rg * 16 + (lane >> 2)) * TSA + (lane & 3);
+        const double* md = Ms + stage * TK * SB + (lane & 3) * SB + cgp * NT * 8 + (lane >> 2);
+#pragma unroll
+        for (int kk = 0; kk < TK / 4; ++kk) {
+            const double a0 = wd[kk * 4], a1 = wd[8 * TSA + kk * 4];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                if (cgp * NT + t < ntiles) {
+                    const double b = md[kk * 4 * SB + t * 8];
+                    dmma(acc[0][t], a0, b);
+                    dmma(acc[1][t], a1, b);
+                }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int64_t row = r0 + rg * 16 + a * 8 + (lane >> 2);
+            const int col = (cgp * NT + t) * 8 + (lane & 3) * 2;
+            if (row >= r || cgp * NT + t >= ntiles) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (col + h >= N) continue;
+                if (col_major) C[int64_t(col + h) * ldc + row] = acc[a][t][h];
+                else C[row * ldc + col + h] = acc[a][t][h];
+            }
+        }
+}
+
+template <int NT>
+void launch_gemm_tall(Ctx& c, const double* W, int64_t r, int64_t K, const double* M, int64_t N,
+                      double* C, int64_t ldc, bool col_major_out, int WC) {
+    const int ntiles = int((N + 7) / 8), NP = 8 * ntiles;
+    const int SB = NP + ((12 - (NP % 16)) + 16) % 16;
+    const int BM = 16 * (8 / WC);
+    const size_t smem = sizeof(double) * (2 * size_t(BM) * TSA + 2 * size_t(TK) * SB);
+    static bool attr = false;
+    if (!attr) {
+        FB_CUDA(cudaFuncSetAttribute(k_gemm_tall<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+        attr = true;
+    }
+    k_gemm_tall<NT><<<unsigned((r + BM - 1) / BM), 256, smem, c.stream>>>(W, r, int(K), M, int(N), C, ldc,
+                                                                       col_major_out ? 1 : 0, WC, SB);
+    FB_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
 __global__ void k_transpose(const double* __restrict__ in, int64_t rows, int64_t cols,
                             double* __restrict__ out) {
     __shared__ double tile[32][33];
@@ -415,6 +523,16 @@ void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M,
                  double* C, int64_t ldc, bool col_major_out) {
     if (r == 0 || N == 0) return;
     Prof prof(c, "rescale_gemm", 8.0 * r * (K + N), 2.0 * r * K * N);
+    if (N <= 256) {
+        const int ntiles = int((N + 7) / 8);
+        const int WC = ntiles > 16 ? 2 : 1;
+        const int nt = (ntiles + WC - 1) / WC;
+        if (nt <= 2) return launch_gemm_tall<2>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
+        if (nt <= 4) return launch_gemm_tall<4>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
+        if (nt <= 8) return launch_gemm_tall<8>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
+        if (nt <= 13) return launch_gemm_tall<13>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
+        return launch_gemm_tall<16>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
+    }
     dim3 grid(unsigned((r + MT - 1) / MT), unsigned((N + NT - 1) / NT));
     k_gemm<<<grid, 128, 0, c.stream>>>(W, r, int(K), M, int(N), C, ldc, col_major_out ? 1 : 0);
     FB_LAUNCH_CHECK();
