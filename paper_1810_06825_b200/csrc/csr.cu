@@ -4,6 +4,8 @@
 // load-balanced SpMM work lists of both.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace fb {
@@ -343,7 +345,13 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         FB_CUDA(cudaMemsetAsync(T.rowptr.get(), 0, T.rowptr.bytes(), s));
     }
     rowid.release();
-    build_hot(c, A, T);
+    // hot-column encoding only for the (experimental) shared-memory staging
+    // of A*X: the decode adds a dependent load per hot nonzero otherwise
+    static const bool hot = [] {
+        const char* e = std::getenv("FRPCA_HOT_STAGING");
+        return e && e[0] == '1';
+    }();
+    if (hot) build_hot(c, A, T);
     build_items(c, A);
     build_items(c, T);
     FB_CUDA(cudaStreamSynchronize(s));

@@ -370,7 +370,7 @@ constexpr int TK = 16;
 constexpr int TSA = TK + 4;
 
 template <int NT>
-__global__ void __launch_bounds__(256, (NT <= 8 ? 2 : 1))
+__global__ void __launch_bounds__(256, 2)
 k_gemm_tall(const double* __restrict__ W, int64_t r, int K, const double* __restrict__ M, int N,
             double* __restrict__ C, int64_t ldc, int col_major, int WC, int SB) {
     extern __shared__ __align__(16) double sm[];
@@ -524,14 +524,15 @@ void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M,
     if (r == 0 || N == 0) return;
     Prof prof(c, "rescale_gemm", 8.0 * r * (K + N), 2.0 * r * K * N);
     if (N <= 256) {
+        // column groups so that each warp holds at most 8 column tiles (64
+        // accumulator registers): 2-3 CTAs per SM, 16-24 warps
         const int ntiles = int((N + 7) / 8);
-        const int WC = ntiles > 16 ? 2 : 1;
+        const int WC = ntiles <= 8 ? 1 : (ntiles <= 16 ? 2 : 4);
         const int nt = (ntiles + WC - 1) / WC;
         if (nt <= 2) return launch_gemm_tall<2>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
         if (nt <= 4) return launch_gemm_tall<4>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
-        if (nt <= 8) return launch_gemm_tall<8>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
-        if (nt <= 13) return launch_gemm_tall<13>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
-        return launch_gemm_tall<16>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
+        if (nt <= 7) return launch_gemm_tall<7>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
+        return launch_gemm_tall<8>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
     }
     dim3 grid(unsigned((r + MT - 1) / MT), unsigned((N + NT - 1) / NT));
     k_gemm<<<grid, 128, 0, c.stream>>>(W, r, int(K), M, int(N), C, ldc, col_major_out ? 1 : 0);
