@@ -449,6 +449,112 @@ k_gemm_tall(const double* __restrict__ W, int64_t r, int K, const double* __rest
         }
 }
 
+// Persistent variant for tall W: the whole column chunk of M (K x NP, NP <= 104)
+// stays in shared memory for the CTA's lifetime and W is streamed through once
+// (M is read once per SM instead of once per 64-row block).
+constexpr int PCOLS = 104;
+template <int NT>
+__global__ void __launch_bounds__(256, 1)
+k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __restrict__ M, int ldm,
+               int N, double* __restrict__ C, int64_t ldc, int col_major, int WC, int SB) {
+    extern __shared__ __align__(16) double sm[];
+    const int BM = 16 * (8 / WC);
+    const int ntiles = (N + 7) / 8;
+    const int NP = 8 * ntiles;
+    double* Ms = sm;                                  // [K][SB]
+    double* Ws = sm + size_t(K) * SB;                 // [2][BM][TSA]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rg = warp / WC, cgp = warp % WC;
+    for (int e = tid; e < K * NP; e += 256) {
+        const int k = e / NP, cc = e % NP;
+        cp_async8(Ms + k * SB + cc, M + (cc < N ? int64_t(k) * ldm + cc : 0), cc < N);
+    }
+    cp_async_commit();
+    const int nsteps = (K + TK - 1) / TK;
+    auto load = [&](int stage, int64_t r0, int k0) {
+        double* wd = Ws + stage * BM * TSA;
+        for (int e = tid; e < BM * TK; e += 256) {
+            const int rr = e / TK, kk = e % TK;
+            const int64_t row = r0 + rr;
+            const int k = k0 + kk;
+            const bool v = row < r && k < K;
+            cp_async8(wd + rr * TSA + kk, W + (v ? row * K + k : 0), v);
+        }
+        cp_async_commit();
+    };
+    const int64_t nblocks = (r + BM - 1) / BM;
+    for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+        const int64_t r0 = blk * BM;
+        double acc[2][NT][2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int t = 0; t < NT; ++t) acc[a][t][0] = acc[a][t][1] = 0.0;
+        load(0, r0, 0);
+        for (int st = 0; st < nsteps; ++st) {
+            const int stage = st & 1;
+            if (st + 1 < nsteps) {
+                load(stage ^ 1, r0, (st + 1) * TK);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            const double* wd = Ws + stage * BM * TSA + (rg * 16 + (lane >> 2)) * TSA + (lane & 3);
+            const double* md = Ms + (st * TK + (lane & 3)) * SB + cgp * NT * 8 + (lane >> 2);
+#pragma unroll
+            for (int kk = 0; kk < TK / 4; ++kk) {
+                if (st * TK + kk * 4 >= K) break;
+                const double a0 = wd[kk * 4], a1 = wd[8 * TSA + kk * 4];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    if (cgp * NT + t < ntiles) {
+                        const double b = md[kk * 4 * SB + t * 8];
+                        dmma(acc[0][t], a0, b);
+                        dmma(acc[1][t], a1, b);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int64_t row = r0 + rg * 16 + a * 8 + (lane >> 2);
+                const int col = (cgp * NT + t) * 8 + (lane & 3) * 2;
+                if (row >= r || cgp * NT + t >= ntiles) continue;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (col + h >= N) continue;
+                    if (col_major) C[int64_t(col + h) * ldc + row] = acc[a][t][h];
+                    else C[row * ldc + col + h] = acc[a][t][h];
+                }
+            }
+    }
+}
+
+template <int NT>
+void launch_gemm_persist(Ctx& c, const double* W, int64_t r, int64_t K, const double* M, int64_t ldm,
+                         int64_t N, double* C, int64_t ldc, bool col_major_out, int WC) {
+    const int ntiles = int((N + 7) / 8), NP = 8 * ntiles;
+    const int SB = NP + ((12 - (NP % 16)) + 16) % 16;
+    const int BM = 16 * (8 / WC);
+    const int Kp = int((K + TK - 1) / TK) * TK;
+    const size_t smem = sizeof(double) * (size_t(Kp) * SB + 2 * size_t(BM) * TSA);
+    static bool attr = false;
+    if (!attr) {
+        FB_CUDA(cudaFuncSetAttribute(k_gemm_persist<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        attr = true;
+    }
+    const int64_t nblocks = (r + BM - 1) / BM;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, nblocks)));
+    k_gemm_persist<NT><<<grid, 256, smem, c.stream>>>(W, r, int(K), M, int(ldm), int(N), C, ldc,
+                                                     col_major_out ? 1 : 0, WC, SB);
+    FB_LAUNCH_CHECK();
+}
+
 template <int NT>
 void launch_gemm_tall(Ctx& c, const double* W, int64_t r, int64_t K, const double* M, int64_t N,
                       double* C, int64_t ldc, bool col_major_out, int WC) {
@@ -523,16 +629,20 @@ void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M,
                  double* C, int64_t ldc, bool col_major_out) {
     if (r == 0 || N == 0) return;
     Prof prof(c, "rescale_gemm", 8.0 * r * (K + N), 2.0 * r * K * N);
-    if (N <= 256) {
-        // column groups so that each warp holds at most 8 column tiles (64
-        // accumulator registers): 2-3 CTAs per SM, 16-24 warps
-        const int ntiles = int((N + 7) / 8);
-        const int WC = ntiles <= 8 ? 1 : (ntiles <= 16 ? 2 : 4);
-        const int nt = (ntiles + WC - 1) / WC;
-        if (nt <= 2) return launch_gemm_tall<2>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
-        if (nt <= 4) return launch_gemm_tall<4>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
-        if (nt <= 7) return launch_gemm_tall<7>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
-        return launch_gemm_tall<8>(c, W, r, K, M, N, C, ldc, col_major_out, WC);
+    // persistent kernel with M resident in shared memory, in column chunks of
+    // <= 104 (K <= 208 keeps a chunk of M within 227 KB)
+    if (K <= 208 && r >= 4096) {
+        for (int64_t c0 = 0; c0 < N; c0 += PCOLS) {
+            const int64_t nc = std::min<int64_t>(PCOLS, N - c0);
+            double* Cc = col_major_out ? C + c0 * ldc : C + c0;
+            const int ntiles = int((nc + 7) / 8);
+            const int WC = ntiles <= 8 ? 1 : 2;
+            const int nt = (ntiles + WC - 1) / WC;
+            if (nt <= 2) launch_gemm_persist<2>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+            else if (nt <= 4) launch_gemm_persist<4>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+            else launch_gemm_persist<7>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+        }
+        return;
     }
     dim3 grid(unsigned((r + MT - 1) / MT), unsigned((N + NT - 1) / NT));
     k_gemm<<<grid, 128, 0, c.stream>>>(W, r, int(K), M, int(N), C, ldc, col_major_out ? 1 : 0);

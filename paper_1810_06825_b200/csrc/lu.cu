@@ -66,7 +66,7 @@ __device__ Cand block_best(Cand c, Cand* sh) {
     return r;
 }
 
-__global__ void __launch_bounds__(kT, 2)
+__global__ void __launch_bounds__(kT, 1)
 k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ P,
      int32_t* __restrict__ pos, Cand* __restrict__ cand, int* __restrict__ err) {
     extern __shared__ double smem[];
@@ -114,7 +114,13 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
             const double d = u[jj];
             Cand nc{-1.0, INT32_MAX, -1};
             for (int64_t i = gtid; i < m; i += nthr) {
+                // all loads of the row first (position + remaining panel
+                // entries are independent), so a row costs one round trip
                 int32_t p = pos[i];
+                double v[NB];
+#pragma unroll
+                for (int t = 0; t < NB; ++t)
+                    if (t >= jj && t < bw) v[t] = P[int64_t(t) * m + i];
                 if (i == pr) {
                     pos[i] = j;
                     continue;
@@ -124,23 +130,20 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
                     pos[i] = p;
                 }
                 if (p > j) {
-                    const double mi = P[int64_t(jj) * m + i] / d;   // :88
-                    P[int64_t(jj) * m + i] = mi;
-                    double nv = 0.0;
-                    // :89-92, 8 columns at a time: independent loads, then updates
-                    for (int t0 = jj + 1; t0 < bw; t0 += 8) {
-                        double a[8];
+                    double mi = 0.0, nv = 0.0;
 #pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            if (t0 + e < bw) a[e] = P[int64_t(t0 + e) * m + i];
+                    for (int t = 0; t < NB; ++t)
+                        if (t == jj) {
+                            mi = v[t] / d;                             // :88
+                            P[int64_t(t) * m + i] = mi;
+                        }
 #pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            if (t0 + e < bw) {
-                                a[e] = a[e] - mi * u[t0 + e];
-                                P[int64_t(t0 + e) * m + i] = a[e];
-                            }
-                        if (t0 == jj + 1) nv = a[0];
-                    }
+                    for (int t = 0; t < NB; ++t)                      // :89-92
+                        if (t > jj && t < bw) {
+                            v[t] = v[t] - mi * u[t];
+                            P[int64_t(t) * m + i] = v[t];
+                            if (t == jj + 1) nv = v[t];
+                        }
                     if (jj + 1 < bw) cand_merge(nc, Cand{fabs(nv), p, int32_t(i)});
                 }
             }
