@@ -187,10 +187,23 @@ k_gram2(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
     };
     const int64_t nsteps = (re - rs + G2_ROWS - 1) / G2_ROWS;
     if (nsteps > 0) load(0, rs);
-    // (ti, tj) of this warp's first tile
-    int ti0 = 0;
-    while ((ti0 + 1) * (ti0 + 2) / 2 <= t0) ++ti0;
-    const int tj0 = t0 - ti0 * (ti0 + 1) / 2;
+    // this warp's tiles: fragment offsets of A (row tile) and B (column tile),
+    // and where the A fragment changes
+    const int nmine = t1 - t0;
+    __shared__ int offs[G2_WARPS][MAXT];  // (A offset << 16) | B offset, in doubles
+    int* off = offs[warp];
+    unsigned areload = 0;
+    {
+        int ti = 0;
+        while ((ti + 1) * (ti + 2) / 2 <= t0) ++ti;
+        int tj = t0 - ti * (ti + 1) / 2;
+#pragma unroll
+        for (int i = 0; i < MAXT; ++i) {
+            if (lane == 0) off[i] = (ti * 8) << 16 | (tj * 8);
+            if (i == 0 || tj == 0) areload |= 1u << i;
+            if (++tj > ti) { ++ti; tj = 0; }
+        }
+    }
     for (int64_t st = 0; st < nsteps; ++st) {
         const int stage = int(st & 1);
         if (st + 1 < nsteps) {
@@ -204,18 +217,12 @@ k_gram2(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
 #pragma unroll
         for (int kk = 0; kk < G2_ROWS / 4; ++kk) {
             const double* rowp = Ws + (kk * 4 + (lane & 3)) * S + (lane >> 2);
-            int ti = ti0, tj = tj0;
-            double a = rowp[ti * 8];
+            double a = 0.0;
 #pragma unroll
             for (int i = 0; i < MAXT; ++i) {
-                if (t0 + i < t1) {
-                    const double b = rowp[tj * 8];
-                    dmma(acc[i], a, b);
-                    if (++tj > ti) {
-                        ++ti;
-                        tj = 0;
-                        a = rowp[min(ti, T - 1) * 8];
-                    }
+                if (i < nmine) {
+                    if (areload & (1u << i)) a = rowp[off[i] >> 16];
+                    dmma(acc[i], a, rowp[off[i] & 0xffff]);
                 }
             }
         }
@@ -453,19 +460,20 @@ k_gemm_tall(const double* __restrict__ W, int64_t r, int K, const double* __rest
 // stays in shared memory for the CTA's lifetime and W is streamed through once
 // (M is read once per SM instead of once per 64-row block).
 constexpr int PCOLS = 104;
+constexpr int GP_THREADS = 512;
 template <int NT>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(GP_THREADS, 1)
 k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __restrict__ M, int ldm,
                int N, double* __restrict__ C, int64_t ldc, int col_major, int WC, int SB) {
     extern __shared__ __align__(16) double sm[];
-    const int BM = 16 * (8 / WC);
+    const int BM = 16 * ((GP_THREADS / 32) / WC);
     const int ntiles = (N + 7) / 8;
     const int NP = 8 * ntiles;
     double* Ms = sm;                                  // [K][SB]
     double* Ws = sm + size_t(K) * SB;                 // [2][BM][TSA]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rg = warp / WC, cgp = warp % WC;
-    for (int e = tid; e < K * NP; e += 256) {
+    for (int e = tid; e < K * NP; e += GP_THREADS) {
         const int k = e / NP, cc = e % NP;
         cp_async8(Ms + k * SB + cc, M + (cc < N ? int64_t(k) * ldm + cc : 0), cc < N);
     }
@@ -473,7 +481,7 @@ k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __r
     const int nsteps = (K + TK - 1) / TK;
     auto load = [&](int stage, int64_t r0, int k0) {
         double* wd = Ws + stage * BM * TSA;
-        for (int e = tid; e < BM * TK; e += 256) {
+        for (int e = tid; e < BM * TK; e += GP_THREADS) {
             const int rr = e / TK, kk = e % TK;
             const int64_t row = r0 + rr;
             const int k = k0 + kk;
@@ -539,7 +547,7 @@ void launch_gemm_persist(Ctx& c, const double* W, int64_t r, int64_t K, const do
                          int64_t N, double* C, int64_t ldc, bool col_major_out, int WC) {
     const int ntiles = int((N + 7) / 8), NP = 8 * ntiles;
     const int SB = NP + ((12 - (NP % 16)) + 16) % 16;
-    const int BM = 16 * (8 / WC);
+    const int BM = 16 * ((GP_THREADS / 32) / WC);
     const int Kp = int((K + TK - 1) / TK) * TK;
     const size_t smem = sizeof(double) * (size_t(Kp) * SB + 2 * size_t(BM) * TSA);
     static bool attr = false;
@@ -550,7 +558,7 @@ void launch_gemm_persist(Ctx& c, const double* W, int64_t r, int64_t K, const do
     }
     const int64_t nblocks = (r + BM - 1) / BM;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, nblocks)));
-    k_gemm_persist<NT><<<grid, 256, smem, c.stream>>>(W, r, int(K), M, int(ldm), int(N), C, ldc,
+    k_gemm_persist<NT><<<grid, GP_THREADS, smem, c.stream>>>(W, r, int(K), M, int(ldm), int(N), C, ldc,
                                                      col_major_out ? 1 : 0, WC, SB);
     FB_LAUNCH_CHECK();
 }

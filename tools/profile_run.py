@@ -23,12 +23,17 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.config]
+    import time
+    t0 = time.time()
     m, n, rp, ci, va = synth.generate(cfg.name, scale=a.scale)
+    print(f"generated {cfg.name}: {m}x{n} nnz={int(rp[-1])} in {time.time() - t0:.1f}s", file=sys.stderr)
+    t0 = time.time()
     ctx = fb.Context(0)
     L = _lib.load()
     h = C.c_void_p()
     _lib.check(L.frpca_dmat_upload(ctx._h, m, n, int(rp[-1]), rp.ctypes.data, ci.ctypes.data,
                                    va.ctypes.data, C.byref(h)))
+    print(f"upload {time.time() - t0:.2f}s", file=sys.stderr)
     import torch
     k = cfg.k
     dU = torch.empty(m * k, dtype=torch.float64, device="cuda")
@@ -37,11 +42,13 @@ def main():
     c = fb.PcaConfig(k=cfg.k, oversample=cfg.s, passes=cfg.q, seed=0).to_c(device_io=True)
     algo = _lib.ALGO_FRPCA if cfg.algorithm == "frpca" else _lib.ALGO_FRPCAT
     for r in range(a.runs):
+        t0 = time.time()
         if r == a.runs - 1:
             ctx.profile(True)
             ctx.profile_reset()
         _lib.check(L.frpca_run(ctx._h, h, algo, C.byref(c), None, 0, 0, C.c_void_p(dU.data_ptr()),
                                C.c_void_p(dS.data_ptr()), C.c_void_p(dV.data_ptr()), None, None, None))
+        print(f"run {r}: {time.time() - t0:.3f}s", file=sys.stderr)
     rep = ctx.profile_report()
     print(json.dumps({"config": cfg.name, "scale": a.scale, "kernels": rep}, indent=1))
     L.frpca_dmat_destroy(h)
