@@ -92,27 +92,27 @@ __global__ void k_rowptr_from_sorted(const int32_t* __restrict__ keys, int64_t n
 // Short rows are grouped: row r starts a group unless its predecessor is a
 // short row in the same bin, bin(r) = (row_ptr[r] + r) / ch (weight of a row
 // = nnz + 1 for its output write), so a group carries <= ~ch of weight.
-__device__ __forceinline__ bool is_long(const int64_t* rp, int64_t r, int64_t ch) {
-    return rp[r + 1] - rp[r] > ch;
+__device__ __forceinline__ bool is_long(const int64_t* rp, int64_t r, int64_t ch, const uint8_t* skip) {
+    return !(skip && skip[r]) && rp[r + 1] - rp[r] > ch;
 }
-__device__ __forceinline__ bool is_start(const int64_t* rp, int64_t r, int64_t ch) {
-    if (is_long(rp, r, ch)) return false;
+__device__ __forceinline__ bool is_start(const int64_t* rp, int64_t r, int64_t ch, const uint8_t* skip) {
+    if (is_long(rp, r, ch, skip)) return false;
     if (r == 0) return true;
-    if (is_long(rp, r - 1, ch)) return true;
+    if (is_long(rp, r - 1, ch, skip)) return true;
     return (rp[r] + r) / ch != (rp[r - 1] + r - 1) / ch;
 }
 
 __global__ void k_item_counts(const int64_t* __restrict__ rp, int64_t m, int64_t ch,
                               int32_t* __restrict__ n_items, int32_t* __restrict__ n_slots,
-                              int32_t* __restrict__ n_comb) {
+                              int32_t* __restrict__ n_comb, const uint8_t* __restrict__ skip) {
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < m;
          r += int64_t(gridDim.x) * blockDim.x) {
         const int64_t nz = rp[r + 1] - rp[r];
-        if (nz > ch) {
+        if (is_long(rp, r, ch, skip)) {
             const int32_t k = int32_t((nz + ch - 1) / ch);
             n_items[r] = k; n_slots[r] = k; n_comb[r] = 1;
         } else {
-            n_items[r] = is_start(rp, r, ch) ? 1 : 0; n_slots[r] = 0; n_comb[r] = 0;
+            n_items[r] = is_start(rp, r, ch, skip) ? 1 : 0; n_slots[r] = 0; n_comb[r] = 0;
         }
     }
 }
@@ -120,11 +120,11 @@ __global__ void k_item_counts(const int64_t* __restrict__ rp, int64_t m, int64_t
 __global__ void k_item_write(const int64_t* __restrict__ rp, int64_t m, int64_t ch,
                              const int32_t* __restrict__ o_items, const int32_t* __restrict__ o_slots,
                              const int32_t* __restrict__ o_comb, WorkItem* __restrict__ items,
-                             Combine* __restrict__ comb) {
+                             Combine* __restrict__ comb, const uint8_t* __restrict__ skip) {
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < m;
          r += int64_t(gridDim.x) * blockDim.x) {
         const int64_t p0 = rp[r], nz = rp[r + 1] - p0;
-        if (nz > ch) {
+        if (is_long(rp, r, ch, skip)) {
             const int32_t k = int32_t((nz + ch - 1) / ch);
             const int32_t s0 = o_slots[r];
             for (int32_t t = 0; t < k; ++t) {
@@ -138,9 +138,9 @@ __global__ void k_item_write(const int64_t* __restrict__ rp, int64_t m, int64_t 
             Combine cb;
             cb.row = int32_t(r); cb.s0 = s0; cb.s1 = s0 + k; cb.pad = 0;
             comb[o_comb[r]] = cb;
-        } else if (is_start(rp, r, ch)) {
+        } else if (is_start(rp, r, ch, skip)) {
             int64_t e = r + 1;
-            while (e < m && !is_long(rp, e, ch) && !is_start(rp, e, ch)) ++e;
+            while (e < m && !is_long(rp, e, ch, skip) && !is_start(rp, e, ch, skip)) ++e;
             WorkItem w;
             w.p0 = 0; w.p1 = 0; w.r0 = int32_t(r); w.r1 = int32_t(e);
             items[o_items[r]] = w;
@@ -175,7 +175,7 @@ void build_items(Ctx& c, DCsr& A) {
     int32_t *ni = cnt.get(), *ns = ni + (m + 1), *nc = ns + (m + 1);
     int32_t *oi = off.get(), *os = oi + (m + 1), *oc = os + (m + 1);
     FB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), c.stream));
-    k_item_counts<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, ni, ns, nc);
+    k_item_counts<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, ni, ns, nc, A.skip.get());
     FB_LAUNCH_CHECK();
     size_t tb = 0;
     FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, ni, oi, m + 1, c.stream));
@@ -189,7 +189,7 @@ void build_items(Ctx& c, DCsr& A) {
     A.items.alloc(size_t(A.nitems), c.stream);
     A.combine.alloc(size_t(std::max<int64_t>(A.ncombine, 1)), c.stream);
     k_item_write<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, oi, os, oc,
-                                                        A.items.get(), A.combine.get());
+                                                        A.items.get(), A.combine.get(), A.skip.get());
     FB_LAUNCH_CHECK();
 }
 
@@ -239,6 +239,102 @@ void build_hot(Ctx& c, DCsr& A, const DCsr& T) {
     k_rank_map<<<grid_for(c, A.nhot), 256, 0, s>>>(A.hot_cols.get(), int(A.nhot), rank_of.get());
     FB_LAUNCH_CHECK();
     k_encode_hot<<<grid_for(c, A.nnz), 256, 0, s>>>(A.col.get(), A.nnz, rank_of.get());
+    FB_LAUNCH_CHECK();
+}
+
+__global__ void k_top_counts(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t m,
+                             const int32_t* __restrict__ rank_of, int64_t* __restrict__ cnt) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t k = 0;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) k += rank_of[col[p]] >= 0;
+        cnt[i] = k;
+    }
+}
+
+__global__ void k_top_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                           const double* __restrict__ val, int64_t m, const int32_t* __restrict__ rank_of,
+                           const int64_t* __restrict__ trp, uint8_t* __restrict__ rank, double* __restrict__ tv) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t o = trp[i];
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            const int32_t r = rank_of[col[p]];
+            if (r >= 0) { rank[o] = uint8_t(r); tv[o] = val[p]; ++o; }
+        }
+    }
+}
+
+__global__ void k_top_skip(const int32_t* __restrict__ top, int ntop, uint8_t* __restrict__ skip) {
+    for (int r = threadIdx.x; r < ntop; r += blockDim.x) skip[top[r]] = 1;
+}
+
+// cut k: first row i with (i + top_rp[i]) >= k * total / G (weight = row + entries)
+__global__ void k_top_cuts(const int64_t* __restrict__ trp, int64_t m, int G, int64_t* __restrict__ cuts) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > G) return;
+    const int64_t total = m + trp[m];
+    const int64_t target = (total * k) / G;
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (mid + trp[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    cuts[k] = (k == G) ? m : lo;
+}
+
+// Top-column streaming structures for A^T*Y (see spmm.cu k_aty_top): the kTop
+// most popular columns, if they hold >= 20% of the nonzeros.
+void build_top(Ctx& c, DMat& M) {
+    DCsr& A = M.A;
+    DCsr& T = M.At;
+    const int64_t n = A.cols, m = A.rows;
+    A.ntop = 0;
+    if (n < 2 * kTop || A.nnz == 0 || m == 0) return;
+    cudaStream_t s = c.stream;
+    DBuf<int32_t> cnt(size_t(n), s), ids(size_t(n), s), cnt_s(size_t(n), s), ids_s(size_t(n), s);
+    k_col_counts<<<grid_for(c, n), 256, 0, s>>>(T.rowptr.get(), n, cnt.get(), ids.get());
+    FB_LAUNCH_CHECK();
+    size_t tb = 0;
+    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.get(), cnt_s.get(), ids.get(),
+                                                      ids_s.get(), n, 0, 32, s));
+    DBuf<unsigned char> tmp(tb, s);
+    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), tb, cnt.get(), cnt_s.get(), ids.get(),
+                                                      ids_s.get(), n, 0, 32, s));
+    std::vector<int32_t> hc(kTop);
+    FB_CUDA(cudaMemcpyAsync(hc.data(), cnt_s.get(), sizeof(int32_t) * kTop, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaStreamSynchronize(s));
+    int64_t top_nnz = 0;
+    for (int32_t x : hc) top_nnz += x;
+    if (double(top_nnz) < 0.2 * double(A.nnz)) return;
+    A.ntop = kTop;
+    A.top_cols.alloc(kTop, s);
+    FB_CUDA(cudaMemcpyAsync(A.top_cols.get(), ids_s.get(), sizeof(int32_t) * kTop, cudaMemcpyDeviceToDevice, s));
+    DBuf<int32_t> rank_of(size_t(n), s);
+    FB_CUDA(cudaMemsetAsync(rank_of.get(), 0xff, rank_of.bytes(), s));
+    k_rank_map<<<1, 256, 0, s>>>(A.top_cols.get(), kTop, rank_of.get());
+    FB_LAUNCH_CHECK();
+    DBuf<int64_t> rc(size_t(m) + 1, s);
+    FB_CUDA(cudaMemsetAsync(rc.get(), 0, rc.bytes(), s));
+    k_top_counts<<<grid_for(c, m), 256, 0, s>>>(A.rowptr.get(), A.col.get(), m, rank_of.get(), rc.get());
+    FB_LAUNCH_CHECK();
+    A.top_rp.alloc(size_t(m) + 1, s);
+    tb = 0;
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, rc.get(), A.top_rp.get(), m + 1, s));
+    DBuf<unsigned char> tmp2(tb, s);
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp2.get(), tb, rc.get(), A.top_rp.get(), m + 1, s));
+    A.top_rank.alloc(size_t(top_nnz), s);
+    A.top_val.alloc(size_t(top_nnz), s);
+    k_top_fill<<<grid_for(c, m), 256, 0, s>>>(A.rowptr.get(), A.col.get(), A.val.get(), m, rank_of.get(),
+                                               A.top_rp.get(), A.top_rank.get(), A.top_val.get());
+    FB_LAUNCH_CHECK();
+    T.skip.alloc(size_t(n), s);
+    FB_CUDA(cudaMemsetAsync(T.skip.get(), 0, T.skip.bytes(), s));
+    k_top_skip<<<1, 256, 0, s>>>(A.top_cols.get(), kTop, T.skip.get());
+    FB_LAUNCH_CHECK();
+    A.ntop_cuts = c.num_sms;
+    A.top_cuts.alloc(size_t(c.num_sms) + 1, s);
+    k_top_cuts<<<(c.num_sms + 1 + 255) / 256, 256, 0, s>>>(A.top_rp.get(), m, c.num_sms, A.top_cuts.get());
     FB_LAUNCH_CHECK();
 }
 
@@ -352,6 +448,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         return e && e[0] == '1';
     }();
     if (hot) build_hot(c, A, T);
+    build_top(c, M);
     build_items(c, A);
     build_items(c, T);
     FB_CUDA(cudaStreamSynchronize(s));

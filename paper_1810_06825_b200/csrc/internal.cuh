@@ -43,7 +43,19 @@ struct DCsr {
     // in `col` as -(rank+1); hot_cols[rank] is the original column id.
     DBuf<int32_t> hot_cols;
     int64_t nhot = 0;
+    // A^T*Y top-column streaming (on A): the kTop most popular columns, their
+    // entries per row of A (rank, value) and row cuts for one CTA per SM.
+    int ntop = 0;
+    DBuf<int32_t> top_cols;
+    DBuf<int64_t> top_rp;
+    DBuf<uint8_t> top_rank;
+    DBuf<double> top_val;
+    DBuf<int64_t> top_cuts;
+    int ntop_cuts = 0;
+    // on A^T: rows served by the streaming path (skipped by the gather kernel)
+    DBuf<uint8_t> skip;
 };
+constexpr int kTop = 64;
 constexpr int kHot = 4096;
 
 struct ProfAgg {
@@ -103,6 +115,9 @@ void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v);
 // ---- spmm.cu : Y (rows x ncols, row-major ldy) = A * X (row-major ldx)
 void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
                  int64_t ldy, const char* tag);
+// Z = A^T Y with the top columns of A streamed (A: CSR of A, T: its transpose)
+void spmm_t_device(Ctx& c, const DCsr& A, const DCsr& T, const double* Y, int64_t ncols, double* Z,
+                   const char* tag);
 
 // ---- dense.cu
 // B (n x n, column-major, full symmetric) = W^T W for row-major W (r x n, ld n).

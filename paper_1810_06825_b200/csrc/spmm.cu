@@ -132,7 +132,7 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
                                            const double* __restrict__ val, const WorkItem* __restrict__ items,
                                            int64_t nitems, const double* __restrict__ X, int64_t ldx,
                                            double* __restrict__ Y, int64_t ldy, double* __restrict__ part,
-                                           int ncols, const Hot& hot) {
+                                           int ncols, const Hot& hot, const uint8_t* __restrict__ skip) {
     using V = Vec<VEC>;
     using T = typename V::T;
     const int lane = threadIdx.x & 31;
@@ -142,6 +142,7 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
         const WorkItem w = items[it];
         if (w.r1 >= 0) {
             for (int32_t r = w.r0; r < w.r1; ++r) {
+                if (skip && skip[r]) continue;  // served by the streaming path
                 T acc[NCH];
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
@@ -172,9 +173,10 @@ __global__ void __launch_bounds__(kThreads, 4)
 k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
        const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
        const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
-       double* __restrict__ part, int ncols, const int32_t* __restrict__ hot_cols) {
+       double* __restrict__ part, int ncols, const int32_t* __restrict__ hot_cols,
+       const uint8_t* __restrict__ skip) {
     const Hot hot{nullptr, 0, HOT ? hot_cols : nullptr};
-    spmm_items<VEC, NCH, HOT>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot);
+    spmm_items<VEC, NCH, HOT>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, skip);
 }
 
 // A * X with the H most popular columns' X rows staged in shared memory: one
@@ -196,7 +198,7 @@ k_spmm_hot(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     }
     __syncthreads();
     const Hot hot{Xs, H, hot_cols};
-    spmm_items<2, NCH, true>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot);
+    spmm_items<2, NCH, true>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, nullptr);
 }
 
 // Long rows: Y[row] = sum of its chunk partials in a fixed order. One CTA per
@@ -249,7 +251,7 @@ void launch_plain(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y
     grid = std::max(grid, 1);
     k_spmm<VEC, NCH, HOT><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
                                                            A.items.get(), A.nitems, X, ldx, Y, ldy, part,
-                                                           ncols, A.hot_cols.get());
+                                                           ncols, A.hot_cols.get(), A.skip.get());
     FB_LAUNCH_CHECK();
 }
 
@@ -283,6 +285,116 @@ void launch(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int6
     if (use_hot && VEC == 2 && ncols % 2 == 0 && A.nitems >= 32 * c.num_sms)
         return launch_hot<NCH>(c, A, X, ldx, Y, ldy, part, ncols);
     launch_plain<VEC, NCH, true>(c, A, X, ldx, Y, ldy, part, ncols);
+}
+
+// ---------------------------------------------------------------------------
+// A^T*Y for the kTop most popular columns of A by STREAMING Y: one CTA per SM
+// walks a contiguous row range of A, stages Y's rows through shared memory
+// (coalesced, each row read once) and accumulates, for every top entry
+// (i, rank, v) of those rows, v * Y[i] into the rank's accumulator. Warp w
+// owns ranks {w, w+16, w+32, w+48} in registers, so the accumulation of every
+// output entry is in ascending row order within the CTA; the per-CTA partials
+// are then added in CTA order (deterministic). This replaces nnz_top random
+// 8*l-byte gathers of Y by one coalesced pass over Y.
+constexpr int TOP_WARPS = 16;
+constexpr int TOP_RB = 16;   // rows staged per batch
+
+template <int NCH>
+__global__ void __launch_bounds__(TOP_WARPS * 32, 1)
+k_aty_top(const double* __restrict__ Y, int64_t ldy, int ncols, const int64_t* __restrict__ top_rp,
+          const uint8_t* __restrict__ top_rank, const double* __restrict__ top_val,
+          const int64_t* __restrict__ cuts, double* __restrict__ part) {
+    extern __shared__ __align__(16) double Ys[];  // [2][TOP_RB][ncols]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t r0 = cuts[blockIdx.x], r1 = cuts[blockIdx.x + 1];
+    double2 acc[4][NCH];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) acc[k][ch] = make_double2(0.0, 0.0);
+    const int half = ncols / 2;
+    auto stage_rows = [&](int buf, int64_t b0) {
+        double* dst = Ys + size_t(buf) * TOP_RB * ncols;
+        const int nrows = (r1 - b0) < TOP_RB ? int(r1 - b0) : TOP_RB;
+        for (int e = tid; e < nrows * half; e += blockDim.x) {
+            const int rr = e / half, c2 = e % half;
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + rr * ncols + 2 * c2));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                         "l"(Y + (b0 + rr) * ldy + 2 * c2));
+        }
+        asm volatile("cp.async.commit_group;\n");
+    };
+    if (r0 < r1) stage_rows(0, r0);
+    int buf = 0;
+    for (int64_t b0 = r0; b0 < r1; b0 += TOP_RB, buf ^= 1) {
+        if (b0 + TOP_RB < r1) {
+            stage_rows(buf ^ 1, b0 + TOP_RB);
+            asm volatile("cp.async.wait_group 1;\n");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n");
+        }
+        __syncthreads();
+        const double* ys = Ys + size_t(buf) * TOP_RB * ncols + lane * 2;
+        const int nrows = (r1 - b0) < TOP_RB ? int(r1 - b0) : TOP_RB;
+        for (int rr = 0; rr < nrows; ++rr) {
+            const int64_t p0 = top_rp[b0 + rr], p1 = top_rp[b0 + rr + 1];
+            for (int64_t p = p0; p < p1; ++p) {
+                const int rk = top_rank[p];
+                if ((rk & (TOP_WARPS - 1)) != warp) continue;
+                const double v = top_val[p];
+                double2 y[NCH];
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch)
+                    y[ch] = (ch * 32 + lane) * 2 < ncols
+                                ? *reinterpret_cast<const double2*>(ys + rr * ncols + ch * 64)
+                                : make_double2(0.0, 0.0);
+                const int k = rk >> 4;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    if (kk == k)
+#pragma unroll
+                        for (int ch = 0; ch < NCH; ++ch) {
+                            acc[kk][ch].x = __fma_rn(v, y[ch].x, acc[kk][ch].x);
+                            acc[kk][ch].y = __fma_rn(v, y[ch].y, acc[kk][ch].y);
+                        }
+            }
+        }
+        __syncthreads();
+    }
+    // partial [cta][rank][ncols]
+    double* out = part + size_t(blockIdx.x) * kTop * ncols;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        const int rk = kk * TOP_WARPS + warp;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+            if ((ch * 32 + lane) * 2 < ncols)
+                *reinterpret_cast<double2*>(out + size_t(rk) * ncols + ch * 64 + lane * 2) = acc[kk][ch];
+    }
+}
+
+// Z[top_cols[r]] = sum over CTAs (in order) of the partials
+__global__ void k_top_combine(const double* __restrict__ part, int nparts, int ncols,
+                              const int32_t* __restrict__ top_cols, double* __restrict__ Z, int64_t ldz) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kTop * ncols; e += gridDim.x * blockDim.x) {
+        const int rk = e / ncols, c = e % ncols;
+        double acc = 0.0;
+        for (int g = 0; g < nparts; ++g) acc += part[size_t(g) * kTop * ncols + e];
+        Z[int64_t(top_cols[rk]) * ldz + c] = acc;
+    }
+}
+
+template <int NCH>
+void launch_top(Ctx& c, const DCsr& A, const double* Y, int64_t ldy, int ncols, double* part) {
+    const size_t smem = sizeof(double) * 2 * TOP_RB * size_t(ncols);
+    static bool attr = false;
+    if (!attr) {
+        FB_CUDA(cudaFuncSetAttribute(k_aty_top<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        attr = true;
+    }
+    k_aty_top<NCH><<<A.ntop_cuts, TOP_WARPS * 32, smem, c.stream>>>(
+        Y, ldy, ncols, A.top_rp.get(), A.top_rank.get(), A.top_val.get(), A.top_cuts.get(), part);
+    FB_LAUNCH_CHECK();
 }
 
 }  // namespace
@@ -329,6 +441,42 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
             }
         }
     }
+}
+
+void spmm_t_device(Ctx& c, const DCsr& A, const DCsr& T, const double* Y, int64_t ncols, double* Z,
+                   const char* tag) {
+    const bool stream = A.ntop > 0 && ncols % 2 == 0 && ncols <= 256 && ncols > 0;
+    if (!stream) {
+        // the gather kernel must not skip the top rows: run it on a view without the mask
+        if (A.ntop > 0) {
+            DCsr& Tm = const_cast<DCsr&>(T);
+            DBuf<uint8_t> keep = std::move(Tm.skip);
+            try {
+                spmm_device(c, T, Y, ncols, ncols, Z, ncols, tag);
+            } catch (...) {
+                Tm.skip = std::move(keep);
+                throw;
+            }
+            Tm.skip = std::move(keep);
+            return;
+        }
+        return spmm_device(c, T, Y, ncols, ncols, Z, ncols, tag);
+    }
+    // the gather kernel handles every row except the top columns, whose rows of
+    // Z are written by the streaming kernel + combine
+    spmm_device(c, T, Y, ncols, ncols, Z, ncols, tag);
+    Prof prof(c, "spmm_AtY_top", 8.0 * double(A.rows) * ncols, 2.0 * double(A.top_val.n) * ncols);
+    DBuf<double> part(size_t(A.ntop_cuts) * kTop * ncols, c.stream);
+    const int nch = int((ncols + 63) / 64);
+    switch (nch) {
+        case 1: launch_top<1>(c, A, Y, ncols, int(ncols), part.get()); break;
+        case 2: launch_top<2>(c, A, Y, ncols, int(ncols), part.get()); break;
+        case 3: launch_top<3>(c, A, Y, ncols, int(ncols), part.get()); break;
+        default: launch_top<4>(c, A, Y, ncols, int(ncols), part.get()); break;
+    }
+    k_top_combine<<<(kTop * int(ncols) + 255) / 256, 256, 0, c.stream>>>(part.get(), A.ntop_cuts, int(ncols),
+                                                                          A.top_cols.get(), Z, ncols);
+    FB_LAUNCH_CHECK();
 }
 
 }  // namespace fb
