@@ -448,7 +448,13 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         return e && e[0] == '1';
     }();
     if (hot) build_hot(c, A, T);
-    build_top(c, M);
+    // top-column streaming of A^T*Y: measured slower than the gather path on
+    // C1/C2 (every warp walks every top entry); opt-in while it is reworked
+    static const bool top = [] {
+        const char* e = std::getenv("FRPCA_TOP_STREAM");
+        return e && e[0] == '1';
+    }();
+    if (top) build_top(c, M);
     build_items(c, A);
     build_items(c, T);
     FB_CUDA(cudaStreamSynchronize(s));

@@ -187,23 +187,10 @@ k_gram2(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
     };
     const int64_t nsteps = (re - rs + G2_ROWS - 1) / G2_ROWS;
     if (nsteps > 0) load(0, rs);
-    // this warp's tiles: fragment offsets of A (row tile) and B (column tile),
-    // and where the A fragment changes
-    const int nmine = t1 - t0;
-    __shared__ int offs[G2_WARPS][MAXT];  // (A offset << 16) | B offset, in doubles
-    int* off = offs[warp];
-    unsigned areload = 0;
-    {
-        int ti = 0;
-        while ((ti + 1) * (ti + 2) / 2 <= t0) ++ti;
-        int tj = t0 - ti * (ti + 1) / 2;
-#pragma unroll
-        for (int i = 0; i < MAXT; ++i) {
-            if (lane == 0) off[i] = (ti * 8) << 16 | (tj * 8);
-            if (i == 0 || tj == 0) areload |= 1u << i;
-            if (++tj > ti) { ++ti; tj = 0; }
-        }
-    }
+    // (ti, tj) of this warp's first tile
+    int ti0 = 0;
+    while ((ti0 + 1) * (ti0 + 2) / 2 <= t0) ++ti0;
+    const int tj0 = t0 - ti0 * (ti0 + 1) / 2;
     for (int64_t st = 0; st < nsteps; ++st) {
         const int stage = int(st & 1);
         if (st + 1 < nsteps) {
@@ -217,12 +204,18 @@ k_gram2(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
 #pragma unroll
         for (int kk = 0; kk < G2_ROWS / 4; ++kk) {
             const double* rowp = Ws + (kk * 4 + (lane & 3)) * S + (lane >> 2);
-            double a = 0.0;
+            int ti = ti0, tj = tj0;
+            double a = rowp[ti * 8];
 #pragma unroll
             for (int i = 0; i < MAXT; ++i) {
-                if (i < nmine) {
-                    if (areload & (1u << i)) a = rowp[off[i] >> 16];
-                    dmma(acc[i], a, rowp[off[i] & 0xffff]);
+                if (t0 + i < t1) {
+                    const double b = rowp[tj * 8];
+                    dmma(acc[i], a, b);
+                    if (++tj > ti) {
+                        ++ti;
+                        tj = 0;
+                        a = rowp[min(ti, T - 1) * 8];
+                    }
                 }
             }
         }

@@ -98,13 +98,21 @@ def test_transpose_matches_oracle(fb, orc, seed):  # test_sparse.cpp:90-100
     assert np.array_equal(T.rowPtr(), rp) and np.array_equal(T.colIdx(), ci) and np.array_equal(T.values(), va)
 
 
-def test_spmm_transpose_bitwise_equals_spmm_on_transpose(fb, orc):
-    """A^T*Y from the load-time transposed CSR == spmm on transpose(A): same kernel, same order."""
+def test_spmm_transpose_equals_spmm_on_transpose(fb, orc):
+    """A^T*Y from the load-time transposed CSR == spmm on transpose(A). Rows of
+    A^T outside the streamed top columns use the same gather kernel in the same
+    order (bitwise equal); the top columns' rows are summed per CTA then
+    combined in CTA order (rounding-level difference only)."""
     oA = powerlaw_csr(orc, 2000, 1500, 60000, 5)
     A = to_fb(fb, oA)
     At = fb.transpose(A)
     Y = orc.gaussian_matrix(2000, 40, 9)
-    assert np.array_equal(fb.spmm_transpose(A, Y), fb.spmm(At, Y))
+    Z1, Z2 = fb.spmm_transpose(A, Y), fb.spmm(At, Y)
+    assert rel_fro(Z1, Z2) <= 1e-13
+    counts = np.diff(At.rowPtr())
+    top = np.argsort(-counts, kind="stable")[:64]
+    rest = np.setdiff1d(np.arange(A.cols()), top)
+    assert np.array_equal(Z1[rest], Z2[rest])
 
 
 def test_pass_counter(fb, orc):  # test_sparse.cpp:111-118
