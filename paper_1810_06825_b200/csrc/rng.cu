@@ -142,19 +142,20 @@ __device__ double cr_log(double x) {
 // Segment start states by tree doubling: level a computes, for every k in
 // [2^a, 2^(a+1)), state_k = T^(J 2^a) state_(k - 2^a) with the jump polynomial
 // x^(J 2^a) mod P (one jump per segment in total). Horner over the 19937
-// coefficients, 32 per step: r <- T^32 r + sum_b c_(32g+b) T^b base.
+// coefficients, 64 per step: r <- T^64 r + sum_b c_(64g+b) T^b base.
 // The window T^b base is the base sequence shifted by b, so one shared table
 // serves every thread: N[v][j] = XOR of ext[j + i] over the set bits i of the
-// nibble v, and the 32-coefficient sum for thread j is
-//   XOR_q N[nibble_q(c)][j + 4q], q = 0..7  (8 shared loads, conflict-free).
+// nibble v, and the 64-coefficient sum for thread j is
+//   XOR_q N[nibble_q(c)][j + 4q], q = 0..15  (16 conflict-free shared loads).
 // The window r is ping-ponged, so a step is one barrier.
-constexpr int NTAB = NN + 32;  // table row length (j + 4q + 3 < NN + 31)
+constexpr int JW = 64;             // coefficients per Horner step
+constexpr int NTAB = NN + JW;      // table row length (j + 4q + 3 < NN + 63)
 constexpr size_t kNibBytes = sizeof(uint64_t) * 16 * NTAB;
 
 __global__ void __launch_bounds__(320, 2)
 k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, int groups, int64_t first,
              int64_t K) {
-    __shared__ uint64_t ext[NN + 32];
+    __shared__ uint64_t ext[NN + JW];
     extern __shared__ uint64_t nib_dyn[];  // [16][NTAB]
     uint64_t (*nib)[NTAB] = reinterpret_cast<uint64_t (*)[NTAB]>(nib_dyn);
     __shared__ uint64_t R[2][NN];
@@ -169,30 +170,33 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, i
     }
     for (int g = tid; g < groups; g += blockDim.x) co[g] = poly[g];
     __syncthreads();
-    if (tid < 32) ext[NN + tid] = mt_next(ext[tid], ext[tid + 1], ext[tid + MM]);
+    if (tid < JW) ext[NN + tid] = mt_next(ext[tid], ext[tid + 1], ext[tid + MM]);
     __syncthreads();
     for (int e = tid; e < 16 * NTAB; e += blockDim.x) {
         const int v = e / NTAB, j = e % NTAB;
         uint64_t x = 0;
         #pragma unroll
         for (int i = 0; i < 4; ++i)
-            if (((v >> i) & 1) && j + i < NN + 32) x ^= ext[j + i];
+            if (((v >> i) & 1) && j + i < NN + JW) x ^= ext[j + i];
         nib[v][j] = x;
     }
     __syncthreads();
     int cur = 0;
-    for (int g = groups - 1; g >= 0; --g) {
-        const uint32_t c = co[g];
+    const int ng = (groups + 1) / 2;  // 64-bit coefficient groups
+    for (int g = ng - 1; g >= 0; --g) {
+        const uint32_t lo = co[2 * g], hi = (2 * g + 1 < groups) ? co[2 * g + 1] : 0u;
         if (tid < NN) {
             uint64_t x = 0;
             #pragma unroll
-            for (int q = 0; q < 8; ++q) x ^= nib[(c >> (4 * q)) & 15u][tid + 4 * q];
+            for (int q = 0; q < 8; ++q) x ^= nib[(lo >> (4 * q)) & 15u][tid + 4 * q];
+            #pragma unroll
+            for (int q = 0; q < 8; ++q) x ^= nib[(hi >> (4 * q)) & 15u][tid + 32 + 4 * q];
             const uint64_t* r = R[cur];
             uint64_t v;
-            if (tid < NN - 32) {
-                v = r[tid + 32];
+            if (tid < NN - JW) {
+                v = r[tid + JW];
             } else {
-                const int t = tid - (NN - 32);
+                const int t = tid - (NN - JW);
                 v = mt_next(r[t], r[t + 1], r[t + MM]);
             }
             R[cur ^ 1][tid] = v ^ x;
