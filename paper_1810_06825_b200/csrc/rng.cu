@@ -345,9 +345,11 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     // attempts needed with margin: accepted ~ Bin(P, pi/4), need 2*acc >= count
     const double half = 0.5 * double(count);
     const int64_t P = int64_t(half / (M_PI / 4.0) + 8.0 * std::sqrt(half / (M_PI / 4.0)) + 64.0);
-    // segments of J = 156 * 2^e words, at most ~2048 of them per level of 2^e
+    // segments of J = 156 * 2^e words: ~2048 per level of 2^e for short
+    // streams; long streams are cut so that every batch (<= 2^30 words) still
+    // holds >= ~1600 segments (the generator is 156-wide per segment)
     int log2S = 6;
-    while (log2S < 14 && (2 * P) / (int64_t(MM) << log2S) > 2048) ++log2S;
+    while (log2S < 12 && (2 * P) / (int64_t(MM) << log2S) > 2048) ++log2S;
     const int64_t steps = int64_t(1) << log2S, J = int64_t(MM) << log2S;
     int groups = 0;
     const uint32_t* polys = device_polys(c, log2S, groups);
@@ -376,7 +378,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         }
     }
     // batches of segments: raw words -> per-chunk counts -> scan -> normals
-    const int64_t seg_per_batch = std::max<int64_t>(1, (int64_t(1) << 28) / J);
+    const int64_t seg_per_batch = std::max<int64_t>(1, (int64_t(1) << 30) / J);
     DBuf<uint64_t> raw(size_t(std::min(K, seg_per_batch) * J), s);
     int64_t pairs_done = 0;  // accepted attempts emitted so far
     for (int64_t seg0 = 0; 2 * pairs_done < count; seg0 += seg_per_batch) {

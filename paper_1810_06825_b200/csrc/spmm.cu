@@ -412,7 +412,24 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
     const double bytes = 12.0 * A.nnz + 8.0 * (A.rows + 1) + 8.0 * ncols * (A.cols + A.rows);
     const double flops = 2.0 * A.nnz * ncols;
     Prof prof(c, tag, bytes, flops);
-    const int64_t slice_max = 256;
+    // L2-aware column slicing: when the gathered operand X (A.cols x ncols) is
+    // only a few times larger than L2, gather it in column slices that fit
+    // (each slice re-reads A's 12 B/nnz, but the 8*w-byte row gathers then hit
+    // L2 instead of HBM). Slices are multiples of 64 columns.
+    int64_t slice_max = 256;
+    {
+        const double budget = 80.0 * 1024 * 1024;
+        const double xbytes = 8.0 * double(A.cols) * double(ncols);
+        if (xbytes > budget && A.nnz > 8 * A.cols) {
+            const int64_t w = int64_t(budget / (8.0 * double(A.cols))) / 64 * 64;
+            if (w >= 64) slice_max = std::min<int64_t>(256, w);
+        }
+    }
+    static const bool no_slice = [] {
+        const char* e = std::getenv("FRPCA_NO_SLICE");
+        return e && e[0] == '1';
+    }();
+    if (no_slice) slice_max = 256;
     DBuf<double> part;
     for (int64_t off = 0; off < ncols; off += slice_max) {
         const int nc = int(std::min<int64_t>(slice_max, ncols - off));
