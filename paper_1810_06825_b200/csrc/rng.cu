@@ -352,7 +352,11 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     while (log2S < 12 && (2 * P) / (int64_t(MM) << log2S) > 2048) ++log2S;
     const int64_t steps = int64_t(1) << log2S, J = int64_t(MM) << log2S;
     int groups = 0;
-    const uint32_t* polys = device_polys(c, log2S, groups);
+    const uint32_t* polys = nullptr;
+    {
+        Prof pp(c, "omega_polys", 0.0, 0.0);
+        polys = device_polys(c, log2S, groups);
+    }
     static bool attr = false;
     if (!attr) {
         FB_CUDA(cudaFuncSetAttribute(k_jump_level, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNibBytes)));
@@ -379,7 +383,11 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     }
     // batches of segments: raw words -> per-chunk counts -> scan -> normals
     const int64_t seg_per_batch = std::max<int64_t>(1, (int64_t(1) << 30) / J);
-    DBuf<uint64_t> raw(size_t(std::min(K, seg_per_batch) * J), s);
+    DBuf<uint64_t> raw;
+    {
+        Prof pa(c, "omega_alloc", 0.0, 0.0);
+        raw.alloc(size_t(std::min(K, seg_per_batch) * J), s);
+    }
     int64_t pairs_done = 0;  // accepted attempts emitted so far
     for (int64_t seg0 = 0; 2 * pairs_done < count; seg0 += seg_per_batch) {
         if (seg0 >= K) {

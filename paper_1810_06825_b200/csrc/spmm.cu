@@ -420,7 +420,7 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
     {
         const double budget = 80.0 * 1024 * 1024;
         const double xbytes = 8.0 * double(A.cols) * double(ncols);
-        if (xbytes > budget && A.nnz > 8 * A.cols) {
+        if (xbytes > budget && A.nnz > 8 * A.cols && std::getenv("FRPCA_SLICE")) {
             const int64_t w = int64_t(budget / (8.0 * double(A.cols))) / 64 * 64;
             if (w >= 64) slice_max = std::min<int64_t>(256, w);
         }
