@@ -418,7 +418,8 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
     // L2 instead of HBM). Slices are multiples of 64 columns.
     int64_t slice_max = 256;
     {
-        const double budget = 80.0 * 1024 * 1024;
+        const char* eb = std::getenv("FRPCA_SLICE_BUDGET_MB");
+        const double budget = (eb ? std::atof(eb) : 80.0) * 1024 * 1024;
         const double xbytes = 8.0 * double(A.cols) * double(ncols);
         if (xbytes > budget && A.nnz > 8 * A.cols && std::getenv("FRPCA_SLICE")) {
             const int64_t w = int64_t(budget / (8.0 * double(A.cols))) / 64 * 64;
