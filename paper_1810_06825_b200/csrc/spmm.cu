@@ -115,14 +115,27 @@ __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) V::fma(acc[ch], v[u], x[u][ch]);
         }
-        for (; j < cnt; ++j) {
-            const int c0 = __shfl_sync(0xffffffffu, myc, j);
-            const double v0 = __shfl_sync(0xffffffffu, myv, j);
-            T x[NCH];
-            gather<VEC, NCH, HOT>(x, c0, Xl, ldx, ok, lane, ncols, hot);
+        if (j < cnt) {
+            // the last 1-3 nonzeros as one group with their loads in flight
+            // together (a sequential tail would pay one round trip each); the
+            // padding slots re-read a valid row with weight 0 and add exactly 0
+            const int rem = cnt - j;
+            int c[3];
+            double v[3];
 #pragma unroll
-            for (int ch = 0; ch < NCH; ++ch)
-                if (ok[ch]) V::fma(acc[ch], v0, x[ch]);
+            for (int u = 0; u < 3; ++u) {
+                const int src = u < rem ? j + u : j;
+                c[u] = __shfl_sync(0xffffffffu, myc, src);
+                const double vv = __shfl_sync(0xffffffffu, myv, src);
+                v[u] = u < rem ? vv : 0.0;
+            }
+            T x[3][NCH];
+#pragma unroll
+            for (int u = 0; u < 3; ++u) gather<VEC, NCH, HOT>(x[u], c[u], Xl, ldx, ok, lane, ncols, hot);
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) V::fma(acc[ch], v[u], x[u][ch]);
         }
     }
 }
