@@ -162,20 +162,18 @@ T read_scalar(Ctx& c, const T* d) {
     return h;
 }
 
-void build_items(Ctx& c, DCsr& A) {
+}  // namespace
+
+void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_t ch) {
     const int64_t m = A.rows;
-    A.nitems = A.ncombine = A.nslots = 0;
+    L.nitems = L.ncomb = L.nslots = 0;
+    L.chunk = ch;
     if (m == 0) return;
-    // chunk size: ~16 items per resident warp, clamped
-    const int64_t target = int64_t(c.num_sms) * 24 * 16;
-    int64_t ch = (A.nnz + m + target - 1) / target;
-    ch = std::max<int64_t>(256, std::min<int64_t>(16384, ch));
-    A.chunk = ch;
     DBuf<int32_t> cnt(3 * (m + 1), c.stream), off(3 * (m + 1), c.stream);
     int32_t *ni = cnt.get(), *ns = ni + (m + 1), *nc = ns + (m + 1);
     int32_t *oi = off.get(), *os = oi + (m + 1), *oc = os + (m + 1);
     FB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), c.stream));
-    k_item_counts<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, ni, ns, nc, A.skip.get());
+    k_item_counts<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, ni, ns, nc, skip);
     FB_LAUNCH_CHECK();
     size_t tb = 0;
     FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, ni, oi, m + 1, c.stream));
@@ -183,14 +181,23 @@ void build_items(Ctx& c, DCsr& A) {
     FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, ni, oi, m + 1, c.stream));
     FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, ns, os, m + 1, c.stream));
     FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, nc, oc, m + 1, c.stream));
-    A.nitems = read_scalar(c, oi + m);
-    A.nslots = read_scalar(c, os + m);
-    A.ncombine = read_scalar(c, oc + m);
-    A.items.alloc(size_t(A.nitems), c.stream);
-    A.combine.alloc(size_t(std::max<int64_t>(A.ncombine, 1)), c.stream);
-    k_item_write<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, oi, os, oc,
-                                                        A.items.get(), A.combine.get(), A.skip.get());
+    L.nitems = read_scalar(c, oi + m);
+    L.nslots = read_scalar(c, os + m);
+    L.ncomb = read_scalar(c, oc + m);
+    L.items.alloc(size_t(L.nitems), c.stream);
+    L.comb.alloc(size_t(std::max<int64_t>(L.ncomb, 1)), c.stream);
+    k_item_write<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, oi, os, oc, L.items.get(),
+                                                        L.comb.get(), skip);
     FB_LAUNCH_CHECK();
+}
+
+namespace {
+
+// chunk size of the work lists: ~16 items per resident warp, clamped
+int64_t default_chunk(const Ctx& c, const DCsr& A) {
+    const int64_t target = int64_t(c.num_sms) * 24 * 16;
+    const int64_t ch = (A.nnz + A.rows + target - 1) / target;
+    return std::max<int64_t>(256, std::min<int64_t>(16384, ch));
 }
 
 __global__ void k_col_counts(const int64_t* __restrict__ trp, int64_t n, int32_t* __restrict__ cnt,
@@ -239,102 +246,6 @@ void build_hot(Ctx& c, DCsr& A, const DCsr& T) {
     k_rank_map<<<grid_for(c, A.nhot), 256, 0, s>>>(A.hot_cols.get(), int(A.nhot), rank_of.get());
     FB_LAUNCH_CHECK();
     k_encode_hot<<<grid_for(c, A.nnz), 256, 0, s>>>(A.col.get(), A.nnz, rank_of.get());
-    FB_LAUNCH_CHECK();
-}
-
-__global__ void k_top_counts(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t m,
-                             const int32_t* __restrict__ rank_of, int64_t* __restrict__ cnt) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        int64_t k = 0;
-        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) k += rank_of[col[p]] >= 0;
-        cnt[i] = k;
-    }
-}
-
-__global__ void k_top_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                           const double* __restrict__ val, int64_t m, const int32_t* __restrict__ rank_of,
-                           const int64_t* __restrict__ trp, uint8_t* __restrict__ rank, double* __restrict__ tv) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        int64_t o = trp[i];
-        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-            const int32_t r = rank_of[col[p]];
-            if (r >= 0) { rank[o] = uint8_t(r); tv[o] = val[p]; ++o; }
-        }
-    }
-}
-
-__global__ void k_top_skip(const int32_t* __restrict__ top, int ntop, uint8_t* __restrict__ skip) {
-    for (int r = threadIdx.x; r < ntop; r += blockDim.x) skip[top[r]] = 1;
-}
-
-// cut k: first row i with (i + top_rp[i]) >= k * total / G (weight = row + entries)
-__global__ void k_top_cuts(const int64_t* __restrict__ trp, int64_t m, int G, int64_t* __restrict__ cuts) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k > G) return;
-    const int64_t total = m + trp[m];
-    const int64_t target = (total * k) / G;
-    int64_t lo = 0, hi = m;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (mid + trp[mid] < target) lo = mid + 1; else hi = mid;
-    }
-    cuts[k] = (k == G) ? m : lo;
-}
-
-// Top-column streaming structures for A^T*Y (see spmm.cu k_aty_top): the kTop
-// most popular columns, if they hold >= 20% of the nonzeros.
-void build_top(Ctx& c, DMat& M) {
-    DCsr& A = M.A;
-    DCsr& T = M.At;
-    const int64_t n = A.cols, m = A.rows;
-    A.ntop = 0;
-    if (n < 2 * kTop || A.nnz == 0 || m == 0) return;
-    cudaStream_t s = c.stream;
-    DBuf<int32_t> cnt(size_t(n), s), ids(size_t(n), s), cnt_s(size_t(n), s), ids_s(size_t(n), s);
-    k_col_counts<<<grid_for(c, n), 256, 0, s>>>(T.rowptr.get(), n, cnt.get(), ids.get());
-    FB_LAUNCH_CHECK();
-    size_t tb = 0;
-    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.get(), cnt_s.get(), ids.get(),
-                                                      ids_s.get(), n, 0, 32, s));
-    DBuf<unsigned char> tmp(tb, s);
-    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), tb, cnt.get(), cnt_s.get(), ids.get(),
-                                                      ids_s.get(), n, 0, 32, s));
-    std::vector<int32_t> hc(kTop);
-    FB_CUDA(cudaMemcpyAsync(hc.data(), cnt_s.get(), sizeof(int32_t) * kTop, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaStreamSynchronize(s));
-    int64_t top_nnz = 0;
-    for (int32_t x : hc) top_nnz += x;
-    if (double(top_nnz) < 0.2 * double(A.nnz)) return;
-    A.ntop = kTop;
-    A.top_cols.alloc(kTop, s);
-    FB_CUDA(cudaMemcpyAsync(A.top_cols.get(), ids_s.get(), sizeof(int32_t) * kTop, cudaMemcpyDeviceToDevice, s));
-    DBuf<int32_t> rank_of(size_t(n), s);
-    FB_CUDA(cudaMemsetAsync(rank_of.get(), 0xff, rank_of.bytes(), s));
-    k_rank_map<<<1, 256, 0, s>>>(A.top_cols.get(), kTop, rank_of.get());
-    FB_LAUNCH_CHECK();
-    DBuf<int64_t> rc(size_t(m) + 1, s);
-    FB_CUDA(cudaMemsetAsync(rc.get(), 0, rc.bytes(), s));
-    k_top_counts<<<grid_for(c, m), 256, 0, s>>>(A.rowptr.get(), A.col.get(), m, rank_of.get(), rc.get());
-    FB_LAUNCH_CHECK();
-    A.top_rp.alloc(size_t(m) + 1, s);
-    tb = 0;
-    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, rc.get(), A.top_rp.get(), m + 1, s));
-    DBuf<unsigned char> tmp2(tb, s);
-    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp2.get(), tb, rc.get(), A.top_rp.get(), m + 1, s));
-    A.top_rank.alloc(size_t(top_nnz), s);
-    A.top_val.alloc(size_t(top_nnz), s);
-    k_top_fill<<<grid_for(c, m), 256, 0, s>>>(A.rowptr.get(), A.col.get(), A.val.get(), m, rank_of.get(),
-                                               A.top_rp.get(), A.top_rank.get(), A.top_val.get());
-    FB_LAUNCH_CHECK();
-    T.skip.alloc(size_t(n), s);
-    FB_CUDA(cudaMemsetAsync(T.skip.get(), 0, T.skip.bytes(), s));
-    k_top_skip<<<1, 256, 0, s>>>(A.top_cols.get(), kTop, T.skip.get());
-    FB_LAUNCH_CHECK();
-    A.ntop_cuts = c.num_sms;
-    A.top_cuts.alloc(size_t(c.num_sms) + 1, s);
-    k_top_cuts<<<(c.num_sms + 1 + 255) / 256, 256, 0, s>>>(A.top_rp.get(), m, c.num_sms, A.top_cuts.get());
     FB_LAUNCH_CHECK();
 }
 
@@ -448,15 +359,167 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         return e && e[0] == '1';
     }();
     if (hot) build_hot(c, A, T);
-    // top-column streaming of A^T*Y: measured slower than the gather path on
-    // C1/C2 (every warp walks every top entry); opt-in while it is reworked
-    static const bool top = [] {
-        const char* e = std::getenv("FRPCA_TOP_STREAM");
-        return e && e[0] == '1';
-    }();
-    if (top) build_top(c, M);
-    build_items(c, A);
-    build_items(c, T);
+    build_items(c, A, nullptr, A.L, default_chunk(c, A));
+    build_items(c, T, nullptr, T.L, default_chunk(c, T));
+    FB_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---- panelled A^T*Y plan (see PanelPlan in internal.cuh) ---------------------
+
+namespace {
+
+__global__ void k_hot_flags(const int64_t* __restrict__ rp, int64_t n, int64_t thot,
+                            uint8_t* __restrict__ skip, int32_t* __restrict__ flag) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        const bool h = rp[r + 1] - rp[r] >= thot;
+        skip[r] = h;
+        flag[r] = h;
+    }
+}
+
+__global__ void k_hot_list(const int32_t* __restrict__ flag, const int32_t* __restrict__ pos, int64_t n,
+                           int32_t* __restrict__ hot) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n;
+         r += int64_t(gridDim.x) * blockDim.x)
+        if (flag[r]) hot[pos[r]] = int32_t(r);
+}
+
+// first position q in [lo, hi) with col[q] >= key (col ascending within the row)
+__device__ __forceinline__ int64_t lower_bound(const int32_t* __restrict__ col, int64_t lo, int64_t hi,
+                                               int64_t key) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (col[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Walks hot row h segment by segment (one non-empty panel each). WRITE = false:
+// chunk counts per (panel, row) and per row; WRITE = true: the items (at the
+// panel-major positions) and the row's combine entry.
+template <bool WRITE>
+__global__ void k_panel_walk(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ hot, int64_t nhot, int64_t pr, int64_t pch,
+                             int32_t* __restrict__ cnt, int32_t* __restrict__ rowslots,
+                             const int32_t* __restrict__ itempos, const int32_t* __restrict__ slotbase,
+                             WorkItem* __restrict__ items, Combine* __restrict__ comb) {
+    for (int64_t h = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; h < nhot;
+         h += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t r = hot[h];
+        int64_t p = rp[r];
+        const int64_t e = rp[r + 1];
+        int32_t slot = WRITE ? slotbase[h] : 0;
+        while (p < e) {
+            const int64_t pan = col[p] / pr;
+            const int64_t q = lower_bound(col, p, e, (pan + 1) * pr);
+            const int32_t k = int32_t((q - p + pch - 1) / pch);
+            if (WRITE) {
+                const int32_t o = itempos[pan * nhot + h];
+                for (int32_t t = 0; t < k; ++t) {
+                    WorkItem w;
+                    w.p0 = p + int64_t(t) * pch;
+                    w.p1 = min(q, p + int64_t(t + 1) * pch);
+                    w.r0 = r;
+                    w.r1 = -(slot + t) - 1;
+                    items[o + t] = w;
+                }
+            } else {
+                cnt[pan * nhot + h] = k;
+            }
+            slot += k;
+            p = q;
+        }
+        if (WRITE) {
+            Combine cb;
+            cb.row = r; cb.s0 = slotbase[h]; cb.s1 = slot; cb.pad = 0;
+            comb[h] = cb;
+        } else {
+            rowslots[h] = slot;
+        }
+    }
+}
+
+}  // namespace
+
+// Builds (or reuses) the panel plan of T for panels of `pr` rows of the
+// gathered operand. Rows with >= thot entries (3 per panel on average: below
+// that a per-panel partial costs more than the HBM gathers it saves) are hot;
+// thot is doubled until the partials fit `slot_cap` rows.
+void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap) {
+    PanelPlan& P = T.pan;
+    if (P.pr == pr) return;
+    P = PanelPlan{};
+    if (T.rows == 0 || T.nnz == 0 || pr <= 0) return;
+    cudaStream_t s = c.stream;
+    const int64_t n = T.rows;
+    const int64_t npan = (T.cols + pr - 1) / pr;
+    const int64_t pch = std::min<int64_t>(T.L.chunk, 1024);
+    DBuf<int32_t> flag(size_t(n) + 1, s), pos(size_t(n) + 1, s);
+    P.skip.alloc(size_t(n), s);
+    int64_t thot = 3 * npan, nhot = 0, nitems = 0;
+    DBuf<int32_t> hot, cnt, rowslots, itempos, slotbase;
+    for (;;) {
+        FB_CUDA(cudaMemsetAsync(flag.get(), 0, flag.bytes(), s));
+        k_hot_flags<<<grid_for(c, n), 256, 0, s>>>(T.rowptr.get(), n, thot, P.skip.get(), flag.get());
+        FB_LAUNCH_CHECK();
+        size_t tb = 0;
+        FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.get(), pos.get(), n + 1, s));
+        DBuf<unsigned char> tmp(tb, s);
+        FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, flag.get(), pos.get(), n + 1, s));
+        nhot = read_scalar(c, pos.get() + n);
+        if (nhot == 0) {
+            P = PanelPlan{};
+            P.pr = pr;  // cached: nothing is hot at this panel size
+            return;
+        }
+        if (double(npan) * double(nhot) >= double(1 << 30)) { thot *= 2; continue; }
+        hot.alloc(size_t(nhot), s);
+        k_hot_list<<<grid_for(c, n), 256, 0, s>>>(flag.get(), pos.get(), n, hot.get());
+        FB_LAUNCH_CHECK();
+        cnt.alloc(size_t(npan * nhot) + 1, s);
+        rowslots.alloc(size_t(nhot) + 1, s);
+        FB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+        FB_CUDA(cudaMemsetAsync(rowslots.get(), 0, rowslots.bytes(), s));
+        k_panel_walk<false><<<grid_for(c, nhot, 128), 128, 0, s>>>(T.rowptr.get(), T.col.get(), hot.get(), nhot,
+                                                                   pr, pch, cnt.get(), rowslots.get(), nullptr,
+                                                                   nullptr, nullptr, nullptr);
+        FB_LAUNCH_CHECK();
+        // 64-bit total first: the int32 scans below need it < 2^31
+        DBuf<int64_t> tot(1, s);
+        size_t tb2 = 0;
+        FB_CUDA(cub::DeviceReduce::Sum(nullptr, tb2, rowslots.get(), tot.get(), nhot, s));
+        DBuf<unsigned char> tmp2(tb2, s);
+        FB_CUDA(cub::DeviceReduce::Sum(tmp2.get(), tb2, rowslots.get(), tot.get(), nhot, s));
+        nitems = read_scalar(c, tot.get());
+        if (nitems <= slot_cap && nitems < (int64_t(1) << 30)) break;
+        thot *= 2;
+    }
+    itempos.alloc(size_t(npan * nhot) + 1, s);
+    slotbase.alloc(size_t(nhot) + 1, s);
+    size_t tb = 0;
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), itempos.get(), npan * nhot + 1, s));
+    DBuf<unsigned char> tmp(tb, s);
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), itempos.get(), npan * nhot + 1, s));
+    tb = 0;
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, rowslots.get(), slotbase.get(), nhot + 1, s));
+    tmp.alloc(tb, s);
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, rowslots.get(), slotbase.get(), nhot + 1, s));
+    P.hot.items.alloc(size_t(nitems), s);
+    P.hot.comb.alloc(size_t(nhot), s);
+    k_panel_walk<true><<<grid_for(c, nhot, 128), 128, 0, s>>>(T.rowptr.get(), T.col.get(), hot.get(), nhot, pr,
+                                                              pch, nullptr, nullptr, itempos.get(), slotbase.get(),
+                                                              P.hot.items.get(), P.hot.comb.get());
+    FB_LAUNCH_CHECK();
+    P.hot.nitems = P.hot.nslots = nitems;
+    P.hot.ncomb = nhot;
+    P.hot.chunk = pch;
+    build_items(c, T, P.skip.get(), P.cold, T.L.chunk);
+    P.counter.alloc(1, s);
+    P.npanels = npan;
+    P.thot = thot;
+    P.nhot = nhot;
+    P.pr = pr;
     FB_CUDA(cudaStreamSynchronize(s));
 }
 

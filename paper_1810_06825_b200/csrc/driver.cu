@@ -298,7 +298,7 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
 }
 
 void spmm_pass(Ctx& c, DMat& M, bool transpose, const double* X, int64_t ncols, double* Y) {
-    if (transpose) spmm_t_device(c, M.A, M.At, X, ncols, Y, "spmm_AtY");
+    if (transpose) spmm_t_device(c, M.At, X, ncols, Y, "spmm_AtY");
     else spmm_device(c, M.A, X, ncols, ncols, Y, ncols, "spmm_AX");
     M.passes.fetch_add(1, std::memory_order_relaxed);  // recordPass, sparse_matrix.hpp:119-122
 }

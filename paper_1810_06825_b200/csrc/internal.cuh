@@ -29,33 +29,42 @@ struct Combine {
     int32_t row, s0, s1, pad;
 };
 
+// A load-balanced SpMM work list (built once at load, see csr.cu).
+struct ItemList {
+    DBuf<WorkItem> items;
+    DBuf<Combine> comb;
+    int64_t nitems = 0, ncomb = 0, nslots = 0, chunk = 0;
+};
+
+// Panelled A^T*Y (csr.cu build_panels, spmm.cu spmm_panelled): when the
+// gathered operand Y (rows x l) is much larger than L2, the entries of the
+// "hot" rows of A^T (popular columns of A) are cut at panel boundaries of Y's
+// rows (`pr` rows per panel) and the chunks are executed panel-major, so the Y
+// rows they gather are L2-resident while a panel is being worked on; the
+// chunk partials are added per row in entry order. The other ("cold") rows
+// keep the plain gather list.
+struct PanelPlan {
+    int64_t pr = 0, npanels = 0, thot = 0, nhot = 0;
+    DBuf<uint8_t> skip;  // hot rows (skipped by the cold list)
+    ItemList hot;        // chunk items, panel-major; slots per row in entry order
+    ItemList cold;       // work list of the other rows
+    DBuf<int32_t> counter;
+};
+
 // Device CSR: int64 row_ptr (8 B/row), int32 col ids, fp64 values (12 B/nnz).
 struct DCsr {
     int64_t rows = 0, cols = 0, nnz = 0;
     DBuf<int64_t> rowptr;
     DBuf<int32_t> col;
     DBuf<double> val;
-    // load-balanced work list (built once at load)
-    DBuf<WorkItem> items;
-    DBuf<Combine> combine;
-    int64_t nitems = 0, ncombine = 0, nslots = 0, chunk = 0;
-    // Hot columns (A only): the kHot most popular columns, by nnz, are encoded
-    // in `col` as -(rank+1); hot_cols[rank] is the original column id.
+    ItemList L;  // work list over all rows
+    // Hot columns (A only, opt-in FRPCA_HOT_STAGING): the kHot most popular
+    // columns, by nnz, are encoded in `col` as -(rank+1); hot_cols[rank] is
+    // the original column id.
     DBuf<int32_t> hot_cols;
     int64_t nhot = 0;
-    // A^T*Y top-column streaming (on A): the kTop most popular columns, their
-    // entries per row of A (rank, value) and row cuts for one CTA per SM.
-    int ntop = 0;
-    DBuf<int32_t> top_cols;
-    DBuf<int64_t> top_rp;
-    DBuf<uint8_t> top_rank;
-    DBuf<double> top_val;
-    DBuf<int64_t> top_cuts;
-    int ntop_cuts = 0;
-    // on A^T: rows served by the streaming path (skipped by the gather kernel)
-    DBuf<uint8_t> skip;
+    PanelPlan pan;  // on A^T only
 };
-constexpr int kTop = 64;
 constexpr int kHot = 4096;
 
 struct ProfAgg {
@@ -111,13 +120,16 @@ struct DMat {
 void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
                        const int64_t* h_rowptr, const int64_t* h_col, const double* h_val);
 void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v);
+// work list of A's rows (rows with skip[r] != 0 left out), chunk size ch
+void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_t ch);
+// panel plan of T (== A^T) for panels of pr rows of the gathered operand
+void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap);
 
 // ---- spmm.cu : Y (rows x ncols, row-major ldy) = A * X (row-major ldx)
 void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
                  int64_t ldy, const char* tag);
-// Z = A^T Y with the top columns of A streamed (A: CSR of A, T: its transpose)
-void spmm_t_device(Ctx& c, const DCsr& A, const DCsr& T, const double* Y, int64_t ncols, double* Z,
-                   const char* tag);
+// Z = A^T Y on T = the transposed CSR of A (panelled for large Y, spmm.cu)
+void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, const char* tag);
 
 // ---- dense.cu
 // B (n x n, column-major, full symmetric) = W^T W for row-major W (r x n, ld n).

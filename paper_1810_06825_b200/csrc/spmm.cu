@@ -251,20 +251,51 @@ k_combine(const Combine* __restrict__ comb, const double* __restrict__ part, int
     }
 }
 
+// Panel chunks of A^T*Y (PanelPlan): every item is a chunk of one hot row
+// inside one panel, summed sequentially into its partial slot. Items are taken
+// in list (= panel-major) order through a global counter, so the resident
+// warps all work on about one panel of the gathered operand at a time.
+template <int NCH>
+__global__ void __launch_bounds__(kThreads, 4)
+k_spmm_panels(const int32_t* __restrict__ col, const double* __restrict__ val,
+              const WorkItem* __restrict__ items, int64_t nitems, const double* __restrict__ X, int64_t ldx,
+              double* __restrict__ part, int ncols, int32_t* __restrict__ counter) {
+    using V = Vec<2>;
+    using T = V::T;
+    const int lane = threadIdx.x & 31;
+    const Hot hot{nullptr, 0, nullptr};
+    for (;;) {
+        int it = 0;
+        if (lane == 0) it = atomicAdd(counter, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nitems) break;
+        const WorkItem w = items[it];
+        T acc[NCH];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
+        row_accumulate<2, NCH, false>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc);
+        double* pr = part + (-int64_t(w.r1) - 1) * ncols + lane * 2;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+            if ((ch * 32 + lane) * 2 < ncols) V::store(pr + ch * 64, acc[ch]);
+    }
+}
+
 template <int VEC, int NCH, bool HOT>
-void launch_plain(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
-                  double* part, int ncols) {
+void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
+                  double* Y, int64_t ldy, double* part, int ncols) {
+    if (!L.nitems) return;
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
         FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<VEC, NCH, HOT>,
                                                               kThreads, 0));
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    int grid = int(std::min<int64_t>(int64_t(c.num_sms) * blocks_per_sm, (A.nitems + 7) / 8));
+    int grid = int(std::min<int64_t>(int64_t(c.num_sms) * blocks_per_sm, (L.nitems + 7) / 8));
     grid = std::max(grid, 1);
     k_spmm<VEC, NCH, HOT><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
-                                                           A.items.get(), A.nitems, X, ldx, Y, ldy, part,
-                                                           ncols, A.hot_cols.get(), A.skip.get());
+                                                           L.items.get(), L.nitems, X, ldx, Y, ldy, part,
+                                                           ncols, A.hot_cols.get(), skip);
     FB_LAUNCH_CHECK();
 }
 
@@ -280,143 +311,61 @@ void launch_hot(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, 
                                      int(kHotSmem)));
         attr = true;
     }
-    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, (A.nitems + 31) / 32)));
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, (A.L.nitems + 31) / 32)));
     k_spmm_hot<NCH><<<grid, kHotThreads, sizeof(double) * size_t(H) * ncols, c.stream>>>(
-        A.rowptr.get(), A.col.get(), A.val.get(), A.items.get(), A.nitems, X, ldx, Y, ldy, part, ncols,
+        A.rowptr.get(), A.col.get(), A.val.get(), A.L.items.get(), A.L.nitems, X, ldx, Y, ldy, part, ncols,
         A.hot_cols.get(), H);
     FB_LAUNCH_CHECK();
 }
 
 template <int VEC, int NCH>
-void launch(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
-            double* part, int ncols) {
-    if (A.nhot == 0) return launch_plain<VEC, NCH, false>(c, A, X, ldx, Y, ldy, part, ncols);
-    static const bool use_hot = [] {
-        const char* e = std::getenv("FRPCA_HOT_STAGING");
-        return e && e[0] == '1';
-    }();
-    if (use_hot && VEC == 2 && ncols % 2 == 0 && A.nitems >= 32 * c.num_sms)
+void launch(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
+            double* Y, int64_t ldy, double* part, int ncols) {
+    if (A.nhot == 0) return launch_plain<VEC, NCH, false>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
+    if (VEC == 2 && ncols % 2 == 0 && &L == &A.L && A.L.nitems >= 32 * c.num_sms)
         return launch_hot<NCH>(c, A, X, ldx, Y, ldy, part, ncols);
-    launch_plain<VEC, NCH, true>(c, A, X, ldx, Y, ldy, part, ncols);
+    launch_plain<VEC, NCH, true>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
 }
 
-// ---------------------------------------------------------------------------
-// A^T*Y for the kTop most popular columns of A by STREAMING Y: one CTA per SM
-// walks a contiguous row range of A, stages Y's rows through shared memory
-// (coalesced, each row read once) and accumulates, for every top entry
-// (i, rank, v) of those rows, v * Y[i] into the rank's accumulator. Warp w
-// owns ranks {w, w+16, w+32, w+48} in registers, so the accumulation of every
-// output entry is in ascending row order within the CTA; the per-CTA partials
-// are then added in CTA order (deterministic). This replaces nnz_top random
-// 8*l-byte gathers of Y by one coalesced pass over Y.
-constexpr int TOP_WARPS = 16;
-constexpr int TOP_RB = 16;   // rows staged per batch
-
-template <int NCH>
-__global__ void __launch_bounds__(TOP_WARPS * 32, 1)
-k_aty_top(const double* __restrict__ Y, int64_t ldy, int ncols, const int64_t* __restrict__ top_rp,
-          const uint8_t* __restrict__ top_rank, const double* __restrict__ top_val,
-          const int64_t* __restrict__ cuts, double* __restrict__ part) {
-    extern __shared__ __align__(16) double Ys[];  // [2][TOP_RB][ncols]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t r0 = cuts[blockIdx.x], r1 = cuts[blockIdx.x + 1];
-    double2 acc[4][NCH];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) acc[k][ch] = make_double2(0.0, 0.0);
-    const int half = ncols / 2;
-    auto stage_rows = [&](int buf, int64_t b0) {
-        double* dst = Ys + size_t(buf) * TOP_RB * ncols;
-        const int nrows = (r1 - b0) < TOP_RB ? int(r1 - b0) : TOP_RB;
-        for (int e = tid; e < nrows * half; e += blockDim.x) {
-            const int rr = e / half, c2 = e % half;
-            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + rr * ncols + 2 * c2));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa),
-                         "l"(Y + (b0 + rr) * ldy + 2 * c2));
-        }
-        asm volatile("cp.async.commit_group;\n");
-    };
-    if (r0 < r1) stage_rows(0, r0);
-    int buf = 0;
-    for (int64_t b0 = r0; b0 < r1; b0 += TOP_RB, buf ^= 1) {
-        if (b0 + TOP_RB < r1) {
-            stage_rows(buf ^ 1, b0 + TOP_RB);
-            asm volatile("cp.async.wait_group 1;\n");
-        } else {
-            asm volatile("cp.async.wait_group 0;\n");
-        }
-        __syncthreads();
-        const double* ys = Ys + size_t(buf) * TOP_RB * ncols + lane * 2;
-        const int nrows = (r1 - b0) < TOP_RB ? int(r1 - b0) : TOP_RB;
-        for (int rr = 0; rr < nrows; ++rr) {
-            const int64_t p0 = top_rp[b0 + rr], p1 = top_rp[b0 + rr + 1];
-            for (int64_t p = p0; p < p1; ++p) {
-                const int rk = top_rank[p];
-                if ((rk & (TOP_WARPS - 1)) != warp) continue;
-                const double v = top_val[p];
-                double2 y[NCH];
-#pragma unroll
-                for (int ch = 0; ch < NCH; ++ch)
-                    y[ch] = (ch * 32 + lane) * 2 < ncols
-                                ? *reinterpret_cast<const double2*>(ys + rr * ncols + ch * 64)
-                                : make_double2(0.0, 0.0);
-                const int k = rk >> 4;
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    if (kk == k)
-#pragma unroll
-                        for (int ch = 0; ch < NCH; ++ch) {
-                            acc[kk][ch].x = __fma_rn(v, y[ch].x, acc[kk][ch].x);
-                            acc[kk][ch].y = __fma_rn(v, y[ch].y, acc[kk][ch].y);
-                        }
-            }
-        }
-        __syncthreads();
-    }
-    // partial [cta][rank][ncols]
-    double* out = part + size_t(blockIdx.x) * kTop * ncols;
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-        const int rk = kk * TOP_WARPS + warp;
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
-            if ((ch * 32 + lane) * 2 < ncols)
-                *reinterpret_cast<double2*>(out + size_t(rk) * ncols + ch * 64 + lane * 2) = acc[kk][ch];
-    }
-}
-
-// Z[top_cols[r]] = sum over CTAs (in order) of the partials
-__global__ void k_top_combine(const double* __restrict__ part, int nparts, int ncols,
-                              const int32_t* __restrict__ top_cols, double* __restrict__ Z, int64_t ldz) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kTop * ncols; e += gridDim.x * blockDim.x) {
-        const int rk = e / ncols, c = e % ncols;
-        double acc = 0.0;
-        for (int g = 0; g < nparts; ++g) acc += part[size_t(g) * kTop * ncols + e];
-        Z[int64_t(top_cols[rk]) * ldz + c] = acc;
-    }
-}
-
-template <int NCH>
-void launch_top(Ctx& c, const DCsr& A, const double* Y, int64_t ldy, int ncols, double* part) {
-    const size_t smem = sizeof(double) * 2 * TOP_RB * size_t(ncols);
-    static bool attr = false;
-    if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_aty_top<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        attr = true;
-    }
-    k_aty_top<NCH><<<A.ntop_cuts, TOP_WARPS * 32, smem, c.stream>>>(
-        Y, ldy, ncols, A.top_rp.get(), A.top_rank.get(), A.top_val.get(), A.top_cuts.get(), part);
+void combine(Ctx& c, const ItemList& L, const double* part, int nc, double* Y, int64_t ldy) {
+    if (!L.ncomb) return;
+    k_combine<<<unsigned(L.ncomb), kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy);
     FB_LAUNCH_CHECK();
+}
+
+// One slice of <= 256 columns over the work list L (rows with skip[r] left
+// out), then the fixed-order combine of its long rows.
+void spmm_list(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
+               int nc, double* Y, int64_t ldy, double* part) {
+    const bool v2 = (nc % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
+                    (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
+    if (v2) {
+        switch ((nc + 63) / 64) {
+            case 1: launch<2, 1>(c, A, L, skip, X, ldx, Y, ldy, part, nc); break;
+            case 2: launch<2, 2>(c, A, L, skip, X, ldx, Y, ldy, part, nc); break;
+            case 3: launch<2, 3>(c, A, L, skip, X, ldx, Y, ldy, part, nc); break;
+            default: launch<2, 4>(c, A, L, skip, X, ldx, Y, ldy, part, nc); break;
+        }
+        combine(c, L, part, nc, Y, ldy);
+        return;
+    }
+    // scalar path (odd widths): slices of <= 128 columns
+    for (int o = 0; o < nc; o += 128) {
+        const int w = std::min(128, nc - o);
+        const int nch = (w + 31) / 32;
+        if (nch <= 1) launch<1, 1>(c, A, L, skip, X + o, ldx, Y + o, ldy, part, w);
+        else if (nch <= 2) launch<1, 2>(c, A, L, skip, X + o, ldx, Y + o, ldy, part, w);
+        else launch<1, 4>(c, A, L, skip, X + o, ldx, Y + o, ldy, part, w);
+        combine(c, L, part, w, Y + o, ldy);
+    }
+}
+
+double env_double(const char* name, double dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atof(e) : dflt;
 }
 
 }  // namespace
-
-void combine(Ctx& c, const DCsr& A, const double* part, int nc, double* Y, int64_t ldy) {
-    if (!A.ncombine) return;
-    k_combine<<<unsigned(A.ncombine), kCombWarps * 32, 0, c.stream>>>(A.combine.get(), part, nc, Y, ldy);
-    FB_LAUNCH_CHECK();
-}
 
 void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
                  int64_t ldy, const char* tag) {
@@ -425,89 +374,49 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
     const double bytes = 12.0 * A.nnz + 8.0 * (A.rows + 1) + 8.0 * ncols * (A.cols + A.rows);
     const double flops = 2.0 * A.nnz * ncols;
     Prof prof(c, tag, bytes, flops);
-    // L2-aware column slicing: when the gathered operand X (A.cols x ncols) is
-    // only a few times larger than L2, gather it in column slices that fit
-    // (each slice re-reads A's 12 B/nnz, but the 8*w-byte row gathers then hit
-    // L2 instead of HBM). Slices are multiples of 64 columns.
-    int64_t slice_max = 256;
-    {
-        const char* eb = std::getenv("FRPCA_SLICE_BUDGET_MB");
-        const double budget = (eb ? std::atof(eb) : 80.0) * 1024 * 1024;
-        const double xbytes = 8.0 * double(A.cols) * double(ncols);
-        if (xbytes > budget && A.nnz > 8 * A.cols && std::getenv("FRPCA_SLICE")) {
-            const int64_t w = int64_t(budget / (8.0 * double(A.cols))) / 64 * 64;
-            if (w >= 64) slice_max = std::min<int64_t>(256, w);
-        }
-    }
-    static const bool no_slice = [] {
-        const char* e = std::getenv("FRPCA_NO_SLICE");
-        return e && e[0] == '1';
-    }();
-    if (no_slice) slice_max = 256;
     DBuf<double> part;
-    for (int64_t off = 0; off < ncols; off += slice_max) {
-        const int nc = int(std::min<int64_t>(slice_max, ncols - off));
-        if (A.nslots && part.n < size_t(A.nslots) * nc) part.alloc(size_t(A.nslots) * nc, c.stream);
-        const bool v2 = (nc % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) && (off % 2 == 0);
-        const double* Xo = X + off;
-        double* Yo = Y + off;
-        if (v2) {
-            const int nch = (nc + 63) / 64;
-            switch (nch) {
-                case 1: launch<2, 1>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
-                case 2: launch<2, 2>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
-                case 3: launch<2, 3>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
-                default: launch<2, 4>(c, A, Xo, ldx, Yo, ldy, part.get(), nc); break;
-            }
-            combine(c, A, part.get(), nc, Yo, ldy);
-        } else {
-            // scalar path (odd widths): slices of <= 128 columns
-            for (int o = 0; o < nc; o += 128) {
-                const int w = std::min(128, nc - o);
-                const int nch = (w + 31) / 32;
-                if (nch <= 1) launch<1, 1>(c, A, Xo + o, ldx, Yo + o, ldy, part.get(), w);
-                else if (nch <= 2) launch<1, 2>(c, A, Xo + o, ldx, Yo + o, ldy, part.get(), w);
-                else launch<1, 4>(c, A, Xo + o, ldx, Yo + o, ldy, part.get(), w);
-                combine(c, A, part.get(), w, Yo + o, ldy);
-            }
-        }
+    for (int64_t off = 0; off < ncols; off += 256) {
+        const int nc = int(std::min<int64_t>(256, ncols - off));
+        if (A.L.nslots && part.n < size_t(A.L.nslots) * nc) part.alloc(size_t(A.L.nslots) * nc, c.stream);
+        spmm_list(c, A, A.L, nullptr, X + off, ldx, nc, Y + off, ldy, part.get());
     }
 }
 
-void spmm_t_device(Ctx& c, const DCsr& A, const DCsr& T, const double* Y, int64_t ncols, double* Z,
-                   const char* tag) {
-    const bool stream = A.ntop > 0 && ncols % 2 == 0 && ncols <= 256 && ncols > 0;
-    if (!stream) {
-        // the gather kernel must not skip the top rows: run it on a view without the mask
-        if (A.ntop > 0) {
-            DCsr& Tm = const_cast<DCsr&>(T);
-            DBuf<uint8_t> keep = std::move(Tm.skip);
-            try {
-                spmm_device(c, T, Y, ncols, ncols, Z, ncols, tag);
-            } catch (...) {
-                Tm.skip = std::move(keep);
-                throw;
-            }
-            Tm.skip = std::move(keep);
-            return;
+// Z = A^T Y on the transposed CSR T. When Y (T.cols x l) is several times
+// larger than a panel, the hot rows of T run through the panel plan first
+// (chunks panel-major + combine), then the cold rows through their own list.
+void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, const char* tag) {
+    if (T.rows == 0 || ncols == 0) return;
+    const int64_t w = std::min<int64_t>(ncols, 256);
+    const double panel_bytes = env_double("FRPCA_PANEL_MB", 32.0) * 1048576.0;
+    const double min_bytes = env_double("FRPCA_PANEL_MIN_MB", 96.0) * 1048576.0;
+    const bool use = ncols % 2 == 0 && 8.0 * double(T.cols) * double(w) > min_bytes &&
+                     env_double("FRPCA_NO_PANELS", 0.0) == 0.0;
+    if (use) {
+        const int64_t pr = std::max<int64_t>(1, int64_t(panel_bytes / (8.0 * double(w))));
+        const int64_t cap = int64_t(env_double("FRPCA_PANEL_PART_GB", 16.0) * 1073741824.0 / (8.0 * double(w)));
+        ensure_panels(c, T, pr, cap);
+    }
+    if (!use || T.pan.nhot == 0) return spmm_device(c, T, Y, ncols, ncols, Z, ncols, tag);
+    const PanelPlan& P = T.pan;
+    const double bytes = 12.0 * T.nnz + 8.0 * (T.rows + 1) + 8.0 * ncols * (T.cols + T.rows);
+    Prof prof(c, tag, bytes, 2.0 * T.nnz * ncols);
+    const size_t slots = size_t(std::max(P.hot.nslots, P.cold.nslots));
+    DBuf<double> part(slots * size_t(w), c.stream);
+    for (int64_t off = 0; off < ncols; off += 256) {
+        const int nc = int(std::min<int64_t>(256, ncols - off));
+        FB_CUDA(cudaMemsetAsync(P.counter.get(), 0, sizeof(int32_t), c.stream));
+        const int grid = c.num_sms * 4;
+        switch ((nc + 63) / 64) {
+            case 1: k_spmm_panels<1><<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y + off, ncols, part.get(), nc, P.counter.get()); break;
+            case 2: k_spmm_panels<2><<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y + off, ncols, part.get(), nc, P.counter.get()); break;
+            case 3: k_spmm_panels<3><<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y + off, ncols, part.get(), nc, P.counter.get()); break;
+            default: k_spmm_panels<4><<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y + off, ncols, part.get(), nc, P.counter.get()); break;
         }
-        return spmm_device(c, T, Y, ncols, ncols, Z, ncols, tag);
+        FB_LAUNCH_CHECK();
+        combine(c, P.hot, part.get(), nc, Z + off, ncols);
+        spmm_list(c, T, P.cold, P.skip.get(), Y + off, ncols, nc, Z + off, ncols, part.get());
     }
-    // the gather kernel handles every row except the top columns, whose rows of
-    // Z are written by the streaming kernel + combine
-    spmm_device(c, T, Y, ncols, ncols, Z, ncols, tag);
-    Prof prof(c, "spmm_AtY_top", 8.0 * double(A.rows) * ncols, 2.0 * double(A.top_val.n) * ncols);
-    DBuf<double> part(size_t(A.ntop_cuts) * kTop * ncols, c.stream);
-    const int nch = int((ncols + 63) / 64);
-    switch (nch) {
-        case 1: launch_top<1>(c, A, Y, ncols, int(ncols), part.get()); break;
-        case 2: launch_top<2>(c, A, Y, ncols, int(ncols), part.get()); break;
-        case 3: launch_top<3>(c, A, Y, ncols, int(ncols), part.get()); break;
-        default: launch_top<4>(c, A, Y, ncols, int(ncols), part.get()); break;
-    }
-    k_top_combine<<<(kTop * int(ncols) + 255) / 256, 256, 0, c.stream>>>(part.get(), A.ntop_cuts, int(ncols),
-                                                                          A.top_cols.get(), Z, ncols);
-    FB_LAUNCH_CHECK();
 }
 
 }  // namespace fb

@@ -153,6 +153,21 @@ def test_frpca_parity_powerlaw_l200(fb, orc, q):
     assert_parity(r, o)
 
 
+@pytest.mark.parametrize("algo", ["frpcat", "frpca"])
+def test_parity_panelled_aty(fb, orc, monkeypatch, algo):
+    """The panelled A^T*Y path (engaged by size on C1-C4) forced at test size."""
+    monkeypatch.setenv("FRPCA_PANEL_MIN_MB", "0")
+    monkeypatch.setenv("FRPCA_PANEL_MB", "0.5")
+    if algo == "frpcat":
+        oA = powerlaw_csr(orc, 20000, 4000, 400000, 23, a_row=1.8, a_col=1.05)
+    else:
+        oA = powerlaw_csr(orc, 3000, 30000, 400000, 29, a_row=1.2, a_col=1.2)
+    f = fb.frpcat if algo == "frpcat" else fb.frpca
+    r = f(to_fb(fb, oA), cfg(fb, 100, 100, 4, seed=0))
+    o = orc.pca(oA, orc.FRPCAT if algo == "frpcat" else orc.FRPCA, 100, 100, 4, seed=0)
+    assert_parity(r, o)
+
+
 def test_injected_omega_parity(fb, orc):
     oA = orc.Csr.random_sparse(500, 200, 0.05, 77)
     om = orc.gaussian_matrix(12, 500, 42)  # even q frpcat: Omega is l x m

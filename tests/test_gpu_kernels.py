@@ -99,20 +99,63 @@ def test_transpose_matches_oracle(fb, orc, seed):  # test_sparse.cpp:90-100
 
 
 def test_spmm_transpose_equals_spmm_on_transpose(fb, orc):
-    """A^T*Y from the load-time transposed CSR == spmm on transpose(A). Rows of
-    A^T outside the streamed top columns use the same gather kernel in the same
-    order (bitwise equal); the top columns' rows are summed per CTA then
-    combined in CTA order (rounding-level difference only)."""
+    """A^T*Y from the load-time transposed CSR == spmm on transpose(A): the
+    same gather kernel over the same work list, so bitwise equal."""
     oA = powerlaw_csr(orc, 2000, 1500, 60000, 5)
     A = to_fb(fb, oA)
     At = fb.transpose(A)
     Y = orc.gaussian_matrix(2000, 40, 9)
-    Z1, Z2 = fb.spmm_transpose(A, Y), fb.spmm(At, Y)
-    assert rel_fro(Z1, Z2) <= 1e-13
-    counts = np.diff(At.rowPtr())
-    top = np.argsort(-counts, kind="stable")[:64]
-    rest = np.setdiff1d(np.arange(A.cols()), top)
-    assert np.array_equal(Z1[rest], Z2[rest])
+    assert np.array_equal(fb.spmm_transpose(A, Y), fb.spmm(At, Y))
+
+
+@pytest.fixture
+def panels(monkeypatch):
+    """Forces the panelled A^T*Y (csr.cu ensure_panels) at test sizes: panels
+    of a few rows of Y instead of tens of MB."""
+    def force(panel_kb=100.0, part_gb=None):
+        monkeypatch.setenv("FRPCA_PANEL_MIN_MB", "0")
+        monkeypatch.setenv("FRPCA_PANEL_MB", str(panel_kb / 1024.0))
+        if part_gb is not None:
+            monkeypatch.setenv("FRPCA_PANEL_PART_GB", str(part_gb))
+    return force
+
+
+@pytest.mark.parametrize("ncols", [2, 40, 150, 200, 300])
+@pytest.mark.parametrize("seed", range(2))
+def test_spmm_transpose_panelled(fb, orc, panels, ncols, seed):
+    """Panel-major chunks of the hot rows + fixed-order combine, cold rows
+    through their own list: parity with the oracle, deterministic."""
+    panels()
+    oA = powerlaw_csr(orc, 3000, 2000, 120000, seed)
+    A = to_fb(fb, oA)
+    Y = orc.gaussian_matrix(3000, ncols, seed + 1)
+    Z = fb.spmm_transpose(A, Y)
+    assert rel_fro(Z, orc.spmm_transpose(oA, Y)) <= SPMM_TOL
+    assert np.array_equal(Z, fb.spmm_transpose(A, Y))
+
+
+@pytest.mark.parametrize("panel_kb,part_gb", [(3.0, None), (40.0, 1e-4), (1000.0, None)])
+def test_spmm_transpose_panel_sizes(fb, orc, panels, panel_kb, part_gb):
+    """Tiny panels (many segments per row), a partial budget that forces the
+    hot threshold up, and panels larger than Y (one panel)."""
+    panels(panel_kb, part_gb)
+    oA = powerlaw_csr(orc, 2500, 800, 90000, 3)
+    A = to_fb(fb, oA)
+    Y = orc.gaussian_matrix(2500, 64, 5)
+    assert rel_fro(fb.spmm_transpose(A, Y), orc.spmm_transpose(oA, Y)) <= SPMM_TOL
+
+
+def test_spmm_transpose_panelled_empty_rows(fb, orc, panels):
+    """Columns of A with no entries (empty rows of A^T) next to hot ones."""
+    panels(1.0)
+    trip = [(i, 0, 1.0 + i) for i in range(400)] + [(i, 5, -0.5) for i in range(0, 400, 3)]
+    A = fb.SparseMatrixCsr.from_triplets(400, 9, trip)
+    Y = orc.gaussian_matrix(400, 10, 2)
+    Z = fb.spmm_transpose(A, Y)
+    ref = np.zeros((9, 10))
+    for i, c, v in trip:
+        ref[c] += v * Y[i]
+    assert rel_fro(Z, ref) <= SPMM_TOL and not Z[[1, 2, 3, 4, 6, 7, 8]].any()
 
 
 def test_pass_counter(fb, orc):  # test_sparse.cpp:111-118
