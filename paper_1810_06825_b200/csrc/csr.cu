@@ -4,6 +4,7 @@
 // load-balanced SpMM work lists of both.
 #include <cub/cub.cuh>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -521,6 +522,10 @@ void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap) {
     P.nhot = nhot;
     P.pr = pr;
     FB_CUDA(cudaStreamSynchronize(s));
+    if (std::getenv("FRPCA_DEBUG_PANELS"))
+        std::fprintf(stderr, "panels: rows %lld pr %lld npanels %lld thot %lld nhot %lld hot_items %lld cold_items %lld "
+                     "cold_slots %lld\n", (long long)T.rows, (long long)pr, (long long)npan, (long long)thot,
+                     (long long)nhot, (long long)nitems, (long long)P.cold.nitems, (long long)P.cold.nslots);
 }
 
 void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v) {

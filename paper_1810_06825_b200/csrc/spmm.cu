@@ -360,6 +360,23 @@ void spmm_list(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, co
     }
 }
 
+void launch_panels(Ctx& c, const DCsr& T, const double* Y, int64_t ldy, double* part, int nc) {
+    const PanelPlan& P = T.pan;
+    FB_CUDA(cudaMemsetAsync(P.counter.get(), 0, sizeof(int32_t), c.stream));
+    const int grid = c.num_sms * 4;
+    auto go = [&](auto kern) {
+        kern<<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y, ldy,
+                                              part, nc, P.counter.get());
+        FB_LAUNCH_CHECK();
+    };
+    switch ((nc + 63) / 64) {
+        case 1: go(k_spmm_panels<1>); break;
+        case 2: go(k_spmm_panels<2>); break;
+        case 3: go(k_spmm_panels<3>); break;
+        default: go(k_spmm_panels<4>); break;
+    }
+}
+
 double env_double(const char* name, double dflt) {
     const char* e = std::getenv(name);
     return e && *e ? std::atof(e) : dflt;
@@ -407,14 +424,15 @@ void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, c
         const int nc = int(std::min<int64_t>(256, ncols - off));
         FB_CUDA(cudaMemsetAsync(P.counter.get(), 0, sizeof(int32_t), c.stream));
         const int grid = c.num_sms * 4;
-        switch ((nc + 63) / 64) {
-            case 1: k_spmm_panels<1><<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y + off, ncols, part.get(), nc, P.counter.get()); break;
-            case 2: k_spmm_panels<2><<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y + off, ncols, part.get(), nc, P.counter.get()); break;
-            case 3: k_spmm_panels<3><<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y + off, ncols, part.get(), nc, P.counter.get()); break;
-            default: k_spmm_panels<4><<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y + off, ncols, part.get(), nc, P.counter.get()); break;
+        {
+            Prof ph(c, "spmm_AtY_panels", 0, 0);
+            launch_panels(c, T, Y + off, ncols, part.get(), nc);
         }
-        FB_LAUNCH_CHECK();
-        combine(c, P.hot, part.get(), nc, Z + off, ncols);
+        {
+            Prof pc(c, "spmm_AtY_pcombine", 0, 0);
+            combine(c, P.hot, part.get(), nc, Z + off, ncols);
+        }
+        Prof pd(c, "spmm_AtY_cold", 0, 0);
         spmm_list(c, T, P.cold, P.skip.get(), Y + off, ncols, nc, Z + off, ncols, part.get());
     }
 }
