@@ -28,7 +28,7 @@
 
 namespace fb {
 
-int mt64_jump_polys(int log2_steps, int n, std::vector<uint32_t>& out, int& groups);
+int mt64_jump_polys(int log2_steps, int levels, std::vector<uint32_t>& out, int& groups);
 void mt64_seed_state(uint64_t seed, uint64_t* state312);
 
 namespace {
@@ -36,7 +36,7 @@ namespace {
 constexpr int NN = 312;
 constexpr int MM = 156;
 constexpr uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL, MA = 0xB5026F5AA96619E9ULL;
-constexpr int kMaxJumps = 16;
+constexpr int kJumpLevels = 4;  // 16-ary jump tree: up to 16^4 segments
 
 __device__ __forceinline__ uint64_t mt_next(uint64_t a, uint64_t b, uint64_t c) {
     const uint64_t y = (a & UM) | (b & LM);
@@ -139,9 +139,10 @@ __device__ double cr_log(double x) {
     return __dadd_rn(r.hi, r.lo);
 }
 
-// Segment start states by tree doubling: level a computes, for every k in
-// [2^a, 2^(a+1)), state_k = T^(J 2^a) state_(k - 2^a) with the jump polynomial
-// x^(J 2^a) mod P (one jump per segment in total). Horner over the 19937
+// Segment start states by a 16-ary tree: level a computes, for every
+// k = q 16^a + r in [16^a, 16^(a+1)) (q = 1..15, r < 16^a),
+// state_k = T^(J q 16^a) state_r with the jump polynomial x^(J q 16^a) mod P
+// (one jump per segment in total, ceil(log16 K) dependent levels). Horner over the 19937
 // coefficients, 64 per step: r <- T^64 r + sum_b c_(64g+b) T^b base.
 // The window T^b base is the base sequence shifted by b, so one shared table
 // serves every thread: N[v][j] = XOR of ext[j + i] over the set bits i of the
@@ -153,17 +154,18 @@ constexpr int NTAB = NN + JW;      // table row length (j + 4q + 3 < NN + 63)
 constexpr size_t kNibBytes = sizeof(uint64_t) * 16 * NTAB;
 
 __global__ void __launch_bounds__(320, 2)
-k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ poly, int groups, int64_t first,
-             int64_t K) {
+k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ polys, int groups, int64_t first,
+             int64_t k0, int64_t k1) {
     __shared__ uint64_t ext[NN + JW];
     extern __shared__ uint64_t nib_dyn[];  // [16][NTAB]
     uint64_t (*nib)[NTAB] = reinterpret_cast<uint64_t (*)[NTAB]>(nib_dyn);
     __shared__ uint64_t R[2][NN];
     __shared__ uint32_t co[640];
     const int tid = threadIdx.x;
-    const int64_t k = first + blockIdx.x;
-    if (k >= K) return;
-    const uint64_t* src = states + size_t(k - first) * NN;
+    const int64_t k = k0 + blockIdx.x;
+    if (k >= k1) return;
+    const uint64_t* src = states + size_t(k % first) * NN;
+    const uint32_t* poly = polys + size_t(k / first - 1) * groups;
     if (tid < NN) {
         ext[tid] = src[tid];
         R[0][tid] = 0;
@@ -327,13 +329,26 @@ const uint32_t* device_polys(Ctx& c, int log2S, int& groups) {
         return it->second;
     }
     std::vector<uint32_t> h;
-    mt64_jump_polys(log2S, kMaxJumps, h, groups);
+    mt64_jump_polys(log2S, kJumpLevels, h, groups);
     pc.groups = groups;
     uint32_t* d = nullptr;
     FB_CUDA(cudaMalloc(&d, h.size() * sizeof(uint32_t)));
     FB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     pc.dev[key] = d;
     return d;
+}
+
+// start states of segments [k0, k1) (those below k0 already computed), level
+// by level of the 16-ary tree
+void jump_states(Ctx& c, uint64_t* states, const uint32_t* polys, int groups, int64_t k0, int64_t k1) {
+    for (int a = 0; a < kJumpLevels; ++a) {
+        const int64_t first = int64_t(1) << (4 * a);
+        const int64_t lo = std::max(k0, first), hi = std::min(k1, 16 * first);
+        if (lo >= hi) continue;
+        k_jump_level<<<unsigned(hi - lo), 320, kNibBytes, c.stream>>>(states, polys + size_t(a) * 15 * groups,
+                                                                      groups, first, lo, hi);
+        FB_LAUNCH_CHECK();
+    }
 }
 
 }  // namespace
@@ -345,11 +360,17 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     // attempts needed with margin: accepted ~ Bin(P, pi/4), need 2*acc >= count
     const double half = 0.5 * double(count);
     const int64_t P = int64_t(half / (M_PI / 4.0) + 8.0 * std::sqrt(half / (M_PI / 4.0)) + 64.0);
-    // segments of J = 156 * 2^e words: ~2048 per level of 2^e for short
-    // streams; long streams are cut so that every batch (<= 2^30 words) still
-    // holds >= ~1600 segments (the generator is 156-wide per segment)
+    // segments of J = 156 * 2^e words: the fewest that still fill the
+    // generator (one 320-thread CTA per segment, k_gen occupancy), capped so
+    // that a batch of <= 2^30 raw words holds >= that many segments
+    static int gen_per_sm = 0;
+    if (!gen_per_sm) {
+        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gen_per_sm, k_gen, 320, 0));
+        gen_per_sm = std::max(gen_per_sm, 1);
+    }
+    const int64_t fill = int64_t(c.num_sms) * gen_per_sm;
     int log2S = 6;
-    while (log2S < 12 && (2 * P) / (int64_t(MM) << log2S) > 2048) ++log2S;
+    while (log2S < 12 && (2 * P + (int64_t(MM) << log2S) - 1) / (int64_t(MM) << log2S) > fill) ++log2S;
     const int64_t steps = int64_t(1) << log2S, J = int64_t(MM) << log2S;
     int groups = 0;
     const uint32_t* polys = nullptr;
@@ -365,21 +386,14 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     uint64_t s0[NN];
     mt64_seed_state(seed, s0);
     int64_t K = (2 * P + J - 1) / J;
-    // segment start states (tree doubling), computed for up to 2K segments
-    // so that the rare shortfall never needs a recomputation
+    // room for 2K + 1 segments so that the rare shortfall extends in place
     const int64_t Kmax = 2 * K + 1;
-    require(Kmax < (int64_t(1) << kMaxJumps), "gaussian_matrix: stream too long for the jump table");
+    require(Kmax <= (int64_t(1) << (4 * kJumpLevels)), "gaussian_matrix: stream too long for the jump table");
     DBuf<uint64_t> states(size_t(Kmax) * NN, s);
     {
         Prof pj(c, "omega_jump", 0.0, 0.0);
         FB_CUDA(cudaMemcpyAsync(states.get(), s0, sizeof(s0), cudaMemcpyHostToDevice, s));
-        for (int a = 0; (int64_t(1) << a) < K; ++a) {
-            const int64_t first = int64_t(1) << a;
-            const int64_t n = std::min<int64_t>(first, K - first);
-            k_jump_level<<<unsigned(n), 320, kNibBytes, s>>>(states.get(), polys + size_t(a) * groups,
-                                                             groups, first, K);
-            FB_LAUNCH_CHECK();
-        }
+        jump_states(c, states.get(), polys, groups, 1, K);
     }
     // batches of segments: raw words -> per-chunk counts -> scan -> normals
     const int64_t seg_per_batch = std::max<int64_t>(1, (int64_t(1) << 30) / J);
@@ -393,13 +407,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         if (seg0 >= K) {
             // shortfall (probability ~ 1e-15): extend the jump table to Kmax
             require(seg0 < Kmax, "gaussian_matrix: device stream generation did not converge");
-            for (int a = 0; (int64_t(1) << a) < Kmax; ++a) {
-                const int64_t first = int64_t(1) << a;
-                if (first + std::min<int64_t>(first, Kmax - first) <= K) continue;
-                k_jump_level<<<unsigned(std::min<int64_t>(first, Kmax - first)), 320, kNibBytes, s>>>(
-                    states.get(), polys + size_t(a) * groups, groups, first, Kmax);
-                FB_LAUNCH_CHECK();
-            }
+            jump_states(c, states.get(), polys, groups, K, Kmax);
             K = Kmax;
         }
         const int64_t nseg = std::min(seg_per_batch, K - seg0);

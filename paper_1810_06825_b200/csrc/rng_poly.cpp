@@ -115,35 +115,59 @@ void square_mod(const Poly& p, Bits& g) {
     if (tail) g.back() &= (uint64_t(1) << tail) - 1;
 }
 
-}  // namespace
+// g <- g * h mod P  (both < L bits)
+void mul_mod(const Poly& p, Bits& g, const Bits& h) {
+    const int64_t L = p.L;
+    Bits pr(size_t((2 * L + 63) / 64 + 2), 0);
+    for (int64_t i = 0; i < L; ++i)
+        if (getb(g, i)) xor_shifted(pr, h, L, i);
+    for (int64_t d = 2 * L - 2; d >= L; --d)
+        if (getb(pr, d)) xor_shifted(pr, p.P, L + 1, d - L);
+    g.assign(size_t((L + 63) / 64), 0);
+    for (int64_t w = 0; w < int64_t(g.size()); ++w) g[size_t(w)] = pr[size_t(w)];
+    const int64_t tail = L & 63;
+    if (tail) g.back() &= (uint64_t(1) << tail) - 1;
+}
 
-// Jump polynomials for J = 156 * 2^log2_steps words (a whole number of the
-// device generator's 156-word steps) and its doublings J*2^a, a < n.
-// Returned as 32-bit coefficient groups: out[a * groups + g] bit b is the
-// coefficient of x^(32 g + b) of x^(J 2^a) mod P. Also returns the degree L.
-int mt64_jump_polys(int log2_steps, int n, std::vector<uint32_t>& out, int& groups) {
+const Poly& char_poly() {
     static std::once_flag once;
     static Poly poly;
     std::call_once(once, [] { poly = characteristic_polynomial(); });
     if (poly.L != 19937) throw std::runtime_error("mt19937_64: unexpected characteristic polynomial degree");
+    return poly;
+}
+
+}  // namespace
+
+// Jump polynomials of a 16-ary jump tree for segments of J = 156 * 2^log2_steps
+// words (a whole number of the device generator's 156-word steps): level a
+// holds x^(J q 16^a) mod P for q = 1..15, so segment k = q 16^a + r starts at
+// T^(J q 16^a) applied to the start of segment r < 16^a.
+// Returned as 32-bit coefficient groups: out[((a * 15) + q - 1) * groups + g]
+// bit b is the coefficient of x^(32 g + b). Also returns the degree L.
+int mt64_jump_polys(int log2_steps, int levels, std::vector<uint32_t>& out, int& groups) {
+    const Poly& poly = char_poly();
     const int64_t L = poly.L;
     groups = int((L + 31) / 32);
-    Bits g(size_t((L + 63) / 64) + 1, 0);
-    g[0] = 1;  // x^0
-    for (int e = 0; e < 156; ++e) {  // g <- x * g mod P
+    Bits base(size_t((L + 63) / 64) + 1, 0);
+    base[0] = 1;  // x^0
+    for (int e = 0; e < 156; ++e) {  // base <- x * base mod P
         uint64_t carry = 0;
-        for (auto& w : g) { const uint64_t nc = w >> 63; w = (w << 1) | carry; carry = nc; }
-        if (getb(g, L)) xor_shifted(g, poly.P, L + 1, 0);
+        for (auto& w : base) { const uint64_t nc = w >> 63; w = (w << 1) | carry; carry = nc; }
+        if (getb(base, L)) xor_shifted(base, poly.P, L + 1, 0);
     }
-    g.resize(size_t((L + 63) / 64));
-    for (int e = 0; e < log2_steps; ++e) square_mod(poly, g);
-    out.assign(size_t(n) * size_t(groups), 0);
-    for (int a = 0; a < n; ++a) {
-        if (a > 0) square_mod(poly, g);
-        for (int gi = 0; gi < groups; ++gi) {
-            const int64_t w = gi / 2;
-            out[size_t(a) * groups + gi] = uint32_t(g[size_t(w)] >> ((gi & 1) * 32));
+    base.resize(size_t((L + 63) / 64));
+    for (int e = 0; e < log2_steps; ++e) square_mod(poly, base);  // x^J
+    out.assign(size_t(levels) * 15 * size_t(groups), 0);
+    for (int a = 0; a < levels; ++a) {
+        Bits g = base;  // x^(J 16^a)
+        for (int q = 1; q <= 15; ++q) {
+            if (q > 1) mul_mod(poly, g, base);
+            uint32_t* dst = out.data() + (size_t(a) * 15 + size_t(q - 1)) * size_t(groups);
+            for (int gi = 0; gi < groups; ++gi) dst[gi] = uint32_t(g[size_t(gi / 2)] >> ((gi & 1) * 32));
         }
+        if (a + 1 < levels)
+            for (int e = 0; e < 4; ++e) square_mod(poly, base);  // x^(J 16^(a+1))
     }
     return int(L);
 }

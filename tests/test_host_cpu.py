@@ -112,3 +112,18 @@ def test_validation_first_failure_order(fb, orc):
     with pytest.raises(ValueError) as e2:
         orc.Csr.create(*args)
     assert str(e1.value) == str(e2.value)
+
+
+def test_jump_polynomials(tmp_path):
+    """The device Omega generator's 16-ary jump tree (rng_poly.cpp) reproduces
+    std::mt19937_64::discard at levels 0 and 1 (host-only check)."""
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "jump_check"
+    subprocess.run(["g++", "-O2", "-std=c++20", os.path.join(root, "tests/cpp/jump_check.cpp"),
+                    os.path.join(root, "paper_1810_06825_b200/csrc/rng_poly.cpp"), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "bad 0" in out.stdout, out.stdout + out.stderr
