@@ -24,6 +24,7 @@
 #include <map>
 #include <mutex>
 
+#include "crlog.cuh"
 #include "internal.cuh"
 
 namespace fb {
@@ -60,84 +61,6 @@ __device__ __forceinline__ double canonical(uint64_t w) {
 }
 
 __device__ __forceinline__ int wrap(int i) { return i >= NN ? i - NN : i; }
-
-// ---- correctly rounded natural log on (0, 1] (double-double evaluation) ----
-// CUDA's log() is faithful (<= 1 ulp); evaluating log(r2) to ~100 bits and
-// rounding once matches glibc's log everywhere glibc itself is correctly
-// rounded (all but ~0.08% of the polar method's inputs, measured).
-struct dd { double hi, lo; };
-__device__ __forceinline__ dd two_sum(double a, double b) {
-    const double s = __dadd_rn(a, b);
-    const double bb = __dsub_rn(s, a);
-    const double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
-    return {s, e};
-}
-__device__ __forceinline__ dd fast_two_sum(double a, double b) {
-    const double s = __dadd_rn(a, b);
-    return {s, __dsub_rn(b, __dsub_rn(s, a))};
-}
-__device__ __forceinline__ dd two_prod(double a, double b) {
-    const double p = __dmul_rn(a, b);
-    return {p, __fma_rn(a, b, -p)};
-}
-__device__ __forceinline__ dd dd_add(dd a, dd b) {
-    dd s = two_sum(a.hi, b.hi);
-    const double t = __dadd_rn(a.lo, b.lo);
-    s.lo = __dadd_rn(s.lo, t);
-    return fast_two_sum(s.hi, s.lo);
-}
-__device__ __forceinline__ dd dd_mul(dd a, dd b) {
-    dd p = two_prod(a.hi, b.hi);
-    p.lo = __fma_rn(a.hi, b.lo, p.lo);
-    p.lo = __fma_rn(a.lo, b.hi, p.lo);
-    return fast_two_sum(p.hi, p.lo);
-}
-__device__ __forceinline__ dd dd_div(dd a, dd b) {
-    const double q1 = __ddiv_rn(a.hi, b.hi);
-    dd r = dd_add(a, dd_mul({-q1, 0.0}, b));
-    const double q2 = __ddiv_rn(r.hi, b.hi);
-    r = dd_add(r, dd_mul({-q2, 0.0}, b));
-    const double q3 = __ddiv_rn(r.hi, b.hi);
-    dd q = fast_two_sum(q1, q2);
-    return dd_add(q, {q3, 0.0});
-}
-
-__device__ double cr_log(double x) {
-    if (x == 1.0) return 0.0;
-    int e;
-    double m = frexp(x, &e);                       // x = m 2^e, m in [0.5, 1)
-    if (m < 0.70710678118654752440) { m = __dmul_rn(m, 2.0); e -= 1; }
-    // log m = 2 atanh(s), s = (m - 1) / (m + 1), |s| < 0.172
-    const double num = __dsub_rn(m, 1.0);         // exact (Sterbenz)
-    const dd den = two_sum(m, 1.0);
-    // s = num / den to ~2^-104: one division, residual by FMA
-    const double rcp = __ddiv_rn(1.0, den.hi);
-    const double q1 = __dmul_rn(num, rcp);
-    const double rem = __dsub_rn(__fma_rn(-q1, den.hi, num), __dmul_rn(q1, den.lo));
-    const double q2 = __dmul_rn(rem, rcp);
-    const dd s = fast_two_sum(q1, q2);
-    const dd s2 = dd_mul(s, s);
-    // tail sum_{k>=4} s2^(k-4) / (2k+1) in double (relative weight < 1e-6)
-    double t = 1.0 / 45.0;
-    #pragma unroll
-    for (int k = 21; k >= 4; --k) t = __fma_rn(t, s2.hi, 1.0 / double(2 * k + 1));
-    // 1 + s2/3 + s2^2/5 + s2^3/7 + s2^4 t, in double-double
-    const dd c3{0x1.5555555555555p-2, 0x1.5555555555555p-56};   // 1/3
-    const dd c5{0x1.999999999999ap-3, -0x1.999999999999ap-57};  // 1/5
-    const dd c7{0x1.2492492492492p-3, 0x1.2492492492492p-57};   // 1/7
-    dd p{t, 0.0};
-    p = dd_add(dd_mul(p, s2), c7);
-    p = dd_add(dd_mul(p, s2), c5);
-    p = dd_add(dd_mul(p, s2), c3);
-    p = dd_add(dd_mul(p, s2), {1.0, 0.0});
-    dd lm = dd_mul(p, s);
-    lm.hi = __dmul_rn(lm.hi, 2.0);
-    lm.lo = __dmul_rn(lm.lo, 2.0);
-    const dd ln2{0x1.62e42fefa39efp-1, 0x1.abc9e3b39803fp-56};
-    const dd el = dd_mul({double(e), 0.0}, ln2);
-    const dd r = dd_add(el, lm);
-    return __dadd_rn(r.hi, r.lo);
-}
 
 // Segment start states by a 16-ary tree: level a computes, for every
 // k = q 16^a + r in [16^a, 16^(a+1)) (q = 1..15, r < 16^a),
@@ -275,7 +198,7 @@ k_count(const uint64_t* __restrict__ raw, int64_t npairs, int64_t* __restrict__ 
 // normals of the accepted attempts, written at their stream positions
 __global__ void __launch_bounds__(PT)
 k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restrict__ off,
-       double* __restrict__ out, int64_t count) {
+       double* __restrict__ out, int64_t count, const crlog::LogEntry* __restrict__ logtab) {
     using Scan = cub::BlockScan<int, PT>;
     __shared__ typename Scan::TempStorage tmp;
     const int64_t base = off[blockIdx.x];
@@ -302,7 +225,7 @@ k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restri
         if (!ok[e]) continue;
         // mult = sqrt(-2 log(r2) / r2); y*mult first, then the saved x*mult; each
         // passes through `ret * stddev + mean` with (1, 0) (random.tcc).
-        const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, cr_log(rs[e])), rs[e]));
+        const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, crlog::fast_log(rs[e], logtab)), rs[e]));
         if (idx < count) out[idx] = __dadd_rn(__dmul_rn(__dmul_rn(ys[e], mult), 1.0), 0.0);
         if (idx + 1 < count) out[idx + 1] = __dadd_rn(__dmul_rn(__dmul_rn(xs[e], mult), 1.0), 0.0);
         idx += 2;
@@ -317,6 +240,22 @@ struct PolyCache {
 PolyCache& cache() {
     static PolyCache c;
     return c;
+}
+
+// table of the correctly rounded log's fast path, one copy per device
+const crlog::LogEntry* device_logtab(Ctx& c) {
+    static std::mutex mu;
+    static std::map<int, crlog::LogEntry*> tabs;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = tabs.find(c.device);
+    if (it != tabs.end()) return it->second;
+    std::vector<crlog::LogEntry> h(crlog::kLogTab);
+    crlog::build_log_table(h.data());
+    crlog::LogEntry* d = nullptr;
+    FB_CUDA(cudaMalloc(&d, h.size() * sizeof(crlog::LogEntry)));
+    FB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(crlog::LogEntry), cudaMemcpyHostToDevice));
+    tabs[c.device] = d;
+    return d;
 }
 
 const uint32_t* device_polys(Ctx& c, int log2S, int& groups) {
@@ -383,6 +322,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         FB_CUDA(cudaFuncSetAttribute(k_jump_level, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNibBytes)));
         attr = true;
     }
+    const crlog::LogEntry* logtab = device_logtab(c);
     uint64_t s0[NN];
     mt64_seed_state(seed, s0);
     int64_t K = (2 * P + J - 1) / J;
@@ -433,7 +373,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         }
         {
             Prof pe(c, "omega_emit", 8.0 * nseg * J + 8.0 * count, 0.0);
-            k_emit<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, off.get(), out, count);
+            k_emit<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, off.get(), out, count, logtab);
             FB_LAUNCH_CHECK();
         }
         FB_CUDA(cudaMemcpyAsync(&pairs_done, off.get() + nchunks, sizeof(int64_t), cudaMemcpyDeviceToHost, s));

@@ -127,3 +127,25 @@ def test_jump_polynomials(tmp_path):
                     os.path.join(root, "paper_1810_06825_b200/csrc/rng_poly.cpp"), "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "bad 0" in out.stdout, out.stdout + out.stderr
+
+
+def test_correctly_rounded_log(tmp_path):
+    """The Omega generator's log (crlog.cuh): the table fast path with its Ziv
+    fallback and the double-double path both equal the correctly rounded
+    quad-precision log on polar-method inputs, near 1, tiny, and at the
+    table's subinterval edges; z*c - 1 is exact at every subinterval end."""
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "log_check"
+    r = subprocess.run(["g++", "-O2", "-std=c++20", "-ffp-contract=off",
+                        os.path.join(root, "tests/cpp/log_check.cpp"), "-lquadmath", "-o", str(exe)],
+                       capture_output=True, text=True)
+    if r.returncode != 0 and "quadmath" in r.stderr:
+        pytest.skip("libquadmath not available")
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe), "1500000"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "table_bad 0 fast_bad 0 cr_bad 0" in out.stdout, out.stdout
