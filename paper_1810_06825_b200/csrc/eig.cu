@@ -1,12 +1,26 @@
 // K5: the l x l symmetric eigenproblem of eig_svd (dense_kernels.hpp:159-161,
-// Eigen SelfAdjointEigenSolver). The north_star allows cuSOLVER here: it is
-// O(l^3) on a 200 x 200 matrix, off the bandwidth-critical path.
+// Eigen SelfAdjointEigenSolver): cuSOLVER syevd, or (opt-in) the library's
+// own l <= 232 solver in syev.cu.
+#include <cstdlib>
+#include <cstring>
+
 #include "internal.cuh"
 
 namespace fb {
 
+bool syev_small(Ctx& c, double* B, int64_t n, double* d_D, std::vector<double>& h_D);
+
 void syevd_device(Ctx& c, double* B, int64_t n, double* d_D, std::vector<double>& h_D) {
     Prof prof(c, "syevd", 8.0 * n * n * 2, 4.0 / 3.0 * n * n * n);
+    // cuSOLVER by default. FRPCA_EIG=custom (or strict: custom, and a fallback
+    // is an error) selects the library's l <= 232 solver (syev.cu), which is
+    // correct but still slower than syevd at l = 200 (measured).
+    const char* mode = std::getenv("FRPCA_EIG");
+    const bool strict = mode && std::strcmp(mode, "strict") == 0;
+    if (mode && (strict || std::strcmp(mode, "custom") == 0)) {
+        if (syev_small(c, B, n, d_D, h_D)) return;
+        if (strict && n <= 232) throw CudaError("syev_small: did not converge (FRPCA_EIG=strict)");
+    }
     int lwork = 0;
     if (cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                     int(n), B, int(n), d_D, &lwork) != CUSOLVER_STATUS_SUCCESS)

@@ -1,0 +1,792 @@
+// K5: the l x l symmetric eigenproblem of eig_svd (dense_kernels.hpp:159-161,
+// Eigen's SelfAdjointEigenSolver in the reference) for l <= kEigMax.
+//
+// cuSOLVER's syevd spends ~1.8 ms on a 200 x 200 matrix, almost all of it
+// launch and host round-trip overhead. This solver is three kernels (opt-in,
+// FRPCA_EIG=custom: at l = 200 it measures ~2.0 ms per call, still latency-
+// bound in the single-CTA tridiagonalisation and the D&C merges):
+//   E1 k_sytrd  one CTA: Householder tridiagonalisation with the packed lower
+//               triangle resident in shared memory (LAPACK dsytd2 order);
+//   E2 k_stedc  one CTA: divide and conquer on the tridiagonal (Cuppen's
+//               rank-one tearing; leaves by implicit QL with Wilkinson shifts,
+//               one warp per leaf; merges with LAPACK-style deflation, the
+//               secular equation solved per root by one warp with the
+//               two-pole ("middle way") rational model under a bisection
+//               bracket, and Gu-Eisenstat's recomputed z so the merged
+//               eigenvectors are orthogonal to working precision);
+//   E3 k_ormtr  one warp per eigenvector: V = H_0 ... H_{n-3} Z.
+// Any non-convergence raises a flag and the caller falls back to cuSOLVER.
+#include <cfloat>
+#include <cstdio>
+#include <cstdlib>
+
+#include "internal.cuh"
+
+namespace fb {
+namespace {
+
+constexpr int kEigMax = 232;  // n(n+1)/2 doubles fit one CTA's shared memory
+constexpr int kET = 1024;
+constexpr int kLeafMax = 32;
+
+__device__ __forceinline__ int pk(int i, int j, int n) { return j * n - (j * (j - 1)) / 2 + (i - j); }
+
+// block-wide sum, same order on every thread (deterministic), result to all
+__device__ double block_sum(double v, double* red) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w];
+    return s;
+}
+
+// ---------------------------------------------------------------- E1
+// Packed lower triangle, row-major: A[i][k] (k <= i) at i(i+1)/2 + k.
+__device__ __forceinline__ int rp(int i) { return (i * (i + 1)) >> 1; }
+
+// every warp reduces the 32 per-warp partials itself (same order everywhere)
+__device__ __forceinline__ double warp_total(const double* red) {
+    double v = red[threadIdx.x & 31];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Four barriers per column: (A) reflector from the norm partials of the
+// previous step, (B) p = tau A22 v with the partials of p^T v, (C) w,
+// (D) A22 -= v w^T + w v^T with the norm partials of the next column.
+__global__ void __launch_bounds__(kET, 1)
+k_sytrd(const double* __restrict__ B, int n, double* __restrict__ Hv, double* __restrict__ tau,
+        double* __restrict__ dg, double* __restrict__ eo) {
+    extern __shared__ double sm[];
+    double* A = sm;                    // packed lower, row-major
+    double* v = A + rp(n);             // Householder vector (v[0] = 1)
+    double* w = v + kEigMax;           // p, then w
+    __shared__ double redA[32], redB[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = warp; i < n; i += 32)
+        for (int k = lane; k <= i; k += 32) A[rp(i) + k] = B[k + size_t(i) * n];  // B symmetric
+    __syncthreads();
+    {   // norm partials of column 0 below its subdiagonal entry
+        double ps = 0.0;
+        for (int i = 2 + warp; i < n; i += 32) {
+            const double x = A[rp(i)];
+            ps = fma(x, x, ps);
+        }
+        if (lane == 0) redA[warp] = ps;
+    }
+    __syncthreads();
+    for (int j = 0; j + 2 < n; ++j) {
+        const int t = n - j - 1;
+        // (A) reflector
+        const double xnorm2 = warp_total(redA);
+        const double alpha = A[rp(j + 1) + j];
+        double beta = alpha, tj = 0.0, scal = 0.0;
+        if (xnorm2 != 0.0) {
+            beta = -copysign(sqrt(fma(alpha, alpha, xnorm2)), alpha);
+            tj = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        if (tid < t) {
+            const double vi = tid == 0 ? 1.0 : A[rp(j + 1 + tid) + j] * scal;
+            v[tid] = vi;
+            Hv[size_t(j) * n + tid] = vi;
+        }
+        if (tid == 0) { tau[j] = tj; eo[j] = beta; dg[j] = A[rp(j) + j]; }
+        __syncthreads();
+        // (B) p = tau * A22 v: one warp per row (two rows in flight), lanes
+        // over the row and its column
+        {
+            double pv = 0.0;
+            for (int i0 = warp; i0 < t; i0 += 64) {
+                const int i1 = i0 + 32;
+                double a0 = 0.0, a1 = 0.0;
+                for (int k = lane; k < t; k += 32) {
+                    const int K = j + 1 + k;
+                    const double vk = v[k];
+                    a0 = fma(k <= i0 ? A[rp(j + 1 + i0) + K] : A[rp(K) + j + 1 + i0], vk, a0);
+                    if (i1 < t) a1 = fma(k <= i1 ? A[rp(j + 1 + i1) + K] : A[rp(K) + j + 1 + i1], vk, a1);
+                }
+                for (int o = 16; o; o >>= 1) {
+                    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+                }
+                a0 *= tj;
+                a1 *= tj;
+                if (lane == 0) {
+                    w[i0] = a0;
+                    if (i1 < t) w[i1] = a1;
+                }
+                pv = fma(a0, v[i0], pv);
+                if (i1 < t) pv = fma(a1, v[i1], pv);
+            }
+            if (lane == 0) redB[warp] = pv;
+        }
+        __syncthreads();
+        // (C) w = p - (tau/2)(p^T v) v
+        {
+            const double alpha2 = -0.5 * tj * warp_total(redB);
+            if (tid < t) w[tid] = fma(alpha2, v[tid], w[tid]);
+        }
+        __syncthreads();
+        // (D) rank-2 update; lane 0 of the row's warp sees the next column
+        {
+            double ps = 0.0;
+            for (int i = warp; i < t; i += 32) {
+                const double vi = v[i], wi = w[i];
+                double* row = A + rp(j + 1 + i) + (j + 1);
+                for (int k = lane; k <= i; k += 32) {
+                    const double x = row[k] - fma(vi, w[k], wi * v[k]);
+                    row[k] = x;
+                    if (k == 0 && i >= 2) ps = fma(x, x, ps);
+                }
+            }
+            if (lane == 0) redA[warp] = ps;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (n >= 2) {
+            dg[n - 2] = A[rp(n - 2) + n - 2];
+            dg[n - 1] = A[rp(n - 1) + n - 1];
+            eo[n - 2] = A[rp(n - 1) + n - 2];
+            tau[n - 2] = 0.0;
+        } else {
+            dg[0] = A[0];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- E2
+struct LeafWs {
+    double z[kLeafMax][kLeafMax + 1];  // row-major, lane = row
+    double d[kLeafMax], e[kLeafMax], rc[kLeafMax], rs[kLeafMax];
+    int perm[kLeafMax];
+};
+
+// Implicit QL with Wilkinson shifts on a b x b tridiagonal (b <= 32): lane 0
+// runs the scalar recurrence and records the rotations of a sweep, then every
+// lane applies them to its row of Z. Eigenvalues left in d (unsorted).
+__device__ bool leaf_ql(int b, LeafWs& w, int lane) {
+    for (int c = 0; c < b; ++c)
+        if (lane < b) w.z[lane][c] = lane == c ? 1.0 : 0.0;
+    if (lane == 0) w.e[b - 1] = 0.0;
+    __syncwarp();
+    for (int l = 0; l < b; ++l) {
+        for (int iter = 0;; ++iter) {
+            int m = l, rlo = l;
+            if (lane == 0) {
+                for (m = l; m < b - 1; ++m) {
+                    const double dd = fabs(w.d[m]) + fabs(w.d[m + 1]);
+                    if (fabs(w.e[m]) <= DBL_EPSILON * dd) break;
+                }
+                if (m != l && iter < 60) {
+                    double g = (w.d[l + 1] - w.d[l]) / (2.0 * w.e[l]);
+                    double r = sqrt(fma(g, g, 1.0));
+                    g = w.d[m] - w.d[l] + w.e[l] / (g + copysign(r, g));
+                    double s = 1.0, c = 1.0, p = 0.0;
+                    int i;
+                    for (i = m - 1; i >= l; --i) {
+                        const double f = s * w.e[i], bb = c * w.e[i];
+                        r = sqrt(fma(f, f, g * g));  // |f|, |g| ~ eigenvalue scale: no overflow
+                        w.e[i + 1] = r;
+                        if (r == 0.0) {
+                            w.d[i + 1] -= p;
+                            w.e[m] = 0.0;
+                            break;
+                        }
+                        const double ri = 1.0 / r;
+                        s = f * ri;
+                        c = g * ri;
+                        g = w.d[i + 1] - p;
+                        r = (w.d[i] - g) * s + 2.0 * c * bb;
+                        p = s * r;
+                        w.d[i + 1] = g + p;
+                        g = c * r - bb;
+                        w.rc[i] = c;
+                        w.rs[i] = s;
+                    }
+                    rlo = i + 1;
+                    if (!(r == 0.0 && i >= l)) {
+                        w.d[l] -= p;
+                        w.e[l] = g;
+                        w.e[m] = 0.0;
+                    }
+                }
+            }
+            m = __shfl_sync(0xffffffffu, m, 0);
+            rlo = __shfl_sync(0xffffffffu, rlo, 0);
+            __syncwarp();
+            if (m == l) break;
+            if (iter >= 60) return false;
+            if (lane < b)
+                for (int i = m - 1; i >= rlo; --i) {
+                    const double f = w.z[lane][i + 1];
+                    w.z[lane][i + 1] = w.rs[i] * w.z[lane][i] + w.rc[i] * f;
+                    w.z[lane][i] = w.rc[i] * w.z[lane][i] - w.rs[i] * f;
+                }
+            __syncwarp();
+        }
+    }
+    return true;
+}
+
+struct MergeWs {
+    double dfull[kEigMax], zfull[kEigMax], ds[kEigMax], zs[kEigMax];
+    double dk[kEigMax], zk[kEigMax], zh[kEigMax], tauk[kEigMax];
+    double ddf[kEigMax], vals[kEigMax];
+    double rc[kEigMax], rs[kEigMax];
+    int cs[kEigMax], ck[kEigMax], cdf[kEigMax], orgk[kEigMax], ri[kEigMax], rj[kEigMax], pos[kEigMax];
+    int k, ndf, nrot, sgn;
+    double rho, zsum2, zn2, dmax;
+};
+
+// The deferred top-level merge, finished by E3: output column c is
+// sum_j Z[:, ck[j]] U[j][src[c]] (src[c] < k) or Z[:, cdf[src[c] - k]].
+struct TopPlan {
+    int k;
+    int ck[kEigMax], cdf[kEigMax], src[kEigMax];
+};
+
+constexpr int kSecLanes = 8;  // lanes per secular root
+constexpr int kLeaves = 16;
+constexpr size_t kUsMax = kLeaves * sizeof(LeafWs) / sizeof(double);  // U staged over the leaf workspace
+
+__device__ __forceinline__ double group_sum(double v, unsigned mask) {
+    for (int o = kSecLanes / 2; o; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+    return v;
+}
+
+// Root i of 1 + rho sum_j z_j^2 / (d_j - lambda) = 0 (d ascending, rho > 0),
+// by a group of kSecLanes lanes: lambda = d_org + tau.
+__device__ bool secular_root(int i, int k, const double* dk, const double* zk, double rho, double zsum2,
+                             int sl, unsigned mask, int& org_out, double& tau_out) {
+    const bool last = i == k - 1;
+    // f and the pole-split derivatives at the bracket midpoint (relative to d_i)
+    const double w = last ? rho * zsum2 : dk[i + 1] - dk[i];
+    const double mid = 0.5 * w;
+    double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, eabs = 0.0;
+    for (int j = sl; j < k; j += kSecLanes) {
+        const double del = (dk[j] - dk[i]) - mid;
+        const double inv = 1.0 / del;
+        const double t = zk[j] * zk[j] * inv;
+        if (j <= i) { psi += t; dpsi = fma(t, inv, dpsi); }
+        else { phi += t; dphi = fma(t, inv, dphi); }
+        eabs += fabs(t);
+    }
+    psi = group_sum(psi, mask); dpsi = group_sum(dpsi, mask);
+    phi = group_sum(phi, mask); dphi = group_sum(dphi, mask);
+    eabs = group_sum(eabs, mask);
+    double f = 1.0 + rho * (psi + phi);
+    int org;
+    double lo, hi, tau;
+    if (last || f >= 0.0) { org = i; lo = 0.0; hi = mid; tau = mid; }
+    else { org = i + 1; lo = mid - w; hi = 0.0; tau = mid - w; }
+    if (last) { hi = w; }
+    const double dorg = dk[org];
+    const double di = dk[i] - dorg, di1 = last ? 0.0 : dk[i + 1] - dorg;
+    bool ok = false;
+    for (int it = 0; it < 200; ++it) {
+        if (it > 0) {
+            psi = dpsi = phi = dphi = eabs = 0.0;
+            for (int j = sl; j < k; j += kSecLanes) {
+                const double del = (dk[j] - dorg) - tau;
+                const double inv = 1.0 / del;
+                const double t = zk[j] * zk[j] * inv;
+                if (j <= i) { psi += t; dpsi = fma(t, inv, dpsi); }
+                else { phi += t; dphi = fma(t, inv, dphi); }
+                eabs += fabs(t);
+            }
+            psi = group_sum(psi, mask); dpsi = group_sum(dpsi, mask);
+            phi = group_sum(phi, mask); dphi = group_sum(dphi, mask);
+            eabs = group_sum(eabs, mask);
+            f = 1.0 + rho * (psi + phi);
+        }
+        if (fabs(f) <= 8.0 * DBL_EPSILON * (1.0 + rho * eabs) * double(k)) { ok = true; break; }
+        if (f < 0.0) lo = tau; else hi = tau;
+        if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) { ok = true; break; }
+        // two-pole rational model through (f, f') at tau, solved for the step eta
+        const double Di = di - tau;
+        double eta = 0.0;
+        bool good = false;
+        if (last) {
+            const double sp = rho * dpsi * Di * Di;
+            const double c = f - sp / Di;
+            if (c != 0.0) { eta = Di + sp / c; good = true; }
+        } else {
+            const double Di1 = di1 - tau;
+            const double sp = rho * dpsi * Di * Di, sf = rho * dphi * Di1 * Di1;
+            const double c = f - sp / Di - sf / Di1;
+            const double bq = c * (Di + Di1) + sp + sf, cq = f * Di * Di1;
+            if (c == 0.0) {
+                if (bq != 0.0) { eta = cq / bq; good = true; }
+            } else {
+                const double disc = bq * bq - 4.0 * c * cq;
+                if (disc >= 0.0) {
+                    const double q = 0.5 * (bq + copysign(sqrt(disc), bq));
+                    const double e1 = q / c, e2 = q != 0.0 ? cq / q : e1;
+                    const bool in1 = tau + e1 > lo && tau + e1 < hi, in2 = tau + e2 > lo && tau + e2 < hi;
+                    if (in1 && in2) eta = fabs(e1) < fabs(e2) ? e1 : e2;
+                    else eta = in1 ? e1 : e2;
+                    good = in1 || in2;
+                }
+            }
+        }
+        const double tn = tau + eta;
+        tau = (good && tn > lo && tn < hi) ? tn : 0.5 * (lo + hi);
+    }
+    org_out = org;
+    tau_out = tau;
+    return ok;
+}
+
+__device__ __forceinline__ void stamp(long long* clk, int slot) {
+    if (clk && threadIdx.x == 0) clk[slot] = clock64();
+}
+
+// merge of the adjacent blocks [s0, s0 + n1) and [s0 + n1, s0 + n1 + n2).
+// top != nullptr: the last merge; its eigenvector product is left to E3.
+__device__ bool merge_blocks(int n, int s0, int n1, int n2, double* Dc, const double* Eo, double* Z,
+                             double* Tmp, double* Ut, double* Us, MergeWs& M, TopPlan* top, long long* clk) {
+    const int tid = threadIdx.x;
+    const int sz = n1 + n2, p = s0 + n1;
+    const double rho0 = Eo[p - 1];
+    const int sgn = rho0 < 0.0 ? -1 : 1;
+    if (tid == 0) { M.zn2 = 0.0; M.dmax = 0.0; }
+    for (int j = tid; j < sz; j += kET) {
+        M.zfull[j] = j < n1 ? Z[(p - 1) + size_t(s0 + j) * n] : Z[p + size_t(s0 + j) * n];
+        M.dfull[j] = Dc[s0 + j];
+    }
+    __syncthreads();
+    // sorted order of sgn * d: position = rank in its own block + rank in the
+    // other (binary search; block 1 first on ties)
+    for (int j = tid; j < sz; j += kET) {
+        const bool b1 = j < n1;
+        const double key = sgn * M.dfull[j];
+        const int own = b1 ? (sgn > 0 ? j : n1 - 1 - j) : (sgn > 0 ? j - n1 : sz - 1 - j);
+        const int o0 = b1 ? n1 : 0, on = b1 ? n2 : n1;
+        int lo = 0, hi = on;  // count of other-block keys < key (b1) or <= key (b2)
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const int idx = o0 + (sgn > 0 ? mid : on - 1 - mid);
+            const double ok = sgn * M.dfull[idx];
+            if (b1 ? ok < key : ok <= key) lo = mid + 1; else hi = mid;
+        }
+        const int pos = own + lo;
+        M.ds[pos] = key;
+        M.zs[pos] = M.zfull[j];
+        M.cs[pos] = j;
+    }
+    if (tid < 32) {
+        double z2 = 0.0, dm = 0.0;
+        for (int j = tid; j < sz; j += 32) { z2 = fma(M.zfull[j], M.zfull[j], z2); dm = fmax(dm, fabs(M.dfull[j])); }
+        for (int o = 16; o; o >>= 1) {
+            z2 += __shfl_xor_sync(0xffffffffu, z2, o);
+            dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+        }
+        if (tid == 0) { M.zn2 = z2; M.dmax = dm; }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // deflation (LAPACK dlaed2 rules) over the sorted sequence; the
+        // rotation test only runs for nearly equal neighbours (|cs| <= 1/2)
+        const double rho = fabs(rho0) * M.zn2;
+        const double zinv = 1.0 / sqrt(M.zn2);
+        const double tol = 8.0 * DBL_EPSILON * fmax(M.dmax, rho);
+        int prev = -1;
+        double dprev = 0.0, zprev = 0.0;
+        int k = 0, ndf = 0, nrot = 0;
+        for (int q = 0; q < sz; ++q) {
+            const int j = M.cs[q];
+            const double dj = M.ds[q], zj = M.zs[q] * zinv;
+            if (rho * fabs(zj) <= tol) {
+                M.ddf[ndf] = dj; M.cdf[ndf] = j; ++ndf;
+                continue;
+            }
+            if (prev >= 0 && fabs(dj - dprev) <= 2.0 * tol) {
+                const double r = sqrt(fma(zprev, zprev, zj * zj));
+                const double c = zj / r, s = zprev / r;
+                if (fabs((dj - dprev) * c * s) <= tol) {
+                    // rotate (prev, j) so that z_prev = 0, then deflate prev
+                    M.ri[nrot] = prev; M.rj[nrot] = j; M.rc[nrot] = c; M.rs[nrot] = s; ++nrot;
+                    const double dp = c * c * dprev + s * s * dj, dn = s * s * dprev + c * c * dj;
+                    M.ddf[ndf] = dp; M.cdf[ndf] = prev; ++ndf;
+                    prev = j; dprev = dn; zprev = r;
+                    continue;
+                }
+            }
+            if (prev >= 0) { M.dk[k] = dprev; M.zk[k] = zprev; M.ck[k] = prev; ++k; }
+            prev = j; dprev = dj; zprev = zj;
+        }
+        if (prev >= 0) { M.dk[k] = dprev; M.zk[k] = zprev; M.ck[k] = prev; ++k; }
+        double zsum = 0.0;
+        for (int j = 0; j < k; ++j) zsum = fma(M.zk[j], M.zk[j], zsum);
+        M.k = k; M.ndf = ndf; M.nrot = nrot; M.sgn = sgn; M.rho = rho; M.zsum2 = zsum;
+    }
+    __syncthreads();
+    stamp(clk, 0);
+    const int k = M.k, ndf = M.ndf, nrot = M.nrot;
+    // Givens rotations of the deflation, in order, on the block's rows
+    if (nrot)
+        for (int r = tid; r < sz; r += kET) {
+            double* zr = Z + (s0 + r);
+            for (int t = 0; t < nrot; ++t) {
+                double& qi = zr[size_t(s0 + M.ri[t]) * n];
+                double& qj = zr[size_t(s0 + M.rj[t]) * n];
+                const double x = qi, y = qj, c = M.rc[t], s = M.rs[t];
+                qi = c * x - s * y;
+                qj = s * x + c * y;
+            }
+        }
+    // secular roots, kSecLanes lanes each
+    bool ok = true;
+    {
+        const int g = tid / kSecLanes, sl = tid % kSecLanes;
+        const unsigned mask = 0xffu << ((tid & 31) & ~(kSecLanes - 1));
+        for (int i = g; i < k; i += kET / kSecLanes) {
+            int org;
+            double tau;
+            const bool r = secular_root(i, k, M.dk, M.zk, M.rho, M.zsum2, sl, mask, org, tau);
+            if (sl == 0) { M.orgk[i] = org; M.tauk[i] = tau; }
+            ok = ok && r;
+        }
+    }
+    ok = __syncthreads_and(ok);
+    if (!ok) return false;
+    stamp(clk, 1);
+    // Gu-Eisenstat: zhat_j^2 = prod_i (lambda_i - d_j) / (rho prod_{i != j} (d_i - d_j)),
+    // one warp per j, lanes split the factors (fixed reduction tree)
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int j = warp; j < k; j += kET / 32) {
+        const double dj = M.dk[j];
+        double prod = 1.0;
+        for (int i = lane; i < k - 1; i += 32) {
+            const double lam = (M.dk[M.orgk[i]] - dj) + M.tauk[i];
+            prod *= lam / (i < j ? (M.dk[i] - dj) : (M.dk[i + 1] - dj));
+        }
+        for (int o = 16; o; o >>= 1) prod *= __shfl_xor_sync(0xffffffffu, prod, o);
+        prod *= ((M.dk[M.orgk[k - 1]] - dj) + M.tauk[k - 1]) / M.rho;
+        if (lane == 0) M.zh[j] = copysign(sqrt(fabs(prod)), M.zk[j]);
+    }
+    __syncthreads();
+    // eigenvectors of D + rho zhat zhat^T (row-major k x k U: U[j][i]), one
+    // warp per column i; into shared memory when the merge is finished here
+    double* U = (top || size_t(k) * k > kUsMax) ? Ut : Us;
+    for (int i = warp; i < k; i += kET / 32) {
+        const double dorg = M.dk[M.orgk[i]], tau = M.tauk[i];
+        double nrm = 0.0;
+        for (int j = lane; j < k; j += 32) {
+            const double u = M.zh[j] / ((M.dk[j] - dorg) - tau);
+            nrm = fma(u, u, nrm);
+        }
+        for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+        const double inv = 1.0 / sqrt(nrm);
+        for (int j = lane; j < k; j += 32) U[size_t(j) * k + i] = (M.zh[j] / ((M.dk[j] - dorg) - tau)) * inv;
+        if (lane == 0) M.vals[i] = M.sgn * (dorg + tau);
+    }
+    for (int t = tid; t < ndf; t += kET) M.vals[k + t] = M.sgn * M.ddf[t];
+    __syncthreads();
+    // ascending order of all sz eigenvalues (rank sort, ties by index)
+    for (int a = tid; a < sz; a += kET) {
+        const double va = M.vals[a];
+        int r = 0;
+        for (int b = 0; b < sz; ++b) {
+            const double vb = M.vals[b];
+            r += (vb < va) || (vb == va && b < a);
+        }
+        M.pos[a] = r;
+    }
+    __syncthreads();
+    stamp(clk, 2);
+    if (top) {  // last merge: hand the product to E3
+        for (int a = tid; a < sz; a += kET) {
+            top->src[M.pos[a]] = a;
+            if (a < k) top->ck[a] = M.ck[a];
+            else top->cdf[a - k] = M.cdf[a - k];
+            Dc[s0 + M.pos[a]] = M.vals[a];
+        }
+        if (tid == 0) top->k = k;
+        __syncthreads();
+        stamp(clk, 3);
+        stamp(clk, 4);
+        return true;
+    }
+    // new eigenvectors into Tmp (sz x sz, ld sz): kept = Z * U (8 columns of U
+    // per task, U row-major k x k), deflated = copy
+    const int ngrp = (k + 7) / 8;
+    for (int e = tid; e < sz * ngrp; e += kET) {
+        const int r = e % sz, a0 = (e / sz) * 8;
+        double acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+        const double* zr = Z + (s0 + r);
+        for (int j = 0; j < k; ++j) {
+            const double zv = zr[size_t(s0 + M.ck[j]) * n];
+            const double* u = U + size_t(j) * k + a0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (a0 + q < k) acc[q] = fma(zv, u[q], acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (a0 + q < k) Tmp[r + size_t(M.pos[a0 + q]) * sz] = acc[q];
+    }
+    for (int e = tid; e < sz * ndf; e += kET) {
+        const int r = e % sz, t = e / sz;
+        Tmp[r + size_t(M.pos[k + t]) * sz] = Z[(s0 + r) + size_t(s0 + M.cdf[t]) * n];
+    }
+    __syncthreads();
+    stamp(clk, 3);
+    for (int e = tid; e < sz * sz; e += kET) {
+        const int r = e % sz, c = e / sz;
+        Z[(s0 + r) + size_t(s0 + c) * n] = Tmp[e];
+    }
+    for (int a = tid; a < sz; a += kET) Dc[s0 + M.pos[a]] = M.vals[a];
+    __syncthreads();
+    stamp(clk, 4);
+    return true;
+}
+
+__global__ void __launch_bounds__(kET, 1)
+k_stedc(int n, const double* __restrict__ dg, const double* __restrict__ eo, double* __restrict__ Z,
+        double* __restrict__ Tmp, double* __restrict__ Ut, double* __restrict__ Dout, TopPlan* __restrict__ top,
+        int* __restrict__ info, long long* __restrict__ clk) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    MergeWs& M = *reinterpret_cast<MergeWs*>(smraw);
+    LeafWs* L = reinterpret_cast<LeafWs*>(smraw + ((sizeof(MergeWs) + 15) / 16) * 16);
+    __shared__ double Dc[kEigMax], Eo[kEigMax];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    stamp(clk, 0);
+    for (int i = tid; i < n; i += kET) {
+        Dc[i] = dg[i];
+        Eo[i] = i + 1 < n ? eo[i] : 0.0;
+    }
+    for (size_t e = tid; e < size_t(n) * n; e += kET) Z[e] = 0.0;
+    __syncthreads();
+    const int LB = (n + kLeaves - 1) / kLeaves, nleaf = (n + LB - 1) / LB;
+    if (tid == 0)
+        for (int b = 1; b < nleaf; ++b) {  // Cuppen tears at the leaf boundaries
+            const int p = b * LB;
+            Dc[p - 1] -= Eo[p - 1];
+            Dc[p] -= Eo[p - 1];
+        }
+    __syncthreads();
+    bool ok = true;
+    if (warp < nleaf) {
+        LeafWs& w = L[warp];
+        const int s = warp * LB, b = min(LB, n - s);
+        if (lane < b) {
+            w.d[lane] = Dc[s + lane];
+            w.e[lane] = lane + 1 < b ? Eo[s + lane] : 0.0;
+        }
+        __syncwarp();
+        ok = leaf_ql(b, w, lane);
+        if (ok) {
+            if (lane == 0) {  // ascending order (insertion sort of indices)
+                for (int i = 0; i < b; ++i) w.perm[i] = i;
+                for (int i = 1; i < b; ++i) {
+                    const int x = w.perm[i];
+                    int j = i - 1;
+                    while (j >= 0 && w.d[w.perm[j]] > w.d[x]) { w.perm[j + 1] = w.perm[j]; --j; }
+                    w.perm[j + 1] = x;
+                }
+            }
+            __syncwarp();
+            if (lane < b) {
+                for (int c = 0; c < b; ++c) Z[(s + lane) + size_t(s + c) * n] = w.z[lane][w.perm[c]];
+                Dc[s + lane] = w.d[w.perm[lane]];
+            }
+        }
+    }
+    ok = __syncthreads_and(ok);
+    if (!ok) {
+        if (tid == 0) *info = 1;
+        return;
+    }
+    stamp(clk, 1);
+    int mi = 0;
+    bool merged = false;
+    for (int width = LB; width < n; width *= 2) {
+        for (int s0 = 0; s0 + width < n; s0 += 2 * width) {
+            const int n1 = width, n2 = min(width, n - s0 - width);
+            const bool last = 2 * width >= n;
+            if (!merge_blocks(n, s0, n1, n2, Dc, Eo, Z, Tmp, Ut, reinterpret_cast<double*>(L), M, last ? top : nullptr,
+                              clk ? clk + 2 + 5 * mi : nullptr)) {
+                if (tid == 0) *info = 2;
+                return;
+            }
+            merged = merged || last;
+            ++mi;
+        }
+    }
+    if (!merged) {  // a single leaf: identity plan
+        for (int a = tid; a < n; a += kET) { top->src[a] = a; top->cdf[a] = a; }
+        if (tid == 0) top->k = 0;
+    }
+    for (int i = tid; i < n; i += kET) Dout[i] = Dc[i];
+}
+
+// ---------------------------------------------------------------- E3
+// V = H_0 H_1 ... H_{n-3} (Z U), 8 columns per CTA: first the deferred top
+// merge (kept columns: Z[:, ck] times the staged columns of U; deflated:
+// copies), then the reflectors, shared by the CTA's warps and staged through
+// shared memory one step ahead (cp.async).
+constexpr int kOrmWarps = 8;
+constexpr int kRefl = 4;  // reflectors per barrier
+__global__ void __launch_bounds__(kOrmWarps * 32)
+k_ormtr(const double* __restrict__ Hv, const double* __restrict__ tau, int n, const double* __restrict__ Z,
+        const double* __restrict__ Ut, const TopPlan* __restrict__ top, double* __restrict__ V,
+        const int* __restrict__ info) {
+    __shared__ double zs[kOrmWarps][kEigMax];
+    __shared__ double us[kOrmWarps][kEigMax];
+    __shared__ __align__(16) double hs[2][kRefl][kEigMax];
+    if (*info) return;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int c0 = blockIdx.x * kOrmWarps;
+    const int k = top->k;
+    // stage the U columns of this CTA's kept outputs
+    for (int e = tid; e < kOrmWarps * k; e += kOrmWarps * 32) {
+        const int q = e / k, j = e % k;
+        const int c = c0 + q;
+        const int a = c < n ? top->src[c] : k;
+        us[q][j] = a < k ? Ut[size_t(j) * k + a] : 0.0;
+    }
+    __syncthreads();
+    for (int r = tid; r < n; r += kOrmWarps * 32) {
+        double acc[kOrmWarps];
+#pragma unroll
+        for (int q = 0; q < kOrmWarps; ++q) acc[q] = 0.0;
+        for (int j = 0; j < k; ++j) {
+            const double zv = Z[r + size_t(top->ck[j]) * n];
+#pragma unroll
+            for (int q = 0; q < kOrmWarps; ++q) acc[q] = fma(zv, us[q][j], acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < kOrmWarps; ++q) {
+            const int c = c0 + q;
+            if (c >= n) break;
+            const int a = top->src[c];
+            zs[q][r] = a < k ? acc[q] : Z[r + size_t(top->cdf[a - k]) * n];
+        }
+    }
+    __syncthreads();
+    const int c = c0 + w;
+    double* z = zs[w];
+    // reflectors n-3 .. 0 in groups of kRefl, double buffered
+    auto stage = [&](int g, int buf) {
+        const int jhi = n - 3 - g * kRefl;
+        for (int q = 0; q < kRefl; ++q) {
+            const int j = jhi - q;
+            if (j < 0) break;
+            const int t = n - j - 1;
+            for (int i = tid; i < t; i += kOrmWarps * 32) {
+                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&hs[buf][q][i]));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(Hv + size_t(j) * n + i));
+            }
+        }
+        asm volatile("cp.async.commit_group;\n");
+    };
+    const int ngroups = n >= 3 ? (n - 3) / kRefl + 1 : 0;
+    if (ngroups) stage(0, 0);
+    for (int g = 0; g < ngroups; ++g) {
+        const int buf = g & 1;
+        if (g + 1 < ngroups) {
+            stage(g + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n");
+        }
+        __syncthreads();
+        if (c < n) {
+            const int jhi = n - 3 - g * kRefl;
+            for (int q = 0; q < kRefl; ++q) {
+                const int j = jhi - q;
+                if (j < 0) break;
+                const double tj = tau[j];
+                if (tj == 0.0) continue;
+                const double* hv = hs[buf][q];
+                const int t = n - j - 1;
+                double dot = 0.0;
+                for (int i = lane; i < t; i += 32) dot = fma(hv[i], z[j + 1 + i], dot);
+                for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                const double f = tj * dot;
+                for (int i = lane; i < t; i += 32) z[j + 1 + i] = fma(-f, hv[i], z[j + 1 + i]);
+                __syncwarp();
+            }
+        }
+        __syncthreads();  // hs[buf] is restaged two groups later
+    }
+    if (c < n)
+        for (int i = lane; i < n; i += 32) V[i + size_t(c) * n] = z[i];
+}
+
+size_t stedc_smem() { return ((sizeof(MergeWs) + 15) / 16) * 16 + kLeaves * sizeof(LeafWs); }
+
+}  // namespace
+
+// Eigenvalues ascending into d_D and eigenvectors over B (column-major), as
+// syevd. Returns false (B untouched) when n is too large or a stage did not
+// converge; the caller then uses cuSOLVER.
+bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>& h_D) {
+    if (n64 < 1 || n64 > kEigMax) return false;
+    const int n = int(n64);
+    cudaStream_t s = c.stream;
+    static bool attr = false;
+    if (!attr) {
+        FB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(double) * (kEigMax * (kEigMax + 1) / 2 + 2 * kEigMax))));
+        FB_CUDA(cudaFuncSetAttribute(k_stedc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(stedc_smem())));
+        attr = true;
+    }
+    const size_t nn = size_t(n) * n;
+    DBuf<double> ws(nn + 3 * size_t(n) + 3 * nn, s);
+    double* H = ws.get();
+    double* tau = H + nn;
+    double* dg = tau + n;
+    double* eo = dg + n;
+    double* Z = eo + n;
+    double* Tmp = Z + nn;
+    double* Ut = Tmp + nn;
+    DBuf<int> info(1, s);
+    DBuf<unsigned char> topbuf(sizeof(TopPlan), s);
+    TopPlan* top = reinterpret_cast<TopPlan*>(topbuf.get());
+    FB_CUDA(cudaMemsetAsync(info.get(), 0, sizeof(int), s));
+    static const bool timing = std::getenv("FRPCA_EIG_TIMING") != nullptr;
+    DBuf<long long> clk(timing ? 128 : 0, s);
+    if (timing) FB_CUDA(cudaMemsetAsync(clk.get(), 0, clk.bytes(), s));
+    {
+        Prof p1(c, "syev_sytrd", 0, 0);
+        k_sytrd<<<1, kET, sizeof(double) * (size_t(n) * (n + 1) / 2 + 2 * kEigMax), s>>>(B, n, H, tau, dg, eo);
+        FB_LAUNCH_CHECK();
+    }
+    {
+        Prof p2(c, "syev_stedc", 0, 0);
+        k_stedc<<<1, kET, stedc_smem(), s>>>(n, dg, eo, Z, Tmp, Ut, d_D, top, info.get(), clk.get());
+        FB_LAUNCH_CHECK();
+    }
+    {
+        Prof p3(c, "syev_ormtr", 0, 0);
+        k_ormtr<<<(n + kOrmWarps - 1) / kOrmWarps, kOrmWarps * 32, 0, s>>>(H, tau, n, Z, Ut, top, B, info.get());
+        FB_LAUNCH_CHECK();
+    }
+    int h_info = 0;
+    h_D.resize(size_t(n));
+    FB_CUDA(cudaMemcpyAsync(&h_info, info.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaMemcpyAsync(h_D.data(), d_D, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaStreamSynchronize(s));
+    if (timing) {
+        long long h[128];
+        FB_CUDA(cudaMemcpy(h, clk.get(), sizeof(h), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "stedc n=%d leaves %lld", n, h[1] - h[0]);
+        long long prev = h[1];
+        for (int m = 0; m < 25 && h[2 + 5 * m + 4]; ++m) {
+            std::fprintf(stderr, " | m%d", m);
+            for (int q = 0; q < 5; ++q) { std::fprintf(stderr, " %lld", h[2 + 5 * m + q] - prev); prev = h[2 + 5 * m + q]; }
+        }
+        std::fprintf(stderr, "\n");
+    }
+    return h_info == 0;
+}
+
+}  // namespace fb

@@ -274,3 +274,55 @@ def test_eig_svd_property(fb, orc, seed):  # test_dense_kernels.cpp:174-186
     assert orthonormality(U) < 1e-10 and orthonormality(V) < 1e-12
     assert np.all(np.diff(S) >= 0) and S[0] >= 0
     assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-10
+
+
+def _with_spectrum(orc, m, s, seed):
+    """m x n matrix with singular values s (any order) and random singular vectors."""
+    n = s.size
+    Q1, _ = np.linalg.qr(orc.gaussian_matrix(m, n, seed))
+    Q2, _ = np.linalg.qr(orc.gaussian_matrix(n, n, seed + 1))
+    return (Q1 * s) @ Q2.T
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 16, 17, 31, 33, 64, 100, 150, 200, 231, 232, 233, 300])
+def test_eig_solver_sizes(fb, orc, monkeypatch, n):
+    """The library's l <= 232 eigensolver (syev.cu: tridiagonalisation, divide
+    and conquer, back-transformation) at every leaf/merge shape; larger n goes
+    to cuSOLVER. FRPCA_EIG=strict turns a silent fallback into a failure."""
+    monkeypatch.setenv("FRPCA_EIG", "strict")
+    A = orc.gaussian_matrix(3 * n + 5, n, 40 + n)
+    U, S, V = fb.eig_svd(A)
+    Sn = np.linalg.svd(A, compute_uv=False)[::-1]
+    assert np.max(np.abs(S - Sn) / Sn) < 1e-12
+    assert orthonormality(V) < 1e-12 and orthonormality(U) < 1e-10
+    assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ["repeated", "clusters", "graded", "two_values", "near_rank"])
+@pytest.mark.parametrize("n", [40, 200])
+def test_eig_solver_hard_spectra(fb, orc, monkeypatch, kind, n):
+    """Repeated and clustered eigenvalues exercise the deflation of the merges
+    (both rotation and small-z deflation); a graded spectrum over 6 decades
+    (12 in the Gram) the secular solver near its poles."""
+    monkeypatch.setenv("FRPCA_EIG", "strict")
+    rng = np.random.default_rng(n)
+    if kind == "repeated":
+        s = np.ones(n)
+    elif kind == "clusters":
+        s = np.repeat([1.0, 2.0, 3.0, 5.0], n // 4) * (1 + 1e-13 * rng.standard_normal(n))
+    elif kind == "graded":
+        s = 10.0 ** np.linspace(0, -6, n)
+    elif kind == "two_values":
+        s = np.where(np.arange(n) % 2 == 0, 1.0, 1e-3)
+    else:
+        s = np.concatenate([np.linspace(1, 2, n - 3), [1e-6, 2e-6, 3e-6]])
+    A = _with_spectrum(orc, 4 * n, s, 7 + n)
+    U, S, V = fb.eig_svd(A)
+    Sn = np.sort(s)
+    # eigenvalues of the Gram to ~eps*||B||: singular values to eps*smax^2/s
+    tol = 1e-13 * (Sn[-1] ** 2) / Sn
+    assert np.all(np.abs(S - Sn) <= np.maximum(tol, 1e-12 * Sn))
+    assert orthonormality(V) < 1e-12
+    top = Sn >= 0.1 * Sn[-1]
+    assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-10
+    assert orthonormality(U[:, top]) < 1e-10
