@@ -24,6 +24,8 @@
 #include <cooperative_groups.h>
 
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -33,7 +35,6 @@ namespace fb {
 namespace {
 
 constexpr int NB = 32;
-constexpr int kT = 256;
 
 struct Cand {
     double v;
@@ -49,6 +50,7 @@ __device__ __forceinline__ void cand_merge(Cand& c, const Cand& o) {
 }
 
 // block-wide reduction; the result is returned to every thread
+template <int kT>
 __device__ Cand block_best(Cand c, Cand* sh) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int o = 16; o; o >>= 1) {
@@ -66,9 +68,10 @@ __device__ Cand block_best(Cand c, Cand* sh) {
     return r;
 }
 
+template <int kT>
 __global__ void __launch_bounds__(kT, 1)
 k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ P,
-     int32_t* __restrict__ pos, Cand* __restrict__ cand, int* __restrict__ err) {
+     int32_t* __restrict__ pos, Cand* __restrict__ cand, int* __restrict__ err, long long* __restrict__ clk) {
     extern __shared__ double smem[];
     double* U12 = smem;                     // NB x l (trailing part used)
     double* L11 = U12 + NB * l;             // NB x NB
@@ -90,7 +93,7 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
             for (int t = 0; t < bw; ++t) P[int64_t(t) * m + i] = wr[t];
             cand_merge(c, Cand{fabs(wr[0]), int32_t(i), int32_t(i)});
         }
-        c = block_best(c, shc);
+        c = block_best<kT>(c, shc);
         if (threadIdx.x == 0) cand[blockIdx.x] = c;
     }
 
@@ -98,11 +101,15 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
         const int bw = min(NB, l - jb);
         for (int jj = 0; jj < bw; ++jj) {
             const int j = jb + jj;
+            const bool tim = clk && j == 100 && blockIdx.x == 0 && threadIdx.x == 0;
+            if (tim) clk[0] = clock64();
             grid.sync();
+            if (tim) clk[1] = clock64();
             // every CTA reduces the candidates identically
             Cand c{-1.0, INT32_MAX, -1};
             for (int k = threadIdx.x; k < nblk; k += kT) cand_merge(c, cand[k]);
-            const Cand best = block_best(c, shc);
+            const Cand best = block_best<kT>(c, shc);
+            if (tim) clk[2] = clock64();
             if (!(best.v > tol) || best.row < 0) {  // zero pivot (:81)
                 if (blockIdx.x == 0 && threadIdx.x == 0) *err = 1;
                 return;  // uniform across the grid
@@ -111,6 +118,7 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
             if (threadIdx.x < bw) u[threadIdx.x] = P[int64_t(threadIdx.x) * m + pr];
             if (threadIdx.x == 0) prow[jj] = pr;
             __syncthreads();
+            if (tim) clk[3] = clock64();
             const double d = u[jj];
             Cand nc{-1.0, INT32_MAX, -1};
             for (int64_t i = gtid; i < m; i += nthr) {
@@ -147,10 +155,12 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
                     if (jj + 1 < bw) cand_merge(nc, Cand{fabs(nv), p, int32_t(i)});
                 }
             }
+            if (tim) clk[4] = clock64();
             if (jj + 1 < bw) {
-                nc = block_best(nc, shc);
+                nc = block_best<kT>(nc, shc);
                 if (threadIdx.x == 0) cand[blockIdx.x] = nc;
             }
+            if (tim) clk[5] = clock64();
         }
         const int c0 = jb + bw, tcols = l - c0;
         grid.sync();  // the last column's update of every pivot row is visible
@@ -217,11 +227,181 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
             }
         }
         if (tcols > 0) {
-            nc = block_best(nc, shc);
+            nc = block_best<kT>(nc, shc);
             if (threadIdx.x == 0) cand[blockIdx.x] = nc;
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory-resident variant (m <= ~119k at l = 200, e.g. C1's n x l
+// panel): CTA b owns the contiguous rows [b R, (b+1) R) and keeps their 32
+// panel columns in shared memory, so a column step touches no global memory
+// but the candidates. Each CTA publishes its best candidate together with
+// that row's remaining panel values, so after the grid barrier the pivot row
+// is one load away. Trailing columns are solved/updated in chunks of UCH
+// (last chunk first, so the chunk holding the next panel is done last and
+// can overwrite the panel). Same arithmetic, in the same order, as k_lu.
+constexpr int UCH = 64;
+
+template <int kT>
+__global__ void __launch_bounds__(kT, 1)
+k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* __restrict__ pos_g,
+          Cand* __restrict__ cand, double* __restrict__ cvals, int* __restrict__ err, long long* __restrict__ clk) {
+    extern __shared__ double smem[];
+    double* Ps = smem;                      // NB x R (column t at Ps + t R)
+    double* U12 = Ps + size_t(NB) * R;      // NB x UCH
+    double* L11 = U12 + NB * UCH;           // NB x (NB + 1)
+    double* u = L11 + NB * (NB + 1);        // NB
+    int32_t* posS = reinterpret_cast<int32_t*>(u + NB);  // R
+    __shared__ Cand shc[kT / 32];
+    __shared__ int32_t prow[NB];
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x;
+    const int64_t r0 = int64_t(blockIdx.x) * R;
+    const int64_t rem = m - r0;
+    const int nr = rem <= 0 ? 0 : (rem < R ? int(rem) : R);
+
+    auto publish = [&](Cand c, int width) {  // after a block_best (Ps final)
+        if (tid == 0) cand[blockIdx.x] = c;
+        if (tid < width) cvals[size_t(blockIdx.x) * NB + tid] = c.row >= 0 ? Ps[size_t(tid) * R + (c.row - r0)] : 0.0;
+    };
+    {
+        const int bw = min(NB, l);
+        Cand c{-1.0, INT32_MAX, -1};
+        for (int r = tid; r < nr; r += kT) {
+            const int64_t i = r0 + r;
+            posS[r] = int32_t(i);
+            const double* wr = W + i * l;
+            for (int t = 0; t < bw; ++t) Ps[size_t(t) * R + r] = wr[t];
+            cand_merge(c, Cand{fabs(wr[0]), int32_t(i), int32_t(i)});
+        }
+        c = block_best<kT>(c, shc);
+        publish(c, bw);
+    }
+    for (int jb = 0; jb < l; jb += NB) {
+        const int bw = min(NB, l - jb);
+        for (int jj = 0; jj < bw; ++jj) {
+            const int j = jb + jj;
+            const bool tim = clk && j == 100 && blockIdx.x == 0 && tid == 0;
+            if (tim) clk[0] = clock64();
+            grid.sync();
+            if (tim) clk[1] = clock64();
+            Cand c{-1.0, INT32_MAX, -1};
+            for (int k = tid; k < int(gridDim.x); k += kT) cand_merge(c, cand[k]);
+            const Cand best = block_best<kT>(c, shc);
+            if (!(best.v > tol) || best.row < 0) {  // zero pivot (:81)
+                if (blockIdx.x == 0 && tid == 0) *err = 1;
+                return;  // uniform across the grid
+            }
+            if (tim) clk[2] = clock64();
+            const int32_t pr = best.row, pb = best.pos;
+            if (tid < bw) u[tid] = cvals[size_t(pr / R) * NB + tid];
+            if (tid == 0) prow[jj] = pr;
+            __syncthreads();
+            if (tim) clk[3] = clock64();
+            const double d = u[jj];
+            Cand nc{-1.0, INT32_MAX, -1};
+            for (int r = tid; r < nr; r += kT) {
+                const int64_t i = r0 + r;
+                int32_t p = posS[r];
+                if (i == pr) {
+                    posS[r] = j;
+                    continue;
+                }
+                if (p == j) {  // displaced by the interchange (:82-85)
+                    p = pb;
+                    posS[r] = p;
+                }
+                if (p > j) {
+                    double* pc = Ps + r;
+                    const double mi = pc[size_t(jj) * R] / d;  // :88
+                    pc[size_t(jj) * R] = mi;
+                    double nv = 0.0;
+                    if (jj + 1 < bw) {
+                        nv = pc[size_t(jj + 1) * R] - mi * u[jj + 1];
+                        pc[size_t(jj + 1) * R] = nv;
+                    }
+#pragma unroll 4
+                    for (int t = jj + 2; t < bw; ++t)  // :89-92
+                        pc[size_t(t) * R] = pc[size_t(t) * R] - mi * u[t];
+                    if (jj + 1 < bw) cand_merge(nc, Cand{fabs(nv), p, int32_t(i)});
+                }
+            }
+            if (tim) clk[4] = clock64();
+            if (jj + 1 < bw) {
+                nc = block_best<kT>(nc, shc);
+                publish(nc, bw);
+            }
+            if (tim) clk[5] = clock64();
+        }
+        if (clk && blockIdx.x == 0 && tid == 0 && jb == 64) clk[6] = clock64();
+        // finished panel of the own rows back to W (L of P^T L; L11 / A12 source)
+        for (int e = tid; e < nr * bw; e += kT) {
+            const int r = e % nr, t = e / nr;
+            if (posS[r] >= jb) W[(r0 + r) * l + jb + t] = Ps[size_t(t) * R + r];
+        }
+        const int c0 = jb + bw, tcols = l - c0;
+        grid.sync();
+        if (tcols <= 0) break;
+        for (int e = tid; e < bw * bw; e += kT) {
+            const int t = e / bw, s2 = e % bw;
+            L11[t * (NB + 1) + s2] = W[int64_t(prow[t]) * l + jb + s2];
+        }
+        const int nbw = min(NB, tcols);
+        const int nch = (tcols + UCH - 1) / UCH;
+        Cand nc{-1.0, INT32_MAX, -1};
+        for (int ch = nch - 1; ch >= 0; --ch) {
+            const int cc0 = ch * UCH, cw = min(UCH, tcols - cc0);
+            __syncthreads();  // L11 staged / previous chunk's U12 consumed
+            for (int e = tid; e < bw * cw; e += kT) {
+                const int t = e / cw, cc = e % cw;
+                U12[t * UCH + cc] = W[int64_t(prow[t]) * l + c0 + cc0 + cc];
+            }
+            __syncthreads();
+            for (int cc = tid; cc < cw; cc += kT)  // U12 = L11^{-1} A12, column by column
+                for (int t = 1; t < bw; ++t) {
+                    double acc = U12[t * UCH + cc];
+                    for (int s2 = 0; s2 < t; ++s2) acc -= L11[t * (NB + 1) + s2] * U12[s2 * UCH + cc];
+                    U12[t * UCH + cc] = acc;
+                }
+            __syncthreads();
+            for (int r = tid; r < nr; r += kT) {
+                const int32_t p = posS[r];
+                if (p < c0) continue;  // pivot of this or an earlier panel
+                double* wr = W + (r0 + r) * l;
+                double Lr[NB];
+#pragma unroll
+                for (int t = 0; t < NB; ++t)
+                    if (t < bw) Lr[t] = Ps[size_t(t) * R + r];
+                for (int cb = 0; cb < cw; cb += 8) {
+                    double a[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (cb + e < cw) a[e] = wr[c0 + cc0 + cb + e];
+#pragma unroll
+                    for (int t = 0; t < NB; ++t)
+                        if (t < bw) {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e)
+                                if (cb + e < cw) a[e] -= Lr[t] * U12[t * UCH + cb + e];
+                        }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (cb + e < cw) {
+                            wr[c0 + cc0 + cb + e] = a[e];
+                            if (cc0 + cb + e < nbw) Ps[size_t(cc0 + cb + e) * R + r] = a[e];
+                        }
+                }
+                if (ch == 0) cand_merge(nc, Cand{fabs(Ps[r]), p, int32_t(r0 + r)});
+            }
+        }
+        nc = block_best<kT>(nc, shc);
+        publish(nc, nbw);
+        if (clk && blockIdx.x == 0 && tid == 0 && jb == 64) clk[7] = clock64();
+    }
+    for (int r = tid; r < nr; r += kT) pos_g[r0 + r] = posS[r];
 }
 
 __global__ void k_assemble(double* __restrict__ W, int64_t m, int l, const int32_t* __restrict__ pos) {
@@ -245,34 +425,83 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
     cudaStream_t s = c.stream;
     const double maxabs = maxabs_device(c, W, m * l);
     const double tol = double(l) * DBL_EPSILON * maxabs;
-    const size_t smem = sizeof(double) * (size_t(NB) * size_t(l) + NB * (NB + 1) + NB);
-    static int attr_set = 0;
-    if (smem > 48 * 1024 || !attr_set) {
-        FB_CUDA(cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(std::max<size_t>(smem, 48 * 1024))));
-        attr_set = 1;
-    }
-    int per_sm = 0;
-    FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu, kT, smem));
-    require(per_sm >= 1, "lu_basis: panel width too large for one CTA's shared memory");
-    int grid = std::max(1, std::min<int>(per_sm * c.num_sms, int((m + kT - 1) / kT)));
     DBuf<int32_t> pos(size_t(m), s);
     DBuf<int> err(1, s);
-    DBuf<Cand> cand(size_t(grid), s);
-    DBuf<double> P(size_t(m) * NB, s);
     FB_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(int), s));
     int L = int(l);
-    double* Pp = P.get();
     int32_t* posp = pos.get();
-    Cand* candp = cand.get();
     int* errp = err.get();
-    void* args[] = {&W, &m, &L, const_cast<double*>(&tol), &Pp, &posp, &candp, &errp};
-    FB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_lu), dim3(grid), dim3(kT), args, smem, s));
+    // shared-memory-resident panel when the rows fit one CTA per SM
+    constexpr int kTS = 512;
+    const int R = int((m + c.num_sms - 1) / c.num_sms);
+    const size_t smem_s = sizeof(double) * (size_t(NB) * R + NB * UCH + NB * (NB + 1) + NB) + sizeof(int32_t) * R;
+    const bool no_smem = std::getenv("FRPCA_LU_GLOBAL") != nullptr;  // tests compare both kernels
+    if (!no_smem && smem_s <= 220 * 1024) {
+        FB_CUDA(cudaFuncSetAttribute(k_lu_smem<kTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
+        int per_sm = 0;
+        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu_smem<kTS>, kTS, smem_s));
+        if (per_sm >= 1) {
+            const int grid = int((m + R - 1) / R);
+            DBuf<Cand> cand(size_t(grid), s);
+            DBuf<double> cvals(size_t(grid) * NB, s);
+            Cand* candp = cand.get();
+            double* cvp = cvals.get();
+            const bool timing = std::getenv("FRPCA_LU_TIMING") != nullptr;
+            DBuf<long long> clk(timing ? 8 : 0, s);
+            long long* clkp = clk.get();
+            void* args[] = {&W, &m, &L, const_cast<double*>(&tol), const_cast<int*>(&R), &posp, &candp, &cvp, &errp,
+                            &clkp};
+            FB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_lu_smem<kTS>), dim3(grid), dim3(kTS), args,
+                                                smem_s, s));
+            count_launch();
+            int h_err = 0;
+            FB_CUDA(cudaMemcpyAsync(&h_err, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+            FB_CUDA(cudaStreamSynchronize(s));
+            if (h_err) throw NumericalError("lu_basis: zero pivot, input is rank-deficient");
+            if (timing) {
+                long long h[8];
+                FB_CUDA(cudaMemcpy(h, clk.get(), sizeof(h), cudaMemcpyDeviceToHost));
+                std::fprintf(stderr, "lu_smem step 100 (cycles): sync %lld cand %lld u %lld rows %lld best %lld | panel end %lld\n",
+                             h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4], h[7] - h[6]);
+            }
+            const int agrid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms * 16, (m * l + 255) / 256)));
+            k_assemble<<<agrid, 256, 0, s>>>(W, m, L, pos.get());
+            FB_LAUNCH_CHECK();
+            return;
+        }
+    }
+    const size_t smem = sizeof(double) * (size_t(NB) * size_t(l) + NB * (NB + 1) + NB);
+    static const int kT = [] {
+        const char* e = std::getenv("FRPCA_LU_THREADS");
+        return e && std::atoi(e) == 512 ? 512 : 256;
+    }();
+    void* kfn = kT == 256 ? reinterpret_cast<void*>(k_lu<256>) : reinterpret_cast<void*>(k_lu<512>);
+    FB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(std::max<size_t>(smem, 48 * 1024))));
+    int per_sm = 0;
+    FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kT, smem));
+    require(per_sm >= 1, "lu_basis: panel width too large for one CTA's shared memory");
+    int grid = std::max(1, std::min<int>(per_sm * c.num_sms, int((m + kT - 1) / kT)));
+    DBuf<Cand> cand(size_t(grid), s);
+    DBuf<double> P(size_t(m) * NB, s);
+    double* Pp = P.get();
+    Cand* candp = cand.get();
+    static const bool timing = std::getenv("FRPCA_LU_TIMING") != nullptr;
+    DBuf<long long> clk(timing ? 8 : 0, s);
+    long long* clkp = clk.get();
+    void* args[] = {&W, &m, &L, const_cast<double*>(&tol), &Pp, &posp, &candp, &errp, &clkp};
+    FB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kT), args, smem, s));
     count_launch();
     int h_err = 0;
     FB_CUDA(cudaMemcpyAsync(&h_err, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     FB_CUDA(cudaStreamSynchronize(s));
     if (h_err) throw NumericalError("lu_basis: zero pivot, input is rank-deficient");
+    if (timing) {
+        long long h[8];
+        FB_CUDA(cudaMemcpy(h, clk.get(), sizeof(long long) * 6, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "lu step 100 (cycles): sync %lld cand %lld u %lld rows %lld best %lld\n", h[1] - h[0],
+                     h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4]);
+    }
     const int agrid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms * 16, (m * l + 255) / 256)));
     k_assemble<<<agrid, 256, 0, s>>>(W, m, L, pos.get());
     FB_LAUNCH_CHECK();

@@ -326,3 +326,15 @@ def test_eig_solver_hard_spectra(fb, orc, monkeypatch, kind, n):
     top = Sn >= 0.1 * Sn[-1]
     assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-10
     assert orthonormality(U[:, top]) < 1e-10
+
+
+@pytest.mark.parametrize("m,l", [(40, 8), (1000, 33), (20000, 200), (100000, 200), (130000, 150)])
+def test_lu_smem_equals_global_kernel(fb, orc, monkeypatch, m, l):
+    """The shared-memory-resident LU (rows fit one CTA per SM) performs the
+    same operations in the same order as the global-panel kernel: bitwise
+    equal results; sizes on both sides of the residency limit."""
+    M = orc.gaussian_matrix(m, l, 3 * m + l)
+    X1 = fb.lu_basis(M)
+    monkeypatch.setenv("FRPCA_LU_GLOBAL", "1")
+    X2 = fb.lu_basis(M)
+    assert np.array_equal(X1, X2)
