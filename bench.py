@@ -336,7 +336,7 @@ def run_gpu_arm(args, cfg):
 
     # ---- roofline of the SpMM kernels (algorithmic bytes / measured launch time)
     hbm_peak, peak_kind = measured_peaks()
-    sp = [v for kname, v in prof.items() if kname.startswith("spmm")]
+    sp = [v for kname, v in prof.items() if kname in ("spmm_AX", "spmm_AtY")]  # sub-tags are nested
     sp_bytes = sum(v["bytes"] for v in sp)
     sp_ms = sum(v["ms"] for v in sp)
     sp_launches = sum(v["launches"] for v in sp)

@@ -337,7 +337,9 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
             if (tim) clk[5] = clock64();
         }
         if (clk && blockIdx.x == 0 && tid == 0 && jb == 64) clk[6] = clock64();
-        // finished panel of the own rows back to W (L of P^T L; L11 / A12 source)
+        // finished panel of the own rows back to W (L of P^T L; L11 / A12 source);
+        // a different thread <-> row map than the column steps: barrier first
+        __syncthreads();
         for (int e = tid; e < nr * bw; e += kT) {
             const int r = e % nr, t = e / nr;
             if (posS[r] >= jb) W[(r0 + r) * l + jb + t] = Ps[size_t(t) * R + r];

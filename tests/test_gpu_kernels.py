@@ -328,13 +328,20 @@ def test_eig_solver_hard_spectra(fb, orc, monkeypatch, kind, n):
     assert orthonormality(U[:, top]) < 1e-10
 
 
-@pytest.mark.parametrize("m,l", [(40, 8), (1000, 33), (20000, 200), (100000, 200), (130000, 150)])
+@pytest.mark.parametrize("m,l", [(40, 8), (1000, 33), (4000, 40), (4000, 200), (20000, 200), (100000, 200),
+                                 (130000, 150)])
 def test_lu_smem_equals_global_kernel(fb, orc, monkeypatch, m, l):
     """The shared-memory-resident LU (rows fit one CTA per SM) performs the
     same operations in the same order as the global-panel kernel: bitwise
     equal results; sizes on both sides of the residency limit."""
     M = orc.gaussian_matrix(m, l, 3 * m + l)
-    X1 = fb.lu_basis(M)
-    monkeypatch.setenv("FRPCA_LU_GLOBAL", "1")
-    X2 = fb.lu_basis(M)
-    assert np.array_equal(X1, X2)
+    # rows scaled over 16 decades and 20% zero rows (pipeline-like Z)
+    rng = np.random.default_rng(m + l)
+    M2 = M * (10.0 ** rng.uniform(-8, 8, size=(m, 1)))
+    M2[rng.choice(m, m // 5, replace=False)] = 0.0
+    for X in (M, M2):
+        monkeypatch.delenv("FRPCA_LU_GLOBAL", raising=False)
+        X1 = fb.lu_basis(X)
+        monkeypatch.setenv("FRPCA_LU_GLOBAL", "1")
+        X2 = fb.lu_basis(X)
+        assert np.array_equal(X1, X2)
