@@ -8,6 +8,8 @@
 // (16 MMAs per k4 step from 8 operand loads), operands are staged in padded
 // shared memory by a 2-stage cp.async pipeline, and split-K partials are
 // reduced in a fixed order so results are deterministic run to run.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace fb {
@@ -253,6 +255,129 @@ __global__ void k_gram2_reduce(const double* __restrict__ part, int nparts, int 
     }
 }
 
+// Gram v3: one warp per 5x5 block of 8x8 tiles of the lower triangle (NBR
+// block rows, NBR(NBR+1)/2 warps), straight-line: per k4 step a warp loads 5
+// (diagonal block) or 10 operand fragments and issues 15 or 25 DMMAs. Rows are
+// split over CTAs and staged through shared memory (2-stage cp.async); the
+// partial tiles use k_gram2's layout and fixed-order reduction.
+constexpr int G3_BT = 5;
+constexpr int G3_ROWS = 32;
+
+template <int NBR>
+__global__ void __launch_bounds__(NBR * (NBR + 1) / 2 * 32, 1)
+k_gram3(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_cta, double* __restrict__ part) {
+    extern __shared__ __align__(16) double sm[];  // [2][G3_ROWS][S], S >= 40 NBR
+    constexpr int NW = NBR * (NBR + 1) / 2;
+    const int T = (n + 7) / 8;
+    const int NT = T * (T + 1) / 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int bi = 0;
+    while ((bi + 1) * (bi + 2) / 2 <= warp) ++bi;
+    const int bj = warp - bi * (bi + 1) / 2;
+    const bool diag = bi == bj;
+    const int64_t rs = int64_t(blockIdx.x) * rows_per_cta;
+    const int64_t re = min(r, rs + rows_per_cta);
+    const int ncol = 8 * G3_BT * NBR;  // staged columns (zero beyond n)
+    double acc[G3_BT][G3_BT][2];
+#pragma unroll
+    for (int a = 0; a < G3_BT; ++a)
+#pragma unroll
+        for (int b = 0; b < G3_BT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    auto load = [&](int stage, int64_t k0) {
+        double* dst = sm + size_t(stage) * G3_ROWS * S;
+        const int per_row = n / 2;  // n even (caller)
+        for (int e = tid; e < G3_ROWS * per_row; e += NW * 32) {
+            const int kr = e / per_row, cc = (e % per_row) * 2;
+            const int64_t row = k0 + kr;
+            const bool v = row < re;
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + kr * S + cc));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
+                         "l"(W + (v ? row * n + cc : 0)), "r"(v ? 16 : 0));
+        }
+        for (int e = tid; e < G3_ROWS * (ncol - n); e += NW * 32) {
+            const int kr = e / (ncol - n), cc = n + e % (ncol - n);
+            dst[kr * S + cc] = 0.0;
+        }
+        cp_async_commit();
+    };
+    const int64_t nsteps = (re - rs + G3_ROWS - 1) / G3_ROWS;
+    if (nsteps > 0) load(0, rs);
+    const int coff = (lane & 3) * S + (lane >> 2);
+    for (int64_t st = 0; st < nsteps; ++st) {
+        const int stage = int(st & 1);
+        if (st + 1 < nsteps) {
+            load(stage ^ 1, rs + (st + 1) * G3_ROWS);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* Ws = sm + size_t(stage) * G3_ROWS * S + coff;
+        if (diag) {
+#pragma unroll
+            for (int kk = 0; kk < G3_ROWS / 4; ++kk) {
+                const double* rowp = Ws + kk * 4 * S + bi * 40;
+                double f[G3_BT];
+#pragma unroll
+                for (int a = 0; a < G3_BT; ++a) f[a] = rowp[a * 8];
+#pragma unroll
+                for (int a = 0; a < G3_BT; ++a)
+#pragma unroll
+                    for (int b = 0; b <= a; ++b) dmma(acc[a][b], f[a], f[b]);
+            }
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < G3_ROWS / 4; ++kk) {
+                const double* rowp = Ws + kk * 4 * S;
+                double fa[G3_BT];
+#pragma unroll
+                for (int a = 0; a < G3_BT; ++a) fa[a] = rowp[bi * 40 + a * 8];
+#pragma unroll
+                for (int b = 0; b < G3_BT; ++b) {
+                    const double fb = rowp[bj * 40 + b * 8];
+#pragma unroll
+                    for (int a = 0; a < G3_BT; ++a) dmma(acc[a][b], fa[a], fb);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    double* out = part + size_t(blockIdx.x) * NT * 64;
+    const int ii = lane >> 2, jj = (lane & 3) * 2;
+#pragma unroll
+    for (int a = 0; a < G3_BT; ++a)
+#pragma unroll
+        for (int b = 0; b < G3_BT; ++b) {
+            const int ti = bi * G3_BT + a, tj = bj * G3_BT + b;
+            if (ti >= T || tj > ti || (diag && b > a)) continue;
+            const int t = ti * (ti + 1) / 2 + tj;
+            *reinterpret_cast<double2*>(out + size_t(t) * 64 + ii * 8 + jj) = make_double2(acc[a][b][0], acc[a][b][1]);
+        }
+}
+
+template <int NBR>
+void launch_gram3(Ctx& c, const double* W, int64_t r, int n, double* B) {
+    constexpr int NW = NBR * (NBR + 1) / 2;
+    const int T = (n + 7) / 8, NT = T * (T + 1) / 2;
+    const int ncol = 8 * G3_BT * NBR;
+    const int S = ncol + ((12 - (ncol % 16)) + 16) % 16;
+    const size_t smem = sizeof(double) * 2 * G3_ROWS * S;
+    static bool attr = false;
+    if (!attr) {
+        FB_CUDA(cudaFuncSetAttribute(k_gram3<NBR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = true;
+    }
+    int64_t nctas = std::min<int64_t>(c.num_sms, std::max<int64_t>(1, (r + G3_ROWS - 1) / G3_ROWS));
+    const int64_t rpc = ((r + nctas - 1) / nctas + G3_ROWS - 1) / G3_ROWS * G3_ROWS;
+    nctas = std::max<int64_t>(1, (r + rpc - 1) / rpc);
+    DBuf<double> part(size_t(nctas) * NT * 64, c.stream);
+    k_gram3<NBR><<<unsigned(nctas), NW * 32, smem, c.stream>>>(W, r, n, S, rpc, part.get());
+    FB_LAUNCH_CHECK();
+    const int outs = NT * 64;
+    k_gram2_reduce<<<(outs + 255) / 256, 256, 0, c.stream>>>(part.get(), int(nctas), n, B);
+    FB_LAUNCH_CHECK();
+}
+
 template <int MAXT>
 void launch_gram2(Ctx& c, const double* W, int64_t r, int n, double* B) {
     const int T = (n + 7) / 8, NT = T * (T + 1) / 2;
@@ -451,15 +576,16 @@ k_gemm_tall(const double* __restrict__ W, int64_t r, int K, const double* __rest
 
 // Persistent variant for tall W: the whole column chunk of M (K x NP, NP <= 104)
 // stays in shared memory for the CTA's lifetime and W is streamed through once
-// (M is read once per SM instead of once per 64-row block).
+// (M is read once per SM instead of once per 64-row block). 8 warps, each
+// owning RT x NT tiles (RT A and NT B fragments per k4 step for RT*NT DMMAs).
 constexpr int PCOLS = 104;
-constexpr int GP_THREADS = 512;
-template <int NT>
+constexpr int GP_THREADS = 256;
+template <int RT, int NT>
 __global__ void __launch_bounds__(GP_THREADS, 1)
 k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __restrict__ M, int ldm,
                int N, double* __restrict__ C, int64_t ldc, int col_major, int WC, int SB) {
     extern __shared__ __align__(16) double sm[];
-    const int BM = 16 * ((GP_THREADS / 32) / WC);
+    const int BM = 8 * RT * ((GP_THREADS / 32) / WC);
     const int ntiles = (N + 7) / 8;
     const int NP = 8 * ntiles;
     double* Ms = sm;                                  // [K][SB]
@@ -486,9 +612,9 @@ k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __r
     const int64_t nblocks = (r + BM - 1) / BM;
     for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
         const int64_t r0 = blk * BM;
-        double acc[2][NT][2];
+        double acc[RT][NT][2];
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
+        for (int a = 0; a < RT; ++a)
 #pragma unroll
             for (int t = 0; t < NT; ++t) acc[a][t][0] = acc[a][t][1] = 0.0;
         load(0, r0, 0);
@@ -501,28 +627,30 @@ k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __r
                 cp_async_wait<0>();
             }
             __syncthreads();
-            const double* wd = Ws + stage * BM * TSA + (rg * 16 + (lane >> 2)) * TSA + (lane & 3);
+            const double* wd = Ws + stage * BM * TSA + (rg * 8 * RT + (lane >> 2)) * TSA + (lane & 3);
             const double* md = Ms + (st * TK + (lane & 3)) * SB + cgp * NT * 8 + (lane >> 2);
 #pragma unroll
             for (int kk = 0; kk < TK / 4; ++kk) {
                 if (st * TK + kk * 4 >= K) break;
-                const double a0 = wd[kk * 4], a1 = wd[8 * TSA + kk * 4];
+                double fa[RT];
+#pragma unroll
+                for (int a = 0; a < RT; ++a) fa[a] = wd[a * 8 * TSA + kk * 4];
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
                     if (cgp * NT + t < ntiles) {
                         const double b = md[kk * 4 * SB + t * 8];
-                        dmma(acc[0][t], a0, b);
-                        dmma(acc[1][t], a1, b);
+#pragma unroll
+                        for (int a = 0; a < RT; ++a) dmma(acc[a][t], fa[a], b);
                     }
                 }
             }
             __syncthreads();
         }
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
+        for (int a = 0; a < RT; ++a)
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                const int64_t row = r0 + rg * 16 + a * 8 + (lane >> 2);
+                const int64_t row = r0 + rg * 8 * RT + a * 8 + (lane >> 2);
                 const int col = (cgp * NT + t) * 8 + (lane & 3) * 2;
                 if (row >= r || cgp * NT + t >= ntiles) continue;
 #pragma unroll
@@ -535,24 +663,24 @@ k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __r
     }
 }
 
-template <int NT>
+template <int RT, int NT>
 void launch_gemm_persist(Ctx& c, const double* W, int64_t r, int64_t K, const double* M, int64_t ldm,
                          int64_t N, double* C, int64_t ldc, bool col_major_out, int WC) {
     const int ntiles = int((N + 7) / 8), NP = 8 * ntiles;
     const int SB = NP + ((12 - (NP % 16)) + 16) % 16;
-    const int BM = 16 * ((GP_THREADS / 32) / WC);
+    const int BM = 8 * RT * ((GP_THREADS / 32) / WC);
     const int Kp = int((K + TK - 1) / TK) * TK;
     const size_t smem = sizeof(double) * (size_t(Kp) * SB + 2 * size_t(BM) * TSA);
     static bool attr = false;
     if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_gemm_persist<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        FB_CUDA(cudaFuncSetAttribute(k_gemm_persist<RT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024));
         attr = true;
     }
     const int64_t nblocks = (r + BM - 1) / BM;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, nblocks)));
-    k_gemm_persist<NT><<<grid, GP_THREADS, smem, c.stream>>>(W, r, int(K), M, int(ldm), int(N), C, ldc,
-                                                     col_major_out ? 1 : 0, WC, SB);
+    k_gemm_persist<RT, NT><<<grid, GP_THREADS, smem, c.stream>>>(W, r, int(K), M, int(ldm), int(N), C, ldc,
+                                                          col_major_out ? 1 : 0, WC, SB);
     FB_LAUNCH_CHECK();
 }
 
@@ -604,6 +732,13 @@ void gram_device(Ctx& c, const double* W, int64_t r, int64_t n, double* B) {
     Prof prof(c, "gram", 8.0 * r * n, double(r) * n * (n + 1));
     if (n <= 224 && r > 0) {
         const int T = int((n + 7) / 8), NT = T * (T + 1) / 2;
+        const bool g2 = std::getenv("FRPCA_GRAM2") != nullptr;  // tests compare both kernels
+        if (!g2 && n % 2 == 0 && r >= 4096) {
+            const int nbr = (T + G3_BT - 1) / G3_BT;
+            if (nbr == 5) return launch_gram3<5>(c, W, r, int(n), B);
+            if (nbr == 4) return launch_gram3<4>(c, W, r, int(n), B);
+            if (nbr == 3) return launch_gram3<3>(c, W, r, int(n), B);
+        }
         const int maxt = (NT + G2_WARPS - 1) / G2_WARPS;
         if (maxt <= 2) return launch_gram2<2>(c, W, r, int(n), B);
         if (maxt <= 4) return launch_gram2<4>(c, W, r, int(n), B);
@@ -639,9 +774,9 @@ void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M,
             const int ntiles = int((nc + 7) / 8);
             const int WC = ntiles <= 8 ? 1 : 2;
             const int nt = (ntiles + WC - 1) / WC;
-            if (nt <= 2) launch_gemm_persist<2>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
-            else if (nt <= 4) launch_gemm_persist<4>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
-            else launch_gemm_persist<7>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+            if (nt <= 2) launch_gemm_persist<4, 2>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+            else if (nt <= 4) launch_gemm_persist<4, 4>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+            else launch_gemm_persist<4, 7>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
         }
         return;
     }

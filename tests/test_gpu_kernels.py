@@ -345,3 +345,16 @@ def test_lu_smem_equals_global_kernel(fb, orc, monkeypatch, m, l):
         monkeypatch.setenv("FRPCA_LU_GLOBAL", "1")
         X2 = fb.lu_basis(X)
         assert np.array_equal(X1, X2)
+
+
+@pytest.mark.parametrize("m,n", [(5000, 200), (100000, 200), (20000, 150), (9000, 96), (30000, 88)])
+def test_gram3_equals_gram2(fb, orc, monkeypatch, m, n):
+    """The register-blocked Gram (k_gram3) issues the same DMMAs per output
+    tile in the same row order as k_gram2: eig_svd results are bitwise equal."""
+    A = orc.gaussian_matrix(m, n, m + 3 * n)
+    monkeypatch.delenv("FRPCA_GRAM2", raising=False)
+    r1 = fb.eig_svd(A)
+    monkeypatch.setenv("FRPCA_GRAM2", "1")
+    r2 = fb.eig_svd(A)
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
