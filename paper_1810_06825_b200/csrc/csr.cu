@@ -458,7 +458,7 @@ void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap) {
     // chunks short enough that the slowest in-flight chunk does not let the
     // work front run many panels ahead (the window must stay L2-resident)
     const char* ec = std::getenv("FRPCA_PANEL_CHUNK");
-    const int64_t pch = std::max<int64_t>(16, ec ? std::atoll(ec) : 128);
+    const int64_t pch = std::max<int64_t>(16, ec ? std::atoll(ec) : 256);
     DBuf<int32_t> flag(size_t(n) + 1, s), pos(size_t(n) + 1, s);
     P.skip.alloc(size_t(n), s);
     int64_t thot = 3 * npan, nhot = 0, nitems = 0;
