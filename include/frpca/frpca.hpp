@@ -4,7 +4,8 @@
 // (/root/reference/proj/include/frpca/{types,sparse_matrix,dense_kernels,randsvd}.hpp)
 // for Scalar = double: same namespace, names, argument conventions and
 // exceptions, so code written against the reference's frpca(), frpcat(),
-// auto_pca(), spmm(), spmm_transpose(), lu_basis(), eig_svd(),
+// auto_pca(), basic_rpca(), basic_rpcat(), spmm(), spmm_transpose(),
+// lu_basis(), orth(), eig_svd(),
 // gaussian_matrix() compiles against this header and runs on a B200.
 //
 // What differs, by necessity: Eigen is not available, so Matrix<double> /
@@ -309,6 +310,15 @@ Matrix<Scalar> lu_basis(const Matrix<Scalar>& M) {
     return X;
 }
 
+// dense_kernels.hpp:30-48
+template <typename Scalar>
+Matrix<Scalar> orth(const Matrix<Scalar>& M) {
+    detail::require(M.rows() >= M.cols() && M.cols() >= 1, "orth: input must be tall (rows >= cols >= 1)");
+    Matrix<Scalar> Q(M.rows(), M.cols());
+    detail::check(frpca_orth(b200::Context::default_context().get(), M.rows(), M.cols(), M.data(), Q.data()));
+    return Q;
+}
+
 template <typename Scalar>
 struct EigSvdResult {  // dense_kernels.hpp:136-143
     Matrix<Scalar> U;
@@ -371,7 +381,8 @@ SvdResult<Scalar> run(int algo, const SparseMatrixCsr<Scalar>& A, const PcaConfi
     out.V = Matrix<Scalar>(A.cols(), k);
     Matrix<Scalar> basis;
     const bool want_basis = stats && stats->capture_basis && l >= 1;
-    if (want_basis) basis = Matrix<Scalar>(eff == FRPCA_ALGO_FRPCA ? A.rows() : A.cols(), l);
+    if (want_basis)
+        basis = Matrix<Scalar>(eff == FRPCA_ALGO_FRPCA || eff == FRPCA_ALGO_BASIC_RPCA ? A.rows() : A.cols(), l);
     frpca_stats st{};
     detail::check(frpca_run(ctx.get(), A.device(ctx), algo, &c, omega ? omega->data() : nullptr,
                             omega ? omega->rows() : 0, omega ? omega->cols() : 0, out.U.data(),
@@ -387,6 +398,22 @@ SvdResult<Scalar> run(int algo, const SparseMatrixCsr<Scalar>& A, const PcaConfi
     return out;
 }
 }  // namespace detail
+
+// randsvd.hpp:99-102
+template <typename Scalar>
+SvdResult<Scalar> basic_rpca(const SparseMatrixCsr<Scalar>& A, const PcaConfig& cfg,
+                             std::type_identity_t<RunStats<Scalar>>* stats = nullptr,
+                             const std::type_identity_t<Matrix<Scalar>>* omega = nullptr) {
+    return detail::run<Scalar>(FRPCA_ALGO_BASIC_RPCA, A, cfg, stats, omega, nullptr);
+}
+
+// randsvd.hpp:139-142
+template <typename Scalar>
+SvdResult<Scalar> basic_rpcat(const SparseMatrixCsr<Scalar>& A, const PcaConfig& cfg,
+                              std::type_identity_t<RunStats<Scalar>>* stats = nullptr,
+                              const std::type_identity_t<Matrix<Scalar>>* omega = nullptr) {
+    return detail::run<Scalar>(FRPCA_ALGO_BASIC_RPCAT, A, cfg, stats, omega, nullptr);
+}
 
 // randsvd.hpp:229-232
 template <typename Scalar>

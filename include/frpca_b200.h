@@ -39,6 +39,8 @@ extern "C" {
 #define FRPCA_ALGO_FRPCA 0  /* Alg. 5, rows <= cols (randsvd.hpp:224-276) */
 #define FRPCA_ALGO_FRPCAT 1 /* Alg. 6, rows >= cols (randsvd.hpp:278-328) */
 #define FRPCA_ALGO_AUTO 2   /* shape dispatch (randsvd.hpp:330-351) */
+#define FRPCA_ALGO_BASIC_RPCA 3  /* baseline, sketch on the right (randsvd.hpp:95-134) */
+#define FRPCA_ALGO_BASIC_RPCAT 4 /* baseline, sketch on the left (randsvd.hpp:136-175) */
 
 /* frpca_run flags */
 #define FRPCA_FLAG_DEVICE_IO 1u   /* omega/U/S/V/basis pointers are device pointers */
@@ -120,6 +122,9 @@ int frpca_gaussian_matrix(frpca_ctx* ctx, int64_t rows, int64_t cols, uint64_t s
                           double* out);
 /* lu_basis (dense_kernels.hpp:50-116): X = P^T L of M (m x l, m >= l). */
 int frpca_lu_basis(frpca_ctx* ctx, int64_t m, int64_t l, const double* M, double* X);
+/* orth (dense_kernels.hpp:30-48): Q (m x l, column-major) of the Householder
+ * QR of M; rank deficiency (|diag R| <= m eps max) -> FRPCA_ERR_NUMERICAL. */
+int frpca_orth(frpca_ctx* ctx, int64_t m, int64_t l, const double* M, double* Q);
 /* eig_svd (dense_kernels.hpp:145-174): U m x n, S ascending (n), V n x n. */
 int frpca_eig_svd(frpca_ctx* ctx, int64_t m, int64_t n, const double* A, double* U, double* S,
                   double* V);

@@ -579,6 +579,144 @@ static Svd frpcat(const Csr& A, const Config& cfg, Stats* stats, const Mat* omeg
     return out;
 }
 
+// ---- orth (dense_kernels.hpp:30-48): Householder QR, Q = H_0..H_{l-1} I ----
+// Eigen::HouseholderQR: per column, makeHouseholderInPlace (beta = -sign(c0)
+// ||x||, tau = (beta - c0) / beta, v = [1; tail / (c0 - beta)]), applied to
+// the trailing columns; rank check on |diag R| <= m eps max|diag R| (:41-44);
+// householderQ() * Identity(m, l) (:46).
+static Mat orth(const Mat& Min) {
+    const Index m = Min.rows, l = Min.cols;
+    require(m >= l && l >= 1, "orth: input must be tall (rows >= cols >= 1)");
+    Mat A = Min;
+    std::vector<double> tau(size_t(l), 0.0), diag(size_t(l), 0.0);
+    for (Index j = 0; j < l; ++j) {
+        double* x = A.col(j) + j;
+        const Index t = m - j;
+        double tail = 0.0;
+        for (Index i = 1; i < t; ++i) tail += x[i] * x[i];
+        const double c0 = x[0];
+        double beta, tj;
+        if (tail <= std::numeric_limits<double>::min()) {
+            tj = 0.0;
+            beta = c0;
+            for (Index i = 1; i < t; ++i) x[i] = 0.0;
+        } else {
+            beta = std::sqrt(c0 * c0 + tail);
+            if (c0 >= 0.0) beta = -beta;
+            const double inv = 1.0 / (c0 - beta);
+            for (Index i = 1; i < t; ++i) x[i] *= inv;
+            tj = (beta - c0) / beta;
+        }
+        x[0] = beta;
+        diag[size_t(j)] = beta;
+        tau[size_t(j)] = tj;
+        if (tj != 0.0) {
+            parallel_for(j + 1, l, [&](Index c) {  // independent columns
+                double* y = A.col(c) + j;
+                double d = y[0];
+                for (Index i = 1; i < t; ++i) d += x[i] * y[i];
+                d *= tj;
+                y[0] -= d;
+                for (Index i = 1; i < t; ++i) y[i] -= d * x[i];
+            });
+        }
+    }
+    double maxd = 0.0;
+    for (double d : diag) maxd = std::max(maxd, std::fabs(d));
+    const double tol = double(m) * std::numeric_limits<double>::epsilon() * maxd;
+    bool bad = maxd == 0.0;
+    for (double d : diag) bad = bad || std::fabs(d) <= tol;
+    if (bad) throw NumericalError("orth: numerically rank-deficient input");
+    Mat Q(m, l);
+    for (Index j = 0; j < l; ++j) Q(j, j) = 1.0;
+    for (Index j = l - 1; j >= 0; --j) {
+        const double tj = tau[size_t(j)];
+        if (tj == 0.0) continue;
+        const double* x = A.col(j) + j;
+        const Index t = m - j;
+        parallel_for(j, l, [&](Index c) {
+            double* y = Q.col(c) + j;
+            double d = y[0];
+            for (Index i = 1; i < t; ++i) d += x[i] * y[i];
+            d *= tj;
+            y[0] -= d;
+            for (Index i = 1; i < t; ++i) y[i] -= d * x[i];
+        });
+    }
+    return Q;
+}
+
+// basic_rpca, randsvd.hpp:95-134 (sketch on the right, QR after every product)
+static Svd basic_rpca(const Csr& A, const Config& cfg, Stats* stats, const Mat* omega, Mat* basis) {
+    check_common(cfg);
+    require(cfg.power >= 0, "basic_rpca: power p must be >= 0");
+    const Index l = cfg.k + cfg.oversample;
+    require(l <= std::min(A.rows, A.cols), "basic_rpca: k + oversample must be <= min(rows, cols)");
+    const uint64_t passes0 = A.passes.load();
+    auto t0 = Clock::now();
+    Mat Omega = sketch_matrix(A.cols, l, cfg, omega);
+    Mat Q = orth(spmm_m(A, Omega));
+    const double t_sketch = since(t0);
+    t0 = Clock::now();
+    for (Index i = 0; i < cfg.power; ++i) {
+        Mat G = orth(spmmT_m(A, Q));
+        Q = orth(spmm_m(A, G));
+    }
+    const double t_power = since(t0);
+    t0 = Clock::now();
+    // economic_svd_short_fat(B), B = (A^T Q)^T: eig_svd(A^T Q) reversed (dense_kernels.hpp:179-190)
+    EigSvd f = eig_svd(spmmT_m(A, Q));
+    const Index s = cfg.oversample;
+    Svd out;
+    out.U = gemm(Q, cols_reversed(f.V, s, cfg.k));
+    out.V = cols_reversed(f.U, s, cfg.k);
+    out.S.resize(size_t(cfg.k));
+    for (Index t = 0; t < cfg.k; ++t) out.S[size_t(t)] = f.S[size_t(s + cfg.k - 1 - t)];
+    if (stats) {
+        stats->sketch_seconds = t_sketch;
+        stats->power_seconds = t_power;
+        stats->finalize_seconds = since(t0);
+        stats->passes_over_matrix = A.passes.load() - passes0;
+    }
+    if (basis) *basis = Q;
+    return out;
+}
+
+// basic_rpcat, randsvd.hpp:136-175 (sketch on the left)
+static Svd basic_rpcat(const Csr& A, const Config& cfg, Stats* stats, const Mat* omega, Mat* basis) {
+    check_common(cfg);
+    require(cfg.power >= 0, "basic_rpcat: power p must be >= 0");
+    const Index l = cfg.k + cfg.oversample;
+    require(l <= std::min(A.rows, A.cols), "basic_rpcat: k + oversample must be <= min(rows, cols)");
+    const uint64_t passes0 = A.passes.load();
+    auto t0 = Clock::now();
+    Mat Omega = sketch_matrix(l, A.rows, cfg, omega);
+    Mat Q = orth(spmmT_m(A, transpose_dense(Omega)));
+    const double t_sketch = since(t0);
+    t0 = Clock::now();
+    for (Index i = 0; i < cfg.power; ++i) {
+        Mat G = orth(spmm_m(A, Q));
+        Q = orth(spmmT_m(A, G));
+    }
+    const double t_power = since(t0);
+    t0 = Clock::now();
+    EigSvd f = eig_svd(spmm_m(A, Q));  // B = (A Q)^T
+    const Index s = cfg.oversample;
+    Svd out;
+    out.U = cols_reversed(f.U, s, cfg.k);
+    out.V = gemm(Q, cols_reversed(f.V, s, cfg.k));
+    out.S.resize(size_t(cfg.k));
+    for (Index t = 0; t < cfg.k; ++t) out.S[size_t(t)] = f.S[size_t(s + cfg.k - 1 - t)];
+    if (stats) {
+        stats->sketch_seconds = t_sketch;
+        stats->power_seconds = t_power;
+        stats->finalize_seconds = since(t0);
+        stats->passes_over_matrix = A.passes.load() - passes0;
+    }
+    if (basis) *basis = Q;
+    return out;
+}
+
 // ---- validation oracle: one-sided Jacobi SVD (validation.hpp:34-121) -------
 static void oracle_svd(const Mat& Ain, Mat& U, std::vector<double>& S, Mat& V) {
     require(Ain.rows >= 1 && Ain.cols >= 1, "oracle_svd: empty matrix");
@@ -747,6 +885,12 @@ int orc_lu_basis(int64_t m, int64_t l, const double* M, double* X) {
         std::memcpy(X, R.d.data(), sizeof(double) * R.d.size());
     });
 }
+int orc_orth(int64_t m, int64_t l, const double* M, double* Q) {
+    return guarded([&] {
+        Mat R = orth(view_colmajor(M, m, l, m));
+        std::memcpy(Q, R.d.data(), sizeof(double) * R.d.size());
+    });
+}
 int orc_eig_svd(int64_t m, int64_t n, const double* A, double* U, double* S, double* V) {
     return guarded([&] {
         EigSvd r = eig_svd(view_colmajor(A, m, n, m));
@@ -780,7 +924,8 @@ int orc_oracle_svd(int64_t m, int64_t n, const double* A, double* U, double* S, 
     });
 }
 
-// algorithm: 0 = frpca, 1 = frpcat, 2 = auto (randsvd.hpp:330-351)
+// algorithm: 0 = frpca, 1 = frpcat, 2 = auto (randsvd.hpp:330-351),
+// 3 = basic_rpca, 4 = basic_rpcat (randsvd.hpp:95-175)
 // omega: optional column-major injected sketch (om_rows x om_cols).
 // U: rows x k, S: k, V: cols x k (column-major). basis: optional copy of Q.
 int orc_pca(void* h, int algorithm, int64_t k, int64_t oversample, int64_t passes, int64_t power,
@@ -799,7 +944,9 @@ int orc_pca(void* h, int algorithm, int64_t k, int64_t oversample, int64_t passe
         if (algo == 2) algo = (A.rows < A.cols) ? 0 : 1;
         if (dispatched) *dispatched = algo;
         if (algo == 0) r = frpca(A, cfg, &st, omp, basis ? &Q : nullptr);
-        else r = frpcat(A, cfg, &st, omp, basis ? &Q : nullptr);
+        else if (algo == 1) r = frpcat(A, cfg, &st, omp, basis ? &Q : nullptr);
+        else if (algo == 3) r = basic_rpca(A, cfg, &st, omp, basis ? &Q : nullptr);
+        else r = basic_rpcat(A, cfg, &st, omp, basis ? &Q : nullptr);
         std::memcpy(U, r.U.d.data(), sizeof(double) * r.U.d.size());
         std::memcpy(S, r.S.data(), sizeof(double) * r.S.size());
         std::memcpy(V, r.V.d.data(), sizeof(double) * r.V.d.size());

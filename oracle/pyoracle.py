@@ -61,6 +61,7 @@ def lib():
         L.orc_spmm.argtypes = [_vp, _dp, _i64, _i64, _dp]
         L.orc_spmm_transpose.argtypes = [_vp, _dp, _i64, _i64, _dp]
         L.orc_lu_basis.argtypes = [_i64, _i64, _dp, _dp]
+        L.orc_orth.argtypes = [_i64, _i64, _dp, _dp]
         L.orc_eig_svd.argtypes = [_i64, _i64, _dp, _dp, _dp, _dp]
         L.orc_eig_sym.argtypes = [_i64, _dp, _dp, _dp]
         L.orc_gram_lower.argtypes = [_i64, _i64, _dp, _dp]
@@ -236,7 +237,16 @@ def oracle_svd(A: np.ndarray):
     return U, S, V
 
 
-FRPCA, FRPCAT, AUTO = 0, 1, 2
+FRPCA, FRPCAT, AUTO, BASIC_RPCA, BASIC_RPCAT = 0, 1, 2, 3, 4
+
+
+def orth(M: np.ndarray) -> np.ndarray:
+    """dense_kernels.hpp:30-48: Householder QR basis of range(M), with the
+    rank-deficiency check."""
+    M = np.asfortranarray(M, dtype=np.float64)
+    Q = np.empty(M.shape, order="F")
+    _check(lib().orc_orth(M.shape[0], M.shape[1], _d(M), _d(Q)))
+    return Q
 
 
 def pca(A: Csr, algorithm: int, k: int, oversample: int = 5, passes: int = 2, seed: int = 0,
@@ -253,7 +263,7 @@ def pca(A: Csr, algorithm: int, k: int, oversample: int = 5, passes: int = 2, se
     S = np.empty(kk)
     V = np.empty((A.cols, kk), order="F")
     stats = np.zeros(4)
-    qrows = A.rows if algo == FRPCA else A.cols
+    qrows = A.rows if algo in (FRPCA, BASIC_RPCA) else A.cols
     basis = np.empty((qrows, max(l, 0)), order="F") if want_basis else None
     disp = C.c_int(-1)
     om_p, om_r, om_c = None, 0, 0

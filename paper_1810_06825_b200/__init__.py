@@ -26,8 +26,8 @@ from ._lib import NumericalError, CudaError  # noqa: F401
 __all__ = [
     "SparseMatrixCsr", "PcaConfig", "RunStats", "SvdResult", "AutoPcaResult", "PcaAlgorithm",
     "NumericalError", "CudaError", "Context", "default_context",
-    "spmm", "spmm_transpose", "transpose", "gaussian_matrix", "lu_basis", "eig_svd",
-    "frpca", "frpcat", "auto_pca", "mix_seed", "kSketchStreamTag",
+    "spmm", "spmm_transpose", "transpose", "gaussian_matrix", "lu_basis", "orth", "eig_svd",
+    "frpca", "frpcat", "auto_pca", "basic_rpca", "basic_rpcat", "mix_seed", "kSketchStreamTag",
 ]
 
 kSketchStreamTag = 0xA11CE  # randsvd.hpp:63
@@ -43,10 +43,12 @@ def mix_seed(seed: int, tag: int) -> int:
 
 
 class PcaAlgorithm(enum.IntEnum):
-    """randsvd.hpp:14 (only the fast algorithms are on this path)."""
+    """randsvd.hpp:14 (eig_svds, the dense Gram baseline, is not provided)."""
     Frpca = _lib.ALGO_FRPCA
     Frpcat = _lib.ALGO_FRPCAT
     Auto = _lib.ALGO_AUTO
+    BasicRpca = _lib.ALGO_BASIC_RPCA
+    BasicRpcat = _lib.ALGO_BASIC_RPCAT
 
 
 @dataclasses.dataclass
@@ -396,6 +398,17 @@ def lu_basis(M, ctx: Context | None = None) -> np.ndarray:
     return X
 
 
+def orth(M, ctx: Context | None = None) -> np.ndarray:
+    """dense_kernels.hpp:30-48: Householder-QR basis of range(M) (tall M);
+    raises NumericalError when |diag R| <= m eps max|diag R|."""
+    M = _colmajor(M)
+    ctx = ctx or default_context()
+    m, l = M.shape
+    Q = np.empty((m, l), order="F")
+    _lib.check(_lib.load().frpca_orth(ctx._h, m, l, _ptr(M), _ptr(Q)))
+    return Q
+
+
 def eig_svd(A, ctx: Context | None = None):
     """dense_kernels.hpp:145-174: returns (U, S ascending, V) of tall full-rank A."""
     A = _colmajor(A)
@@ -421,7 +434,7 @@ def _run(algo: int, A: SparseMatrixCsr, cfg: PcaConfig, stats: RunStats | None, 
     V = np.empty((n, k), order="F")
     basis = None
     if stats is not None and stats.capture_basis and l >= 1:
-        basis = np.empty((m if eff == _lib.ALGO_FRPCA else n, l), order="F")
+        basis = np.empty((m if eff in (_lib.ALGO_FRPCA, _lib.ALGO_BASIC_RPCA) else n, l), order="F")
     om = None if omega is None else _colmajor(omega)
     st = _lib.FrpcaStats()
     disp = C.c_int(-1)
@@ -450,6 +463,19 @@ def frpcat(A: SparseMatrixCsr, cfg: PcaConfig, stats: RunStats | None = None, om
            ctx: Context | None = None) -> SvdResult:
     """Alg. 6 (randsvd.hpp:278-328), rows >= cols."""
     return _run(_lib.ALGO_FRPCAT, A, cfg, stats, omega, ctx)[0]
+
+
+def basic_rpca(A: SparseMatrixCsr, cfg: PcaConfig, stats: RunStats | None = None, omega=None,
+               ctx: Context | None = None) -> SvdResult:
+    """Baseline randomized PCA, sketch on the right (randsvd.hpp:95-134):
+    Householder QR after every product, 2p + 2 passes (cfg.power = p)."""
+    return _run(_lib.ALGO_BASIC_RPCA, A, cfg, stats, omega, ctx)[0]
+
+
+def basic_rpcat(A: SparseMatrixCsr, cfg: PcaConfig, stats: RunStats | None = None, omega=None,
+                ctx: Context | None = None) -> SvdResult:
+    """Baseline with the sketch on the left (randsvd.hpp:136-175)."""
+    return _run(_lib.ALGO_BASIC_RPCAT, A, cfg, stats, omega, ctx)[0]
 
 
 def auto_pca(A: SparseMatrixCsr, cfg: PcaConfig, stats: RunStats | None = None,

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libfrpca_b200.so")
 
 OK, ERR_INVALID, ERR_IO, ERR_NUMERICAL, ERR_CUDA = 0, 2, 3, 4, 5
-ALGO_FRPCA, ALGO_FRPCAT, ALGO_AUTO = 0, 1, 2
+ALGO_FRPCA, ALGO_FRPCAT, ALGO_AUTO, ALGO_BASIC_RPCA, ALGO_BASIC_RPCAT = 0, 1, 2, 3, 4
 FLAG_DEVICE_IO, FLAG_HOST_OMEGA = 1, 2
 
 _i64, _u64, _i32, _u32 = C.c_int64, C.c_uint64, C.c_int32, C.c_uint32
@@ -53,6 +53,7 @@ SIGNATURES = {
     "frpca_spmm": (C.c_int, [_vp, _vp, C.c_int, _vp, _i64, _i64, _vp]),
     "frpca_gaussian_matrix": (C.c_int, [_vp, _i64, _i64, _u64, _vp]),
     "frpca_lu_basis": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
+    "frpca_orth": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
     "frpca_eig_svd": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "frpca_run": (C.c_int, [_vp, _vp, C.c_int, C.POINTER(FrpcaConfig), _vp, _i64, _i64,
                             _vp, _vp, _vp, _vp, C.POINTER(FrpcaStats), C.POINTER(C.c_int)]),

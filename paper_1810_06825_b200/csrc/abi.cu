@@ -322,6 +322,19 @@ int frpca_lu_basis(frpca_ctx* c, int64_t m, int64_t l, const double* Mh, double*
     });
 }
 
+int frpca_orth(frpca_ctx* c, int64_t m, int64_t l, const double* Mh, double* Q) {
+    return guarded([&] {
+        check_ctx(c);
+        require(m >= l && l >= 1, "orth: input must be tall (rows >= cols >= 1)");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        DBuf<double> W(size_t(m * l), c->stream);
+        upload_colmajor(*c, Mh, m, l, m, W.get());
+        orth_device(*c, W.get(), m, l);
+        download_colmajor(*c, W.get(), m, l, Q);
+    });
+}
+
 int frpca_eig_svd(frpca_ctx* c, int64_t m, int64_t n, const double* Ah, double* U, double* S,
                   double* V) {
     return guarded([&] {
@@ -360,10 +373,13 @@ int frpca_run(frpca_ctx* c, frpca_dmat* M, int algorithm, const frpca_config* cf
         a.device_io = (cfg->flags & FRPCA_FLAG_DEVICE_IO) != 0;
         int algo = algorithm;
         if (algo == FRPCA_ALGO_AUTO) algo = (M->grows < M->gcols) ? FRPCA_ALGO_FRPCA : FRPCA_ALGO_FRPCAT;
-        require(algo == FRPCA_ALGO_FRPCA || algo == FRPCA_ALGO_FRPCAT, "frpca_run: unknown algorithm");
+        require(algo == FRPCA_ALGO_FRPCA || algo == FRPCA_ALGO_FRPCAT || algo == FRPCA_ALGO_BASIC_RPCA ||
+                    algo == FRPCA_ALGO_BASIC_RPCAT,
+                "frpca_run: unknown algorithm");
         if (dispatched) *dispatched = algo;
         if (algo == FRPCA_ALGO_FRPCA) run_frpca(*c, *M, a, stats);
-        else run_frpcat(*c, *M, a, stats);
+        else if (algo == FRPCA_ALGO_FRPCAT) run_frpcat(*c, *M, a, stats);
+        else run_basic(*c, *M, a, stats, algo == FRPCA_ALGO_BASIC_RPCAT);
     });
 }
 

@@ -297,6 +297,99 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Baselines: basic_rpca, randsvd.hpp:95-134 (sketch on the
+// right) and basic_rpcat, :136-175 (sketch on the left). Q is re-orthonormalised
+// by Householder QR after every product; the small SVD of B = Q^T A (resp.
+// (A Q)^T) is eig_svd of its transpose reversed (economic_svd_short_fat,
+// dense_kernels.hpp:179-190), i.e. the same finalisation as frpca (resp.
+// frpcat). 2p + 2 passes. Single GPU.
+void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
+    const frpca_config& cfg = a.cfg;
+    const char* nm = left ? "basic_rpcat" : "basic_rpca";
+    check_common(cfg);
+    require(cfg.power >= 0, left ? "basic_rpcat: power p must be >= 0" : "basic_rpca: power p must be >= 0");
+    const int64_t l = cfg.k + cfg.oversample;
+    require(l <= std::min(M.grows, M.gcols), left ? "basic_rpcat: k + oversample must be <= min(rows, cols)"
+                                                  : "basic_rpca: k + oversample must be <= min(rows, cols)");
+    require(c.world == 1, "basic_rpca / basic_rpcat: single GPU only");
+    (void)nm;
+    const int64_t m = M.A.rows, n = M.A.cols, k = cfg.k, s = cfg.oversample, p = cfg.power;
+    const uint64_t passes0 = M.passes.load();
+    cudaStream_t S = c.stream;
+    DBuf<double> bufM(size_t(std::max<int64_t>(m, 1) * l), S), bufN(size_t(std::max<int64_t>(n, 1) * l), S);
+
+    auto t0 = Clock::now();
+    if (!left) {
+        // Omega n x l column-major -> row-major; Q = orth(A Omega), m x l
+        DBuf<double> om(size_t(n * l), S);
+        sketch_stream(c, a, n, l, om.get());
+        transpose_device(c, om.get(), l, n, bufN.get());
+        spmm_pass(c, M, false, bufN.get(), l, bufM.get());
+        orth_device(c, bufM.get(), m, l);
+    } else {
+        // Omega l x m column-major == Omega^T row-major m x l; Q = orth(A^T Omega^T), n x l
+        sketch_stream(c, a, l, m, bufM.get());
+        spmm_pass(c, M, true, bufM.get(), l, bufN.get());
+        orth_device(c, bufN.get(), n, l);
+    }
+    FB_CUDA(cudaStreamSynchronize(S));
+    const double t_sketch = since(t0);
+
+    t0 = Clock::now();
+    for (int64_t i = 0; i < p; ++i) {
+        if (!left) {
+            spmm_pass(c, M, true, bufM.get(), l, bufN.get());   // G = orth(A^T Q)
+            orth_device(c, bufN.get(), n, l);
+            spmm_pass(c, M, false, bufN.get(), l, bufM.get());  // Q = orth(A G)
+            orth_device(c, bufM.get(), m, l);
+        } else {
+            spmm_pass(c, M, false, bufN.get(), l, bufM.get());  // G = orth(A Q)
+            orth_device(c, bufM.get(), m, l);
+            spmm_pass(c, M, true, bufM.get(), l, bufN.get());   // Q = orth(A^T G)
+            orth_device(c, bufN.get(), n, l);
+        }
+    }
+    FB_CUDA(cudaStreamSynchronize(S));
+    const double t_power = since(t0);
+
+    t0 = Clock::now();
+    DBuf<double> Uo(size_t(std::max<int64_t>(m, 1) * k), S), Vo(size_t(std::max<int64_t>(n, 1) * k), S),
+        So(size_t(k), S);
+    DBuf<double> MU(size_t(l * k), S), MV(size_t(l * k), S);
+    EigWork e;
+    if (!left) {
+        DBuf<double> W(size_t(std::max<int64_t>(n, 1) * l), S);
+        spmm_pass(c, M, true, bufM.get(), l, W.get());          // W = A^T Q, n x l
+        e.run(c, W.get(), n, l);
+        e.factor(c, int(s), int(k), int(k), true, false, MU.get());  // U = Q V(:, ind)
+        e.factor(c, int(s), int(k), int(k), true, true, MV.get());   // V = W V(:, ind) / S
+        gemm_device(c, bufM.get(), m, l, MU.get(), k, Uo.get(), std::max<int64_t>(m, 1), true);
+        gemm_device(c, W.get(), n, l, MV.get(), k, Vo.get(), std::max<int64_t>(n, 1), true);
+        basis_out(c, a, bufM.get(), m, l);
+    } else {
+        DBuf<double> W(size_t(std::max<int64_t>(m, 1) * l), S);
+        spmm_pass(c, M, false, bufN.get(), l, W.get());         // W = A Q, m x l
+        e.run(c, W.get(), m, l);
+        e.factor(c, int(s), int(k), int(k), true, true, MU.get());   // U = W V(:, ind) / S
+        e.factor(c, int(s), int(k), int(k), true, false, MV.get());  // V = Q V(:, ind)
+        gemm_device(c, W.get(), m, l, MU.get(), k, Uo.get(), std::max<int64_t>(m, 1), true);
+        gemm_device(c, bufN.get(), n, l, MV.get(), k, Vo.get(), std::max<int64_t>(n, 1), true);
+        basis_out(c, a, bufN.get(), n, l);
+    }
+    e.singular_values(c, int(s), int(k), true, So.get());
+    copy_out(c, a, a.U, Uo.get(), m * k);
+    copy_out(c, a, a.V, Vo.get(), n * k);
+    copy_out(c, a, a.S, So.get(), k);
+    FB_CUDA(cudaStreamSynchronize(S));
+    if (st) {
+        st->sketch_seconds = t_sketch;
+        st->power_seconds = t_power;
+        st->finalize_seconds = since(t0);
+        st->passes_over_matrix = M.passes.load() - passes0;
+    }
+}
+
 void spmm_pass(Ctx& c, DMat& M, bool transpose, const double* X, int64_t ncols, double* Y) {
     if (transpose) spmm_t_device(c, M.At, X, ncols, Y, "spmm_AtY");
     else spmm_device(c, M.A, X, ncols, ncols, Y, ncols, "spmm_AX");

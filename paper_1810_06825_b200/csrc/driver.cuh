@@ -27,6 +27,8 @@ void eig_svd_U(Ctx& c, const double* W, int64_t r, int64_t n, double* Uout);
 void spmm_pass(Ctx& c, DMat& M, bool transpose, const double* X, int64_t ncols, double* Y);
 void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st);
 void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st);
+// basic_rpca (left = false) / basic_rpcat (left = true), randsvd.hpp:95-175
+void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left);
 uint64_t mix_seed(uint64_t seed, uint64_t tag);
 
 // comm.cu: in-place sum over ranks (no-op on one GPU).

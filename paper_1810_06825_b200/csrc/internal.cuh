@@ -147,6 +147,9 @@ double maxabs_device(Ctx& c, const double* x, int64_t n);
 // V (column-major) eigenvectors, D ascending eigenvalues (device), D copied to h_D.
 void syevd_device(Ctx& c, double* B_inout_V, int64_t n, double* d_D, std::vector<double>& h_D);
 
+// ---- orth.cu : in place: W (r x l row-major) -> Q of its Householder QR.
+void orth_device(Ctx& c, double* W, int64_t r, int64_t l);
+
 // ---- lu.cu : in place: W (m x l row-major) -> P^T L (row-major), lu_basis.
 void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l);
 

@@ -89,6 +89,26 @@ int main() {
     auto a = frpca::frpca(W, make_config(2, 2, 5, 2024));
     auto b = frpca::frpca(W, make_config(2, 2, 5, 2024));
     CHECK(a.S == b.S && a.U == b.U && a.V == b.V);
+    // baselines (randsvd.hpp:95-175) and orth (dense_kernels.hpp:30-48)
+    {
+        frpca::PcaConfig cd = make_config(2, 3, 0);  // test_randsvd.cpp:55-69: q = 0, p = 2
+        cd.power = 2;
+        auto b1 = frpca::basic_rpca(diag_sparse({5, 4, 3, 2, 1}, 5, 5), cd);
+        CHECK(std::abs(b1.S(0) - 5.0) < 1e-8 && std::abs(b1.S(1) - 4.0) < 1e-8);
+        auto b2 = frpca::basic_rpcat(diag_sparse({5, 4, 3, 2, 1}, 5, 5), cd);
+        CHECK(std::abs(b2.S(0) - 5.0) < 1e-8 && std::abs(b2.S(1) - 4.0) < 1e-8);
+        frpca::RunStats<double> st;
+        frpca::PcaConfig c = make_config(2, 2, 2);
+        c.power = 3;
+        frpca::basic_rpca(W, c, &st);
+        CHECK(st.passes_over_matrix == 8u);
+        frpca::Matrix<double> M(2, 1);
+        M(0, 0) = 3.0;
+        M(1, 0) = 4.0;
+        auto Qm = frpca::orth(M);
+        CHECK(std::abs(std::abs(Qm(0, 0)) - 0.6) < 1e-15 && std::abs(std::abs(Qm(1, 0)) - 0.8) < 1e-15);
+        CHECK((throws<frpca::NumericalError>([&] { frpca::orth(frpca::Matrix<double>(4, 2)); })));
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }

@@ -343,3 +343,100 @@ def test_shared_seed_equals_injected(orc):
     a = orc.pca(A, orc.FRPCAT, 4, 2, 3, seed=seed)
     b = orc.pca(A, orc.FRPCAT, 4, 2, 3, seed=999, omega=om)
     assert np.array_equal(a["S"], b["S"])
+
+# ------------------------------------------------ f4: orth and the baselines
+
+
+def test_orth_identity_and_single_column(orc):  # test_dense_kernels.cpp:38-43, :54-60
+    Q = orc.orth(np.eye(5, 3))
+    assert np.abs(Q.T @ Q - np.eye(3)).max() < 1e-14
+    assert projector_gap_dense(Q, np.eye(5, 3)) < 1e-14
+    q = orc.orth(np.array([[3.0], [4.0]]))
+    assert abs(abs(q[0, 0]) - 0.6) < 1e-15 and abs(abs(q[1, 0]) - 0.8) < 1e-15
+
+
+def test_orth_near_dependent(orc):  # test_dense_kernels.cpp:45-52
+    M = np.array([[1.0, 1.0], [1.0, 1.0 + 1e-3], [0.0, 0.0]])
+    Q = orc.orth(M)
+    assert np.abs(Q.T @ Q - np.eye(2)).max() < 1e-13
+    assert projector_gap_dense(Q, orth(M)) < 1e-10
+
+
+def test_orth_rejects(orc):  # test_dense_kernels.cpp:62-69
+    M = np.zeros((4, 2))
+    M[:, 0] = np.linspace(1.0, 4.0, 4)
+    M[:, 1] = 2.0 * M[:, 0]
+    with pytest.raises(orc.NumericalError):
+        orc.orth(M)
+    with pytest.raises(ValueError):
+        orc.orth(orc.gaussian_matrix(2, 4, 1))
+    with pytest.raises(orc.NumericalError):
+        orc.orth(np.zeros((4, 2)))
+
+
+def test_basic_diag(orc):  # test_randsvd.cpp:55-69
+    A = diag_sparse([5, 4, 3, 2, 1], 5, 5, orc)
+    for algo in (orc.BASIC_RPCA, orc.BASIC_RPCAT):
+        r = orc.pca(A, algo, 2, 3, 0, power=2)
+        assert abs(r["S"][0] - 5) < 1e-8 and abs(r["S"][1] - 4) < 1e-8
+        check_invariants(r)
+
+
+def test_basic_exact_rank3(orc):  # test_randsvd.cpp:87-96
+    A, D = exact_rank3(100, 80, 11, orc)
+    na = np.linalg.norm(D)
+    for algo in (orc.BASIC_RPCA, orc.BASIC_RPCAT):
+        r = orc.pca(A, algo, 3, 0, 0, power=0)
+        assert np.linalg.norm(D - (r["U"] * r["S"]) @ r["V"].T) < 1e-9 * na
+
+
+def test_basic_zero_matrix_rejected(orc):  # test_randsvd.cpp:106-108
+    with pytest.raises(orc.NumericalError):
+        orc.pca(orc.Csr.from_triplets(6, 6, []), orc.BASIC_RPCA, 2, 1, 0, power=1)
+
+
+def _recon(r):
+    return (r["U"] * r["S"]) @ r["V"].T
+
+
+@pytest.mark.parametrize("q", [4, 6, 10])
+@pytest.mark.parametrize("fast,basic,shape,oseed", [("FRPCA", "BASIC_RPCA", (80, 120), 42),
+                                                   ("FRPCAT", "BASIC_RPCAT", (120, 80), 43)])
+def test_theorem_equivalence(orc, q, fast, basic, shape, oseed):  # test_randsvd.cpp:140-172
+    """Theorems 1/2 of the paper: the fast algorithm with q passes and the
+    baseline with p = (q - 2) / 2 power iterations give the same factorisation
+    for the same sketch."""
+    m, n = shape
+    A = orc.Csr.random_sparse(m, n, 0.15, 77 if fast == "FRPCA" else 78)
+    D = A.to_dense() if hasattr(A, "to_dense") else None
+    l = 8 + 5
+    Om = orc.gaussian_matrix(n, l, oseed) if fast == "FRPCA" else orc.gaussian_matrix(l, m, oseed)
+    p = (q - 2) // 2
+    f = orc.pca(A, getattr(orc, fast), 8, 5, q, seed=5, omega=Om, power=p, want_basis=True)
+    b = orc.pca(A, getattr(orc, basic), 8, 5, q, seed=5, omega=Om, power=p, want_basis=True)
+    na = np.linalg.norm(_recon(f))
+    assert np.linalg.norm(_recon(f) - _recon(b)) / na < 1e-8
+    assert projector_gap_dense(f["basis"], b["basis"]) < 1e-8
+    assert b["stats"]["passes_over_matrix"] == 2 * p + 2
+
+
+def test_shared_seed_pairs_sketches(orc):  # test_randsvd.cpp:174-180
+    A = orc.Csr.random_sparse(60, 90, 0.2, 79)
+    f = orc.pca(A, orc.FRPCA, 5, 5, 6, seed=1234, power=2)
+    b = orc.pca(A, orc.BASIC_RPCA, 5, 5, 6, seed=1234, power=2)
+    assert np.linalg.norm(_recon(f) - _recon(b)) / np.linalg.norm(_recon(f)) < 1e-8
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 3])
+def test_basic_pass_accounting(orc, p):  # test_randsvd.cpp:200-209
+    A = orc.Csr.random_sparse(50, 70, 0.3, 55)
+    for algo in (orc.BASIC_RPCA, orc.BASIC_RPCAT):
+        assert orc.pca(A, algo, 4, 4, 2, power=p)["stats"]["passes_over_matrix"] == 2 * p + 2
+
+
+def test_basic_preconditions(orc):  # test_randsvd.cpp:253-262
+    A = orc.Csr.random_sparse(20, 30, 0.3, 1)
+    with pytest.raises(ValueError, match="power p must be >= 0"):
+        orc.pca(A, orc.BASIC_RPCA, 2, 5, 2, power=-1)
+    with pytest.raises(ValueError, match="k \\+ oversample must be <= min"):
+        orc.pca(A, orc.BASIC_RPCAT, 15, 10, 2, power=0)
