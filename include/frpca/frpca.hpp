@@ -5,7 +5,7 @@
 // for Scalar = double: same namespace, names, argument conventions and
 // exceptions, so code written against the reference's frpca(), frpcat(),
 // auto_pca(), basic_rpca(), basic_rpcat(), spmm(), spmm_transpose(),
-// lu_basis(), orth(), eig_svd(),
+// lu_basis(), orth(), eig_svd(), load_matrix_market(), write_matrix_market(),
 // gaussian_matrix() compiles against this header and runs on a B200.
 //
 // What differs, by necessity: Eigen is not available, so Matrix<double> /
@@ -336,6 +336,36 @@ EigSvdResult<Scalar> eig_svd(const Matrix<Scalar>& A) {
     detail::check(frpca_eig_svd(b200::Context::default_context().get(), A.rows(), A.cols(), A.data(),
                                 r.U.data(), r.S.data(), r.V.data()));
     return r;
+}
+
+// ---- matrix_market.hpp (the load step) -------------------------
+// load_matrix_market (:27-93): the parse runs on the host (parallel chunks),
+// from_triplets (sparse_matrix.hpp:62-95) on the device.
+template <typename Scalar = double>
+SparseMatrixCsr<Scalar> load_matrix_market(const std::string& path) {
+    frpca_mtx* h = nullptr;
+    int64_t rows = 0, cols = 0, n = 0;
+    detail::check(frpca_mtx_read(path.c_str(), &h, &rows, &cols, &n));
+    std::vector<int64_t> r(static_cast<size_t>(n)), c(static_cast<size_t>(n));
+    std::vector<double> v(static_cast<size_t>(n));
+    const int st = frpca_mtx_entries(h, r.data(), c.data(), v.data());
+    frpca_mtx_free(h);
+    detail::check(st);
+    std::vector<Index> rp(static_cast<size_t>(rows) + 1), ci(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    std::vector<Scalar> va(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    int64_t nnz = 0;
+    detail::check(frpca_csr_from_triplets(b200::Context::default_context().get(), rows, cols, n, r.data(),
+                                          c.data(), v.data(), &nnz, rp.data(), ci.data(), va.data()));
+    ci.resize(static_cast<size_t>(nnz));
+    va.resize(static_cast<size_t>(nnz));
+    return SparseMatrixCsr<Scalar>(rows, cols, std::move(rp), std::move(ci), std::move(va));
+}
+
+// write_matrix_market (:95-116): general coordinate, %.17g values
+template <typename Scalar>
+void write_matrix_market(const std::string& path, const SparseMatrixCsr<Scalar>& A) {
+    detail::check(frpca_mtx_write(path.c_str(), A.rows(), A.cols(), A.rowPtr().data(), A.colIdx().data(),
+                                  A.values().data()));
 }
 
 // ---- randsvd.hpp -------------------------------------------------------------

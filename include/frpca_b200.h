@@ -110,6 +110,28 @@ int frpca_dmat_reset_pass_count(frpca_dmat* A);
 int frpca_dmat_get_transpose(const frpca_dmat* A, int64_t* t_row_ptr, int64_t* t_col_idx,
                              double* t_values);
 
+/* ---- load step ------------------------------------------------
+ * load_matrix_market (matrix_market.hpp:27-93) up to from_triplets: parses a
+ * coordinate real/integer, general/symmetric file (symmetric off-diagonal
+ * entries also yield the mirrored entry) into an opaque handle; rows, cols and
+ * the number of triplets n are returned. Errors: FRPCA_ERR_IO with the
+ * reference's message. frpca_mtx_entries copies the 0-based triplets (file
+ * order) into caller arrays of length n. */
+typedef struct frpca_mtx frpca_mtx;
+int frpca_mtx_read(const char* path, frpca_mtx** out, int64_t* rows, int64_t* cols, int64_t* n);
+int frpca_mtx_entries(const frpca_mtx* h, int64_t* r, int64_t* c, double* v);
+void frpca_mtx_free(frpca_mtx* h);
+/* write_matrix_market (matrix_market.hpp:95-116): general, %.17g values. */
+int frpca_mtx_write(const char* path, int64_t rows, int64_t cols, const int64_t* row_ptr,
+                    const int64_t* col_idx, const double* values);
+/* SparseMatrixCsr::from_triplets (sparse_matrix.hpp:62-95) on the device:
+ * sort by (row, col), sum duplicates, drop exact-zero sums. Outputs (host):
+ * nnz, row_ptr (rows + 1), col_idx and values (capacity n). Out-of-bounds
+ * entries -> FRPCA_ERR_INVALID "from_triplets: entry out of bounds". */
+int frpca_csr_from_triplets(frpca_ctx* ctx, int64_t rows, int64_t cols, int64_t n, const int64_t* r,
+                            const int64_t* c, const double* v, int64_t* nnz, int64_t* row_ptr,
+                            int64_t* col_idx, double* values);
+
 /* ---- kernels (sparse_matrix.hpp:177-240, dense_kernels.hpp:16-174) --------- */
 /* Y = A*X (transpose=0, spmm :177-206) or Y = A^T*X (transpose=1,
  * spmm_transpose :208-240). X: (A.cols or A.rows) x ncols column-major with

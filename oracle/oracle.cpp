@@ -41,6 +41,9 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <cctype>
+#include <sstream>
+#include <fstream>
 
 #include <thread>
 
@@ -717,6 +720,71 @@ static Svd basic_rpcat(const Csr& A, const Config& cfg, Stats* stats, const Mat*
     return out;
 }
 
+// ---- load_matrix_market (matrix_market.hpp:27-93), up to from_triplets -----
+// Restated with the reference's own stream machinery (ifstream, getline,
+// istringstream extraction) so the library's parallel parser can be pinned
+// against it: accepted formats, symmetric expansion, messages.
+struct IoError : std::runtime_error {
+    explicit IoError(const std::string& w) : std::runtime_error(w) {}
+};
+struct MtxTriplets { Index rows = 0, cols = 0; std::vector<Triplet> e; };
+
+static std::string lowercase(std::string s) {
+    for (char& c : s) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+    return s;
+}
+
+static MtxTriplets mtx_parse(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw IoError("cannot open '" + path + "' for reading");
+    std::string line;
+    if (!std::getline(in, line)) throw IoError(path + ": empty file");
+    std::istringstream banner(line);
+    std::string tag, object, format, field, symmetry;
+    banner >> tag >> object >> format >> field >> symmetry;
+    if (tag != "%%MatrixMarket") throw IoError(path + ": missing %%MatrixMarket banner");
+    object = lowercase(object);
+    format = lowercase(format);
+    field = lowercase(field);
+    symmetry = lowercase(symmetry);
+    if (object != "matrix" || format != "coordinate")
+        throw IoError(path + ": only coordinate matrices are supported");
+    if (field != "real" && field != "integer")
+        throw IoError(path + ": only real-valued matrices are supported");
+    if (symmetry != "general" && symmetry != "symmetric")
+        throw IoError(path + ": only general or symmetric storage is supported");
+    const bool symmetric = symmetry == "symmetric";
+    do {
+        if (!std::getline(in, line)) throw IoError(path + ": missing size line");
+    } while (line.empty() || line[0] == '%');
+    long long rows = -1, cols = -1, nnz = -1;
+    {
+        std::istringstream sizes(line);
+        if (!(sizes >> rows >> cols >> nnz) || rows < 0 || cols < 0 || nnz < 0)
+            throw IoError(path + ": malformed size line '" + line + "'");
+    }
+    if (symmetric && rows != cols) throw IoError(path + ": symmetric matrix must be square");
+    MtxTriplets out;
+    out.rows = rows;
+    out.cols = cols;
+    for (long long e = 0; e < nnz; ++e) {
+        do {
+            if (!std::getline(in, line))
+                throw IoError(path + ": unexpected end of file after " + std::to_string(e) + " entries");
+        } while (line.empty() || line[0] == '%');
+        std::istringstream entry(line);
+        long long i = 0, j = 0;
+        double v = 0.0;
+        if (!(entry >> i >> j >> v)) throw IoError(path + ": malformed entry line '" + line + "'");
+        if (i < 1 || i > rows || j < 1 || j > cols)
+            throw IoError(path + ": entry (" + std::to_string(i) + ", " + std::to_string(j) +
+                          ") outside declared dimensions");
+        out.e.push_back({Index(i - 1), Index(j - 1), v});
+        if (symmetric && i != j) out.e.push_back({Index(j - 1), Index(i - 1), v});
+    }
+    return out;
+}
+
 // ---- validation oracle: one-sided Jacobi SVD (validation.hpp:34-121) -------
 static void oracle_svd(const Mat& Ain, Mat& U, std::vector<double>& S, Mat& V) {
     require(Ain.rows >= 1 && Ain.cols >= 1, "oracle_svd: empty matrix");
@@ -806,6 +874,7 @@ static int guarded(F&& f) {
     try { f(); return 0; }
     catch (const std::invalid_argument& e) { g_err = e.what(); return 2; }
     catch (const orc::NumericalError& e) { g_err = e.what(); return 4; }
+    catch (const orc::IoError& e) { g_err = e.what(); return 3; }
     catch (const std::exception& e) { g_err = e.what(); return 1; }
 }
 
@@ -885,6 +954,20 @@ int orc_lu_basis(int64_t m, int64_t l, const double* M, double* X) {
         std::memcpy(X, R.d.data(), sizeof(double) * R.d.size());
     });
 }
+// Matrix Market parse: handle with the triplets (file order)
+int orc_mtx_read(const char* path, void** out, int64_t* rows, int64_t* cols, int64_t* n) {
+    return guarded([&] {
+        auto* t = new MtxTriplets(mtx_parse(path));
+        *out = t;
+        *rows = t->rows; *cols = t->cols; *n = int64_t(t->e.size());
+    });
+}
+void orc_mtx_entries(void* h, int64_t* r, int64_t* c, double* v) {
+    const auto* t = static_cast<MtxTriplets*>(h);
+    for (size_t i = 0; i < t->e.size(); ++i) { r[i] = t->e[i].row; c[i] = t->e[i].col; v[i] = t->e[i].value; }
+}
+void orc_mtx_free(void* h) { delete static_cast<MtxTriplets*>(h); }
+
 int orc_orth(int64_t m, int64_t l, const double* M, double* Q) {
     return guarded([&] {
         Mat R = orth(view_colmajor(M, m, l, m));

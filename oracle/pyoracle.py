@@ -62,6 +62,12 @@ def lib():
         L.orc_spmm_transpose.argtypes = [_vp, _dp, _i64, _i64, _dp]
         L.orc_lu_basis.argtypes = [_i64, _i64, _dp, _dp]
         L.orc_orth.argtypes = [_i64, _i64, _dp, _dp]
+        L.orc_mtx_read.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(_i64), C.POINTER(_i64),
+                                   C.POINTER(_i64)]
+        L.orc_mtx_entries.argtypes = [C.c_void_p, C.POINTER(_i64), C.POINTER(_i64), _dp]
+        L.orc_mtx_entries.restype = None
+        L.orc_mtx_free.argtypes = [C.c_void_p]
+        L.orc_mtx_free.restype = None
         L.orc_eig_svd.argtypes = [_i64, _i64, _dp, _dp, _dp, _dp]
         L.orc_eig_sym.argtypes = [_i64, _dp, _dp, _dp]
         L.orc_gram_lower.argtypes = [_i64, _i64, _dp, _dp]
@@ -80,6 +86,8 @@ def _check(status: int):
         raise ValueError(msg)
     if status == 4:
         raise NumericalError(msg)
+    if status == 3:
+        raise OSError(msg)
     raise RuntimeError(msg)
 
 
@@ -238,6 +246,23 @@ def oracle_svd(A: np.ndarray):
 
 
 FRPCA, FRPCAT, AUTO, BASIC_RPCA, BASIC_RPCAT = 0, 1, 2, 3, 4
+
+
+def read_matrix_market(path: str):
+    """matrix_market.hpp:27-93 (the parse, before from_triplets): (rows, cols,
+    r, c, v), 0-based, file order, symmetric storage expanded."""
+    import os
+    h = C.c_void_p()
+    rows, cols, n = _i64(0), _i64(0), _i64(0)
+    _check(lib().orc_mtx_read(os.fsencode(path), C.byref(h), C.byref(rows), C.byref(cols), C.byref(n)))
+    try:
+        r = np.empty(n.value, dtype=np.int64)
+        c = np.empty(n.value, dtype=np.int64)
+        v = np.empty(n.value, dtype=np.float64)
+        lib().orc_mtx_entries(h, r.ctypes.data_as(C.POINTER(_i64)), c.ctypes.data_as(C.POINTER(_i64)), _d(v))
+    finally:
+        lib().orc_mtx_free(h)
+    return rows.value, cols.value, r, c, v
 
 
 def orth(M: np.ndarray) -> np.ndarray:

@@ -16,18 +16,20 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import enum
+import os
 import threading
 
 import numpy as np
 
 from . import _lib
-from ._lib import NumericalError, CudaError  # noqa: F401
+from ._lib import NumericalError, CudaError, IoError  # noqa: F401
 
 __all__ = [
     "SparseMatrixCsr", "PcaConfig", "RunStats", "SvdResult", "AutoPcaResult", "PcaAlgorithm",
     "NumericalError", "CudaError", "Context", "default_context",
     "spmm", "spmm_transpose", "transpose", "gaussian_matrix", "lu_basis", "orth", "eig_svd",
     "frpca", "frpcat", "auto_pca", "basic_rpca", "basic_rpcat", "mix_seed", "kSketchStreamTag",
+    "read_matrix_market", "load_matrix_market", "write_matrix_market", "IoError",
 ]
 
 kSketchStreamTag = 0xA11CE  # randsvd.hpp:63
@@ -237,9 +239,11 @@ class SparseMatrixCsr:
         _ = rowid
 
     @classmethod
-    def from_triplets(cls, rows: int, cols: int, entries) -> "SparseMatrixCsr":
+    def from_triplets(cls, rows: int, cols: int, entries, device: bool = False,
+                      ctx: "Context | None" = None) -> "SparseMatrixCsr":
         """sparse_matrix.hpp:62-95: sort by (row, col), sum duplicates in order,
-        drop entries that sum to exactly zero."""
+        drop entries that sum to exactly zero. device=True builds the CSR on
+        the GPU (frpca_csr_from_triplets: radix sort, run sums, compaction)."""
         if rows < 0 or cols < 0:
             raise ValueError("from_triplets: negative dimension")
         if isinstance(entries, tuple) and len(entries) == 3 and hasattr(entries[0], "__len__"):
@@ -250,6 +254,19 @@ class SparseMatrixCsr:
             r = np.array([e[0] for e in ent], dtype=np.int64)
             c = np.array([e[1] for e in ent], dtype=np.int64)
             v = np.array([e[2] for e in ent], dtype=np.float64)
+        if device:
+            ctx = ctx or default_context()
+            r, c, v = np.ascontiguousarray(r), np.ascontiguousarray(c), np.ascontiguousarray(v)
+            n = r.size
+            row_ptr = np.empty(rows + 1, dtype=np.int64)
+            col = np.empty(max(n, 1), dtype=np.int64)
+            val = np.empty(max(n, 1), dtype=np.float64)
+            nnz = C.c_int64(0)
+            _lib.check(_lib.load().frpca_csr_from_triplets(
+                ctx._h, rows, cols, n, _ptr(r), _ptr(c), _ptr(v), C.byref(nnz), _ptr(row_ptr), _ptr(col),
+                _ptr(val)))
+            k = nnz.value
+            return cls(rows, cols, row_ptr, col[:k].copy(), val[:k].copy(), validate=False)
         if r.size and ((r < 0).any() or (r >= rows).any() or (c < 0).any() or (c >= cols).any()):
             raise ValueError("from_triplets: entry out of bounds")
         order = np.lexsort((c, r))  # stable: duplicates keep input order
@@ -344,6 +361,38 @@ def _colmajor(X) -> np.ndarray:
     if X.ndim == 1:
         X = X.reshape(-1, 1)
     return np.asfortranarray(X)
+
+
+def read_matrix_market(path: str):
+    """The parse of load_matrix_market (matrix_market.hpp:27-93): returns
+    (rows, cols, r, c, v) with 0-based triplets in file order, symmetric
+    storage expanded. Host code (no GPU needed). Errors: IoError."""
+    L = _lib.load()
+    h = C.c_void_p()
+    rows, cols, n = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+    _lib.check(L.frpca_mtx_read(os.fsencode(path), C.byref(h), C.byref(rows), C.byref(cols), C.byref(n)))
+    try:
+        r = np.empty(n.value, dtype=np.int64)
+        c = np.empty(n.value, dtype=np.int64)
+        v = np.empty(n.value, dtype=np.float64)
+        _lib.check(L.frpca_mtx_entries(h, _ptr(r), _ptr(c), _ptr(v)))
+    finally:
+        L.frpca_mtx_free(h)
+    return rows.value, cols.value, r, c, v
+
+
+def load_matrix_market(path: str, ctx: Context | None = None) -> SparseMatrixCsr:
+    """matrix_market.hpp:27-93: parse on the host, from_triplets on the GPU."""
+    rows, cols, r, c, v = read_matrix_market(path)
+    return SparseMatrixCsr.from_triplets(rows, cols, (r, c, v), device=True, ctx=ctx)
+
+
+def write_matrix_market(path: str, A: SparseMatrixCsr) -> None:
+    """matrix_market.hpp:95-116: general coordinate, %.17g values."""
+    rp = np.ascontiguousarray(A.rowPtr(), dtype=np.int64)
+    ci = np.ascontiguousarray(A.colIdx(), dtype=np.int64)
+    va = np.ascontiguousarray(A.values(), dtype=np.float64)
+    _lib.check(_lib.load().frpca_mtx_write(os.fsencode(path), A.rows(), A.cols(), _ptr(rp), _ptr(ci), _ptr(va)))
 
 
 def spmm(A: SparseMatrixCsr, X, ctx: Context | None = None) -> np.ndarray:

@@ -46,6 +46,11 @@ SIGNATURES = {
     "frpca_dmat_upload_shard": (C.c_int, [_vp, _i64, _i64, _i32, _i64, _i64, _i64, _i64,
                                           _vp, _vp, _vp, C.POINTER(_vp)]),
     "frpca_dmat_destroy": (C.c_int, [_vp]),
+    "frpca_mtx_read": (C.c_int, [C.c_char_p, C.POINTER(_vp), _lp, _lp, _lp]),
+    "frpca_mtx_entries": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "frpca_mtx_free": (None, [_vp]),
+    "frpca_mtx_write": (C.c_int, [C.c_char_p, _i64, _i64, _vp, _vp, _vp]),
+    "frpca_csr_from_triplets": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _lp, _vp, _vp, _vp]),
     "frpca_dmat_info": (C.c_int, [_vp, _lp, _lp, _lp]),
     "frpca_dmat_pass_count": (C.c_int, [_vp, C.POINTER(_u64)]),
     "frpca_dmat_reset_pass_count": (C.c_int, [_vp]),
@@ -95,6 +100,10 @@ class CudaError(RuntimeError):
     """CUDA / NCCL / cuSOLVER failure (status 5)."""
 
 
+class IoError(OSError):
+    """frpca::IoError (types.hpp:19-22): file I/O and Matrix Market format errors."""
+
+
 def check(status: int):
     if status == OK:
         return
@@ -104,5 +113,5 @@ def check(status: int):
     if status == ERR_NUMERICAL:
         raise NumericalError(msg)
     if status == ERR_IO:
-        raise OSError(msg)
+        raise IoError(msg)
     raise CudaError(msg)

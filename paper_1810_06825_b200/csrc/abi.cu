@@ -25,6 +25,9 @@ int guarded(F&& f) {
     } catch (const NumericalError& e) {
         g_err = e.what();
         return FRPCA_ERR_NUMERICAL;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return FRPCA_ERR_IO;
     } catch (const CudaError& e) {
         g_err = e.what();
         return FRPCA_ERR_CUDA;
@@ -319,6 +322,60 @@ int frpca_lu_basis(frpca_ctx* c, int64_t m, int64_t l, const double* Mh, double*
         upload_colmajor(*c, Mh, m, l, m, W.get());
         lu_basis_device(*c, W.get(), m, l);
         download_colmajor(*c, W.get(), m, l, X);
+    });
+}
+
+struct frpca_mtx {
+    fb::MtxData d;
+};
+
+int frpca_mtx_read(const char* path, frpca_mtx** out, int64_t* rows, int64_t* cols, int64_t* n) {
+    return guarded([&] {
+        require(path != nullptr && out != nullptr, "frpca_mtx_read: null argument");
+        auto* h = new frpca_mtx;
+        try {
+            mtx_read(path, h->d);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+        if (rows) *rows = h->d.rows;
+        if (cols) *cols = h->d.cols;
+        if (n) *n = int64_t(h->d.v.size());
+    });
+}
+
+int frpca_mtx_entries(const frpca_mtx* h, int64_t* r, int64_t* c, double* v) {
+    return guarded([&] {
+        require(h != nullptr, "frpca_mtx_entries: null handle");
+        const size_t n = h->d.v.size();
+        if (r) std::memcpy(r, h->d.r.data(), sizeof(int64_t) * n);
+        if (c) std::memcpy(c, h->d.c.data(), sizeof(int64_t) * n);
+        if (v) std::memcpy(v, h->d.v.data(), sizeof(double) * n);
+    });
+}
+
+void frpca_mtx_free(frpca_mtx* h) { delete h; }
+
+int frpca_mtx_write(const char* path, int64_t rows, int64_t cols, const int64_t* row_ptr, const int64_t* col_idx,
+                    const double* values) {
+    return guarded([&] {
+        require(path != nullptr && row_ptr != nullptr, "frpca_mtx_write: null argument");
+        mtx_write(path, rows, cols, row_ptr, col_idx, values);
+    });
+}
+
+int frpca_csr_from_triplets(frpca_ctx* c, int64_t rows, int64_t cols, int64_t n, const int64_t* r,
+                            const int64_t* ci, const double* v, int64_t* nnz, int64_t* row_ptr, int64_t* col_idx,
+                            double* values) {
+    return guarded([&] {
+        check_ctx(c);
+        require(rows >= 0 && cols >= 0, "from_triplets: negative dimension");
+        require(n >= 0 && (n == 0 || (r && ci && v)) && nnz && row_ptr, "from_triplets: null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        csr_from_triplets_device(*c, rows, cols, n, r, ci, v, nnz, row_ptr, col_idx, values);
     });
 }
 

@@ -14,20 +14,12 @@
 #include <vector>
 
 #include "../../include/frpca_b200.h"
+#include "errors.hpp"
 
 namespace fb {
 
-// Exceptions carried to the C-ABI boundary and mapped to FRPCA_ERR_* codes.
-struct InvalidArgument : std::runtime_error {
-    explicit InvalidArgument(const std::string& w) : std::runtime_error(w) {}
-};
-struct NumericalError : std::runtime_error {
-    explicit NumericalError(const std::string& w) : std::runtime_error(w) {}
-};
-struct CudaError : std::runtime_error {
-    explicit CudaError(const std::string& w) : std::runtime_error(w) {}
-};
-
+// Exceptions carried to the C-ABI boundary: errors.hpp (plain C++, shared
+// with the host-only sources).
 // detail::require of types.hpp:45-47: std::invalid_argument with the message.
 inline void require(bool cond, const char* msg) {
     if (!cond) throw InvalidArgument(msg);

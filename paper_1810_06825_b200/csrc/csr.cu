@@ -531,6 +531,143 @@ void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap) {
                      (long long)nhot, (long long)nitems, (long long)P.cold.nitems, (long long)P.cold.nslots);
 }
 
+// ---- from_triplets on the device (sparse_matrix.hpp:62-95) -----
+// Keys row*cols+col, stable radix sort (duplicates keep input order), each run
+// of equal keys summed sequentially, exact-zero sums dropped, row pointers by
+// counting. The reference sorts with std::sort (not stable), so for three or
+// more duplicates of one coordinate its summation order can differ (rounding
+// level); with at most two the sums are identical (a + b == b + a).
+
+namespace {
+
+__global__ void k_trip_check(const int64_t* __restrict__ r, const int64_t* __restrict__ c, int64_t n, int64_t rows,
+                             int64_t cols, unsigned long long* __restrict__ keys, int* __restrict__ bad) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t ri = r[i], ci = c[i];
+        if (ri < 0 || ri >= rows || ci < 0 || ci >= cols) {
+            atomicOr(bad, 1);
+            keys[i] = 0;
+        } else {
+            keys[i] = (unsigned long long)ri * (unsigned long long)cols + (unsigned long long)ci;
+        }
+    }
+}
+
+__global__ void k_run_heads(const unsigned long long* __restrict__ k, int64_t n, int64_t* __restrict__ head) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        head[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
+}
+
+// run starting at i (a head): sequential sum; keep[s] = (sum != 0)
+__global__ void k_run_sums(const unsigned long long* __restrict__ k, const double* __restrict__ v, int64_t n,
+                           const int64_t* __restrict__ head, const int64_t* __restrict__ seg,
+                           unsigned long long* __restrict__ skey, double* __restrict__ ssum,
+                           int64_t* __restrict__ keep) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        if (!head[i]) continue;
+        const unsigned long long key = k[i];
+        double sum = 0.0;
+        for (int64_t t = i; t < n && k[t] == key; ++t) sum += v[t];
+        const int64_t s = seg[i];
+        skey[s] = key;
+        ssum[s] = sum;
+        keep[s] = sum != 0.0 ? 1 : 0;
+    }
+}
+
+__global__ void k_trip_emit(const unsigned long long* __restrict__ skey, const double* __restrict__ ssum,
+                            const int64_t* __restrict__ keep, const int64_t* __restrict__ pos, int64_t nseg,
+                            int64_t cols, int64_t* __restrict__ col, double* __restrict__ val,
+                            int64_t* __restrict__ rowcnt) {
+    for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < nseg; s += int64_t(gridDim.x) * blockDim.x) {
+        if (!keep[s]) continue;
+        const int64_t o = pos[s];
+        const int64_t row = int64_t(skey[s] / (unsigned long long)cols);
+        col[o] = int64_t(skey[s] % (unsigned long long)cols);
+        val[o] = ssum[s];
+        atomicAdd(reinterpret_cast<unsigned long long*>(rowcnt + row + 1), 1ull);
+    }
+}
+
+template <class T>
+void exclusive_scan(Ctx& c, const T* in, T* out, int64_t n) {
+    size_t tb = 0;
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, c.stream));
+    DBuf<unsigned char> tmp(tb, c.stream);
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, in, out, n, c.stream));
+}
+
+}  // namespace
+
+void csr_from_triplets_device(Ctx& c, int64_t rows, int64_t cols, int64_t n, const int64_t* r, const int64_t* ci,
+                              const double* v, int64_t* nnz, int64_t* row_ptr, int64_t* col_idx, double* values) {
+    cudaStream_t s = c.stream;
+    if (n == 0) {
+        std::memset(row_ptr, 0, sizeof(int64_t) * size_t(rows + 1));
+        *nnz = 0;
+        return;
+    }
+    DBuf<int64_t> dr(size_t(n), s), dc(size_t(n), s);
+    DBuf<double> dv(size_t(n), s), dv2(size_t(n), s);
+    DBuf<unsigned long long> key(size_t(n), s), key2(size_t(n), s);
+    DBuf<int> bad(1, s);
+    FB_CUDA(cudaMemcpyAsync(dr.get(), r, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    FB_CUDA(cudaMemcpyAsync(dc.get(), ci, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    FB_CUDA(cudaMemcpyAsync(dv.get(), v, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    FB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    k_trip_check<<<grid_for(c, n), 256, 0, s>>>(dr.get(), dc.get(), n, rows, cols, key.get(), bad.get());
+    FB_LAUNCH_CHECK();
+    if (read_scalar(c, bad.get())) throw InvalidArgument("from_triplets: entry out of bounds");
+    dr.release();
+    dc.release();
+    int end_bit = 1;
+    const unsigned long long kmax = (unsigned long long)std::max<int64_t>(rows, 1) * (unsigned long long)cols;
+    while (end_bit < 64 && (1ull << end_bit) < kmax) ++end_bit;
+    {
+        size_t tb = 0;
+        FB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.get(), key2.get(), dv.get(), dv2.get(), n, 0,
+                                                end_bit, s));
+        DBuf<unsigned char> tmp(tb, s);
+        FB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, key.get(), key2.get(), dv.get(), dv2.get(), n, 0,
+                                                end_bit, s));
+    }
+    DBuf<int64_t> head(size_t(n) + 1, s), seg(size_t(n) + 1, s);
+    FB_CUDA(cudaMemsetAsync(head.get(), 0, head.bytes(), s));
+    k_run_heads<<<grid_for(c, n), 256, 0, s>>>(key2.get(), n, head.get());
+    FB_LAUNCH_CHECK();
+    exclusive_scan(c, head.get(), seg.get(), n + 1);
+    const int64_t nseg = read_scalar(c, seg.get() + n);
+    DBuf<unsigned long long> skey(size_t(nseg), s);
+    DBuf<double> ssum(size_t(nseg), s);
+    DBuf<int64_t> keep(size_t(nseg) + 1, s), pos(size_t(nseg) + 1, s);
+    FB_CUDA(cudaMemsetAsync(keep.get(), 0, keep.bytes(), s));
+    k_run_sums<<<grid_for(c, n), 256, 0, s>>>(key2.get(), dv2.get(), n, head.get(), seg.get(), skey.get(), ssum.get(),
+                                              keep.get());
+    FB_LAUNCH_CHECK();
+    exclusive_scan(c, keep.get(), pos.get(), nseg + 1);
+    const int64_t total = read_scalar(c, pos.get() + nseg);
+    DBuf<int64_t> ocol(size_t(std::max<int64_t>(total, 1)), s), cnt(size_t(rows) + 1, s), rp(size_t(rows) + 1, s);
+    DBuf<double> oval(size_t(std::max<int64_t>(total, 1)), s);
+    FB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+    k_trip_emit<<<grid_for(c, nseg), 256, 0, s>>>(skey.get(), ssum.get(), keep.get(), pos.get(), nseg, cols,
+                                                  ocol.get(), oval.get(), cnt.get());
+    FB_LAUNCH_CHECK();
+    // cnt[r + 1] = entries of row r -> inclusive prefix = row_ptr
+    {
+        size_t tb = 0;
+        FB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, cnt.get(), rp.get(), rows + 1, s));
+        DBuf<unsigned char> tmp(tb, s);
+        FB_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), tb, cnt.get(), rp.get(), rows + 1, s));
+    }
+    FB_CUDA(cudaMemcpyAsync(row_ptr, rp.get(), sizeof(int64_t) * (rows + 1), cudaMemcpyDeviceToHost, s));
+    if (total) {
+        FB_CUDA(cudaMemcpyAsync(col_idx, ocol.get(), sizeof(int64_t) * total, cudaMemcpyDeviceToHost, s));
+        FB_CUDA(cudaMemcpyAsync(values, oval.get(), sizeof(double) * total, cudaMemcpyDeviceToHost, s));
+    }
+    FB_CUDA(cudaStreamSynchronize(s));
+    *nnz = total;
+}
+
 void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v) {
     std::vector<int32_t> tmp(static_cast<size_t>(A.nnz));
     FB_CUDA(cudaMemcpyAsync(rp, A.rowptr.get(), sizeof(int64_t) * (A.rows + 1),

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "mtx.hpp"
 
 typedef struct ncclComm* ncclComm_t;
 
@@ -146,6 +147,11 @@ double maxabs_device(Ctx& c, const double* x, int64_t n);
 // ---- eig.cu : symmetric eigensolve of column-major n x n B (lower used):
 // V (column-major) eigenvectors, D ascending eigenvalues (device), D copied to h_D.
 void syevd_device(Ctx& c, double* B_inout_V, int64_t n, double* d_D, std::vector<double>& h_D);
+
+// ---- csr.cu : from_triplets (sparse_matrix.hpp:62-95) on the device; host
+// outputs row_ptr (rows + 1), col_idx / values (>= nnz entries; n suffices).
+void csr_from_triplets_device(Ctx& c, int64_t rows, int64_t cols, int64_t n, const int64_t* r, const int64_t* ci,
+                              const double* v, int64_t* nnz, int64_t* row_ptr, int64_t* col_idx, double* values);
 
 // ---- orth.cu : in place: W (r x l row-major) -> Q of its Householder QR.
 void orth_device(Ctx& c, double* W, int64_t r, int64_t l);

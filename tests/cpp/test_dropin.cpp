@@ -109,6 +109,15 @@ int main() {
         CHECK(std::abs(std::abs(Qm(0, 0)) - 0.6) < 1e-15 && std::abs(std::abs(Qm(1, 0)) - 0.8) < 1e-15);
         CHECK((throws<frpca::NumericalError>([&] { frpca::orth(frpca::Matrix<double>(4, 2)); })));
     }
+    // Matrix Market round trip (matrix_market.hpp:27-116)
+    {
+        const std::string path = "/tmp/frpca_dropin_test.mtx";
+        frpca::write_matrix_market(path, W);
+        auto L = frpca::load_matrix_market<double>(path);
+        CHECK(L.rows() == W.rows() && L.cols() == W.cols());
+        CHECK(L.rowPtr() == W.rowPtr() && L.colIdx() == W.colIdx() && L.values() == W.values());
+        CHECK((throws<frpca::IoError>([] { frpca::load_matrix_market<double>("/nonexistent/x.mtx"); })));
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }
