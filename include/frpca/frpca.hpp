@@ -16,6 +16,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -470,6 +471,98 @@ AutoPcaResult<Scalar> auto_pca(const SparseMatrixCsr<Scalar>& A, const PcaConfig
     out.svd = detail::run<Scalar>(FRPCA_ALGO_AUTO, A, cfg, stats, nullptr, &d);
     out.dispatched = d == FRPCA_ALGO_FRPCA ? PcaAlgorithm::Frpca : PcaAlgorithm::Frpcat;
     return out;
+}
+
+// ---- validation.hpp: metrics on the GPU --------------------------
+enum class ErrorNorm { Frobenius, Spectral };                      // :17
+constexpr std::uint64_t kDefaultOracleEntryLimit = 4'000'000;      // :26
+
+template <typename Scalar>
+struct OracleSvd {  // :73-77 (computed by the caller; the metrics need S and U)
+    Matrix<Scalar> U;
+    Vector<Scalar> S;
+    Matrix<Scalar> V;
+};
+
+// :170-203
+template <typename Scalar>
+Scalar low_rank_error(const SparseMatrixCsr<Scalar>& A, const SvdResult<Scalar>& r, ErrorNorm norm,
+                      std::uint64_t entry_limit = kDefaultOracleEntryLimit) {
+    detail::require(r.U.rows() == A.rows() && r.V.rows() == A.cols(), "low_rank_error: shape mismatch");
+    detail::require(r.U.cols() == r.S.size() && r.V.cols() == r.S.size(),
+                    "low_rank_error: inconsistent factor widths");
+    auto& ctx = b200::Context::default_context();
+    double out = 0.0;
+    detail::check(frpca_low_rank_error(ctx.get(), A.device(ctx), r.S.size(), r.U.data(), r.S.data(), r.V.data(),
+                                       norm == ErrorNorm::Spectral ? FRPCA_NORM_SPECTRAL : FRPCA_NORM_FROBENIUS,
+                                       entry_limit, &out));
+    return Scalar(out);
+}
+
+// :207-215
+template <typename Scalar>
+Scalar best_rank_k_error(const Vector<Scalar>& s, Index k, ErrorNorm norm) {
+    detail::require(k >= 0, "best_rank_k_error: negative k");
+    const Index n = s.size();
+    if (k >= n) return Scalar(0);
+    if (norm == ErrorNorm::Spectral) return s(k);
+    Scalar acc = 0;
+    for (Index i = k; i < n; ++i) acc += s(i) * s(i);
+    return std::sqrt(acc);
+}
+
+// :228-246
+template <typename Scalar>
+Vector<Scalar> pc_correlation(const Matrix<Scalar>& U_test, const Matrix<Scalar>& U_ref) {
+    detail::require(U_test.rows() == U_ref.rows() && U_test.cols() == U_ref.cols(), "pc_correlation: shape mismatch");
+    detail::require(U_test.rows() >= 2, "pc_correlation: need at least two samples");
+    Vector<Scalar> corr(U_test.cols());
+    detail::check(frpca_pc_correlation(b200::Context::default_context().get(), U_test.rows(), U_test.cols(),
+                                       U_test.data(), U_ref.data(), corr.data()));
+    return corr;
+}
+
+// :264-282
+template <typename Scalar>
+Scalar projector_distance(const Matrix<Scalar>& Q1, const Matrix<Scalar>& Q2) {
+    detail::require(Q1.rows() == Q2.rows(), "projector_distance: row mismatch");
+    double out = 0.0;
+    detail::check(frpca_projector_distance(b200::Context::default_context().get(), Q1.rows(), Q1.cols(), Q1.data(),
+                                           Q2.cols(), Q2.data(), &out));
+    return Scalar(out);
+}
+
+// :287-319 (to_json needs nlohmann::json, which this header does not pull in)
+struct AccuracyReport {
+    std::vector<double> singular_value_rel_err;
+    double recon_err_frobenius = 0.0;
+    double recon_err_spectral = 0.0;
+    double best_rank_k_err = 0.0;
+    double eps_equivalent = 0.0;
+    std::vector<double> pc_correlations;
+};
+
+template <typename Scalar>
+AccuracyReport make_accuracy_report(const SparseMatrixCsr<Scalar>& A, const SvdResult<Scalar>& r,
+                                    const OracleSvd<Scalar>& oracle) {
+    const Index k = r.S.size();
+    detail::require(oracle.S.size() >= k, "make_accuracy_report: oracle has fewer values than k");
+    AccuracyReport rep;
+    rep.singular_value_rel_err.resize(static_cast<std::size_t>(k));
+    for (Index i = 0; i < k; ++i) {
+        const double ref = static_cast<double>(oracle.S(i));
+        rep.singular_value_rel_err[static_cast<std::size_t>(i)] =
+            ref == 0.0 ? std::abs(static_cast<double>(r.S(i))) : std::abs(static_cast<double>(r.S(i)) - ref) / ref;
+    }
+    rep.recon_err_frobenius = double(low_rank_error(A, r, ErrorNorm::Frobenius));
+    rep.recon_err_spectral = double(low_rank_error(A, r, ErrorNorm::Spectral));
+    rep.best_rank_k_err = double(best_rank_k_error(oracle.S, k, ErrorNorm::Spectral));
+    rep.eps_equivalent = rep.best_rank_k_err == 0.0 ? 0.0 : rep.recon_err_spectral / rep.best_rank_k_err - 1.0;
+    Matrix<Scalar> Uk(oracle.U.rows(), k);
+    std::memcpy(Uk.data(), oracle.U.data(), sizeof(Scalar) * std::size_t(oracle.U.rows() * k));
+    Vector<Scalar> corr = pc_correlation(r.U, Uk);
+    rep.pc_correlations.assign(corr.data(), corr.data() + corr.size());
+    return rep;
 }
 
 }  // namespace frpca

@@ -162,6 +162,24 @@ int frpca_run(frpca_ctx* ctx, frpca_dmat* A, int algorithm, const frpca_config* 
               const double* omega, int64_t omega_rows, int64_t omega_cols, double* U,
               double* S, double* V, double* basis, frpca_stats* stats, int* dispatched);
 
+/* ---- validation metrics (validation.hpp:125-282) ------------
+ * Host column-major inputs. low_rank_error: |A - U diag(S) V^T| (U rows x k,
+ * S k, V cols x k) in FRPCA_NORM_FROBENIUS (dense residual when rows*cols <=
+ * entry_limit, else the cross-term identity) or FRPCA_NORM_SPECTRAL (power
+ * iteration through the SpMM kernels; counts passes over A like the
+ * reference). pc_correlation: |Pearson| of matching columns (m x k each).
+ * projector_distance: |Q1 Q1^T - Q2 Q2^T|_2 for orthonormal Q1 (m x k1),
+ * Q2 (m x k2). Messages and error codes as the reference. */
+#define FRPCA_NORM_FROBENIUS 0
+#define FRPCA_NORM_SPECTRAL 1
+#define FRPCA_ORACLE_ENTRY_LIMIT 4000000ull /* kDefaultOracleEntryLimit, validation.hpp:26 */
+int frpca_low_rank_error(frpca_ctx* ctx, frpca_dmat* A, int64_t k, const double* U, const double* S,
+                         const double* V, int norm, uint64_t entry_limit, double* out);
+int frpca_pc_correlation(frpca_ctx* ctx, int64_t m, int64_t k, const double* U_test, const double* U_ref,
+                         double* corr);
+int frpca_projector_distance(frpca_ctx* ctx, int64_t m, int64_t k1, const double* Q1, int64_t k2,
+                             const double* Q2, double* out);
+
 /* ---- timing helpers (device-side events on the ctx stream) ---------------- */
 /* Last-run per-kernel accounting: name, launches, total device ms, algorithmic
  * bytes and flops (for the roofline report). idx out of range -> 2. */

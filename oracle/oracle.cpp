@@ -785,6 +785,167 @@ static MtxTriplets mtx_parse(const std::string& path) {
     return out;
 }
 
+// ---- validation metrics (validation.hpp:125-282), restated ------------------
+// operator_two_norm (:145-165): power iteration on Op^T Op from a seeded
+// Gaussian start, Rayleigh-quotient stop at 1e-12 relative, <= 2000 steps.
+template <class Apply, class ApplyT>
+static double operator_two_norm(Apply apply, ApplyT apply_t, Index ncols, uint64_t seed) {
+    Mat g = gaussian_matrix(ncols, 1, seed);
+    std::vector<double> v(g.d.begin(), g.d.end());
+    double nv = 0.0;
+    for (double x : v) nv += x * x;
+    nv = std::sqrt(nv);
+    for (double& x : v) x /= nv;
+    double lambda_prev = 0.0;
+    for (int it = 0; it < 2000; ++it) {
+        std::vector<double> u = apply_t(apply(v));
+        double lambda = 0.0, nu = 0.0;
+        for (size_t i = 0; i < v.size(); ++i) lambda += v[i] * u[i];
+        for (double x : u) nu += x * x;
+        nu = std::sqrt(nu);
+        if (nu == 0.0) return 0.0;
+        for (size_t i = 0; i < v.size(); ++i) v[i] = u[i] / nu;
+        if (it > 0 && std::fabs(lambda - lambda_prev) <= 1e-12 * std::fabs(lambda)) {
+            lambda_prev = lambda;
+            break;
+        }
+        lambda_prev = lambda;
+    }
+    return std::sqrt(std::max(lambda_prev, 0.0));
+}
+
+// low_rank_error (:170-203): norm 0 = Frobenius, 1 = spectral
+static double low_rank_error(const Csr& A, const Mat& U, const std::vector<double>& S, const Mat& V, int norm,
+                             uint64_t entry_limit) {
+    require(U.rows == A.rows && V.rows == A.cols, "low_rank_error: shape mismatch");
+    const Index k = Index(S.size());
+    require(U.cols == k && V.cols == k, "low_rank_error: inconsistent factor widths");
+    if (norm == 1) {  // ResidualOp (:127-141)
+        auto apply = [&](const std::vector<double>& x) {
+            std::vector<double> y(size_t(A.rows), 0.0);
+            spmm(A, x.data(), A.cols, 1, y.data());
+            std::vector<double> t(size_t(k), 0.0);
+            for (Index i = 0; i < k; ++i) {
+                double d = 0.0;
+                for (Index c = 0; c < A.cols; ++c) d += V(c, i) * x[size_t(c)];
+                t[size_t(i)] = S[size_t(i)] * d;
+            }
+            for (Index r = 0; r < A.rows; ++r) {
+                double d = 0.0;
+                for (Index i = 0; i < k; ++i) d += U(r, i) * t[size_t(i)];
+                y[size_t(r)] -= d;
+            }
+            return y;
+        };
+        auto apply_t = [&](const std::vector<double>& y) {
+            std::vector<double> x(size_t(A.cols), 0.0);
+            spmm_transpose(A, y.data(), A.rows, 1, x.data());
+            std::vector<double> t(size_t(k), 0.0);
+            for (Index i = 0; i < k; ++i) {
+                double d = 0.0;
+                for (Index r = 0; r < A.rows; ++r) d += U(r, i) * y[size_t(r)];
+                t[size_t(i)] = S[size_t(i)] * d;
+            }
+            for (Index c = 0; c < A.cols; ++c) {
+                double d = 0.0;
+                for (Index i = 0; i < k; ++i) d += V(c, i) * t[size_t(i)];
+                x[size_t(c)] -= d;
+            }
+            return x;
+        };
+        return operator_two_norm(apply, apply_t, A.cols, 0x9e3779b9u);
+    }
+    const uint64_t entries = uint64_t(A.rows) * uint64_t(A.cols);
+    if (entries <= entry_limit) {
+        Mat R(A.rows, A.cols);
+        for (Index i = 0; i < A.rows; ++i)
+            for (Index p = A.row_ptr[size_t(i)]; p < A.row_ptr[size_t(i) + 1]; ++p)
+                R(i, A.col_idx[size_t(p)]) = A.values[size_t(p)];
+        for (Index c = 0; c < A.cols; ++c)
+            for (Index r = 0; r < A.rows; ++r) {
+                double d = 0.0;
+                for (Index i = 0; i < k; ++i) d += U(r, i) * S[size_t(i)] * V(c, i);
+                R(r, c) -= d;
+            }
+        double acc = 0.0;
+        for (double x : R.d) acc += x * x;
+        return std::sqrt(acc);
+    }
+    // cross-term identity (:189-202)
+    Mat W(A.rows, k);
+    spmm(A, V.d.data(), V.rows, k, W.d.data());
+    double cross = 0.0;
+    for (Index i = 0; i < k; ++i) {
+        double d = 0.0;
+        for (Index r = 0; r < A.rows; ++r) d += U(r, i) * W(r, i);
+        cross += S[size_t(i)] * d;
+    }
+    double m2 = 0.0;
+    for (Index i = 0; i < k; ++i)
+        for (Index j = 0; j < k; ++j) {
+            double gu = 0.0, gv = 0.0;
+            for (Index r = 0; r < A.rows; ++r) gu += U(r, i) * U(r, j);
+            for (Index c = 0; c < A.cols; ++c) gv += V(c, i) * V(c, j);
+            m2 += S[size_t(i)] * S[size_t(j)] * gu * gv;
+        }
+    double a2 = 0.0;
+    for (double x : A.values) a2 += x * x;
+    return std::sqrt(std::max(a2 - 2.0 * cross + m2, 0.0));
+}
+
+// pc_correlation (:228-246)
+static std::vector<double> pc_correlation(const Mat& Ut, const Mat& Ur) {
+    require(Ut.rows == Ur.rows && Ut.cols == Ur.cols, "pc_correlation: shape mismatch");
+    require(Ut.rows >= 2, "pc_correlation: need at least two samples");
+    std::vector<double> corr(size_t(Ut.cols));
+    for (Index j = 0; j < Ut.cols; ++j) {
+        double mx = 0.0, my = 0.0;
+        for (Index r = 0; r < Ut.rows; ++r) { mx += Ut(r, j); my += Ur(r, j); }
+        mx /= double(Ut.rows);
+        my /= double(Ut.rows);
+        double xy = 0.0, xx = 0.0, yy = 0.0;
+        for (Index r = 0; r < Ut.rows; ++r) {
+            const double x = Ut(r, j) - mx, y = Ur(r, j) - my;
+            xy += x * y; xx += x * x; yy += y * y;
+        }
+        const double denom = std::sqrt(xx) * std::sqrt(yy);
+        if (denom == 0.0) throw std::invalid_argument("pc_correlation: zero-variance column " + std::to_string(j));
+        corr[size_t(j)] = std::fabs(xy / denom);
+    }
+    return corr;
+}
+
+// projector_distance (:264-282)
+static double projector_distance(const Mat& Q1, const Mat& Q2) {
+    require(Q1.rows == Q2.rows, "projector_distance: row mismatch");
+    auto check = [](const Mat& Q, const char* which) {
+        double mx = 0.0;
+        for (Index i = 0; i < Q.cols; ++i)
+            for (Index j = 0; j < Q.cols; ++j) {
+                double d = 0.0;
+                for (Index r = 0; r < Q.rows; ++r) d += Q(r, i) * Q(r, j);
+                mx = std::max(mx, std::fabs(d - (i == j ? 1.0 : 0.0)));
+            }
+        if (mx > 1e-8)
+            throw std::invalid_argument(std::string("projector_distance: ") + which + " is not orthonormal within 1e-8");
+    };
+    check(Q1, "first basis");
+    check(Q2, "second basis");
+    auto apply = [&](const std::vector<double>& x) {
+        std::vector<double> y(size_t(Q1.rows), 0.0);
+        for (const Mat* Q : {&Q1, &Q2}) {
+            const double sgn = Q == &Q1 ? 1.0 : -1.0;
+            for (Index i = 0; i < Q->cols; ++i) {
+                double d = 0.0;
+                for (Index r = 0; r < Q->rows; ++r) d += (*Q)(r, i) * x[size_t(r)];
+                for (Index r = 0; r < Q->rows; ++r) y[size_t(r)] += sgn * (*Q)(r, i) * d;
+            }
+        }
+        return y;
+    };
+    return operator_two_norm(apply, apply, Q1.rows, 0x51f15eedu);
+}
+
 // ---- validation oracle: one-sided Jacobi SVD (validation.hpp:34-121) -------
 static void oracle_svd(const Mat& Ain, Mat& U, std::vector<double>& S, Mat& V) {
     require(Ain.rows >= 1 && Ain.cols >= 1, "oracle_svd: empty matrix");
@@ -967,6 +1128,25 @@ void orc_mtx_entries(void* h, int64_t* r, int64_t* c, double* v) {
     for (size_t i = 0; i < t->e.size(); ++i) { r[i] = t->e[i].row; c[i] = t->e[i].col; v[i] = t->e[i].value; }
 }
 void orc_mtx_free(void* h) { delete static_cast<MtxTriplets*>(h); }
+
+int orc_low_rank_error(void* h, int64_t k, const double* U, const double* S, const double* V, int norm,
+                       uint64_t entry_limit, double* out) {
+    return guarded([&] {
+        const Csr& A = *static_cast<Csr*>(h);
+        std::vector<double> Sv(S, S + k);
+        *out = low_rank_error(A, view_colmajor(U, A.rows, k, A.rows), Sv, view_colmajor(V, A.cols, k, A.cols), norm,
+                              entry_limit);
+    });
+}
+int orc_pc_correlation(int64_t m, int64_t k, const double* Ut, const double* Ur, double* corr) {
+    return guarded([&] {
+        std::vector<double> c = pc_correlation(view_colmajor(Ut, m, k, m), view_colmajor(Ur, m, k, m));
+        std::memcpy(corr, c.data(), sizeof(double) * c.size());
+    });
+}
+int orc_projector_distance(int64_t m, int64_t k1, const double* Q1, int64_t k2, const double* Q2, double* out) {
+    return guarded([&] { *out = projector_distance(view_colmajor(Q1, m, k1, m), view_colmajor(Q2, m, k2, m)); });
+}
 
 int orc_orth(int64_t m, int64_t l, const double* M, double* Q) {
     return guarded([&] {

@@ -66,6 +66,9 @@ def lib():
                                    C.POINTER(_i64)]
         L.orc_mtx_entries.argtypes = [C.c_void_p, C.POINTER(_i64), C.POINTER(_i64), _dp]
         L.orc_mtx_entries.restype = None
+        L.orc_low_rank_error.argtypes = [C.c_void_p, _i64, _dp, _dp, _dp, C.c_int, _u64, _dp]
+        L.orc_pc_correlation.argtypes = [_i64, _i64, _dp, _dp, _dp]
+        L.orc_projector_distance.argtypes = [_i64, _i64, _dp, _i64, _dp, _dp]
         L.orc_mtx_free.argtypes = [C.c_void_p]
         L.orc_mtx_free.restype = None
         L.orc_eig_svd.argtypes = [_i64, _i64, _dp, _dp, _dp, _dp]
@@ -263,6 +266,39 @@ def read_matrix_market(path: str):
     finally:
         lib().orc_mtx_free(h)
     return rows.value, cols.value, r, c, v
+
+
+FROBENIUS, SPECTRAL = 0, 1
+ENTRY_LIMIT = 4_000_000  # validation.hpp:26
+
+
+def low_rank_error(A: "Csr", U, S, V, norm: int, entry_limit: int = ENTRY_LIMIT) -> float:
+    """validation.hpp:170-203."""
+    U, V = np.asfortranarray(U, dtype=np.float64), np.asfortranarray(V, dtype=np.float64)
+    S = np.ascontiguousarray(S, dtype=np.float64)
+    out = C.c_double(0.0)
+    _check(lib().orc_low_rank_error(A._h, S.size, _d(U), _d(S), _d(V), norm, entry_limit, C.byref(out)))
+    return out.value
+
+
+def pc_correlation(Ut, Ur) -> np.ndarray:
+    """validation.hpp:228-246."""
+    Ut, Ur = np.asfortranarray(Ut, dtype=np.float64), np.asfortranarray(Ur, dtype=np.float64)
+    if Ut.shape != Ur.shape:
+        raise ValueError("pc_correlation: shape mismatch")
+    corr = np.empty(Ut.shape[1])
+    _check(lib().orc_pc_correlation(Ut.shape[0], Ut.shape[1], _d(Ut), _d(Ur), _d(corr)))
+    return corr
+
+
+def projector_distance(Q1, Q2) -> float:
+    """validation.hpp:264-282."""
+    Q1, Q2 = np.asfortranarray(Q1, dtype=np.float64), np.asfortranarray(Q2, dtype=np.float64)
+    if Q1.shape[0] != Q2.shape[0]:
+        raise ValueError("projector_distance: row mismatch")
+    out = C.c_double(0.0)
+    _check(lib().orc_projector_distance(Q1.shape[0], Q1.shape[1], _d(Q1), Q2.shape[1], _d(Q2), C.byref(out)))
+    return out.value
 
 
 def orth(M: np.ndarray) -> np.ndarray:

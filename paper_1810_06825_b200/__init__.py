@@ -30,6 +30,8 @@ __all__ = [
     "spmm", "spmm_transpose", "transpose", "gaussian_matrix", "lu_basis", "orth", "eig_svd",
     "frpca", "frpcat", "auto_pca", "basic_rpca", "basic_rpcat", "mix_seed", "kSketchStreamTag",
     "read_matrix_market", "load_matrix_market", "write_matrix_market", "IoError",
+    "ErrorNorm", "low_rank_error", "best_rank_k_error", "pc_correlation", "projector_distance",
+    "AccuracyReport", "make_accuracy_report", "kDefaultOracleEntryLimit",
 ]
 
 kSketchStreamTag = 0xA11CE  # randsvd.hpp:63
@@ -532,3 +534,97 @@ def auto_pca(A: SparseMatrixCsr, cfg: PcaConfig, stats: RunStats | None = None,
     """randsvd.hpp:336-351: frpca when rows < cols, else frpcat (square -> frpcat)."""
     svd, d = _run(_lib.ALGO_AUTO, A, cfg, stats, None, ctx)
     return AutoPcaResult(svd, PcaAlgorithm(d))
+
+
+# ---- validation metrics (validation.hpp:125-332, SURVEY §8 f3) -------------------
+kDefaultOracleEntryLimit = 4_000_000  # validation.hpp:26
+
+
+class ErrorNorm(enum.IntEnum):
+    """validation.hpp:17."""
+    Frobenius = 0
+    Spectral = 1
+
+
+def low_rank_error(A: SparseMatrixCsr, r: SvdResult, norm: ErrorNorm,
+                   entry_limit: int = kDefaultOracleEntryLimit, ctx: Context | None = None) -> float:
+    """validation.hpp:170-203 on the GPU: |A - U diag(S) V^T| (spectral by
+    matrix-free power iteration through the SpMM kernels)."""
+    U, S, V = _colmajor(r.U), np.ascontiguousarray(r.S, dtype=np.float64), _colmajor(r.V)
+    if U.shape[0] != A.rows() or V.shape[0] != A.cols():
+        raise ValueError("low_rank_error: shape mismatch")
+    if U.shape[1] != S.size or V.shape[1] != S.size:
+        raise ValueError("low_rank_error: inconsistent factor widths")
+    ctx = ctx or default_context()
+    out = C.c_double(0.0)
+    _lib.check(_lib.load().frpca_low_rank_error(ctx._h, A.device(ctx), S.size, _ptr(U), _ptr(S), _ptr(V),
+                                                int(norm), int(entry_limit), C.byref(out)))
+    return out.value
+
+
+def best_rank_k_error(singular_values, k: int, norm: ErrorNorm) -> float:
+    """validation.hpp:207-215 (host): sigma_{k+1} (spectral) or the root of
+    the tail sum of squares (Frobenius)."""
+    if k < 0:
+        raise ValueError("best_rank_k_error: negative k")
+    s = np.asarray(singular_values, dtype=np.float64)
+    if k >= s.size:
+        return 0.0
+    return float(s[k]) if norm == ErrorNorm.Spectral else float(np.sqrt(np.sum(s[k:] ** 2)))
+
+
+def pc_correlation(U_test, U_ref, ctx: Context | None = None) -> np.ndarray:
+    """validation.hpp:228-246 on the GPU: |Pearson correlation| per column."""
+    A, B = _colmajor(U_test), _colmajor(U_ref)
+    if A.shape != B.shape:
+        raise ValueError("pc_correlation: shape mismatch")
+    if A.shape[0] < 2:
+        raise ValueError("pc_correlation: need at least two samples")
+    ctx = ctx or default_context()
+    corr = np.empty(A.shape[1])
+    _lib.check(_lib.load().frpca_pc_correlation(ctx._h, A.shape[0], A.shape[1], _ptr(A), _ptr(B), _ptr(corr)))
+    return corr
+
+
+def projector_distance(Q1, Q2, ctx: Context | None = None) -> float:
+    """validation.hpp:264-282 on the GPU: |Q1 Q1^T - Q2 Q2^T|_2."""
+    A, B = _colmajor(Q1), _colmajor(Q2)
+    if A.shape[0] != B.shape[0]:
+        raise ValueError("projector_distance: row mismatch")
+    ctx = ctx or default_context()
+    out = C.c_double(0.0)
+    _lib.check(_lib.load().frpca_projector_distance(ctx._h, A.shape[0], A.shape[1], _ptr(A), B.shape[1], _ptr(B),
+                                                    C.byref(out)))
+    return out.value
+
+
+@dataclasses.dataclass
+class AccuracyReport:
+    """validation.hpp:287-294 (field order = to_json's key order, :321-330)."""
+    singular_value_rel_err: list
+    recon_err_frobenius: float
+    recon_err_spectral: float
+    best_rank_k_err: float
+    eps_equivalent: float
+    pc_correlations: list
+
+    def to_json(self) -> dict:
+        return dataclasses.asdict(self)
+
+
+def make_accuracy_report(A: SparseMatrixCsr, r: SvdResult, oracle_S, oracle_U,
+                         ctx: Context | None = None) -> AccuracyReport:
+    """validation.hpp:297-319, with the oracle's singular values / left
+    vectors supplied by the caller (the metrics run on the GPU)."""
+    k = r.S.size
+    oS = np.asarray(oracle_S, dtype=np.float64)
+    if oS.size < k:
+        raise ValueError("make_accuracy_report: oracle has fewer values than k")
+    rel = [abs(float(r.S[i])) if oS[i] == 0.0 else abs(float(r.S[i]) - float(oS[i])) / float(oS[i])
+           for i in range(k)]
+    fro = low_rank_error(A, r, ErrorNorm.Frobenius, ctx=ctx)
+    spec = low_rank_error(A, r, ErrorNorm.Spectral, ctx=ctx)
+    best = best_rank_k_error(oS, k, ErrorNorm.Spectral)
+    eps = 0.0 if best == 0.0 else spec / best - 1.0
+    corr = pc_correlation(r.U, np.asarray(oracle_U)[:, :k], ctx=ctx)
+    return AccuracyReport(rel, fro, spec, best, eps, corr.tolist())

@@ -51,6 +51,9 @@ SIGNATURES = {
     "frpca_mtx_free": (None, [_vp]),
     "frpca_mtx_write": (C.c_int, [C.c_char_p, _i64, _i64, _vp, _vp, _vp]),
     "frpca_csr_from_triplets": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _lp, _vp, _vp, _vp]),
+    "frpca_low_rank_error": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, C.c_int, _u64, _dp]),
+    "frpca_pc_correlation": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
+    "frpca_projector_distance": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _dp]),
     "frpca_dmat_info": (C.c_int, [_vp, _lp, _lp, _lp]),
     "frpca_dmat_pass_count": (C.c_int, [_vp, C.POINTER(_u64)]),
     "frpca_dmat_reset_pass_count": (C.c_int, [_vp]),

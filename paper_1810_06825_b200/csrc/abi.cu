@@ -379,6 +379,57 @@ int frpca_csr_from_triplets(frpca_ctx* c, int64_t rows, int64_t cols, int64_t n,
     });
 }
 
+int frpca_low_rank_error(frpca_ctx* c, frpca_dmat* M, int64_t k, const double* U, const double* S, const double* V,
+                         int norm, uint64_t entry_limit, double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        require(M != nullptr && out != nullptr && k >= 0, "low_rank_error: null argument");
+        require(norm == FRPCA_NORM_FROBENIUS || norm == FRPCA_NORM_SPECTRAL, "low_rank_error: unknown norm");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        const int64_t m = M->A.rows, n = M->A.cols;
+        cudaStream_t s = c->stream;
+        DBuf<double> dU(size_t(std::max<int64_t>(m * k, 1)), s), dS(size_t(std::max<int64_t>(k, 1)), s),
+            dV(size_t(std::max<int64_t>(n * k, 1)), s);
+        if (k) {
+            FB_CUDA(cudaMemcpyAsync(dU.get(), U, sizeof(double) * m * k, cudaMemcpyHostToDevice, s));
+            FB_CUDA(cudaMemcpyAsync(dS.get(), S, sizeof(double) * k, cudaMemcpyHostToDevice, s));
+            FB_CUDA(cudaMemcpyAsync(dV.get(), V, sizeof(double) * n * k, cudaMemcpyHostToDevice, s));
+        }
+        *out = low_rank_error_device(*c, *M, k, dU.get(), dS.get(), dV.get(), norm, entry_limit);
+    });
+}
+
+int frpca_pc_correlation(frpca_ctx* c, int64_t m, int64_t k, const double* Ut, const double* Ur, double* corr) {
+    return guarded([&] {
+        check_ctx(c);
+        require(m >= 0 && k >= 0 && corr != nullptr, "pc_correlation: null argument");
+        require(m >= 2, "pc_correlation: need at least two samples");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        DBuf<double> a(size_t(std::max<int64_t>(m * k, 1)), c->stream), b(size_t(std::max<int64_t>(m * k, 1)), c->stream);
+        if (k) {
+            FB_CUDA(cudaMemcpyAsync(a.get(), Ut, sizeof(double) * m * k, cudaMemcpyHostToDevice, c->stream));
+            FB_CUDA(cudaMemcpyAsync(b.get(), Ur, sizeof(double) * m * k, cudaMemcpyHostToDevice, c->stream));
+        }
+        pc_correlation_device(*c, m, k, a.get(), b.get(), corr);
+    });
+}
+
+int frpca_projector_distance(frpca_ctx* c, int64_t m, int64_t k1, const double* Q1, int64_t k2, const double* Q2,
+                             double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        require(m >= 1 && k1 >= 0 && k2 >= 0 && out != nullptr, "projector_distance: null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        DBuf<double> a(size_t(std::max<int64_t>(m * k1, 1)), c->stream), b(size_t(std::max<int64_t>(m * k2, 1)), c->stream);
+        if (k1) FB_CUDA(cudaMemcpyAsync(a.get(), Q1, sizeof(double) * m * k1, cudaMemcpyHostToDevice, c->stream));
+        if (k2) FB_CUDA(cudaMemcpyAsync(b.get(), Q2, sizeof(double) * m * k2, cudaMemcpyHostToDevice, c->stream));
+        *out = projector_distance_device(*c, m, k1, a.get(), k2, b.get());
+    });
+}
+
 int frpca_orth(frpca_ctx* c, int64_t m, int64_t l, const double* Mh, double* Q) {
     return guarded([&] {
         check_ctx(c);

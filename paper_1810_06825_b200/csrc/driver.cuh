@@ -31,6 +31,12 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st);
 void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left);
 uint64_t mix_seed(uint64_t seed, uint64_t tag);
 
+// validation.cu (validation.hpp:125-282); U, S, V, Q device, column-major
+double low_rank_error_device(Ctx& c, DMat& M, int64_t k, const double* U, const double* S, const double* V,
+                             int norm, uint64_t entry_limit);
+void pc_correlation_device(Ctx& c, int64_t m, int64_t k, const double* Ut, const double* Ur, double* corr_host);
+double projector_distance_device(Ctx& c, int64_t m, int64_t k1, const double* Q1, int64_t k2, const double* Q2);
+
 // comm.cu: in-place sum over ranks (no-op on one GPU).
 void allreduce_sum(Ctx& c, double* x, int64_t count);
 void comm_init(Ctx& c, int rank, int world, const void* id128);

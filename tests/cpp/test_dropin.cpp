@@ -118,6 +118,21 @@ int main() {
         CHECK(L.rowPtr() == W.rowPtr() && L.colIdx() == W.colIdx() && L.values() == W.values());
         CHECK((throws<frpca::IoError>([] { frpca::load_matrix_market<double>("/nonexistent/x.mtx"); })));
     }
+    // validation metrics (validation.hpp:170-282): zero factors give |A|
+    {
+        Csr D2 = diag_sparse({3.0, 4.0}, 2, 2);
+        frpca::SvdResult<double> z;
+        z.U = frpca::Matrix<double>(2, 1);
+        z.U(0, 0) = 1.0;
+        z.S = frpca::Vector<double>(1);
+        z.V = z.U;
+        CHECK(std::abs(frpca::low_rank_error(D2, z, frpca::ErrorNorm::Frobenius) - 5.0) < 1e-12);
+        CHECK(std::abs(frpca::low_rank_error(D2, z, frpca::ErrorNorm::Spectral) - 4.0) < 1e-8);
+        frpca::Matrix<double> Q1(6, 2), Q2(6, 2);
+        Q1(0, 0) = Q1(1, 1) = 1.0;
+        Q2(2, 0) = Q2(3, 1) = 1.0;
+        CHECK(std::abs(frpca::projector_distance(Q1, Q2) - 1.0) < 1e-10);
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }
