@@ -178,7 +178,11 @@ int frpca_ctx_destroy(frpca_ctx* c) {
         if (c->timer_a) cudaEventDestroy(c->timer_a);
         if (c->timer_b) cudaEventDestroy(c->timer_b);
         if (c->solver) cusolverDnDestroy(c->solver);
-        if (c->stream) cudaStreamDestroy(c->stream);
+        c->omega_raw.release();  // stream-ordered free before the stream goes
+        if (c->stream) {
+            cudaStreamSynchronize(c->stream);
+            cudaStreamDestroy(c->stream);
+        }
         delete c;
     });
 }

@@ -50,6 +50,7 @@ struct PanelPlan {
     ItemList hot;        // chunk items, panel-major; slots per row in entry order
     ItemList cold;       // work list of the other rows
     DBuf<int32_t> counter;
+    DBuf<double> part;   // chunk partials, kept with the plan (grown on demand)
 };
 
 // Device CSR: int64 row_ptr (8 B/row), int32 col ids, fp64 values (12 B/nnz).
@@ -82,6 +83,7 @@ struct Ctx {
     int num_sms = 148;
     std::mutex mu;  // the ABI serialises calls on one context
     cudaEvent_t timer_a = nullptr, timer_b = nullptr;
+    DBuf<uint64_t> omega_raw;  // raw-word buffer of the Omega generator, kept (grown on demand)
 
     // profiling: events around each launch, folded into per-kernel aggregates
     bool prof = false;

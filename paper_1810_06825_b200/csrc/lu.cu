@@ -288,9 +288,17 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
             if (tim) clk[0] = clock64();
             grid.sync();
             if (tim) clk[1] = clock64();
-            Cand c{-1.0, INT32_MAX, -1};
-            for (int k = tid; k < int(gridDim.x); k += kT) cand_merge(c, cand[k]);
-            const Cand best = block_best<kT>(c, shc);
+            // every warp reduces all CTAs' candidates itself (a total order:
+            // the same winner everywhere, no block barrier)
+            Cand best{-1.0, INT32_MAX, -1};
+            for (int k = (tid & 31); k < int(gridDim.x); k += 32) cand_merge(best, cand[k]);
+            for (int o = 16; o; o >>= 1) {
+                Cand x;
+                x.v = __shfl_xor_sync(0xffffffffu, best.v, o);
+                x.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
+                x.row = __shfl_xor_sync(0xffffffffu, best.row, o);
+                cand_merge(best, x);
+            }
             if (!(best.v > tol) || best.row < 0) {  // zero pivot (:81)
                 if (blockIdx.x == 0 && tid == 0) *err = 1;
                 return;  // uniform across the grid

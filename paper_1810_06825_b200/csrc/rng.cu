@@ -337,10 +337,11 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     }
     // batches of segments: raw words -> per-chunk counts -> scan -> normals
     const int64_t seg_per_batch = std::max<int64_t>(1, (int64_t(1) << 30) / J);
-    DBuf<uint64_t> raw;
+    DBuf<uint64_t>& raw = c.omega_raw;  // kept on the context (see DESIGN: pool remaps)
     {
         Prof pa(c, "omega_alloc", 0.0, 0.0);
-        raw.alloc(size_t(std::min(K, seg_per_batch) * J), s);
+        const size_t need = size_t(std::min(K, seg_per_batch) * J);
+        if (raw.n < need) raw.alloc(need, s);
     }
     int64_t pairs_done = 0;  // accepted attempts emitted so far
     for (int64_t seg0 = 0; 2 * pairs_done < count; seg0 += seg_per_batch) {

@@ -419,7 +419,10 @@ void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, c
     const double bytes = 12.0 * T.nnz + 8.0 * (T.rows + 1) + 8.0 * ncols * (T.cols + T.rows);
     Prof prof(c, tag, bytes, 2.0 * T.nnz * ncols);
     const size_t slots = size_t(std::max(P.hot.nslots, P.cold.nslots));
-    DBuf<double> part(slots * size_t(w), c.stream);
+    // persistent with the plan: a per-call multi-GB allocation can remap pool
+    // memory every run (measured: ~150 ms per call at C3)
+    DBuf<double>& part = const_cast<PanelPlan&>(P).part;
+    if (part.n < slots * size_t(w)) part.alloc(slots * size_t(w), c.stream);
     for (int64_t off = 0; off < ncols; off += 256) {
         const int nc = int(std::min<int64_t>(256, ncols - off));
         FB_CUDA(cudaMemsetAsync(P.counter.get(), 0, sizeof(int32_t), c.stream));
