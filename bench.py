@@ -310,6 +310,15 @@ def run_gpu_arm(args, cfg):
     hV = alloc(n_loc * k, np.float64)
 
     def run_e2e():
+        if world == 1:
+            # the one-shot host-CSR call (frpca_run_csr): upload, run, outputs
+            # back to pinned host memory; the sketch overlaps the upload
+            _lib.check(L.frpca_run_csr(ctx._h, shard_["rows"], shard_["cols"], nnz_loc,
+                                       shard_["rp"].ctypes.data, shard_["ci"].ctypes.data,
+                                       shard_["va"].ctypes.data, algo, C.byref(cfg_host), None, 0, 0,
+                                       C.c_void_p(hU.ctypes.data), C.c_void_p(hS.ctypes.data),
+                                       C.c_void_p(hV.ctypes.data), None, None, None))
+            return
         h = upload()
         try:
             _lib.check(L.frpca_run(ctx._h, h, algo, C.byref(cfg_host), None, 0, 0,

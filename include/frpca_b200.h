@@ -180,6 +180,16 @@ int frpca_pc_correlation(frpca_ctx* ctx, int64_t m, int64_t k, const double* U_t
 int frpca_projector_distance(frpca_ctx* ctx, int64_t m, int64_t k1, const double* Q1, int64_t k2,
                              const double* Q2, double* out);
 
+/* One-shot run from a host CSR (upload, run, release): the reference-facing
+ * call for a matrix that is not kept on the device. The sketch depends only on
+ * the seed and the shape, so it is generated on a second stream while the CSR
+ * is uploaded and validated and the transpose is built. Same arguments,
+ * outputs and errors as frpca_dmat_upload + frpca_run; single GPU. */
+int frpca_run_csr(frpca_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                  const int64_t* col_idx, const double* values, int algorithm, const frpca_config* cfg,
+                  const double* omega, int64_t omega_rows, int64_t omega_cols, double* U, double* S,
+                  double* V, double* basis, frpca_stats* stats, int* dispatched);
+
 /* ---- timing helpers (device-side events on the ctx stream) ---------------- */
 /* Last-run per-kernel accounting: name, launches, total device ms, algorithmic
  * bytes and flops (for the roofline report). idx out of range -> 2. */

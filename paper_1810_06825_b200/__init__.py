@@ -30,7 +30,7 @@ __all__ = [
     "spmm", "spmm_transpose", "transpose", "gaussian_matrix", "lu_basis", "orth", "eig_svd",
     "frpca", "frpcat", "auto_pca", "basic_rpca", "basic_rpcat", "mix_seed", "kSketchStreamTag",
     "read_matrix_market", "load_matrix_market", "write_matrix_market", "IoError",
-    "ErrorNorm", "low_rank_error", "best_rank_k_error", "pc_correlation", "projector_distance",
+    "run_csr", "ErrorNorm", "low_rank_error", "best_rank_k_error", "pc_correlation", "projector_distance",
     "AccuracyReport", "make_accuracy_report", "kDefaultOracleEntryLimit",
 ]
 
@@ -497,6 +497,41 @@ def _run(algo: int, A: SparseMatrixCsr, cfg: PcaConfig, stats: RunStats | None, 
     if stats is not None:
         stats.sketch_seconds = st.sketch_seconds
         stats.power_seconds = st.power_seconds
+        stats.finalize_seconds = st.finalize_seconds
+        stats.passes_over_matrix = int(st.passes_over_matrix)
+        if stats.capture_basis:
+            stats.basis = basis
+    return SvdResult(U, S, V), disp.value
+
+
+def run_csr(A: SparseMatrixCsr, cfg: PcaConfig, algorithm: "PcaAlgorithm" = None, stats: RunStats | None = None,
+            ctx: Context | None = None) -> tuple[SvdResult, int]:
+    """One-shot run from the host CSR (frpca_run_csr): upload, run, release,
+    with the sketch generated on a second stream during the upload. Returns
+    (result, dispatched algorithm)."""
+    ctx = ctx or default_context()
+    algo = _lib.ALGO_AUTO if algorithm is None else int(algorithm)
+    m, n = A.rows(), A.cols()
+    eff = algo if algo != _lib.ALGO_AUTO else (_lib.ALGO_FRPCA if m < n else _lib.ALGO_FRPCAT)
+    k = max(int(cfg.k), 0)
+    l = cfg.k + cfg.oversample
+    U = np.empty((m, k), order="F")
+    S = np.empty(k)
+    V = np.empty((n, k), order="F")
+    basis = None
+    if stats is not None and stats.capture_basis and l >= 1:
+        basis = np.empty((m if eff in (_lib.ALGO_FRPCA, _lib.ALGO_BASIC_RPCA) else n, l), order="F")
+    st = _lib.FrpcaStats()
+    disp = C.c_int(-1)
+    ccfg = cfg.to_c()
+    rp = np.ascontiguousarray(A.rowPtr(), dtype=np.int64)
+    ci = np.ascontiguousarray(A.colIdx(), dtype=np.int64)
+    va = np.ascontiguousarray(A.values(), dtype=np.float64)
+    _lib.check(_lib.load().frpca_run_csr(ctx._h, m, n, int(rp[-1]), _ptr(rp), _ptr(ci), _ptr(va), algo,
+                                         C.byref(ccfg), None, 0, 0, _ptr(U), _ptr(S), _ptr(V), _ptr(basis),
+                                         C.byref(st), C.byref(disp)))
+    if stats is not None:
+        stats.sketch_seconds, stats.power_seconds = st.sketch_seconds, st.power_seconds
         stats.finalize_seconds = st.finalize_seconds
         stats.passes_over_matrix = int(st.passes_over_matrix)
         if stats.capture_basis:

@@ -51,6 +51,8 @@ SIGNATURES = {
     "frpca_mtx_free": (None, [_vp]),
     "frpca_mtx_write": (C.c_int, [C.c_char_p, _i64, _i64, _vp, _vp, _vp]),
     "frpca_csr_from_triplets": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _lp, _vp, _vp, _vp]),
+    "frpca_run_csr": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, C.c_int, C.POINTER(FrpcaConfig), _vp,
+                                _i64, _i64, _vp, _vp, _vp, _vp, C.POINTER(FrpcaStats), C.POINTER(C.c_int)]),
     "frpca_low_rank_error": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, C.c_int, _u64, _dp]),
     "frpca_pc_correlation": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "frpca_projector_distance": (C.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _dp]),

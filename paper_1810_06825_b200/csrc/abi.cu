@@ -6,6 +6,9 @@
 #include <cstring>
 #include <string>
 
+#include <exception>
+#include <thread>
+
 #include "driver.cuh"
 
 using namespace fb;
@@ -178,6 +181,14 @@ int frpca_ctx_destroy(frpca_ctx* c) {
         if (c->timer_a) cudaEventDestroy(c->timer_a);
         if (c->timer_b) cudaEventDestroy(c->timer_b);
         if (c->solver) cusolverDnDestroy(c->solver);
+        for (auto& b : c->slots) b.release();
+        if (c->side) {
+            for (auto& b : c->side->slots) b.release();
+            c->side->omega_raw.release();
+            cudaStreamSynchronize(c->side->stream);
+            cudaStreamDestroy(c->side->stream);
+            c->side.reset();
+        }
         c->omega_raw.release();  // stream-ordered free before the stream goes
         if (c->stream) {
             cudaStreamSynchronize(c->stream);
@@ -492,6 +503,99 @@ int frpca_run(frpca_ctx* c, frpca_dmat* M, int algorithm, const frpca_config* cf
         if (algo == FRPCA_ALGO_FRPCA) run_frpca(*c, *M, a, stats);
         else if (algo == FRPCA_ALGO_FRPCAT) run_frpcat(*c, *M, a, stats);
         else run_basic(*c, *M, a, stats, algo == FRPCA_ALGO_BASIC_RPCAT);
+    });
+}
+
+// One-shot run from a host CSR: upload + run + release, with the sketch (which
+// depends only on the seed and the shape) generated on a second stream by a
+// second host thread while the CSR is uploaded and the device transpose built.
+int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                  const int64_t* col_idx, const double* values, int algorithm, const frpca_config* cfg,
+                  const double* omega, int64_t omega_rows, int64_t omega_cols, double* U, double* S, double* V,
+                  double* basis, frpca_stats* stats, int* dispatched) {
+    return guarded([&] {
+        check_ctx(c);
+        require(cfg != nullptr, "frpca_run: null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        int algo = algorithm;
+        if (algo == FRPCA_ALGO_AUTO) algo = (rows < cols) ? FRPCA_ALGO_FRPCA : FRPCA_ALGO_FRPCAT;
+        // shape of the sketch each algorithm draws (randsvd.hpp:110, :150, :239, :291)
+        const int64_t l = cfg->k + cfg->oversample, q = cfg->passes;
+        int64_t orow = 0, ocol = 0;
+        bool ok = !omega && !(cfg->flags & FRPCA_FLAG_HOST_OMEGA) && c->world == 1 && cfg->k >= 1 &&
+                  cfg->oversample >= 0 && l >= 1 && rows >= 1 && cols >= 1;
+        if (ok) {
+            if (algo == FRPCA_ALGO_FRPCA) {
+                ok = rows <= cols && q >= 2 && l <= rows;
+                if (q % 2 == 0) { orow = cols; ocol = l; } else { orow = rows; ocol = l; }
+            } else if (algo == FRPCA_ALGO_FRPCAT) {
+                ok = rows >= cols && q >= 2 && l <= cols;
+                if (q % 2 == 0) { orow = l; ocol = rows; } else { orow = cols; ocol = l; }
+            } else if (algo == FRPCA_ALGO_BASIC_RPCA) {
+                ok = cfg->power >= 0 && l <= std::min(rows, cols);
+                orow = cols; ocol = l;
+            } else if (algo == FRPCA_ALGO_BASIC_RPCAT) {
+                ok = cfg->power >= 0 && l <= std::min(rows, cols);
+                orow = l; ocol = rows;
+            } else {
+                ok = false;
+            }
+        }
+        DBuf<double>* pre = nullptr;
+        std::exception_ptr side_err;
+        std::thread side_thread;
+        if (ok) {
+            if (!c->side) {
+                auto sd = std::make_unique<Ctx>();
+                sd->device = c->device;
+                sd->num_sms = c->num_sms;
+                FB_CUDA(cudaStreamCreateWithFlags(&sd->stream, cudaStreamNonBlocking));
+                c->side = std::move(sd);
+            }
+            Ctx* side = c->side.get();
+            const uint64_t seed = mix_seed(cfg->seed, 0xA11CEull);
+            const int64_t count = orow * ocol;
+            side_thread = std::thread([side, seed, count, &pre, &side_err] {
+                try {
+                    FB_CUDA(cudaSetDevice(side->device));
+                    pre = &side->slot(0, size_t(count));  // kept: swapped with the run's slot
+                    gaussian_stream_device(*side, seed, count, pre->get());
+                    FB_CUDA(cudaStreamSynchronize(side->stream));
+                } catch (...) {
+                    side_err = std::current_exception();
+                }
+            });
+        }
+        std::unique_ptr<frpca_dmat> M;
+        try {
+            M.reset(new frpca_dmat);
+            M->ctx = c;
+            M->grows = rows;
+            M->gcols = cols;
+            dcsr_upload_build(*c, *M, rows, cols, nnz, row_ptr, col_idx, values);
+        } catch (...) {
+            if (side_thread.joinable()) side_thread.join();
+            throw;
+        }
+        if (side_thread.joinable()) side_thread.join();
+        if (side_err) std::rethrow_exception(side_err);
+        RunArgs a;
+        a.cfg = *cfg;
+        a.omega = omega;
+        a.omega_rows = omega_rows;
+        a.omega_cols = omega_cols;
+        a.U = U; a.S = S; a.V = V; a.basis = basis;
+        a.device_io = (cfg->flags & FRPCA_FLAG_DEVICE_IO) != 0;
+        a.pre = ok ? pre : nullptr;
+        if (dispatched) *dispatched = algo;
+        require(algo == FRPCA_ALGO_FRPCA || algo == FRPCA_ALGO_FRPCAT || algo == FRPCA_ALGO_BASIC_RPCA ||
+                    algo == FRPCA_ALGO_BASIC_RPCAT,
+                "frpca_run: unknown algorithm");
+        if (algo == FRPCA_ALGO_FRPCA) run_frpca(*c, *M, a, stats);
+        else if (algo == FRPCA_ALGO_FRPCAT) run_frpcat(*c, *M, a, stats);
+        else run_basic(*c, *M, a, stats, algo == FRPCA_ALGO_BASIC_RPCAT);
+        FB_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
 

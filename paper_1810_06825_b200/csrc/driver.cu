@@ -103,6 +103,21 @@ void sketch_stream(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, double*
     }
 }
 
+// Omega (rows x cols, column-major stream order) into dst: the pre-generated
+// stream when frpca_run_csr overlapped it with the upload, else generated now.
+static void sketch_into(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, DBuf<double>& dst) {
+    const size_t count = size_t(rows) * size_t(cols);
+    if (a.pre && a.pre->get() && a.pre->n >= count && !a.omega) {
+        cudaStream_t ps = a.pre->s;
+        std::swap(dst, *a.pre);  // both buffers stay allocated (workspace slots)
+        dst.s = c.stream;
+        a.pre->s = ps;
+        return;
+    }
+    if (dst.n < count) dst.alloc(count, c.stream);
+    sketch_stream(c, a, rows, cols, dst.get());
+}
+
 static void check_common(const frpca_config& cfg) {  // randsvd.hpp:78-81
     require(cfg.k >= 1, "config: rank k must be >= 1");
     require(cfg.oversample >= 0, "config: oversampling must be >= 0");
@@ -139,15 +154,16 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     const uint64_t passes0 = M.passes.load();
     cudaStream_t S = c.stream;
 
-    DBuf<double> bufM(size_t(std::max<int64_t>(m, 1) * l), S);
-    DBuf<double> Q(size_t(n * l), S), Z(size_t(n * l), S);
+    DBuf<double>& bufM = c.slot(0, size_t(std::max<int64_t>(m, 1) * l));
+    DBuf<double>& Q = c.slot(1, size_t(n * l));
+    DBuf<double>& Z = c.slot(2, size_t(n * l));
 
     auto t0 = Clock::now();
     if (q % 2 == 0) {
         // Omega (l x grows, column-major) == Omega^T row-major: this rank's rows
         // are the stream slice [offset*l, (offset+m)*l).
         if (M.offset == 0 && m == M.grows) {
-            sketch_stream(c, a, l, M.grows, bufM.get());
+            sketch_into(c, a, l, M.grows, bufM);
         } else {
             DBuf<double> full(size_t(M.grows * l), S);
             sketch_stream(c, a, l, M.grows, full.get());
@@ -163,8 +179,8 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
             std::swap(Q, Z);
         }
     } else {
-        DBuf<double> om(size_t(n * l), S);
-        sketch_stream(c, a, n, l, om.get());              // n x l column-major
+        DBuf<double>& om = c.slot(3, 0);
+        sketch_into(c, a, n, l, om);                      // n x l column-major
         transpose_device(c, om.get(), l, n, Q.get());     // -> row-major n x l
     }
     FB_CUDA(cudaStreamSynchronize(S));
@@ -192,7 +208,9 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     DBuf<double> MU(size_t(l * k), S), MV(size_t(l * k), S);
     e.factor(c, int(s), int(k), int(k), true, true, MU.get());
     e.factor(c, int(s), int(k), int(k), true, false, MV.get());
-    DBuf<double> Uo(size_t(std::max<int64_t>(m, 1) * k), S), Vo(size_t(n * k), S), So(size_t(k), S);
+    DBuf<double>& Uo = c.slot(4, size_t(std::max<int64_t>(m, 1) * k));
+    DBuf<double>& Vo = c.slot(5, size_t(n * k));
+    DBuf<double> So(size_t(k), S);
     gemm_device(c, bufM.get(), m, l, MU.get(), k, Uo.get(), std::max<int64_t>(m, 1), true);
     gemm_device(c, Q.get(), n, l, MV.get(), k, Vo.get(), n, true);
     e.singular_values(c, int(s), int(k), true, So.get());
@@ -226,14 +244,15 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     const uint64_t passes0 = M.passes.load();
     cudaStream_t S = c.stream;
 
-    DBuf<double> Q(size_t(m * l), S), Y(size_t(m * l), S);
-    DBuf<double> bufN(size_t(std::max<int64_t>(n, 1) * l), S);
+    DBuf<double>& Q = c.slot(0, size_t(m * l));
+    DBuf<double>& Y = c.slot(1, size_t(m * l));
+    DBuf<double>& bufN = c.slot(2, size_t(std::max<int64_t>(n, 1) * l));
 
     auto t0 = Clock::now();
     if (q % 2 == 0) {
         // Omega: gcols x l column-major; this rank needs rows [offset, offset+n)
-        DBuf<double> om(size_t(M.gcols * l), S);
-        sketch_stream(c, a, M.gcols, l, om.get());
+        DBuf<double>& om = c.slot(3, 0);
+        sketch_into(c, a, M.gcols, l, om);
         if (M.offset == 0 && n == M.gcols) {
             transpose_device(c, om.get(), l, n, bufN.get());
         } else {
@@ -251,8 +270,8 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
             eig_svd_U(c, Y.get(), m, l, Q.get());
         }
     } else {
-        DBuf<double> om(size_t(m * l), S);
-        sketch_stream(c, a, m, l, om.get());
+        DBuf<double>& om = c.slot(3, 0);
+        sketch_into(c, a, m, l, om);
         transpose_device(c, om.get(), l, m, Q.get());
     }
     FB_CUDA(cudaStreamSynchronize(S));
@@ -280,7 +299,9 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     DBuf<double> MU(size_t(l * k), S), MV(size_t(l * k), S);
     e.factor(c, int(s), int(k), int(k), true, false, MU.get());   // U = Q * V(:, ind)
     e.factor(c, int(s), int(k), int(k), true, true, MV.get());    // V = f.U(:, ind)
-    DBuf<double> Uo(size_t(m * k), S), Vo(size_t(std::max<int64_t>(n, 1) * k), S), So(size_t(k), S);
+    DBuf<double>& Uo = c.slot(4, size_t(m * k));
+    DBuf<double>& Vo = c.slot(5, size_t(std::max<int64_t>(n, 1) * k));
+    DBuf<double> So(size_t(k), S);
     gemm_device(c, Q.get(), m, l, MU.get(), k, Uo.get(), m, true);
     gemm_device(c, bufN.get(), n, l, MV.get(), k, Vo.get(), std::max<int64_t>(n, 1), true);
     e.singular_values(c, int(s), int(k), true, So.get());
@@ -317,19 +338,20 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
     const int64_t m = M.A.rows, n = M.A.cols, k = cfg.k, s = cfg.oversample, p = cfg.power;
     const uint64_t passes0 = M.passes.load();
     cudaStream_t S = c.stream;
-    DBuf<double> bufM(size_t(std::max<int64_t>(m, 1) * l), S), bufN(size_t(std::max<int64_t>(n, 1) * l), S);
+    DBuf<double>& bufM = c.slot(0, size_t(std::max<int64_t>(m, 1) * l));
+    DBuf<double>& bufN = c.slot(1, size_t(std::max<int64_t>(n, 1) * l));
 
     auto t0 = Clock::now();
     if (!left) {
         // Omega n x l column-major -> row-major; Q = orth(A Omega), m x l
-        DBuf<double> om(size_t(n * l), S);
-        sketch_stream(c, a, n, l, om.get());
+        DBuf<double>& om = c.slot(3, 0);
+        sketch_into(c, a, n, l, om);
         transpose_device(c, om.get(), l, n, bufN.get());
         spmm_pass(c, M, false, bufN.get(), l, bufM.get());
         orth_device(c, bufM.get(), m, l);
     } else {
         // Omega l x m column-major == Omega^T row-major m x l; Q = orth(A^T Omega^T), n x l
-        sketch_stream(c, a, l, m, bufM.get());
+        sketch_into(c, a, l, m, bufM);
         spmm_pass(c, M, true, bufM.get(), l, bufN.get());
         orth_device(c, bufN.get(), n, l);
     }
@@ -354,12 +376,13 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
     const double t_power = since(t0);
 
     t0 = Clock::now();
-    DBuf<double> Uo(size_t(std::max<int64_t>(m, 1) * k), S), Vo(size_t(std::max<int64_t>(n, 1) * k), S),
-        So(size_t(k), S);
+    DBuf<double>& Uo = c.slot(4, size_t(std::max<int64_t>(m, 1) * k));
+    DBuf<double>& Vo = c.slot(5, size_t(std::max<int64_t>(n, 1) * k));
+    DBuf<double> So(size_t(k), S);
     DBuf<double> MU(size_t(l * k), S), MV(size_t(l * k), S);
     EigWork e;
     if (!left) {
-        DBuf<double> W(size_t(std::max<int64_t>(n, 1) * l), S);
+        DBuf<double>& W = c.slot(2, size_t(std::max<int64_t>(n, 1) * l));
         spmm_pass(c, M, true, bufM.get(), l, W.get());          // W = A^T Q, n x l
         e.run(c, W.get(), n, l);
         e.factor(c, int(s), int(k), int(k), true, false, MU.get());  // U = Q V(:, ind)
@@ -368,7 +391,7 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
         gemm_device(c, W.get(), n, l, MV.get(), k, Vo.get(), std::max<int64_t>(n, 1), true);
         basis_out(c, a, bufM.get(), m, l);
     } else {
-        DBuf<double> W(size_t(std::max<int64_t>(m, 1) * l), S);
+        DBuf<double>& W = c.slot(2, size_t(std::max<int64_t>(m, 1) * l));
         spmm_pass(c, M, false, bufN.get(), l, W.get());         // W = A Q, m x l
         e.run(c, W.get(), m, l);
         e.factor(c, int(s), int(k), int(k), true, true, MU.get());   // U = W V(:, ind) / S

@@ -11,6 +11,7 @@ struct RunArgs {
     int64_t omega_rows = 0, omega_cols = 0;
     double *U = nullptr, *S = nullptr, *V = nullptr, *basis = nullptr;
     bool device_io = false;
+    DBuf<double>* pre = nullptr;  // Omega generated ahead (frpca_run_csr), moved in
 };
 
 // eig_svd pipeline state: Gram -> (allreduce) -> syevd (B becomes V) -> rank check.

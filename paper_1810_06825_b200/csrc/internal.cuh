@@ -84,6 +84,22 @@ struct Ctx {
     std::mutex mu;  // the ABI serialises calls on one context
     cudaEvent_t timer_a = nullptr, timer_b = nullptr;
     DBuf<uint64_t> omega_raw;  // raw-word buffer of the Omega generator, kept (grown on demand)
+    std::unique_ptr<Ctx> side;  // second stream for work overlapped with the upload (frpca_run_csr)
+    // Run workspaces by role, kept between runs and grown on demand: a fresh
+    // multi-GB allocation per run makes the stream-ordered pool remap memory
+    // (measured 0.8 s for a 16 GB output buffer at C4).
+    static constexpr int kSlots = 8;
+    DBuf<double> slots[kSlots];  // fixed storage: references handed out stay valid
+    DBuf<double>& slot(int i, size_t n) {
+        if (i < 0 || i >= kSlots) throw CudaError("workspace slot out of range");
+        DBuf<double>& b = slots[i];
+        if (b.n < n) {
+            b.release();
+            b.alloc(n, stream);
+        }
+        b.s = stream;
+        return b;
+    }
 
     // profiling: events around each launch, folded into per-kernel aggregates
     bool prof = false;

@@ -30,7 +30,9 @@ struct Vec<2> {
         a.x = __fma_rn(v, x.x, a.x);
         a.y = __fma_rn(v, x.y, a.y);
     }
-    __device__ static void store(double* p, const T& a) { *reinterpret_cast<double2*>(p) = a; }
+    // outputs and partials are not re-read by this kernel: streaming stores
+    // keep them from evicting the gathered operand's rows from L2
+    __device__ static void store(double* p, const T& a) { __stcs(reinterpret_cast<double2*>(p), a); }
     __device__ static T zero() { return make_double2(0.0, 0.0); }
 };
 template <>
@@ -38,7 +40,7 @@ struct Vec<1> {
     using T = double;
     __device__ static T load(const double* p) { return __ldg(p); }
     __device__ static void fma(T& a, double v, const T& x) { a = __fma_rn(v, x, a); }
-    __device__ static void store(double* p, const T& a) { *p = a; }
+    __device__ static void store(double* p, const T& a) { __stcs(p, a); }
     __device__ static T zero() { return 0.0; }
 };
 

@@ -183,3 +183,27 @@ def test_capture_basis(fb, orc):
     o = orc.pca(oA, orc.FRPCAT, 8, 4, 3, want_basis=True)
     assert st.basis.shape == o["basis"].shape
     assert subspace_dist(o["basis"], st.basis) < 1e-9
+
+
+@pytest.mark.parametrize("algo,shape,q", [(1, (20000, 4000), 4), (1, (20000, 4000), 3), (0, (3000, 30000), 4),
+                                          (0, (3000, 30000), 5), (3, (3000, 2000), 2), (4, (3000, 2000), 2)])
+def test_run_csr_equals_upload_and_run(fb, orc, algo, shape, q):
+    """frpca_run_csr (sketch generated on a second stream during the upload)
+    gives bitwise the result of upload + frpca_run."""
+    m, n = shape
+    oA = powerlaw_csr(orc, m, n, 300000, 41, a_row=1.5, a_col=1.1)
+    A = to_fb(fb, oA)
+    c = fb.PcaConfig(k=20, oversample=12, passes=q, power=1, seed=9)
+    r1, d1 = fb.run_csr(A, c, fb.PcaAlgorithm(algo))
+    f = {0: fb.frpca, 1: fb.frpcat, 3: fb.basic_rpca, 4: fb.basic_rpcat}[algo]
+    r2 = f(to_fb(fb, oA), c)
+    assert d1 == algo
+    assert np.array_equal(r1.S, r2.S) and np.array_equal(r1.U, r2.U) and np.array_equal(r1.V, r2.V)
+
+
+def test_run_csr_errors(fb, orc):
+    A = to_fb(fb, orc.Csr.random_sparse(50, 40, 0.2, 3))
+    with pytest.raises(ValueError, match="frpca: requires rows <= cols"):
+        fb.run_csr(A, fb.PcaConfig(k=3, oversample=2, passes=4), fb.PcaAlgorithm.Frpca)
+    with pytest.raises(fb.NumericalError):
+        fb.run_csr(fb.SparseMatrixCsr.from_triplets(6, 6, []), fb.PcaConfig(k=2, oversample=1, passes=4))
