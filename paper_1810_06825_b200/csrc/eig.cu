@@ -1,6 +1,6 @@
 // K5: the l x l symmetric eigenproblem of eig_svd (dense_kernels.hpp:159-161,
-// Eigen SelfAdjointEigenSolver): cuSOLVER syevd, or (opt-in) the library's
-// own l <= 232 solver in syev.cu.
+// Eigen SelfAdjointEigenSolver): the library's own l <= 232 solver in syev.cu,
+// cuSOLVER syevd above that size or when the small solver reports failure.
 #include <cstdlib>
 #include <cstring>
 
@@ -12,12 +12,12 @@ bool syev_small(Ctx& c, double* B, int64_t n, double* d_D, std::vector<double>& 
 
 void syevd_device(Ctx& c, double* B, int64_t n, double* d_D, std::vector<double>& h_D) {
     Prof prof(c, "syevd", 8.0 * n * n * 2, 4.0 / 3.0 * n * n * n);
-    // cuSOLVER by default. FRPCA_EIG=custom (or strict: custom, and a fallback
-    // is an error) selects the library's l <= 232 solver (syev.cu), which is
-    // correct but still slower than syevd at l = 200 (measured).
+    // The small solver (syev.cu) by default: faster than syevd at l = 200
+    // (DESIGN.md §4). FRPCA_EIG=cusolver forces syevd; FRPCA_EIG=strict makes
+    // a fallback from the small solver an error (tests).
     const char* mode = std::getenv("FRPCA_EIG");
     const bool strict = mode && std::strcmp(mode, "strict") == 0;
-    if (mode && (strict || std::strcmp(mode, "custom") == 0)) {
+    if (!(mode && std::strcmp(mode, "cusolver") == 0)) {
         if (syev_small(c, B, n, d_D, h_D)) return;
         if (strict && n <= 232) throw CudaError("syev_small: did not converge (FRPCA_EIG=strict)");
     }

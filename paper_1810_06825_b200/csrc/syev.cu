@@ -1,15 +1,15 @@
 // K5: the l x l symmetric eigenproblem of eig_svd (dense_kernels.hpp:159-161,
 // Eigen's SelfAdjointEigenSolver in the reference) for l <= kEigMax.
 //
-// cuSOLVER's syevd spends ~1.8 ms on a 200 x 200 matrix, almost all of it
-// launch and host round-trip overhead. This solver is three kernels (opt-in,
-// FRPCA_EIG=custom: at l = 200 it measures ~2.0 ms per call, still latency-
-// bound in the single-CTA tridiagonalisation and the D&C merges):
+// cuSOLVER's syevd spends ~1.9 ms on a 200 x 200 matrix, almost all of it
+// launch and host round-trip overhead. This solver is three kernels (the
+// default for l <= 232; latency-bound in the single-CTA tridiagonalisation):
 //   E1 k_sytrd  one CTA: Householder tridiagonalisation with the packed lower
 //               triangle resident in shared memory (LAPACK dsytd2 order);
 //   E2 k_stedc  one CTA: divide and conquer on the tridiagonal (Cuppen's
 //               rank-one tearing; leaves by implicit QL with Wilkinson shifts,
-//               one warp per leaf; merges with LAPACK-style deflation, the
+//               one warp per leaf; the merges of one level run concurrently,
+//               each on its own group of warps; LAPACK-style deflation, the
 //               secular equation solved per root by one warp with the
 //               two-pole ("middle way") rational model under a bisection
 //               bracket, and Gu-Eisenstat's recomputed z so the merged
@@ -46,31 +46,47 @@ __device__ double block_sum(double v, double* red) {
 // Packed lower triangle, row-major: A[i][k] (k <= i) at i(i+1)/2 + k.
 __device__ __forceinline__ int rp(int i) { return (i * (i + 1)) >> 1; }
 
-// every warp reduces the 32 per-warp partials itself (same order everywhere)
+constexpr int kST = 512;  // k_sytrd threads: 128 registers each for the lane-resident slices
+constexpr int kSW = kST / 32;
+
+// every warp reduces the kSW per-warp partials itself (same order everywhere)
 __device__ __forceinline__ double warp_total(const double* red) {
-    double v = red[threadIdx.x & 31];
+    const int lane = threadIdx.x & 31;
+    double v = lane < kSW ? red[lane] : 0.0;
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
-// Four barriers per column: (A) reflector from the norm partials of the
-// previous step, (B) p = tau A22 v with the partials of p^T v, (C) w,
-// (D) A22 -= v w^T + w v^T with the norm partials of the next column.
-__global__ void __launch_bounds__(kET, 1)
+constexpr size_t kSmemMax = 226 * 1024;  // dynamic, next to the static reduction arrays
+// the kSW x n column partials of (B) fit next to the packed matrix
+__host__ __device__ constexpr bool sytrd_colp(int n) {
+    return sizeof(double) * (size_t(n) * (n + 1) / 2 + 2 * kEigMax + kSW * size_t(n)) <= kSmemMax;
+}
+__host__ __device__ constexpr size_t sytrd_smem(int n) {
+    return sizeof(double) * (size_t(n) * (n + 1) / 2 + 2 * kEigMax + (sytrd_colp(n) ? kSW * size_t(n) : 0));
+}
+
+// Per column: (A) reflector from the norm partials of the previous step,
+// (B) p = tau A22 v with the partials of p^T v, (C) w, (D) A22 -= v w^T +
+// w v^T with the norm partials of the next column. With the column partials
+// (n <= ~215) every stored element is read once in (B) and v, w live in
+// registers (lane-resident slices k = lane + 32 m).
+__global__ void __launch_bounds__(kST, 1)
 k_sytrd(const double* __restrict__ B, int n, double* __restrict__ Hv, double* __restrict__ tau,
-        double* __restrict__ dg, double* __restrict__ eo) {
+        double* __restrict__ dg, double* __restrict__ eo, long long* __restrict__ clk) {
     extern __shared__ double sm[];
     double* A = sm;                    // packed lower, row-major
     double* v = A + rp(n);             // Householder vector (v[0] = 1)
     double* w = v + kEigMax;           // p, then w
+    double* colp = sytrd_colp(n) ? w + kEigMax : nullptr;  // kSW x n column partials of p
     __shared__ double redA[32], redB[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = warp; i < n; i += 32)
+    for (int i = warp; i < n; i += kSW)
         for (int k = lane; k <= i; k += 32) A[rp(i) + k] = B[k + size_t(i) * n];  // B symmetric
     __syncthreads();
     {   // norm partials of column 0 below its subdiagonal entry
         double ps = 0.0;
-        for (int i = 2 + warp; i < n; i += 32) {
+        for (int i = 2 + warp; i < n; i += kSW) {
             const double x = A[rp(i)];
             ps = fma(x, x, ps);
         }
@@ -79,6 +95,8 @@ k_sytrd(const double* __restrict__ B, int n, double* __restrict__ Hv, double* __
     __syncthreads();
     for (int j = 0; j + 2 < n; ++j) {
         const int t = n - j - 1;
+        const bool tim = clk && j == 20 && tid == 0;
+        if (tim) clk[140] = clock64();
         // (A) reflector
         const double xnorm2 = warp_total(redA);
         const double alpha = A[rp(j + 1) + j];
@@ -95,12 +113,116 @@ k_sytrd(const double* __restrict__ B, int n, double* __restrict__ Hv, double* __
         }
         if (tid == 0) { tau[j] = tj; eo[j] = beta; dg[j] = A[rp(j) + j]; }
         __syncthreads();
-        // (B) p = tau * A22 v: one warp per row (two rows in flight), lanes
-        // over the row and its column
-        {
+        if (tim) clk[141] = clock64();
+        if (colp) {
+            // (B) rows i = i0 + kSW r (r < 8) of a batch: the row part over
+            // the lanes (x v[k]), the column part into lane-owned
+            // accumulators (x v[i]); the 8 row sums leave the warp by a
+            // transpose reduction (lane l ends with row (l >> 2) & 7)
+            double vr[8], cacc[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int k = lane + 32 * m;
+                vr[m] = k < t ? v[k] : 0.0;
+                cacc[m] = 0.0;
+            }
+            for (int i0 = warp; i0 < t; i0 += 8 * kSW) {
+                double a[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    a[r] = 0.0;
+                    const int i = i0 + kSW * r;
+                    if (i < t) {
+                        const double* row = A + rp(j + 1 + i) + (j + 1);
+                        const double vi = v[i];
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            if (32 * m > i) break;
+                            const int k = lane + 32 * m;
+                            if (k <= i) {
+                                const double x = row[k];
+                                a[r] = fma(x, vr[m], a[r]);
+                                if (k < i) cacc[m] = fma(x, vi, cacc[m]);
+                            }
+                        }
+                    }
+                }
+                {
+                    const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double snd = h4 ? a[q] : a[q + 4], keep = h4 ? a[q + 4] : a[q];
+                        a[q] = keep + __shfl_xor_sync(0xffffffffu, snd, 16);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const double snd = h3 ? a[q] : a[q + 2], keep = h3 ? a[q + 2] : a[q];
+                        a[q] = keep + __shfl_xor_sync(0xffffffffu, snd, 8);
+                    }
+                    {
+                        const double snd = h2 ? a[0] : a[1], keep = h2 ? a[1] : a[0];
+                        a[0] = keep + __shfl_xor_sync(0xffffffffu, snd, 4);
+                    }
+                    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+                    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+                    const int i = i0 + kSW * ((lane >> 2) & 7);
+                    if ((lane & 3) == 0 && i < t) w[i] = a[0];
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int k = lane + 32 * m;
+                if (k < t) colp[warp * n + k] = cacc[m];
+            }
+            __syncthreads();
             double pv = 0.0;
-            for (int i0 = warp; i0 < t; i0 += 64) {
-                const int i1 = i0 + 32;
+            if (tid < t) {
+                double a = w[tid];
+#pragma unroll
+                for (int q = 0; q < kSW; ++q) a += colp[q * n + tid];
+                a *= tj;
+                w[tid] = a;
+                pv = a * v[tid];
+            }
+            for (int o = 16; o; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+            if (lane == 0) redB[warp] = pv;
+            __syncthreads();
+            if (tim) clk[142] = clock64();
+            // (C) w = p - (tau/2)(p^T v) v, each warp its own register slice
+            const double alpha2 = -0.5 * tj * warp_total(redB);
+            double wr[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int k = lane + 32 * m;
+                wr[m] = k < t ? fma(alpha2, vr[m], w[k]) : 0.0;
+            }
+            __syncthreads();  // every warp has read p before w is overwritten
+            if (tid < t) w[tid] = fma(alpha2, v[tid], w[tid]);
+            __syncthreads();
+            if (tim) clk[143] = clock64();
+            // (D) rank-2 update from the register slices
+            double ps = 0.0;
+            for (int i = warp; i < t; i += kSW) {
+                const double vi = v[i], wi = w[i];
+                double* row = A + rp(j + 1 + i) + (j + 1);
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    if (32 * m > i) break;
+                    const int k = lane + 32 * m;
+                    if (k <= i) {
+                        const double x = row[k] - fma(vi, wr[m], wi * vr[m]);
+                        row[k] = x;
+                        if (m == 0 && lane == 0 && i >= 2) ps = fma(x, x, ps);
+                    }
+                }
+            }
+            if (lane == 0) redA[warp] = ps;
+        } else {
+            // (B) p = tau * A22 v: one warp per row (two rows in flight), lanes
+            // over the row and its column
+            double pv = 0.0;
+            for (int i0 = warp; i0 < t; i0 += 2 * kSW) {
+                const int i1 = i0 + kSW;
                 double a0 = 0.0, a1 = 0.0;
                 for (int k = lane; k < t; k += 32) {
                     const int K = j + 1 + k;
@@ -122,18 +244,18 @@ k_sytrd(const double* __restrict__ B, int n, double* __restrict__ Hv, double* __
                 if (i1 < t) pv = fma(a1, v[i1], pv);
             }
             if (lane == 0) redB[warp] = pv;
-        }
-        __syncthreads();
-        // (C) w = p - (tau/2)(p^T v) v
-        {
-            const double alpha2 = -0.5 * tj * warp_total(redB);
-            if (tid < t) w[tid] = fma(alpha2, v[tid], w[tid]);
-        }
-        __syncthreads();
-        // (D) rank-2 update; lane 0 of the row's warp sees the next column
-        {
+            __syncthreads();
+            if (tim) clk[142] = clock64();
+            // (C) w = p - (tau/2)(p^T v) v
+            {
+                const double alpha2 = -0.5 * tj * warp_total(redB);
+                if (tid < t) w[tid] = fma(alpha2, v[tid], w[tid]);
+            }
+            __syncthreads();
+            if (tim) clk[143] = clock64();
+            // (D) rank-2 update; lane 0 of the row's warp sees the next column
             double ps = 0.0;
-            for (int i = warp; i < t; i += 32) {
+            for (int i = warp; i < t; i += kSW) {
                 const double vi = v[i], wi = w[i];
                 double* row = A + rp(j + 1 + i) + (j + 1);
                 for (int k = lane; k <= i; k += 32) {
@@ -145,6 +267,7 @@ k_sytrd(const double* __restrict__ B, int n, double* __restrict__ Hv, double* __
             if (lane == 0) redA[warp] = ps;
         }
         __syncthreads();
+        if (tim) clk[144] = clock64();
     }
     if (tid == 0) {
         if (n >= 2) {
@@ -238,9 +361,17 @@ struct MergeWs {
     double ddf[kEigMax], vals[kEigMax];
     double rc[kEigMax], rs[kEigMax];
     int cs[kEigMax], ck[kEigMax], cdf[kEigMax], orgk[kEigMax], ri[kEigMax], rj[kEigMax], pos[kEigMax];
-    int k, ndf, nrot, sgn;
-    double rho, zsum2, zn2, dmax;
+    struct Scal {
+        int k, ndf, nrot, sgn, ok;
+        double rho, zsum2, zn2, dmax;
+    } sc[16];  // per concurrent merge
 };
+
+// A group of whole warps working on one merge; `bar.sync id, nt` is its barrier.
+struct Grp {
+    int t, nt, id;
+};
+__device__ __forceinline__ void gsync(const Grp& g) { asm volatile("bar.sync %0, %1;\n" ::"r"(g.id), "r"(g.nt)); }
 
 // The deferred top-level merge, finished by E3: output column c is
 // sum_j Z[:, ck[j]] U[j][src[c]] (src[c] < k) or Z[:, cdf[src[c] - k]].
@@ -347,182 +478,179 @@ __device__ __forceinline__ void stamp(long long* clk, int slot) {
 
 // merge of the adjacent blocks [s0, s0 + n1) and [s0 + n1, s0 + n1 + n2).
 // top != nullptr: the last merge; its eigenvector product is left to E3.
-__device__ bool merge_blocks(int n, int s0, int n1, int n2, double* Dc, const double* Eo, double* Z,
-                             double* Tmp, double* Ut, double* Us, MergeWs& M, TopPlan* top, long long* clk) {
-    const int tid = threadIdx.x;
+// merge of the adjacent blocks [s0, s0 + n1) and [s0 + n1, s0 + n1 + n2) by
+// the thread group G (merges of one level run concurrently on disjoint slices
+// of the workspaces: arrays at [s0, s0 + sz), U and Tmp at row s0 * n).
+// top != nullptr: the last merge; its eigenvector product is left to E3.
+__device__ bool merge_blocks(int n, int s0, int n1, int n2, double* Dc, const double* Eo, double* Z, double* TmpAll,
+                             double* UtAll, double* Us, size_t us_cap, MergeWs& MW, int gi, TopPlan* top,
+                             const Grp& G) {
+    const int tid = G.t, NT = G.nt;
     const int sz = n1 + n2, p = s0 + n1;
+    double *dfull = MW.dfull + s0, *zfull = MW.zfull + s0, *ds = MW.ds + s0, *zs = MW.zs + s0;
+    double *dk = MW.dk + s0, *zk = MW.zk + s0, *zh = MW.zh + s0, *tauk = MW.tauk + s0;
+    double *ddf = MW.ddf + s0, *vals = MW.vals + s0, *rcv = MW.rc + s0, *rsv = MW.rs + s0;
+    int *cs = MW.cs + s0, *ck = MW.ck + s0, *cdf = MW.cdf + s0, *orgk = MW.orgk + s0;
+    int *ri = MW.ri + s0, *rj = MW.rj + s0, *pos = MW.pos + s0;
+    MergeWs::Scal& sc = MW.sc[gi];
+    double* Tmp = TmpAll + size_t(s0) * n;
+    double* Ut = UtAll + size_t(s0) * n;
     const double rho0 = Eo[p - 1];
     const int sgn = rho0 < 0.0 ? -1 : 1;
-    if (tid == 0) { M.zn2 = 0.0; M.dmax = 0.0; }
-    for (int j = tid; j < sz; j += kET) {
-        M.zfull[j] = j < n1 ? Z[(p - 1) + size_t(s0 + j) * n] : Z[p + size_t(s0 + j) * n];
-        M.dfull[j] = Dc[s0 + j];
+    for (int j = tid; j < sz; j += NT) {
+        zfull[j] = j < n1 ? Z[(p - 1) + size_t(s0 + j) * n] : Z[p + size_t(s0 + j) * n];
+        dfull[j] = Dc[s0 + j];
     }
-    __syncthreads();
+    gsync(G);
     // sorted order of sgn * d: position = rank in its own block + rank in the
     // other (binary search; block 1 first on ties)
-    for (int j = tid; j < sz; j += kET) {
+    for (int j = tid; j < sz; j += NT) {
         const bool b1 = j < n1;
-        const double key = sgn * M.dfull[j];
+        const double key = sgn * dfull[j];
         const int own = b1 ? (sgn > 0 ? j : n1 - 1 - j) : (sgn > 0 ? j - n1 : sz - 1 - j);
         const int o0 = b1 ? n1 : 0, on = b1 ? n2 : n1;
-        int lo = 0, hi = on;  // count of other-block keys < key (b1) or <= key (b2)
+        int lo = 0, hi = on;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             const int idx = o0 + (sgn > 0 ? mid : on - 1 - mid);
-            const double ok = sgn * M.dfull[idx];
-            if (b1 ? ok < key : ok <= key) lo = mid + 1; else hi = mid;
+            const double okey = sgn * dfull[idx];
+            if (b1 ? okey < key : okey <= key) lo = mid + 1; else hi = mid;
         }
-        const int pos = own + lo;
-        M.ds[pos] = key;
-        M.zs[pos] = M.zfull[j];
-        M.cs[pos] = j;
+        const int q = own + lo;
+        ds[q] = key;
+        zs[q] = zfull[j];
+        cs[q] = j;
     }
     if (tid < 32) {
         double z2 = 0.0, dm = 0.0;
-        for (int j = tid; j < sz; j += 32) { z2 = fma(M.zfull[j], M.zfull[j], z2); dm = fmax(dm, fabs(M.dfull[j])); }
+        for (int j = tid; j < sz; j += 32) { z2 = fma(zfull[j], zfull[j], z2); dm = fmax(dm, fabs(dfull[j])); }
         for (int o = 16; o; o >>= 1) {
             z2 += __shfl_xor_sync(0xffffffffu, z2, o);
             dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
         }
-        if (tid == 0) { M.zn2 = z2; M.dmax = dm; }
+        if (tid == 0) { sc.zn2 = z2; sc.dmax = dm; sc.ok = 1; }
     }
-    __syncthreads();
+    gsync(G);
     if (tid == 0) {
         // deflation (LAPACK dlaed2 rules) over the sorted sequence; the
         // rotation test only runs for nearly equal neighbours (|cs| <= 1/2)
-        const double rho = fabs(rho0) * M.zn2;
-        const double zinv = 1.0 / sqrt(M.zn2);
-        const double tol = 8.0 * DBL_EPSILON * fmax(M.dmax, rho);
+        const double rho = fabs(rho0) * sc.zn2;
+        const double zinv = 1.0 / sqrt(sc.zn2);
+        const double tol = 8.0 * DBL_EPSILON * fmax(sc.dmax, rho);
         int prev = -1;
         double dprev = 0.0, zprev = 0.0;
         int k = 0, ndf = 0, nrot = 0;
         for (int q = 0; q < sz; ++q) {
-            const int j = M.cs[q];
-            const double dj = M.ds[q], zj = M.zs[q] * zinv;
+            const int j = cs[q];
+            const double dj = ds[q], zj = zs[q] * zinv;
             if (rho * fabs(zj) <= tol) {
-                M.ddf[ndf] = dj; M.cdf[ndf] = j; ++ndf;
+                ddf[ndf] = dj; cdf[ndf] = j; ++ndf;
                 continue;
             }
             if (prev >= 0 && fabs(dj - dprev) <= 2.0 * tol) {
                 const double r = sqrt(fma(zprev, zprev, zj * zj));
-                const double c = zj / r, s = zprev / r;
-                if (fabs((dj - dprev) * c * s) <= tol) {
-                    // rotate (prev, j) so that z_prev = 0, then deflate prev
-                    M.ri[nrot] = prev; M.rj[nrot] = j; M.rc[nrot] = c; M.rs[nrot] = s; ++nrot;
-                    const double dp = c * c * dprev + s * s * dj, dn = s * s * dprev + c * c * dj;
-                    M.ddf[ndf] = dp; M.cdf[ndf] = prev; ++ndf;
+                const double c = zj / r, sn = zprev / r;
+                if (fabs((dj - dprev) * c * sn) <= tol) {
+                    ri[nrot] = prev; rj[nrot] = j; rcv[nrot] = c; rsv[nrot] = sn; ++nrot;
+                    const double dp = c * c * dprev + sn * sn * dj, dn = sn * sn * dprev + c * c * dj;
+                    ddf[ndf] = dp; cdf[ndf] = prev; ++ndf;
                     prev = j; dprev = dn; zprev = r;
                     continue;
                 }
             }
-            if (prev >= 0) { M.dk[k] = dprev; M.zk[k] = zprev; M.ck[k] = prev; ++k; }
+            if (prev >= 0) { dk[k] = dprev; zk[k] = zprev; ck[k] = prev; ++k; }
             prev = j; dprev = dj; zprev = zj;
         }
-        if (prev >= 0) { M.dk[k] = dprev; M.zk[k] = zprev; M.ck[k] = prev; ++k; }
+        if (prev >= 0) { dk[k] = dprev; zk[k] = zprev; ck[k] = prev; ++k; }
         double zsum = 0.0;
-        for (int j = 0; j < k; ++j) zsum = fma(M.zk[j], M.zk[j], zsum);
-        M.k = k; M.ndf = ndf; M.nrot = nrot; M.sgn = sgn; M.rho = rho; M.zsum2 = zsum;
+        for (int j = 0; j < k; ++j) zsum = fma(zk[j], zk[j], zsum);
+        sc.k = k; sc.ndf = ndf; sc.nrot = nrot; sc.sgn = sgn; sc.rho = rho; sc.zsum2 = zsum;
     }
-    __syncthreads();
-    stamp(clk, 0);
-    const int k = M.k, ndf = M.ndf, nrot = M.nrot;
-    // Givens rotations of the deflation, in order, on the block's rows
+    gsync(G);
+    const int k = sc.k, ndf = sc.ndf, nrot = sc.nrot;
     if (nrot)
-        for (int r = tid; r < sz; r += kET) {
+        for (int r = tid; r < sz; r += NT) {
             double* zr = Z + (s0 + r);
             for (int t = 0; t < nrot; ++t) {
-                double& qi = zr[size_t(s0 + M.ri[t]) * n];
-                double& qj = zr[size_t(s0 + M.rj[t]) * n];
-                const double x = qi, y = qj, c = M.rc[t], s = M.rs[t];
-                qi = c * x - s * y;
-                qj = s * x + c * y;
+                double& qi = zr[size_t(s0 + ri[t]) * n];
+                double& qj = zr[size_t(s0 + rj[t]) * n];
+                const double x = qi, y = qj, c = rcv[t], sn = rsv[t];
+                qi = c * x - sn * y;
+                qj = sn * x + c * y;
             }
         }
-    // secular roots, kSecLanes lanes each
-    bool ok = true;
-    {
-        const int g = tid / kSecLanes, sl = tid % kSecLanes;
-        const unsigned mask = 0xffu << ((tid & 31) & ~(kSecLanes - 1));
-        for (int i = g; i < k; i += kET / kSecLanes) {
+    {   // secular roots, kSecLanes lanes each
+        const int g8 = tid / kSecLanes, sl = tid % kSecLanes;
+        const unsigned mask = 0xffu << ((threadIdx.x & 31) & ~(kSecLanes - 1));
+        for (int i = g8; i < k; i += NT / kSecLanes) {
             int org;
             double tau;
-            const bool r = secular_root(i, k, M.dk, M.zk, M.rho, M.zsum2, sl, mask, org, tau);
-            if (sl == 0) { M.orgk[i] = org; M.tauk[i] = tau; }
-            ok = ok && r;
+            const bool r = secular_root(i, k, dk, zk, sc.rho, sc.zsum2, sl, mask, org, tau);
+            if (sl == 0) { orgk[i] = org; tauk[i] = tau; }
+            if (!r) sc.ok = 0;
         }
     }
-    ok = __syncthreads_and(ok);
-    if (!ok) return false;
-    stamp(clk, 1);
-    // Gu-Eisenstat: zhat_j^2 = prod_i (lambda_i - d_j) / (rho prod_{i != j} (d_i - d_j)),
-    // one warp per j, lanes split the factors (fixed reduction tree)
-    const int lane = tid & 31, warp = tid >> 5;
-    for (int j = warp; j < k; j += kET / 32) {
-        const double dj = M.dk[j];
+    gsync(G);
+    if (!sc.ok) return false;
+    const int lane = tid & 31, warp = tid >> 5, nw = NT >> 5;
+    // Gu-Eisenstat zhat, one warp per j, lanes split the factors (fixed tree)
+    for (int j = warp; j < k; j += nw) {
+        const double dj = dk[j];
         double prod = 1.0;
         for (int i = lane; i < k - 1; i += 32) {
-            const double lam = (M.dk[M.orgk[i]] - dj) + M.tauk[i];
-            prod *= lam / (i < j ? (M.dk[i] - dj) : (M.dk[i + 1] - dj));
+            const double lam = (dk[orgk[i]] - dj) + tauk[i];
+            prod *= lam / (i < j ? (dk[i] - dj) : (dk[i + 1] - dj));
         }
         for (int o = 16; o; o >>= 1) prod *= __shfl_xor_sync(0xffffffffu, prod, o);
-        prod *= ((M.dk[M.orgk[k - 1]] - dj) + M.tauk[k - 1]) / M.rho;
-        if (lane == 0) M.zh[j] = copysign(sqrt(fabs(prod)), M.zk[j]);
+        prod *= ((dk[orgk[k - 1]] - dj) + tauk[k - 1]) / sc.rho;
+        if (lane == 0) zh[j] = copysign(sqrt(fabs(prod)), zk[j]);
     }
-    __syncthreads();
-    // eigenvectors of D + rho zhat zhat^T (row-major k x k U: U[j][i]), one
-    // warp per column i; into shared memory when the merge is finished here
-    double* U = (top || size_t(k) * k > kUsMax) ? Ut : Us;
-    for (int i = warp; i < k; i += kET / 32) {
-        const double dorg = M.dk[M.orgk[i]], tau = M.tauk[i];
+    gsync(G);
+    double* U = (top || size_t(k) * k > us_cap) ? Ut : Us;
+    for (int i = warp; i < k; i += nw) {
+        const double dorg = dk[orgk[i]], tau = tauk[i];
         double nrm = 0.0;
         for (int j = lane; j < k; j += 32) {
-            const double u = M.zh[j] / ((M.dk[j] - dorg) - tau);
+            const double u = zh[j] / ((dk[j] - dorg) - tau);
             nrm = fma(u, u, nrm);
         }
         for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
         const double inv = 1.0 / sqrt(nrm);
-        for (int j = lane; j < k; j += 32) U[size_t(j) * k + i] = (M.zh[j] / ((M.dk[j] - dorg) - tau)) * inv;
-        if (lane == 0) M.vals[i] = M.sgn * (dorg + tau);
+        for (int j = lane; j < k; j += 32) U[size_t(j) * k + i] = (zh[j] / ((dk[j] - dorg) - tau)) * inv;
+        if (lane == 0) vals[i] = sc.sgn * (dorg + tau);
     }
-    for (int t = tid; t < ndf; t += kET) M.vals[k + t] = M.sgn * M.ddf[t];
-    __syncthreads();
-    // ascending order of all sz eigenvalues (rank sort, ties by index)
-    for (int a = tid; a < sz; a += kET) {
-        const double va = M.vals[a];
+    for (int t = tid; t < ndf; t += NT) vals[k + t] = sc.sgn * ddf[t];
+    gsync(G);
+    for (int a = tid; a < sz; a += NT) {  // ascending order of all sz values (rank sort)
+        const double va = vals[a];
         int r = 0;
         for (int b = 0; b < sz; ++b) {
-            const double vb = M.vals[b];
+            const double vb = vals[b];
             r += (vb < va) || (vb == va && b < a);
         }
-        M.pos[a] = r;
+        pos[a] = r;
     }
-    __syncthreads();
-    stamp(clk, 2);
+    gsync(G);
     if (top) {  // last merge: hand the product to E3
-        for (int a = tid; a < sz; a += kET) {
-            top->src[M.pos[a]] = a;
-            if (a < k) top->ck[a] = M.ck[a];
-            else top->cdf[a - k] = M.cdf[a - k];
-            Dc[s0 + M.pos[a]] = M.vals[a];
+        for (int a = tid; a < sz; a += NT) {
+            top->src[pos[a]] = a;
+            if (a < k) top->ck[a] = ck[a];
+            else top->cdf[a - k] = cdf[a - k];
+            Dc[s0 + pos[a]] = vals[a];
         }
         if (tid == 0) top->k = k;
-        __syncthreads();
-        stamp(clk, 3);
-        stamp(clk, 4);
+        gsync(G);
         return true;
     }
-    // new eigenvectors into Tmp (sz x sz, ld sz): kept = Z * U (8 columns of U
-    // per task, U row-major k x k), deflated = copy
     const int ngrp = (k + 7) / 8;
-    for (int e = tid; e < sz * ngrp; e += kET) {
+    for (int e = tid; e < sz * ngrp; e += NT) {
         const int r = e % sz, a0 = (e / sz) * 8;
         double acc[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[q] = 0.0;
         const double* zr = Z + (s0 + r);
         for (int j = 0; j < k; ++j) {
-            const double zv = zr[size_t(s0 + M.ck[j]) * n];
+            const double zv = zr[size_t(s0 + ck[j]) * n];
             const double* u = U + size_t(j) * k + a0;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
@@ -530,21 +658,19 @@ __device__ bool merge_blocks(int n, int s0, int n1, int n2, double* Dc, const do
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            if (a0 + q < k) Tmp[r + size_t(M.pos[a0 + q]) * sz] = acc[q];
+            if (a0 + q < k) Tmp[r + size_t(pos[a0 + q]) * sz] = acc[q];
     }
-    for (int e = tid; e < sz * ndf; e += kET) {
+    for (int e = tid; e < sz * ndf; e += NT) {
         const int r = e % sz, t = e / sz;
-        Tmp[r + size_t(M.pos[k + t]) * sz] = Z[(s0 + r) + size_t(s0 + M.cdf[t]) * n];
+        Tmp[r + size_t(pos[k + t]) * sz] = Z[(s0 + r) + size_t(s0 + cdf[t]) * n];
     }
-    __syncthreads();
-    stamp(clk, 3);
-    for (int e = tid; e < sz * sz; e += kET) {
+    gsync(G);
+    for (int e = tid; e < sz * sz; e += NT) {
         const int r = e % sz, c = e / sz;
         Z[(s0 + r) + size_t(s0 + c) * n] = Tmp[e];
     }
-    for (int a = tid; a < sz; a += kET) Dc[s0 + M.pos[a]] = M.vals[a];
-    __syncthreads();
-    stamp(clk, 4);
+    for (int a = tid; a < sz; a += NT) Dc[s0 + pos[a]] = vals[a];
+    gsync(G);
     return true;
 }
 
@@ -605,20 +731,33 @@ k_stedc(int n, const double* __restrict__ dg, const double* __restrict__ eo, dou
         return;
     }
     stamp(clk, 1);
-    int mi = 0;
+    __shared__ int fail;
+    if (tid == 0) fail = 0;
+    __syncthreads();
     bool merged = false;
-    for (int width = LB; width < n; width *= 2) {
-        for (int s0 = 0; s0 + width < n; s0 += 2 * width) {
-            const int n1 = width, n2 = min(width, n - s0 - width);
-            const bool last = 2 * width >= n;
-            if (!merge_blocks(n, s0, n1, n2, Dc, Eo, Z, Tmp, Ut, reinterpret_cast<double*>(L), M, last ? top : nullptr,
-                              clk ? clk + 2 + 5 * mi : nullptr)) {
-                if (tid == 0) *info = 2;
-                return;
-            }
-            merged = merged || last;
-            ++mi;
+    int level = 0;
+    for (int width = LB; width < n; width *= 2, ++level) {
+        int G = 0;
+        for (int s0 = 0; s0 + width < n; s0 += 2 * width) ++G;
+        const bool last = 2 * width >= n;
+        // warps [g * 32 / G, (g + 1) * 32 / G) merge the g-th pair
+        int g = 0;
+        while (g + 1 < G && ((g + 1) * 32) / G <= warp) ++g;
+        const int w0 = (g * 32) / G, w1 = ((g + 1) * 32) / G;
+        const Grp grp{tid - w0 * 32, (w1 - w0) * 32, 1 + g};
+        const int s0 = g * 2 * width;
+        const int n1 = width, n2 = min(width, n - s0 - width);
+        const size_t us_cap = kUsMax / size_t(G);
+        if (!merge_blocks(n, s0, n1, n2, Dc, Eo, Z, Tmp, Ut, reinterpret_cast<double*>(L) + size_t(g) * us_cap, us_cap,
+                          M, g, last ? top : nullptr, grp))
+            if (grp.t == 0) atomicExch(&fail, 1);
+        __syncthreads();
+        if (fail) {
+            if (tid == 0) *info = 2;
+            return;
         }
+        stamp(clk, 2 + level);
+        merged = merged || last;
     }
     if (!merged) {  // a single leaf: identity plan
         for (int a = tid; a < n; a += kET) { top->src[a] = a; top->cdf[a] = a; }
@@ -734,8 +873,7 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>
     cudaStream_t s = c.stream;
     static bool attr = false;
     if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(sizeof(double) * (kEigMax * (kEigMax + 1) / 2 + 2 * kEigMax))));
+        FB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)));
         FB_CUDA(cudaFuncSetAttribute(k_stedc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(stedc_smem())));
         attr = true;
     }
@@ -753,11 +891,11 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>
     TopPlan* top = reinterpret_cast<TopPlan*>(topbuf.get());
     FB_CUDA(cudaMemsetAsync(info.get(), 0, sizeof(int), s));
     static const bool timing = std::getenv("FRPCA_EIG_TIMING") != nullptr;
-    DBuf<long long> clk(timing ? 128 : 0, s);
+    DBuf<long long> clk(timing ? 160 : 0, s);
     if (timing) FB_CUDA(cudaMemsetAsync(clk.get(), 0, clk.bytes(), s));
     {
         Prof p1(c, "syev_sytrd", 0, 0);
-        k_sytrd<<<1, kET, sizeof(double) * (size_t(n) * (n + 1) / 2 + 2 * kEigMax), s>>>(B, n, H, tau, dg, eo);
+        k_sytrd<<<1, kST, sytrd_smem(n), s>>>(B, n, H, tau, dg, eo, clk.get());
         FB_LAUNCH_CHECK();
     }
     {
@@ -776,13 +914,15 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>
     FB_CUDA(cudaMemcpyAsync(h_D.data(), d_D, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     FB_CUDA(cudaStreamSynchronize(s));
     if (timing) {
-        long long h[128];
+        long long h[160];
         FB_CUDA(cudaMemcpy(h, clk.get(), sizeof(h), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "sytrd step 20: A %lld B %lld C %lld D %lld\n", h[141] - h[140], h[142] - h[141],
+                     h[143] - h[142], h[144] - h[143]);
         std::fprintf(stderr, "stedc n=%d leaves %lld", n, h[1] - h[0]);
         long long prev = h[1];
-        for (int m = 0; m < 25 && h[2 + 5 * m + 4]; ++m) {
-            std::fprintf(stderr, " | m%d", m);
-            for (int q = 0; q < 5; ++q) { std::fprintf(stderr, " %lld", h[2 + 5 * m + q] - prev); prev = h[2 + 5 * m + q]; }
+        for (int m = 0; m < 12 && h[2 + m]; ++m) {
+            std::fprintf(stderr, " | L%d %lld", m, h[2 + m] - prev);
+            prev = h[2 + m];
         }
         std::fprintf(stderr, "\n");
     }
