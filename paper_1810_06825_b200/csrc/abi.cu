@@ -190,6 +190,10 @@ int frpca_ctx_destroy(frpca_ctx* c) {
             c->side.reset();
         }
         c->omega_raw.release();  // stream-ordered free before the stream goes
+        if (c->copy) {
+            cudaStreamSynchronize(c->copy);
+            cudaStreamDestroy(c->copy);
+        }
         if (c->stream) {
             cudaStreamSynchronize(c->stream);
             cudaStreamDestroy(c->stream);

@@ -137,6 +137,67 @@ static void basis_out(Ctx& c, const RunArgs& a, const double* Q, int64_t r, int6
     copy_out(c, a, a.basis, t.get(), r * l);
 }
 
+
+// The two output products (U = W_u MU, V = W_v MV, column-major, ld = rows)
+// and S. With host outputs, the device->host copies overlap the GEMMs: the
+// smaller product and S are computed first and copied on the copy stream
+// while the larger one runs in row chunks, each chunk copied as soon as it is
+// done. Chunks keep >= 4096 rows, so every entry comes from the same kernel
+// and K order as the unchunked product.
+struct OutProduct {
+    const double* W;  // rows x l, row-major
+    int64_t rows;
+    const double* M;  // l x k
+    double* dev;      // rows x k, column-major
+    double* user;     // U or V of the call (may be null)
+};
+
+static void output_products(Ctx& c, const RunArgs& a, int64_t l, int64_t k, OutProduct u, OutProduct v,
+                            EigWork& e, int s, double* So) {
+    cudaStream_t S = c.stream;
+    const bool overlap = !a.device_io && (u.user || v.user || a.S);
+    if (!overlap) {
+        gemm_device(c, u.W, u.rows, l, u.M, k, u.dev, std::max<int64_t>(u.rows, 1), true);
+        gemm_device(c, v.W, v.rows, l, v.M, k, v.dev, std::max<int64_t>(v.rows, 1), true);
+        e.singular_values(c, s, int(k), true, So);
+        copy_out(c, a, a.U, u.dev, u.rows * k);
+        copy_out(c, a, a.V, v.dev, v.rows * k);
+        copy_out(c, a, a.S, So, k);
+        return;
+    }
+    if (!c.copy) FB_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+    OutProduct& big = u.rows >= v.rows ? u : v;
+    OutProduct& sml = u.rows >= v.rows ? v : u;
+    std::vector<cudaEvent_t> evs;
+    auto fence = [&](cudaStream_t from, cudaStream_t to) {
+        cudaEvent_t ev;
+        FB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        evs.push_back(ev);
+        FB_CUDA(cudaEventRecord(ev, from));
+        FB_CUDA(cudaStreamWaitEvent(to, ev, 0));
+    };
+    gemm_device(c, sml.W, sml.rows, l, sml.M, k, sml.dev, std::max<int64_t>(sml.rows, 1), true);
+    e.singular_values(c, s, int(k), true, So);
+    fence(S, c.copy);
+    if (sml.user && sml.rows * k)
+        FB_CUDA(cudaMemcpyAsync(sml.user, sml.dev, sizeof(double) * sml.rows * k, cudaMemcpyDeviceToHost, c.copy));
+    if (a.S && k) FB_CUDA(cudaMemcpyAsync(a.S, So, sizeof(double) * k, cudaMemcpyDeviceToHost, c.copy));
+    const int64_t R = big.rows;
+    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(8, R / 4096));
+    for (int64_t q = 0; q < nch; ++q) {
+        const int64_t r0 = R * q / nch, r1 = R * (q + 1) / nch;
+        if (r1 == r0) continue;
+        gemm_device(c, big.W + r0 * l, r1 - r0, l, big.M, k, big.dev + r0, R, true);
+        if (!big.user || !k) continue;
+        fence(S, c.copy);
+        FB_CUDA(cudaMemcpy2DAsync(big.user + r0, sizeof(double) * R, big.dev + r0, sizeof(double) * R,
+                                  sizeof(double) * (r1 - r0), size_t(k), cudaMemcpyDeviceToHost, c.copy));
+    }
+    fence(c.copy, S);  // the run's final synchronisation covers the copies
+    FB_CUDA(cudaStreamSynchronize(S));
+    for (auto ev : evs) cudaEventDestroy(ev);
+}
+
 // ---------------------------------------------------------------------------
 // frpcat (Alg. 6), randsvd.hpp:278-328. Row-sharded: this rank holds rows
 // [offset, offset + m_loc) of A; A^T partials and Gram partials are summed
@@ -211,12 +272,8 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     DBuf<double>& Uo = c.slot(4, size_t(std::max<int64_t>(m, 1) * k));
     DBuf<double>& Vo = c.slot(5, size_t(n * k));
     DBuf<double> So(size_t(k), S);
-    gemm_device(c, bufM.get(), m, l, MU.get(), k, Uo.get(), std::max<int64_t>(m, 1), true);
-    gemm_device(c, Q.get(), n, l, MV.get(), k, Vo.get(), n, true);
-    e.singular_values(c, int(s), int(k), true, So.get());
-    copy_out(c, a, a.U, Uo.get(), m * k);
-    copy_out(c, a, a.V, Vo.get(), n * k);
-    copy_out(c, a, a.S, So.get(), k);
+    output_products(c, a, l, k, {bufM.get(), m, MU.get(), Uo.get(), a.U}, {Q.get(), n, MV.get(), Vo.get(), a.V}, e,
+                    int(s), So.get());
     basis_out(c, a, Q.get(), n, l);
     FB_CUDA(cudaStreamSynchronize(S));
     if (st) {
@@ -302,12 +359,8 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     DBuf<double>& Uo = c.slot(4, size_t(m * k));
     DBuf<double>& Vo = c.slot(5, size_t(std::max<int64_t>(n, 1) * k));
     DBuf<double> So(size_t(k), S);
-    gemm_device(c, Q.get(), m, l, MU.get(), k, Uo.get(), m, true);
-    gemm_device(c, bufN.get(), n, l, MV.get(), k, Vo.get(), std::max<int64_t>(n, 1), true);
-    e.singular_values(c, int(s), int(k), true, So.get());
-    copy_out(c, a, a.U, Uo.get(), m * k);
-    copy_out(c, a, a.V, Vo.get(), n * k);
-    copy_out(c, a, a.S, So.get(), k);
+    output_products(c, a, l, k, {Q.get(), m, MU.get(), Uo.get(), a.U}, {bufN.get(), n, MV.get(), Vo.get(), a.V}, e,
+                    int(s), So.get());
     basis_out(c, a, Q.get(), m, l);
     FB_CUDA(cudaStreamSynchronize(S));
     if (st) {

@@ -85,6 +85,7 @@ struct Ctx {
     cudaEvent_t timer_a = nullptr, timer_b = nullptr;
     DBuf<uint64_t> omega_raw;  // raw-word buffer of the Omega generator, kept (grown on demand)
     std::unique_ptr<Ctx> side;  // second stream for work overlapped with the upload (frpca_run_csr)
+    cudaStream_t copy = nullptr;  // device->host copies of results overlapped with the output GEMMs
     // Run workspaces by role, kept between runs and grown on demand: a fresh
     // multi-GB allocation per run makes the stream-ordered pool remap memory
     // (measured 0.8 s for a 16 GB output buffer at C4).
