@@ -275,12 +275,14 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     A.col.alloc(size_t(nnz), s);
     A.val.alloc(size_t(nnz), s);
     DBuf<int64_t> col64(size_t(nnz), s);
+    std::unique_ptr<Prof> ph(new Prof(c, "upload_h2d", 8.0 * (rows + 1) + 16.0 * nnz, 0));
     FB_CUDA(cudaMemcpyAsync(A.rowptr.get(), h_rp, sizeof(int64_t) * (rows + 1),
                             cudaMemcpyHostToDevice, s));
     if (nnz) {
         FB_CUDA(cudaMemcpyAsync(col64.get(), h_col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
         FB_CUDA(cudaMemcpyAsync(A.val.get(), h_val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
     }
+    ph.reset(new Prof(c, "upload_validate", 0, 0));
     DBuf<unsigned long long> err(2, s);
     FB_CUDA(cudaMemsetAsync(err.get(), 0xff, err.bytes(), s));
     if (rows) {
@@ -323,6 +325,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     }
     if (m_valid < rows) throw InvalidArgument(kValidateMsg[0]);
     col64.release();
+    ph.reset(new Prof(c, "upload_transpose", 0, 0));
 
     // ---- transposed CSR (stable radix sort by column keeps ascending rows,
     // the order spmm_transpose accumulates in, sparse_matrix.hpp:229-237)
@@ -359,9 +362,11 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         const char* e = std::getenv("FRPCA_HOT_STAGING");
         return e && e[0] == '1';
     }();
+    ph.reset(new Prof(c, "upload_items", 0, 0));
     if (hot) build_hot(c, A, T);
     build_items(c, A, nullptr, A.L, default_chunk(c, A));
     build_items(c, T, nullptr, T.L, default_chunk(c, T));
+    ph.reset();
     FB_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -450,6 +455,7 @@ __global__ void k_panel_walk(const int64_t* __restrict__ rp, const int32_t* __re
 void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap) {
     PanelPlan& P = T.pan;
     if (P.pr == pr) return;
+    Prof prof(c, "panel_plan", 0, 0);
     P = PanelPlan{};
     if (T.rows == 0 || T.nnz == 0 || pr <= 0) return;
     cudaStream_t s = c.stream;

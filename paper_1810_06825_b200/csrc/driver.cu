@@ -183,7 +183,11 @@ static void output_products(Ctx& c, const RunArgs& a, int64_t l, int64_t k, OutP
         FB_CUDA(cudaMemcpyAsync(sml.user, sml.dev, sizeof(double) * sml.rows * k, cudaMemcpyDeviceToHost, c.copy));
     if (a.S && k) FB_CUDA(cudaMemcpyAsync(a.S, So, sizeof(double) * k, cudaMemcpyDeviceToHost, c.copy));
     const int64_t R = big.rows;
-    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(8, R / 4096));
+    static const int64_t maxch = [] {
+        const char* e = std::getenv("FRPCA_OUT_CHUNKS");
+        return e ? std::max(1, std::atoi(e)) : 8;
+    }();
+    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(maxch, R / 4096));
     for (int64_t q = 0; q < nch; ++q) {
         const int64_t r0 = R * q / nch, r1 = R * (q + 1) / nch;
         if (r1 == r0) continue;

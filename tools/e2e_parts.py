@@ -83,3 +83,18 @@ def d2h_only():
 
 for name, f in (("upload", upload), ("run_dev", run_dev), ("run_host", run_host), ("run_csr", run_csr)):
     print(name, *timed(f), flush=True)
+
+# per-stage profile of one run_csr (main stream only; Omega runs on the side stream)
+_lib.check(L.frpca_profile_reset(ctx._h))
+_lib.check(L.frpca_profile_enable(ctx._h, 1))
+run_csr()
+_lib.check(L.frpca_profile_enable(ctx._h, 0))
+cnt = C.c_int()
+_lib.check(L.frpca_profile_count(ctx._h, C.byref(cnt)))
+rows = []
+for i in range(cnt.value):
+    nm = C.c_char_p(); la = C.c_int64(); ms = C.c_double(); by = C.c_double(); fl = C.c_double()
+    _lib.check(L.frpca_profile_get(ctx._h, i, C.byref(nm), C.byref(la), C.byref(ms), C.byref(by), C.byref(fl)))
+    rows.append((ms.value, nm.value.decode(), la.value))
+for ms, nm, la in sorted(rows, reverse=True):
+    print(f"  {nm:24s} {la:3d} {ms:8.3f} ms")
