@@ -49,10 +49,8 @@ __device__ __forceinline__ void cand_merge(Cand& c, const Cand& o) {
     if (better(o.v, o.pos, c.v, c.pos)) c = o;
 }
 
-// block-wide reduction; the result is returned to every thread
-template <int kT>
-__device__ Cand block_best(Cand c, Cand* sh) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Warp-wide best candidate (cand_merge's total order), returned to every lane.
+__device__ __forceinline__ Cand warp_best(Cand c) {
     for (int o = 16; o; o >>= 1) {
         Cand x;
         x.v = __shfl_xor_sync(0xffffffffu, c.v, o);
@@ -60,6 +58,14 @@ __device__ Cand block_best(Cand c, Cand* sh) {
         x.row = __shfl_xor_sync(0xffffffffu, c.row, o);
         cand_merge(c, x);
     }
+    return c;
+}
+
+// block-wide reduction; the result is returned to every thread
+template <int kT>
+__device__ Cand block_best(Cand c, Cand* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    c = warp_best(c);
     if (lane == 0) sh[warp] = c;
     __syncthreads();
     Cand r = sh[0];
@@ -248,7 +254,8 @@ constexpr int UCH = 64;
 template <int kT>
 __global__ void __launch_bounds__(kT, 1)
 k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* __restrict__ pos_g,
-          Cand* __restrict__ cand, double* __restrict__ cvals, int* __restrict__ err, long long* __restrict__ clk) {
+          Cand* __restrict__ cand, double* __restrict__ cvals, int* __restrict__ err, long long* __restrict__ clk,
+          int novec) {
     extern __shared__ double smem[];
     double* Ps = smem;                      // NB x R (column t at Ps + t R)
     double* U12 = Ps + size_t(NB) * R;      // NB x UCH
@@ -290,15 +297,23 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
             if (tim) clk[1] = clock64();
             // every warp reduces all CTAs' candidates itself (a total order:
             // the same winner everywhere, no block barrier)
+            // (all loads in flight before the merges: the merge order does not
+            // matter, the order is total)
             Cand best{-1.0, INT32_MAX, -1};
-            for (int k = (tid & 31); k < int(gridDim.x); k += 32) cand_merge(best, cand[k]);
-            for (int o = 16; o; o >>= 1) {
-                Cand x;
-                x.v = __shfl_xor_sync(0xffffffffu, best.v, o);
-                x.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
-                x.row = __shfl_xor_sync(0xffffffffu, best.row, o);
-                cand_merge(best, x);
+            {
+                constexpr int kPer = 8;
+                const int lane = tid & 31, G = int(gridDim.x);
+                Cand cs[kPer];
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) {
+                    const int k = lane + 32 * q;
+                    cs[q] = k < G ? cand[k] : Cand{-1.0, INT32_MAX, -1};
+                }
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) cand_merge(best, cs[q]);
+                for (int k = lane + 32 * kPer; k < G; k += 32) cand_merge(best, cand[k]);
             }
+            best = warp_best(best);
             if (!(best.v > tol) || best.row < 0) {  // zero pivot (:81)
                 if (blockIdx.x == 0 && tid == 0) *err = 1;
                 return;  // uniform across the grid
@@ -352,8 +367,11 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
             const int r = e % nr, t = e / nr;
             if (posS[r] >= jb) W[(r0 + r) * l + jb + t] = Ps[size_t(t) * R + r];
         }
+        const bool ptim = clk && blockIdx.x == 0 && tid == 0 && jb == 64;
+        if (ptim) clk[8] = clock64();
         const int c0 = jb + bw, tcols = l - c0;
         grid.sync();
+        if (ptim) clk[9] = clock64();
         if (tcols <= 0) break;
         for (int e = tid; e < bw * bw; e += kT) {
             const int t = e / bw, s2 = e % bw;
@@ -361,6 +379,9 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
         }
         const int nbw = min(NB, tcols);
         const int nch = (tcols + UCH - 1) / UCH;
+        // nbw is a multiple of 8 whenever the vector path writes Ps (cc0 + cb < nbw)
+        const bool vec = !novec && bw == NB && (l % 2) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
+                         (nbw % 8) == 0;
         Cand nc{-1.0, INT32_MAX, -1};
         for (int ch = nch - 1; ch >= 0; --ch) {
             const int cc0 = ch * UCH, cw = min(UCH, tcols - cc0);
@@ -370,6 +391,7 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
                 U12[t * UCH + cc] = W[int64_t(prow[t]) * l + c0 + cc0 + cc];
             }
             __syncthreads();
+            if (ptim && ch < 2) clk[10 + 3 * ch] = clock64();
             for (int cc = tid; cc < cw; cc += kT)  // U12 = L11^{-1} A12, column by column
                 for (int t = 1; t < bw; ++t) {
                     double acc = U12[t * UCH + cc];
@@ -377,6 +399,7 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
                     U12[t * UCH + cc] = acc;
                 }
             __syncthreads();
+            if (ptim && ch < 2) clk[11 + 3 * ch] = clock64();
             for (int r = tid; r < nr; r += kT) {
                 const int32_t p = posS[r];
                 if (p < c0) continue;  // pivot of this or an earlier panel
@@ -386,6 +409,34 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
                 for (int t = 0; t < NB; ++t)
                     if (t < bw) Lr[t] = Ps[size_t(t) * R + r];
                 for (int cb = 0; cb < cw; cb += 8) {
+                    if (vec && cb + 8 <= cw) {
+                        // full panel, full 8-column block: no guards, W and
+                        // U12 as double2 (same FMA order as below)
+                        double2* w2 = reinterpret_cast<double2*>(wr + c0 + cc0 + cb);
+                        double2 a2[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) a2[e] = w2[e];
+#pragma unroll
+                        for (int t = 0; t < NB; ++t) {
+                            const double2* u2 = reinterpret_cast<const double2*>(U12 + t * UCH + cb);
+                            const double lt = -Lr[t];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const double2 uu = u2[e];
+                                a2[e].x = fma(lt, uu.x, a2[e].x);
+                                a2[e].y = fma(lt, uu.y, a2[e].y);
+                            }
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) w2[e] = a2[e];
+                        if (cc0 + cb < nbw)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                Ps[size_t(cc0 + cb + 2 * e) * R + r] = a2[e].x;
+                                Ps[size_t(cc0 + cb + 2 * e + 1) * R + r] = a2[e].y;
+                            }
+                        continue;
+                    }
                     double a[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e)
@@ -406,6 +457,7 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
                 }
                 if (ch == 0) cand_merge(nc, Cand{fabs(Ps[r]), p, int32_t(r0 + r)});
             }
+            if (ptim && ch < 2) clk[12 + 3 * ch] = clock64();
         }
         nc = block_best<kT>(nc, shc);
         publish(nc, nbw);
@@ -457,10 +509,12 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
             Cand* candp = cand.get();
             double* cvp = cvals.get();
             const bool timing = std::getenv("FRPCA_LU_TIMING") != nullptr;
-            DBuf<long long> clk(timing ? 8 : 0, s);
+            DBuf<long long> clk(timing ? 24 : 0, s);
+            if (timing) FB_CUDA(cudaMemsetAsync(clk.get(), 0, clk.bytes(), s));
             long long* clkp = clk.get();
+            int novec = std::getenv("FRPCA_LU_NOVEC") != nullptr;
             void* args[] = {&W, &m, &L, const_cast<double*>(&tol), const_cast<int*>(&R), &posp, &candp, &cvp, &errp,
-                            &clkp};
+                            &clkp, &novec};
             FB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_lu_smem<kTS>), dim3(grid), dim3(kTS), args,
                                                 smem_s, s));
             count_launch();
@@ -469,10 +523,14 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
             FB_CUDA(cudaStreamSynchronize(s));
             if (h_err) throw NumericalError("lu_basis: zero pivot, input is rank-deficient");
             if (timing) {
-                long long h[8];
+                long long h[24];
                 FB_CUDA(cudaMemcpy(h, clk.get(), sizeof(h), cudaMemcpyDeviceToHost));
                 std::fprintf(stderr, "lu_smem step 100 (cycles): sync %lld cand %lld u %lld rows %lld best %lld | panel end %lld\n",
                              h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4], h[7] - h[6]);
+                std::fprintf(stderr, "  panel 64: writeback %lld gridsync %lld | chunk1 stage %lld trsm %lld update %lld |"
+                             " chunk0 stage %lld trsm %lld update %lld | best %lld\n",
+                             h[8] - h[6], h[9] - h[8], h[13] - h[9], h[14] - h[13], h[15] - h[14], h[10] - h[15],
+                             h[11] - h[10], h[12] - h[11], h[7] - h[12]);
             }
             const int agrid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms * 16, (m * l + 255) / 256)));
             k_assemble<<<agrid, 256, 0, s>>>(W, m, L, pos.get());
