@@ -37,6 +37,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_BYTES = 126 * 1024 * 1024
+# L2 gather ceiling of this B200: a warp per 1600-byte row from an L2-resident
+# table (tools/probe/l2_bw.cu, profiles/r1_l2_probe.txt; 8.8 TB/s from a
+# uniform 160 MB table, 16.9 TB/s from 32 MB)
+L2_GATHER_PEAK_GBS = 16933.7
 
 
 def log(*a):
@@ -351,6 +355,18 @@ def run_gpu_arm(args, cfg):
     sp_launches = sum(v["launches"] for v in sp)
     achieved = (sp_bytes / (sp_ms / 1e3)) / 1e9 if sp_ms > 0 else 0.0
     achieved = dist.sum(achieved) if world > 1 else achieved
+    # the binding unit at l = 200: every nonzero gathers one l-double row of the
+    # dense operand through L2 (nnz * l * 8 bytes per launch)
+    l_cols = cfg.k + cfg.s
+    l2_gathers = {}
+    for kname in ("spmm_AX", "spmm_AtY"):
+        v = prof.get(kname)
+        if v and v["ms"] > 0:
+            l2_gathers[kname] = round(nnz_loc * l_cols * 8.0 * v["launches"] / (v["ms"] / 1e3) / 1e9, 1)
+    l2_ms = sum(prof[kn]["ms"] for kn in l2_gathers)
+    l2_launch = sum(prof[kn]["launches"] for kn in l2_gathers)
+    l2_achieved = nnz_loc * l_cols * 8.0 * l2_launch / (l2_ms / 1e3) / 1e9 if l2_ms > 0 else 0.0
+    l2_achieved = dist.sum(l2_achieved) if world > 1 else l2_achieved
     total_ms = sum(v["ms"] for kname, v in prof.items() if kname not in ("lu_basis",)) or 1.0
     kernels = {kname: {"launches": v["launches"] // max(1, args.steps) if v["launches"] >= args.steps else v["launches"],
                        "ms_per_step": round(v["ms"] / args.steps, 4),
@@ -380,6 +396,11 @@ def run_gpu_arm(args, cfg):
                      "traffic": ncu_traffic(cfg.name),
                      "launches_per_step": sp_launches // max(1, args.steps),
                      "share_of_step": round(sp_ms / max(1e-9, sum(step_ms)), 4)},
+        "roofline_l2": {"bound": "l2", "kernel": "spmm row gathers (nnz * l * 8 B per launch)",
+                        "achieved": round(l2_achieved, 1), "peak": L2_GATHER_PEAK_GBS, "unit": "GB/s",
+                        "frac": round(l2_achieved / L2_GATHER_PEAK_GBS, 4),
+                        "peak_kind": "measured L2-resident row gather (profiles/r1_l2_probe.txt)",
+                        "per_kernel": l2_gathers},
         "e2e": {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "statistic": "median of steps",
                 "mean": round(e2e_mean_s, 6), "call": "frpca_run_csr" if world == 1 else "frpca_dmat_upload_shard + frpca_run"},

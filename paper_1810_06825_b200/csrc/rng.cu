@@ -174,11 +174,12 @@ constexpr int CHUNK = PT * PPT;
 __global__ void __launch_bounds__(PT)
 k_count(const uint64_t* __restrict__ raw, int64_t npairs, int64_t* __restrict__ cnt) {
     __shared__ int red[PT / 32];
-    const int64_t p0 = int64_t(blockIdx.x) * CHUNK + threadIdx.x * PPT;
+    // chunk b = attempts [b CHUNK, (b + 1) CHUNK), lane-interleaved (coalesced)
+    const int64_t p0 = int64_t(blockIdx.x) * CHUNK + threadIdx.x;
     int c = 0;
     #pragma unroll
     for (int e = 0; e < PPT; ++e) {
-        const int64_t q = p0 + e;
+        const int64_t q = p0 + int64_t(e) * PT;
         if (q < npairs) {
             const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(raw + 2 * q);
             double x, y, r2;
@@ -196,39 +197,53 @@ k_count(const uint64_t* __restrict__ raw, int64_t npairs, int64_t* __restrict__ 
 }
 
 // normals of the accepted attempts, written at their stream positions
-__global__ void __launch_bounds__(PT)
+__global__ void __launch_bounds__(PT, 5)
 k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restrict__ off,
        double* __restrict__ out, int64_t count, const crlog::LogEntry* __restrict__ logtab) {
-    using Scan = cub::BlockScan<int, PT>;
+    // round e of the chunk = attempts b CHUNK + e PT + [0, PT) (coalesced
+    // loads); the stream position of an accepted attempt = accepted attempts
+    // of the earlier rounds + of the lower lanes of its round: one block scan
+    // of the per-round flags packed in 16-bit fields
+    using Scan = cub::BlockScan<unsigned long long, PT>;
     __shared__ typename Scan::TempStorage tmp;
     const int64_t base = off[blockIdx.x];
     if (2 * base >= count) return;
-    const int64_t p0 = int64_t(blockIdx.x) * CHUNK + threadIdx.x * PPT;
+    const int64_t p0 = int64_t(blockIdx.x) * CHUNK + threadIdx.x;
     double xs[PPT], ys[PPT], rs[PPT];
     bool ok[PPT];
-    int c = 0;
+    unsigned long long flags = 0;
     #pragma unroll
     for (int e = 0; e < PPT; ++e) {
-        const int64_t q = p0 + e;
+        const int64_t q = p0 + int64_t(e) * PT;
         ok[e] = false;
         if (q < npairs) {
             const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(raw + 2 * q);
             ok[e] = attempt(w.x, w.y, xs[e], ys[e], rs[e]);
         }
-        c += ok[e] ? 1 : 0;
+        flags |= (ok[e] ? 1ull : 0ull) << (16 * e);
     }
-    int pre = 0;
-    Scan(tmp).ExclusiveSum(c, pre);
-    int64_t idx = 2 * (base + pre);
+    unsigned long long pre = 0, tot = 0;
+    Scan(tmp).ExclusiveSum(flags, pre, tot);
+    const bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    int64_t rb = base;
     #pragma unroll
     for (int e = 0; e < PPT; ++e) {
-        if (!ok[e]) continue;
-        // mult = sqrt(-2 log(r2) / r2); y*mult first, then the saved x*mult; each
-        // passes through `ret * stddev + mean` with (1, 0) (random.tcc).
-        const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, crlog::fast_log(rs[e], logtab)), rs[e]));
-        if (idx < count) out[idx] = __dadd_rn(__dmul_rn(__dmul_rn(ys[e], mult), 1.0), 0.0);
-        if (idx + 1 < count) out[idx + 1] = __dadd_rn(__dmul_rn(__dmul_rn(xs[e], mult), 1.0), 0.0);
-        idx += 2;
+        if (ok[e]) {
+            const int64_t idx = 2 * (rb + int64_t((pre >> (16 * e)) & 0xffffull));
+            // mult = sqrt(-2 log(r2) / r2); y*mult first, then the saved
+            // x*mult; each passes through `ret * stddev + mean` with (1, 0)
+            // (random.tcc).
+            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, crlog::fast_log(rs[e], logtab)), rs[e]));
+            const double a = __dadd_rn(__dmul_rn(__dmul_rn(ys[e], mult), 1.0), 0.0);
+            const double b = __dadd_rn(__dmul_rn(__dmul_rn(xs[e], mult), 1.0), 0.0);
+            if (vec && idx + 1 < count) {
+                __stcs(reinterpret_cast<double2*>(out + idx), make_double2(a, b));
+            } else {
+                if (idx < count) out[idx] = a;
+                if (idx + 1 < count) out[idx + 1] = b;
+            }
+        }
+        rb += int64_t((tot >> (16 * e)) & 0xffffull);
     }
 }
 
