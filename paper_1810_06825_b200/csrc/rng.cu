@@ -132,28 +132,34 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ polys, 
     if (tid < NN) states[size_t(k) * NN + tid] = R[cur][tid];
 }
 
-// Raw stream of a segment: 156 new words per step, one barrier per step
-// (ping-ponged window); the tempered outputs go straight to global memory.
-__global__ void __launch_bounds__(320)
+// Raw stream of a segment: 156 new words per step, one barrier per step. The
+// words live in a ring of 4 x 156: step s reads its window at ring offset
+// (s mod 4) 156 ([b, b + 312)) and writes the new words at [b + 312, b + 468)
+// (mod 624), so no window copy; the tempered outputs go straight to global
+// memory (coalesced). 160 threads: the last 4 only keep the barrier count.
+constexpr int GT = 160;
+constexpr int kGenPerSm = 6;  // segments per SM the host plans for (5 warps each)
+__global__ void __launch_bounds__(GT)
 k_gen(const uint64_t* __restrict__ states, int64_t seg0, int64_t steps, uint64_t* __restrict__ raw) {
-    __shared__ uint64_t X[2][NN];
+    constexpr int RING = 4 * MM;
+    __shared__ uint64_t X[RING];
     const int tid = threadIdx.x;
     const int64_t seg = seg0 + blockIdx.x;
-    if (tid < NN) X[0][tid] = states[seg * NN + tid];
+    for (int i = tid; i < NN; i += GT) X[i] = states[seg * NN + i];
     __syncthreads();
-    uint64_t* dst = raw + int64_t(blockIdx.x) * steps * MM;
-    int cur = 0;
+    uint64_t* dst = raw + int64_t(blockIdx.x) * steps * MM + tid;
+    int b = 0;
     for (int64_t st = 0; st < steps; ++st) {
         if (tid < MM) {
-            X[cur ^ 1][tid] = X[cur][tid + MM];
-        } else if (tid < NN) {
-            const int t = tid - MM;
-            const uint64_t* x = X[cur];
-            const uint64_t nw = mt_next(x[t], x[t + 1], x[t + MM]);
-            X[cur ^ 1][tid] = nw;
-            dst[st * MM + t] = temper(nw);
+            const int i0 = b + tid;
+            const int i1 = i0 + 1 < RING ? i0 + 1 : i0 + 1 - RING;
+            const int i2 = i0 + MM < RING ? i0 + MM : i0 + MM - RING;
+            const int io = i0 + 2 * MM < RING ? i0 + 2 * MM : i0 + 2 * MM - RING;
+            const uint64_t nw = mt_next(X[i0], X[i1], X[i2]);
+            X[io] = nw;
+            dst[st * MM] = temper(nw);
         }
-        cur ^= 1;
+        b = b + MM < RING ? b + MM : 0;
         __syncthreads();
     }
 }
@@ -315,14 +321,9 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     const double half = 0.5 * double(count);
     const int64_t P = int64_t(half / (M_PI / 4.0) + 8.0 * std::sqrt(half / (M_PI / 4.0)) + 64.0);
     // segments of J = 156 * 2^e words: the fewest that still fill the
-    // generator (one 320-thread CTA per segment, k_gen occupancy), capped so
+    // generator (one CTA per segment, kGenPerSm per SM), capped so
     // that a batch of <= 2^30 raw words holds >= that many segments
-    static int gen_per_sm = 0;
-    if (!gen_per_sm) {
-        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gen_per_sm, k_gen, 320, 0));
-        gen_per_sm = std::max(gen_per_sm, 1);
-    }
-    const int64_t fill = int64_t(c.num_sms) * gen_per_sm;
+    const int64_t fill = int64_t(c.num_sms) * kGenPerSm;
     int log2S = 6;
     while (log2S < 12 && (2 * P + (int64_t(MM) << log2S) - 1) / (int64_t(MM) << log2S) > fill) ++log2S;
     const int64_t steps = int64_t(1) << log2S, J = int64_t(MM) << log2S;
@@ -371,7 +372,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         const int64_t nchunks = (npairs + CHUNK - 1) / CHUNK;
         {
             Prof pg(c, "omega_gen", 8.0 * nseg * J, 0.0);
-            k_gen<<<unsigned(nseg), 320, 0, s>>>(states.get(), seg0, steps, raw.get());
+            k_gen<<<unsigned(nseg), GT, 0, s>>>(states.get(), seg0, steps, raw.get());
             FB_LAUNCH_CHECK();
         }
         DBuf<int64_t> cnt(size_t(nchunks) + 1, s), off(size_t(nchunks) + 1, s);
