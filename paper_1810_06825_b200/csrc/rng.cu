@@ -76,23 +76,22 @@ constexpr int JW = 64;             // coefficients per Horner step
 constexpr int NTAB = NN + JW;      // table row length (j + 4q + 3 < NN + 63)
 constexpr size_t kNibBytes = sizeof(uint64_t) * 16 * NTAB;
 
-__global__ void __launch_bounds__(320, 2)
+// (ext is dead once the nibble table is built and holds the first window:
+// 56 KB per CTA, four CTAs per SM)
+__global__ void __launch_bounds__(320, 4)
 k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ polys, int groups, int64_t first,
              int64_t k0, int64_t k1) {
     __shared__ uint64_t ext[NN + JW];
     extern __shared__ uint64_t nib_dyn[];  // [16][NTAB]
     uint64_t (*nib)[NTAB] = reinterpret_cast<uint64_t (*)[NTAB]>(nib_dyn);
-    __shared__ uint64_t R[2][NN];
+    __shared__ uint64_t R1[NN];
     __shared__ uint32_t co[640];
     const int tid = threadIdx.x;
     const int64_t k = k0 + blockIdx.x;
     if (k >= k1) return;
     const uint64_t* src = states + size_t(k % first) * NN;
     const uint32_t* poly = polys + size_t(k / first - 1) * groups;
-    if (tid < NN) {
-        ext[tid] = src[tid];
-        R[0][tid] = 0;
-    }
+    if (tid < NN) ext[tid] = src[tid];
     for (int g = tid; g < groups; g += blockDim.x) co[g] = poly[g];
     __syncthreads();
     if (tid < JW) ext[NN + tid] = mt_next(ext[tid], ext[tid + 1], ext[tid + MM]);
@@ -106,6 +105,8 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ polys, 
         nib[v][j] = x;
     }
     __syncthreads();
+    if (tid < NN) ext[tid] = 0;  // window 0
+    __syncthreads();
     int cur = 0;
     const int ng = (groups + 1) / 2;  // 64-bit coefficient groups
     for (int g = ng - 1; g >= 0; --g) {
@@ -116,7 +117,7 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ polys, 
             for (int q = 0; q < 8; ++q) x ^= nib[(lo >> (4 * q)) & 15u][tid + 4 * q];
             #pragma unroll
             for (int q = 0; q < 8; ++q) x ^= nib[(hi >> (4 * q)) & 15u][tid + 32 + 4 * q];
-            const uint64_t* r = R[cur];
+            const uint64_t* r = cur ? R1 : ext;
             uint64_t v;
             if (tid < NN - JW) {
                 v = r[tid + JW];
@@ -124,12 +125,12 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ polys, 
                 const int t = tid - (NN - JW);
                 v = mt_next(r[t], r[t + 1], r[t + MM]);
             }
-            R[cur ^ 1][tid] = v ^ x;
+            (cur ? ext : R1)[tid] = v ^ x;
         }
         cur ^= 1;
         __syncthreads();
     }
-    if (tid < NN) states[size_t(k) * NN + tid] = R[cur][tid];
+    if (tid < NN) states[size_t(k) * NN + tid] = (cur ? R1 : ext)[tid];
 }
 
 // Raw stream of a segment: 156 new words per step, one barrier per step. The
