@@ -7,3 +7,5 @@ for c in C2 C3 C4; do python bench.py --config $c --steps 3 --warmup 3 --no-cpu-
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c1_short.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1.csv \
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_spmm" -c 6 -o gpurun_out/spmm_c1 -f \
+  python tools/profile_run.py --config C1 --runs 1 > gpurun_out/ncu_spmm.log 2>&1
