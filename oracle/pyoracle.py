@@ -14,7 +14,9 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "_build", "liboracle.so")
+# ORACLE_VARIANT=fma selects the FMA-contracted build (noise-floor runs only)
+_SO = os.path.join(_HERE, "_build", "liboracle_fma.so" if os.environ.get("ORACLE_VARIANT") == "fma"
+                   else "liboracle.so")
 
 _i64 = C.c_int64
 _u64 = C.c_uint64
@@ -30,11 +32,32 @@ class NumericalError(RuntimeError):
 def build() -> str:
     if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(
             os.path.join(_HERE, "oracle.cpp")):
-        subprocess.check_call(["make", "-s", "-C", _HERE])
+        subprocess.check_call(["make", "-s", "-C", _HERE, os.path.relpath(_SO, _HERE)])
     return _SO
 
 
 _lib = None
+
+
+class variant:
+    """`with variant("fma"):` binds the FMA-contracted build of the same
+    restatement for the enclosed calls (noise-floor measurement only; objects
+    created inside must be used inside)."""
+
+    def __init__(self, name: str):
+        self.so = os.path.join(_HERE, "_build", f"liboracle_{name}.so")
+
+    def __enter__(self):
+        global _lib, _SO
+        self.saved = (_lib, _SO)
+        _lib, _SO = None, self.so
+        build()
+        return self
+
+    def __exit__(self, *exc):
+        global _lib, _SO
+        _lib, _SO = self.saved
+        return False
 
 
 def lib():

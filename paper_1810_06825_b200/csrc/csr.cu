@@ -250,6 +250,41 @@ void build_hot(Ctx& c, DCsr& A, const DCsr& T) {
     FB_LAUNCH_CHECK();
 }
 
+__global__ void k_rank_all(const int32_t* __restrict__ ids, int64_t n, int32_t* __restrict__ rank_of) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x)
+        rank_of[ids[r]] = int32_t(r);
+}
+
+__global__ void k_flag_hint(int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ rank_of,
+                            int64_t H) {
+    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < nnz;
+         p += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t cc = col[p] & kColMask;
+        col[p] = rank_of[cc] < H ? int32_t(uint32_t(cc) | 0x80000000u) : cc;
+    }
+}
+
+// Popularity rank of every column of A (counts = row lengths of T), kept for
+// the L2 hints of A*X.
+void build_ranks(Ctx& c, DCsr& A, const DCsr& T) {
+    const int64_t n = A.cols;
+    if (n == 0 || A.nnz == 0) return;
+    cudaStream_t s = c.stream;
+    DBuf<int32_t> cnt(size_t(n), s), ids(size_t(n), s), cnt_s(size_t(n), s), ids_s(size_t(n), s);
+    k_col_counts<<<grid_for(c, n), 256, 0, s>>>(T.rowptr.get(), n, cnt.get(), ids.get());
+    FB_LAUNCH_CHECK();
+    size_t tb = 0;
+    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.get(), cnt_s.get(), ids.get(),
+                                                      ids_s.get(), n, 0, 32, s));
+    DBuf<unsigned char> tmp(tb, s);
+    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), tb, cnt.get(), cnt_s.get(), ids.get(),
+                                                      ids_s.get(), n, 0, 32, s));
+    A.rank_of.alloc(size_t(n), s);
+    k_rank_all<<<grid_for(c, n), 256, 0, s>>>(ids_s.get(), n, A.rank_of.get());
+    FB_LAUNCH_CHECK();
+    A.hint_h = 0;
+}
+
 const char* kValidateMsg[3] = {
     "csr: row_ptr must be non-decreasing",
     "csr: column index out of range",
@@ -364,6 +399,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     }();
     ph.reset(new Prof(c, "upload_items", 0, 0));
     if (hot) build_hot(c, A, T);
+    else build_ranks(c, A, T);
     build_items(c, A, nullptr, A.L, default_chunk(c, A));
     build_items(c, T, nullptr, T.L, default_chunk(c, T));
     ph.reset();
@@ -674,6 +710,21 @@ void csr_from_triplets_device(Ctx& c, int64_t rows, int64_t cols, int64_t n, con
     *nnz = total;
 }
 
+void ensure_hint(Ctx& c, DCsr& A, int64_t w) {
+    if (!A.rank_of.n || A.nhot) return;
+    // budget of L2-kept X rows; hints only when X is well beyond it
+    const char* e = std::getenv("FRPCA_HINT_MB");
+    const double mb = e && *e ? std::atof(e) : 64.0;
+    const double budget = mb * 1048576.0;
+    int64_t H = 0;
+    if (budget > 0 && 8.0 * double(A.cols) * double(w) > 2.0 * budget)
+        H = std::min<int64_t>(A.cols, std::max<int64_t>(1, int64_t(budget / (8.0 * double(w)))));
+    if (H == A.hint_h) return;
+    k_flag_hint<<<grid_for(c, A.nnz), 256, 0, c.stream>>>(A.col.get(), A.nnz, A.rank_of.get(), H);
+    FB_LAUNCH_CHECK();
+    A.hint_h = H;
+}
+
 void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v) {
     std::vector<int32_t> tmp(static_cast<size_t>(A.nnz));
     FB_CUDA(cudaMemcpyAsync(rp, A.rowptr.get(), sizeof(int64_t) * (A.rows + 1),
@@ -685,7 +736,7 @@ void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v) {
                                 c.stream));
     }
     FB_CUDA(cudaStreamSynchronize(c.stream));
-    for (int64_t i = 0; i < A.nnz; ++i) ci[i] = tmp[size_t(i)];
+    for (int64_t i = 0; i < A.nnz; ++i) ci[i] = tmp[size_t(i)] & kColMask;
 }
 
 }  // namespace fb

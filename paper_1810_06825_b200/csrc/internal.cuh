@@ -65,8 +65,15 @@ struct DCsr {
     // the original column id.
     DBuf<int32_t> hot_cols;
     int64_t nhot = 0;
+    // L2 hints (A only): popularity rank of every column (nnz, ties to the
+    // lower id), and the number hint_h of top-ranked columns whose ids carry
+    // the sign bit (X rows kept in L2 with evict_last, spmm.cu MODE_HINT).
+    // Re-encoded by ensure_hint when the call's width changes the budget.
+    DBuf<int32_t> rank_of;
+    int64_t hint_h = 0;
     PanelPlan pan;  // on A^T only
 };
+constexpr int32_t kColMask = 0x7fffffff;
 constexpr int kHot = 4096;
 
 struct ProfAgg {
@@ -142,6 +149,8 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
 void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v);
 // work list of A's rows (rows with skip[r] != 0 left out), chunk size ch
 void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_t ch);
+// sign-bit L2 hints on A's column ids for an A*X of width w (<= 256)
+void ensure_hint(Ctx& c, DCsr& A, int64_t w);
 // panel plan of T (== A^T) for panels of pr rows of the gathered operand
 void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap);
 

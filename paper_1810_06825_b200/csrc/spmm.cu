@@ -26,6 +26,12 @@ template <>
 struct Vec<2> {
     using T = double2;
     __device__ static T load(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+    __device__ static T load_pol(const double* p, uint64_t pol) {
+        T r;
+        asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+        return r;
+    }
     __device__ static void fma(T& a, double v, const T& x) {
         a.x = __fma_rn(v, x.x, a.x);
         a.y = __fma_rn(v, x.y, a.y);
@@ -39,6 +45,11 @@ template <>
 struct Vec<1> {
     using T = double;
     __device__ static T load(const double* p) { return __ldg(p); }
+    __device__ static T load_pol(const double* p, uint64_t pol) {
+        T r;
+        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+        return r;
+    }
     __device__ static void fma(T& a, double v, const T& x) { a = __fma_rn(v, x, a); }
     __device__ static void store(double* p, const T& a) { __stcs(p, a); }
     __device__ static T zero() { return 0.0; }
@@ -52,15 +63,34 @@ struct Hot {
     const double* Xs;        // H x ncols in shared memory (nullptr when H == 0)
     int H;
     const int32_t* cols;     // rank -> original column id
+    uint64_t keep, stream;   // L2 policies of MODE_HINT: evict_last / evict_first
 };
 
-template <int VEC, int NCH, bool HOT>
+// Gather modes: plain ids; hot ids -(rank+1) (staging, opt-in); ids whose
+// sign bit marks an L2-hot X row (DCsr::hint_h): hot rows are loaded with an
+// evict_last policy, the others evict_first, so the rare rows streamed from
+// HBM do not push the popular rows out of L2.
+constexpr int MODE_PLAIN = 0, MODE_HOT = 1, MODE_HINT = 2;
+
+__device__ __forceinline__ void make_policies(Hot& h) {
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(h.keep));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(h.stream));
+}
+
+template <int VEC, int NCH, int MODE>
 __device__ __forceinline__ void gather(typename Vec<VEC>::T (&x)[NCH], int c, const double* __restrict__ Xl,
                                        int64_t ldx, const bool (&ok)[NCH], int lane, int ncols,
                                        const Hot& hot) {
     using V = Vec<VEC>;
     using T = typename V::T;
-    if (HOT) {
+    if (MODE == MODE_HINT) {
+        const uint64_t pol = c < 0 ? hot.keep : hot.stream;
+        const double* src = Xl + int64_t(c & 0x7fffffff) * ldx;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) x[ch] = ok[ch] ? V::load_pol(src + ch * 32 * VEC, pol) : V::zero();
+        return;
+    }
+    if (MODE == MODE_HOT) {
         // one generic pointer for both sources: shared copy or global row
         const double* src;
         if (c < 0) {
@@ -80,7 +110,7 @@ __device__ __forceinline__ void gather(typename Vec<VEC>::T (&x)[NCH], int c, co
         x[ch] = ok[ch] ? V::load(Xl + int64_t(c) * ldx + ch * 32 * VEC) : V::zero();
 }
 
-template <int VEC, int NCH, bool HOT>
+template <int VEC, int NCH, int MODE>
 __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
                                                const double* __restrict__ val, int64_t p0, int64_t p1,
                                                const double* __restrict__ X, int64_t ldx,
@@ -111,7 +141,7 @@ __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
             }
             T x[4][NCH];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) gather<VEC, NCH, HOT>(x[u], c[u], Xl, ldx, ok, lane, ncols, hot);
+            for (int u = 0; u < 4; ++u) gather<VEC, NCH, MODE>(x[u], c[u], Xl, ldx, ok, lane, ncols, hot);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -133,7 +163,7 @@ __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
             }
             T x[3][NCH];
 #pragma unroll
-            for (int u = 0; u < 3; ++u) gather<VEC, NCH, HOT>(x[u], c[u], Xl, ldx, ok, lane, ncols, hot);
+            for (int u = 0; u < 3; ++u) gather<VEC, NCH, MODE>(x[u], c[u], Xl, ldx, ok, lane, ncols, hot);
 #pragma unroll
             for (int u = 0; u < 3; ++u)
 #pragma unroll
@@ -142,7 +172,7 @@ __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
     }
 }
 
-template <int VEC, int NCH, bool HOT>
+template <int VEC, int NCH, int MODE>
 __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                            const double* __restrict__ val, const WorkItem* __restrict__ items,
                                            int64_t nitems, const double* __restrict__ X, int64_t ldx,
@@ -161,7 +191,7 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
                 T acc[NCH];
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
-                row_accumulate<VEC, NCH, HOT>(col, val, rowptr[r], rowptr[r + 1], X, ldx, lane, ncols, hot, acc);
+                row_accumulate<VEC, NCH, MODE>(col, val, rowptr[r], rowptr[r + 1], X, ldx, lane, ncols, hot, acc);
                 double* yr = Y + int64_t(r) * ldy + lane * VEC;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch)
@@ -171,7 +201,7 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
             T acc[NCH];
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
-            row_accumulate<VEC, NCH, HOT>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc);
+            row_accumulate<VEC, NCH, MODE>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc);
             const int64_t slot = -int64_t(w.r1) - 1;
             double* pr = part + slot * ncols + lane * VEC;
 #pragma unroll
@@ -182,16 +212,17 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
 }
 
 // Plain kernel (A^T * Y, and A * X when no column is hot enough to stage).
-// HOT = true here only decodes hot ids through the rank table (H = 0).
-template <int VEC, int NCH, bool HOT>
+// MODE_HOT here only decodes hot ids through the rank table (H = 0).
+template <int VEC, int NCH, int MODE>
 __global__ void __launch_bounds__(kThreads, 4)
 k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
        const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
        const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
        double* __restrict__ part, int ncols, const int32_t* __restrict__ hot_cols,
        const uint8_t* __restrict__ skip) {
-    const Hot hot{nullptr, 0, HOT ? hot_cols : nullptr};
-    spmm_items<VEC, NCH, HOT>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, skip);
+    Hot hot{nullptr, 0, MODE == MODE_HOT ? hot_cols : nullptr, 0, 0};
+    if (MODE == MODE_HINT) make_policies(hot);
+    spmm_items<VEC, NCH, MODE>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, skip);
 }
 
 // A * X with the H most popular columns' X rows staged in shared memory: one
@@ -212,8 +243,8 @@ k_spmm_hot(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
             __ldg(reinterpret_cast<const double2*>(X + int64_t(hot_cols[r]) * ldx) + c2);
     }
     __syncthreads();
-    const Hot hot{Xs, H, hot_cols};
-    spmm_items<2, NCH, true>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, nullptr);
+    const Hot hot{Xs, H, hot_cols, 0, 0};
+    spmm_items<2, NCH, MODE_HOT>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, nullptr);
 }
 
 // Long rows: Y[row] = sum of its chunk partials in a fixed order. One CTA per
@@ -265,7 +296,7 @@ k_spmm_panels(const int32_t* __restrict__ col, const double* __restrict__ val,
     using V = Vec<2>;
     using T = V::T;
     const int lane = threadIdx.x & 31;
-    const Hot hot{nullptr, 0, nullptr};
+    const Hot hot{nullptr, 0, nullptr, 0, 0};
     for (;;) {
         int it = 0;
         if (lane == 0) it = atomicAdd(counter, 1);
@@ -275,7 +306,7 @@ k_spmm_panels(const int32_t* __restrict__ col, const double* __restrict__ val,
         T acc[NCH];
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
-        row_accumulate<2, NCH, false>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc);
+        row_accumulate<2, NCH, MODE_PLAIN>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc);
         double* pr = part + (-int64_t(w.r1) - 1) * ncols + lane * 2;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
@@ -283,19 +314,19 @@ k_spmm_panels(const int32_t* __restrict__ col, const double* __restrict__ val,
     }
 }
 
-template <int VEC, int NCH, bool HOT>
+template <int VEC, int NCH, int MODE>
 void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
                   double* Y, int64_t ldy, double* part, int ncols) {
     if (!L.nitems) return;
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
-        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<VEC, NCH, HOT>,
+        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<VEC, NCH, MODE>,
                                                               kThreads, 0));
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     int grid = int(std::min<int64_t>(int64_t(c.num_sms) * blocks_per_sm, (L.nitems + 7) / 8));
     grid = std::max(grid, 1);
-    k_spmm<VEC, NCH, HOT><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
+    k_spmm<VEC, NCH, MODE><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
                                                            L.items.get(), L.nitems, X, ldx, Y, ldy, part,
                                                            ncols, A.hot_cols.get(), skip);
     FB_LAUNCH_CHECK();
@@ -323,10 +354,11 @@ void launch_hot(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, 
 template <int VEC, int NCH>
 void launch(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
             double* Y, int64_t ldy, double* part, int ncols) {
-    if (A.nhot == 0) return launch_plain<VEC, NCH, false>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
+    if (A.hint_h > 0 && &L == &A.L) return launch_plain<VEC, NCH, MODE_HINT>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
+    if (A.nhot == 0) return launch_plain<VEC, NCH, MODE_PLAIN>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
     if (VEC == 2 && ncols % 2 == 0 && &L == &A.L && A.L.nitems >= 32 * c.num_sms)
         return launch_hot<NCH>(c, A, X, ldx, Y, ldy, part, ncols);
-    launch_plain<VEC, NCH, true>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
+    launch_plain<VEC, NCH, MODE_HOT>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
 }
 
 void combine(Ctx& c, const ItemList& L, const double* part, int nc, double* Y, int64_t ldy) {
@@ -389,6 +421,7 @@ double env_double(const char* name, double dflt) {
 void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
                  int64_t ldy, const char* tag) {
     if (A.rows == 0 || ncols == 0) return;
+    ensure_hint(c, const_cast<DCsr&>(A), std::min<int64_t>(ncols, 256));
     // algorithmic bytes: 12 B/nnz + 8 B/row ptr + dense in + out
     const double bytes = 12.0 * A.nnz + 8.0 * (A.rows + 1) + 8.0 * ncols * (A.cols + A.rows);
     const double flops = 2.0 * A.nnz * ncols;

@@ -90,7 +90,7 @@ __global__ void k_lowrank_dense(const double* __restrict__ U, const double* __re
 __global__ void k_scatter_dense(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                 const double* __restrict__ val, int64_t m, double* __restrict__ R) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
-        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) R[i + int64_t(col[p]) * m] = val[p];
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) R[i + int64_t(col[p] & kColMask) * m] = val[p];
 }
 
 int vgrid(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>(4096, (n + 255) / 256))); }

@@ -145,6 +145,25 @@ def test_spmm_transpose_panel_sizes(fb, orc, panels, panel_kb, part_gb):
     assert rel_fro(fb.spmm_transpose(A, Y), orc.spmm_transpose(oA, Y)) <= SPMM_TOL
 
 
+@pytest.mark.parametrize("ncols", [1, 40, 200, 150, 64])
+def test_spmm_l2_hints(fb, orc, monkeypatch, ncols):
+    """A*X with sign-bit L2 hints on the popular columns (csr.cu
+    ensure_hint, spmm.cu MODE_HINT) forced at test size: only the cache
+    policy of the gathers changes, so results are bitwise equal to the plain
+    kernel; re-encoding across widths and the masked id download."""
+    oA = powerlaw_csr(orc, 3000, 2000, 120000, 11)
+    A = to_fb(fb, oA)
+    X = orc.gaussian_matrix(2000, ncols, 4)
+    monkeypatch.setenv("FRPCA_HINT_MB", "0")
+    Y0 = fb.spmm(A, X)
+    monkeypatch.setenv("FRPCA_HINT_MB", "0.02")
+    Y1 = fb.spmm(A, X)
+    assert np.array_equal(Y0, Y1)
+    assert rel_fro(Y1, orc.spmm(oA, X)) <= SPMM_TOL
+    X2 = orc.gaussian_matrix(2000, 7, 5)
+    assert rel_fro(fb.spmm(A, X2), orc.spmm(oA, X2)) <= SPMM_TOL
+
+
 def test_spmm_transpose_panelled_empty_rows(fb, orc, panels):
     """Columns of A with no entries (empty rows of A^T) next to hot ones."""
     panels(1.0)
@@ -358,3 +377,4 @@ def test_gram3_equals_gram2(fb, orc, monkeypatch, m, n):
     r2 = fb.eig_svd(A)
     for x, y in zip(r1, r2):
         assert np.array_equal(x, y)
+

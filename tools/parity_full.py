@@ -1,0 +1,105 @@
+"""Full-size parity of a BASELINE config: the B200 path (C ABI) against the CPU
+oracle on the same seeded matrix and the same Omega stream (seed 0).
+
+    python tools/parity_full.py --config C3 [--threads N] [--out file.json]
+
+Reports the north_star bars: max relative sigma error over the
+top-k (<= 1e-10), ||UU^T - U'U'^T||_2 and ||VV^T - V'V'^T||_2 (<= 1e-8),
+computed without m x m matrices, plus pass counts, wall times and host info.
+The oracle is test infrastructure: this tool only checks the product."""
+import argparse
+import json
+import os
+import platform
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_1810_06825_b200 as fb  # noqa: E402
+from paper_1810_06825_b200 import synth  # noqa: E402
+from metrics import sigma_rel, subspace_dist  # noqa: E402
+
+
+def run(name: str, threads: int | None = None, scale: float = 1.0, floor: bool = False) -> dict:
+    cfg = synth.CONFIGS[name]
+    t0 = time.time()
+    m, n, rp, ci, va = synth.generate(name, scale=scale)
+    nnz = int(rp[-1])
+    t_gen = time.time() - t0
+    nth = threads or os.cpu_count() or 1
+    oracle.build()
+    oracle.set_threads(nth)
+    pc = fb.PcaConfig(k=cfg.k, oversample=cfg.s, passes=cfg.q, seed=0)
+    A = fb.SparseMatrixCsr(m, n, rp, ci, va)
+    st = fb.RunStats()
+    algo = fb.frpca if cfg.algorithm == "frpca" else fb.frpcat
+    t0 = time.time()
+    r = algo(A, pc, st)
+    t_gpu = time.time() - t0
+    del A
+    algo_o = oracle.FRPCA if cfg.algorithm == "frpca" else oracle.FRPCAT
+    oA = oracle.Csr.create(m, n, rp, ci, va)
+    t0 = time.time()
+    o = oracle.pca(oA, algo_o, cfg.k, cfg.s, cfg.q, seed=0)
+    t_cpu = time.time() - t0
+    del oA
+    fl = None
+    if floor:
+        # the method's own fp64 floor: the same restatement built with FMA
+        # contraction (different rounding everywhere) against the pinned build
+        with oracle.variant("fma"):
+            oracle.set_threads(nth)
+            o2 = oracle.pca(oracle.Csr.create(m, n, rp, ci, va), algo_o, cfg.k, cfg.s, cfg.q, seed=0)
+        fl = {"sigma_rel": sigma_rel(o2["S"], o["S"]), "subspace_U": subspace_dist(o["U"], o2["U"]),
+              "subspace_V": subspace_dist(o["V"], o2["V"]),
+              "what": "oracle built with -ffp-contract=fast -march=x86-64-v3 vs the pinned build"}
+        del o2
+    del rp, ci, va
+    # conditioning of the extracted spectrum (eig_svd's floor ~ eps (s1/sk)^2)
+    s_ratio = float(o["S"][0] / o["S"][-1])
+    res = {
+        "config": name, "scale": scale, "algorithm": cfg.algorithm, "rows": m, "cols": n,
+        "nnz": nnz,
+        "k": cfg.k, "s": cfg.s, "q": cfg.q, "seed": 0,
+        "sigma_rel": sigma_rel(r.S, o["S"]),
+        "subspace_U": subspace_dist(o["U"], r.U),
+        "subspace_V": subspace_dist(o["V"], r.V),
+        "passes_gpu": st.passes_over_matrix, "passes_oracle": o["stats"]["passes_over_matrix"],
+        "bars": {"sigma_rel": 1e-10, "subspace": 1e-8},
+        "sigma1_over_sigmak": s_ratio,
+        "noise_floor": fl,
+        "seconds": {"generate": round(t_gen, 2), "gpu_call_host_buffers": round(t_gpu, 3),
+                    "oracle": round(t_cpu, 2)},
+        "oracle_threads": nth,
+        "host": {"cpu": platform.processor() or platform.machine(), "nproc": os.cpu_count()},
+    }
+    res["pass"] = bool(res["sigma_rel"] <= 1e-10 and res["subspace_U"] <= 1e-8 and res["subspace_V"] <= 1e-8
+                       and res["passes_gpu"] == cfg.q == res["passes_oracle"])
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--out", default="")
+    ap.add_argument("--floor", action="store_true", help="also measure the oracle's own fp64 noise floor")
+    a = ap.parse_args()
+    res = run(a.config, a.threads or None, a.scale, a.floor)
+    s = json.dumps(res, indent=1)
+    print(s)
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write(s + "\n")
+    sys.exit(0 if res["pass"] else 1)
+
+
+if __name__ == "__main__":
+    main()
