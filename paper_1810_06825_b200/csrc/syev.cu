@@ -65,6 +65,13 @@ __host__ __device__ constexpr bool sytrd_colp(int n) {
 __host__ __device__ constexpr size_t sytrd_smem(int n) {
     return sizeof(double) * (size_t(n) * (n + 1) / 2 + 2 * kEigMax + (sytrd_colp(n) ? kSW * size_t(n) : 0));
 }
+// k_sytrd_fused: packed matrix, double-buffered v and w, column partials
+__host__ __device__ constexpr bool sytrd_fused_fits(int n) {
+    return sizeof(double) * (size_t(n) * (n + 1) / 2 + 4 * kEigMax + kSW * size_t(n)) <= kSmemMax;
+}
+__host__ __device__ constexpr size_t sytrd_fused_smem(int n) {
+    return sizeof(double) * (size_t(n) * (n + 1) / 2 + 4 * kEigMax + kSW * size_t(n));
+}
 
 // Per column: (A) reflector from the norm partials of the previous step,
 // (B) p = tau A22 v with the partials of p^T v, (C) w, (D) A22 -= v w^T +
@@ -278,6 +285,222 @@ k_sytrd(const double* __restrict__ B, int n, double* __restrict__ Hv, double* __
         } else {
             dg[0] = A[0];
         }
+    }
+}
+
+// Fused variant (n <= ~213, the column-partial layout): the rank-2 update of
+// step j and the symmetric product of step j + 1 are one pass over the
+// trailing matrix, so every stored element is loaded and stored once per
+// column instead of being read by (B) and read + written again by (D).
+// Per column j:
+//   (D1) column j + 1 updated with (v_j, w_j) and its norm partials;
+//   (A)  reflector v_{j+1} (double-buffered v, w);
+//   (DB) rows/columns >= j + 2: a -= v_j w_j^T + w_j v_j^T, and in the same
+//        visit p += a v_{j+1} (row part over the lanes, column part into
+//        lane-owned accumulators);
+//   (C)  w_{j+1} = p - (tau/2)(p^T v) v.
+// Same arithmetic per element as k_sytrd; the symmetric-product sums run in
+// the same per-warp / per-lane order.
+template <bool UPD, bool SYM>
+__device__ __forceinline__ void sytrd_pass(double* __restrict__ A, int c0, int n, const double* __restrict__ vo,
+                                           const double* __restrict__ wo, const double* __restrict__ vn,
+                                           double* __restrict__ pw, double* __restrict__ colp) {
+    // trailing block: rows / columns c0 .. n-1 (relative index i', k);
+    // (vo, wo) are indexed relative to c0 - 1 (the step being applied),
+    // vn relative to c0 (the step whose product is formed)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t2 = n - c0;
+    double vr[8], wr[8], nr[8], cacc[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int k = lane + 32 * m;
+        vr[m] = UPD && k < t2 ? vo[k + 1] : 0.0;
+        wr[m] = UPD && k < t2 ? wo[k + 1] : 0.0;
+        nr[m] = SYM && k < t2 ? vn[k] : 0.0;
+        cacc[m] = 0.0;
+    }
+    for (int i0 = warp; i0 < t2; i0 += 8 * kSW) {
+        double a[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            a[r] = 0.0;
+            const int i = i0 + kSW * r;
+            if (i < t2) {
+                double* row = A + rp(c0 + i) + c0;
+                const double vi = UPD ? vo[i + 1] : 0.0, wi = UPD ? wo[i + 1] : 0.0;
+                const double ni = SYM ? vn[i] : 0.0;
+                double x[8];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const int k = lane + 32 * m;
+                    x[m] = (32 * m <= i && k <= i) ? row[k] : 0.0;
+                }
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    if (32 * m > i) break;
+                    const int k = lane + 32 * m;
+                    if (k <= i) {
+                        double y = x[m];
+                        if (UPD) {
+                            y = y - fma(vi, wr[m], wi * vr[m]);
+                            row[k] = y;
+                        }
+                        if (SYM) {
+                            a[r] = fma(y, nr[m], a[r]);
+                            if (k < i) cacc[m] = fma(y, ni, cacc[m]);
+                        }
+                    }
+                }
+            }
+        }
+        if (SYM) {
+            const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double snd = h4 ? a[q] : a[q + 4], keep = h4 ? a[q + 4] : a[q];
+                a[q] = keep + __shfl_xor_sync(0xffffffffu, snd, 16);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const double snd = h3 ? a[q] : a[q + 2], keep = h3 ? a[q + 2] : a[q];
+                a[q] = keep + __shfl_xor_sync(0xffffffffu, snd, 8);
+            }
+            {
+                const double snd = h2 ? a[0] : a[1], keep = h2 ? a[1] : a[0];
+                a[0] = keep + __shfl_xor_sync(0xffffffffu, snd, 4);
+            }
+            a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+            a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+            const int i = i0 + kSW * ((lane >> 2) & 7);
+            if ((lane & 3) == 0 && i < t2) pw[i] = a[0];
+        }
+    }
+    if (SYM) {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int k = lane + 32 * m;
+            if (k < t2) colp[warp * n + k] = cacc[m];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kST, 1)
+k_sytrd_fused(const double* __restrict__ B, int n, double* __restrict__ Hv, double* __restrict__ tau,
+              double* __restrict__ dg, double* __restrict__ eo, long long* __restrict__ clk) {
+    extern __shared__ double sm[];
+    double* A = sm;                     // packed lower, row-major
+    double* vb = A + rp(n);             // [2][kEigMax] Householder vectors (v[0] = 1)
+    double* wb = vb + 2 * kEigMax;      // [2][kEigMax] p, then w
+    double* colp = wb + 2 * kEigMax;    // kSW x n column partials of p
+    __shared__ double redA[32], redB[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = warp; i < n; i += kSW)
+        for (int k = lane; k <= i; k += 32) A[rp(i) + k] = B[k + size_t(i) * n];  // B symmetric
+    __syncthreads();
+    if (n < 3) {
+        if (tid == 0) {
+            if (n == 2) {
+                dg[0] = A[0]; dg[1] = A[2]; eo[0] = A[1]; tau[0] = 0.0;
+            } else if (n == 1) {
+                dg[0] = A[0];
+            }
+        }
+        return;
+    }
+    // reflector of column j into (vb + buf): norm partials in redA
+    auto reflector = [&](int j, int buf, double& tj) {
+        const int t = n - j - 1;
+        const double xnorm2 = warp_total(redA);
+        const double alpha = A[rp(j + 1) + j];
+        double beta = alpha, scal = 0.0;
+        tj = 0.0;
+        if (xnorm2 != 0.0) {
+            beta = -copysign(sqrt(fma(alpha, alpha, xnorm2)), alpha);
+            tj = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        if (tid < t) {
+            const double vi = tid == 0 ? 1.0 : A[rp(j + 1 + tid) + j] * scal;
+            vb[buf * kEigMax + tid] = vi;
+            Hv[size_t(j) * n + tid] = vi;
+        }
+        if (tid == 0) { tau[j] = tj; eo[j] = beta; dg[j] = A[rp(j) + j]; }
+    };
+    // p from the partials, p^T v, then w = p - (tau/2)(p^T v) v, in place
+    auto make_w = [&](int j, int buf, double tj) {
+        const int t = n - j - 1;
+        double* w = wb + buf * kEigMax;
+        const double* v = vb + buf * kEigMax;
+        double a = 0.0, pv = 0.0;
+        if (tid < t) {
+            a = w[tid];
+#pragma unroll
+            for (int q = 0; q < kSW; ++q) a += colp[q * n + tid];
+            a *= tj;
+            pv = a * v[tid];
+        }
+        for (int o = 16; o; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+        if (lane == 0) redB[warp] = pv;
+        __syncthreads();
+        const double alpha2 = -0.5 * tj * warp_total(redB);
+        if (tid < t) w[tid] = fma(alpha2, v[tid], a);
+        __syncthreads();
+    };
+    {   // norm partials of column 0 below its subdiagonal entry
+        double ps = 0.0;
+        for (int i = 2 + warp; i < n; i += kSW) {
+            const double x = A[rp(i)];
+            ps = fma(x, x, ps);
+        }
+        if (lane == 0) redA[warp] = ps;
+    }
+    __syncthreads();
+    double tj;
+    reflector(0, 0, tj);
+    __syncthreads();
+    sytrd_pass<false, true>(A, 1, n, nullptr, nullptr, vb, wb, colp);
+    __syncthreads();
+    make_w(0, 0, tj);
+    for (int j = 0; j + 2 < n; ++j) {
+        const int cur = j & 1, nxt = cur ^ 1;
+        const int t = n - j - 1;
+        const double* vo = vb + cur * kEigMax;
+        const double* wo = wb + cur * kEigMax;
+        const bool tim = clk && j == 20 && tid == 0;
+        if (tim) clk[140] = clock64();
+        {   // (D1) column j + 1 (relative row tid, column 0) and its norm partials
+            double ps = 0.0;
+            if (tid < t) {
+                double* e = A + rp(j + 1 + tid) + (j + 1);
+                const double x = *e - fma(vo[tid], wo[0], wo[tid] * vo[0]);
+                *e = x;
+                if (tid >= 2) ps = x * x;
+            }
+            for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+            if (lane == 0) redA[warp] = ps;
+        }
+        __syncthreads();
+        if (tim) clk[141] = clock64();
+        if (j + 3 < n) {
+            double tn;
+            reflector(j + 1, nxt, tn);
+            __syncthreads();
+            if (tim) clk[142] = clock64();
+            sytrd_pass<true, true>(A, j + 2, n, vo, wo, vb + nxt * kEigMax, wb + nxt * kEigMax, colp);
+            __syncthreads();
+            if (tim) clk[143] = clock64();
+            make_w(j + 1, nxt, tn);
+        } else {
+            sytrd_pass<true, false>(A, j + 2, n, vo, wo, nullptr, nullptr, nullptr);
+            __syncthreads();
+        }
+        if (tim) clk[144] = clock64();
+    }
+    if (tid == 0) {
+        dg[n - 2] = A[rp(n - 2) + n - 2];
+        dg[n - 1] = A[rp(n - 1) + n - 1];
+        eo[n - 2] = A[rp(n - 1) + n - 2];
+        tau[n - 2] = 0.0;
     }
 }
 
@@ -874,6 +1097,7 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>
     static bool attr = false;
     if (!attr) {
         FB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)));
+        FB_CUDA(cudaFuncSetAttribute(k_sytrd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)));
         FB_CUDA(cudaFuncSetAttribute(k_stedc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(stedc_smem())));
         attr = true;
     }
@@ -895,7 +1119,11 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>
     if (timing) FB_CUDA(cudaMemsetAsync(clk.get(), 0, clk.bytes(), s));
     {
         Prof p1(c, "syev_sytrd", 0, 0);
-        k_sytrd<<<1, kST, sytrd_smem(n), s>>>(B, n, H, tau, dg, eo, clk.get());
+        const char* eo_ = std::getenv("FRPCA_SYTRD_UNFUSED");  // tests compare both kernels
+        if (sytrd_fused_fits(n) && !(eo_ && eo_[0] == '1'))
+            k_sytrd_fused<<<1, kST, sytrd_fused_smem(n), s>>>(B, n, H, tau, dg, eo, clk.get());
+        else
+            k_sytrd<<<1, kST, sytrd_smem(n), s>>>(B, n, H, tau, dg, eo, clk.get());
         FB_LAUNCH_CHECK();
     }
     {

@@ -378,3 +378,22 @@ def test_gram3_equals_gram2(fb, orc, monkeypatch, m, n):
     for x, y in zip(r1, r2):
         assert np.array_equal(x, y)
 
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 33, 64, 150, 200, 213, 214, 232])
+def test_sytrd_fused_vs_unfused(fb, orc, monkeypatch, n):
+    """The fused tridiagonalisation (rank-2 update of step j and symmetric
+    product of step j + 1 in one pass) against the two-pass kernel: same
+    spectrum to ~eps ||B||, both within the solver's accuracy bar."""
+    monkeypatch.setenv("FRPCA_EIG", "strict")
+    A = orc.gaussian_matrix(3 * n + 7, n, 11 * n)
+    monkeypatch.delenv("FRPCA_SYTRD_UNFUSED", raising=False)
+    U1, S1, V1 = fb.eig_svd(A)
+    monkeypatch.setenv("FRPCA_SYTRD_UNFUSED", "1")
+    U2, S2, V2 = fb.eig_svd(A)
+    Sn = np.linalg.svd(A, compute_uv=False)[::-1]
+    for U, S, V in ((U1, S1, V1), (U2, S2, V2)):
+        assert np.max(np.abs(S - Sn) / Sn) < 1e-12
+        assert orthonormality(V) < 1e-12 and orthonormality(U) < 1e-10
+        assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-12
+    assert np.max(np.abs(S1 - S2) / S2) < 1e-13
