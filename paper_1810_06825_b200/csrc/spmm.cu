@@ -284,6 +284,67 @@ k_combine(const Combine* __restrict__ comb, const double* __restrict__ part, int
     }
 }
 
+// Even widths: the same partition and summation order as k_combine (bitwise
+// equal), with each lane owning column pairs {64 ch + 2 lane, +1} (double2)
+// and two slots' rows in flight per step, so a warp streams whole 8 l-byte
+// partial rows instead of one 256-byte column strip at a time.
+template <int NCH>
+__global__ void __launch_bounds__(kCombWarps * 32)
+k_combine2(const Combine* __restrict__ comb, const double* __restrict__ part, int ncols,
+           double* __restrict__ Y, int64_t ldy) {
+    __shared__ double2 red[kCombWarps][NCH * 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const Combine cb = comb[blockIdx.x];
+    const int ns = cb.s1 - cb.s0;
+    const int per = (ns + kCombWarps - 1) / kCombWarps;
+    const int s0 = cb.s0 + min(ns, warp * per), s1 = cb.s0 + min(ns, (warp + 1) * per);
+    bool ok[NCH];
+    double2 acc[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        ok[ch] = 64 * ch + 2 * lane < ncols;
+        acc[ch] = make_double2(0.0, 0.0);
+    }
+    const double* pl = part + 2 * lane;
+    int s = s0;
+    for (; s + 2 <= s1; s += 2) {
+        double2 a[NCH], b[NCH];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+            a[ch] = ok[ch] ? __ldcs(reinterpret_cast<const double2*>(pl + int64_t(s) * ncols + 64 * ch))
+                           : make_double2(0.0, 0.0);
+            b[ch] = ok[ch] ? __ldcs(reinterpret_cast<const double2*>(pl + int64_t(s + 1) * ncols + 64 * ch))
+                           : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+            acc[ch].x += a[ch].x; acc[ch].y += a[ch].y;
+            acc[ch].x += b[ch].x; acc[ch].y += b[ch].y;
+        }
+    }
+    if (s < s1) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+            if (ok[ch]) {
+                const double2 a = __ldcs(reinterpret_cast<const double2*>(pl + int64_t(s) * ncols + 64 * ch));
+                acc[ch].x += a.x; acc[ch].y += a.y;
+            }
+    }
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) red[warp][ch * 32 + lane] = acc[ch];
+    __syncthreads();
+    for (int e = threadIdx.x; e < NCH * 32; e += kCombWarps * 32) {
+        const int c = 64 * (e >> 5) + 2 * (e & 31);
+        if (c >= ncols) continue;
+        double2 r = red[0][e];
+        for (int w = 1; w < kCombWarps; ++w) {
+            r.x += red[w][e].x;
+            r.y += red[w][e].y;
+        }
+        *reinterpret_cast<double2*>(Y + int64_t(cb.row) * ldy + c) = r;
+    }
+}
+
 // Panel chunks of A^T*Y (PanelPlan): every item is a chunk of one hot row
 // inside one panel, summed sequentially into its partial slot. Items are taken
 // in list (= panel-major) order through a global counter, so the resident
@@ -363,6 +424,18 @@ void launch(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const
 
 void combine(Ctx& c, const ItemList& L, const double* part, int nc, double* Y, int64_t ldy) {
     if (!L.ncomb) return;
+    const char* e = std::getenv("FRPCA_COMBINE1");  // tests compare both kernels
+    if (nc % 2 == 0 && ldy % 2 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 && !(e && e[0] == '1')) {
+        const unsigned g = unsigned(L.ncomb);
+        switch ((nc + 63) / 64) {
+            case 1: k_combine2<1><<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
+            case 2: k_combine2<2><<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
+            case 3: k_combine2<3><<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
+            default: k_combine2<4><<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
+        }
+        FB_LAUNCH_CHECK();
+        return;
+    }
     k_combine<<<unsigned(L.ncomb), kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy);
     FB_LAUNCH_CHECK();
 }

@@ -397,3 +397,22 @@ def test_sytrd_fused_vs_unfused(fb, orc, monkeypatch, n):
         assert orthonormality(V) < 1e-12 and orthonormality(U) < 1e-10
         assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-12
     assert np.max(np.abs(S1 - S2) / S2) < 1e-13
+
+
+@pytest.mark.parametrize("ncols", [2, 40, 64, 150, 200, 256])
+def test_combine2_bitwise(fb, orc, panels, monkeypatch, ncols):
+    """The double2 partial combine (k_combine2) keeps k_combine's partition
+    and summation order: bitwise equal A*X (chunked long rows) and panelled
+    A^T*Y."""
+    panels()
+    oA = powerlaw_csr(orc, 3000, 2000, 120000, 21)
+    A = to_fb(fb, oA)
+    X = orc.gaussian_matrix(2000, ncols, 1)
+    Y = orc.gaussian_matrix(3000, ncols, 2)
+    monkeypatch.delenv("FRPCA_COMBINE1", raising=False)
+    r1 = (fb.spmm(A, X), fb.spmm_transpose(A, Y))
+    monkeypatch.setenv("FRPCA_COMBINE1", "1")
+    r2 = (fb.spmm(A, X), fb.spmm_transpose(A, Y))
+    for a, b in zip(r1, r2):
+        assert np.array_equal(a, b)
+    assert rel_fro(r1[1], orc.spmm_transpose(oA, Y)) <= SPMM_TOL
