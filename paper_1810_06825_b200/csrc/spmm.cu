@@ -311,10 +311,10 @@ k_combine2(const Combine* __restrict__ comb, const double* __restrict__ part, in
         double2 a[NCH], b[NCH];
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
-            a[ch] = ok[ch] ? __ldcs(reinterpret_cast<const double2*>(pl + int64_t(s) * ncols + 64 * ch))
-                           : make_double2(0.0, 0.0);
-            b[ch] = ok[ch] ? __ldcs(reinterpret_cast<const double2*>(pl + int64_t(s + 1) * ncols + 64 * ch))
-                           : make_double2(0.0, 0.0);
+            const double2* pa = reinterpret_cast<const double2*>(pl + int64_t(s) * ncols + 64 * ch);
+            const double2* pb = reinterpret_cast<const double2*>(pl + int64_t(s + 1) * ncols + 64 * ch);
+            a[ch] = ok[ch] ? __ldcs(pa) : make_double2(0.0, 0.0);
+            b[ch] = ok[ch] ? __ldcs(pb) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
@@ -326,7 +326,8 @@ k_combine2(const Combine* __restrict__ comb, const double* __restrict__ part, in
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
             if (ok[ch]) {
-                const double2 a = __ldcs(reinterpret_cast<const double2*>(pl + int64_t(s) * ncols + 64 * ch));
+                const double2* pa = reinterpret_cast<const double2*>(pl + int64_t(s) * ncols + 64 * ch);
+                const double2 a = __ldcs(pa);
                 acc[ch].x += a.x; acc[ch].y += a.y;
             }
     }
@@ -424,15 +425,22 @@ void launch(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const
 
 void combine(Ctx& c, const ItemList& L, const double* part, int nc, double* Y, int64_t ldy) {
     if (!L.ncomb) return;
-    const char* e = std::getenv("FRPCA_COMBINE1");  // tests compare both kernels
-    if (nc % 2 == 0 && ldy % 2 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 && !(e && e[0] == '1')) {
+    // k_combine2 wins when rows have few partials (C4's A^T*Y: 11 per row,
+    // 11.2 -> 6.0 ms per run) and loses with many (C1: 49 per row, 0.45 ->
+    // 0.61 ms; C3: 636, 3.7 -> 4.1 ms), so it is chosen by the mean
+    const char* e = std::getenv("FRPCA_COMBINE1");  // tests force either kernel
+    const bool few = L.nslots <= 16 * L.ncomb || (e && e[0] == '2');
+    if (nc % 2 == 0 && ldy % 2 == 0 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 && few && !(e && e[0] == '1')) {
         const unsigned g = unsigned(L.ncomb);
-        switch ((nc + 63) / 64) {
-            case 1: k_combine2<1><<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
-            case 2: k_combine2<2><<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
-            case 3: k_combine2<3><<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
-            default: k_combine2<4><<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
-        }
+        auto go = [&](auto k1, auto k2, auto k3, auto k4) {
+            switch ((nc + 63) / 64) {
+                case 1: k1<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
+                case 2: k2<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
+                case 3: k3<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
+                default: k4<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
+            }
+        };
+        go(k_combine2<1>, k_combine2<2>, k_combine2<3>, k_combine2<4>);
         FB_LAUNCH_CHECK();
         return;
     }

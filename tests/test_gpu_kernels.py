@@ -409,7 +409,7 @@ def test_combine2_bitwise(fb, orc, panels, monkeypatch, ncols):
     A = to_fb(fb, oA)
     X = orc.gaussian_matrix(2000, ncols, 1)
     Y = orc.gaussian_matrix(3000, ncols, 2)
-    monkeypatch.delenv("FRPCA_COMBINE1", raising=False)
+    monkeypatch.setenv("FRPCA_COMBINE1", "2")  # k_combine2 regardless of the partial count
     r1 = (fb.spmm(A, X), fb.spmm_transpose(A, Y))
     monkeypatch.setenv("FRPCA_COMBINE1", "1")
     r2 = (fb.spmm(A, X), fb.spmm_transpose(A, Y))
