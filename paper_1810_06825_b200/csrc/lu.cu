@@ -494,16 +494,14 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
     int32_t* posp = pos.get();
     int* errp = err.get();
     // shared-memory-resident panel when the rows fit one CTA per SM
-    const char* et = std::getenv("FRPCA_LU_SMEM_THREADS");
-    const int kTS = et && std::atoi(et) == 1024 ? 1024 : 512;
-    void* kfs = kTS == 1024 ? reinterpret_cast<void*>(k_lu_smem<1024>) : reinterpret_cast<void*>(k_lu_smem<512>);
+    constexpr int kTS = 512;
     const int R = int((m + c.num_sms - 1) / c.num_sms);
     const size_t smem_s = sizeof(double) * (size_t(NB) * R + NB * UCH + NB * (NB + 1) + NB) + sizeof(int32_t) * R;
     const bool no_smem = std::getenv("FRPCA_LU_GLOBAL") != nullptr;  // tests compare both kernels
     if (!no_smem && smem_s <= 220 * 1024) {
-        FB_CUDA(cudaFuncSetAttribute(kfs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
+        FB_CUDA(cudaFuncSetAttribute(k_lu_smem<kTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
         int per_sm = 0;
-        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfs, kTS, smem_s));
+        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu_smem<kTS>, kTS, smem_s));
         if (per_sm >= 1) {
             const int grid = int((m + R - 1) / R);
             DBuf<Cand> cand(size_t(grid), s);
@@ -517,7 +515,7 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
             int novec = std::getenv("FRPCA_LU_NOVEC") != nullptr;
             void* args[] = {&W, &m, &L, const_cast<double*>(&tol), const_cast<int*>(&R), &posp, &candp, &cvp, &errp,
                             &clkp, &novec};
-            FB_CUDA(cudaLaunchCooperativeKernel(kfs, dim3(grid), dim3(kTS), args,
+            FB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_lu_smem<kTS>), dim3(grid), dim3(kTS), args,
                                                 smem_s, s));
             count_launch();
             int h_err = 0;
