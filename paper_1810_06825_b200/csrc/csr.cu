@@ -712,12 +712,13 @@ void csr_from_triplets_device(Ctx& c, int64_t rows, int64_t cols, int64_t n, con
 
 void ensure_hint(Ctx& c, DCsr& A, int64_t w) {
     if (!A.rank_of.n || A.nhot) return;
-    // budget of L2-kept X rows; hints only when X is well beyond it
+    // budget of L2-kept X rows
     const char* e = std::getenv("FRPCA_HINT_MB");
     const double mb = e && *e ? std::atof(e) : 64.0;
     const double budget = mb * 1048576.0;
     int64_t H = 0;
-    if (budget > 0 && 8.0 * double(A.cols) * double(w) > 2.0 * budget)
+    // (at C1, X = 2.5x the budget, the hints cost 2%: only well beyond it)
+    if (budget > 0 && 8.0 * double(A.cols) * double(w) > 4.0 * budget)
         H = std::min<int64_t>(A.cols, std::max<int64_t>(1, int64_t(budget / (8.0 * double(w)))));
     if (H == A.hint_h) return;
     k_flag_hint<<<grid_for(c, A.nnz), 256, 0, c.stream>>>(A.col.get(), A.nnz, A.rank_of.get(), H);
