@@ -185,11 +185,13 @@ int frpca_ctx_destroy(frpca_ctx* c) {
         if (c->side) {
             for (auto& b : c->side->slots) b.release();
             c->side->omega_raw.release();
+            c->side->dflag.release();
             cudaStreamSynchronize(c->side->stream);
             cudaStreamDestroy(c->side->stream);
             c->side.reset();
         }
-        c->omega_raw.release();  // stream-ordered free before the stream goes
+        c->omega_raw.release();  // stream-ordered frees before the stream goes
+        c->dflag.release();
         if (c->copy) {
             cudaStreamSynchronize(c->copy);
             cudaStreamDestroy(c->copy);
@@ -324,7 +326,7 @@ int frpca_gaussian_matrix(frpca_ctx* c, int64_t rows, int64_t cols, uint64_t see
         std::lock_guard<std::mutex> lk(c->mu);
         FB_CUDA(cudaSetDevice(c->device));
         DBuf<double> d(size_t(rows * cols), c->stream);
-        gaussian_stream_device(*c, seed, rows * cols, d.get());
+        with_checks(*c, [&] { gaussian_stream_device(*c, seed, rows * cols, d.get()); });
         FB_CUDA(cudaMemcpyAsync(out, d.get(), sizeof(double) * rows * cols, cudaMemcpyDeviceToHost,
                                 c->stream));
         FB_CUDA(cudaStreamSynchronize(c->stream));
@@ -339,7 +341,7 @@ int frpca_lu_basis(frpca_ctx* c, int64_t m, int64_t l, const double* Mh, double*
         FB_CUDA(cudaSetDevice(c->device));
         DBuf<double> W(size_t(m * l), c->stream);
         upload_colmajor(*c, Mh, m, l, m, W.get());
-        lu_basis_device(*c, W.get(), m, l);
+        with_checks(*c, [&] { lu_basis_device(*c, W.get(), m, l); });
         download_colmajor(*c, W.get(), m, l, X);
     });
 }
@@ -472,7 +474,7 @@ int frpca_eig_svd(frpca_ctx* c, int64_t m, int64_t n, const double* Ah, double* 
         DBuf<double> W(size_t(m * n), c->stream), Ud(size_t(m * n), c->stream);
         upload_colmajor(*c, Ah, m, n, m, W.get());
         EigWork e;
-        e.run(*c, W.get(), m, n);
+        with_checks(*c, [&] { e.run(*c, W.get(), m, n); });
         DBuf<double> Mf(size_t(n * n), c->stream), Sd(size_t(n), c->stream);
         e.factor(*c, 0, int(n), int(n), false, true, Mf.get());
         gemm_device(*c, W.get(), m, n, Mf.get(), n, Ud.get(), n, false);
@@ -504,9 +506,7 @@ int frpca_run(frpca_ctx* c, frpca_dmat* M, int algorithm, const frpca_config* cf
                     algo == FRPCA_ALGO_BASIC_RPCAT,
                 "frpca_run: unknown algorithm");
         if (dispatched) *dispatched = algo;
-        if (algo == FRPCA_ALGO_FRPCA) run_frpca(*c, *M, a, stats);
-        else if (algo == FRPCA_ALGO_FRPCAT) run_frpcat(*c, *M, a, stats);
-        else run_basic(*c, *M, a, stats, algo == FRPCA_ALGO_BASIC_RPCAT);
+        run_algorithm(*c, *M, a, stats, algo);
     });
 }
 
@@ -554,6 +554,7 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
                 auto sd = std::make_unique<Ctx>();
                 sd->device = c->device;
                 sd->num_sms = c->num_sms;
+                sd->omega_sync = true;  // checked on its own thread (off the critical path)
                 FB_CUDA(cudaStreamCreateWithFlags(&sd->stream, cudaStreamNonBlocking));
                 c->side = std::move(sd);
             }
@@ -596,9 +597,7 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
         require(algo == FRPCA_ALGO_FRPCA || algo == FRPCA_ALGO_FRPCAT || algo == FRPCA_ALGO_BASIC_RPCA ||
                     algo == FRPCA_ALGO_BASIC_RPCAT,
                 "frpca_run: unknown algorithm");
-        if (algo == FRPCA_ALGO_FRPCA) run_frpca(*c, *M, a, stats);
-        else if (algo == FRPCA_ALGO_FRPCAT) run_frpcat(*c, *M, a, stats);
-        else run_basic(*c, *M, a, stats, algo == FRPCA_ALGO_BASIC_RPCAT);
+        run_algorithm(*c, *M, a, stats, algo);
         FB_CUDA(cudaStreamSynchronize(c->stream));
     });
 }

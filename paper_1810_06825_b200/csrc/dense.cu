@@ -793,6 +793,15 @@ void transpose_device(Ctx& c, const double* in, int64_t rows, int64_t cols, doub
     FB_LAUNCH_CHECK();
 }
 
+void maxabs_device_async(Ctx& c, const double* x, int64_t n, unsigned long long* out) {
+    FB_CUDA(cudaMemsetAsync(out, 0, 8, c.stream));
+    if (n) {
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms * 8, (n + 255) / 256)));
+        k_maxabs<<<grid, 256, 0, c.stream>>>(x, n, out);
+        FB_LAUNCH_CHECK();
+    }
+}
+
 double maxabs_device(Ctx& c, const double* x, int64_t n) {
     DBuf<unsigned long long> d(1, c.stream);
     FB_CUDA(cudaMemsetAsync(d.get(), 0, 8, c.stream));

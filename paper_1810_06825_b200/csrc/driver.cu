@@ -15,10 +15,24 @@
 namespace fb {
 namespace {
 
-using Clock = std::chrono::steady_clock;
-double since(Clock::time_point t0) {
-    return std::chrono::duration<double>(Clock::now() - t0).count();
-}
+// RunStats stage times (randsvd.hpp:42-53) from events on the run's stream,
+// so the stages need no host synchronisation between them.
+struct StageTimer {
+    cudaStream_t s;
+    cudaEvent_t ev[4] = {};
+    explicit StageTimer(cudaStream_t st) : s(st) {
+        for (auto& e : ev) FB_CUDA(cudaEventCreate(&e));
+    }
+    ~StageTimer() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+    void mark(int i) { FB_CUDA(cudaEventRecord(ev[i], s)); }
+    double seconds(int i) const {  // stage i: between marks i and i + 1 (stream complete)
+        float ms = 0.f;
+        FB_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+        return 1e-3 * double(ms);
+    }
+};
 
 // M (row-major l x ncols): column t takes eigenvector src(t) of V (column-major
 // l x l), src(t) = rev ? s + k - 1 - t : t, scaled by 1/S[src] when `scale`
@@ -38,6 +52,13 @@ __global__ void k_factor(const double* __restrict__ V, const double* __restrict_
     }
 }
 
+// rank check of eig_svd (dense_kernels.hpp:163-167) on the device: the same
+// comparison as the reference (a NaN spectrum passes it, as there)
+__global__ void k_rank_check(const double* __restrict__ D, int n, int* __restrict__ flag) {
+    const double lambda_max = D[n - 1];
+    if (lambda_max <= 0.0 || D[0] <= double(n) * DBL_EPSILON * lambda_max) atomicCAS(flag, 0, kErrEigRank);
+}
+
 __global__ void k_sing_out(const double* __restrict__ D, int s, int k, int rev, double* __restrict__ S) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < k; t += gridDim.x * blockDim.x)
         S[t] = sqrt(D[rev ? (s + k - 1 - t) : t]);
@@ -50,11 +71,10 @@ void EigWork::run(Ctx& c, const double* W, int64_t r, int64_t n) {
     D.alloc(size_t(n), c.stream);
     gram_device(c, W, r, n, B.get());
     allreduce_sum(c, B.get(), n * n);  // row-sharded W: Gram partials
-    syevd_device(c, B.get(), n, D.get(), hD);
-    // rank check (dense_kernels.hpp:163-167)
-    const double lambda_max = hD[size_t(n - 1)];
-    if (lambda_max <= 0.0 || hD[0] <= double(n) * DBL_EPSILON * lambda_max)
-        throw NumericalError("eig_svd: input does not have full numerical column rank");
+    syevd_device(c, B.get(), n, D.get());
+    // rank check (dense_kernels.hpp:163-167), reported by err_check
+    k_rank_check<<<1, 1, 0, c.stream>>>(D.get(), int(n), err_flag(c));
+    FB_LAUNCH_CHECK();
     l = n;
 }
 
@@ -223,7 +243,8 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     DBuf<double>& Q = c.slot(1, size_t(n * l));
     DBuf<double>& Z = c.slot(2, size_t(n * l));
 
-    auto t0 = Clock::now();
+    StageTimer T(S);
+    T.mark(0);
     if (q % 2 == 0) {
         // Omega (l x grows, column-major) == Omega^T row-major: this rank's rows
         // are the stream slice [offset*l, (offset+m)*l).
@@ -248,10 +269,8 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
         sketch_into(c, a, n, l, om);                      // n x l column-major
         transpose_device(c, om.get(), l, n, Q.get());     // -> row-major n x l
     }
-    FB_CUDA(cudaStreamSynchronize(S));
-    const double t_sketch = since(t0);
+    T.mark(1);
 
-    t0 = Clock::now();
     for (int64_t i = 1; i <= loops; ++i) {
         spmm_pass(c, M, false, Q.get(), l, bufM.get());   // A Q, m x l
         spmm_pass(c, M, true, bufM.get(), l, Z.get());    // A^T (A Q), n x l
@@ -263,10 +282,8 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
             std::swap(Q, Z);
         }
     }
-    FB_CUDA(cudaStreamSynchronize(S));
-    const double t_power = since(t0);
+    T.mark(2);
 
-    t0 = Clock::now();
     spmm_pass(c, M, false, Q.get(), l, bufM.get());       // W = A Q, m x l
     EigWork e;
     e.run(c, bufM.get(), m, l);
@@ -279,11 +296,12 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     output_products(c, a, l, k, {bufM.get(), m, MU.get(), Uo.get(), a.U}, {Q.get(), n, MV.get(), Vo.get(), a.V}, e,
                     int(s), So.get());
     basis_out(c, a, Q.get(), n, l);
+    T.mark(3);
     FB_CUDA(cudaStreamSynchronize(S));
     if (st) {
-        st->sketch_seconds = t_sketch;
-        st->power_seconds = t_power;
-        st->finalize_seconds = since(t0);
+        st->sketch_seconds = T.seconds(0);
+        st->power_seconds = T.seconds(1);
+        st->finalize_seconds = T.seconds(2);
         st->passes_over_matrix = M.passes.load() - passes0;
     }
 }
@@ -309,7 +327,8 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     DBuf<double>& Y = c.slot(1, size_t(m * l));
     DBuf<double>& bufN = c.slot(2, size_t(std::max<int64_t>(n, 1) * l));
 
-    auto t0 = Clock::now();
+    StageTimer T(S);
+    T.mark(0);
     if (q % 2 == 0) {
         // Omega: gcols x l column-major; this rank needs rows [offset, offset+n)
         DBuf<double>& om = c.slot(3, 0);
@@ -335,10 +354,8 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
         sketch_into(c, a, m, l, om);
         transpose_device(c, om.get(), l, m, Q.get());
     }
-    FB_CUDA(cudaStreamSynchronize(S));
-    const double t_sketch = since(t0);
+    T.mark(1);
 
-    t0 = Clock::now();
     for (int64_t i = 1; i <= loops; ++i) {
         spmm_pass(c, M, true, Q.get(), l, bufN.get());    // A^T Q, n x l
         spmm_pass(c, M, false, bufN.get(), l, Y.get());   // A (A^T Q), m x l
@@ -350,10 +367,8 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
             std::swap(Q, Y);
         }
     }
-    FB_CUDA(cudaStreamSynchronize(S));
-    const double t_power = since(t0);
+    T.mark(2);
 
-    t0 = Clock::now();
     spmm_pass(c, M, true, Q.get(), l, bufN.get());        // W = A^T Q, n x l
     EigWork e;
     e.run(c, bufN.get(), n, l);
@@ -366,11 +381,12 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     output_products(c, a, l, k, {Q.get(), m, MU.get(), Uo.get(), a.U}, {bufN.get(), n, MV.get(), Vo.get(), a.V}, e,
                     int(s), So.get());
     basis_out(c, a, Q.get(), m, l);
+    T.mark(3);
     FB_CUDA(cudaStreamSynchronize(S));
     if (st) {
-        st->sketch_seconds = t_sketch;
-        st->power_seconds = t_power;
-        st->finalize_seconds = since(t0);
+        st->sketch_seconds = T.seconds(0);
+        st->power_seconds = T.seconds(1);
+        st->finalize_seconds = T.seconds(2);
         st->passes_over_matrix = M.passes.load() - passes0;
     }
 }
@@ -398,7 +414,8 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
     DBuf<double>& bufM = c.slot(0, size_t(std::max<int64_t>(m, 1) * l));
     DBuf<double>& bufN = c.slot(1, size_t(std::max<int64_t>(n, 1) * l));
 
-    auto t0 = Clock::now();
+    StageTimer T(S);
+    T.mark(0);
     if (!left) {
         // Omega n x l column-major -> row-major; Q = orth(A Omega), m x l
         DBuf<double>& om = c.slot(3, 0);
@@ -412,10 +429,8 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
         spmm_pass(c, M, true, bufM.get(), l, bufN.get());
         orth_device(c, bufN.get(), n, l);
     }
-    FB_CUDA(cudaStreamSynchronize(S));
-    const double t_sketch = since(t0);
+    T.mark(1);
 
-    t0 = Clock::now();
     for (int64_t i = 0; i < p; ++i) {
         if (!left) {
             spmm_pass(c, M, true, bufM.get(), l, bufN.get());   // G = orth(A^T Q)
@@ -429,10 +444,8 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
             orth_device(c, bufN.get(), n, l);
         }
     }
-    FB_CUDA(cudaStreamSynchronize(S));
-    const double t_power = since(t0);
+    T.mark(2);
 
-    t0 = Clock::now();
     DBuf<double>& Uo = c.slot(4, size_t(std::max<int64_t>(m, 1) * k));
     DBuf<double>& Vo = c.slot(5, size_t(std::max<int64_t>(n, 1) * k));
     DBuf<double> So(size_t(k), S);
@@ -461,11 +474,12 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
     copy_out(c, a, a.U, Uo.get(), m * k);
     copy_out(c, a, a.V, Vo.get(), n * k);
     copy_out(c, a, a.S, So.get(), k);
+    T.mark(3);
     FB_CUDA(cudaStreamSynchronize(S));
     if (st) {
-        st->sketch_seconds = t_sketch;
-        st->power_seconds = t_power;
-        st->finalize_seconds = since(t0);
+        st->sketch_seconds = T.seconds(0);
+        st->power_seconds = T.seconds(1);
+        st->finalize_seconds = T.seconds(2);
         st->passes_over_matrix = M.passes.load() - passes0;
     }
 }
@@ -481,6 +495,46 @@ uint64_t mix_seed(uint64_t seed, uint64_t tag) {  // types.hpp:52-57
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
     return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// Deferred errors (Ctx::dflag): first failure code of the running call.
+int* err_flag(Ctx& c) {
+    if (!c.dflag.get()) {
+        c.dflag.alloc(1, c.stream);
+        FB_CUDA(cudaMemsetAsync(c.dflag.get(), 0, sizeof(int), c.stream));
+    }
+    return c.dflag.get();
+}
+
+void err_reset(Ctx& c) { FB_CUDA(cudaMemsetAsync(err_flag(c), 0, sizeof(int), c.stream)); }
+
+void err_check(Ctx& c) {
+    int h = 0;
+    FB_CUDA(cudaMemcpyAsync(&h, err_flag(c), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    FB_CUDA(cudaStreamSynchronize(c.stream));
+    if (h == 0) return;
+    FB_CUDA(cudaMemsetAsync(c.dflag.get(), 0, sizeof(int), c.stream));
+    if (h == kErrLuPivot) throw NumericalError("lu_basis: zero pivot, input is rank-deficient");  // :81
+    if (h == kErrEigRank) throw NumericalError("eig_svd: input does not have full numerical column rank");
+    if (h == kErrEigNoConv) {
+        const char* mode = std::getenv("FRPCA_EIG");
+        if (mode && std::strcmp(mode, "strict") == 0)
+            throw CudaError("syev_small: did not converge (FRPCA_EIG=strict)");
+        throw RetryCall(kErrEigNoConv);
+    }
+    if (h == kErrOmegaShort) throw RetryCall(kErrOmegaShort);
+    throw CudaError("unknown deferred error code " + std::to_string(h));
+}
+
+void run_algorithm(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, int algo) {
+    const uint64_t passes0 = M.passes.load();
+    with_checks(c, [&] {
+        M.passes.store(passes0);  // a re-run counts its passes once
+        if (algo == FRPCA_ALGO_FRPCA) run_frpca(c, M, a, st);
+        else if (algo == FRPCA_ALGO_FRPCAT) run_frpcat(c, M, a, st);
+        else run_basic(c, M, a, st, algo == FRPCA_ALGO_BASIC_RPCAT);
+    });
 }
 
 }  // namespace fb

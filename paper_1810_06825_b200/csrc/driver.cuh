@@ -17,7 +17,6 @@ struct RunArgs {
 // eig_svd pipeline state: Gram -> (allreduce) -> syevd (B becomes V) -> rank check.
 struct EigWork {
     DBuf<double> B, D;
-    std::vector<double> hD;
     int64_t l = 0;
     void run(Ctx& c, const double* W, int64_t r, int64_t n);
     void factor(Ctx& c, int s, int k, int ncols, bool rev, bool scale, double* M);
@@ -30,6 +29,35 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st);
 void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st);
 // basic_rpca (left = false) / basic_rpcat (left = true), randsvd.hpp:95-175
 void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left);
+// one of the four algorithms with the deferred-error protocol: reset, run,
+// check; a small-eigensolver non-convergence re-runs the call with cuSOLVER
+void run_algorithm(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, int algo);
+// f() under the deferred-error protocol (the standalone kernel entry points)
+template <class F>
+void with_checks(Ctx& c, F&& f) {
+    for (int attempt = 0;; ++attempt) {
+        try {
+            err_reset(c);
+            c.checked = true;
+            f();
+            c.checked = false;
+            err_check(c);
+            break;
+        } catch (const RetryCall& r) {
+            c.checked = false;
+            if (attempt >= 2) {
+                c.force_cusolver = c.omega_sync = false;
+                throw CudaError("deferred-error retry did not succeed");
+            }
+            if (r.code == kErrEigNoConv) c.force_cusolver = true;
+            else c.omega_sync = true;
+        } catch (...) {
+            c.checked = c.force_cusolver = c.omega_sync = false;
+            throw;
+        }
+    }
+    c.force_cusolver = c.omega_sync = false;
+}
 uint64_t mix_seed(uint64_t seed, uint64_t tag);
 
 // validation.cu (validation.hpp:125-282); U, S, V, Q device, column-major

@@ -90,6 +90,13 @@ struct Ctx {
     int num_sms = 148;
     std::mutex mu;  // the ABI serialises calls on one context
     cudaEvent_t timer_a = nullptr, timer_b = nullptr;
+    // Deferred errors: kernels record the first failure of a call here
+    // (atomicCAS from 0; codes kErr*), read once when the call finishes, so a
+    // run has no host round trip between its stages (err_reset / err_check).
+    DBuf<int> dflag;
+    bool force_cusolver = false;  // re-run after the small eigensolver did not converge
+    bool omega_sync = false;      // Omega batches checked on the host (re-run after a shortfall; side stream)
+    bool checked = false;         // inside with_checks: deferred errors will be read
     DBuf<uint64_t> omega_raw;  // raw-word buffer of the Omega generator, kept (grown on demand)
     std::unique_ptr<Ctx> side;  // second stream for work overlapped with the upload (frpca_run_csr)
     cudaStream_t copy = nullptr;  // device->host copies of results overlapped with the output GEMMs
@@ -171,10 +178,26 @@ void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M,
 // column-major <-> row-major conversion of an r x c matrix.
 void transpose_device(Ctx& c, const double* in, int64_t rows, int64_t cols, double* out);
 double maxabs_device(Ctx& c, const double* x, int64_t n);
+// max |x| into *out (bit pattern of a non-negative double), no host round trip
+void maxabs_device_async(Ctx& c, const double* x, int64_t n, unsigned long long* out);
+
+// ---- deferred errors (driver.cu)
+constexpr int kErrLuPivot = 1, kErrEigRank = 2, kErrEigNoConv = 3, kErrOmegaShort = 4;
+int* err_flag(Ctx& c);
+void err_reset(Ctx& c);
+// waits for the stream; throws the first recorded error (NumericalError with
+// the reference's message), or RetryCall when the call must be repeated with
+// a slower path: cuSOLVER after a small-eigensolver non-convergence, the
+// host-checked Omega loop after a (probability ~1e-15) stream shortfall
+void err_check(Ctx& c);
+struct RetryCall : std::runtime_error {
+    int code;
+    explicit RetryCall(int cd) : std::runtime_error("retry"), code(cd) {}
+};
 
 // ---- eig.cu : symmetric eigensolve of column-major n x n B (lower used):
 // V (column-major) eigenvectors, D ascending eigenvalues (device), D copied to h_D.
-void syevd_device(Ctx& c, double* B_inout_V, int64_t n, double* d_D, std::vector<double>& h_D);
+void syevd_device(Ctx& c, double* B_inout_V, int64_t n, double* d_D);
 
 // ---- csr.cu : from_triplets (sparse_matrix.hpp:62-95) on the device; host
 // outputs row_ptr (rows + 1), col_idx / values (>= nnz entries; n suffices).

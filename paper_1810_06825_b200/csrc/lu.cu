@@ -76,8 +76,9 @@ __device__ Cand block_best(Cand c, Cand* sh) {
 
 template <int kT>
 __global__ void __launch_bounds__(kT, 1)
-k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ P,
+k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restrict__ dmax, double* __restrict__ P,
      int32_t* __restrict__ pos, Cand* __restrict__ cand, int* __restrict__ err, long long* __restrict__ clk) {
+    const double tol = double(l) * DBL_EPSILON * __longlong_as_double((long long)*dmax);  // :64-65
     extern __shared__ double smem[];
     double* U12 = smem;                     // NB x l (trailing part used)
     double* L11 = U12 + NB * l;             // NB x NB
@@ -117,7 +118,7 @@ k_lu(double* __restrict__ W, int64_t m, int l, double tol, double* __restrict__ 
             const Cand best = block_best<kT>(c, shc);
             if (tim) clk[2] = clock64();
             if (!(best.v > tol) || best.row < 0) {  // zero pivot (:81)
-                if (blockIdx.x == 0 && threadIdx.x == 0) *err = 1;
+                if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(err, 0, kErrLuPivot);
                 return;  // uniform across the grid
             }
             const int32_t pr = best.row, pb = best.pos;
@@ -253,9 +254,11 @@ constexpr int UCH = 64;
 
 template <int kT>
 __global__ void __launch_bounds__(kT, 1)
-k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* __restrict__ pos_g,
+k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restrict__ dmax, int R,
+          int32_t* __restrict__ pos_g,
           Cand* __restrict__ cand, double* __restrict__ cvals, int* __restrict__ err, long long* __restrict__ clk,
           int novec) {
+    const double tol = double(l) * DBL_EPSILON * __longlong_as_double((long long)*dmax);  // :64-65
     extern __shared__ double smem[];
     double* Ps = smem;                      // NB x R (column t at Ps + t R)
     double* U12 = Ps + size_t(NB) * R;      // NB x UCH
@@ -315,7 +318,7 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, double tol, int R, int32_t* 
             }
             best = warp_best(best);
             if (!(best.v > tol) || best.row < 0) {  // zero pivot (:81)
-                if (blockIdx.x == 0 && tid == 0) *err = 1;
+                if (blockIdx.x == 0 && tid == 0) atomicCAS(err, 0, kErrLuPivot);
                 return;  // uniform across the grid
             }
             if (tim) clk[2] = clock64();
@@ -485,14 +488,14 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
     require(m < (int64_t(1) << 31), "lu_basis: rows must be < 2^31");
     Prof prof(c, "lu_basis", 16.0 * m * l, double(m) * l * l - double(l) * l * l / 3.0);
     cudaStream_t s = c.stream;
-    const double maxabs = maxabs_device(c, W, m * l);
-    const double tol = double(l) * DBL_EPSILON * maxabs;
+    // tol = l eps max|M| (:64-65) is formed in the kernels from the device max
+    DBuf<unsigned long long> dmax(1, s);
+    maxabs_device_async(c, W, m * l, dmax.get());
+    const unsigned long long* dmaxp = dmax.get();
     DBuf<int32_t> pos(size_t(m), s);
-    DBuf<int> err(1, s);
-    FB_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(int), s));
     int L = int(l);
     int32_t* posp = pos.get();
-    int* errp = err.get();
+    int* errp = err_flag(c);  // zero pivot: deferred NumericalError (err_check)
     // shared-memory-resident panel when the rows fit one CTA per SM
     constexpr int kTS = 512;
     const int R = int((m + c.num_sms - 1) / c.num_sms);
@@ -513,16 +516,14 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
             if (timing) FB_CUDA(cudaMemsetAsync(clk.get(), 0, clk.bytes(), s));
             long long* clkp = clk.get();
             int novec = std::getenv("FRPCA_LU_NOVEC") != nullptr;
-            void* args[] = {&W, &m, &L, const_cast<double*>(&tol), const_cast<int*>(&R), &posp, &candp, &cvp, &errp,
+            void* args[] = {&W, &m, &L, const_cast<unsigned long long**>(&dmaxp), const_cast<int*>(&R), &posp, &candp,
+                            &cvp, &errp,
                             &clkp, &novec};
             FB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_lu_smem<kTS>), dim3(grid), dim3(kTS), args,
                                                 smem_s, s));
             count_launch();
-            int h_err = 0;
-            FB_CUDA(cudaMemcpyAsync(&h_err, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-            FB_CUDA(cudaStreamSynchronize(s));
-            if (h_err) throw NumericalError("lu_basis: zero pivot, input is rank-deficient");
             if (timing) {
+                FB_CUDA(cudaStreamSynchronize(s));
                 long long h[24];
                 FB_CUDA(cudaMemcpy(h, clk.get(), sizeof(h), cudaMemcpyDeviceToHost));
                 std::fprintf(stderr, "lu_smem step 100 (cycles): sync %lld cand %lld u %lld rows %lld best %lld | panel end %lld\n",
@@ -557,14 +558,11 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
     static const bool timing = std::getenv("FRPCA_LU_TIMING") != nullptr;
     DBuf<long long> clk(timing ? 8 : 0, s);
     long long* clkp = clk.get();
-    void* args[] = {&W, &m, &L, const_cast<double*>(&tol), &Pp, &posp, &candp, &errp, &clkp};
+    void* args[] = {&W, &m, &L, const_cast<unsigned long long**>(&dmaxp), &Pp, &posp, &candp, &errp, &clkp};
     FB_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kT), args, smem, s));
     count_launch();
-    int h_err = 0;
-    FB_CUDA(cudaMemcpyAsync(&h_err, err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaStreamSynchronize(s));
-    if (h_err) throw NumericalError("lu_basis: zero pivot, input is rank-deficient");
     if (timing) {
+        FB_CUDA(cudaStreamSynchronize(s));
         long long h[8];
         FB_CUDA(cudaMemcpy(h, clk.get(), sizeof(long long) * 6, cudaMemcpyDeviceToHost));
         std::fprintf(stderr, "lu step 100 (cycles): sync %lld cand %lld u %lld rows %lld best %lld\n", h[1] - h[0],

@@ -25,6 +25,8 @@
 #include <mutex>
 
 #include "crlog.cuh"
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace fb {
@@ -254,6 +256,11 @@ k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restri
     }
 }
 
+// single-batch Omega: the shortfall check of the host loop, on the device
+__global__ void k_check_short(const int64_t* __restrict__ pairs, int64_t count, int* __restrict__ flag) {
+    if (2 * pairs[0] < count) atomicCAS(flag, 0, kErrOmegaShort);
+}
+
 struct PolyCache {
     std::mutex mu;
     std::map<std::pair<int, int>, uint32_t*> dev;  // (device, log2 steps) -> polys
@@ -361,6 +368,10 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         if (raw.n < need) raw.alloc(need, s);
     }
     int64_t pairs_done = 0;  // accepted attempts emitted so far
+    // one batch covers the stream (every BASELINE config): no host round trip,
+    // the shortfall test is deferred (err_check re-runs the call with
+    // omega_sync); otherwise the batches are checked on the host
+    const bool defer = c.checked && !c.omega_sync && K <= seg_per_batch;
     for (int64_t seg0 = 0; 2 * pairs_done < count; seg0 += seg_per_batch) {
         if (seg0 >= K) {
             // shortfall (probability ~ 1e-15): extend the jump table to Kmax
@@ -393,6 +404,13 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
             Prof pe(c, "omega_emit", 8.0 * nseg * J + 8.0 * count, 0.0);
             k_emit<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, off.get(), out, count, logtab);
             FB_LAUNCH_CHECK();
+        }
+        if (defer) {
+            // FRPCA_TEST_OMEGA_SHORT: tests force the shortfall -> re-run path
+            const bool force = std::getenv("FRPCA_TEST_OMEGA_SHORT") != nullptr;
+            k_check_short<<<1, 1, 0, s>>>(off.get() + nchunks, force ? INT64_MAX : count, err_flag(c));
+            FB_LAUNCH_CHECK();
+            break;
         }
         FB_CUDA(cudaMemcpyAsync(&pairs_done, off.get() + nchunks, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FB_CUDA(cudaStreamSynchronize(s));

@@ -25,7 +25,8 @@
 namespace fb {
 namespace {
 
-constexpr int kEigMax = 232;  // n(n+1)/2 doubles fit one CTA's shared memory
+constexpr int kEigMax = 232;
+const int kNoConvCode = kErrEigNoConv;  // n(n+1)/2 doubles fit one CTA's shared memory
 constexpr int kET = 1024;
 constexpr int kLeafMax = 32;
 
@@ -950,7 +951,7 @@ k_stedc(int n, const double* __restrict__ dg, const double* __restrict__ eo, dou
     }
     ok = __syncthreads_and(ok);
     if (!ok) {
-        if (tid == 0) *info = 1;
+        if (tid == 0) atomicCAS(info, 0, kErrEigNoConv);
         return;
     }
     stamp(clk, 1);
@@ -976,7 +977,7 @@ k_stedc(int n, const double* __restrict__ dg, const double* __restrict__ eo, dou
             if (grp.t == 0) atomicExch(&fail, 1);
         __syncthreads();
         if (fail) {
-            if (tid == 0) *info = 2;
+            if (tid == 0) atomicCAS(info, 0, kErrEigNoConv);
             return;
         }
         stamp(clk, 2 + level);
@@ -1090,8 +1091,8 @@ size_t stedc_smem() { return ((sizeof(MergeWs) + 15) / 16) * 16 + kLeaves * size
 // Eigenvalues ascending into d_D and eigenvectors over B (column-major), as
 // syevd. Returns false (B untouched) when n is too large or a stage did not
 // converge; the caller then uses cuSOLVER.
-bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>& h_D) {
-    if (n64 < 1 || n64 > kEigMax) return false;
+bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D) {
+    if (n64 < 1 || n64 > kEigMax || c.force_cusolver) return false;
     const int n = int(n64);
     cudaStream_t s = c.stream;
     static bool attr = false;
@@ -1110,10 +1111,11 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>
     double* Z = eo + n;
     double* Tmp = Z + nn;
     double* Ut = Tmp + nn;
-    DBuf<int> info(1, s);
+    // non-convergence of a stage: deferred (err_check -> cuSOLVER re-run);
+    // the stages after a failed one return early
+    int* info = err_flag(c);
     DBuf<unsigned char> topbuf(sizeof(TopPlan), s);
     TopPlan* top = reinterpret_cast<TopPlan*>(topbuf.get());
-    FB_CUDA(cudaMemsetAsync(info.get(), 0, sizeof(int), s));
     static const bool timing = std::getenv("FRPCA_EIG_TIMING") != nullptr;
     DBuf<long long> clk(timing ? 160 : 0, s);
     if (timing) FB_CUDA(cudaMemsetAsync(clk.get(), 0, clk.bytes(), s));
@@ -1128,20 +1130,19 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>
     }
     {
         Prof p2(c, "syev_stedc", 0, 0);
-        k_stedc<<<1, kET, stedc_smem(), s>>>(n, dg, eo, Z, Tmp, Ut, d_D, top, info.get(), clk.get());
+        k_stedc<<<1, kET, stedc_smem(), s>>>(n, dg, eo, Z, Tmp, Ut, d_D, top, info, clk.get());
         FB_LAUNCH_CHECK();
+    }
+    if (std::getenv("FRPCA_TEST_EIG_NOCONV")) {  // tests: the non-convergence -> cuSOLVER re-run path
+        FB_CUDA(cudaMemcpyAsync(info, &kNoConvCode, sizeof(int), cudaMemcpyHostToDevice, s));
     }
     {
         Prof p3(c, "syev_ormtr", 0, 0);
-        k_ormtr<<<(n + kOrmWarps - 1) / kOrmWarps, kOrmWarps * 32, 0, s>>>(H, tau, n, Z, Ut, top, B, info.get());
+        k_ormtr<<<(n + kOrmWarps - 1) / kOrmWarps, kOrmWarps * 32, 0, s>>>(H, tau, n, Z, Ut, top, B, info);
         FB_LAUNCH_CHECK();
     }
-    int h_info = 0;
-    h_D.resize(size_t(n));
-    FB_CUDA(cudaMemcpyAsync(&h_info, info.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaMemcpyAsync(h_D.data(), d_D, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaStreamSynchronize(s));
     if (timing) {
+        FB_CUDA(cudaStreamSynchronize(s));
         long long h[160];
         FB_CUDA(cudaMemcpy(h, clk.get(), sizeof(h), cudaMemcpyDeviceToHost));
         std::fprintf(stderr, "sytrd step 20: A %lld B %lld C %lld D %lld\n", h[141] - h[140], h[142] - h[141],
@@ -1154,7 +1155,7 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D, std::vector<double>
         }
         std::fprintf(stderr, "\n");
     }
-    return h_info == 0;
+    return true;
 }
 
 }  // namespace fb

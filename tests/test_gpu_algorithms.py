@@ -207,3 +207,55 @@ def test_run_csr_errors(fb, orc):
         fb.run_csr(A, fb.PcaConfig(k=3, oversample=2, passes=4), fb.PcaAlgorithm.Frpca)
     with pytest.raises(fb.NumericalError):
         fb.run_csr(fb.SparseMatrixCsr.from_triplets(6, 6, []), fb.PcaConfig(k=2, oversample=1, passes=4))
+
+
+# ---- deferred errors (Ctx::dflag): retries and messages --------------------
+
+def test_eig_noconv_retry_with_cusolver(fb, orc, monkeypatch):
+    """A small-eigensolver non-convergence is recorded on the device and read
+    once at the end of the call, which then re-runs with cuSOLVER: same
+    answer as FRPCA_EIG=cusolver; FRPCA_EIG=strict turns it into an error."""
+    oA = powerlaw_csr(orc, 3000, 800, 60000, 3)
+    A = to_fb(fb, oA)
+    c = cfg(fb, 20, 20, 4)
+    monkeypatch.setenv("FRPCA_EIG", "cusolver")
+    ref = fb.frpcat(A, c)
+    monkeypatch.delenv("FRPCA_EIG")
+    monkeypatch.setenv("FRPCA_TEST_EIG_NOCONV", "1")
+    st = fb.RunStats()
+    r = fb.frpcat(A, c, st)
+    assert np.array_equal(r.S, ref.S) and np.array_equal(r.U, ref.U) and np.array_equal(r.V, ref.V)
+    assert st.passes_over_matrix == 4
+    monkeypatch.setenv("FRPCA_EIG", "strict")
+    with pytest.raises(Exception, match="did not converge"):
+        fb.frpcat(A, c)
+
+
+def test_omega_shortfall_retry(fb, orc, monkeypatch):
+    """The single-batch Omega defers its shortfall test to the end of the
+    call; a shortfall re-runs the call with the host-checked batch loop."""
+    oA = orc.Csr.random_sparse(600, 300, 0.05, 1234)
+    A = to_fb(fb, oA)
+    for q in (3, 4):
+        ref = fb.frpcat(A, cfg(fb, 10, 10, q, seed=3))
+        monkeypatch.setenv("FRPCA_TEST_OMEGA_SHORT", "1")
+        r = fb.frpcat(A, cfg(fb, 10, 10, q, seed=3))
+        monkeypatch.delenv("FRPCA_TEST_OMEGA_SHORT")
+        assert np.array_equal(r.S, ref.S) and np.array_equal(r.U, ref.U)
+    g0 = fb.gaussian_matrix(5000, 7, 9)
+    monkeypatch.setenv("FRPCA_TEST_OMEGA_SHORT", "1")
+    assert np.array_equal(fb.gaussian_matrix(5000, 7, 9), g0)
+
+
+def test_deferred_error_then_clean_call(fb, orc):
+    """A failed call (zero pivot / rank deficiency, reported at its end) leaves
+    no state behind: the next call on the same context succeeds."""
+    Z = fb.SparseMatrixCsr.from_triplets(50, 20, [])
+    with pytest.raises(fb.NumericalError):
+        fb.frpcat(Z, cfg(fb, 3, 2, 4))
+    with pytest.raises(fb.NumericalError):
+        fb.frpcat(Z, cfg(fb, 3, 2, 3))
+    oA = orc.Csr.random_sparse(600, 300, 0.05, 1234)
+    r = fb.frpcat(to_fb(fb, oA), cfg(fb, 10, 10, 4, seed=3))
+    o = orc.pca(oA, orc.FRPCAT, 10, 10, 4, seed=3)
+    assert_parity(r, o)
