@@ -74,17 +74,17 @@ __device__ Cand block_best(Cand c, Cand* sh) {
     return r;
 }
 
-template <int kT>
+template <int kT, int NBK>
 __global__ void __launch_bounds__(kT, 1)
 k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restrict__ dmax, double* __restrict__ P,
      int32_t* __restrict__ pos, Cand* __restrict__ cand, int* __restrict__ err, long long* __restrict__ clk) {
     const double tol = double(l) * DBL_EPSILON * __longlong_as_double((long long)*dmax);  // :64-65
     extern __shared__ double smem[];
-    double* U12 = smem;                     // NB x l (trailing part used)
-    double* L11 = U12 + NB * l;             // NB x NB
-    double* u = L11 + NB * (NB + 1);        // NB
+    double* U12 = smem;                     // NBK x l (trailing part used)
+    double* L11 = U12 + NBK * l;             // NBK x NBK
+    double* u = L11 + NBK * (NBK + 1);        // NBK
     __shared__ Cand shc[kT / 32];
-    __shared__ int32_t prow[NB];
+    __shared__ int32_t prow[NBK];
     cg::grid_group grid = cg::this_grid();
     const int64_t gtid = int64_t(blockIdx.x) * kT + threadIdx.x;
     const int64_t nthr = int64_t(gridDim.x) * kT;
@@ -92,7 +92,7 @@ k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restr
 
     // prologue: positions, panel 0, candidates of column 0
     {
-        const int bw = min(NB, l);
+        const int bw = min(NBK, l);
         Cand c{-1.0, INT32_MAX, -1};
         for (int64_t i = gtid; i < m; i += nthr) {
             pos[i] = int32_t(i);
@@ -104,8 +104,8 @@ k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restr
         if (threadIdx.x == 0) cand[blockIdx.x] = c;
     }
 
-    for (int jb = 0; jb < l; jb += NB) {
-        const int bw = min(NB, l - jb);
+    for (int jb = 0; jb < l; jb += NBK) {
+        const int bw = min(NBK, l - jb);
         for (int jj = 0; jj < bw; ++jj) {
             const int j = jb + jj;
             const bool tim = clk && j == 100 && blockIdx.x == 0 && threadIdx.x == 0;
@@ -132,9 +132,9 @@ k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restr
                 // all loads of the row first (position + remaining panel
                 // entries are independent), so a row costs one round trip
                 int32_t p = pos[i];
-                double v[NB];
+                double v[NBK];
 #pragma unroll
-                for (int t = 0; t < NB; ++t)
+                for (int t = 0; t < NBK; ++t)
                     if (t >= jj && t < bw) v[t] = P[int64_t(t) * m + i];
                 if (i == pr) {
                     pos[i] = j;
@@ -147,13 +147,13 @@ k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restr
                 if (p > j) {
                     double mi = 0.0, nv = 0.0;
 #pragma unroll
-                    for (int t = 0; t < NB; ++t)
+                    for (int t = 0; t < NBK; ++t)
                         if (t == jj) {
                             mi = v[t] / d;                             // :88
                             P[int64_t(t) * m + i] = mi;
                         }
 #pragma unroll
-                    for (int t = 0; t < NB; ++t)                      // :89-92
+                    for (int t = 0; t < NBK; ++t)                      // :89-92
                         if (t > jj && t < bw) {
                             v[t] = v[t] - mi * u[t];
                             P[int64_t(t) * m + i] = v[t];
@@ -175,7 +175,7 @@ k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restr
             // L11 (unit lower) of the bw pivot rows and A12 = their trailing columns
             for (int e = threadIdx.x; e < bw * bw; e += kT) {
                 const int t = e / bw, s = e % bw;
-                L11[t * (NB + 1) + s] = P[int64_t(s) * m + prow[t]];
+                L11[t * (NBK + 1) + s] = P[int64_t(s) * m + prow[t]];
             }
             for (int e = threadIdx.x; e < bw * tcols; e += kT) {
                 const int t = e / tcols, cc = e % tcols;
@@ -186,22 +186,22 @@ k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restr
             for (int cc = threadIdx.x; cc < tcols; cc += kT)
                 for (int t = 1; t < bw; ++t) {
                     double acc = U12[t * tcols + cc];
-                    for (int s = 0; s < t; ++s) acc -= L11[t * (NB + 1) + s] * U12[s * tcols + cc];
+                    for (int s = 0; s < t; ++s) acc -= L11[t * (NBK + 1) + s] * U12[s * tcols + cc];
                     U12[t * tcols + cc] = acc;
                 }
             __syncthreads();
         }
         // own rows: write the finished panel back to W, trailing update
         // A22 -= L21 U12 (:101-104), stage the next panel, candidates.
-        const int nbw = min(NB, tcols);
+        const int nbw = min(NBK, tcols);
         Cand nc{-1.0, INT32_MAX, -1};
         for (int64_t i = gtid; i < m; i += nthr) {
             const int32_t p = pos[i];
             if (p < jb) continue;  // pivot of an earlier panel: finished
             double* wr = W + i * l;
-            double Lr[NB];
+            double Lr[NBK];
 #pragma unroll
-            for (int t = 0; t < NB; ++t) {
+            for (int t = 0; t < NBK; ++t) {
                 if (t < bw) {
                     Lr[t] = P[int64_t(t) * m + i];
                     wr[jb + t] = Lr[t];
@@ -217,7 +217,7 @@ k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restr
                     for (int e = 0; e < 8; ++e)
                         if (cb + e < tcols) a[e] = wr[c0 + cb + e];
 #pragma unroll
-                    for (int t = 0; t < NB; ++t)
+                    for (int t = 0; t < NBK; ++t)
                         if (t < bw) {
 #pragma unroll
                             for (int e = 0; e < 8; ++e)
@@ -539,12 +539,23 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
             return;
         }
     }
-    const size_t smem = sizeof(double) * (size_t(NB) * size_t(l) + NB * (NB + 1) + NB);
+    // Panel width of the global-panel kernel: the column-major panel copy P is
+    // re-read and rewritten every column step; at 16 columns it is half the
+    // traffic and stays L2-resident (C2 LU 9.1 -> 7.45 ms, C4 6.4 -> 6.2 ms). The width does not change the
+    // arithmetic: every element receives the same FMAs in the same order
+    // (in-panel rank-1 updates == TRSM + trailing update, both in pivot
+    // order), checked bitwise against the shared-memory kernel (NB = 32).
+    const char* enb = std::getenv("FRPCA_LU_NB");
+    const int nbk = enb ? std::atoi(enb) : 16;
+    require(nbk == 8 || nbk == 16 || nbk == 32, "FRPCA_LU_NB must be 8, 16 or 32");
+    const size_t smem = sizeof(double) * (size_t(nbk) * size_t(l) + nbk * (nbk + 1) + nbk);
     static const int kT = [] {
         const char* e = std::getenv("FRPCA_LU_THREADS");
         return e && std::atoi(e) == 512 ? 512 : 256;
     }();
-    void* kfn = kT == 256 ? reinterpret_cast<void*>(k_lu<256>) : reinterpret_cast<void*>(k_lu<512>);
+    void* kfn = nbk == 8 ? (kT == 256 ? reinterpret_cast<void*>(k_lu<256, 8>) : reinterpret_cast<void*>(k_lu<512, 8>))
+              : nbk == 16 ? (kT == 256 ? reinterpret_cast<void*>(k_lu<256, 16>) : reinterpret_cast<void*>(k_lu<512, 16>))
+                          : (kT == 256 ? reinterpret_cast<void*>(k_lu<256, 32>) : reinterpret_cast<void*>(k_lu<512, 32>));
     FB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(std::max<size_t>(smem, 48 * 1024))));
     int per_sm = 0;
@@ -552,7 +563,7 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
     require(per_sm >= 1, "lu_basis: panel width too large for one CTA's shared memory");
     int grid = std::max(1, std::min<int>(per_sm * c.num_sms, int((m + kT - 1) / kT)));
     DBuf<Cand> cand(size_t(grid), s);
-    DBuf<double> P(size_t(m) * NB, s);
+    DBuf<double> P(size_t(m) * nbk, s);
     double* Pp = P.get();
     Cand* candp = cand.get();
     static const bool timing = std::getenv("FRPCA_LU_TIMING") != nullptr;
