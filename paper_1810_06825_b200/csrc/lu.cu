@@ -252,7 +252,7 @@ k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restr
 // can overwrite the panel). Same arithmetic, in the same order, as k_lu.
 constexpr int UCH = 64;
 
-template <int kT>
+template <int kT, int NBK>
 __global__ void __launch_bounds__(kT, 1)
 k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restrict__ dmax, int R,
           int32_t* __restrict__ pos_g,
@@ -260,13 +260,13 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
           int novec) {
     const double tol = double(l) * DBL_EPSILON * __longlong_as_double((long long)*dmax);  // :64-65
     extern __shared__ double smem[];
-    double* Ps = smem;                      // NB x R (column t at Ps + t R)
-    double* U12 = Ps + size_t(NB) * R;      // NB x UCH
-    double* L11 = U12 + NB * UCH;           // NB x (NB + 1)
-    double* u = L11 + NB * (NB + 1);        // NB
-    int32_t* posS = reinterpret_cast<int32_t*>(u + NB);  // R
+    double* Ps = smem;                      // NBK x R (column t at Ps + t R)
+    double* U12 = Ps + size_t(NBK) * R;      // NBK x UCH
+    double* L11 = U12 + NBK * UCH;           // NBK x (NBK + 1)
+    double* u = L11 + NBK * (NBK + 1);        // NBK
+    int32_t* posS = reinterpret_cast<int32_t*>(u + NBK);  // R
     __shared__ Cand shc[kT / 32];
-    __shared__ int32_t prow[NB];
+    __shared__ int32_t prow[NBK];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x;
     const int64_t r0 = int64_t(blockIdx.x) * R;
@@ -275,10 +275,10 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
 
     auto publish = [&](Cand c, int width) {  // after a block_best (Ps final)
         if (tid == 0) cand[blockIdx.x] = c;
-        if (tid < width) cvals[size_t(blockIdx.x) * NB + tid] = c.row >= 0 ? Ps[size_t(tid) * R + (c.row - r0)] : 0.0;
+        if (tid < width) cvals[size_t(blockIdx.x) * NBK + tid] = c.row >= 0 ? Ps[size_t(tid) * R + (c.row - r0)] : 0.0;
     };
     {
-        const int bw = min(NB, l);
+        const int bw = min(NBK, l);
         Cand c{-1.0, INT32_MAX, -1};
         for (int r = tid; r < nr; r += kT) {
             const int64_t i = r0 + r;
@@ -290,8 +290,8 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
         c = block_best<kT>(c, shc);
         publish(c, bw);
     }
-    for (int jb = 0; jb < l; jb += NB) {
-        const int bw = min(NB, l - jb);
+    for (int jb = 0; jb < l; jb += NBK) {
+        const int bw = min(NBK, l - jb);
         for (int jj = 0; jj < bw; ++jj) {
             const int j = jb + jj;
             const bool tim = clk && j == 100 && blockIdx.x == 0 && tid == 0;
@@ -323,7 +323,7 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
             }
             if (tim) clk[2] = clock64();
             const int32_t pr = best.row, pb = best.pos;
-            if (tid < bw) u[tid] = cvals[size_t(pr / R) * NB + tid];
+            if (tid < bw) u[tid] = cvals[size_t(pr / R) * NBK + tid];
             if (tid == 0) prow[jj] = pr;
             __syncthreads();
             if (tim) clk[3] = clock64();
@@ -378,12 +378,12 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
         if (tcols <= 0) break;
         for (int e = tid; e < bw * bw; e += kT) {
             const int t = e / bw, s2 = e % bw;
-            L11[t * (NB + 1) + s2] = W[int64_t(prow[t]) * l + jb + s2];
+            L11[t * (NBK + 1) + s2] = W[int64_t(prow[t]) * l + jb + s2];
         }
-        const int nbw = min(NB, tcols);
+        const int nbw = min(NBK, tcols);
         const int nch = (tcols + UCH - 1) / UCH;
         // nbw is a multiple of 8 whenever the vector path writes Ps (cc0 + cb < nbw)
-        const bool vec = !novec && bw == NB && (l % 2) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
+        const bool vec = !novec && bw == NBK && (l % 2) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
                          (nbw % 8) == 0;
         Cand nc{-1.0, INT32_MAX, -1};
         for (int ch = nch - 1; ch >= 0; --ch) {
@@ -398,7 +398,7 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
             for (int cc = tid; cc < cw; cc += kT)  // U12 = L11^{-1} A12, column by column
                 for (int t = 1; t < bw; ++t) {
                     double acc = U12[t * UCH + cc];
-                    for (int s2 = 0; s2 < t; ++s2) acc -= L11[t * (NB + 1) + s2] * U12[s2 * UCH + cc];
+                    for (int s2 = 0; s2 < t; ++s2) acc -= L11[t * (NBK + 1) + s2] * U12[s2 * UCH + cc];
                     U12[t * UCH + cc] = acc;
                 }
             __syncthreads();
@@ -407,9 +407,9 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
                 const int32_t p = posS[r];
                 if (p < c0) continue;  // pivot of this or an earlier panel
                 double* wr = W + (r0 + r) * l;
-                double Lr[NB];
+                double Lr[NBK];
 #pragma unroll
-                for (int t = 0; t < NB; ++t)
+                for (int t = 0; t < NBK; ++t)
                     if (t < bw) Lr[t] = Ps[size_t(t) * R + r];
                 for (int cb = 0; cb < cw; cb += 8) {
                     if (vec && cb + 8 <= cw) {
@@ -420,7 +420,7 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
 #pragma unroll
                         for (int e = 0; e < 4; ++e) a2[e] = w2[e];
 #pragma unroll
-                        for (int t = 0; t < NB; ++t) {
+                        for (int t = 0; t < NBK; ++t) {
                             const double2* u2 = reinterpret_cast<const double2*>(U12 + t * UCH + cb);
                             const double lt = -Lr[t];
 #pragma unroll
@@ -445,7 +445,7 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
                     for (int e = 0; e < 8; ++e)
                         if (cb + e < cw) a[e] = wr[c0 + cc0 + cb + e];
 #pragma unroll
-                    for (int t = 0; t < NB; ++t)
+                    for (int t = 0; t < NBK; ++t)
                         if (t < bw) {
 #pragma unroll
                             for (int e = 0; e < 8; ++e)
@@ -496,19 +496,28 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
     int L = int(l);
     int32_t* posp = pos.get();
     int* errp = err_flag(c);  // zero pivot: deferred NumericalError (err_check)
-    // shared-memory-resident panel when the rows fit one CTA per SM
+    // shared-memory-resident panel when the rows fit one CTA per SM, 16
+    // columns wide (rows up to ~214k: C1 and C4; C1 1.98 -> 1.94 ms at 16 vs
+    // 32, C4 6.2 -> 3.4 ms against the global kernel); the width does not
+    // change the arithmetic (see the global kernel below)
     constexpr int kTS = 512;
     const int R = int((m + c.num_sms - 1) / c.num_sms);
-    const size_t smem_s = sizeof(double) * (size_t(NB) * R + NB * UCH + NB * (NB + 1) + NB) + sizeof(int32_t) * R;
+    auto smem_for = [&](int nb) {
+        return sizeof(double) * (size_t(nb) * R + nb * UCH + nb * (nb + 1) + nb) + sizeof(int32_t) * R;
+    };
+    const char* esb = std::getenv("FRPCA_LU_SMEM_NB");
+    const int snb = esb ? std::atoi(esb) : 16;
+    const size_t smem_s = smem_for(snb);
+    void* kfs = snb == 16 ? reinterpret_cast<void*>(k_lu_smem<kTS, 16>) : reinterpret_cast<void*>(k_lu_smem<kTS, 32>);
     const bool no_smem = std::getenv("FRPCA_LU_GLOBAL") != nullptr;  // tests compare both kernels
-    if (!no_smem && smem_s <= 220 * 1024) {
-        FB_CUDA(cudaFuncSetAttribute(k_lu_smem<kTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
+    if (!no_smem && (snb == 16 || snb == 32) && smem_s <= 220 * 1024) {
+        FB_CUDA(cudaFuncSetAttribute(kfs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_s)));
         int per_sm = 0;
-        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu_smem<kTS>, kTS, smem_s));
+        FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfs, kTS, smem_s));
         if (per_sm >= 1) {
             const int grid = int((m + R - 1) / R);
             DBuf<Cand> cand(size_t(grid), s);
-            DBuf<double> cvals(size_t(grid) * NB, s);
+            DBuf<double> cvals(size_t(grid) * snb, s);
             Cand* candp = cand.get();
             double* cvp = cvals.get();
             const bool timing = std::getenv("FRPCA_LU_TIMING") != nullptr;
@@ -519,7 +528,7 @@ void lu_basis_device(Ctx& c, double* W, int64_t m, int64_t l) {
             void* args[] = {&W, &m, &L, const_cast<unsigned long long**>(&dmaxp), const_cast<int*>(&R), &posp, &candp,
                             &cvp, &errp,
                             &clkp, &novec};
-            FB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_lu_smem<kTS>), dim3(grid), dim3(kTS), args,
+            FB_CUDA(cudaLaunchCooperativeKernel(kfs, dim3(grid), dim3(kTS), args,
                                                 smem_s, s));
             count_launch();
             if (timing) {

@@ -418,7 +418,8 @@ def test_combine2_bitwise(fb, orc, panels, monkeypatch, ncols):
     assert rel_fro(r1[1], orc.spmm_transpose(oA, Y)) <= SPMM_TOL
 
 
-@pytest.mark.parametrize("m,l", [(1000, 33), (40000, 200), (100000, 200), (130000, 150), (500000, 150)])
+@pytest.mark.parametrize("m,l", [(1000, 33), (40000, 200), (100000, 200), (130000, 150), (200000, 200),
+                                 (500000, 150)])
 def test_lu_panel_width_bitwise(fb, orc, monkeypatch, m, l):
     """The global-panel LU at panel width 16 (used above ~262k rows to keep
     the panel copy L2-resident) and 32, and the shared-memory kernel (32):
@@ -429,13 +430,18 @@ def test_lu_panel_width_bitwise(fb, orc, monkeypatch, m, l):
     M *= 10.0 ** rng.uniform(-6, 6, size=(m, 1))
     M[rng.choice(m, m // 7, replace=False)] = 0.0
     out = []
-    for glob, nb in ((False, None), (True, "32"), (True, "16"), (True, "8")):
+    for glob, nb, snb in ((False, None, None), (False, None, "32"), (True, "32", None), (True, "16", None),
+                          (True, "8", None)):
         if glob:
             monkeypatch.setenv("FRPCA_LU_GLOBAL", "1")
         else:
             monkeypatch.delenv("FRPCA_LU_GLOBAL", raising=False)
         if nb:
             monkeypatch.setenv("FRPCA_LU_NB", nb)
+        if snb:
+            monkeypatch.setenv("FRPCA_LU_SMEM_NB", snb)
+        else:
+            monkeypatch.delenv("FRPCA_LU_SMEM_NB", raising=False)
         out.append(fb.lu_basis(M))
     for o in out[1:]:
         assert np.array_equal(out[0], o)
