@@ -26,6 +26,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
     const int n = valid ? 8 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -263,10 +268,10 @@ __global__ void k_gram2_reduce(const double* __restrict__ part, int nparts, int 
 constexpr int G3_BT = 5;
 constexpr int G3_ROWS = 32;
 
-template <int NBR>
+template <int NBR, int ROWS>
 __global__ void __launch_bounds__(NBR * (NBR + 1) / 2 * 32, 1)
 k_gram3(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_cta, double* __restrict__ part) {
-    extern __shared__ __align__(16) double sm[];  // [2][G3_ROWS][S], S >= 40 NBR
+    extern __shared__ __align__(16) double sm[];  // [2][ROWS][S], S >= 40 NBR
     constexpr int NW = NBR * (NBR + 1) / 2;
     const int T = (n + 7) / 8;
     const int NT = T * (T + 1) / 2;
@@ -284,9 +289,9 @@ k_gram3(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
 #pragma unroll
         for (int b = 0; b < G3_BT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     auto load = [&](int stage, int64_t k0) {
-        double* dst = sm + size_t(stage) * G3_ROWS * S;
+        double* dst = sm + size_t(stage) * ROWS * S;
         const int per_row = n / 2;  // n even (caller)
-        for (int e = tid; e < G3_ROWS * per_row; e += NW * 32) {
+        for (int e = tid; e < ROWS * per_row; e += NW * 32) {
             const int kr = e / per_row, cc = (e % per_row) * 2;
             const int64_t row = k0 + kr;
             const bool v = row < re;
@@ -294,28 +299,28 @@ k_gram3(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
                          "l"(W + (v ? row * n + cc : 0)), "r"(v ? 16 : 0));
         }
-        for (int e = tid; e < G3_ROWS * (ncol - n); e += NW * 32) {
+        for (int e = tid; e < ROWS * (ncol - n); e += NW * 32) {
             const int kr = e / (ncol - n), cc = n + e % (ncol - n);
             dst[kr * S + cc] = 0.0;
         }
         cp_async_commit();
     };
-    const int64_t nsteps = (re - rs + G3_ROWS - 1) / G3_ROWS;
+    const int64_t nsteps = (re - rs + ROWS - 1) / ROWS;
     if (nsteps > 0) load(0, rs);
     const int coff = (lane & 3) * S + (lane >> 2);
     for (int64_t st = 0; st < nsteps; ++st) {
         const int stage = int(st & 1);
         if (st + 1 < nsteps) {
-            load(stage ^ 1, rs + (st + 1) * G3_ROWS);
+            load(stage ^ 1, rs + (st + 1) * ROWS);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
-        const double* Ws = sm + size_t(stage) * G3_ROWS * S + coff;
+        const double* Ws = sm + size_t(stage) * ROWS * S + coff;
         if (diag) {
 #pragma unroll
-            for (int kk = 0; kk < G3_ROWS / 4; ++kk) {
+            for (int kk = 0; kk < ROWS / 4; ++kk) {
                 const double* rowp = Ws + kk * 4 * S + bi * 40;
                 double f[G3_BT];
 #pragma unroll
@@ -327,7 +332,7 @@ k_gram3(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
             }
         } else {
 #pragma unroll
-            for (int kk = 0; kk < G3_ROWS / 4; ++kk) {
+            for (int kk = 0; kk < ROWS / 4; ++kk) {
                 const double* rowp = Ws + kk * 4 * S;
                 double fa[G3_BT];
 #pragma unroll
@@ -355,27 +360,38 @@ k_gram3(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
         }
 }
 
-template <int NBR>
-void launch_gram3(Ctx& c, const double* W, int64_t r, int n, double* B) {
+template <int NBR, int ROWS>
+void launch_gram3_rows(Ctx& c, const double* W, int64_t r, int n, double* B) {
     constexpr int NW = NBR * (NBR + 1) / 2;
     const int T = (n + 7) / 8, NT = T * (T + 1) / 2;
     const int ncol = 8 * G3_BT * NBR;
     const int S = ncol + ((12 - (ncol % 16)) + 16) % 16;
-    const size_t smem = sizeof(double) * 2 * G3_ROWS * S;
+    const size_t smem = sizeof(double) * 2 * ROWS * S;
     static bool attr = false;
     if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_gram3<NBR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        FB_CUDA(cudaFuncSetAttribute(k_gram3<NBR, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         attr = true;
     }
+    // the row split over CTAs stays at 32-row granularity whatever the staging
+    // depth, so the split-K partials (and the result) do not depend on ROWS
     int64_t nctas = std::min<int64_t>(c.num_sms, std::max<int64_t>(1, (r + G3_ROWS - 1) / G3_ROWS));
     const int64_t rpc = ((r + nctas - 1) / nctas + G3_ROWS - 1) / G3_ROWS * G3_ROWS;
     nctas = std::max<int64_t>(1, (r + rpc - 1) / rpc);
     DBuf<double> part(size_t(nctas) * NT * 64, c.stream);
-    k_gram3<NBR><<<unsigned(nctas), NW * 32, smem, c.stream>>>(W, r, n, S, rpc, part.get());
+    k_gram3<NBR, ROWS><<<unsigned(nctas), NW * 32, smem, c.stream>>>(W, r, n, S, rpc, part.get());
     FB_LAUNCH_CHECK();
     const int outs = NT * 64;
     k_gram2_reduce<<<(outs + 255) / 256, 256, 0, c.stream>>>(part.get(), int(nctas), n, B);
     FB_LAUNCH_CHECK();
+}
+
+template <int NBR>
+void launch_gram3(Ctx& c, const double* W, int64_t r, int n, double* B) {
+    // staging depth (does not change the result): 64 rows per stage halves the
+    // block barriers (C1 1.77 -> 1.74 ms, C3 22.4 -> 21.2 ms)
+    const char* e = std::getenv("FRPCA_GRAM_ROWS");
+    if (e && std::atoi(e) == 32) return launch_gram3_rows<NBR, 32>(c, W, r, n, B);
+    launch_gram3_rows<NBR, 64>(c, W, r, n, B);
 }
 
 template <int MAXT>
@@ -598,18 +614,34 @@ k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __r
     }
     cp_async_commit();
     const int nsteps = (K + TK - 1) / TK;
+    // 16-byte staging when the rows of W are 16-byte aligned
+    const bool even = (K & 1) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0;
     auto load = [&](int stage, int64_t r0, int k0) {
         double* wd = Ws + stage * BM * TSA;
-        for (int e = tid; e < BM * TK; e += GP_THREADS) {
-            const int rr = e / TK, kk = e % TK;
-            const int64_t row = r0 + rr;
-            const int k = k0 + kk;
-            const bool v = row < r && k < K;
-            cp_async8(wd + rr * TSA + kk, W + (v ? row * K + k : 0), v);
+        if (even) {
+            for (int e = tid; e < BM * (TK / 2); e += GP_THREADS) {
+                const int rr = e / (TK / 2), c2 = e % (TK / 2);
+                const int64_t row = r0 + rr;
+                const int k = k0 + 2 * c2;
+                const bool v = row < r && k < K;
+                cp_async16(wd + rr * TSA + 2 * c2, W + (v ? row * K + k : 0), v);
+            }
+        } else {
+            for (int e = tid; e < BM * TK; e += GP_THREADS) {
+                const int rr = e / TK, kk = e % TK;
+                const int64_t row = r0 + rr;
+                const int k = k0 + kk;
+                const bool v = row < r && k < K;
+                cp_async8(wd + rr * TSA + kk, W + (v ? row * K + k : 0), v);
+            }
         }
         cp_async_commit();
     };
+    // one continuous two-stage pipeline over (row block, k stage): the last
+    // stage of a block prefetches the first stage of the CTA's next block
     const int64_t nblocks = (r + BM - 1) / BM;
+    if (int64_t(blockIdx.x) < nblocks) load(0, int64_t(blockIdx.x) * BM, 0);
+    int stage = 0;
     for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
         const int64_t r0 = blk * BM;
         double acc[RT][NT][2];
@@ -617,11 +649,13 @@ k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __r
         for (int a = 0; a < RT; ++a)
 #pragma unroll
             for (int t = 0; t < NT; ++t) acc[a][t][0] = acc[a][t][1] = 0.0;
-        load(0, r0, 0);
         for (int st = 0; st < nsteps; ++st) {
-            const int stage = st & 1;
+            const int64_t nb = blk + gridDim.x;
             if (st + 1 < nsteps) {
                 load(stage ^ 1, r0, (st + 1) * TK);
+                cp_async_wait<1>();
+            } else if (nb < nblocks) {
+                load(stage ^ 1, nb * BM, 0);
                 cp_async_wait<1>();
             } else {
                 cp_async_wait<0>();
@@ -645,6 +679,7 @@ k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __r
                 }
             }
             __syncthreads();
+            stage ^= 1;
         }
 #pragma unroll
         for (int a = 0; a < RT; ++a)

@@ -445,3 +445,16 @@ def test_lu_panel_width_bitwise(fb, orc, monkeypatch, m, l):
         out.append(fb.lu_basis(M))
     for o in out[1:]:
         assert np.array_equal(out[0], o)
+
+
+@pytest.mark.parametrize("m,n", [(5000, 200), (100000, 200), (20000, 150), (4130, 96)])
+def test_gram_staging_depth_bitwise(fb, orc, monkeypatch, m, n):
+    """k_gram3 with 32- or 64-row stages: the CTA row split is fixed at 32-row
+    granularity, so the partials and the result are bitwise equal."""
+    A = orc.gaussian_matrix(m, n, 3 * m + n)
+    monkeypatch.setenv("FRPCA_GRAM_ROWS", "32")
+    r1 = fb.eig_svd(A)
+    monkeypatch.setenv("FRPCA_GRAM_ROWS", "64")
+    r2 = fb.eig_svd(A)
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
