@@ -192,9 +192,16 @@ int frpca_ctx_destroy(frpca_ctx* c) {
         }
         c->omega_raw.release();  // stream-ordered frees before the stream goes
         c->dflag.release();
+        c->wcount.release();
         if (c->copy) {
             cudaStreamSynchronize(c->copy);
             cudaStreamDestroy(c->copy);
+        }
+        if (c->aux) {
+            cudaStreamSynchronize(c->aux);
+            cudaStreamDestroy(c->aux);
+            cudaEventDestroy(c->ev_fork);
+            cudaEventDestroy(c->ev_join);
         }
         if (c->stream) {
             cudaStreamSynchronize(c->stream);

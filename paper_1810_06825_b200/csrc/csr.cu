@@ -196,7 +196,9 @@ namespace {
 
 // chunk size of the work lists: ~16 items per resident warp, clamped
 int64_t default_chunk(const Ctx& c, const DCsr& A) {
-    const int64_t target = int64_t(c.num_sms) * 24 * 16;
+    const char* e = std::getenv("FRPCA_CHUNK_ITEMS");  // items per warp (A/B knob)
+    const int64_t per = e && *e ? std::max(1, std::atoi(e)) : 16;
+    const int64_t target = int64_t(c.num_sms) * 24 * per;
     const int64_t ch = (A.nnz + A.rows + target - 1) / target;
     return std::max<int64_t>(256, std::min<int64_t>(16384, ch));
 }

@@ -100,6 +100,10 @@ struct Ctx {
     DBuf<uint64_t> omega_raw;  // raw-word buffer of the Omega generator, kept (grown on demand)
     std::unique_ptr<Ctx> side;  // second stream for work overlapped with the upload (frpca_run_csr)
     cudaStream_t copy = nullptr;  // device->host copies of results overlapped with the output GEMMs
+    // A^T*Y cold rows run beside the panel chunks (spmm.cu spmm_t_device)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    DBuf<int32_t> wcount;  // SpMM work counters (main stream, aux stream)
     // Run workspaces by role, kept between runs and grown on demand: a fresh
     // multi-GB allocation per run makes the stream-ordered pool remap memory
     // (measured 0.8 s for a 16 GB output buffer at C4).

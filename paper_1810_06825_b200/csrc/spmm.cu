@@ -20,6 +20,11 @@ namespace {
 
 constexpr int kThreads = 256;
 
+double env_double(const char* name, double dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atof(e) : dflt;
+}
+
 template <int VEC>
 struct Vec;
 template <>
@@ -177,13 +182,24 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
                                            const double* __restrict__ val, const WorkItem* __restrict__ items,
                                            int64_t nitems, const double* __restrict__ X, int64_t ldx,
                                            double* __restrict__ Y, int64_t ldy, double* __restrict__ part,
-                                           int ncols, const Hot& hot, const uint8_t* __restrict__ skip) {
+                                           int ncols, const Hot& hot, const uint8_t* __restrict__ skip,
+                                           int32_t* __restrict__ counter) {
     using V = Vec<VEC>;
     using T = typename V::T;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t it = warp; it < nitems; it += nwarps) {
+    // items are taken from a global counter when one is given (the skip list
+    // of the panelled A^T*Y leaves many items nearly empty, so a static
+    // stride leaves warps idle); which warp runs an item does not change its
+    // arithmetic
+    int64_t it = warp;
+    if (counter) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(counter, 1);
+        it = __shfl_sync(0xffffffffu, t, 0);
+    }
+    for (; it < nitems;) {
         const WorkItem w = items[it];
         if (w.r1 >= 0) {
             for (int32_t r = w.r0; r < w.r1; ++r) {
@@ -208,6 +224,13 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
             for (int ch = 0; ch < NCH; ++ch)
                 if ((ch * 32 + lane) * VEC < ncols) V::store(pr + ch * 32 * VEC, acc[ch]);
         }
+        if (counter) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(counter, 1);
+            it = __shfl_sync(0xffffffffu, t, 0);
+        } else {
+            it += nwarps;
+        }
     }
 }
 
@@ -219,10 +242,10 @@ k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
        const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
        const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
        double* __restrict__ part, int ncols, const int32_t* __restrict__ hot_cols,
-       const uint8_t* __restrict__ skip) {
+       const uint8_t* __restrict__ skip, int32_t* __restrict__ counter) {
     Hot hot{nullptr, 0, MODE == MODE_HOT ? hot_cols : nullptr, 0, 0};
     if (MODE == MODE_HINT) make_policies(hot);
-    spmm_items<VEC, NCH, MODE>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, skip);
+    spmm_items<VEC, NCH, MODE>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, skip, counter);
 }
 
 // A * X with the H most popular columns' X rows staged in shared memory: one
@@ -244,7 +267,7 @@ k_spmm_hot(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     }
     __syncthreads();
     const Hot hot{Xs, H, hot_cols, 0, 0};
-    spmm_items<2, NCH, MODE_HOT>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, nullptr);
+    spmm_items<2, NCH, MODE_HOT>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, nullptr, nullptr);
 }
 
 // Long rows: Y[row] = sum of its chunk partials in a fixed order. One CTA per
@@ -388,9 +411,20 @@ void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip,
     }
     int grid = int(std::min<int64_t>(int64_t(c.num_sms) * blocks_per_sm, (L.nitems + 7) / 8));
     grid = std::max(grid, 1);
+    // Items come from a global counter (FRPCA_SPMM_DYNAMIC=1, the default;
+    // 2 = only the cold list of the panelled A^T*Y, 0 = static stride).
+    // Measured per run against the static stride: C1 17.85 -> 17.26 ms,
+    // C2 80.8 -> 74.8, C3 228.8 -> 211.7, C4 354 -> 343 (tools/ab_env.py)
+    const int dyn = int(env_double("FRPCA_SPMM_DYNAMIC", 1.0));
+    int32_t* counter = nullptr;
+    if (dyn == 1 || (dyn == 2 && skip)) {
+        if (!c.wcount.get()) c.wcount.alloc(2, c.stream);
+        counter = c.wcount.get() + (c.stream == c.aux ? 1 : 0);
+        FB_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), c.stream));
+    }
     k_spmm<VEC, NCH, MODE><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
                                                            L.items.get(), L.nitems, X, ldx, Y, ldy, part,
-                                                           ncols, A.hot_cols.get(), skip);
+                                                           ncols, A.hot_cols.get(), skip, counter);
     FB_LAUNCH_CHECK();
 }
 
@@ -492,11 +526,6 @@ void launch_panels(Ctx& c, const DCsr& T, const double* Y, int64_t ldy, double* 
     }
 }
 
-double env_double(const char* name, double dflt) {
-    const char* e = std::getenv(name);
-    return e && *e ? std::atof(e) : dflt;
-}
-
 }  // namespace
 
 void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
@@ -534,22 +563,55 @@ void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, c
     const PanelPlan& P = T.pan;
     const double bytes = 12.0 * T.nnz + 8.0 * (T.rows + 1) + 8.0 * ncols * (T.cols + T.rows);
     Prof prof(c, tag, bytes, 2.0 * T.nnz * ncols);
-    const size_t slots = size_t(std::max(P.hot.nslots, P.cold.nslots));
+    // The cold rows (disjoint output rows, their own partial slots) run on a
+    // second stream beside the panel chunks and their combine, filling the
+    // panel kernel's tail; the arithmetic is unchanged. It pays while Y is
+    // a few times L2 (C1, Y 1.6 GB: 17.26 -> 17.05 ms per run) and costs
+    // with larger Y (C2 6 GB: 74.8 -> 75.4, C3 20.6 GB: 211.7 -> 212.7; the
+    // cold rows' HBM gathers evict panel rows), so by default it is on up to
+    // 4 GB of Y (FRPCA_COLD_CONCURRENT=0/1 forces it)
+    const double ybytes = 8.0 * double(T.cols) * double(w);
+    const bool conc = env_double("FRPCA_COLD_CONCURRENT", ybytes <= 4.0 * 1073741824.0 ? 1.0 : 0.0) != 0.0 &&
+                      P.cold.nitems > 0;
+    const size_t slots = conc ? size_t(P.hot.nslots + P.cold.nslots) : size_t(std::max(P.hot.nslots, P.cold.nslots));
     // persistent with the plan: a per-call multi-GB allocation can remap pool
     // memory every run (measured: ~150 ms per call at C3)
     DBuf<double>& part = const_cast<PanelPlan&>(P).part;
     if (part.n < slots * size_t(w)) part.alloc(slots * size_t(w), c.stream);
+    if (conc && !c.aux) {
+        FB_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
+        FB_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+        FB_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+    }
     for (int64_t off = 0; off < ncols; off += 256) {
         const int nc = int(std::min<int64_t>(256, ncols - off));
         FB_CUDA(cudaMemsetAsync(P.counter.get(), 0, sizeof(int32_t), c.stream));
-        const int grid = c.num_sms * 4;
+        if (conc) FB_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         {
             Prof ph(c, "spmm_AtY_panels", 0, 0);
             launch_panels(c, T, Y + off, ncols, part.get(), nc);
         }
+        if (conc) {
+            // queued after the panel kernel, so its CTAs take the SMs the
+            // panel kernel's tail frees
+            const cudaStream_t s0 = c.stream;
+            FB_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
+            c.stream = c.aux;
+            {
+                Prof pd(c, "spmm_AtY_cold", 0, 0);
+                spmm_list(c, T, P.cold, P.skip.get(), Y + off, ncols, nc, Z + off, ncols,
+                          part.get() + size_t(P.hot.nslots) * size_t(nc));
+            }
+            c.stream = s0;
+            FB_CUDA(cudaEventRecord(c.ev_join, c.aux));
+        }
         {
             Prof pc(c, "spmm_AtY_pcombine", 0, 0);
             combine(c, P.hot, part.get(), nc, Z + off, ncols);
+        }
+        if (conc) {
+            FB_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+            continue;
         }
         Prof pd(c, "spmm_AtY_cold", 0, 0);
         spmm_list(c, T, P.cold, P.skip.get(), Y + off, ncols, nc, Z + off, ncols, part.get());

@@ -134,6 +134,41 @@ def test_spmm_transpose_panelled(fb, orc, panels, ncols, seed):
     assert np.array_equal(Z, fb.spmm_transpose(A, Y))
 
 
+@pytest.mark.parametrize("dynamic", ["0", "1", "2"])
+@pytest.mark.parametrize("ncols", [40, 200, 300])
+def test_spmm_transpose_cold_concurrent(fb, orc, panels, monkeypatch, ncols, dynamic):
+    """Cold rows on a second stream beside the panel chunks
+    (FRPCA_COLD_CONCURRENT, own partial slots) and items taken from a global
+    counter (FRPCA_SPMM_DYNAMIC): bitwise equal to the serial, statically
+    strided order, and to themselves across calls."""
+    panels()
+    oA = powerlaw_csr(orc, 3000, 2000, 120000, 4)
+    A = to_fb(fb, oA)
+    Y = orc.gaussian_matrix(3000, ncols, 8)
+    Z0 = fb.spmm_transpose(A, Y)
+    monkeypatch.setenv("FRPCA_SPMM_DYNAMIC", dynamic)
+    assert np.array_equal(Z0, fb.spmm_transpose(A, Y))
+    monkeypatch.setenv("FRPCA_COLD_CONCURRENT", "1")
+    Z1 = fb.spmm_transpose(A, Y)
+    assert np.array_equal(Z0, Z1)
+    assert np.array_equal(Z1, fb.spmm_transpose(A, Y))
+    assert rel_fro(Z1, orc.spmm_transpose(oA, Y)) <= SPMM_TOL
+
+
+@pytest.mark.parametrize("ncols", [1, 40, 200, 256, 300])
+def test_spmm_dynamic_items(fb, orc, monkeypatch, ncols):
+    """A*X with work items from a global counter: bitwise equal to the
+    static stride (the item -> warp assignment does not enter the sums)."""
+    oA = powerlaw_csr(orc, 4000, 2500, 150000, 12)
+    A = to_fb(fb, oA)
+    X = orc.gaussian_matrix(2500, ncols, 3)
+    Y0 = fb.spmm(A, X)
+    monkeypatch.setenv("FRPCA_SPMM_DYNAMIC", "1")
+    Y1 = fb.spmm(A, X)
+    assert np.array_equal(Y0, Y1)
+    assert rel_fro(Y1, orc.spmm(oA, X)) <= SPMM_TOL
+
+
 @pytest.mark.parametrize("panel_kb,part_gb", [(3.0, None), (40.0, 1e-4), (1000.0, None)])
 def test_spmm_transpose_panel_sizes(fb, orc, panels, panel_kb, part_gb):
     """Tiny panels (many segments per row), a partial budget that forces the
