@@ -334,6 +334,8 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
     const int64_t fill = int64_t(c.num_sms) * kGenPerSm;
     int log2S = 6;
     while (log2S < 12 && (2 * P + (int64_t(MM) << log2S) - 1) / (int64_t(MM) << log2S) > fill) ++log2S;
+    if (const char* e = std::getenv("FRPCA_OMEGA_LOG2S"))  // segment length override (A/B, tests)
+        if (*e) log2S = std::max(6, std::min(14, std::atoi(e)));
     const int64_t steps = int64_t(1) << log2S, J = int64_t(MM) << log2S;
     int groups = 0;
     const uint32_t* polys = nullptr;
