@@ -740,15 +740,19 @@ void launch_gemm_tall(Ctx& c, const double* W, int64_t r, int64_t K, const doubl
 __global__ void k_transpose(const double* __restrict__ in, int64_t rows, int64_t cols,
                             double* __restrict__ out) {
     __shared__ double tile[32][33];
-    const int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
-    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-        const int64_t r = r0 + k, c = c0 + threadIdx.x;
-        if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
-    }
-    __syncthreads();
-    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-        const int64_t c = c0 + k, r = r0 + threadIdx.x;
-        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+    const int64_t c0 = int64_t(blockIdx.x) * 32;
+    // row tiles loop past grid.y's 65535 limit (outputs taller than 2M rows)
+    for (int64_t r0 = int64_t(blockIdx.y) * 32; r0 < rows; r0 += int64_t(gridDim.y) * 32) {
+        __syncthreads();  // previous tile consumed
+        for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+            const int64_t r = r0 + k, c = c0 + threadIdx.x;
+            if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
+        }
+        __syncthreads();
+        for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+            const int64_t c = c0 + k, r = r0 + threadIdx.x;
+            if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+        }
     }
 }
 
@@ -823,7 +827,7 @@ void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M,
 void transpose_device(Ctx& c, const double* in, int64_t rows, int64_t cols, double* out) {
     if (rows == 0 || cols == 0) return;
     Prof prof(c, "transpose", 16.0 * rows * cols, 0.0);
-    dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32));
+    dim3 grid(unsigned((cols + 31) / 32), unsigned(std::min<int64_t>(65535, (rows + 31) / 32)));
     k_transpose<<<grid, dim3(32, 8), 0, c.stream>>>(in, rows, cols, out);
     FB_LAUNCH_CHECK();
 }

@@ -108,6 +108,21 @@ def test_spmm_transpose_equals_spmm_on_transpose(fb, orc):
     assert np.array_equal(fb.spmm_transpose(A, Y), fb.spmm(At, Y))
 
 
+@pytest.mark.parametrize("ncols", [2, 3])
+def test_spmm_tall_output_layout(fb, ncols):
+    """A 5M-row output goes back to the host's column-major layout through
+    the tiled device transpose: more than 65535 row tiles, which the kernel
+    loops over (grid.y limit)."""
+    m, n = 5_000_000, 10
+    rp = np.arange(m + 1, dtype=np.int64)
+    ci = np.arange(m, dtype=np.int64) % n
+    va = np.ones(m)
+    A = fb.SparseMatrixCsr(m, n, rp, ci, va)
+    X = np.arange(n * ncols, dtype=np.float64).reshape(n, ncols) + 0.5
+    Y = fb.spmm(A, X)
+    assert np.array_equal(Y, X[ci])
+
+
 @pytest.fixture
 def panels(monkeypatch):
     """Forces the panelled A^T*Y (csr.cu ensure_panels) at test sizes: panels
