@@ -481,7 +481,7 @@ int frpca_eig_svd(frpca_ctx* c, int64_t m, int64_t n, const double* Ah, double* 
         DBuf<double> W(size_t(m * n), c->stream), Ud(size_t(m * n), c->stream);
         upload_colmajor(*c, Ah, m, n, m, W.get());
         EigWork e;
-        with_checks(*c, [&] { e.run(*c, W.get(), m, n); });
+        with_checks(*c, [&] { e.run(*c, W.get(), m, n, /*row_sharded=*/false); });
         DBuf<double> Mf(size_t(n * n), c->stream), Sd(size_t(n), c->stream);
         e.factor(*c, 0, int(n), int(n), false, true, Mf.get());
         gemm_device(*c, W.get(), m, n, Mf.get(), n, Ud.get(), n, false);

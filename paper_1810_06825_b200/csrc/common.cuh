@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -72,6 +74,23 @@ struct DBuf {
     T* get() const { return p; }
     size_t bytes() const { return n * sizeof(T); }
 };
+
+// Opt-in of `fn` to `bytes` of dynamic shared memory on the CURRENT device.
+// The attribute is per device, so it is tracked per (kernel, device) and raised
+// when a later call needs more; calls from several host threads are serialised.
+inline void smem_optin(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    FB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = done[{fn, dev}];
+    if (cur >= bytes) return;
+    FB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    cur = bytes;
+}
+template <class K>
+inline void smem_optin(K* fn, size_t bytes) { smem_optin(reinterpret_cast<const void*>(fn), bytes); }
 
 inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
 

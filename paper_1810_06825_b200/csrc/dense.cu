@@ -367,11 +367,7 @@ void launch_gram3_rows(Ctx& c, const double* W, int64_t r, int n, double* B) {
     const int ncol = 8 * G3_BT * NBR;
     const int S = ncol + ((12 - (ncol % 16)) + 16) % 16;
     const size_t smem = sizeof(double) * 2 * ROWS * S;
-    static bool attr = false;
-    if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_gram3<NBR, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        attr = true;
-    }
+    smem_optin(k_gram3<NBR, ROWS>, size_t(smem));
     // the row split over CTAs stays at 32-row granularity whatever the staging
     // depth, so the split-K partials (and the result) do not depend on ROWS
     int64_t nctas = std::min<int64_t>(c.num_sms, std::max<int64_t>(1, (r + G3_ROWS - 1) / G3_ROWS));
@@ -399,11 +395,7 @@ void launch_gram2(Ctx& c, const double* W, int64_t r, int n, double* B) {
     const int T = (n + 7) / 8, NT = T * (T + 1) / 2;
     const int S = n + ((12 - (n % 16)) + 16) % 16 + ((8 * T > n + ((12 - (n % 16)) + 16) % 16) ? 16 : 0);
     const size_t smem = sizeof(double) * 2 * G2_ROWS * S;
-    static bool attr = false;
-    if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_gram2<MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    smem_optin(k_gram2<MAXT>, size_t(200 * 1024));
     int64_t nctas = std::min<int64_t>(c.num_sms, std::max<int64_t>(1, (r + G2_ROWS - 1) / G2_ROWS));
     const int64_t rpc = ((r + nctas - 1) / nctas + G2_ROWS - 1) / G2_ROWS * G2_ROWS;
     nctas = std::max<int64_t>(1, (r + rpc - 1) / rpc);
@@ -706,12 +698,7 @@ void launch_gemm_persist(Ctx& c, const double* W, int64_t r, int64_t K, const do
     const int BM = 8 * RT * ((GP_THREADS / 32) / WC);
     const int Kp = int((K + TK - 1) / TK) * TK;
     const size_t smem = sizeof(double) * (size_t(Kp) * SB + 2 * size_t(BM) * TSA);
-    static bool attr = false;
-    if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_gemm_persist<RT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
-        attr = true;
-    }
+    smem_optin(k_gemm_persist<RT, NT>, size_t(227 * 1024));
     const int64_t nblocks = (r + BM - 1) / BM;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, nblocks)));
     k_gemm_persist<RT, NT><<<grid, GP_THREADS, smem, c.stream>>>(W, r, int(K), M, int(ldm), int(N), C, ldc,
@@ -726,11 +713,7 @@ void launch_gemm_tall(Ctx& c, const double* W, int64_t r, int64_t K, const doubl
     const int SB = NP + ((12 - (NP % 16)) + 16) % 16;
     const int BM = 16 * (8 / WC);
     const size_t smem = sizeof(double) * (2 * size_t(BM) * TSA + 2 * size_t(TK) * SB);
-    static bool attr = false;
-    if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_gemm_tall<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-        attr = true;
-    }
+    smem_optin(k_gemm_tall<NT>, size_t(112 * 1024));
     k_gemm_tall<NT><<<unsigned((r + BM - 1) / BM), 256, smem, c.stream>>>(W, r, int(K), M, int(N), C, ldc,
                                                                        col_major_out ? 1 : 0, WC, SB);
     FB_LAUNCH_CHECK();

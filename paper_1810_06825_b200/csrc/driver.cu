@@ -66,11 +66,11 @@ __global__ void k_sing_out(const double* __restrict__ D, int s, int k, int rev, 
 
 }  // namespace
 
-void EigWork::run(Ctx& c, const double* W, int64_t r, int64_t n) {
+void EigWork::run(Ctx& c, const double* W, int64_t r, int64_t n, bool row_sharded) {
     B.alloc(size_t(n * n), c.stream);
     D.alloc(size_t(n), c.stream);
     gram_device(c, W, r, n, B.get());
-    allreduce_sum(c, B.get(), n * n);  // row-sharded W: Gram partials
+    if (row_sharded) allreduce_sum(c, B.get(), n * n);  // Gram partials of the rank's rows
     syevd_device(c, B.get(), n, D.get());
     // rank check (dense_kernels.hpp:163-167), reported by err_check
     k_rank_check<<<1, 1, 0, c.stream>>>(D.get(), int(n), err_flag(c));
@@ -90,10 +90,11 @@ void EigWork::singular_values(Ctx& c, int s, int k, bool rev, double* S) {
     FB_LAUNCH_CHECK();
 }
 
-// eig_svd(W).U: Uout (row-major r x n) = W * V diag(1/S).
+// eig_svd(W).U: Uout (row-major r x n) = W * V diag(1/S), for a W that is
+// replicated on every rank (the power iteration's Z / Y after their allreduce).
 void eig_svd_U(Ctx& c, const double* W, int64_t r, int64_t n, double* Uout) {
     EigWork e;
-    e.run(c, W, r, n);
+    e.run(c, W, r, n, /*row_sharded=*/false);
     DBuf<double> M(size_t(n * n), c.stream);
     e.factor(c, 0, int(n), int(n), false, true, M.get());
     gemm_device(c, W, r, n, M.get(), n, Uout, n, false);
@@ -286,7 +287,7 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
 
     spmm_pass(c, M, false, Q.get(), l, bufM.get());       // W = A Q, m x l
     EigWork e;
-    e.run(c, bufM.get(), m, l);
+    e.run(c, bufM.get(), m, l, /*row_sharded=*/true);     // this rank's rows of W
     DBuf<double> MU(size_t(l * k), S), MV(size_t(l * k), S);
     e.factor(c, int(s), int(k), int(k), true, true, MU.get());
     e.factor(c, int(s), int(k), int(k), true, false, MV.get());
@@ -371,7 +372,7 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
 
     spmm_pass(c, M, true, Q.get(), l, bufN.get());        // W = A^T Q, n x l
     EigWork e;
-    e.run(c, bufN.get(), n, l);
+    e.run(c, bufN.get(), n, l, /*row_sharded=*/true);     // this rank's columns of A = rows of W
     DBuf<double> MU(size_t(l * k), S), MV(size_t(l * k), S);
     e.factor(c, int(s), int(k), int(k), true, false, MU.get());   // U = Q * V(:, ind)
     e.factor(c, int(s), int(k), int(k), true, true, MV.get());    // V = f.U(:, ind)
@@ -454,7 +455,7 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
     if (!left) {
         DBuf<double>& W = c.slot(2, size_t(std::max<int64_t>(n, 1) * l));
         spmm_pass(c, M, true, bufM.get(), l, W.get());          // W = A^T Q, n x l
-        e.run(c, W.get(), n, l);
+        e.run(c, W.get(), n, l, false);
         e.factor(c, int(s), int(k), int(k), true, false, MU.get());  // U = Q V(:, ind)
         e.factor(c, int(s), int(k), int(k), true, true, MV.get());   // V = W V(:, ind) / S
         gemm_device(c, bufM.get(), m, l, MU.get(), k, Uo.get(), std::max<int64_t>(m, 1), true);
@@ -463,7 +464,7 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
     } else {
         DBuf<double>& W = c.slot(2, size_t(std::max<int64_t>(m, 1) * l));
         spmm_pass(c, M, false, bufN.get(), l, W.get());         // W = A Q, m x l
-        e.run(c, W.get(), m, l);
+        e.run(c, W.get(), m, l, false);
         e.factor(c, int(s), int(k), int(k), true, true, MU.get());   // U = W V(:, ind) / S
         e.factor(c, int(s), int(k), int(k), true, false, MV.get());  // V = Q V(:, ind)
         gemm_device(c, W.get(), m, l, MU.get(), k, Uo.get(), std::max<int64_t>(m, 1), true);
@@ -529,11 +530,14 @@ void err_check(Ctx& c) {
 
 void run_algorithm(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, int algo) {
     const uint64_t passes0 = M.passes.load();
+    RunArgs cur = a;
     with_checks(c, [&] {
         M.passes.store(passes0);  // a re-run counts its passes once
-        if (algo == FRPCA_ALGO_FRPCA) run_frpca(c, M, a, st);
-        else if (algo == FRPCA_ALGO_FRPCAT) run_frpcat(c, M, a, st);
-        else run_basic(c, M, a, st, algo == FRPCA_ALGO_BASIC_RPCAT);
+        const RunArgs now = cur;
+        cur.pre = nullptr;        // the pre-generated Omega is consumed by the first attempt only
+        if (algo == FRPCA_ALGO_FRPCA) run_frpca(c, M, now, st);
+        else if (algo == FRPCA_ALGO_FRPCAT) run_frpcat(c, M, now, st);
+        else run_basic(c, M, now, st, algo == FRPCA_ALGO_BASIC_RPCAT);
     });
 }
 

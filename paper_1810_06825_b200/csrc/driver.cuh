@@ -11,14 +11,20 @@ struct RunArgs {
     int64_t omega_rows = 0, omega_cols = 0;
     double *U = nullptr, *S = nullptr, *V = nullptr, *basis = nullptr;
     bool device_io = false;
-    DBuf<double>* pre = nullptr;  // Omega generated ahead (frpca_run_csr), moved in
+    // Omega generated ahead (frpca_run_csr), moved into the run's slot by the
+    // first sketch_into of the call; a repeated call (run_algorithm's retry)
+    // regenerates it
+    DBuf<double>* pre = nullptr;
 };
 
 // eig_svd pipeline state: Gram -> (allreduce) -> syevd (B becomes V) -> rank check.
+// `row_sharded`: W holds this rank's rows of a row-distributed matrix, so the
+// Gram partials are summed over ranks; a replicated W (identical on every
+// rank, e.g. Z after its allreduce) is not summed.
 struct EigWork {
     DBuf<double> B, D;
     int64_t l = 0;
-    void run(Ctx& c, const double* W, int64_t r, int64_t n);
+    void run(Ctx& c, const double* W, int64_t r, int64_t n, bool row_sharded);
     void factor(Ctx& c, int s, int k, int ncols, bool rev, bool scale, double* M);
     void singular_values(Ctx& c, int s, int k, bool rev, double* S);
 };

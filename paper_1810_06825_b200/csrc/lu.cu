@@ -117,7 +117,7 @@ k_lu(double* __restrict__ W, int64_t m, int l, const unsigned long long* __restr
             for (int k = threadIdx.x; k < nblk; k += kT) cand_merge(c, cand[k]);
             const Cand best = block_best<kT>(c, shc);
             if (tim) clk[2] = clock64();
-            if (!(best.v > tol) || best.row < 0) {  // zero pivot (:81)
+            if (best.v <= tol || best.row < 0) {  // zero pivot (:81); NaN passes, as there
                 if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(err, 0, kErrLuPivot);
                 return;  // uniform across the grid
             }
@@ -317,7 +317,7 @@ k_lu_smem(double* __restrict__ W, int64_t m, int l, const unsigned long long* __
                 for (int k = lane + 32 * kPer; k < G; k += 32) cand_merge(best, cand[k]);
             }
             best = warp_best(best);
-            if (!(best.v > tol) || best.row < 0) {  // zero pivot (:81)
+            if (best.v <= tol || best.row < 0) {  // zero pivot (:81); NaN passes, as there
                 if (blockIdx.x == 0 && tid == 0) atomicCAS(err, 0, kErrLuPivot);
                 return;  // uniform across the grid
             }

@@ -343,11 +343,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         Prof pp(c, "omega_polys", 0.0, 0.0);
         polys = device_polys(c, log2S, groups);
     }
-    static bool attr = false;
-    if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_jump_level, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNibBytes)));
-        attr = true;
-    }
+    smem_optin(k_jump_level, size_t(kNibBytes));
     const crlog::LogEntry* logtab = device_logtab(c);
     uint64_t s0[NN];
     mt64_seed_state(seed, s0);

@@ -434,12 +434,7 @@ template <int NCH>
 void launch_hot(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
                 double* part, int ncols) {
     const int H = int(std::min<int64_t>(A.nhot, int64_t(kHotSmem / (sizeof(double) * ncols))));
-    static bool attr = false;
-    if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_spmm_hot<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kHotSmem)));
-        attr = true;
-    }
+    smem_optin(k_spmm_hot<NCH>, size_t(kHotSmem));
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, (A.L.nitems + 31) / 32)));
     k_spmm_hot<NCH><<<grid, kHotThreads, sizeof(double) * size_t(H) * ncols, c.stream>>>(
         A.rowptr.get(), A.col.get(), A.val.get(), A.L.items.get(), A.L.nitems, X, ldx, Y, ldy, part, ncols,

@@ -1095,13 +1095,9 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D) {
     if (n64 < 1 || n64 > kEigMax || c.force_cusolver) return false;
     const int n = int(n64);
     cudaStream_t s = c.stream;
-    static bool attr = false;
-    if (!attr) {
-        FB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)));
-        FB_CUDA(cudaFuncSetAttribute(k_sytrd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)));
-        FB_CUDA(cudaFuncSetAttribute(k_stedc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(stedc_smem())));
-        attr = true;
-    }
+    smem_optin(k_sytrd, size_t(kSmemMax));
+    smem_optin(k_sytrd_fused, size_t(kSmemMax));
+    smem_optin(k_stedc, size_t(stedc_smem()));
     const size_t nn = size_t(n) * n;
     DBuf<double> ws(nn + 3 * size_t(n) + 3 * nn, s);
     double* H = ws.get();
