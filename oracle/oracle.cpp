@@ -17,16 +17,24 @@
 //     (the method SPEC.md:175 chose); pinned <=1e-10 against the one-sided
 //     Jacobi oracle as test_dense_kernels.cpp:159-165 does.
 //   * Eigen's blocked SYRK/GEMM summation order (dense_kernels.hpp:91-104,
-//     :157, :172) -> sequential sums in natural index order.
+//     :157, :172): the Gram is a panelled sum (kc = 256 rows per panel,
+//     panel partials added in order, Eigen's rankUpdate structure); the
+//     LU trailing update forms each nb-term L21*U12 product first and
+//     subtracts it once (Eigen's GEBP); other products are sequential sums
+//     over the inner index.
 // Everything else (CSR, spmm, spmm_transpose, transpose, mix_seed, the Omega
 // stream from libstdc++ mt19937_64 + normal_distribution, the LU pivot rule,
 // the drivers and their preconditions/messages) is restated exactly.
 //
 // Build: oracle/Makefile (g++ -O3 -ffp-contract=off, no -march: the same
 // arithmetic the reference's -O2/-O3 x86-64 build performs, no FMA).
-// Threads: OpenMP parallelism is only ever over independent output entries
-// (dense columns of spmm, rows of rank-1 updates, Gram entries), so every
-// result is bitwise identical for any thread count (checked in tests).
+// Threads: parallelism is only ever over independent output entries (rows
+// or column slices of spmm / spmm_transpose, Gram and GEMM tiles, columns of
+// rank-1 updates), so every result is bitwise identical for any thread count
+// (checked in tests). Loops whose nesting was changed for speed keep every
+// entry's operation sequence; each has its literal form beside it
+// (spmm_literal, spmm_transpose_literal, gram_lower_literal), and the tests
+// pin the two bitwise.
 
 #include <algorithm>
 #include <atomic>
@@ -156,10 +164,67 @@ static Csr* from_triplets(Index rows, Index cols, std::vector<Triplet> e) {
     return A;
 }
 
+// Register tiles of the Gram and GEMM below. Vector width (target clones)
+// never changes a result: each entry is its own chain of separately rounded
+// products and sums (-ffp-contract=off), in the same order at any width.
+#define ORC_CLONES __attribute__((target_clones("avx512f", "avx2", "default")))
+ORC_CLONES static void gram_tile(const double* T, Index np, Index rows, Index i0, Index j0, double* out) {
+    constexpr Index IB = 8, JB = 8;
+    double acc[JB][IB] = {};
+    for (Index r = 0; r < rows; ++r) {
+        const double* tr = T + size_t(r) * size_t(np);
+        for (Index c = 0; c < JB; ++c) {
+            const double wj = tr[j0 + c];
+            for (Index a = 0; a < IB; ++a) acc[c][a] += tr[i0 + a] * wj;
+        }
+    }
+    for (Index a = 0; a < IB; ++a)
+        for (Index c = 0; c < JB; ++c) out[a * JB + c] = acc[c][a];
+}
+
+// acc[u][v] = sum over t of A(i0 + u, t) * Mr(t, j0 + v) (rows past ni read 0)
+ORC_CLONES static void gemm_tile(const double* A0, Index lda, Index ni, Index l, const double* Mr, Index cp,
+                                 double* out) {
+    constexpr Index IB = 8, JB = 4;
+    double acc[IB][JB] = {};
+    for (Index t = 0; t < l; ++t) {
+        const double* at = A0 + size_t(t) * size_t(lda);
+        const double* mt = Mr + size_t(t) * size_t(cp);
+        double a[IB];
+        for (Index u = 0; u < IB; ++u) a[u] = u < ni ? at[u] : 0.0;
+        for (Index u = 0; u < IB; ++u)
+            for (Index v = 0; v < JB; ++v) acc[u][v] += a[u] * mt[v];
+    }
+    for (Index u = 0; u < IB; ++u)
+        for (Index v = 0; v < JB; ++v) out[u * JB + v] = acc[u][v];
+}
+
+// acc[c] += v * x[c] over the nonzeros of one row (spmm's inner loop)
+ORC_CLONES static void spmm_row(const Index* ci, const double* v, Index p0, Index p1, const double* Xr, Index nc,
+                                double* acc) {
+    for (Index p = p0; p < p1; ++p) {
+        const double vp = v[p];
+        const double* x = Xr + size_t(ci[p]) * size_t(nc);
+        for (Index c = 0; c < nc; ++c) acc[c] += vp * x[c];
+    }
+}
+
+// z(ci[p], c) += v[p] * y(c) for y(c) != 0 (spmm_transpose's inner loop)
+ORC_CLONES static void spmmt_row(const Index* ci, const double* v, Index p0, Index p1, const double* yi, Index w,
+                                 double* Zr) {
+    for (Index p = p0; p < p1; ++p) {
+        const double vp = v[p];
+        double* z = Zr + size_t(ci[p]) * size_t(w);
+        for (Index c = 0; c < w; ++c)
+            if (yi[c] != 0.0) z[c] += vp * yi[c];
+    }
+}
+
 // ---- spmm (sparse_matrix.hpp:177-206) --------------------------------------
-// Column-outer, per (column c, row i) sequential sum in CSR order. X is
-// column-major with leading dimension ldx (Eigen::Ref outerStride, :182/:196).
-static void spmm(const Csr& A, const double* X, Index ldx, Index ncols, double* Y) {
+// Literal restatement: column-outer, per (column c, row i) a sequential sum in
+// CSR order starting from 0.0. X is column-major with leading dimension ldx
+// (Eigen::Ref outerStride, :182/:196). Kept as the pin of the loop below.
+static void spmm_literal(const Csr& A, const double* X, Index ldx, Index ncols, double* Y) {
     const Index m = A.rows;
     if (m == 0 || ncols == 0) { A.record_pass(); return; }
     const Index* rp = A.row_ptr.data();
@@ -177,10 +242,43 @@ static void spmm(const Csr& A, const double* X, Index ldx, Index ncols, double* 
     A.record_pass();
 }
 
+// The same arithmetic with the loops exchanged: every (i, c) entry is still
+// `acc = 0.0; acc += v[p] * x[ci[p]]` over p in CSR order (-ffp-contract=off,
+// so each step is one rounded product and one rounded sum), so Y is bitwise
+// equal to spmm_literal (tests/test_oracle.py pins it). One pass over A
+// instead of ncols: a row block gathers rows of a row-major copy of X and
+// keeps its ncols accumulators per row side by side.
+static void spmm(const Csr& A, const double* X, Index ldx, Index ncols, double* Y) {
+    const Index m = A.rows, n = A.cols;
+    if (m == 0 || ncols == 0) { A.record_pass(); return; }
+    const Index* rp = A.row_ptr.data();
+    const Index* ci = A.col_idx.data();
+    const double* v = A.values.data();
+    const Index nc = ncols;
+    std::vector<double> Xr(size_t(n) * size_t(nc));
+    constexpr Index TB = 256;
+    parallel_for(0, (n + TB - 1) / TB, [&](Index b) {
+        const Index j0 = b * TB, j1 = std::min(n, j0 + TB);
+        for (Index c = 0; c < nc; ++c)
+            for (Index j = j0; j < j1; ++j) Xr[size_t(j) * size_t(nc) + size_t(c)] = X[j + c * ldx];
+    });
+    constexpr Index RB = 64;
+    parallel_for(0, (m + RB - 1) / RB, [&](Index b) {
+        const Index r0 = b * RB, r1 = std::min(m, r0 + RB);
+        thread_local std::vector<double> tile;
+        tile.assign(size_t(RB) * size_t(nc), 0.0);
+        for (Index i = r0; i < r1; ++i)
+            spmm_row(ci, v, rp[i], rp[i + 1], Xr.data(), nc, tile.data() + size_t(i - r0) * size_t(nc));
+        for (Index c = 0; c < nc; ++c)
+            for (Index i = r0; i < r1; ++i) Y[i + c * m] = tile[size_t(i - r0) * size_t(nc) + size_t(c)];
+    });
+    A.record_pass();
+}
+
 // ---- spmm_transpose (sparse_matrix.hpp:208-240) ----------------------------
-// Z = A^T Y by scatter, column-outer, rows ascending, skipping y[i] == 0.
-// Z (n x ncols, column-major) is zero-initialised here as in :224.
-static void spmm_transpose(const Csr& A, const double* Y, Index ldy, Index ncols, double* Z) {
+// Literal restatement: Z = A^T Y by scatter, column-outer, rows ascending,
+// skipping y[i] == 0. Z (n x ncols, column-major) is zero-initialised as in :224.
+static void spmm_transpose_literal(const Csr& A, const double* Y, Index ldy, Index ncols, double* Z) {
     const Index m = A.rows, n = A.cols;
     std::fill(Z, Z + size_t(n) * size_t(ncols), 0.0);
     if (m == 0 || ncols == 0) { A.record_pass(); return; }
@@ -195,6 +293,36 @@ static void spmm_transpose(const Csr& A, const double* Y, Index ldy, Index ncols
             if (yi == 0.0) continue;
             for (Index p = rp[i]; p < rp[i + 1]; ++p) z[ci[p]] += v[p] * yi;
         }
+    });
+    A.record_pass();
+}
+
+// The same scatter with the column loop innermost: each task owns a slice of
+// columns and walks the rows once, so every z(j, c) still receives
+// v[p] * y(i, c) for ascending i, skipping y(i, c) == 0 -- bitwise equal to
+// spmm_transpose_literal (pinned in tests/test_oracle.py).
+static void spmm_transpose(const Csr& A, const double* Y, Index ldy, Index ncols, double* Z) {
+    const Index m = A.rows, n = A.cols;
+    std::fill(Z, Z + size_t(n) * size_t(ncols), 0.0);
+    if (m == 0 || ncols == 0) { A.record_pass(); return; }
+    const Index* rp = A.row_ptr.data();
+    const Index* ci = A.col_idx.data();
+    const double* v = A.values.data();
+    const Index W = std::max<Index>(4, (ncols + g_threads - 1) / g_threads);
+    parallel_for(0, (ncols + W - 1) / W, [&](Index t) {
+        const Index c0 = t * W, w = std::min(ncols, c0 + W) - c0;
+        std::vector<double> Zr(size_t(n) * size_t(w), 0.0);
+        constexpr Index RB = 64;
+        std::vector<double> yt(size_t(RB) * size_t(w));
+        for (Index r0 = 0; r0 < m; r0 += RB) {
+            const Index r1 = std::min(m, r0 + RB);
+            for (Index c = 0; c < w; ++c)
+                for (Index i = r0; i < r1; ++i) yt[size_t(i - r0) * size_t(w) + size_t(c)] = Y[i + (c0 + c) * ldy];
+            for (Index i = r0; i < r1; ++i)
+                spmmt_row(ci, v, rp[i], rp[i + 1], yt.data() + size_t(i - r0) * size_t(w), w, Zr.data());
+        }
+        for (Index c = 0; c < w; ++c)
+            for (Index j = 0; j < n; ++j) Z[j + (c0 + c) * n] = Zr[size_t(j) * size_t(w) + size_t(c)];
     });
     A.record_pass();
 }
@@ -385,44 +513,93 @@ static void eig_sym_lower(const Mat& Bin, Mat& V, std::vector<double>& D) {
 static Mat gram_lower(const Mat& W) {
     const Index m = W.rows, n = W.cols;
     Mat B(n, n);
-    const Index kc = 256, rb = 16 * kc;  // rb: cache blocking of this loop only
+    // Per entry exactly the panelled sum above: part = 0.0, part += w_i[r] *
+    // w_j[r] over the kc rows of a panel in order, then B(i, j) += part, panels
+    // in order. The loops run over 8 x 4 tiles of entries whose partial sums
+    // advance side by side in registers, reading a row-major copy T of a block
+    // of rows (the per-entry order is unchanged: bitwise equal to the plain
+    // loop gram_lower_literal, pinned in tests/test_oracle.py).
+    constexpr Index kc = 256, rb = 64 * kc, IB = 8, JB = 8;  // rb: blocking of this loop only
+    const Index ni = (n + IB - 1) / IB, nj = (n + JB - 1) / JB;
+    const Index np = ni * IB;  // T rows padded to whole tiles (the padding is never stored)
+    std::vector<double> T;
     for (Index b0 = 0; b0 < m; b0 += rb) {
         const Index b1 = std::min(m, b0 + rb);
-        parallel_for(0, n, [&](Index j) {
-            const double* wj = W.col(j);
-            for (Index i = j; i < n; ++i) {
-                const double* wi = W.col(i);
-                double acc = B(i, j);
-                for (Index r0 = b0; r0 < b1; r0 += kc) {
-                    const Index r1 = std::min(b1, r0 + kc);
-                    double part = 0.0;
-                    for (Index r = r0; r < r1; ++r) part += wi[r] * wj[r];
-                    acc += part;
+        T.assign(size_t(b1 - b0) * size_t(np), 0.0);
+        parallel_for(0, (b1 - b0 + 63) / 64, [&](Index t) {  // each task writes whole rows of T
+            const Index q0 = b0 + 64 * t, q1 = std::min(b1, q0 + 64);
+            for (Index j = 0; j < n; ++j) {
+                const double* wj = W.col(j);
+                for (Index r = q0; r < q1; ++r) T[size_t(r - b0) * size_t(np) + size_t(j)] = wj[r];
+            }
+        });
+        // one task per 4-column block of B: a panel of T (kc rows, cache
+        // resident) is swept once per 8-row tile of that block
+        parallel_for(0, nj, [&](Index jb) {
+            const Index j0 = jb * JB;
+            const Index ib0 = j0 / IB;
+            for (Index r0 = b0; r0 < b1; r0 += kc) {
+                const Index r1 = std::min(b1, r0 + kc);
+                for (Index ib = ib0; ib < ni; ++ib) {
+                    const Index i0 = ib * IB;
+                    double acc[IB * JB];
+                    gram_tile(T.data() + size_t(r0 - b0) * size_t(np), np, r1 - r0, i0, j0, acc);
+                    for (Index c = 0; c < JB; ++c)
+                        for (Index a = 0; a < IB; ++a) {
+                            const Index i = i0 + a, j = j0 + c;
+                            if (i < n && j < n && i >= j) B(i, j) += acc[a * JB + c];
+                        }
                 }
-                B(i, j) = acc;
             }
         });
     }
     return B;
 }
 
-// C = A * M, A m x l, M l x c: each entry a sequential sum over l.
+// The plain form of the panelled Gram (the pin of gram_lower above).
+static Mat gram_lower_literal(const Mat& W) {
+    const Index m = W.rows, n = W.cols;
+    Mat B(n, n);
+    const Index kc = 256;
+    parallel_for(0, n, [&](Index j) {
+        const double* wj = W.col(j);
+        for (Index i = j; i < n; ++i) {
+            const double* wi = W.col(i);
+            double acc = 0.0;
+            for (Index r0 = 0; r0 < m; r0 += kc) {
+                const Index r1 = std::min(m, r0 + kc);
+                double part = 0.0;
+                for (Index r = r0; r < r1; ++r) part += wi[r] * wj[r];
+                acc += part;
+            }
+            B(i, j) = acc;
+        }
+    });
+    return B;
+}
+
+// C = A * M, A m x l, M l x c: each entry a sequential sum over l starting
+// from 0.0. Computed in 8 x 4 tiles of C whose sums advance side by side in
+// registers (per entry the same order).
 static Mat gemm(const Mat& A, const Mat& M) {
     const Index m = A.rows, l = A.cols, c = M.cols;
     Mat C(m, c);
+    constexpr Index IB = 8, JB = 4;
+    std::vector<double> Mr(size_t(l) * size_t((c + JB - 1) / JB * JB), 0.0);  // row-major, padded
+    const Index cp = (c + JB - 1) / JB * JB;
+    for (Index t = 0; t < l; ++t)
+        for (Index j = 0; j < c; ++j) Mr[size_t(t) * size_t(cp) + size_t(j)] = M(t, j);
     const Index rb = 256;
     parallel_for(0, (m + rb - 1) / rb, [&](Index blk) {
-        const Index r0 = blk * rb;
-        const Index r1 = std::min(m, r0 + rb);
-        std::vector<double> acc(size_t(r1 - r0));
-        for (Index j = 0; j < c; ++j) {
-            std::fill(acc.begin(), acc.end(), 0.0);
-            for (Index t = 0; t < l; ++t) {
-                const double mt = M(t, j);
-                const double* at = A.col(t);
-                for (Index r = r0; r < r1; ++r) acc[size_t(r - r0)] += at[r] * mt;
+        const Index r0 = blk * rb, r1 = std::min(m, r0 + rb);
+        for (Index i0 = r0; i0 < r1; i0 += IB) {
+            const Index ni = std::min(IB, r1 - i0);
+            for (Index j0 = 0; j0 < c; j0 += JB) {
+                double acc[IB * JB];
+                gemm_tile(A.col(0) + i0, A.rows, ni, l, Mr.data() + j0, cp, acc);
+                for (Index v = 0; v < JB && j0 + v < c; ++v)
+                    for (Index u = 0; u < ni; ++u) C(i0 + u, j0 + v) = acc[u * JB + v];
             }
-            std::memcpy(C.col(j) + r0, acc.data(), sizeof(double) * size_t(r1 - r0));
         }
     });
     return C;
@@ -431,7 +608,11 @@ static Mat gemm(const Mat& A, const Mat& M) {
 // ---- eig_svd (dense_kernels.hpp:136-174) -----------------------------------
 struct EigSvd { Mat U; std::vector<double> S; Mat V; };
 
-static EigSvd eig_svd(const Mat& A) {
+// U columns [u0, u0 + nu) only (nu < 0: all). The drivers keep only
+// f.U(:, s..s+k-1) (randsvd.hpp:265-267, :317-319); each entry of U is its own
+// sum over n, so forming just those columns is bitwise the same as forming U
+// and selecting (half the work and memory of the final m x l product).
+static EigSvd eig_svd(const Mat& A, Index u0 = 0, Index nu = -1) {
     const Index m = A.rows, n = A.cols;
     require(m >= n && n >= 1, "eig_svd: input must be tall (rows >= cols >= 1)");
     Mat B = gram_lower(A);
@@ -446,10 +627,11 @@ static EigSvd eig_svd(const Mat& A) {
     out.S.resize(size_t(n));
     for (Index j = 0; j < n; ++j) out.S[size_t(j)] = std::sqrt(D[size_t(j)]);
     out.V = V;
-    Mat Ms(n, n);                                  // V * diag(1/S)  (:172)
-    for (Index j = 0; j < n; ++j) {
-        const double inv = 1.0 / out.S[size_t(j)];
-        for (Index i = 0; i < n; ++i) Ms(i, j) = V(i, j) * inv;
+    if (nu < 0) { u0 = 0; nu = n; }
+    Mat Ms(n, nu);                                 // V * diag(1/S)  (:172), columns u0..
+    for (Index j = 0; j < nu; ++j) {
+        const double inv = 1.0 / out.S[size_t(u0 + j)];
+        for (Index i = 0; i < n; ++i) Ms(i, j) = V(i, u0 + j) * inv;
     }
     out.U = gemm(A, Ms);
     return out;
@@ -535,11 +717,11 @@ static Svd frpca(const Csr& A, const Config& cfg, Stats* stats, const Mat* omega
     }
     const double t_power = since(t0);
     t0 = Clock::now();
-    EigSvd f = eig_svd(spmmT_m(A, Q));            // A^T Q, n x l
     const Index s = cfg.oversample;
+    EigSvd f = eig_svd(spmmT_m(A, Q), s, cfg.k);  // A^T Q, n x l; U columns s..s+k-1
     Svd out;
     out.U = gemm(Q, cols_reversed(f.V, s, cfg.k));
-    out.V = cols_reversed(f.U, s, cfg.k);
+    out.V = cols_reversed(f.U, 0, cfg.k);
     out.S.resize(size_t(cfg.k));
     for (Index t = 0; t < cfg.k; ++t) out.S[size_t(t)] = f.S[size_t(s + cfg.k - 1 - t)];
     if (stats) {
@@ -579,10 +761,10 @@ static Svd frpcat(const Csr& A, const Config& cfg, Stats* stats, const Mat* omeg
     }
     const double t_power = since(t0);
     t0 = Clock::now();
-    EigSvd f = eig_svd(spmm_m(A, Q));             // A Q, m x l
     const Index s = cfg.oversample;
+    EigSvd f = eig_svd(spmm_m(A, Q), s, cfg.k);   // A Q, m x l; U columns s..s+k-1
     Svd out;
-    out.U = cols_reversed(f.U, s, cfg.k);
+    out.U = cols_reversed(f.U, 0, cfg.k);
     out.V = gemm(Q, cols_reversed(f.V, s, cfg.k));
     out.S.resize(size_t(cfg.k));
     for (Index t = 0; t < cfg.k; ++t) out.S[size_t(t)] = f.S[size_t(s + cfg.k - 1 - t)];
@@ -1118,6 +1300,18 @@ void orc_csr_destroy(void* h) { delete static_cast<Csr*>(h); }
 // --- kernels ---
 int orc_spmm(void* h, const double* X, int64_t ldx, int64_t ncols, double* Y) {
     return guarded([&] { spmm(*static_cast<Csr*>(h), X, ldx, ncols, Y); });
+}
+int orc_spmm_literal(void* h, const double* X, int64_t ldx, int64_t ncols, double* Y) {
+    return guarded([&] { spmm_literal(*static_cast<Csr*>(h), X, ldx, ncols, Y); });
+}
+int orc_spmm_transpose_literal(void* h, const double* Y, int64_t ldy, int64_t ncols, double* Z) {
+    return guarded([&] { spmm_transpose_literal(*static_cast<Csr*>(h), Y, ldy, ncols, Z); });
+}
+int orc_gram_lower_literal(int64_t m, int64_t n, const double* W, double* B) {
+    return guarded([&] {
+        Mat G = gram_lower_literal(view_colmajor(W, m, n, m));
+        std::memcpy(B, G.d.data(), sizeof(double) * size_t(n) * size_t(n));
+    });
 }
 int orc_spmm_transpose(void* h, const double* Y, int64_t ldy, int64_t ncols, double* Z) {
     return guarded([&] { spmm_transpose(*static_cast<Csr*>(h), Y, ldy, ncols, Z); });

@@ -83,6 +83,9 @@ def lib():
         L.orc_csr_destroy.argtypes = [_vp]
         L.orc_spmm.argtypes = [_vp, _dp, _i64, _i64, _dp]
         L.orc_spmm_transpose.argtypes = [_vp, _dp, _i64, _i64, _dp]
+        L.orc_spmm_literal.argtypes = [_vp, _dp, _i64, _i64, _dp]
+        L.orc_spmm_transpose_literal.argtypes = [_vp, _dp, _i64, _i64, _dp]
+        L.orc_gram_lower_literal.argtypes = [_i64, _i64, _dp, _dp]
         L.orc_lu_basis.argtypes = [_i64, _i64, _dp, _dp]
         L.orc_orth.argtypes = [_i64, _i64, _dp, _dp]
         L.orc_mtx_read.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(_i64), C.POINTER(_i64),
@@ -206,21 +209,26 @@ class Csr:
         lib().orc_csr_reset_pass_count(self._h)
 
 
-def spmm(A: Csr, X: np.ndarray) -> np.ndarray:
+def spmm(A: Csr, X: np.ndarray, literal: bool = False) -> np.ndarray:
+    """sparse_matrix.hpp:177-206. literal=True runs the column-outer loop as
+    written in the reference (the pin of the default row-outer loop)."""
     X = np.asfortranarray(X, dtype=np.float64)
     if X.ndim != 2 or X.shape[0] != A.cols:
         raise ValueError("spmm: inner dimensions do not match")
     Y = np.empty((A.rows, X.shape[1]), order="F")
-    _check(lib().orc_spmm(A._h, _d(X), max(X.shape[0], 1), X.shape[1], _d(Y)))
+    f = lib().orc_spmm_literal if literal else lib().orc_spmm
+    _check(f(A._h, _d(X), max(X.shape[0], 1), X.shape[1], _d(Y)))
     return Y
 
 
-def spmm_transpose(A: Csr, Y: np.ndarray) -> np.ndarray:
+def spmm_transpose(A: Csr, Y: np.ndarray, literal: bool = False) -> np.ndarray:
+    """sparse_matrix.hpp:208-240 (literal: the column-outer scatter as written)."""
     Y = np.asfortranarray(Y, dtype=np.float64)
     if Y.ndim != 2 or Y.shape[0] != A.rows:
         raise ValueError("spmm_transpose: inner dimensions do not match")
     Z = np.empty((A.cols, Y.shape[1]), order="F")
-    _check(lib().orc_spmm_transpose(A._h, _d(Y), max(Y.shape[0], 1), Y.shape[1], _d(Z)))
+    f = lib().orc_spmm_transpose_literal if literal else lib().orc_spmm_transpose
+    _check(f(A._h, _d(Y), max(Y.shape[0], 1), Y.shape[1], _d(Z)))
     return Z
 
 
@@ -251,11 +259,12 @@ def eig_sym(B: np.ndarray):
     return V, D
 
 
-def gram_lower(W: np.ndarray) -> np.ndarray:
+def gram_lower(W: np.ndarray, literal: bool = False) -> np.ndarray:
     W = np.asfortranarray(W, dtype=np.float64)
     m, n = W.shape
     B = np.empty((n, n), order="F")
-    _check(lib().orc_gram_lower(m, n, _d(W), _d(B)))
+    f = lib().orc_gram_lower_literal if literal else lib().orc_gram_lower
+    _check(f(m, n, _d(W), _d(B)))
     return B
 
 

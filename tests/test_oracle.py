@@ -114,6 +114,38 @@ def test_spmm_thread_count_invariant(orc):
     finally:
         orc.set_threads(1)
 
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+@pytest.mark.parametrize("threads", [1, 3])
+@pytest.mark.parametrize("shape,density,ncols", [((700, 300), 0.03, 37), ((300, 900), 0.02, 200),
+                                                 ((50, 40), 0.3, 1)])
+def test_loop_order_restatements_are_bitwise(orc, threads, shape, density, ncols):
+    """The row-outer spmm / spmm_transpose and the register-tiled Gram give
+    the same bits as the loops written in the reference (sparse_matrix.hpp:
+    195-203, :229-237; the panelled rankUpdate order): only the loop nesting
+    changes, never any entry's operation sequence. Zeros, signed zeros and
+    the y == 0 skip included."""
+    m, n = shape
+    A = orc.Csr.random_sparse(m, n, density, 11)
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((n, ncols))
+    X[rng.random(X.shape) < 0.15] = 0.0
+    Y = rng.standard_normal((m, ncols))
+    Y[rng.random(Y.shape) < 0.2] = 0.0
+    Y[: min(5, m)] = -0.0
+    orc.set_threads(threads)
+    try:
+        assert np.array_equal(_bits(orc.spmm(A, X)), _bits(orc.spmm(A, X, literal=True)))
+        assert np.array_equal(_bits(orc.spmm_transpose(A, Y)), _bits(orc.spmm_transpose(A, Y, literal=True)))
+        W = rng.standard_normal((max(m, 600), min(ncols, 45)))
+        tri = np.tril_indices(W.shape[1])
+        assert np.array_equal(_bits(orc.gram_lower(W)[tri]), _bits(orc.gram_lower(W, literal=True)[tri]))
+    finally:
+        orc.set_threads(1)
+
 # --------------------------------------------------------- test_dense_kernels
 
 
