@@ -15,7 +15,7 @@ synthetic CSR (SURVEY §8d generators, seeded), Omega from PcaConfig::seed = 0.
   cpu_baseline: the CPU oracle (a faithful port of the reference, oracle/)
           on the box's host cores, rank 0 only.
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1]
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
        python bench.py --impl reference ...   (CPU reference arm)
 Multi-GPU (N > 1): launched by torchrun, one rank per GPU; frpcat row-block /
 frpca column-block shards with NCCL allreduce inside the library.
@@ -168,9 +168,20 @@ def ncu_traffic(config: str):
 
 # --------------------------------------------------------------------------- arms
 
-def cpu_reference_seconds(cfg, A_arrays, threads: int, budget_s: float = 30.0):
-    """Times the oracle (CPU port of the reference path) on the config's matrix.
-    Returns (seconds, sample description, threads)."""
+def config_dict(cfg, m, n, nnz):
+    """The workload, identical in both arms (the driver compares them)."""
+    return {"workload": cfg.name, "algorithm": cfg.algorithm, "rows": int(m), "cols": int(n), "nnz": int(nnz),
+            "k": cfg.k, "s": cfg.s, "q": cfg.q, "seed": 0, "matrix_seed": cfg.seed}
+
+
+REF_NOTE = ("oracle/ (C++ restatement of the reference path, bitwise equal for any thread count); the "
+            "reference's own kernels are single-threaded (proj/README.md:145-146), so a multi-core run of "
+            "the port makes the GPU/CPU ratio conservative")
+
+
+def cpu_reference_seconds(cfg, A_arrays, threads: int):
+    """Times the oracle (CPU port of the reference path) on the config's matrix:
+    one full run. Returns (seconds, sample description)."""
     import oracle
     oracle.build()
     oracle.set_threads(threads)
@@ -180,35 +191,52 @@ def cpu_reference_seconds(cfg, A_arrays, threads: int, budget_s: float = 30.0):
     t0 = time.perf_counter()
     oracle.pca(A, algo, cfg.k, cfg.s, cfg.q, seed=0)
     dt = time.perf_counter() - t0
-    return dt, f"full {cfg.name} frpca run (k={cfg.k}, s={cfg.s}, q={cfg.q}) on the oracle"
+    return dt, (f"one full {cfg.name} {cfg.algorithm} run (k={cfg.k}, s={cfg.s}, q={cfg.q}) on the oracle, "
+                f"{threads} threads")
 
 
 def run_reference_arm(args, cfg):
+    """The reference's CPU path (the oracle port: the reference itself cannot
+    be built, Eigen is absent) on the same matrix and config.
+    Each step is one full run; the steps stop early when the next one would
+    exceed --ref-budget seconds (at least one step always runs), and the line
+    says how many ran."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from paper_1810_06825_b200 import synth
     threads = os.cpu_count() or 1
-    scale = args.ref_scale
-    A = synth.generate(cfg.name, scale=scale)
+    A = synth.generate(cfg.name)
+    m, n, rp = A[0], A[1], A[2]
     times = []
+    t_start = time.perf_counter()
+    warm_done = 0
     for it in range(args.warmup + args.steps):
+        elapsed = time.perf_counter() - t_start
+        est = statistics.mean(times) if times else 0.0
+        if times and elapsed + est > args.ref_budget:
+            break
         dt, sample = cpu_reference_seconds(cfg, A, threads)
-        if it >= args.warmup:
-            times.append(dt / scale if scale != 1.0 else dt)
+        if it < args.warmup and elapsed + 2 * dt < args.ref_budget / 2:
+            warm_done += 1
+            continue
+        times.append(dt)
     v = statistics.mean(times)
-    if scale != 1.0:
-        sample = f"{cfg.name} scaled x{scale} ({A[0]}x{A[1]}, nnz={int(A[2][-1])}), extrapolated linearly"
     line = {
         "impl": "reference", "metric": "frPCA seconds to top-k PCs", "value": round(v, 6), "unit": "s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1e3, 3),
+        "n_gpus": world, "steps": len(times), "warmup": warm_done, "steps_requested": args.steps,
+        "warmup_requested": args.warmup, "ms_per_step": round(v * 1e3, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, SURVEY §8d)",
-        "config": {"workload": cfg.name, "algorithm": cfg.algorithm, "k": cfg.k, "s": cfg.s, "q": cfg.q},
+        "config": config_dict(cfg, m, n, rp[-1]),
         "cpu_baseline": {"value": round(v, 6), "unit": "s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "note": REF_NOTE},
         "e2e": {"value": round(v, 6), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "statistic": "mean of steps",
     }
+    if len(times) < args.steps:
+        line["steps_note"] = (f"{len(times)} of {args.steps} steps: each is a full {cfg.name} run; the arm stops "
+                              f"before exceeding {args.ref_budget:.0f} s")
     print(json.dumps(line), flush=True)
     return 0
 
@@ -385,11 +413,10 @@ def run_gpu_arm(args, cfg):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(value_s * 1e3, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, SURVEY §8d)",
-        "config": {"workload": cfg.name, "algorithm": cfg.algorithm, "rows": m, "cols": n,
-                   "nnz": int(rp[-1]), "k": cfg.k, "s": cfg.s, "q": cfg.q, "seed": 0,
-                   "parallelism": f"{'row' if algo == _lib.ALGO_FRPCAT else 'col'}-block x{world}",
-                   "l2": "flushed between timed steps (256 MB write)",
-                   "omega": "host libstdc++" if args.host_omega else "device (bit-compatible)"},
+        "config": config_dict(cfg, m, n, rp[-1]),
+        "parallelism": f"{'row' if algo == _lib.ALGO_FRPCAT else 'col'}-block x{world}",
+        "l2": "flushed between timed steps (256 MB write)",
+        "omega": "host libstdc++" if args.host_omega else "device (bit-compatible)",
         "roofline": {"bound": "hbm", "kernel": "spmm (K1 A*X + K2 A^T*Y)",
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "peak_kind": peak_kind,
@@ -415,7 +442,7 @@ def run_gpu_arm(args, cfg):
         threads = os.cpu_count() or 1
         cpu_s, sample = cpu_reference_seconds(cfg, A_arrays, threads)
         line["cpu_baseline"] = {"value": round(cpu_s, 3), "unit": "s", "cores": threads,
-                                "kind": "port", "sample": sample}
+                                "kind": "port", "sample": sample, "note": REF_NOTE}
     if rank == 0:
         print(json.dumps(line), flush=True)
     for p in pinned:
@@ -425,18 +452,35 @@ def run_gpu_arm(args, cfg):
     return 0
 
 
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: start N ranks with torchrun on
+    this node (127.0.0.1 rendezvous) and pass the same arguments through."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=0)
-    ap.add_argument("--config", default="C1", choices=["C0", "C1", "C2", "C3", "C4"])
+    # C3 (the AMiner shape, PAPER.md:531) is the largest config frpcat serves
+    # on one GPU: the north_star's "largest config"; C4 is the frpca one
+    ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--host-omega", action="store_true")
-    ap.add_argument("--ref-scale", type=float, default=1.0)
+    ap.add_argument("--ref-budget", type=float, default=900.0,
+                    help="seconds the reference arm may spend on its steps")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
     from paper_1810_06825_b200.synth import CONFIGS
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
