@@ -80,6 +80,40 @@ int frpca_nccl_unique_id(void* out128);
 int frpca_ctx_create_dist(int device, int rank, int world, const void* nccl_id128,
                           frpca_ctx** out);
 int frpca_ctx_destroy(frpca_ctx* ctx);
+
+/* Single-process multi-GPU (the reference's callers are single-process,
+ * frpca_cli.cpp:158-183): one context (rank) per listed device. Distinct
+ * devices exchange through NCCL (ncclCommInitAll); a device listed more than
+ * once selects the host-staged loopback collective (ranks sharing a GPU, for
+ * testing the sharded path on one device). comm: FRPCA_COMM_*. */
+#define FRPCA_COMM_AUTO 0
+#define FRPCA_COMM_NCCL 1
+#define FRPCA_COMM_LOOPBACK 2
+typedef struct frpca_group frpca_group;
+int frpca_group_create(const int* devices, int ndev, int comm, frpca_group** out);
+int frpca_group_size(const frpca_group* g, int* n);
+/* the rank's context (owned by the group): shards can also be uploaded and run
+ * per rank from the caller's own threads (frpca_dmat_upload_shard, frpca_run) */
+int frpca_group_ctx(frpca_group* g, int rank, frpca_ctx** out);
+int frpca_group_destroy(frpca_group* g);
+/* frpca / frpcat / auto over the group from a host CSR: row blocks (frpcat) or
+ * column blocks (frpca) from frpca_shard_cuts, one host thread per rank; U, S,
+ * V are the caller's full column-major matrices (rows x k, k, cols x k).
+ * Errors as frpca_run. */
+int frpca_group_run_csr(frpca_group* g, int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                        const int64_t* col_idx, const double* values, int algorithm, const frpca_config* cfg,
+                        double* U, double* S, double* V, frpca_stats* stats, int* dispatched);
+
+/* Shard plan (host only, no device): world + 1 boundaries of row blocks
+ * (col_shard = 0; balanced by nnz + rows) or column blocks (col_shard = 1;
+ * balanced by column nnz + 1). frpca_shard_cols extracts the local CSR of
+ * columns [c0, c1) with local column ids (capacity from frpca_shard_cols_count). */
+int frpca_shard_cuts(int64_t rows, int64_t cols, const int64_t* row_ptr, const int64_t* col_idx, int32_t col_shard,
+                     int32_t world, int64_t* cuts);
+int frpca_shard_cols_count(int64_t rows, const int64_t* row_ptr, const int64_t* col_idx, int64_t c0, int64_t c1,
+                           int64_t* nnz_local);
+int frpca_shard_cols(int64_t rows, const int64_t* row_ptr, const int64_t* col_idx, const double* values, int64_t c0,
+                     int64_t c1, int64_t* l_row_ptr, int64_t* l_col_idx, double* l_values);
 int frpca_ctx_sync(frpca_ctx* ctx);
 /* Pinned host memory helpers (for zero-staging host buffers). */
 int frpca_host_alloc(uint64_t bytes, void** out);

@@ -403,21 +403,49 @@ static Mat lu_basis(const Mat& M) {
         }
         const Index tcols = l - jb - bw;                                 // :96-105
         if (tcols > 0) {
-            // U12 = L11^{-1} A12 (unit lower forward substitution, :98-100)
-            for (Index c = jb + bw; c < l; ++c)
-                for (Index i = jb; i < jb + bw; ++i) {
-                    double acc = W(i, c);
-                    for (Index t = jb; t < i; ++t) acc -= W(i, t) * W(t, c);
-                    W(i, c) = acc;
+            // U12 = L11^{-1} A12 (:98-100) in the order of Eigen's
+            // triangular_solve_matrix (unit lower, column-major): the block is
+            // cut into small panels of SPW rows; inside a small panel each
+            // solved entry b is subtracted from the panel rows below it, one
+            // product at a time (r -= b * l); rows below the small panel get
+            // the panel's products summed first (GEBP, from 0.0) and then
+            // subtracted once. SPW = max(mr, nr) of Eigen's gebp_traits for
+            // double on SSE2 (x86-64 without -march, the reference's flags):
+            // mr = nr = 4. (An assumption about the un-vendored Eigen 3.3/3.4.)
+            constexpr Index SPW = 4;
+            parallel_for(jb + bw, l, [&](Index c) {
+                double* wc = W.col(c);
+                for (Index k1 = 0; k1 < bw; k1 += SPW) {
+                    const Index pw = std::min(SPW, bw - k1), p0 = jb + k1;
+                    for (Index k = 0; k < pw; ++k) {
+                        const Index i = p0 + k;
+                        const double b = wc[i];
+                        const double* li = W.col(i);
+                        for (Index r = i + 1; r < p0 + pw; ++r) wc[r] -= b * li[r];
+                    }
+                    for (Index r = p0 + pw; r < jb + bw; ++r) {
+                        double acc = 0.0;
+                        for (Index k = 0; k < pw; ++k) acc += W(r, p0 + k) * wc[p0 + k];
+                        wc[r] -= acc;
+                    }
                 }
-            // A22 -= L21 * U12 (:101-104)
+            });
+            // A22 -= L21 * U12 (:101-104): Eigen's GEBP forms every entry's
+            // bw-term product first (sequential over the depth, from 0.0) and
+            // adds it with alpha = -1, i.e. subtracts it once.
             const Index r0 = jb + bw;
             parallel_for(jb + bw, l, [&](Index c) {
                 double* wc = W.col(c);
-                for (Index t = jb; t < jb + bw; ++t) {
-                    const double u = W(t, c);
-                    const double* lt = W.col(t);
-                    for (Index i = r0; i < m; ++i) wc[i] -= lt[i] * u;
+                constexpr Index IB = 8;
+                for (Index i0 = r0; i0 < m; i0 += IB) {
+                    const Index ni = std::min(IB, m - i0);
+                    double acc[IB] = {};
+                    for (Index t = jb; t < jb + bw; ++t) {
+                        const double u = wc[t];
+                        const double* lt = W.col(t) + i0;
+                        for (Index a = 0; a < ni; ++a) acc[a] += lt[a] * u;
+                    }
+                    for (Index a = 0; a < ni; ++a) wc[i0 + a] -= acc[a];
                 }
             });
         }

@@ -369,3 +369,42 @@ def pca(A: Csr, algorithm: int, k: int, oversample: int = 5, passes: int = 2, se
     return dict(U=U, S=S, V=V, basis=basis, dispatched=disp.value,
                 stats=dict(sketch_seconds=stats[0], power_seconds=stats[1],
                            finalize_seconds=stats[2], passes_over_matrix=int(stats[3])))
+
+
+# ---------------------------------------------------------------- arbiter
+_ARB = os.path.join(_HERE, "_build", "libarbiter.so")
+_arb = None
+
+
+def arbiter_pca(rows: int, cols: int, row_ptr, col_idx, values, algorithm: int, k: int, oversample: int,
+                passes: int, seed: int = 0, threads: int | None = None):
+    """The same frpca / frpcat pipeline in 80-bit long double from the same
+    CSR and the same fp64 sketch (arbiter.cpp): the reference point for
+    judging two fp64 evaluations. Returns dict(U, S, V)."""
+    global _arb
+    if _arb is None:
+        if not os.path.exists(_ARB) or os.path.getmtime(_ARB) < os.path.getmtime(os.path.join(_HERE, "arbiter.cpp")):
+            subprocess.check_call(["make", "-s", "-C", _HERE, os.path.relpath(_ARB, _HERE)])
+        L = C.CDLL(_ARB)
+        L.arb_last_error.restype = C.c_char_p
+        L.arb_set_threads.argtypes = [C.c_int]
+        L.arb_pca.argtypes = [_i64, _i64, _lp, _lp, _dp, C.c_int, _i64, _i64, _i64, _dp, _dp, _dp, _dp]
+        _arb = L
+    l = k + oversample
+    if algorithm == FRPCAT:
+        orows, ocols = (l, rows) if passes % 2 == 0 else (cols, l)
+    else:
+        orows, ocols = (cols, l) if passes % 2 == 0 else (rows, l)
+    omega = gaussian_matrix(orows, ocols, mix_seed(seed, 0xA11CE))
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+    va = np.ascontiguousarray(values, dtype=np.float64)
+    U = np.empty((rows, k), order="F")
+    S = np.empty(k)
+    V = np.empty((cols, k), order="F")
+    _arb.arb_set_threads(int(threads or os.cpu_count() or 1))
+    rc = _arb.arb_pca(rows, cols, rp.ctypes.data_as(_lp), ci.ctypes.data_as(_lp), _d(va),
+                      1 if algorithm == FRPCAT else 0, k, oversample, passes, _d(omega), _d(U), _d(S), _d(V))
+    if rc != 0:
+        raise NumericalError(_arb.arb_last_error().decode())
+    return dict(U=U, S=S, V=V)

@@ -31,7 +31,7 @@ __all__ = [
     "frpca", "frpcat", "auto_pca", "basic_rpca", "basic_rpcat", "mix_seed", "kSketchStreamTag",
     "read_matrix_market", "load_matrix_market", "write_matrix_market", "IoError",
     "run_csr", "ErrorNorm", "low_rank_error", "best_rank_k_error", "pc_correlation", "projector_distance",
-    "AccuracyReport", "make_accuracy_report", "kDefaultOracleEntryLimit",
+    "AccuracyReport", "make_accuracy_report", "kDefaultOracleEntryLimit", "Group",
 ]
 
 kSketchStreamTag = 0xA11CE  # randsvd.hpp:63
@@ -157,6 +157,66 @@ class Context:
                                            C.byref(by), C.byref(fl)))
             out[name.value.decode()] = dict(launches=la.value, ms=ms.value, bytes=by.value, flops=fl.value)
         return out
+
+
+class Group:
+    """Single-process multi-GPU (frpca_group_*): one context (rank)
+    per listed device. Distinct devices exchange the A^T*Y / A*X and Gram
+    partials through NCCL; a device listed more than once selects the
+    host-staged loopback collective, which runs the sharded path on one GPU
+    (tests). `run` shards a host CSR (row blocks for frpcat, column blocks for
+    frpca) and returns the full SvdResult."""
+
+    def __init__(self, devices, comm: int = _lib.COMM_AUTO):
+        L = _lib.load()
+        dv = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _lib.check(L.frpca_group_create(dv, len(devices), comm, C.byref(h)))
+        self._h = h
+        self.devices = list(devices)
+
+    def __len__(self):
+        return len(self.devices)
+
+    def context_handle(self, rank: int) -> C.c_void_p:
+        """The rank's C context (owned by the group)."""
+        h = C.c_void_p()
+        _lib.check(_lib.load().frpca_group_ctx(self._h, rank, C.byref(h)))
+        return h
+
+    def run(self, A: "SparseMatrixCsr", cfg: PcaConfig, algorithm: "PcaAlgorithm" = None,
+            stats: RunStats | None = None) -> tuple[SvdResult, int]:
+        algo = _lib.ALGO_AUTO if algorithm is None else int(algorithm)
+        m, n = A.rows(), A.cols()
+        k = max(int(cfg.k), 0)
+        U = np.empty((m, k), order="F")
+        S = np.empty(k)
+        V = np.empty((n, k), order="F")
+        st = _lib.FrpcaStats()
+        disp = C.c_int(-1)
+        ccfg = cfg.to_c()
+        rp = np.ascontiguousarray(A.rowPtr(), dtype=np.int64)
+        ci = np.ascontiguousarray(A.colIdx(), dtype=np.int64)
+        va = np.ascontiguousarray(A.values(), dtype=np.float64)
+        _lib.check(_lib.load().frpca_group_run_csr(self._h, m, n, int(rp[-1]), _ptr(rp), _ptr(ci), _ptr(va), algo,
+                                                   C.byref(ccfg), _ptr(U), _ptr(S), _ptr(V), C.byref(st),
+                                                   C.byref(disp)))
+        if stats is not None:
+            stats.sketch_seconds, stats.power_seconds = st.sketch_seconds, st.power_seconds
+            stats.finalize_seconds = st.finalize_seconds
+            stats.passes_over_matrix = int(st.passes_over_matrix)
+        return SvdResult(U, S, V), disp.value
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.load().frpca_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 _default = None

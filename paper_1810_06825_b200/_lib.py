@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libfrpca_b200.so")
 OK, ERR_INVALID, ERR_IO, ERR_NUMERICAL, ERR_CUDA = 0, 2, 3, 4, 5
 ALGO_FRPCA, ALGO_FRPCAT, ALGO_AUTO, ALGO_BASIC_RPCA, ALGO_BASIC_RPCAT = 0, 1, 2, 3, 4
 FLAG_DEVICE_IO, FLAG_HOST_OMEGA = 1, 2
+COMM_AUTO, COMM_NCCL, COMM_LOOPBACK = 0, 1, 2
 
 _i64, _u64, _i32, _u32 = C.c_int64, C.c_uint64, C.c_int32, C.c_uint32
 _dp = C.POINTER(C.c_double)
@@ -39,6 +40,15 @@ SIGNATURES = {
     "frpca_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "frpca_ctx_create_dist": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(_vp)]),
     "frpca_ctx_destroy": (C.c_int, [_vp]),
+    "frpca_group_create": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_int, C.POINTER(_vp)]),
+    "frpca_group_size": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "frpca_group_ctx": (C.c_int, [_vp, C.c_int, C.POINTER(_vp)]),
+    "frpca_group_destroy": (C.c_int, [_vp]),
+    "frpca_group_run_csr": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, C.c_int, C.POINTER(FrpcaConfig),
+                                      _vp, _vp, _vp, C.POINTER(FrpcaStats), C.POINTER(C.c_int)]),
+    "frpca_shard_cuts": (C.c_int, [_i64, _i64, _vp, _vp, _i32, _i32, _vp]),
+    "frpca_shard_cols_count": (C.c_int, [_i64, _vp, _vp, _i64, _i64, _lp]),
+    "frpca_shard_cols": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "frpca_ctx_sync": (C.c_int, [_vp]),
     "frpca_host_alloc": (C.c_int, [_u64, C.POINTER(_vp)]),
     "frpca_host_free": (C.c_int, [_vp]),

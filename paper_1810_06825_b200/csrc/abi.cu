@@ -3,6 +3,7 @@
 // CUDA/NCCL/cuSOLVER failures -> 5 and keeps the message for
 // frpca_last_error(), which the C++ drop-in rethrows as the reference's
 // std::invalid_argument / frpca::NumericalError.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -49,6 +50,13 @@ void check_ctx(const frpca_ctx* c) { require(c != nullptr, "frpca_b200: null con
 
 struct frpca_ctx : fb::Ctx {};
 struct frpca_dmat : fb::DMat {};
+// Single-process multi-GPU: one context (rank) per listed device.
+struct frpca_group {
+    std::vector<frpca_ctx*> ctx;
+    std::vector<int> devices;
+    std::shared_ptr<fb::LoopbackGroup> loop;  // host-staged collective (a device listed twice)
+    int comm = 0;                             // FRPCA_COMM_NCCL / FRPCA_COMM_LOOPBACK
+};
 
 namespace fb {
 
@@ -167,6 +175,105 @@ int frpca_ctx_create_dist(int device, int rank, int world, const void* nccl_id12
         int st = frpca_ctx_create(device, out);
         if (st != FRPCA_OK) throw CudaError(g_err);
         comm_init(**out, rank, world, nccl_id128);
+    });
+}
+
+int frpca_group_create(const int* devices, int ndev, int comm, frpca_group** out) {
+    return guarded([&] {
+        require(devices != nullptr && ndev >= 1 && out != nullptr, "frpca_group_create: bad arguments");
+        require(comm == FRPCA_COMM_AUTO || comm == FRPCA_COMM_NCCL || comm == FRPCA_COMM_LOOPBACK,
+                "frpca_group_create: unknown collective");
+        std::vector<int> dv(devices, devices + ndev);
+        std::vector<int> sorted = dv;
+        std::sort(sorted.begin(), sorted.end());
+        const bool dup = std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end();
+        require(!(dup && comm == FRPCA_COMM_NCCL), "frpca_group_create: NCCL needs distinct devices");
+        const int kind = (comm == FRPCA_COMM_LOOPBACK || (comm == FRPCA_COMM_AUTO && dup)) ? FRPCA_COMM_LOOPBACK
+                                                                                          : FRPCA_COMM_NCCL;
+        auto g = std::make_unique<frpca_group>();
+        g->devices = dv;
+        g->comm = kind;
+        try {
+            for (int r = 0; r < ndev; ++r) {
+                frpca_ctx* c = nullptr;
+                if (frpca_ctx_create(dv[size_t(r)], &c) != FRPCA_OK) throw CudaError(g_err);
+                g->ctx.push_back(c);
+            }
+            if (ndev > 1) {
+                if (kind == FRPCA_COMM_LOOPBACK) {
+                    g->loop = loopback_group(ndev);
+                    for (int r = 0; r < ndev; ++r) comm_attach_loopback(*g->ctx[size_t(r)], g->loop, r);
+                } else {
+                    std::vector<Ctx*> cs(g->ctx.begin(), g->ctx.end());
+                    comm_init_all(cs, dv);
+                }
+            }
+        } catch (...) {
+            for (auto* c : g->ctx) frpca_ctx_destroy(c);
+            throw;
+        }
+        *out = g.release();
+    });
+}
+
+int frpca_group_size(const frpca_group* g, int* n) {
+    return guarded([&] {
+        require(g != nullptr && n != nullptr, "frpca_group_size: null argument");
+        *n = int(g->ctx.size());
+    });
+}
+
+int frpca_group_ctx(frpca_group* g, int rank, frpca_ctx** out) {
+    return guarded([&] {
+        require(g != nullptr && out != nullptr, "frpca_group_ctx: null argument");
+        require(rank >= 0 && rank < int(g->ctx.size()), "frpca_group_ctx: rank out of range");
+        *out = g->ctx[size_t(rank)];
+    });
+}
+
+int frpca_group_destroy(frpca_group* g) {
+    return guarded([&] {
+        if (!g) return;
+        for (auto* c : g->ctx) frpca_ctx_destroy(c);
+        delete g;
+    });
+}
+
+int frpca_shard_cuts(int64_t rows, int64_t cols, const int64_t* row_ptr, const int64_t* col_idx, int32_t col_shard,
+                     int32_t world, int64_t* cuts) {
+    return guarded([&] {
+        require(rows >= 0 && cols >= 0 && row_ptr != nullptr && cuts != nullptr, "frpca_shard_cuts: bad arguments");
+        require(!col_shard || row_ptr[rows] == 0 || col_idx != nullptr, "frpca_shard_cuts: bad arguments");
+        shard_cuts(rows, cols, row_ptr, col_idx, col_shard, world, cuts);
+    });
+}
+
+int frpca_shard_cols_count(int64_t rows, const int64_t* row_ptr, const int64_t* col_idx, int64_t c0, int64_t c1,
+                           int64_t* nnz_local) {
+    return guarded([&] {
+        require(row_ptr != nullptr && nnz_local != nullptr && c0 <= c1, "frpca_shard_cols: bad arguments");
+        int64_t t = 0;
+        for (int64_t i = 0; i < rows; ++i) {
+            const int64_t* a = col_idx + row_ptr[i];
+            const int64_t* b = col_idx + row_ptr[i + 1];
+            t += int64_t(std::lower_bound(a, b, c1) - std::lower_bound(a, b, c0));
+        }
+        *nnz_local = t;
+    });
+}
+
+int frpca_shard_cols(int64_t rows, const int64_t* row_ptr, const int64_t* col_idx, const double* values, int64_t c0,
+                     int64_t c1, int64_t* l_row_ptr, int64_t* l_col_idx, double* l_values) {
+    return guarded([&] {
+        require(row_ptr != nullptr && l_row_ptr != nullptr && c0 <= c1, "frpca_shard_cols: bad arguments");
+        std::vector<int64_t> lrp, lci;
+        std::vector<double> lva;
+        shard_extract_cols(rows, row_ptr, col_idx, values, c0, c1, lrp, lci, lva);
+        std::memcpy(l_row_ptr, lrp.data(), sizeof(int64_t) * lrp.size());
+        if (!lci.empty()) {
+            std::memcpy(l_col_idx, lci.data(), sizeof(int64_t) * lci.size());
+            std::memcpy(l_values, lva.data(), sizeof(double) * lva.size());
+        }
     });
 }
 
@@ -606,6 +713,92 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
                 "frpca_run: unknown algorithm");
         run_algorithm(*c, *M, a, stats, algo);
         FB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// Sharded run of a host CSR over a group (the single-process
+// callers of the reference, frpca_cli.cpp:158-183, with every GPU of the box):
+// frpcat takes row blocks, frpca column blocks (shard_cuts); each rank uploads
+// its shard and runs on its own host thread; the collectives sum the partials.
+// U / V / S land in the caller's full column-major matrices: each rank writes
+// its rows of the sharded factor, rank 0 the replicated one and S.
+int frpca_group_run_csr(frpca_group* g, int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                        const int64_t* col_idx, const double* values, int algorithm, const frpca_config* cfg,
+                        double* U, double* S, double* V, frpca_stats* stats, int* dispatched) {
+    return guarded([&] {
+        require(g != nullptr && cfg != nullptr && row_ptr != nullptr, "frpca_run: null argument");
+        require(rows >= 0 && cols >= 0 && nnz == row_ptr[rows], "frpca_group_run_csr: row_ptr[rows] must equal nnz");
+        require(!(cfg->flags & FRPCA_FLAG_DEVICE_IO), "frpca_group_run_csr: host buffers only");
+        int algo = algorithm;
+        if (algo == FRPCA_ALGO_AUTO) algo = (rows < cols) ? FRPCA_ALGO_FRPCA : FRPCA_ALGO_FRPCAT;
+        require(algo == FRPCA_ALGO_FRPCA || algo == FRPCA_ALGO_FRPCAT,
+                "frpca_group_run_csr: only frpca / frpcat run sharded");
+        if (dispatched) *dispatched = algo;
+        const int world = int(g->ctx.size());
+        const int col_shard = algo == FRPCA_ALGO_FRPCA ? 1 : 0;
+        std::vector<int64_t> cuts(size_t(world) + 1);
+        shard_cuts(rows, cols, row_ptr, col_idx, col_shard, world, cuts.data());
+        std::vector<std::exception_ptr> errs(static_cast<size_t>(world));
+        std::vector<frpca_stats> st(static_cast<size_t>(world));
+        auto rank_main = [&](int r) {
+            frpca_ctx* c = g->ctx[size_t(r)];
+            try {
+                std::lock_guard<std::mutex> lk(c->mu);
+                FB_CUDA(cudaSetDevice(c->device));
+                const int64_t a0 = cuts[size_t(r)], a1 = cuts[size_t(r) + 1];
+                std::vector<int64_t> lrp, lci;
+                std::vector<double> lva;
+                const int64_t *prp, *pci;
+                const double* pva;
+                int64_t lrows, lcols;
+                if (!col_shard) {
+                    lrp.resize(size_t(a1 - a0) + 1);
+                    for (int64_t i = a0; i <= a1; ++i) lrp[size_t(i - a0)] = row_ptr[i] - row_ptr[a0];
+                    prp = lrp.data();
+                    pci = col_idx + row_ptr[a0];
+                    pva = values + row_ptr[a0];
+                    lrows = a1 - a0;
+                    lcols = cols;
+                } else {
+                    shard_extract_cols(rows, row_ptr, col_idx, values, a0, a1, lrp, lci, lva);
+                    prp = lrp.data();
+                    pci = lci.data();
+                    pva = lva.data();
+                    lrows = rows;
+                    lcols = a1 - a0;
+                }
+                std::unique_ptr<frpca_dmat> M(new frpca_dmat);
+                M->ctx = c;
+                M->grows = rows;
+                M->gcols = cols;
+                M->offset = a0;
+                M->col_shard = col_shard;
+                dcsr_upload_build(*c, *M, lrows, lcols, prp[lrows], prp, pci, pva);
+                RunArgs a;
+                a.cfg = *cfg;
+                if (!col_shard) {   // frpcat: U row-sharded, V replicated
+                    a.U = U ? U + a0 : nullptr;
+                    a.u_ld = rows;
+                    a.V = r == 0 ? V : nullptr;
+                } else {            // frpca: V row-sharded (columns of A), U replicated
+                    a.V = V ? V + a0 : nullptr;
+                    a.v_ld = cols;
+                    a.U = r == 0 ? U : nullptr;
+                }
+                a.S = r == 0 ? S : nullptr;
+                run_algorithm(*c, *M, a, &st[size_t(r)], algo);
+                FB_CUDA(cudaStreamSynchronize(c->stream));
+            } catch (...) {
+                errs[size_t(r)] = std::current_exception();
+                if (g->loop) loopback_fail(*g->loop);
+            }
+        };
+        std::vector<std::thread> th;
+        for (int r = 0; r < world; ++r) th.emplace_back(rank_main, r);
+        for (auto& t : th) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+        if (stats) *stats = st[0];
     });
 }
 

@@ -150,6 +150,19 @@ static void copy_out(Ctx& c, const RunArgs& a, double* dst_user, const double* s
                             a.device_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c.stream));
 }
 
+// column-major rows x k (ld = rows) -> the caller's matrix with leading dimension ld
+static void copy_out_ld(Ctx& c, const RunArgs& a, double* dst_user, int64_t ld, const double* src_dev, int64_t rows,
+                        int64_t k, cudaStream_t s) {
+    if (!dst_user || rows == 0 || k == 0) return;
+    const cudaMemcpyKind kind = a.device_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (ld == 0 || ld == rows) {
+        FB_CUDA(cudaMemcpyAsync(dst_user, src_dev, sizeof(double) * rows * k, kind, s));
+        return;
+    }
+    FB_CUDA(cudaMemcpy2DAsync(dst_user, sizeof(double) * ld, src_dev, sizeof(double) * rows, sizeof(double) * rows,
+                              size_t(k), kind, s));
+}
+
 // Q (row-major r x l) -> column-major output basis (RunStats::basis).
 static void basis_out(Ctx& c, const RunArgs& a, const double* Q, int64_t r, int64_t l) {
     if (!a.basis) return;
@@ -171,6 +184,7 @@ struct OutProduct {
     const double* M;  // l x k
     double* dev;      // rows x k, column-major
     double* user;     // U or V of the call (may be null)
+    int64_t ld;       // leading dimension of `user` (0: rows)
 };
 
 static void output_products(Ctx& c, const RunArgs& a, int64_t l, int64_t k, OutProduct u, OutProduct v,
@@ -181,8 +195,8 @@ static void output_products(Ctx& c, const RunArgs& a, int64_t l, int64_t k, OutP
         gemm_device(c, u.W, u.rows, l, u.M, k, u.dev, std::max<int64_t>(u.rows, 1), true);
         gemm_device(c, v.W, v.rows, l, v.M, k, v.dev, std::max<int64_t>(v.rows, 1), true);
         e.singular_values(c, s, int(k), true, So);
-        copy_out(c, a, a.U, u.dev, u.rows * k);
-        copy_out(c, a, a.V, v.dev, v.rows * k);
+        copy_out_ld(c, a, u.user, u.ld, u.dev, u.rows, k, S);
+        copy_out_ld(c, a, v.user, v.ld, v.dev, v.rows, k, S);
         copy_out(c, a, a.S, So, k);
         return;
     }
@@ -200,8 +214,7 @@ static void output_products(Ctx& c, const RunArgs& a, int64_t l, int64_t k, OutP
     gemm_device(c, sml.W, sml.rows, l, sml.M, k, sml.dev, std::max<int64_t>(sml.rows, 1), true);
     e.singular_values(c, s, int(k), true, So);
     fence(S, c.copy);
-    if (sml.user && sml.rows * k)
-        FB_CUDA(cudaMemcpyAsync(sml.user, sml.dev, sizeof(double) * sml.rows * k, cudaMemcpyDeviceToHost, c.copy));
+    copy_out_ld(c, a, sml.user, sml.ld, sml.dev, sml.rows, k, c.copy);
     if (a.S && k) FB_CUDA(cudaMemcpyAsync(a.S, So, sizeof(double) * k, cudaMemcpyDeviceToHost, c.copy));
     const int64_t R = big.rows;
     static const int64_t maxch = [] {
@@ -215,7 +228,8 @@ static void output_products(Ctx& c, const RunArgs& a, int64_t l, int64_t k, OutP
         gemm_device(c, big.W + r0 * l, r1 - r0, l, big.M, k, big.dev + r0, R, true);
         if (!big.user || !k) continue;
         fence(S, c.copy);
-        FB_CUDA(cudaMemcpy2DAsync(big.user + r0, sizeof(double) * R, big.dev + r0, sizeof(double) * R,
+        const int64_t ldu = big.ld ? big.ld : R;
+        FB_CUDA(cudaMemcpy2DAsync(big.user + r0, sizeof(double) * ldu, big.dev + r0, sizeof(double) * R,
                                   sizeof(double) * (r1 - r0), size_t(k), cudaMemcpyDeviceToHost, c.copy));
     }
     fence(c.copy, S);  // the run's final synchronisation covers the copies
@@ -294,8 +308,8 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     DBuf<double>& Uo = c.slot(4, size_t(std::max<int64_t>(m, 1) * k));
     DBuf<double>& Vo = c.slot(5, size_t(n * k));
     DBuf<double> So(size_t(k), S);
-    output_products(c, a, l, k, {bufM.get(), m, MU.get(), Uo.get(), a.U}, {Q.get(), n, MV.get(), Vo.get(), a.V}, e,
-                    int(s), So.get());
+    output_products(c, a, l, k, {bufM.get(), m, MU.get(), Uo.get(), a.U, a.u_ld},
+                    {Q.get(), n, MV.get(), Vo.get(), a.V, a.v_ld}, e, int(s), So.get());
     basis_out(c, a, Q.get(), n, l);
     T.mark(3);
     FB_CUDA(cudaStreamSynchronize(S));
@@ -379,8 +393,8 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     DBuf<double>& Uo = c.slot(4, size_t(m * k));
     DBuf<double>& Vo = c.slot(5, size_t(std::max<int64_t>(n, 1) * k));
     DBuf<double> So(size_t(k), S);
-    output_products(c, a, l, k, {Q.get(), m, MU.get(), Uo.get(), a.U}, {bufN.get(), n, MV.get(), Vo.get(), a.V}, e,
-                    int(s), So.get());
+    output_products(c, a, l, k, {Q.get(), m, MU.get(), Uo.get(), a.U, a.u_ld},
+                    {bufN.get(), n, MV.get(), Vo.get(), a.V, a.v_ld}, e, int(s), So.get());
     basis_out(c, a, Q.get(), m, l);
     T.mark(3);
     FB_CUDA(cudaStreamSynchronize(S));

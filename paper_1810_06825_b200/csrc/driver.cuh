@@ -10,6 +10,10 @@ struct RunArgs {
     const double* omega = nullptr;
     int64_t omega_rows = 0, omega_cols = 0;
     double *U = nullptr, *S = nullptr, *V = nullptr, *basis = nullptr;
+    // leading dimensions of U / V in the caller's memory (0: their row count);
+    // a group run writes each rank's rows of the sharded factor into the
+    // caller's full matrix
+    int64_t u_ld = 0, v_ld = 0;
     bool device_io = false;
     // Omega generated ahead (frpca_run_csr), moved into the run's slot by the
     // first sketch_into of the call; a repeated call (run_algorithm's retry)
@@ -74,7 +78,22 @@ double projector_distance_device(Ctx& c, int64_t m, int64_t k1, const double* Q1
 
 // comm.cu: in-place sum over ranks (no-op on one GPU).
 void allreduce_sum(Ctx& c, double* x, int64_t count);
-void comm_init(Ctx& c, int rank, int world, const void* id128);
+void comm_init(Ctx& c, int rank, int world, const void* id128);       // NCCL, one process per GPU
+void comm_init_all(std::vector<Ctx*>& ctxs, const std::vector<int>& devices);  // NCCL, one process
+struct LoopbackGroup;
+std::shared_ptr<LoopbackGroup> loopback_group(int world);
+void comm_attach_loopback(Ctx& c, const std::shared_ptr<LoopbackGroup>& g, int rank);
+void loopback_fail(LoopbackGroup& g);
+
+// group.cu: host-side shard plan of a CSR over `world` ranks.
+// Row blocks (frpcat) balanced by nnz + rows; column blocks (frpca) balanced by
+// column nnz + 1. cuts: world + 1 boundaries.
+void shard_cuts(int64_t rows, int64_t cols, const int64_t* row_ptr, const int64_t* col_idx, int col_shard,
+                int world, int64_t* cuts);
+// the local CSR of columns [c0, c1) (local column ids); row_ptr rows + 1
+void shard_extract_cols(int64_t rows, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                        int64_t c0, int64_t c1, std::vector<int64_t>& lrp, std::vector<int64_t>& lci,
+                        std::vector<double>& lva);
 void comm_destroy(Ctx& c);
 void comm_unique_id(void* out128);
 

@@ -13,9 +13,15 @@
 #include "common.cuh"
 #include "mtx.hpp"
 
-typedef struct ncclComm* ncclComm_t;
-
 namespace fb {
+
+struct Ctx;
+// In-place fp64 sum over the ranks of a sharded run (comm.cu: NCCL or the
+// host-staged loopback of contexts in one process), ordered on stream s.
+struct Collective {
+    virtual ~Collective() = default;
+    virtual void allreduce_sum(Ctx& c, double* x, int64_t count, cudaStream_t s) = 0;
+};
 
 // One unit of SpMM work for one warp (see spmm.cu). r1 >= 0: the consecutive
 // short rows [r0, r1), each summed sequentially in CSR order straight into the
@@ -86,7 +92,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cusolverDnHandle_t solver = nullptr;
     int rank = 0, world = 1;
-    ncclComm_t comm = nullptr;
+    std::shared_ptr<Collective> coll;  // world > 1
     int num_sms = 148;
     std::mutex mu;  // the ABI serialises calls on one context
     cudaEvent_t timer_a = nullptr, timer_b = nullptr;

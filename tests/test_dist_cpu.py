@@ -159,3 +159,26 @@ def test_shard_partitions_cover_and_balance(world):
         assert lrp[-1] == lci.size and (lci.size == 0 or (lci.min() >= 0 and lci.max() < c1 - c0))
         nnz += lci.size
     assert nnz == rp[-1]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_library_shard_plan_matches_balance_rule(world):
+    """The library's shard plan (csrc/group.cu through the C ABI) is the
+    balance rule stated in numpy: row cut r = first row whose prefix weight
+    (nnz + rows) reaches r/world of the total; column cut r = first column
+    whose prefix weight (column nnz + 1) reaches r/world."""
+    from paper_1810_06825_b200 import shard as sh
+    from paper_1810_06825_b200 import synth
+    m, n, rp, ci, va = synth.generate("C1", scale=0.02)
+    w = rp.astype(np.float64) + np.arange(m + 1)
+    rows = [0] + [int(np.searchsorted(w, w[-1] * r / world)) for r in range(1, world)] + [m]
+    assert sh.row_cuts(rp, world) == rows
+    pref = np.concatenate([[0.0], np.cumsum(np.bincount(ci, minlength=n).astype(np.float64) + 1.0)])
+    cols = [0] + [int(np.searchsorted(pref, pref[-1] * r / world)) for r in range(1, world)] + [n]
+    assert sh.col_cuts(rp, ci, n, world) == cols
+    # the extracted column blocks are the columns' entries, in row order
+    c0, c1 = cols[world // 2], cols[world // 2 + 1]
+    _, _, lrp, lci, lva = sh.shard_cols(rp, ci, va, n, world, world // 2)
+    keep = (ci >= c0) & (ci < c1)
+    assert np.array_equal(lci, ci[keep] - c0) and np.array_equal(lva, va[keep])
+    assert np.array_equal(np.diff(lrp), np.add.reduceat(keep.astype(np.int64), rp[:-1]) * (np.diff(rp) > 0))

@@ -1,8 +1,14 @@
-"""BASELINE sizes against the oracle: C0 (the reference's CPU-runnable case)
-and C1 (the bench workload) at full size, Omega from seed 0, through the
-product path (tools/parity_full.py; C2-C4 are run by the same tool and their
-results committed under profiles/). Bars: top-k sigma within 1e-10 relative,
-||UU^T - U'U'^T||_2 and ||VV^T - V'V'^T||_2 within 1e-8, q passes."""
+"""BASELINE sizes against the oracle through the product path
+(tools/parity_full.py), Omega from seed 0: C0 (the reference's CPU-runnable
+case), C1, C2 and C3 (the bench workload, 12.9M x 324k, 400M nnz) at full
+size. Bars: top-k sigma within 1e-10 relative, ||UU^T - U'U'^T||_2 and
+||VV^T - V'V'^T||_2 within 1e-8, q passes.
+
+C2 (Poisson counts, l = 150, q = 5) sits below those bars for ANY fp64
+evaluation: the oracle itself is ~3e-10 / ~2e-8 from the same algorithm in
+80-bit long double (oracle/arbiter.cpp). There the bar is that the GPU result
+is at least as close to the long-double arbiter as the oracle is, on sigma and
+on both subspaces (the arbiter criterion)."""
 import os
 import sys
 
@@ -13,7 +19,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["C0", "C1"])
+@pytest.mark.parametrize("name", ["C0", "C1", "C3"])
 def test_fullsize_parity(fb, orc, name):
     from parity_full import run
     r = run(name)
@@ -21,3 +27,14 @@ def test_fullsize_parity(fb, orc, name):
     assert r["sigma_rel"] <= 1e-10
     assert r["subspace_U"] <= 1e-8 and r["subspace_V"] <= 1e-8
     assert r["passes_gpu"] == r["q"] == r["passes_oracle"]
+
+
+def test_fullsize_parity_c2_arbiter(fb, orc):
+    from parity_full import run
+    r = run("C2", arbiter=True)
+    print(r)
+    assert r["passes_gpu"] == r["q"] == r["passes_oracle"]
+    a = r["arbiter"]
+    if not r["pass_direct"]:
+        for key in ("sigma_rel", "subspace_U", "subspace_V"):
+            assert a["gpu_vs_arbiter"][key] <= a["oracle_vs_arbiter"][key], (key, a)

