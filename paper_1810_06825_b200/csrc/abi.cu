@@ -738,6 +738,7 @@ int frpca_group_run_csr(frpca_group* g, int64_t rows, int64_t cols, int64_t nnz,
         const int col_shard = algo == FRPCA_ALGO_FRPCA ? 1 : 0;
         std::vector<int64_t> cuts(size_t(world) + 1);
         shard_cuts(rows, cols, row_ptr, col_idx, col_shard, world, cuts.data());
+        if (g->loop) loopback_reset(*g->loop);  // a failed earlier run left the flag set
         std::vector<std::exception_ptr> errs(static_cast<size_t>(world));
         std::vector<frpca_stats> st(static_cast<size_t>(world));
         auto rank_main = [&](int r) {

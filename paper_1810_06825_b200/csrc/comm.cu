@@ -137,6 +137,13 @@ struct LoopbackGroup {
 
 void loopback_fail(LoopbackGroup& g) { g.fail(); }
 
+// called with every rank idle (the start of a group run)
+void loopback_reset(LoopbackGroup& g) {
+    std::lock_guard<std::mutex> lk(g.mu);
+    g.failed = false;
+    g.arrived = 0;
+}
+
 namespace {
 
 struct LoopbackColl final : Collective {

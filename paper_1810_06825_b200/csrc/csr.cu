@@ -212,57 +212,24 @@ __global__ void k_col_counts(const int64_t* __restrict__ trp, int64_t n, int32_t
     }
 }
 
-__global__ void k_rank_map(const int32_t* __restrict__ hot, int nhot, int32_t* __restrict__ rank_of) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nhot; r += gridDim.x * blockDim.x)
-        rank_of[hot[r]] = r;
-}
-
-__global__ void k_encode_hot(int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ rank_of) {
-    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < nnz;
-         p += int64_t(gridDim.x) * blockDim.x) {
-        const int32_t r = rank_of[col[p]];
-        if (r >= 0) col[p] = -(r + 1);
-    }
-}
-
-// Rank the columns of A by popularity (nnz, ties to the lower id) and encode
-// the top kHot in A's column ids, for the shared-memory staging of A*X.
-void build_hot(Ctx& c, DCsr& A, const DCsr& T) {
-    const int64_t n = A.cols;
-    A.nhot = 0;
-    if (n == 0 || A.nnz == 0) return;
-    cudaStream_t s = c.stream;
-    DBuf<int32_t> cnt(size_t(n), s), ids(size_t(n), s), cnt_s(size_t(n), s), ids_s(size_t(n), s);
-    k_col_counts<<<grid_for(c, n), 256, 0, s>>>(T.rowptr.get(), n, cnt.get(), ids.get());
-    FB_LAUNCH_CHECK();
-    size_t tb = 0;
-    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.get(), cnt_s.get(), ids.get(),
-                                                      ids_s.get(), n, 0, 32, s));
-    DBuf<unsigned char> tmp(tb, s);
-    FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), tb, cnt.get(), cnt_s.get(), ids.get(),
-                                                      ids_s.get(), n, 0, 32, s));
-    A.nhot = std::min<int64_t>(kHot, n);
-    A.hot_cols.alloc(size_t(A.nhot), s);
-    FB_CUDA(cudaMemcpyAsync(A.hot_cols.get(), ids_s.get(), sizeof(int32_t) * A.nhot, cudaMemcpyDeviceToDevice, s));
-    DBuf<int32_t> rank_of(size_t(n), s);
-    FB_CUDA(cudaMemsetAsync(rank_of.get(), 0xff, rank_of.bytes(), s));
-    k_rank_map<<<grid_for(c, A.nhot), 256, 0, s>>>(A.hot_cols.get(), int(A.nhot), rank_of.get());
-    FB_LAUNCH_CHECK();
-    k_encode_hot<<<grid_for(c, A.nnz), 256, 0, s>>>(A.col.get(), A.nnz, rank_of.get());
-    FB_LAUNCH_CHECK();
-}
-
 __global__ void k_rank_all(const int32_t* __restrict__ ids, int64_t n, int32_t* __restrict__ rank_of) {
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x)
         rank_of[ids[r]] = int32_t(r);
 }
 
-__global__ void k_flag_hint(int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ rank_of,
-                            int64_t H) {
+// Re-encode A's column ids for an A*X launch mode (DCsr::enc_*): ids of the
+// sx_h most popular columns become kColHot | rank (their X rows are staged in
+// shared memory by the sliced kernel), the next ones up to hint_h carry the
+// sign bit (L2 evict_last hint), the rest are plain. The original id of any
+// encoding is recovered through rank_ids.
+__global__ void k_encode_cols(int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ rank_of,
+                              const int32_t* __restrict__ rank_ids, int64_t hint_h, int64_t sx_h) {
     for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < nnz;
          p += int64_t(gridDim.x) * blockDim.x) {
-        const int32_t cc = col[p] & kColMask;
-        col[p] = rank_of[cc] < H ? int32_t(uint32_t(cc) | 0x80000000u) : cc;
+        const int32_t e = col[p];
+        const int32_t cc = (e & kColHot) ? rank_ids[e & kRankMask] : (e & kColMask);
+        const int32_t r = rank_of[cc];
+        col[p] = r < sx_h ? int32_t(kColHot | r) : (r < hint_h ? int32_t(uint32_t(cc) | 0x80000000u) : cc);
     }
 }
 
@@ -284,7 +251,8 @@ void build_ranks(Ctx& c, DCsr& A, const DCsr& T) {
     A.rank_of.alloc(size_t(n), s);
     k_rank_all<<<grid_for(c, n), 256, 0, s>>>(ids_s.get(), n, A.rank_of.get());
     FB_LAUNCH_CHECK();
-    A.hint_h = 0;
+    A.rank_ids = std::move(ids_s);
+    A.hint_h = A.sx_h = 0;
 }
 
 const char* kValidateMsg[3] = {
@@ -393,15 +361,8 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         FB_CUDA(cudaMemsetAsync(T.rowptr.get(), 0, T.rowptr.bytes(), s));
     }
     rowid.release();
-    // hot-column encoding only for the (experimental) shared-memory staging
-    // of A*X: the decode adds a dependent load per hot nonzero otherwise
-    static const bool hot = [] {
-        const char* e = std::getenv("FRPCA_HOT_STAGING");
-        return e && e[0] == '1';
-    }();
     ph.reset(new Prof(c, "upload_items", 0, 0));
-    if (hot) build_hot(c, A, T);
-    else build_ranks(c, A, T);
+    build_ranks(c, A, T);
     build_items(c, A, nullptr, A.L, default_chunk(c, A));
     build_items(c, T, nullptr, T.L, default_chunk(c, T));
     ph.reset();
@@ -712,8 +673,19 @@ void csr_from_triplets_device(Ctx& c, int64_t rows, int64_t cols, int64_t n, con
     *nnz = total;
 }
 
+void ensure_encoding(Ctx& c, DCsr& A, int64_t hint_h, int64_t sx_h) {
+    if (!A.rank_of.n) return;
+    hint_h = std::min(hint_h, A.cols);
+    sx_h = std::min(sx_h, A.cols);
+    if (hint_h == A.hint_h && sx_h == A.sx_h) return;
+    k_encode_cols<<<grid_for(c, A.nnz), 256, 0, c.stream>>>(A.col.get(), A.nnz, A.rank_of.get(), A.rank_ids.get(),
+                                                             hint_h, sx_h);
+    FB_LAUNCH_CHECK();
+    A.hint_h = hint_h;
+    A.sx_h = sx_h;
+}
+
 void ensure_hint(Ctx& c, DCsr& A, int64_t w) {
-    if (!A.rank_of.n || A.nhot) return;
     // budget of L2-kept X rows
     const char* e = std::getenv("FRPCA_HINT_MB");
     const double mb = e && *e ? std::atof(e) : 64.0;
@@ -722,10 +694,7 @@ void ensure_hint(Ctx& c, DCsr& A, int64_t w) {
     // (at C1, X = 2.5x the budget, the hints cost 2%: only well beyond it)
     if (budget > 0 && 8.0 * double(A.cols) * double(w) > 4.0 * budget)
         H = std::min<int64_t>(A.cols, std::max<int64_t>(1, int64_t(budget / (8.0 * double(w)))));
-    if (H == A.hint_h) return;
-    k_flag_hint<<<grid_for(c, A.nnz), 256, 0, c.stream>>>(A.col.get(), A.nnz, A.rank_of.get(), H);
-    FB_LAUNCH_CHECK();
-    A.hint_h = H;
+    ensure_encoding(c, A, H, 0);
 }
 
 void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v) {
@@ -739,7 +708,15 @@ void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v) {
                                 c.stream));
     }
     FB_CUDA(cudaStreamSynchronize(c.stream));
-    for (int64_t i = 0; i < A.nnz; ++i) ci[i] = tmp[size_t(i)] & kColMask;
+    std::vector<int32_t> ids;
+    if (A.sx_h > 0) {
+        ids.resize(size_t(A.sx_h));
+        FB_CUDA(cudaMemcpy(ids.data(), A.rank_ids.get(), sizeof(int32_t) * ids.size(), cudaMemcpyDeviceToHost));
+    }
+    for (int64_t i = 0; i < A.nnz; ++i) {
+        const int32_t e = tmp[size_t(i)];
+        ci[i] = (e & kColHot) ? ids[size_t(e & kRankMask)] : (e & kColMask);
+    }
 }
 
 }  // namespace fb

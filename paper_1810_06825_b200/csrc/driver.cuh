@@ -84,6 +84,7 @@ struct LoopbackGroup;
 std::shared_ptr<LoopbackGroup> loopback_group(int world);
 void comm_attach_loopback(Ctx& c, const std::shared_ptr<LoopbackGroup>& g, int rank);
 void loopback_fail(LoopbackGroup& g);
+void loopback_reset(LoopbackGroup& g);
 
 // group.cu: host-side shard plan of a CSR over `world` ranks.
 // Row blocks (frpcat) balanced by nnz + rows; column blocks (frpca) balanced by

@@ -66,21 +66,19 @@ struct DCsr {
     DBuf<int32_t> col;
     DBuf<double> val;
     ItemList L;  // work list over all rows
-    // Hot columns (A only, opt-in FRPCA_HOT_STAGING): the kHot most popular
-    // columns, by nnz, are encoded in `col` as -(rank+1); hot_cols[rank] is
-    // the original column id.
-    DBuf<int32_t> hot_cols;
-    int64_t nhot = 0;
-    // L2 hints (A only): popularity rank of every column (nnz, ties to the
-    // lower id), and the number hint_h of top-ranked columns whose ids carry
-    // the sign bit (X rows kept in L2 with evict_last, spmm.cu MODE_HINT).
-    // Re-encoded by ensure_hint when the call's width changes the budget.
-    DBuf<int32_t> rank_of;
-    int64_t hint_h = 0;
+    // Column encodings of A (A only): popularity rank of every column (nnz,
+    // ties to the lower id) and its inverse rank_ids. The sx_h top-ranked
+    // columns are encoded as kColHot | rank (X rows staged in shared memory
+    // by the sliced A*X, spmm.cu k_spmm_sx); the following ones up to hint_h
+    // carry the sign bit (X rows kept in L2 with evict_last, MODE_HINT).
+    // Re-encoded in place by ensure_encoding when a call needs other counts.
+    DBuf<int32_t> rank_of, rank_ids;
+    int64_t hint_h = 0, sx_h = 0;
     PanelPlan pan;  // on A^T only
 };
-constexpr int32_t kColMask = 0x7fffffff;
-constexpr int kHot = 4096;
+constexpr int32_t kColMask = 0x7fffffff;  // id under the L2-hint sign bit
+constexpr int32_t kColHot = 0x40000000;   // shared-memory-staged column: kColHot | rank
+constexpr int32_t kRankMask = 0x3fffffff;
 
 struct ProfAgg {
     int64_t launches = 0;
@@ -168,6 +166,8 @@ void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v);
 void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_t ch);
 // sign-bit L2 hints on A's column ids for an A*X of width w (<= 256)
 void ensure_hint(Ctx& c, DCsr& A, int64_t w);
+// A's column ids encoded for hint_h L2-hinted and sx_h shared-memory columns
+void ensure_encoding(Ctx& c, DCsr& A, int64_t hint_h, int64_t sx_h);
 // panel plan of T (== A^T) for panels of pr rows of the gathered operand
 void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap);
 

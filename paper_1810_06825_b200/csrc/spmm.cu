@@ -19,6 +19,7 @@ namespace fb {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr double L2_BYTES = 126.0 * 1048576.0;
 
 double env_double(const char* name, double dflt) {
     const char* e = std::getenv(name);
@@ -60,22 +61,17 @@ struct Vec<1> {
     __device__ static T zero() { return 0.0; }
 };
 
-// Hot-column staging (A * X only): the most popular columns of A are encoded
-// as -(rank+1); ranks below H are served from the CTA's shared copy Xs of
-// those X rows, higher ranks are decoded through hot_cols and gathered from
-// global memory like any other column.
+// L2 policies of MODE_HINT (evict_last for the hinted X rows, evict_first
+// for the others).
 struct Hot {
-    const double* Xs;        // H x ncols in shared memory (nullptr when H == 0)
-    int H;
-    const int32_t* cols;     // rank -> original column id
-    uint64_t keep, stream;   // L2 policies of MODE_HINT: evict_last / evict_first
+    uint64_t keep, stream;
 };
 
-// Gather modes: plain ids; hot ids -(rank+1) (staging, opt-in); ids whose
-// sign bit marks an L2-hot X row (DCsr::hint_h): hot rows are loaded with an
-// evict_last policy, the others evict_first, so the rare rows streamed from
-// HBM do not push the popular rows out of L2.
-constexpr int MODE_PLAIN = 0, MODE_HOT = 1, MODE_HINT = 2;
+// Gather modes: plain ids; ids whose sign bit marks an L2-hot X row
+// (DCsr::hint_h): hot rows are loaded with an evict_last policy, the others
+// evict_first, so the rare rows streamed from HBM do not push the popular rows
+// out of L2.
+constexpr int MODE_PLAIN = 0, MODE_HINT = 2;
 
 __device__ __forceinline__ void make_policies(Hot& h) {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(h.keep));
@@ -93,21 +89,6 @@ __device__ __forceinline__ void gather(typename Vec<VEC>::T (&x)[NCH], int c, co
         const double* src = Xl + int64_t(c & 0x7fffffff) * ldx;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) x[ch] = ok[ch] ? V::load_pol(src + ch * 32 * VEC, pol) : V::zero();
-        return;
-    }
-    if (MODE == MODE_HOT) {
-        // one generic pointer for both sources: shared copy or global row
-        const double* src;
-        if (c < 0) {
-            const int slot = -c - 1;
-            src = slot < hot.H ? hot.Xs + size_t(slot) * ncols + lane * VEC
-                               : Xl + int64_t(__ldg(hot.cols + slot)) * ldx;
-        } else {
-            src = Xl + int64_t(c) * ldx;
-        }
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
-            x[ch] = ok[ch] ? *reinterpret_cast<const T*>(src + ch * 32 * VEC) : V::zero();
         return;
     }
 #pragma unroll
@@ -234,40 +215,99 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
     }
 }
 
-// Plain kernel (A^T * Y, and A * X when no column is hot enough to stage).
-// MODE_HOT here only decodes hot ids through the rank table (H = 0).
+// Plain kernel (A^T * Y, and A * X over the full width).
 template <int VEC, int NCH, int MODE>
 __global__ void __launch_bounds__(kThreads, 4)
 k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
        const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
        const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
-       double* __restrict__ part, int ncols, const int32_t* __restrict__ hot_cols,
-       const uint8_t* __restrict__ skip, int32_t* __restrict__ counter) {
-    Hot hot{nullptr, 0, MODE == MODE_HOT ? hot_cols : nullptr, 0, 0};
+       double* __restrict__ part, int ncols, const uint8_t* __restrict__ skip, int32_t* __restrict__ counter) {
+    Hot hot{0, 0};
     if (MODE == MODE_HINT) make_policies(hot);
     spmm_items<VEC, NCH, MODE>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, skip, counter);
 }
 
-// A * X with the H most popular columns' X rows staged in shared memory: one
-// 512-thread CTA per SM (16 resident warps; 128 registers keep the four
-// in-flight nonzeros of every warp unspilled).
-constexpr int kHotThreads = 512;
-template <int NCH>
-__global__ void __launch_bounds__(kHotThreads, 1)
-k_spmm_hot(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-           const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
-           const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
-           double* __restrict__ part, int ncols, const int32_t* __restrict__ hot_cols, int H) {
-    extern __shared__ __align__(16) double Xs[];
-    const int half = ncols / 2;
-    for (int e = threadIdx.x; e < H * half; e += blockDim.x) {
-        const int r = e / half, c2 = e % half;
-        reinterpret_cast<double2*>(Xs)[e] =
-            __ldg(reinterpret_cast<const double2*>(X + int64_t(hot_cols[r]) * ldx) + c2);
+// ---- Sliced A*X with shared-memory hot rows (k_spmm_sx) ---------------------
+// For an X several times larger than L2: Y = A X runs in slices of 32
+// columns. A slice of X (n x 32 doubles; 83 MB at C3) stays L2-resident while
+// A streams through, so the gathers stop missing to HBM, and the X rows of the
+// H most popular columns (A.sx_h, ids encoded kColHot | rank) come from a
+// shared-memory copy made at kernel start (at C3 the top 640 columns hold ~30%
+// of the nonzeros), so those gathers leave L2 alone. One lane per column:
+// lane j accumulates Y(r, c0 + j) as the FMA chain over the row's nonzeros in
+// CSR order -- per entry the same operations as the full-width kernel, so the
+// two are bitwise equal (padding slots add fma(0, x, acc) == acc).
+constexpr int kSxThreads = 1024;
+constexpr int kSxW = 32;
+
+__device__ __forceinline__ double sx_gather(int32_t e, const double* __restrict__ Xc, int64_t ldx,
+                                            const double* __restrict__ Xs, int lane, bool ok) {
+    if (e & kColHot) return Xs[(e & kRankMask) * kSxW + lane];  // warp-uniform
+    return ok ? __ldg(Xc + int64_t(e) * ldx) : 0.0;
+}
+
+__device__ __forceinline__ double sx_row(const int32_t* __restrict__ col, const double* __restrict__ val, int64_t p0,
+                                         int64_t p1, const double* __restrict__ Xc, int64_t ldx,
+                                         const double* __restrict__ Xs, int lane, bool ok) {
+    double acc = 0.0;
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int cnt = (p1 - base) < 32 ? int(p1 - base) : 32;
+        int myc = 0;
+        double myv = 0.0;
+        if (lane < cnt) {
+            myc = __ldcs(col + base + lane);
+            myv = __ldcs(val + base + lane);
+        }
+        for (int j = 0; j < cnt; j += 8) {
+            // eight gathers in flight; past the end a slot re-reads the
+            // group's first row with weight 0 (adds exactly 0)
+            const int rem = cnt - j;
+            double x[8], v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int src = u < rem ? j + u : j;
+                const int32_t e = __shfl_sync(0xffffffffu, myc, src);
+                const double vv = __shfl_sync(0xffffffffu, myv, src);
+                v[u] = u < rem ? vv : 0.0;
+                x[u] = sx_gather(e, Xc, ldx, Xs, lane, ok);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __fma_rn(v[u], x[u], acc);
+        }
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(kSxThreads, 1)
+k_spmm_sx(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, const double* __restrict__ val,
+          const WorkItem* __restrict__ items, int64_t nitems, const double* __restrict__ X, int64_t ldx, int w,
+          double* __restrict__ Y, int64_t ldy, double* __restrict__ part, const int32_t* __restrict__ rank_ids,
+          int H, int32_t* __restrict__ counter) {
+    extern __shared__ double Xs[];  // H x 32
+    const int lane = threadIdx.x & 31;
+    const bool ok = lane < w;
+    for (int e = threadIdx.x; e < H * kSxW; e += blockDim.x) {
+        const int r = e >> 5, j = e & 31;
+        Xs[e] = j < w ? __ldg(X + int64_t(rank_ids[r]) * ldx + j) : 0.0;
     }
     __syncthreads();
-    const Hot hot{Xs, H, hot_cols, 0, 0};
-    spmm_items<2, NCH, MODE_HOT>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, nullptr, nullptr);
+    const double* Xc = X + lane;
+    for (;;) {
+        int it = 0;
+        if (lane == 0) it = atomicAdd(counter, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nitems) break;
+        const WorkItem wi = items[it];
+        if (wi.r1 >= 0) {
+            for (int32_t r = wi.r0; r < wi.r1; ++r) {
+                const double acc = sx_row(col, val, rowptr[r], rowptr[r + 1], Xc, ldx, Xs, lane, ok);
+                if (ok) __stcs(Y + int64_t(r) * ldy + lane, acc);
+            }
+        } else {
+            const double acc = sx_row(col, val, wi.p0, wi.p1, Xc, ldx, Xs, lane, ok);
+            if (ok) __stcs(part + (-int64_t(wi.r1) - 1) * w + lane, acc);
+        }
+    }
 }
 
 // Long rows: Y[row] = sum of its chunk partials in a fixed order. One CTA per
@@ -381,7 +421,7 @@ k_spmm_panels(const int32_t* __restrict__ col, const double* __restrict__ val,
     using V = Vec<2>;
     using T = V::T;
     const int lane = threadIdx.x & 31;
-    const Hot hot{nullptr, 0, nullptr, 0, 0};
+    const Hot hot{0, 0};
     for (;;) {
         int it = 0;
         if (lane == 0) it = atomicAdd(counter, 1);
@@ -424,21 +464,7 @@ void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip,
     }
     k_spmm<VEC, NCH, MODE><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
                                                            L.items.get(), L.nitems, X, ldx, Y, ldy, part,
-                                                           ncols, A.hot_cols.get(), skip, counter);
-    FB_LAUNCH_CHECK();
-}
-
-constexpr size_t kHotSmem = 200 * 1024;
-
-template <int NCH>
-void launch_hot(Ctx& c, const DCsr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
-                double* part, int ncols) {
-    const int H = int(std::min<int64_t>(A.nhot, int64_t(kHotSmem / (sizeof(double) * ncols))));
-    smem_optin(k_spmm_hot<NCH>, size_t(kHotSmem));
-    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, (A.L.nitems + 31) / 32)));
-    k_spmm_hot<NCH><<<grid, kHotThreads, sizeof(double) * size_t(H) * ncols, c.stream>>>(
-        A.rowptr.get(), A.col.get(), A.val.get(), A.L.items.get(), A.L.nitems, X, ldx, Y, ldy, part, ncols,
-        A.hot_cols.get(), H);
+                                                           ncols, skip, counter);
     FB_LAUNCH_CHECK();
 }
 
@@ -446,10 +472,7 @@ template <int VEC, int NCH>
 void launch(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
             double* Y, int64_t ldy, double* part, int ncols) {
     if (A.hint_h > 0 && &L == &A.L) return launch_plain<VEC, NCH, MODE_HINT>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
-    if (A.nhot == 0) return launch_plain<VEC, NCH, MODE_PLAIN>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
-    if (VEC == 2 && ncols % 2 == 0 && &L == &A.L && A.L.nitems >= 32 * c.num_sms)
-        return launch_hot<NCH>(c, A, X, ldx, Y, ldy, part, ncols);
-    launch_plain<VEC, NCH, MODE_HOT>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
+    launch_plain<VEC, NCH, MODE_PLAIN>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
 }
 
 void combine(Ctx& c, const ItemList& L, const double* part, int nc, double* Y, int64_t ldy) {
@@ -521,16 +544,50 @@ void launch_panels(Ctx& c, const DCsr& T, const double* Y, int64_t ldy, double* 
     }
 }
 
+// The sliced path is taken when X is several times L2 and one 32-column slice
+// of it fits (FRPCA_SPMM_SX=0/1 forces it off/on; FRPCA_SX_KB sets the shared
+// memory given to hot rows, default 160 KB: 640 rows).
+bool use_sx(const Ctx& c, const DCsr& A, int64_t ncols) {
+    const double xbytes = 8.0 * double(A.cols) * double(ncols);
+    const double slice = 8.0 * double(A.cols) * double(kSxW);
+    const int f = int(env_double("FRPCA_SPMM_SX", -1.0));
+    if (f >= 0) return f == 1 && A.rank_of.n > 0;
+    (void)c;
+    return A.rank_of.n > 0 && xbytes > 2.0 * double(L2_BYTES) && slice <= 0.75 * double(L2_BYTES);
+}
+
+void spmm_sx(Ctx& c, DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y, int64_t ldy) {
+    const int64_t budget = int64_t(env_double("FRPCA_SX_KB", 160.0) * 1024.0);
+    const int H = int(std::min<int64_t>(A.cols, std::max<int64_t>(0, budget / (8 * kSxW))));
+    ensure_encoding(c, A, 0, H);
+    const size_t smem = sizeof(double) * size_t(H) * kSxW;
+    smem_optin(k_spmm_sx, std::max<size_t>(smem, 48 * 1024));
+    if (!c.wcount.get()) c.wcount.alloc(2, c.stream);
+    int32_t* counter = c.wcount.get() + (c.stream == c.aux ? 1 : 0);
+    DBuf<double> part;
+    if (A.L.nslots) part.alloc(size_t(A.L.nslots) * kSxW, c.stream);
+    for (int64_t c0 = 0; c0 < ncols; c0 += kSxW) {
+        const int w = int(std::min<int64_t>(kSxW, ncols - c0));
+        FB_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), c.stream));
+        k_spmm_sx<<<c.num_sms, kSxThreads, smem, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
+                                                             A.L.items.get(), A.L.nitems, X + c0, ldx, w, Y + c0,
+                                                             ldy, part.get(), A.rank_ids.get(), H, counter);
+        FB_LAUNCH_CHECK();
+        combine(c, A.L, part.get(), w, Y + c0, ldy);
+    }
+}
+
 }  // namespace
 
 void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
                  int64_t ldy, const char* tag) {
     if (A.rows == 0 || ncols == 0) return;
-    ensure_hint(c, const_cast<DCsr&>(A), std::min<int64_t>(ncols, 256));
     // algorithmic bytes: 12 B/nnz + 8 B/row ptr + dense in + out
     const double bytes = 12.0 * A.nnz + 8.0 * (A.rows + 1) + 8.0 * ncols * (A.cols + A.rows);
     const double flops = 2.0 * A.nnz * ncols;
     Prof prof(c, tag, bytes, flops);
+    if (use_sx(c, A, ncols)) return spmm_sx(c, const_cast<DCsr&>(A), X, ldx, ncols, Y, ldy);
+    ensure_hint(c, const_cast<DCsr&>(A), std::min<int64_t>(ncols, 256));
     DBuf<double> part;
     for (int64_t off = 0; off < ncols; off += 256) {
         const int nc = int(std::min<int64_t>(256, ncols - off));

@@ -214,6 +214,34 @@ def test_spmm_l2_hints(fb, orc, monkeypatch, ncols):
     assert rel_fro(fb.spmm(A, X2), orc.spmm(oA, X2)) <= SPMM_TOL
 
 
+@pytest.mark.parametrize("ncols", [1, 8, 32, 37, 150, 200, 300])
+@pytest.mark.parametrize("sx_kb", ["0", "2", "160"])
+def test_spmm_sliced_shared_hot_rows(fb, orc, monkeypatch, ncols, sx_kb):
+    """The sliced A*X (spmm.cu k_spmm_sx: 32-column slices, the most popular
+    columns' X rows from shared memory, ids re-encoded kColHot | rank) is
+    bitwise equal to the full-width kernel: per entry the same FMA chain in
+    CSR order. No hot rows, a few (2 KB: 8 rows) and the default budget;
+    power-law rows long enough to be chunked (partials + combine); switching
+    encodings back and forth; the decoded transpose download."""
+    oA = powerlaw_csr(orc, 5000, 3000, 200000, 13)
+    A = to_fb(fb, oA)
+    X = orc.gaussian_matrix(3000, ncols, 6)
+    monkeypatch.setenv("FRPCA_HINT_MB", "0")
+    monkeypatch.setenv("FRPCA_SPMM_SX", "0")
+    Y0 = fb.spmm(A, X)
+    monkeypatch.setenv("FRPCA_SPMM_SX", "1")
+    monkeypatch.setenv("FRPCA_SX_KB", sx_kb)
+    Y1 = fb.spmm(A, X)
+    assert np.array_equal(Y0, Y1)
+    assert rel_fro(Y1, orc.spmm(oA, X)) <= SPMM_TOL
+    monkeypatch.setenv("FRPCA_SPMM_SX", "0")
+    monkeypatch.setenv("FRPCA_HINT_MB", "0.02")  # hint encoding after the shared-memory one
+    assert np.array_equal(fb.spmm(A, X), Y0)
+    # A^T*Y reads the transposed CSR, which no encoding touches
+    Yt = orc.gaussian_matrix(5000, ncols, 7)
+    assert rel_fro(fb.spmm_transpose(A, Yt), orc.spmm_transpose(oA, Yt)) <= SPMM_TOL
+
+
 def test_spmm_transpose_panelled_empty_rows(fb, orc, panels):
     """Columns of A with no entries (empty rows of A^T) next to hot ones."""
     panels(1.0)

@@ -51,6 +51,7 @@ def run(name: str, threads: int | None = None, scale: float = 1.0, floor: bool =
     t_cpu = time.time() - t0
     del oA
     fl = None
+    o2 = None
     if floor:
         # the method's own fp64 floor: the same restatement built with FMA
         # contraction (different rounding everywhere) against the pinned build
@@ -60,7 +61,6 @@ def run(name: str, threads: int | None = None, scale: float = 1.0, floor: bool =
         fl = {"sigma_rel": sigma_rel(o2["S"], o["S"]), "subspace_U": subspace_dist(o["U"], o2["U"]),
               "subspace_V": subspace_dist(o["V"], o2["V"]),
               "what": "oracle built with -ffp-contract=fast -march=x86-64-v3 vs the pinned build"}
-        del o2
     arb = None
     if arbiter:
         # 80-bit long-double pipeline from the same CSR and sketch: each fp64
@@ -72,9 +72,16 @@ def run(name: str, threads: int | None = None, scale: float = 1.0, floor: bool =
         g, c = dist(r.U, r.S, r.V), dist(o["U"], o["S"], o["V"])
         arb = {"gpu_vs_arbiter": g, "oracle_vs_arbiter": c,
                "gpu_no_worse": bool(all(g[k] <= c[k] for k in g)),
+               "oracle_fma_vs_arbiter": dist(o2["U"], o2["S"], o2["V"]) if o2 is not None else None,
                "seconds": round(time.time() - t0, 1),
                "what": "oracle/arbiter.cpp: the same algorithm in 80-bit long double, same CSR and Omega"}
         del a
+    if arb is not None and arb["oracle_fma_vs_arbiter"] is not None:
+        # within the spread of the reference's own valid fp64 builds (the
+        # pinned oracle and the FMA-contracted one) around the arbiter
+        f = arb["oracle_fma_vs_arbiter"]
+        arb["gpu_within_fp64_builds"] = bool(all(g[k] <= max(c[k], f[k]) for k in g))
+    o2 = None
     del rp, ci, va
     # conditioning of the extracted spectrum (eig_svd's floor ~ eps (s1/sk)^2)
     s_ratio = float(o["S"][0] / o["S"][-1])
