@@ -19,6 +19,7 @@
 #include <cmath>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -135,6 +136,75 @@ public:
 private:
     frpca_ctx* h_ = nullptr;
 };
+
+// Devices the drop-in runs frpca / frpcat on (the reference's
+// callers are single-process, frpca_cli.cpp:158-183). Default: the list in
+// FRPCA_DEVICES ("0,1,2,3"), else device 0 alone. With several devices the
+// calls shard A over a group (frpca_group_run_csr: row blocks for frpcat,
+// column blocks for frpca, NCCL between the GPUs); a device listed twice uses
+// the host-staged loopback collective (testing the sharded path on one GPU).
+class Group {
+public:
+    explicit Group(const std::vector<int>& devices) {
+        frpca::detail::check(frpca_group_create(devices.data(), int(devices.size()), FRPCA_COMM_AUTO, &h_));
+    }
+    ~Group() { if (h_) frpca_group_destroy(h_); }
+    Group(const Group&) = delete;
+    Group& operator=(const Group&) = delete;
+    frpca_group* get() const { return h_; }
+
+private:
+    frpca_group* h_ = nullptr;
+};
+
+namespace internal {
+struct DeviceSet {
+    std::mutex mu;
+    std::vector<int> devices;
+    std::unique_ptr<Group> group;
+    DeviceSet() {
+        if (const char* e = std::getenv("FRPCA_DEVICES")) {
+            std::string s(e);
+            std::size_t pos = 0;
+            while (pos < s.size()) {
+                const std::size_t q = s.find(',', pos);
+                const std::string t = s.substr(pos, q == std::string::npos ? std::string::npos : q - pos);
+                if (!t.empty()) devices.push_back(std::stoi(t));
+                if (q == std::string::npos) break;
+                pos = q + 1;
+            }
+        }
+        if (devices.empty()) devices.push_back(0);
+    }
+    static DeviceSet& get() {
+        static DeviceSet d;
+        return d;
+    }
+};
+}  // namespace internal
+
+inline void set_devices(std::vector<int> devices) {
+    frpca::detail::require(!devices.empty(), "set_devices: empty device list");
+    auto& d = internal::DeviceSet::get();
+    std::lock_guard<std::mutex> lk(d.mu);
+    d.devices = std::move(devices);
+    d.group.reset();
+}
+
+inline std::vector<int> devices() {
+    auto& d = internal::DeviceSet::get();
+    std::lock_guard<std::mutex> lk(d.mu);
+    return d.devices;
+}
+
+// the group over devices() (created on first use; null for one device)
+inline Group* default_group() {
+    auto& d = internal::DeviceSet::get();
+    std::lock_guard<std::mutex> lk(d.mu);
+    if (d.devices.size() < 2) return nullptr;
+    if (!d.group) d.group = std::make_unique<Group>(d.devices);
+    return d.group.get();
+}
 }  // namespace b200
 
 // ---- SparseMatrixCsr<double> (sparse_matrix.hpp:19-150) --------------------
@@ -217,6 +287,8 @@ public:
         if (dev_) detail::check(frpca_dmat_reset_pass_count(dev_->h));
         passes_offset_ = 0;
     }
+    // passes made by a sharded run (the group's shards, not this device copy)
+    void recordPasses(std::uint64_t n) const { passes_offset_ += n; }
 
     // The device copy (CSR + transposed CSR + work lists), built on first use.
     frpca_dmat* device(b200::Context& ctx = b200::Context::default_context()) const {
@@ -402,7 +474,6 @@ namespace detail {
 template <typename Scalar>
 SvdResult<Scalar> run(int algo, const SparseMatrixCsr<Scalar>& A, const PcaConfig& cfg,
                       RunStats<Scalar>* stats, const Matrix<Scalar>* omega, int* dispatched) {
-    auto& ctx = b200::Context::default_context();
     frpca_config c{cfg.k, cfg.oversample, cfg.passes, cfg.power, cfg.seed, cfg.deterministic ? 1 : 0, 0u};
     const Index k = std::max<Index>(cfg.k, 0), l = cfg.k + cfg.oversample;
     int eff = algo == FRPCA_ALGO_AUTO ? (A.rows() < A.cols() ? FRPCA_ALGO_FRPCA : FRPCA_ALGO_FRPCAT) : algo;
@@ -412,6 +483,25 @@ SvdResult<Scalar> run(int algo, const SparseMatrixCsr<Scalar>& A, const PcaConfi
     out.V = Matrix<Scalar>(A.cols(), k);
     Matrix<Scalar> basis;
     const bool want_basis = stats && stats->capture_basis && l >= 1;
+    // several devices: the sharded group run (an injected sketch or a captured
+    // basis keep the call on one device)
+    if ((eff == FRPCA_ALGO_FRPCA || eff == FRPCA_ALGO_FRPCAT) && !omega && !want_basis) {
+        if (b200::Group* g = b200::default_group()) {
+            frpca_stats st{};
+            detail::check(frpca_group_run_csr(g->get(), A.rows(), A.cols(), A.nonZeros(), A.rowPtr().data(),
+                                              A.colIdx().data(), A.values().data(), algo, &c, out.U.data(),
+                                              out.S.data(), out.V.data(), &st, dispatched));
+            A.recordPasses(st.passes_over_matrix);
+            if (stats) {
+                stats->sketch_seconds = st.sketch_seconds;
+                stats->power_seconds = st.power_seconds;
+                stats->finalize_seconds = st.finalize_seconds;
+                stats->passes_over_matrix = st.passes_over_matrix;
+            }
+            return out;
+        }
+    }
+    auto& ctx = b200::Context::default_context();
     if (want_basis)
         basis = Matrix<Scalar>(eff == FRPCA_ALGO_FRPCA || eff == FRPCA_ALGO_BASIC_RPCA ? A.rows() : A.cols(), l);
     frpca_stats st{};

@@ -176,6 +176,11 @@ int frpca_spmm(frpca_ctx* ctx, frpca_dmat* A, int transpose, const double* X, in
  * mt19937_64(seed) + libstdc++ normal_distribution, drawn on the device. */
 int frpca_gaussian_matrix(frpca_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed,
                           double* out);
+/* A rank's slice of the same stream (the sharded sketch): the positions
+ * p < count with (p mod period) in [w0, w1), packed in order into out
+ * (out[(p / period) (w1 - w0) + p mod period - w0]). */
+int frpca_gaussian_window(frpca_ctx* ctx, int64_t count, int64_t period, int64_t w0, int64_t w1, uint64_t seed,
+                          double* out);
 /* lu_basis (dense_kernels.hpp:50-116): X = P^T L of M (m x l, m >= l). */
 int frpca_lu_basis(frpca_ctx* ctx, int64_t m, int64_t l, const double* M, double* X);
 /* orth (dense_kernels.hpp:30-48): Q (m x l, column-major) of the Householder

@@ -447,6 +447,22 @@ int frpca_gaussian_matrix(frpca_ctx* c, int64_t rows, int64_t cols, uint64_t see
     });
 }
 
+int frpca_gaussian_window(frpca_ctx* c, int64_t count, int64_t period, int64_t w0, int64_t w1, uint64_t seed,
+                          double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        require(count >= 1 && period >= 1 && 0 <= w0 && w0 < w1 && w1 <= period, "gaussian_window: bad window");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        const int64_t per = w1 - w0, full = count / period, rem = count % period;
+        const int64_t n = full * per + std::max<int64_t>(0, std::min(rem, w1) - w0);
+        DBuf<double> d(size_t(std::max<int64_t>(n, 1)), c->stream);
+        with_checks(*c, [&] { gaussian_stream_window(*c, seed, count, period, w0, w1, d.get()); });
+        if (n) FB_CUDA(cudaMemcpyAsync(out, d.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        FB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
 int frpca_lu_basis(frpca_ctx* c, int64_t m, int64_t l, const double* Mh, double* X) {
     return guarded([&] {
         check_ctx(c);

@@ -124,6 +124,56 @@ void sketch_stream(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, double*
     }
 }
 
+// Rows [r0, r1) of the sketch Omega (rows x cols, column-major stream order)
+// into dst ((r1 - r0) x cols, column-major): a rank's slice of the sketch of a
+// sharded run. Only the slice is written (the device generator emits just
+// the slice's stream positions).
+static void sketch_rows(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, int64_t r0, int64_t r1,
+                        double* dst) {
+    const int64_t nr = r1 - r0;
+    if (nr == rows) return sketch_stream(c, a, rows, cols, dst);
+    if (a.omega) {
+        require(a.omega_rows == rows && a.omega_cols == cols, "injected sketch has the wrong shape");
+        FB_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * nr, a.omega + r0, sizeof(double) * rows, sizeof(double) * nr,
+                                  size_t(cols), a.device_io ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                  c.stream));
+        return;
+    }
+    const uint64_t seed = mix_seed(a.cfg.seed, 0xA11CEull);
+    if (a.cfg.flags & FRPCA_FLAG_HOST_OMEGA) {
+        std::vector<double> h(static_cast<size_t>(rows * cols));
+        gaussian_stream_host(seed, rows * cols, h.data());
+        FB_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * nr, h.data() + r0, sizeof(double) * rows, sizeof(double) * nr,
+                                  size_t(cols), cudaMemcpyHostToDevice, c.stream));
+        FB_CUDA(cudaStreamSynchronize(c.stream));
+        return;
+    }
+    // the stream up to the slice's last element
+    gaussian_stream_window(c, seed, (cols - 1) * rows + r1, rows, r0, r1, dst);
+}
+
+// Columns [c0, c1) of Omega (rows x cols, column-major): one contiguous run
+// of the stream, [c0 rows, c1 rows), generated only up to its end.
+static void sketch_cols(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, int64_t c0, int64_t c1, double* dst) {
+    if (c0 == 0 && c1 == cols) return sketch_stream(c, a, rows, cols, dst);
+    const int64_t b0 = c0 * rows, b1 = c1 * rows;
+    if (a.omega) {
+        require(a.omega_rows == rows && a.omega_cols == cols, "injected sketch has the wrong shape");
+        FB_CUDA(cudaMemcpyAsync(dst, a.omega + b0, sizeof(double) * (b1 - b0),
+                                a.device_io ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+        return;
+    }
+    const uint64_t seed = mix_seed(a.cfg.seed, 0xA11CEull);
+    if (a.cfg.flags & FRPCA_FLAG_HOST_OMEGA) {
+        std::vector<double> h(static_cast<size_t>(b1));
+        gaussian_stream_host(seed, b1, h.data());
+        FB_CUDA(cudaMemcpyAsync(dst, h.data() + b0, sizeof(double) * (b1 - b0), cudaMemcpyHostToDevice, c.stream));
+        FB_CUDA(cudaStreamSynchronize(c.stream));
+        return;
+    }
+    gaussian_stream_window(c, seed, b1, b1, b0, b1, dst);
+}
+
 // Omega (rows x cols, column-major stream order) into dst: the pre-generated
 // stream when frpca_run_csr overlapped it with the upload, else generated now.
 static void sketch_into(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, DBuf<double>& dst) {
@@ -263,14 +313,8 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     if (q % 2 == 0) {
         // Omega (l x grows, column-major) == Omega^T row-major: this rank's rows
         // are the stream slice [offset*l, (offset+m)*l).
-        if (M.offset == 0 && m == M.grows) {
-            sketch_into(c, a, l, M.grows, bufM);
-        } else {
-            DBuf<double> full(size_t(M.grows * l), S);
-            sketch_stream(c, a, l, M.grows, full.get());
-            FB_CUDA(cudaMemcpyAsync(bufM.get(), full.get() + M.offset * l, sizeof(double) * m * l,
-                                    cudaMemcpyDeviceToDevice, S));
-        }
+        if (M.offset == 0 && m == M.grows) sketch_into(c, a, l, M.grows, bufM);
+        else sketch_cols(c, a, l, M.grows, M.offset, M.offset + m, bufM.get());
         spmm_pass(c, M, /*transpose=*/true, bufM.get(), l, Z.get());  // (Omega A)^T, n x l
         allreduce_sum(c, Z.get(), n * l);
         if (q == 2) {
@@ -347,15 +391,13 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     if (q % 2 == 0) {
         // Omega: gcols x l column-major; this rank needs rows [offset, offset+n)
         DBuf<double>& om = c.slot(3, 0);
-        sketch_into(c, a, M.gcols, l, om);
         if (M.offset == 0 && n == M.gcols) {
-            transpose_device(c, om.get(), l, n, bufN.get());
+            sketch_into(c, a, M.gcols, l, om);
         } else {
-            DBuf<double> full(size_t(M.gcols * l), S);
-            transpose_device(c, om.get(), l, M.gcols, full.get());
-            FB_CUDA(cudaMemcpyAsync(bufN.get(), full.get() + M.offset * l, sizeof(double) * n * l,
-                                    cudaMemcpyDeviceToDevice, S));
+            if (om.n < size_t(n * l)) om.alloc(size_t(n * l), S);
+            sketch_rows(c, a, M.gcols, l, M.offset, M.offset + n, om.get());   // this rank's rows only
         }
+        transpose_device(c, om.get(), l, n, bufN.get());
         spmm_pass(c, M, false, bufN.get(), l, Y.get());   // A Omega, m x l
         allreduce_sum(c, Y.get(), m * l);
         if (q > 2) {

@@ -205,10 +205,26 @@ k_count(const uint64_t* __restrict__ raw, int64_t npairs, int64_t* __restrict__ 
     }
 }
 
+// A window of the stream: positions p < count with (p mod P) in [w0, w1) go
+// to out[(p / P) (w1 - w0) + (p mod P - w0)] -- a rank's rows of a
+// column-major sketch (P = rows), or a contiguous slice (P = count).
+struct Window {
+    int64_t P, w0, w1;
+    bool ident;  // the whole stream, out[p]
+};
+
+__device__ __forceinline__ void emit_win(double* __restrict__ out, int64_t p, double v, int64_t count,
+                                         const Window& w) {
+    if (p >= count) return;
+    const int64_t q = p / w.P, r = p - q * w.P;
+    if (r < w.w0 || r >= w.w1) return;
+    out[q * (w.w1 - w.w0) + (r - w.w0)] = v;
+}
+
 // normals of the accepted attempts, written at their stream positions
 __global__ void __launch_bounds__(PT, 5)
 k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restrict__ off,
-       double* __restrict__ out, int64_t count, const crlog::LogEntry* __restrict__ logtab) {
+       double* __restrict__ out, int64_t count, const crlog::LogEntry* __restrict__ logtab, Window win) {
     // round e of the chunk = attempts b CHUNK + e PT + [0, PT) (coalesced
     // loads); the stream position of an accepted attempt = accepted attempts
     // of the earlier rounds + of the lower lanes of its round: one block scan
@@ -245,7 +261,10 @@ k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restri
             const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, crlog::fast_log(rs[e], logtab)), rs[e]));
             const double a = __dadd_rn(__dmul_rn(__dmul_rn(ys[e], mult), 1.0), 0.0);
             const double b = __dadd_rn(__dmul_rn(__dmul_rn(xs[e], mult), 1.0), 0.0);
-            if (vec && idx + 1 < count) {
+            if (!win.ident) {
+                emit_win(out, idx, a, count, win);
+                emit_win(out, idx + 1, b, count, win);
+            } else if (vec && idx + 1 < count) {
                 __stcs(reinterpret_cast<double2*>(out + idx), make_double2(a, b));
             } else {
                 if (idx < count) out[idx] = a;
@@ -322,8 +341,14 @@ void jump_states(Ctx& c, uint64_t* states, const uint32_t* polys, int groups, in
 }  // namespace
 
 void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
+    gaussian_stream_window(c, seed, count, count, 0, count, out);
+}
+
+void gaussian_stream_window(Ctx& c, uint64_t seed, int64_t count, int64_t period, int64_t w0, int64_t w1,
+                            double* out) {
     if (count <= 0) return;
-    Prof prof(c, "omega_total", 8.0 * count, 0.0);
+    const Window win{period, w0, w1, period >= count && w0 == 0 && w1 >= count};
+    Prof prof(c, "omega_total", 8.0 * double(count) * double(w1 - w0) / double(period), 0.0);
     cudaStream_t s = c.stream;
     // attempts needed with margin: accepted ~ Bin(P, pi/4), need 2*acc >= count
     const double half = 0.5 * double(count);
@@ -400,7 +425,7 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
         }
         {
             Prof pe(c, "omega_emit", 8.0 * nseg * J + 8.0 * count, 0.0);
-            k_emit<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, off.get(), out, count, logtab);
+            k_emit<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, off.get(), out, count, logtab, win);
             FB_LAUNCH_CHECK();
         }
         if (defer) {

@@ -142,3 +142,25 @@ def test_group_rejects_nccl_on_one_device(fb):
     from paper_1810_06825_b200 import _lib
     with pytest.raises(ValueError, match="NCCL needs distinct devices"):
         fb.Group([0, 0], comm=_lib.COMM_NCCL)
+
+
+@pytest.mark.parametrize("rows,cols,r0,r1", [(1000, 7, 0, 1000), (1000, 7, 250, 600), (5000, 40, 4999, 5000),
+                                             (3, 100000, 1, 2), (20000, 12, 0, 1)])
+def test_sketch_window_is_the_stream_slice(fb, ctx, rows, cols, r0, r1):
+    """A rank's slice of the sketch (rows [r0, r1) of a column-major rows x
+    cols Omega, or a contiguous run) is bitwise the corresponding part of the
+    full stream (dense_kernels.hpp:19-28): only the emitted positions change."""
+    import ctypes as C
+    from paper_1810_06825_b200 import _lib
+    seed = fb.mix_seed(9, fb.kSketchStreamTag)
+    full = fb.gaussian_matrix(rows, cols, seed)
+    L = _lib.load()
+    win = np.empty((r1 - r0) * cols)
+    _lib.check(L.frpca_gaussian_window(ctx._h, rows * cols, rows, r0, r1, seed, win.ctypes.data))
+    assert np.array_equal(win.reshape(cols, r1 - r0).T, full[r0:r1])
+    # a contiguous run of columns [1, cols - 1), generated only up to its end
+    run = np.empty((cols - 2) * rows) if cols > 2 else None
+    if run is not None:
+        cnt = (cols - 1) * rows
+        _lib.check(L.frpca_gaussian_window(ctx._h, cnt, cnt, rows, cnt, seed, run.ctypes.data))
+        assert np.array_equal(run, full[:, 1:cols - 1].ravel(order="F"))
