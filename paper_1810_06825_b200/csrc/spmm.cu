@@ -19,7 +19,6 @@ namespace fb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr double L2_BYTES = 126.0 * 1048576.0;
 
 double env_double(const char* name, double dflt) {
     const char* e = std::getenv(name);
@@ -544,16 +543,15 @@ void launch_panels(Ctx& c, const DCsr& T, const double* Y, int64_t ldy, double* 
     }
 }
 
-// The sliced path is taken when X is several times L2 and one 32-column slice
-// of it fits (FRPCA_SPMM_SX=0/1 forces it off/on; FRPCA_SX_KB sets the shared
-// memory given to hot rows, default 160 KB: 640 rows).
+// Opt-in (FRPCA_SPMM_SX=1; FRPCA_SX_KB sets the shared memory given to hot
+// rows, default 160 KB: 640 rows). Measured slower than the full-width kernel
+// at every config (per run: C1 17.1 -> 23.3 ms, C2 72.3 -> 118.9, C3 208 ->
+// 361; profiles/r2_ab_spmm_sx.json): re-streaming A's ids and values once per
+// slice and the 256-byte gathers cost more than the L2 misses they remove.
 bool use_sx(const Ctx& c, const DCsr& A, int64_t ncols) {
-    const double xbytes = 8.0 * double(A.cols) * double(ncols);
-    const double slice = 8.0 * double(A.cols) * double(kSxW);
-    const int f = int(env_double("FRPCA_SPMM_SX", -1.0));
-    if (f >= 0) return f == 1 && A.rank_of.n > 0;
     (void)c;
-    return A.rank_of.n > 0 && xbytes > 2.0 * double(L2_BYTES) && slice <= 0.75 * double(L2_BYTES);
+    (void)ncols;
+    return int(env_double("FRPCA_SPMM_SX", 0.0)) == 1 && A.rank_of.n > 0;
 }
 
 void spmm_sx(Ctx& c, DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y, int64_t ldy) {
