@@ -1244,6 +1244,71 @@ static Csr* random_sparse(Index rows, Index cols, double density, uint64_t seed)
     return from_triplets(rows, cols, std::move(e));
 }
 
+// ---- generate_sparse (generate.hpp:60-138), geometric spectrum ------------
+// Dense orthogonally rotated diagonal blocks with a prescribed descending
+// spectrum (round-robin over the blocks), rows and columns shuffled with
+// mt19937_64(mix_seed(seed, 0x6E6E)) and std::shuffle (libstdc++, as the
+// reference). Used by the ported accuracy tests (acceptance.cpp:156-214,
+// test_randsvd.cpp:225-251); the block product P diag(d) R^T is formed with
+// this file's GEMM, so entries may differ from an Eigen build in the last bit.
+static Csr* generate_sparse_geometric(Index rows, Index cols, Index nnz_per_row, double ratio, double floor_v,
+                                      uint64_t seed) {
+    require(rows >= 1 && cols >= 1, "gen: dimensions must be >= 1");
+    require(nnz_per_row >= 1, "gen: nonzeros per row must be >= 1");
+    require(ratio > 0.0 && ratio < 1.0, "gen: geometric ratio must be in (0, 1)");
+    const Index blocks = std::max<Index>(
+        1, std::min({rows, cols, Index(std::llround(double(cols) / double(nnz_per_row)))}));
+    auto chunk_sizes = [](Index total, Index parts) {
+        std::vector<Index> sizes(static_cast<size_t>(parts), total / parts);
+        for (Index i = 0; i < total % parts; ++i) ++sizes[size_t(i)];
+        return sizes;
+    };
+    const std::vector<Index> row_chunk = chunk_sizes(rows, blocks), col_chunk = chunk_sizes(cols, blocks);
+    Index total_rank = 0;
+    std::vector<Index> block_rank(static_cast<size_t>(blocks));
+    for (Index b = 0; b < blocks; ++b) {
+        block_rank[size_t(b)] = std::min(row_chunk[size_t(b)], col_chunk[size_t(b)]);
+        total_rank += block_rank[size_t(b)];
+    }
+    std::vector<double> sv(static_cast<size_t>(total_rank));
+    {
+        double v = 1.0;
+        for (auto& x : sv) { x = std::max(v, floor_v); v *= ratio; }
+    }
+    std::vector<std::vector<double>> block_sv(static_cast<size_t>(blocks));
+    {
+        Index b = 0;
+        for (double v : sv) {
+            while (Index(block_sv[size_t(b)].size()) >= block_rank[size_t(b)]) b = (b + 1) % blocks;
+            block_sv[size_t(b)].push_back(v);
+            b = (b + 1) % blocks;
+        }
+    }
+    std::vector<Index> row_map(static_cast<size_t>(rows)), col_map(static_cast<size_t>(cols));
+    std::iota(row_map.begin(), row_map.end(), Index(0));
+    std::iota(col_map.begin(), col_map.end(), Index(0));
+    std::mt19937_64 rng(mix_seed(seed, 0x6E6Eu));
+    std::shuffle(row_map.begin(), row_map.end(), rng);
+    std::shuffle(col_map.begin(), col_map.end(), rng);
+    std::vector<Triplet> entries;
+    Index row0 = 0, col0 = 0;
+    for (Index b = 0; b < blocks; ++b) {
+        const Index rs = row_chunk[size_t(b)], cs = col_chunk[size_t(b)], r = block_rank[size_t(b)];
+        Mat P = orth(gaussian_matrix(rs, r, mix_seed(seed, uint64_t(2 * b + 17))));
+        Mat R = orth(gaussian_matrix(cs, r, mix_seed(seed, uint64_t(2 * b + 18))));
+        Mat Rt(r, cs);  // diag(d) R^T
+        for (Index j = 0; j < cs; ++j)
+            for (Index i = 0; i < r; ++i) Rt(i, j) = block_sv[size_t(b)][size_t(i)] * R(j, i);
+        Mat block = gemm(P, Rt);
+        for (Index j = 0; j < cs; ++j)
+            for (Index i = 0; i < rs; ++i)
+                entries.push_back({row_map[size_t(row0 + i)], col_map[size_t(col0 + j)], block(i, j)});
+        row0 += rs;
+        col0 += cs;
+    }
+    return from_triplets(rows, cols, std::move(entries));
+}
+
 }  // namespace orc
 
 // ============================================================================
@@ -1307,6 +1372,10 @@ int orc_csr_from_triplets(int64_t rows, int64_t cols, int64_t n, const int64_t* 
 }
 int orc_csr_random_sparse(int64_t rows, int64_t cols, double density, uint64_t seed, void** out) {
     return guarded([&] { *out = random_sparse(rows, cols, density, seed); });
+}
+int orc_csr_generate_geometric(int64_t rows, int64_t cols, int64_t nnz_per_row, double ratio, double floor_v,
+                               uint64_t seed, void** out) {
+    return guarded([&] { *out = generate_sparse_geometric(rows, cols, nnz_per_row, ratio, floor_v, seed); });
 }
 int orc_csr_transpose(void* h, void** out) {
     return guarded([&] { *out = transpose(*static_cast<Csr*>(h)); });

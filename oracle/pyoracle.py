@@ -74,6 +74,7 @@ def lib():
         L.orc_csr_create.argtypes = [_i64, _i64, _i64, _lp, _lp, _dp, C.POINTER(_vp)]
         L.orc_csr_from_triplets.argtypes = [_i64, _i64, _i64, _lp, _lp, _dp, C.POINTER(_vp)]
         L.orc_csr_random_sparse.argtypes = [_i64, _i64, C.c_double, _u64, C.POINTER(_vp)]
+        L.orc_csr_generate_geometric.argtypes = [_i64, _i64, _i64, C.c_double, C.c_double, _u64, C.POINTER(_vp)]
         L.orc_csr_transpose.argtypes = [_vp, C.POINTER(_vp)]
         L.orc_csr_info.argtypes = [_vp, _lp, _lp, _lp]
         L.orc_csr_copy.argtypes = [_vp, _lp, _lp, _dp]
@@ -181,6 +182,13 @@ class Csr:
         """test_support.hpp:46-55 (same libstdc++ stream => same matrix)."""
         h = _vp()
         _check(lib().orc_csr_random_sparse(rows, cols, density, seed, C.byref(h)))
+        return Csr(h.value)
+
+    @staticmethod
+    def generate_geometric(rows, cols, nnz_per_row, ratio, seed, floor=1e-8) -> "Csr":
+        """generate_sparse (generate.hpp:60-138) with a geometric spectrum."""
+        h = _vp()
+        _check(lib().orc_csr_generate_geometric(rows, cols, nnz_per_row, ratio, floor, seed, C.byref(h)))
         return Csr(h.value)
 
     def transpose(self) -> "Csr":

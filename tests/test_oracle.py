@@ -472,3 +472,22 @@ def test_basic_preconditions(orc):  # test_randsvd.cpp:253-262
         orc.pca(A, orc.BASIC_RPCA, 2, 5, 2, power=-1)
     with pytest.raises(ValueError, match="k \\+ oversample must be <= min"):
         orc.pca(A, orc.BASIC_RPCAT, 15, 10, 2, power=0)
+
+
+@pytest.mark.parametrize("rows,cols,npr,ratio,seed", [(200, 150, 30, 0.9, 7000), (60, 100, 20, 0.8, 7),
+                                                       (2000, 1500, 75, 0.9, 42)])
+def test_generate_sparse_spectrum(orc, rows, cols, npr, ratio, seed):
+    """generate_sparse (generate.hpp:60-138): block-diagonal structure with
+    about nnz_per_row entries per row, exactly the prescribed geometric
+    spectrum (floor 1e-8), rows/columns shuffled."""
+    A = orc.Csr.generate_geometric(rows, cols, npr, ratio, seed)
+    rp, ci, va = A.arrays()
+    D = np.zeros((rows, cols))
+    for i in range(rows):
+        D[i, ci[rp[i]:rp[i + 1]]] = va[rp[i]:rp[i + 1]]
+    s = np.linalg.svd(D, compute_uv=False)
+    r = min(rows, cols)
+    want = np.maximum(ratio ** np.arange(r), 1e-8)
+    assert np.allclose(s[:r], np.sort(want)[::-1], rtol=1e-10, atol=1e-12)
+    assert abs(rp[-1] / rows - cols / round(cols / npr)) < 1.0
+    assert not np.array_equal(np.argmax(np.abs(D), axis=1), np.sort(np.argmax(np.abs(D), axis=1)))
