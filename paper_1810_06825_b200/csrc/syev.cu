@@ -613,6 +613,13 @@ __device__ __forceinline__ double group_sum(double v, unsigned mask) {
     return v;
 }
 
+// Convergence factor of the secular solver: |f| <= c eps (1 + rho sum |terms|),
+// LAPACK dlaed4's test up to its constant. (An earlier factor c = 8 k, up to
+// 1600 at n = 200, left the roots loose enough that the eigenvectors, and
+// through eig_svd's S^-1 the power iteration's basis, lost ~1.5x in subspace
+// accuracy against the long-double arbiter at C2.) Set per launch.
+__constant__ double c_sec_tol = 8.0;
+
 // Root i of 1 + rho sum_j z_j^2 / (d_j - lambda) = 0 (d ascending, rho > 0),
 // by a group of kSecLanes lanes: lambda = d_org + tau.
 __device__ bool secular_root(int i, int k, const double* dk, const double* zk, double rho, double zsum2,
@@ -658,7 +665,7 @@ __device__ bool secular_root(int i, int k, const double* dk, const double* zk, d
             eabs = group_sum(eabs, mask);
             f = 1.0 + rho * (psi + phi);
         }
-        if (fabs(f) <= 8.0 * DBL_EPSILON * (1.0 + rho * eabs) * double(k)) { ok = true; break; }
+        if (fabs(f) <= c_sec_tol * DBL_EPSILON * (1.0 + rho * eabs)) { ok = true; break; }
         if (f < 0.0) lo = tau; else hi = tau;
         if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) { ok = true; break; }
         // two-pole rational model through (f, f') at tau, solved for the step eta
@@ -1126,6 +1133,12 @@ bool syev_small(Ctx& c, double* B, int64_t n64, double* d_D) {
     }
     {
         Prof p2(c, "syev_stedc", 0, 0);
+        static const double sec_tol = [] {
+            const char* e = std::getenv("FRPCA_SEC_TOL");  // A/B and tests
+            return e && *e ? std::atof(e) : 8.0;
+        }();
+        const double tol = sec_tol > 0 ? sec_tol : 8.0 * double(n);  // <= 0: the old 8 k factor
+        FB_CUDA(cudaMemcpyToSymbolAsync(c_sec_tol, &tol, sizeof(double), 0, cudaMemcpyHostToDevice, s));
         k_stedc<<<1, kET, stedc_smem(), s>>>(n, dg, eo, Z, Tmp, Ut, d_D, top, info, clk.get());
         FB_LAUNCH_CHECK();
     }
