@@ -283,10 +283,29 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     std::unique_ptr<Prof> ph(new Prof(c, "upload_h2d", 8.0 * (rows + 1) + 16.0 * nnz, 0));
     FB_CUDA(cudaMemcpyAsync(A.rowptr.get(), h_rp, sizeof(int64_t) * (rows + 1),
                             cudaMemcpyHostToDevice, s));
+    // the values are first needed by the transpose's gather: they cross PCIe
+    // on the copy stream while the ids are validated and sorted
+    cudaEvent_t ev_ids = nullptr, ev_val = nullptr;
     if (nnz) {
         FB_CUDA(cudaMemcpyAsync(col64.get(), h_col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
-        FB_CUDA(cudaMemcpyAsync(A.val.get(), h_val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+        if (!c.copy) FB_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+        FB_CUDA(cudaEventCreateWithFlags(&ev_ids, cudaEventDisableTiming));
+        FB_CUDA(cudaEventCreateWithFlags(&ev_val, cudaEventDisableTiming));
+        FB_CUDA(cudaEventRecord(ev_ids, s));
+        FB_CUDA(cudaStreamWaitEvent(c.copy, ev_ids, 0));
+        FB_CUDA(cudaMemcpyAsync(A.val.get(), h_val, sizeof(double) * nnz, cudaMemcpyHostToDevice, c.copy));
+        FB_CUDA(cudaEventRecord(ev_val, c.copy));
     }
+    struct EvGuard {
+        cudaEvent_t& a;
+        cudaEvent_t& b;
+        cudaStream_t cs;
+        ~EvGuard() {
+            if (b) cudaStreamSynchronize(cs);  // an early throw must not leave the copy in flight
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } evg{ev_ids, ev_val, c.copy};
     ph.reset(new Prof(c, "upload_validate", 0, 0));
     DBuf<unsigned long long> err(2, s);
     FB_CUDA(cudaMemsetAsync(err.get(), 0xff, err.bytes(), s));
@@ -351,6 +370,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         DBuf<unsigned char> tmp(tb, s);
         FB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, A.col.get(), keys_out.get(),
                                                 perm_in.get(), perm_out.get(), nnz, 0, end_bit, s));
+        FB_CUDA(cudaStreamWaitEvent(s, ev_val, 0));
         k_gather_transpose<<<grid_for(c, nnz), 256, 0, s>>>(perm_out.get(), rowid.get(), A.val.get(),
                                                             nnz, T.col.get(), T.val.get());
         FB_LAUNCH_CHECK();

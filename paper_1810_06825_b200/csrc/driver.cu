@@ -71,7 +71,7 @@ void EigWork::run(Ctx& c, const double* W, int64_t r, int64_t n, bool row_sharde
     D.alloc(size_t(n), c.stream);
     gram_device(c, W, r, n, B.get());
     if (row_sharded) allreduce_sum(c, B.get(), n * n);  // Gram partials of the rank's rows
-    syevd_device(c, B.get(), n, D.get());
+    syevd_device(c, B.get(), n, D.get(), row_sharded);
     // rank check (dense_kernels.hpp:163-167), reported by err_check
     k_rank_check<<<1, 1, 0, c.stream>>>(D.get(), int(n), err_flag(c));
     FB_LAUNCH_CHECK();

@@ -10,13 +10,16 @@ namespace fb {
 
 bool syev_small(Ctx& c, double* B, int64_t n, double* d_D);
 
-void syevd_device(Ctx& c, double* B, int64_t n, double* d_D) {
+void syevd_device(Ctx& c, double* B, int64_t n, double* d_D, bool final_step) {
     Prof prof(c, "syevd", 8.0 * n * n * 2, 4.0 / 3.0 * n * n * n);
     // The small solver (syev.cu) by default: faster than syevd at l = 200
     // (DESIGN.md §4); its non-convergence is reported by err_check, which makes
     // the caller re-run the call with cuSOLVER (or fail, FRPCA_EIG=strict).
-    // FRPCA_EIG=cusolver forces syevd.
-    const char* mode = std::getenv("FRPCA_EIG");
+    // FRPCA_EIG=cusolver forces syevd; FRPCA_EIG_LOOP / FRPCA_EIG_FINAL
+    // (cusolver | small) choose per role: the power iteration's eig_svd or the
+    // final one (A/B of accuracy against the arbiter).
+    const char* mode = std::getenv(final_step ? "FRPCA_EIG_FINAL" : "FRPCA_EIG_LOOP");
+    if (!mode || !*mode) mode = std::getenv("FRPCA_EIG");
     if (!(mode && std::strcmp(mode, "cusolver") == 0)) {
         if (syev_small(c, B, n, d_D)) return;
     }

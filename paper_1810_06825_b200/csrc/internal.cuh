@@ -207,7 +207,7 @@ struct RetryCall : std::runtime_error {
 
 // ---- eig.cu : symmetric eigensolve of column-major n x n B (lower used):
 // V (column-major) eigenvectors, D ascending eigenvalues (device), D copied to h_D.
-void syevd_device(Ctx& c, double* B_inout_V, int64_t n, double* d_D);
+void syevd_device(Ctx& c, double* B_inout_V, int64_t n, double* d_D, bool final_step = false);
 
 // ---- csr.cu : from_triplets (sparse_matrix.hpp:62-95) on the device; host
 // outputs row_ptr (rows + 1), col_idx / values (>= nnz entries; n suffices).

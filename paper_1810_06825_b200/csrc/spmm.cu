@@ -64,25 +64,7 @@ struct Vec<1> {
 // for the others).
 struct Hot {
     uint64_t keep, stream;
-    // L2 prefetch of the gathered rows `pf` nonzeros ahead of the warp's
-    // position in its work item (cp.async.bulk.prefetch, pf_bytes per row;
-    // pf = 0: off). No register or shared-memory cost: the demand loads of a
-    // later group then find their rows in L2 instead of waiting on HBM.
-    int pf;
-    uint32_t pf_bytes;
 };
-
-__device__ __forceinline__ void prefetch_rows(const int32_t* __restrict__ col, const double* __restrict__ X,
-                                              int64_t ldx, int64_t& pfc, int64_t want, int lane, const Hot& hot) {
-    const int64_t n = want - pfc;
-    if (n <= 0) return;
-    if (lane < n) {
-        const int32_t cc = __ldg(col + pfc + lane) & 0x7fffffff;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X + int64_t(cc) * ldx), "r"(hot.pf_bytes)
-                     : "memory");
-    }
-    pfc += n < 32 ? n : 32;
-}
 
 // Gather modes: plain ids; ids whose sign bit marks an L2-hot X row
 // (DCsr::hint_h): hot rows are loaded with an evict_last policy, the others
@@ -118,7 +100,7 @@ __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
                                                const double* __restrict__ val, int64_t p0, int64_t p1,
                                                const double* __restrict__ X, int64_t ldx,
                                                int lane, int ncols, const Hot& hot,
-                                               typename Vec<VEC>::T (&acc)[NCH], int64_t& pfc, int64_t pend) {
+                                               typename Vec<VEC>::T (&acc)[NCH]) {
     using V = Vec<VEC>;
     using T = typename V::T;
     bool ok[NCH];
@@ -135,7 +117,6 @@ __device__ __forceinline__ void row_accumulate(const int32_t* __restrict__ col,
         }
         int j = 0;
         for (; j + 4 <= cnt; j += 4) {
-            if (VEC == 2 && hot.pf) prefetch_rows(col, X, ldx, pfc, min(pend, base + j + 4 + hot.pf), lane, hot);
             int c[4];
             double v[4];
 #pragma unroll
@@ -201,18 +182,12 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
     for (; it < nitems;) {
         const WorkItem w = items[it];
         if (w.r1 >= 0) {
-            // prefetch cursor over the item's nonzeros (its rows are consecutive,
-            // so their nonzeros are one contiguous range)
-            int64_t pfc = rowptr[w.r0];
-            const int64_t pend = rowptr[w.r1];
             for (int32_t r = w.r0; r < w.r1; ++r) {
                 if (skip && skip[r]) continue;  // served by the streaming path
                 T acc[NCH];
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
-                if (pfc < rowptr[r]) pfc = rowptr[r];
-                row_accumulate<VEC, NCH, MODE>(col, val, rowptr[r], rowptr[r + 1], X, ldx, lane, ncols, hot, acc,
-                                               pfc, pend);
+                row_accumulate<VEC, NCH, MODE>(col, val, rowptr[r], rowptr[r + 1], X, ldx, lane, ncols, hot, acc);
                 double* yr = Y + int64_t(r) * ldy + lane * VEC;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch)
@@ -222,8 +197,7 @@ __device__ __forceinline__ void spmm_items(const int64_t* __restrict__ rowptr, c
             T acc[NCH];
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
-            int64_t pfc = w.p0;
-            row_accumulate<VEC, NCH, MODE>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc, pfc, w.p1);
+            row_accumulate<VEC, NCH, MODE>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc);
             const int64_t slot = -int64_t(w.r1) - 1;
             double* pr = part + slot * ncols + lane * VEC;
 #pragma unroll
@@ -246,9 +220,8 @@ __global__ void __launch_bounds__(kThreads, 4)
 k_spmm(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
        const double* __restrict__ val, const WorkItem* __restrict__ items, int64_t nitems,
        const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
-       double* __restrict__ part, int ncols, const uint8_t* __restrict__ skip, int32_t* __restrict__ counter,
-       int pf) {
-    Hot hot{0, 0, pf, uint32_t(ncols) * 8u};
+       double* __restrict__ part, int ncols, const uint8_t* __restrict__ skip, int32_t* __restrict__ counter) {
+    Hot hot{0, 0};
     if (MODE == MODE_HINT) make_policies(hot);
     spmm_items<VEC, NCH, MODE>(rowptr, col, val, items, nitems, X, ldx, Y, ldy, part, ncols, hot, skip, counter);
 }
@@ -443,11 +416,11 @@ template <int NCH>
 __global__ void __launch_bounds__(kThreads, 4)
 k_spmm_panels(const int32_t* __restrict__ col, const double* __restrict__ val,
               const WorkItem* __restrict__ items, int64_t nitems, const double* __restrict__ X, int64_t ldx,
-              double* __restrict__ part, int ncols, int32_t* __restrict__ counter, int pf) {
+              double* __restrict__ part, int ncols, int32_t* __restrict__ counter) {
     using V = Vec<2>;
     using T = V::T;
     const int lane = threadIdx.x & 31;
-    const Hot hot{0, 0, pf, uint32_t(ncols) * 8u};
+    const Hot hot{0, 0};
     for (;;) {
         int it = 0;
         if (lane == 0) it = atomicAdd(counter, 1);
@@ -457,21 +430,12 @@ k_spmm_panels(const int32_t* __restrict__ col, const double* __restrict__ val,
         T acc[NCH];
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
-        int64_t pfc = w.p0;
-        row_accumulate<2, NCH, MODE_PLAIN>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc, pfc, w.p1);
+        row_accumulate<2, NCH, MODE_PLAIN>(col, val, w.p0, w.p1, X, ldx, lane, ncols, hot, acc);
         double* pr = part + (-int64_t(w.r1) - 1) * ncols + lane * 2;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
             if ((ch * 32 + lane) * 2 < ncols) V::store(pr + ch * 64, acc[ch]);
     }
-}
-
-// L2 prefetch distance of the gathers (FRPCA_SPMM_PF nonzeros ahead, 0 off):
-// bulk prefetches need 16-byte aligned rows of a multiple of 16 bytes
-int prefetch_distance(int vec, int ncols, int64_t ldx, const double* X) {
-    const int pf = int(env_double("FRPCA_SPMM_PF", 8.0));
-    const bool aligned = vec == 2 && ncols % 2 == 0 && ldx % 2 == 0 && (reinterpret_cast<uintptr_t>(X) % 16) == 0;
-    return aligned && pf > 0 ? pf : 0;
 }
 
 template <int VEC, int NCH, int MODE>
@@ -499,7 +463,7 @@ void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip,
     }
     k_spmm<VEC, NCH, MODE><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
                                                            L.items.get(), L.nitems, X, ldx, Y, ldy, part,
-                                                           ncols, skip, counter, prefetch_distance(VEC, ncols, ldx, X));
+                                                           ncols, skip, counter);
     FB_LAUNCH_CHECK();
 }
 
@@ -568,7 +532,7 @@ void launch_panels(Ctx& c, const DCsr& T, const double* Y, int64_t ldy, double* 
     const int grid = c.num_sms * 4;
     auto go = [&](auto kern) {
         kern<<<grid, kThreads, 0, c.stream>>>(T.col.get(), T.val.get(), P.hot.items.get(), P.hot.nitems, Y, ldy,
-                                              part, nc, P.counter.get(), prefetch_distance(2, nc, ldy, Y));
+                                              part, nc, P.counter.get());
         FB_LAUNCH_CHECK();
     };
     switch ((nc + 63) / 64) {
