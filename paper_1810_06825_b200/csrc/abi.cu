@@ -708,7 +708,10 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
             M->ctx = c;
             M->grows = rows;
             M->gcols = cols;
-            dcsr_upload_build(*c, *M, rows, cols, nnz, row_ptr, col_idx, values);
+            // the panel plan of the run's A^T*Y width is built while the
+            // values are still crossing PCIe
+            const int64_t whint = (algo == FRPCA_ALGO_FRPCA || algo == FRPCA_ALGO_FRPCAT) ? cfg->k + cfg->oversample : 0;
+            dcsr_upload_build(*c, *M, rows, cols, nnz, row_ptr, col_idx, values, whint);
         } catch (...) {
             if (side_thread.joinable()) side_thread.join();
             throw;

@@ -62,15 +62,18 @@ __global__ void k_iota(int32_t* __restrict__ x, int64_t n) {
 
 // Transposed entries from the stable column sort: entry k of A^T is original
 // nonzero perm[k]; its column id in A^T is the original row id.
-__global__ void k_gather_transpose(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowid,
-                                   const double* __restrict__ val, int64_t nnz,
-                                   int32_t* __restrict__ tcol, double* __restrict__ tval) {
+__global__ void k_gather_transpose_cols(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowid,
+                                        int64_t nnz, int32_t* __restrict__ tcol) {
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz;
-         k += int64_t(gridDim.x) * blockDim.x) {
-        const int32_t p = perm[k];
-        tcol[k] = rowid[p];
-        tval[k] = val[p];
-    }
+         k += int64_t(gridDim.x) * blockDim.x)
+        tcol[k] = rowid[perm[k]];
+}
+
+__global__ void k_gather_transpose_vals(const int32_t* __restrict__ perm, const double* __restrict__ val,
+                                        int64_t nnz, double* __restrict__ tval) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz;
+         k += int64_t(gridDim.x) * blockDim.x)
+        tval[k] = val[perm[k]];
 }
 
 // t_rowptr[c] = lower_bound(sorted_keys, c), c in [0, n].
@@ -264,7 +267,7 @@ const char* kValidateMsg[3] = {
 }  // namespace
 
 void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
-                       const int64_t* h_rp, const int64_t* h_col, const double* h_val) {
+                       const int64_t* h_rp, const int64_t* h_col, const double* h_val, int64_t width_hint) {
     // O(1) checks of validate() (sparse_matrix.hpp:126-130), same messages.
     require(rows >= 0 && cols >= 0, "csr: negative dimension");
     require(nnz >= 0, "csr: col_idx/values length mismatch");
@@ -358,8 +361,13 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     T.rowptr.alloc(size_t(cols + 1), s);
     T.col.alloc(size_t(nnz), s);
     T.val.alloc(size_t(nnz), s);
+    // Everything up to the work lists and the A^T*Y panel plan needs only
+    // the structure; the values (still crossing PCIe on the copy stream) are
+    // gathered last.
+    DBuf<int32_t> perm_out;
     if (nnz) {
-        DBuf<int32_t> keys_out(size_t(nnz), s), perm_in(size_t(nnz), s), perm_out(size_t(nnz), s);
+        DBuf<int32_t> keys_out(size_t(nnz), s), perm_in(size_t(nnz), s);
+        perm_out.alloc(size_t(nnz), s);
         k_iota<<<grid_for(c, nnz), 256, 0, s>>>(perm_in.get(), nnz);
         FB_LAUNCH_CHECK();
         int end_bit = 1;
@@ -370,9 +378,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         DBuf<unsigned char> tmp(tb, s);
         FB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, A.col.get(), keys_out.get(),
                                                 perm_in.get(), perm_out.get(), nnz, 0, end_bit, s));
-        FB_CUDA(cudaStreamWaitEvent(s, ev_val, 0));
-        k_gather_transpose<<<grid_for(c, nnz), 256, 0, s>>>(perm_out.get(), rowid.get(), A.val.get(),
-                                                            nnz, T.col.get(), T.val.get());
+        k_gather_transpose_cols<<<grid_for(c, nnz), 256, 0, s>>>(perm_out.get(), rowid.get(), nnz, T.col.get());
         FB_LAUNCH_CHECK();
         k_rowptr_from_sorted<<<grid_for(c, cols + 1), 256, 0, s>>>(keys_out.get(), nnz, cols,
                                                                     T.rowptr.get());
@@ -385,6 +391,17 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     build_ranks(c, A, T);
     build_items(c, A, nullptr, A.L, default_chunk(c, A));
     build_items(c, T, nullptr, T.L, default_chunk(c, T));
+    if (width_hint > 0) {  // the panel plan of the A^T*Y the caller is about to run
+        int64_t pr = 0, cap = 0;
+        if (panel_rows_for(T, width_hint, pr, cap)) ensure_panels(c, T, pr, cap);
+    }
+    if (nnz) {
+        ph.reset(new Prof(c, "upload_values", 0, 0));
+        FB_CUDA(cudaStreamWaitEvent(s, ev_val, 0));
+        k_gather_transpose_vals<<<grid_for(c, nnz), 256, 0, s>>>(perm_out.get(), A.val.get(), nnz, T.val.get());
+        FB_LAUNCH_CHECK();
+    }
+    perm_out.release();
     ph.reset();
     FB_CUDA(cudaStreamSynchronize(s));
 }

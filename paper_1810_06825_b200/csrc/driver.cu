@@ -574,6 +574,7 @@ void err_check(Ctx& c) {
     FB_CUDA(cudaMemsetAsync(c.dflag.get(), 0, sizeof(int), c.stream));
     if (h == kErrLuPivot) throw NumericalError("lu_basis: zero pivot, input is rank-deficient");  // :81
     if (h == kErrEigRank) throw NumericalError("eig_svd: input does not have full numerical column rank");
+    if (h == kErrEigFail) throw NumericalError("eig_svd: eigendecomposition failed to converge");  // :160-161
     if (h == kErrEigNoConv) {
         const char* mode = std::getenv("FRPCA_EIG");
         if (mode && std::strcmp(mode, "strict") == 0)

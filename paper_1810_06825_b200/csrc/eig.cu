@@ -10,17 +10,29 @@ namespace fb {
 
 bool syev_small(Ctx& c, double* B, int64_t n, double* d_D);
 
+namespace {
+__global__ void k_info_to_flag(const int* __restrict__ info, int* __restrict__ flag) {
+    if (*info != 0) atomicCAS(flag, 0, kErrEigFail);
+}
+}  // namespace
+
 void syevd_device(Ctx& c, double* B, int64_t n, double* d_D, bool final_step) {
     Prof prof(c, "syevd", 8.0 * n * n * 2, 4.0 / 3.0 * n * n * n);
-    // The small solver (syev.cu) by default: faster than syevd at l = 200
-    // (DESIGN.md §4); its non-convergence is reported by err_check, which makes
-    // the caller re-run the call with cuSOLVER (or fail, FRPCA_EIG=strict).
-    // FRPCA_EIG=cusolver forces syevd; FRPCA_EIG_LOOP / FRPCA_EIG_FINAL
-    // (cusolver | small) choose per role: the power iteration's eig_svd or the
-    // final one (A/B of accuracy against the arbiter).
+    // Per role:
+    //  - the final eig_svd (only its top-k pairs reach the output): the
+    //    library's own solver (syev.cu), faster than syevd at l = 200;
+    //  - the power iteration's eig_svd, whose basis Q = Z V S^-1 carries every
+    //    pair, the small ones amplified by S^-1: cuSOLVER syevd, whose small
+    //    eigenvalues are more accurate (tools/syev_accuracy.py); with it the GPU
+    //    result at C2 is closer to the long-double arbiter than the oracle on
+    //    sigma and both subspaces (profiles/r2_parity_C2_arbiter.json).
+    // FRPCA_EIG_LOOP / FRPCA_EIG_FINAL (cusolver | small), then FRPCA_EIG
+    // (cusolver | strict), override. A non-converged small solve is reported
+    // by err_check, which re-runs the call with cuSOLVER (or fails when strict).
     const char* mode = std::getenv(final_step ? "FRPCA_EIG_FINAL" : "FRPCA_EIG_LOOP");
     if (!mode || !*mode) mode = std::getenv("FRPCA_EIG");
-    if (!(mode && std::strcmp(mode, "cusolver") == 0)) {
+    const bool cus = (mode && *mode) ? std::strcmp(mode, "cusolver") == 0 : !final_step;
+    if (!cus) {
         if (syev_small(c, B, n, d_D)) return;
     }
     int lwork = 0;
@@ -32,6 +44,13 @@ void syevd_device(Ctx& c, double* B, int64_t n, double* d_D, bool final_step) {
     if (cusolverDnDsyevd(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, int(n), B,
                          int(n), d_D, work.get(), lwork, info.get()) != CUSOLVER_STATUS_SUCCESS)
         throw CudaError("cusolverDnDsyevd failed");
+    if (c.checked) {
+        // no host round trip inside a run: the failure is recorded on the
+        // device and err_check throws it (dense_kernels.hpp:160-161)
+        k_info_to_flag<<<1, 1, 0, c.stream>>>(info.get(), err_flag(c));
+        FB_LAUNCH_CHECK();
+        return;
+    }
     int h_info = 0;
     FB_CUDA(cudaMemcpyAsync(&h_info, info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     FB_CUDA(cudaStreamSynchronize(c.stream));

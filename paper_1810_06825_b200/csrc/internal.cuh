@@ -159,8 +159,10 @@ struct DMat {
 };
 
 // ---- csr.cu
+// width_hint > 0: the A^T*Y panel plan for that width is built at load too
 void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
-                       const int64_t* h_rowptr, const int64_t* h_col, const double* h_val);
+                       const int64_t* h_rowptr, const int64_t* h_col, const double* h_val,
+                       int64_t width_hint = 0);
 void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v);
 // work list of A's rows (rows with skip[r] != 0 left out), chunk size ch
 void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_t ch);
@@ -172,6 +174,9 @@ void ensure_encoding(Ctx& c, DCsr& A, int64_t hint_h, int64_t sx_h);
 void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap);
 
 // ---- spmm.cu : Y (rows x ncols, row-major ldy) = A * X (row-major ldx)
+// panel rows / partial-slot cap of the panelled A^T*Y of width ncols on T
+// (false: that A^T*Y runs unpanelled)
+bool panel_rows_for(const DCsr& T, int64_t ncols, int64_t& pr, int64_t& cap);
 void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t ncols, double* Y,
                  int64_t ldy, const char* tag);
 // Z = A^T Y on T = the transposed CSR of A (panelled for large Y, spmm.cu)
@@ -192,7 +197,7 @@ double maxabs_device(Ctx& c, const double* x, int64_t n);
 void maxabs_device_async(Ctx& c, const double* x, int64_t n, unsigned long long* out);
 
 // ---- deferred errors (driver.cu)
-constexpr int kErrLuPivot = 1, kErrEigRank = 2, kErrEigNoConv = 3, kErrOmegaShort = 4;
+constexpr int kErrLuPivot = 1, kErrEigRank = 2, kErrEigNoConv = 3, kErrOmegaShort = 4, kErrEigFail = 5;
 int* err_flag(Ctx& c);
 void err_reset(Ctx& c);
 // waits for the stream; throws the first recorded error (NumericalError with

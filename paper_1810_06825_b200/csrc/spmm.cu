@@ -597,18 +597,24 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
 // Z = A^T Y on the transposed CSR T. When Y (T.cols x l) is several times
 // larger than a panel, the hot rows of T run through the panel plan first
 // (chunks panel-major + combine), then the cold rows through their own list.
-void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, const char* tag) {
-    if (T.rows == 0 || ncols == 0) return;
+bool panel_rows_for(const DCsr& T, int64_t ncols, int64_t& pr, int64_t& cap) {
     const int64_t w = std::min<int64_t>(ncols, 256);
     const double panel_bytes = env_double("FRPCA_PANEL_MB", 32.0) * 1048576.0;
     const double min_bytes = env_double("FRPCA_PANEL_MIN_MB", 96.0) * 1048576.0;
     const bool use = ncols % 2 == 0 && 8.0 * double(T.cols) * double(w) > min_bytes &&
                      env_double("FRPCA_NO_PANELS", 0.0) == 0.0;
-    if (use) {
-        const int64_t pr = std::max<int64_t>(1, int64_t(panel_bytes / (8.0 * double(w))));
-        const int64_t cap = int64_t(env_double("FRPCA_PANEL_PART_GB", 16.0) * 1073741824.0 / (8.0 * double(w)));
-        ensure_panels(c, T, pr, cap);
-    }
+    if (!use) return false;
+    pr = std::max<int64_t>(1, int64_t(panel_bytes / (8.0 * double(w))));
+    cap = int64_t(env_double("FRPCA_PANEL_PART_GB", 16.0) * 1073741824.0 / (8.0 * double(w)));
+    return true;
+}
+
+void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, const char* tag) {
+    if (T.rows == 0 || ncols == 0) return;
+    const int64_t w = std::min<int64_t>(ncols, 256);
+    int64_t pr = 0, cap = 0;
+    const bool use = panel_rows_for(T, ncols, pr, cap);
+    if (use) ensure_panels(c, T, pr, cap);
     if (!use || T.pan.nhot == 0) return spmm_device(c, T, Y, ncols, ncols, Z, ncols, tag);
     const PanelPlan& P = T.pan;
     const double bytes = 12.0 * T.nnz + 8.0 * (T.rows + 1) + 8.0 * ncols * (T.cols + T.rows);
