@@ -430,7 +430,8 @@ def run_gpu_arm(args, cfg):
                         "per_kernel": l2_gathers},
         "e2e": {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "statistic": "median of steps",
-                "mean": round(e2e_mean_s, 6), "call": "frpca_run_csr" if world == 1 else "frpca_dmat_upload_shard + frpca_run"},
+                "mean": round(e2e_mean_s, 6), "steps_ms": [round(x, 2) for x in e2e_ms],
+                "call": "frpca_run_csr" if world == 1 else "frpca_dmat_upload_shard + frpca_run"},
         "gpu_launches": int((lc1.value - lc0.value) // max(1, args.steps)),
         "passes_over_matrix": int(passes),
         "kernels": kernels,

@@ -360,6 +360,188 @@ k_gram3(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
         }
 }
 
+// ---------------------------------------------------------------------------
+// Gram v4: k_gram3's warps and DMMA sequence, fed by the Blackwell async copy
+// path instead of a block-wide cp.async pipeline. Each W row goes to its
+// padded shared-memory slot with a 1-D bulk copy (cp.async.bulk, SASS UBLKCP)
+// that completes on the stage's "full" mbarrier; the warps wait on that
+// barrier, run their DMMAs, and release the stage on its "empty" mbarrier. No block-wide barrier and no per-element
+// index arithmetic remain in the loop. Per tile, the DMMAs are issued in the
+// same order over the same 4-row groups as k_gram3 (tail rows zero-filled the
+// same way), so the partials and the result are bitwise equal to it.
+constexpr int G4_ROWS = 32;
+constexpr int G4_STAGES = 4;
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(b))),
+                 "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(b))),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(b)))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "W: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W;\n}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(bytes), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+
+// Warp 0 (a diagonal block: 15 DMMAs per k4 step where the others issue 25)
+// doubles as the producer, so the CTA keeps k_gram3's 15 warps and register
+// budget: at step st it refills the slot step st - 1 used (after every warp
+// released it) with step st + STAGES - 1, then computes step st.
+__device__ __forceinline__ void gram4_fill(const double* __restrict__ W, int n, int S, int64_t rs, int64_t re,
+                                           int st, double* sm, uint64_t* full, int lane) {
+    const int slot = int(st % G4_STAGES);
+    const int64_t k0 = rs + st * G4_ROWS;
+    const int valid = int(min(int64_t(G4_ROWS), re - k0));
+    double* dst = sm + size_t(slot) * G4_ROWS * S;
+    // rows past the CTA's range read as zero (as k_gram3's zero-size copies)
+    for (int e = lane; e < (G4_ROWS - valid) * n; e += 32) dst[(valid + e / n) * S + e % n] = 0.0;
+    __syncwarp();
+    if (lane == 0) mbar_expect_tx(full + slot, unsigned(valid) * unsigned(n) * 8u);
+    __syncwarp();
+    for (int kr = lane; kr < valid; kr += 32) bulk_g2s(dst + kr * S, W + (k0 + kr) * n, unsigned(n) * 8u, full + slot);
+}
+
+// 15 warps x 136 registers fill the register file exactly (the producer's
+// bookkeeping does not fit in k_gram3's 128 without spilling)
+template <int NBR>
+__global__ void __maxnreg__(NBR == 5 ? 136 : 168)
+k_gram4(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_cta, double* __restrict__ part) {
+    extern __shared__ __align__(128) double sm[];  // [G4_STAGES][G4_ROWS][S], then the barriers
+    constexpr int NW = NBR * (NBR + 1) / 2;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + size_t(G4_STAGES) * G4_ROWS * S);
+    uint64_t* empty = full + G4_STAGES;
+    const int T = (n + 7) / 8;
+    const int NT = T * (T + 1) / 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t rs = int64_t(blockIdx.x) * rows_per_cta;
+    const int64_t re = min(r, rs + rows_per_cta);
+    const int ncol = 8 * G3_BT * NBR;
+    const int64_t nsteps = (re - rs + G4_ROWS - 1) / G4_ROWS;
+    // padding columns [n, ncol) are never written by the copies: zero once
+    for (int e = tid; e < G4_STAGES * G4_ROWS * (ncol - n); e += blockDim.x) {
+        const int q = e / (ncol - n), cc = n + e % (ncol - n);
+        sm[size_t(q) * S + cc] = 0.0;
+    }
+    if (tid == 0) {
+        for (int st = 0; st < G4_STAGES; ++st) {
+            mbar_init(full + st, 1);
+            mbar_init(empty + st, NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int nst = int(nsteps);
+    if (warp == 0)
+        for (int st = 0; st < min(nst, G4_STAGES - 1); ++st) gram4_fill(W, n, S, rs, re, st, sm, full, lane);
+    int bi = 0;
+    while ((bi + 1) * (bi + 2) / 2 <= warp) ++bi;
+    const int bj = warp - bi * (bi + 1) / 2;
+    const bool diag = bi == bj;
+    double acc[G3_BT][G3_BT][2];
+#pragma unroll
+    for (int a = 0; a < G3_BT; ++a)
+#pragma unroll
+        for (int b = 0; b < G3_BT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const int coff = (lane & 3) * S + (lane >> 2);
+    int slot = 0;
+    unsigned phase = 0;  // parity of the current pass over the stage ring
+    for (int st = 0; st < nst; ++st) {
+        if (warp == 0 && st + G4_STAGES - 1 < nst) {
+            if (st >= 1) {
+                const int ps = slot == 0 ? G4_STAGES - 1 : slot - 1;
+                mbar_wait(empty + ps, slot == 0 ? phase ^ 1u : phase);
+            }
+            gram4_fill(W, n, S, rs, re, st + G4_STAGES - 1, sm, full, lane);
+        }
+        mbar_wait(full + slot, phase);
+        const double* Ws = sm + size_t(slot) * G4_ROWS * S + coff;
+        if (diag) {
+#pragma unroll
+            for (int kk = 0; kk < G4_ROWS / 4; ++kk) {
+                const double* rowp = Ws + kk * 4 * S + bi * 40;
+                double f[G3_BT];
+#pragma unroll
+                for (int a = 0; a < G3_BT; ++a) f[a] = rowp[a * 8];
+#pragma unroll
+                for (int a = 0; a < G3_BT; ++a)
+#pragma unroll
+                    for (int b = 0; b <= a; ++b) dmma(acc[a][b], f[a], f[b]);
+            }
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < G4_ROWS / 4; ++kk) {
+                const double* rowp = Ws + kk * 4 * S;
+                double fa[G3_BT];
+#pragma unroll
+                for (int a = 0; a < G3_BT; ++a) fa[a] = rowp[bi * 40 + a * 8];
+#pragma unroll
+                for (int b = 0; b < G3_BT; ++b) {
+                    const double fb = rowp[bj * 40 + b * 8];
+#pragma unroll
+                    for (int a = 0; a < G3_BT; ++a) dmma(acc[a][b], fa[a], fb);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);
+        if (++slot == G4_STAGES) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+    double* out = part + size_t(blockIdx.x) * NT * 64;
+    const int ii = lane >> 2, jj = (lane & 3) * 2;
+#pragma unroll
+    for (int a = 0; a < G3_BT; ++a)
+#pragma unroll
+        for (int b = 0; b < G3_BT; ++b) {
+            const int ti = bi * G3_BT + a, tj = bj * G3_BT + b;
+            if (ti >= T || tj > ti || (diag && b > a)) continue;
+            const int t = ti * (ti + 1) / 2 + tj;
+            *reinterpret_cast<double2*>(out + size_t(t) * 64 + ii * 8 + jj) = make_double2(acc[a][b][0], acc[a][b][1]);
+        }
+}
+
+template <int NBR>
+void launch_gram4(Ctx& c, const double* W, int64_t r, int n, double* B) {
+    constexpr int NW = NBR * (NBR + 1) / 2;
+    const int T = (n + 7) / 8, NT = T * (T + 1) / 2;
+    const int ncol = 8 * G3_BT * NBR;
+    const int S = ncol + ((12 - (ncol % 16)) + 16) % 16;
+    const size_t smem = sizeof(double) * size_t(G4_STAGES) * G4_ROWS * S + 2 * G4_STAGES * sizeof(uint64_t);
+    smem_optin(k_gram4<NBR>, smem);
+    // the same 32-row CTA split as k_gram3 (identical partials)
+    int64_t nctas = std::min<int64_t>(c.num_sms, std::max<int64_t>(1, (r + G3_ROWS - 1) / G3_ROWS));
+    const int64_t rpc = ((r + nctas - 1) / nctas + G3_ROWS - 1) / G3_ROWS * G3_ROWS;
+    nctas = std::max<int64_t>(1, (r + rpc - 1) / rpc);
+    DBuf<double> part(size_t(nctas) * NT * 64, c.stream);
+    k_gram4<NBR><<<unsigned(nctas), NW * 32, smem, c.stream>>>(W, r, n, S, rpc, part.get());
+    FB_LAUNCH_CHECK();
+    const int outs = NT * 64;
+    k_gram2_reduce<<<(outs + 255) / 256, 256, 0, c.stream>>>(part.get(), int(nctas), n, B);
+    FB_LAUNCH_CHECK();
+}
+
 template <int NBR, int ROWS>
 void launch_gram3_rows(Ctx& c, const double* W, int64_t r, int n, double* B) {
     constexpr int NW = NBR * (NBR + 1) / 2;
@@ -757,6 +939,14 @@ void gram_device(Ctx& c, const double* W, int64_t r, int64_t n, double* B) {
         const bool g2 = std::getenv("FRPCA_GRAM2") != nullptr;  // tests compare both kernels
         if (!g2 && n % 2 == 0 && r >= 4096) {
             const int nbr = (T + G3_BT - 1) / G3_BT;
+            // the bulk-copy kernel needs 16-byte rows and addresses
+            const char* g3 = std::getenv("FRPCA_GRAM3");  // A/B and tests
+            const bool bulk = !(g3 && *g3 == '1') && (reinterpret_cast<uintptr_t>(W) % 16) == 0;
+            if (bulk) {
+                if (nbr == 5) return launch_gram4<5>(c, W, r, int(n), B);
+                if (nbr == 4) return launch_gram4<4>(c, W, r, int(n), B);
+                if (nbr == 3) return launch_gram4<3>(c, W, r, int(n), B);
+            }
             if (nbr == 5) return launch_gram3<5>(c, W, r, int(n), B);
             if (nbr == 4) return launch_gram3<4>(c, W, r, int(n), B);
             if (nbr == 3) return launch_gram3<3>(c, W, r, int(n), B);

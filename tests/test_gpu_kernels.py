@@ -458,6 +458,21 @@ def test_gram3_equals_gram2(fb, orc, monkeypatch, m, n):
 
 
 
+@pytest.mark.parametrize("m,n", [(4096, 80), (5000, 120), (70001, 150), (123457, 200), (4100, 200)])
+def test_gram4_bulk_copies_equal_gram3(fb, orc, monkeypatch, m, n):
+    """The Gram fed by 1-D bulk copies and mbarriers (k_gram4) issues the same
+    DMMAs per tile over the same 4-row groups as k_gram3 (zero-filled tail
+    rows included): bitwise equal eig_svd results; CTA row ranges that are
+    not whole stages, odd row counts and widths with zero padding columns."""
+    A = orc.gaussian_matrix(m, n, m + 7 * n)
+    monkeypatch.setenv("FRPCA_GRAM3", "1")
+    r1 = fb.eig_svd(A)
+    monkeypatch.delenv("FRPCA_GRAM3")
+    r2 = fb.eig_svd(A)
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
+
+
 @pytest.mark.parametrize("n", [3, 4, 5, 33, 64, 150, 200, 213, 214, 232])
 def test_sytrd_fused_vs_unfused(fb, orc, monkeypatch, n):
     """The fused tridiagonalisation (rank-2 update of step j and symmetric
