@@ -403,14 +403,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  : "memory");
 }
 
-// Warp 0 (a diagonal block: 15 DMMAs per k4 step where the others issue 25)
-// doubles as the producer, so the CTA keeps k_gram3's 15 warps and register
-// budget: at step st it refills the slot step st - 1 used (after every warp
-// released it) with step st + STAGES - 1, then computes step st.
+// A 16th warp is the producer (15 consumer warps + 1 = 512 threads at 128
+// registers: a 15-warp CTA at 136 would put 4 x 136-register warps on one
+// SM sub-partition, more than its 16K registers).
 __device__ __forceinline__ void gram4_fill(const double* __restrict__ W, int n, int S, int64_t rs, int64_t re,
-                                           int st, double* sm, uint64_t* full, int lane) {
-    const int slot = int(st % G4_STAGES);
-    const int64_t k0 = rs + st * G4_ROWS;
+                                           int st, int slot, double* sm, uint64_t* full, int lane) {
+    const int64_t k0 = rs + int64_t(st) * G4_ROWS;
     const int valid = int(min(int64_t(G4_ROWS), re - k0));
     double* dst = sm + size_t(slot) * G4_ROWS * S;
     // rows past the CTA's range read as zero (as k_gram3's zero-size copies)
@@ -421,26 +419,30 @@ __device__ __forceinline__ void gram4_fill(const double* __restrict__ W, int n, 
     for (int kr = lane; kr < valid; kr += 32) bulk_g2s(dst + kr * S, W + (k0 + kr) * n, unsigned(n) * 8u, full + slot);
 }
 
-// 15 warps x 136 registers fill the register file exactly (the producer's
-// bookkeeping does not fit in k_gram3's 128 without spilling)
 template <int NBR>
-__global__ void __maxnreg__(NBR == 5 ? 136 : 168)
-k_gram4(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_cta, double* __restrict__ part) {
+constexpr int g4_stride() {  // padded row stride: 12 mod 16 doubles, conflict-free fragments
+    return 8 * G3_BT * NBR + ((12 - ((8 * G3_BT * NBR) % 16)) + 16) % 16;
+}
+
+template <int NBR>
+__global__ void __launch_bounds__((NBR * (NBR + 1) / 2 + 1) * 32, 1)
+k_gram4(const double* __restrict__ W, int64_t r, int n, int64_t rows_per_cta, double* __restrict__ part) {
     extern __shared__ __align__(128) double sm[];  // [G4_STAGES][G4_ROWS][S], then the barriers
     constexpr int NW = NBR * (NBR + 1) / 2;
+    constexpr int S = g4_stride<NBR>();
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + size_t(G4_STAGES) * G4_ROWS * S);
     uint64_t* empty = full + G4_STAGES;
-    const int T = (n + 7) / 8;
-    const int NT = T * (T + 1) / 2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t rs = int64_t(blockIdx.x) * rows_per_cta;
     const int64_t re = min(r, rs + rows_per_cta);
-    const int ncol = 8 * G3_BT * NBR;
-    const int64_t nsteps = (re - rs + G4_ROWS - 1) / G4_ROWS;
-    // padding columns [n, ncol) are never written by the copies: zero once
-    for (int e = tid; e < G4_STAGES * G4_ROWS * (ncol - n); e += blockDim.x) {
-        const int q = e / (ncol - n), cc = n + e % (ncol - n);
-        sm[size_t(q) * S + cc] = 0.0;
+    const int nst = int((re - rs + G4_ROWS - 1) / G4_ROWS);
+    {
+        // padding columns [n, ncol) are never written by the copies: zero once
+        const int ncol = 8 * G3_BT * NBR;
+        for (int e = tid; e < G4_STAGES * G4_ROWS * (ncol - n); e += blockDim.x) {
+            const int q = e / (ncol - n), cc = n + e % (ncol - n);
+            sm[size_t(q) * S + cc] = 0.0;
+        }
     }
     if (tid == 0) {
         for (int st = 0; st < G4_STAGES; ++st) {
@@ -450,9 +452,19 @@ k_gram4(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int nst = int(nsteps);
-    if (warp == 0)
-        for (int st = 0; st < min(nst, G4_STAGES - 1); ++st) gram4_fill(W, n, S, rs, re, st, sm, full, lane);
+    if (warp == NW) {  // producer
+        int slot = 0;
+        unsigned phase = 0;
+        for (int st = 0; st < nst; ++st) {
+            if (st >= G4_STAGES) mbar_wait(empty + slot, phase ^ 1u);
+            gram4_fill(W, n, S, rs, re, st, slot, sm, full, lane);
+            if (++slot == G4_STAGES) {
+                slot = 0;
+                phase ^= 1u;
+            }
+        }
+        return;
+    }
     int bi = 0;
     while ((bi + 1) * (bi + 2) / 2 <= warp) ++bi;
     const int bj = warp - bi * (bi + 1) / 2;
@@ -462,23 +474,28 @@ k_gram4(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
     for (int a = 0; a < G3_BT; ++a)
 #pragma unroll
         for (int b = 0; b < G3_BT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    const int coff = (lane & 3) * S + (lane >> 2);
+    // stage and barrier addresses as 32-bit shared-window offsets (registers)
+    const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(full));
+    constexpr unsigned stage_bytes = unsigned(G4_ROWS * S) * 8u;
+    const int lane_off = (lane & 3) * S + (lane >> 2) + (diag ? bi * 40 : 0);
+    unsigned soff = 0;  // current stage, byte offset
     int slot = 0;
-    unsigned phase = 0;  // parity of the current pass over the stage ring
-    for (int st = 0; st < nst; ++st) {
-        if (warp == 0 && st + G4_STAGES - 1 < nst) {
-            if (st >= 1) {
-                const int ps = slot == 0 ? G4_STAGES - 1 : slot - 1;
-                mbar_wait(empty + ps, slot == 0 ? phase ^ 1u : phase);
-            }
-            gram4_fill(W, n, S, rs, re, st + G4_STAGES - 1, sm, full, lane);
+    unsigned phase = 0;
+    for (int st = nst; st > 0; --st) {
+        {
+            const unsigned a = full0 + 8u * unsigned(slot);
+            asm volatile(
+                "{\n .reg .pred p;\n"
+                "W4: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+                " @!p bra W4;\n}" ::"r"(a),
+                "r"(phase)
+                : "memory");
         }
-        mbar_wait(full + slot, phase);
-        const double* Ws = sm + size_t(slot) * G4_ROWS * S + coff;
+        const double* Ws = reinterpret_cast<const double*>(reinterpret_cast<const char*>(sm) + soff) + lane_off;
         if (diag) {
 #pragma unroll
             for (int kk = 0; kk < G4_ROWS / 4; ++kk) {
-                const double* rowp = Ws + kk * 4 * S + bi * 40;
+                const double* rowp = Ws + kk * 4 * S;
                 double f[G3_BT];
 #pragma unroll
                 for (int a = 0; a < G3_BT; ++a) f[a] = rowp[a * 8];
@@ -503,12 +520,19 @@ k_gram4(const double* __restrict__ W, int64_t r, int n, int S, int64_t rows_per_
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty + slot);
+        if (lane == 0) {
+            const unsigned a = full0 + 8u * unsigned(G4_STAGES + slot);
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+        }
+        soff += stage_bytes;
         if (++slot == G4_STAGES) {
             slot = 0;
+            soff = 0;
             phase ^= 1u;
         }
     }
+    const int T = (n + 7) / 8;
+    const int NT = T * (T + 1) / 2;
     double* out = part + size_t(blockIdx.x) * NT * 64;
     const int ii = lane >> 2, jj = (lane & 3) * 2;
 #pragma unroll
@@ -526,8 +550,7 @@ template <int NBR>
 void launch_gram4(Ctx& c, const double* W, int64_t r, int n, double* B) {
     constexpr int NW = NBR * (NBR + 1) / 2;
     const int T = (n + 7) / 8, NT = T * (T + 1) / 2;
-    const int ncol = 8 * G3_BT * NBR;
-    const int S = ncol + ((12 - (ncol % 16)) + 16) % 16;
+    constexpr int S = g4_stride<NBR>();
     const size_t smem = sizeof(double) * size_t(G4_STAGES) * G4_ROWS * S + 2 * G4_STAGES * sizeof(uint64_t);
     smem_optin(k_gram4<NBR>, smem);
     // the same 32-row CTA split as k_gram3 (identical partials)
@@ -535,7 +558,7 @@ void launch_gram4(Ctx& c, const double* W, int64_t r, int n, double* B) {
     const int64_t rpc = ((r + nctas - 1) / nctas + G3_ROWS - 1) / G3_ROWS * G3_ROWS;
     nctas = std::max<int64_t>(1, (r + rpc - 1) / rpc);
     DBuf<double> part(size_t(nctas) * NT * 64, c.stream);
-    k_gram4<NBR><<<unsigned(nctas), NW * 32, smem, c.stream>>>(W, r, n, S, rpc, part.get());
+    k_gram4<NBR><<<unsigned(nctas), (NW + 1) * 32, smem, c.stream>>>(W, r, n, rpc, part.get());
     FB_LAUNCH_CHECK();
     const int outs = NT * 64;
     k_gram2_reduce<<<(outs + 255) / 256, 256, 0, c.stream>>>(part.get(), int(nctas), n, B);
