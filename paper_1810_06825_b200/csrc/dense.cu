@@ -8,7 +8,11 @@
 // (16 MMAs per k4 step from 8 operand loads), operands are staged in padded
 // shared memory by a 2-stage cp.async pipeline, and split-K partials are
 // reduced in a fixed order so results are deterministic run to run.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <mutex>
 
 #include "internal.cuh"
 
@@ -895,6 +899,178 @@ k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __r
     }
 }
 
+// ---------------------------------------------------------------------------
+// The persistent GEMM fed by the Tensor Memory Accelerator: each (row block,
+// k stage) tile of W (BM rows x TK = 16 columns) arrives in shared memory with
+// one cp.async.bulk.tensor.2d (SASS UTMALDG) whose 128-byte swizzle makes the
+// fragment loads conflict-free without padding; out-of-range rows and the
+// columns past K are zero-filled by the TMA unit. Lane 0 of warp 0 issues the
+// copies (after every warp released the stage on its "empty" mbarrier); the
+// warps wait on the stage's "full" mbarrier. Same warp tiling, the same DMMAs
+// in the same k order per output tile as k_gemm_persist: bitwise equal.
+constexpr int GT_STAGES = 2;
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+        : "memory");
+}
+
+template <int RT, int NT>
+__global__ void __launch_bounds__(GP_THREADS, 1)
+k_gemm_tma(const __grid_constant__ CUtensorMap wmap, int64_t r, int K, const double* __restrict__ M, int ldm, int N,
+           double* __restrict__ C, int64_t ldc, int col_major, int WC, int SB) {
+    extern __shared__ __align__(1024) double sm_raw[];
+    // the 128-byte swizzle needs 1024-byte aligned stage tiles (1 KB of slack
+    // is allocated for this)
+    double* sm = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+    const int BM = 8 * RT * ((GP_THREADS / 32) / WC);
+    const int ntiles = (N + 7) / 8;
+    const int NP = 8 * ntiles;
+    double* Ws = sm;                                  // [GT_STAGES][BM][TK], 1024-aligned, swizzled
+    double* Ms = sm + size_t(GT_STAGES) * BM * TK;    // [K][SB]
+    uint64_t* full = reinterpret_cast<uint64_t*>(Ms + size_t(K) * SB);
+    uint64_t* empty = full + GT_STAGES;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rg = warp / WC, cgp = warp % WC;
+    for (int e = tid; e < K * NP; e += GP_THREADS) {
+        const int k = e / NP, cc = e % NP;
+        cp_async8(Ms + k * SB + cc, M + (cc < N ? int64_t(k) * ldm + cc : 0), cc < N);
+    }
+    cp_async_commit();
+    if (tid == 0) {
+        for (int st = 0; st < GT_STAGES; ++st) {
+            mbar_init(full + st, 1);
+            mbar_init(empty + st, GP_THREADS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    const int nsteps = (K + TK - 1) / TK;
+    const int64_t nblocks = (r + BM - 1) / BM;
+    const int64_t myblocks = int64_t(blockIdx.x) < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t total = myblocks * nsteps;
+    const unsigned stage_bytes = unsigned(BM) * TK * 8u;
+    auto issue = [&](int64_t g) {  // tile g of this CTA into slot g % 2
+        const int64_t blk = blockIdx.x + (g / nsteps) * int64_t(gridDim.x);
+        const int st = int(g % nsteps);
+        const int slot = int(g & 1);
+        mbar_expect_tx(full + slot, stage_bytes);
+        tma_load_2d(Ws + size_t(slot) * BM * TK, &wmap, st * TK, int(blk * BM), full + slot);
+    };
+    if (warp == 0 && lane == 0) {
+        for (int64_t g = 0; g < min(total, int64_t(GT_STAGES)); ++g) issue(g);
+    }
+    // fragment rows of this lane within the stage tile, and their swizzle key
+    const int rbase = rg * 8 * RT + (lane >> 2);
+    int64_t g = 0;
+    for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+        const int64_t r0 = blk * BM;
+        double acc[RT][NT][2];
+#pragma unroll
+        for (int a = 0; a < RT; ++a)
+#pragma unroll
+            for (int t = 0; t < NT; ++t) acc[a][t][0] = acc[a][t][1] = 0.0;
+        for (int st = 0; st < nsteps; ++st, ++g) {
+            const int slot = int(g & 1);
+            mbar_wait(full + slot, unsigned((g >> 1) & 1));
+            const char* wd = reinterpret_cast<const char*>(Ws + size_t(slot) * BM * TK);
+            const double* md = Ms + (st * TK + (lane & 3)) * SB + cgp * NT * 8 + (lane >> 2);
+#pragma unroll
+            for (int kk = 0; kk < TK / 4; ++kk) {
+                if (st * TK + kk * 4 >= K) break;
+                const int k = kk * 4 + (lane & 3);
+                double fa[RT];
+#pragma unroll
+                for (int a = 0; a < RT; ++a) {
+                    const int row = rbase + a * 8;  // row & 7 == lane >> 2 (row tiles are 8-aligned)
+                    fa[a] = *reinterpret_cast<const double*>(wd + row * 128 + ((((k >> 1) ^ (lane >> 2)) & 7) << 4) +
+                                                             ((k & 1) << 3));
+                }
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    if (cgp * NT + t < ntiles) {
+                        const double b = md[kk * 4 * SB + t * 8];
+#pragma unroll
+                        for (int a = 0; a < RT; ++a) dmma(acc[a][t], fa[a], b);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + slot);
+            if (warp == 0 && lane == 0 && g + GT_STAGES < total) {
+                mbar_wait(empty + slot, unsigned((g >> 1) & 1));  // every warp is done with tile g
+                issue(g + GT_STAGES);
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < RT; ++a)
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int64_t row = r0 + rg * 8 * RT + a * 8 + (lane >> 2);
+                const int col = (cgp * NT + t) * 8 + (lane & 3) * 2;
+                if (row >= r || cgp * NT + t >= ntiles) continue;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (col + h >= N) continue;
+                    if (col_major) C[int64_t(col + h) * ldc + row] = acc[a][t][h];
+                    else C[row * ldc + col + h] = acc[a][t][h];
+                }
+            }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// W (r x K row-major) as a 2-D tensor with boxes of TK columns x BM rows,
+// 128-byte swizzle, zero fill out of range; false if it cannot be described
+// (alignment, driver entry point)
+bool make_w_map(CUtensorMap& map, const double* W, int64_t r, int64_t K, int BM) {
+    auto enc = tensor_map_encoder();
+    if (!enc || (reinterpret_cast<uintptr_t>(W) & 15) || (K * 8) % 16 || r >= (int64_t(1) << 31)) return false;
+    const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(r)};
+    const cuuint64_t strides[1] = {cuuint64_t(K) * 8};
+    const cuuint32_t box[2] = {cuuint32_t(TK), cuuint32_t(BM)};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(W), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int RT, int NT>
+bool launch_gemm_tma(Ctx& c, const double* W, int64_t r, int64_t K, const double* M, int64_t ldm, int64_t N,
+                     double* C, int64_t ldc, bool col_major_out, int WC) {
+    const int ntiles = int((N + 7) / 8), NP = 8 * ntiles;
+    const int SB = NP + ((12 - (NP % 16)) + 16) % 16;
+    const int BM = 8 * RT * ((GP_THREADS / 32) / WC);
+    const size_t smem = sizeof(double) * (size_t(GT_STAGES) * BM * TK + size_t(K) * SB) + 4 * sizeof(uint64_t) + 1024;
+    if (smem > 227 * 1024 || BM > 256) return false;
+    CUtensorMap map;
+    if (!make_w_map(map, W, r, K, BM)) return false;
+    smem_optin(k_gemm_tma<RT, NT>, smem);
+    const int64_t nblocks = (r + BM - 1) / BM;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(c.num_sms, nblocks)));
+    k_gemm_tma<RT, NT><<<grid, GP_THREADS, smem, c.stream>>>(map, r, int(K), M, int(ldm), int(N), C, ldc,
+                                                              col_major_out ? 1 : 0, WC, SB);
+    FB_LAUNCH_CHECK();
+    return true;
+}
+
 template <int RT, int NT>
 void launch_gemm_persist(Ctx& c, const double* W, int64_t r, int64_t K, const double* M, int64_t ldm,
                          int64_t N, double* C, int64_t ldc, bool col_major_out, int WC) {
@@ -1009,9 +1185,18 @@ void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M,
             const int ntiles = int((nc + 7) / 8);
             const int WC = ntiles <= 8 ? 1 : 2;
             const int nt = (ntiles + WC - 1) / WC;
-            if (nt <= 2) launch_gemm_persist<4, 2>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
-            else if (nt <= 4) launch_gemm_persist<4, 4>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
-            else launch_gemm_persist<4, 7>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+            const char* ge = std::getenv("FRPCA_GEMM_CPASYNC");  // A/B and tests
+            const bool tma = !(ge && *ge == '1');
+            if (nt <= 2) {
+                if (!tma || !launch_gemm_tma<4, 2>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC))
+                    launch_gemm_persist<4, 2>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+            } else if (nt <= 4) {
+                if (!tma || !launch_gemm_tma<4, 4>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC))
+                    launch_gemm_persist<4, 4>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+            } else {
+                if (!tma || !launch_gemm_tma<4, 7>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC))
+                    launch_gemm_persist<4, 7>(c, W, r, K, M + c0, N, nc, Cc, ldc, col_major_out, WC);
+            }
         }
         return;
     }

@@ -473,6 +473,33 @@ def test_gram4_bulk_copies_equal_gram3(fb, orc, monkeypatch, m, n):
         assert np.array_equal(x, y)
 
 
+@pytest.mark.parametrize("m,n", [(4096, 16), (5000, 40), (70001, 150), (123457, 200), (4100, 208)])
+def test_gemm_tma_equals_cp_async(fb, orc, monkeypatch, m, n):
+    """The rescale GEMM fed by 2-D TMA tiles (k_gemm_tma: 128-byte swizzle,
+    zero fill past the last row and column) issues the same DMMAs per output
+    tile in the same k order as the cp.async kernel: bitwise equal eig_svd
+    U (row-major output) and frpcat U/V (column-major outputs, k of l
+    columns)."""
+    A = orc.gaussian_matrix(m, n, m + 5 * n)
+    monkeypatch.setenv("FRPCA_GEMM_CPASYNC", "1")
+    r1 = fb.eig_svd(A)
+    monkeypatch.delenv("FRPCA_GEMM_CPASYNC")
+    r2 = fb.eig_svd(A)
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
+
+
+def test_gemm_tma_outputs_of_a_run(fb, orc, monkeypatch):
+    oA = powerlaw_csr(orc, 9000, 1500, 150000, 21)
+    A = to_fb(fb, oA)
+    c = fb.PcaConfig(k=60, oversample=44, passes=3, seed=1)
+    monkeypatch.setenv("FRPCA_GEMM_CPASYNC", "1")
+    r1 = fb.frpcat(A, c)
+    monkeypatch.delenv("FRPCA_GEMM_CPASYNC")
+    r2 = fb.frpcat(A, c)
+    assert np.array_equal(r1.U, r2.U) and np.array_equal(r1.V, r2.V) and np.array_equal(r1.S, r2.S)
+
+
 @pytest.mark.parametrize("n", [3, 4, 5, 33, 64, 150, 200, 213, 214, 232])
 def test_sytrd_fused_vs_unfused(fb, orc, monkeypatch, n):
     """The fused tridiagonalisation (rank-2 update of step j and symmetric
