@@ -809,9 +809,12 @@ k_gemm_persist(const double* __restrict__ W, int64_t r, int K, const double* __r
     double* Ws = sm + size_t(K) * SB;                 // [2][BM][TSA]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rg = warp / WC, cgp = warp % WC;
-    for (int e = tid; e < K * NP; e += GP_THREADS) {
+    // rows K .. Kp-1 of M are read against zero-filled W columns: zero them
+    // (an uninitialised Inf/NaN there would turn 0 * x into NaN)
+    const int Kp = (K + TK - 1) / TK * TK;
+    for (int e = tid; e < Kp * NP; e += GP_THREADS) {
         const int k = e / NP, cc = e % NP;
-        cp_async8(Ms + k * SB + cc, M + (cc < N ? int64_t(k) * ldm + cc : 0), cc < N);
+        cp_async8(Ms + k * SB + cc, M + (cc < N && k < K ? int64_t(k) * ldm + cc : 0), cc < N && k < K);
     }
     cp_async_commit();
     const int nsteps = (K + TK - 1) / TK;
@@ -930,15 +933,16 @@ k_gemm_tma(const __grid_constant__ CUtensorMap wmap, int64_t r, int K, const dou
     const int BM = 8 * RT * ((GP_THREADS / 32) / WC);
     const int ntiles = (N + 7) / 8;
     const int NP = 8 * ntiles;
+    const int Kp = (K + TK - 1) / TK * TK;
     double* Ws = sm;                                  // [GT_STAGES][BM][TK], 1024-aligned, swizzled
-    double* Ms = sm + size_t(GT_STAGES) * BM * TK;    // [K][SB]
-    uint64_t* full = reinterpret_cast<uint64_t*>(Ms + size_t(K) * SB);
+    double* Ms = sm + size_t(GT_STAGES) * BM * TK;    // [Kp][SB], rows K.. zero
+    uint64_t* full = reinterpret_cast<uint64_t*>(Ms + size_t(Kp) * SB);
     uint64_t* empty = full + GT_STAGES;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rg = warp / WC, cgp = warp % WC;
-    for (int e = tid; e < K * NP; e += GP_THREADS) {
+    for (int e = tid; e < Kp * NP; e += GP_THREADS) {
         const int k = e / NP, cc = e % NP;
-        cp_async8(Ms + k * SB + cc, M + (cc < N ? int64_t(k) * ldm + cc : 0), cc < N);
+        cp_async8(Ms + k * SB + cc, M + (cc < N && k < K ? int64_t(k) * ldm + cc : 0), cc < N && k < K);
     }
     cp_async_commit();
     if (tid == 0) {
@@ -1058,7 +1062,8 @@ bool launch_gemm_tma(Ctx& c, const double* W, int64_t r, int64_t K, const double
     const int ntiles = int((N + 7) / 8), NP = 8 * ntiles;
     const int SB = NP + ((12 - (NP % 16)) + 16) % 16;
     const int BM = 8 * RT * ((GP_THREADS / 32) / WC);
-    const size_t smem = sizeof(double) * (size_t(GT_STAGES) * BM * TK + size_t(K) * SB) + 4 * sizeof(uint64_t) + 1024;
+    const int Kp = int((K + TK - 1) / TK) * TK;
+    const size_t smem = sizeof(double) * (size_t(GT_STAGES) * BM * TK + size_t(Kp) * SB) + 4 * sizeof(uint64_t) + 1024;
     if (smem > 227 * 1024 || BM > 256) return false;
     CUtensorMap map;
     if (!make_w_map(map, W, r, K, BM)) return false;
