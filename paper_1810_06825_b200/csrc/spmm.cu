@@ -309,6 +309,158 @@ k_spmm_sx(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, c
     }
 }
 
+// ---- Ring-staged gathers (k_spmm_ring) ---------------------------------------
+// The gather kernels are latency-bound (ncu at C3: 77% of issue stalls on the
+// long scoreboard, DRAM and L2 both near 57%): a warp can keep only the few
+// rows in flight that its registers hold. Here each warp owns a ring of R
+// shared-memory slots; one lane per nonzero moves the X row into a slot with a
+// 1-D bulk copy (cp.async.bulk, completing on the slot's mbarrier), so R rows
+// stay in flight continuously without registers, and the warp consumes the
+// slots in CSR order: per output entry the same FMA chain as k_spmm (bitwise
+// equal).
+constexpr int kRingWarps = 16;
+constexpr int kRingSlots = 8;
+
+__device__ __forceinline__ void ring_mbar_init(uint64_t* b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(b))));
+}
+__device__ __forceinline__ void ring_wait(uint64_t* b, unsigned parity) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "RW: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra RW;\n}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+// expect the row's bytes on the slot barrier and start its copy
+__device__ __forceinline__ void ring_issue(double* slot, uint64_t* bar, const double* src, unsigned bytes,
+                                           uint64_t pol) {
+    const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            static_cast<unsigned>(__cvta_generic_to_shared(slot))),
+        "l"(src), "r"(bytes), "r"(b), "l"(pol)
+        : "memory");
+}
+
+template <int NCH, int MODE>
+__global__ void __launch_bounds__(kRingWarps * 32, 1)
+k_spmm_ring(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, const double* __restrict__ val,
+            const WorkItem* __restrict__ items, int64_t nitems, const double* __restrict__ X, int64_t ldx,
+            double* __restrict__ Y, int64_t ldy, double* __restrict__ part, int ncols, int32_t* __restrict__ counter,
+            int stride) {
+    using V = Vec<2>;
+    using T = V::T;
+    extern __shared__ __align__(128) double ring_sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* ring = ring_sm + size_t(warp) * kRingSlots * stride;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring_sm + size_t(kRingWarps) * kRingSlots * stride) + warp * kRingSlots;
+    if (lane < kRingSlots) ring_mbar_init(bars + lane);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    Hot hot{0, 0};
+    if (MODE == MODE_HINT) make_policies(hot);
+    const unsigned bytes = unsigned(ncols) * 8u;
+    bool ok[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) ok[ch] = (ch * 32 + lane) * 2 < ncols;
+    // nonzero q -> its X row and L2 policy
+    auto src_of = [&](int32_t cc, uint64_t& pol) {
+        pol = (MODE == MODE_HINT && cc < 0) ? hot.keep : hot.stream;
+        return X + int64_t(cc & 0x7fffffff) * ldx;
+    };
+    uint32_t gi = 0, gc = 0;  // running issue / consume counts: slot g % R, parity (g / R) & 1
+    for (;;) {
+        int it = 0;
+        if (lane == 0) it = atomicAdd(counter, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nitems) break;
+        const WorkItem w = items[it];
+        const bool chunk = w.r1 < 0;
+        const int64_t P0 = chunk ? w.p0 : rowptr[w.r0], P1 = chunk ? w.p1 : rowptr[w.r1];
+        // first R nonzeros in flight, one lane each
+        int64_t qi = P0;
+        {
+            const int n = int(min(int64_t(kRingSlots), P1 - P0));
+            if (lane < n) {
+                uint64_t pol;
+                const double* src = src_of(__ldcs(col + P0 + lane), pol);
+                const int slot = int((gi + lane) % kRingSlots);
+                ring_issue(ring + slot * stride, bars + slot, src, bytes, pol);
+            }
+            qi += n;
+            gi += n;
+        }
+        // ids of the next nonzeros to issue, 32 at a time
+        int64_t cbase = qi;
+        int32_t myc = (qi + lane < P1) ? __ldcs(col + qi + lane) : 0;
+        int64_t vbase = P0;
+        double myv = (P0 + lane < P1) ? __ldcs(val + P0 + lane) : 0.0;
+        int32_t r = w.r0;
+        int64_t rend = chunk ? P1 : rowptr[r + 1];
+        T acc[NCH];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) acc[ch] = V::zero();
+        for (int64_t qc = P0; qc < P1; ++qc) {
+            while (!chunk && qc == rend) {  // rows that end here (empty rows too)
+                double* yr = Y + int64_t(r) * ldy + lane * 2;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    if (ok[ch]) V::store(yr + ch * 64, acc[ch]);
+                    acc[ch] = V::zero();
+                }
+                ++r;
+                rend = rowptr[r + 1];
+            }
+            if (qc - vbase >= 32) {
+                vbase = qc;
+                myv = (qc + lane < P1) ? __ldcs(val + qc + lane) : 0.0;
+            }
+            const double v = __shfl_sync(0xffffffffu, myv, int(qc - vbase));
+            const int slot = int(gc % kRingSlots);
+            ring_wait(bars + slot, (gc / kRingSlots) & 1u);
+            const double* xs = ring + slot * stride + lane * 2;
+            T x[NCH];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) x[ch] = ok[ch] ? *reinterpret_cast<const T*>(xs + ch * 64) : V::zero();
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) V::fma(acc[ch], v, x[ch]);
+            ++gc;
+            __syncwarp();  // every lane has read the slot before it is refilled
+            if (qi < P1) {
+                if (qi - cbase >= 32) {
+                    cbase = qi;
+                    myc = (qi + lane < P1) ? __ldcs(col + qi + lane) : 0;
+                }
+                if (lane == int(qi - cbase)) {
+                    uint64_t pol;
+                    const double* src = src_of(myc, pol);
+                    ring_issue(ring + slot * stride, bars + slot, src, bytes, pol);  // gi % R == slot
+                }
+                ++qi;
+                ++gi;
+            }
+        }
+        if (chunk) {
+            double* pr = part + (-int64_t(w.r1) - 1) * ncols + lane * 2;
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                if (ok[ch]) V::store(pr + ch * 64, acc[ch]);
+        } else {
+            for (; r < w.r1; ++r) {  // the item's last rows (and empty rows after them)
+                double* yr = Y + int64_t(r) * ldy + lane * 2;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    if (ok[ch]) V::store(yr + ch * 64, acc[ch]);
+                    acc[ch] = V::zero();
+                }
+            }
+        }
+    }
+}
+
 // Long rows: Y[row] = sum of its chunk partials in a fixed order. One CTA per
 // long row; warp w sums the w-th contiguous eighth of the row's chunks
 // sequentially (loads unrolled), then the eight warp sums are added in warp
@@ -467,9 +619,36 @@ void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip,
     FB_LAUNCH_CHECK();
 }
 
+// Ring kernel for a list without skipped rows (FRPCA_SPMM_RING=0/1); rows of
+// X must be 16-byte multiples at 16-byte aligned addresses (bulk copies)
+template <int NCH, int MODE>
+bool launch_ring(Ctx& c, const DCsr& A, const ItemList& L, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                 double* part, int ncols) {
+    if (int(env_double("FRPCA_SPMM_RING", 1.0)) == 0) return false;
+    if (ncols % 2 || ldx % 2 || (reinterpret_cast<uintptr_t>(X) % 16)) return false;
+    const int stride = (ncols + 1) / 2 * 2;  // doubles per slot (16-byte multiple)
+    const size_t smem = sizeof(double) * size_t(kRingWarps) * kRingSlots * stride +
+                        sizeof(uint64_t) * kRingWarps * kRingSlots;
+    if (smem > 227 * 1024) return false;
+    smem_optin(k_spmm_ring<NCH, MODE>, smem);
+    if (!c.wcount.get()) c.wcount.alloc(2, c.stream);
+    int32_t* counter = c.wcount.get() + (c.stream == c.aux ? 1 : 0);
+    FB_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), c.stream));
+    k_spmm_ring<NCH, MODE><<<c.num_sms, kRingWarps * 32, smem, c.stream>>>(
+        A.rowptr.get(), A.col.get(), A.val.get(), L.items.get(), L.nitems, X, ldx, Y, ldy, part, ncols, counter,
+        stride);
+    FB_LAUNCH_CHECK();
+    return true;
+}
+
 template <int VEC, int NCH>
 void launch(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
             double* Y, int64_t ldy, double* part, int ncols) {
+    if (VEC == 2 && !skip && L.nitems) {
+        const bool done = A.hint_h > 0 && &L == &A.L ? launch_ring<NCH, MODE_HINT>(c, A, L, X, ldx, Y, ldy, part, ncols)
+                                                       : launch_ring<NCH, MODE_PLAIN>(c, A, L, X, ldx, Y, ldy, part, ncols);
+        if (done) return;
+    }
     if (A.hint_h > 0 && &L == &A.L) return launch_plain<VEC, NCH, MODE_HINT>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
     launch_plain<VEC, NCH, MODE_PLAIN>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
 }

@@ -214,6 +214,41 @@ def test_spmm_l2_hints(fb, orc, monkeypatch, ncols):
     assert rel_fro(fb.spmm(A, X2), orc.spmm(oA, X2)) <= SPMM_TOL
 
 
+@pytest.mark.parametrize("ncols", [2, 8, 40, 150, 200, 256, 300])
+@pytest.mark.parametrize("hint", ["0", "0.02"])
+def test_spmm_ring_equals_register_gathers(fb, orc, monkeypatch, ncols, hint):
+    """A*X and A^T*Y with the X rows moved into per-warp shared-memory rings by
+    bulk copies (spmm.cu k_spmm_ring) are bitwise equal to the register-gather
+    kernel: per output entry the same FMA chain in CSR order. Power-law rows
+    (chunked long rows + combine), empty rows, L2-hinted ids, widths past 256
+    (two column slices)."""
+    oA = powerlaw_csr(orc, 5000, 3000, 200000, 17)
+    trip_extra = None
+    A = to_fb(fb, oA)
+    X = orc.gaussian_matrix(3000, ncols, 9)
+    Y = orc.gaussian_matrix(5000, ncols, 10)
+    monkeypatch.setenv("FRPCA_HINT_MB", hint)
+    monkeypatch.setenv("FRPCA_SPMM_RING", "0")
+    Y0, Z0 = fb.spmm(A, X), fb.spmm_transpose(A, Y)
+    monkeypatch.setenv("FRPCA_SPMM_RING", "1")
+    Y1, Z1 = fb.spmm(A, X), fb.spmm_transpose(A, Y)
+    assert np.array_equal(Y0, Y1) and np.array_equal(Z0, Z1)
+    assert rel_fro(Y1, orc.spmm(oA, X)) <= SPMM_TOL
+    _ = trip_extra
+
+
+def test_spmm_ring_empty_rows_and_single_nonzeros(fb, orc, monkeypatch):
+    trip = [(i, (7 * i) % 50, 1.0 + i) for i in range(0, 400, 3)] + [(5, j, -0.5) for j in range(50)]
+    A = fb.SparseMatrixCsr.from_triplets(400, 50, trip)
+    X = orc.gaussian_matrix(50, 64, 3)
+    monkeypatch.setenv("FRPCA_SPMM_RING", "0")
+    Y0 = fb.spmm(A, X)
+    monkeypatch.setenv("FRPCA_SPMM_RING", "1")
+    Y1 = fb.spmm(A, X)
+    assert np.array_equal(Y0, Y1)
+    assert np.array_equal(Y1, A.toDense() @ X) or rel_fro(Y1, A.toDense() @ X) <= 1e-15
+
+
 @pytest.mark.parametrize("ncols", [1, 8, 32, 37, 150, 200, 300])
 @pytest.mark.parametrize("sx_kb", ["0", "2", "160"])
 def test_spmm_sliced_shared_hot_rows(fb, orc, monkeypatch, ncols, sx_kb):
