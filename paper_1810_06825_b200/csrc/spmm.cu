@@ -624,7 +624,7 @@ void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip,
 template <int NCH, int MODE>
 bool launch_ring(Ctx& c, const DCsr& A, const ItemList& L, const double* X, int64_t ldx, double* Y, int64_t ldy,
                  double* part, int ncols) {
-    if (int(env_double("FRPCA_SPMM_RING", 1.0)) == 0) return false;
+    if (int(env_double("FRPCA_SPMM_RING", 0.0)) == 0) return false;  // opt-in: measured slower
     if (ncols % 2 || ldx % 2 || (reinterpret_cast<uintptr_t>(X) % 16)) return false;
     const int stride = (ncols + 1) / 2 * 2;  // doubles per slot (16-byte multiple)
     const size_t smem = sizeof(double) * size_t(kRingWarps) * kRingSlots * stride +
