@@ -304,6 +304,10 @@ int frpca_ctx_destroy(frpca_ctx* c) {
             cudaStreamSynchronize(c->copy);
             cudaStreamDestroy(c->copy);
         }
+        if (c->comm_stream) {
+            cudaStreamSynchronize(c->comm_stream);
+            cudaStreamDestroy(c->comm_stream);
+        }
         if (c->aux) {
             cudaStreamSynchronize(c->aux);
             cudaStreamDestroy(c->aux);

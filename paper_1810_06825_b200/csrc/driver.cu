@@ -315,8 +315,7 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
         // are the stream slice [offset*l, (offset+m)*l).
         if (M.offset == 0 && m == M.grows) sketch_into(c, a, l, M.grows, bufM);
         else sketch_cols(c, a, l, M.grows, M.offset, M.offset + m, bufM.get());
-        spmm_pass(c, M, /*transpose=*/true, bufM.get(), l, Z.get());  // (Omega A)^T, n x l
-        allreduce_sum(c, Z.get(), n * l);
+        spmm_pass_reduced(c, M, /*transpose=*/true, bufM.get(), l, Z.get());  // (Omega A)^T, n x l, summed
         if (q == 2) {
             eig_svd_U(c, Z.get(), n, l, Q.get());
         } else {
@@ -332,8 +331,7 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
 
     for (int64_t i = 1; i <= loops; ++i) {
         spmm_pass(c, M, false, Q.get(), l, bufM.get());   // A Q, m x l
-        spmm_pass(c, M, true, bufM.get(), l, Z.get());    // A^T (A Q), n x l
-        allreduce_sum(c, Z.get(), n * l);
+        spmm_pass_reduced(c, M, true, bufM.get(), l, Z.get());  // A^T (A Q), n x l, summed over ranks
         if (i == loops) {
             eig_svd_U(c, Z.get(), n, l, Q.get());
         } else {
@@ -398,8 +396,7 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
             sketch_rows(c, a, M.gcols, l, M.offset, M.offset + n, om.get());   // this rank's rows only
         }
         transpose_device(c, om.get(), l, n, bufN.get());
-        spmm_pass(c, M, false, bufN.get(), l, Y.get());   // A Omega, m x l
-        allreduce_sum(c, Y.get(), m * l);
+        spmm_pass_reduced(c, M, false, bufN.get(), l, Y.get());  // A Omega, m x l, summed over ranks
         if (q > 2) {
             lu_basis_device(c, Y.get(), m, l);
             std::swap(Q, Y);
@@ -415,8 +412,7 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
 
     for (int64_t i = 1; i <= loops; ++i) {
         spmm_pass(c, M, true, Q.get(), l, bufN.get());    // A^T Q, n x l
-        spmm_pass(c, M, false, bufN.get(), l, Y.get());   // A (A^T Q), m x l
-        allreduce_sum(c, Y.get(), m * l);
+        spmm_pass_reduced(c, M, false, bufN.get(), l, Y.get());  // A (A^T Q), m x l, summed over ranks
         if (i == loops) {
             eig_svd_U(c, Y.get(), m, l, Q.get());
         } else {
@@ -539,6 +535,14 @@ void run_basic(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st, bool left) {
         st->finalize_seconds = T.seconds(2);
         st->passes_over_matrix = M.passes.load() - passes0;
     }
+}
+
+// spmm_pass followed by the sum of Y over the ranks, overlapped chunk by chunk
+// (the exchange steps of randsvd.hpp:255-258 / :307-310 when sharded)
+void spmm_pass_reduced(Ctx& c, DMat& M, bool transpose, const double* X, int64_t ncols, double* Y) {
+    if (transpose) spmm_t_device_reduced(c, M.At, X, ncols, Y, "spmm_AtY");
+    else spmm_device_reduced(c, M.A, X, ncols, Y, "spmm_AX");
+    M.passes.fetch_add(1, std::memory_order_relaxed);  // recordPass, sparse_matrix.hpp:119-122
 }
 
 void spmm_pass(Ctx& c, DMat& M, bool transpose, const double* X, int64_t ncols, double* Y) {

@@ -35,6 +35,7 @@ struct EigWork {
 
 void eig_svd_U(Ctx& c, const double* W, int64_t r, int64_t n, double* Uout);
 void spmm_pass(Ctx& c, DMat& M, bool transpose, const double* X, int64_t ncols, double* Y);
+void spmm_pass_reduced(Ctx& c, DMat& M, bool transpose, const double* X, int64_t ncols, double* Y);
 void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st);
 void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st);
 // basic_rpca (left = false) / basic_rpcat (left = true), randsvd.hpp:95-175

@@ -41,7 +41,14 @@ struct ItemList {
     DBuf<WorkItem> items;
     DBuf<Combine> comb;
     int64_t nitems = 0, ncomb = 0, nslots = 0, chunk = 0;
+    // kCuts row ranges at item boundaries (a long row's chunks stay together),
+    // for a product whose output rows are handed on chunk by chunk (the
+    // sharded allreduce overlapped with the rest of the product): chunk k is
+    // rows [cut_row[k], cut_row[k+1]), items [cut_item[k], ..), combines
+    // [cut_comb[k], ..)
+    std::vector<int64_t> cut_row, cut_item, cut_comb;
 };
+constexpr int kCuts = 8;
 
 // Panelled A^T*Y (csr.cu build_panels, spmm.cu spmm_panelled): when the
 // gathered operand Y (rows x l) is much larger than L2, the entries of the
@@ -104,6 +111,9 @@ struct Ctx {
     DBuf<uint64_t> omega_raw;  // raw-word buffer of the Omega generator, kept (grown on demand)
     std::unique_ptr<Ctx> side;  // second stream for work overlapped with the upload (frpca_run_csr)
     cudaStream_t copy = nullptr;  // device->host copies of results overlapped with the output GEMMs
+    // sharded runs: the allreduce of a product's finished row chunks runs here
+    // while the next chunks are computed (spmm.cu *_reduced)
+    cudaStream_t comm_stream = nullptr;
     // A^T*Y cold rows run beside the panel chunks (spmm.cu spmm_t_device)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -181,6 +191,14 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
                  int64_t ldy, const char* tag);
 // Z = A^T Y on T = the transposed CSR of A (panelled for large Y, spmm.cu)
 void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, const char* tag);
+// The same products followed by the in-place sum of the output over the
+// ranks, overlapped: each chunk of output rows (ItemList::cut_*) is summed on
+// Ctx::comm_stream as soon as it is final, while the next chunk is computed.
+// ldy == ncols. One GPU: the plain product.
+void spmm_device_reduced(Ctx& c, const DCsr& A, const double* X, int64_t ncols, double* Y, const char* tag);
+// comm.cu: in-place sum over ranks on the ctx stream (no-op on one GPU)
+void allreduce_sum(Ctx& c, double* x, int64_t count);
+void spmm_t_device_reduced(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, const char* tag);
 
 // ---- dense.cu
 // B (n x n, column-major, full symmetric) = W^T W for row-major W (r x n, ld n).

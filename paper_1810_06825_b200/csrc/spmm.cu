@@ -590,8 +590,27 @@ k_spmm_panels(const int32_t* __restrict__ col, const double* __restrict__ val,
     }
 }
 
+// Non-owning view of a work list, or of one of its chunks (ItemList::cut_*)
+struct Items {
+    const WorkItem* items;
+    int64_t nitems;
+    const Combine* comb;
+    int64_t ncomb, nslots;
+    bool main;  // A's own list (carries the L2-hint ids)
+    Items(const ItemList& L, bool main_list) : Items(L, main_list, -1) {}
+    Items(const ItemList& L, bool main_list, int k) : main(main_list) {
+        const int64_t i0 = k < 0 ? 0 : L.cut_item[size_t(k)], i1 = k < 0 ? L.nitems : L.cut_item[size_t(k) + 1];
+        const int64_t c0 = k < 0 ? 0 : L.cut_comb[size_t(k)], c1 = k < 0 ? L.ncomb : L.cut_comb[size_t(k) + 1];
+        items = L.items.get() + i0;
+        nitems = i1 - i0;
+        comb = L.comb.get() + c0;
+        ncomb = c1 - c0;
+        nslots = L.nslots;
+    }
+};
+
 template <int VEC, int NCH, int MODE>
-void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
+void launch_plain(Ctx& c, const DCsr& A, const Items& L, const uint8_t* skip, const double* X, int64_t ldx,
                   double* Y, int64_t ldy, double* part, int ncols) {
     if (!L.nitems) return;
     static int blocks_per_sm = 0;
@@ -614,7 +633,7 @@ void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip,
         FB_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), c.stream));
     }
     k_spmm<VEC, NCH, MODE><<<grid, kThreads, 0, c.stream>>>(A.rowptr.get(), A.col.get(), A.val.get(),
-                                                           L.items.get(), L.nitems, X, ldx, Y, ldy, part,
+                                                           L.items, L.nitems, X, ldx, Y, ldy, part,
                                                            ncols, skip, counter);
     FB_LAUNCH_CHECK();
 }
@@ -622,7 +641,7 @@ void launch_plain(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip,
 // Ring kernel for a list without skipped rows (FRPCA_SPMM_RING=0/1); rows of
 // X must be 16-byte multiples at 16-byte aligned addresses (bulk copies)
 template <int NCH, int MODE>
-bool launch_ring(Ctx& c, const DCsr& A, const ItemList& L, const double* X, int64_t ldx, double* Y, int64_t ldy,
+bool launch_ring(Ctx& c, const DCsr& A, const Items& L, const double* X, int64_t ldx, double* Y, int64_t ldy,
                  double* part, int ncols) {
     if (int(env_double("FRPCA_SPMM_RING", 0.0)) == 0) return false;  // opt-in: measured slower
     if (ncols % 2 || ldx % 2 || (reinterpret_cast<uintptr_t>(X) % 16)) return false;
@@ -635,25 +654,26 @@ bool launch_ring(Ctx& c, const DCsr& A, const ItemList& L, const double* X, int6
     int32_t* counter = c.wcount.get() + (c.stream == c.aux ? 1 : 0);
     FB_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), c.stream));
     k_spmm_ring<NCH, MODE><<<c.num_sms, kRingWarps * 32, smem, c.stream>>>(
-        A.rowptr.get(), A.col.get(), A.val.get(), L.items.get(), L.nitems, X, ldx, Y, ldy, part, ncols, counter,
+        A.rowptr.get(), A.col.get(), A.val.get(), L.items, L.nitems, X, ldx, Y, ldy, part, ncols, counter,
         stride);
     FB_LAUNCH_CHECK();
     return true;
 }
 
 template <int VEC, int NCH>
-void launch(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
+void launch(Ctx& c, const DCsr& A, const Items& L, const uint8_t* skip, const double* X, int64_t ldx,
             double* Y, int64_t ldy, double* part, int ncols) {
+    const bool hint = A.hint_h > 0 && L.main;
     if (VEC == 2 && !skip && L.nitems) {
-        const bool done = A.hint_h > 0 && &L == &A.L ? launch_ring<NCH, MODE_HINT>(c, A, L, X, ldx, Y, ldy, part, ncols)
-                                                       : launch_ring<NCH, MODE_PLAIN>(c, A, L, X, ldx, Y, ldy, part, ncols);
+        const bool done = hint ? launch_ring<NCH, MODE_HINT>(c, A, L, X, ldx, Y, ldy, part, ncols)
+                               : launch_ring<NCH, MODE_PLAIN>(c, A, L, X, ldx, Y, ldy, part, ncols);
         if (done) return;
     }
-    if (A.hint_h > 0 && &L == &A.L) return launch_plain<VEC, NCH, MODE_HINT>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
+    if (hint) return launch_plain<VEC, NCH, MODE_HINT>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
     launch_plain<VEC, NCH, MODE_PLAIN>(c, A, L, skip, X, ldx, Y, ldy, part, ncols);
 }
 
-void combine(Ctx& c, const ItemList& L, const double* part, int nc, double* Y, int64_t ldy) {
+void combine(Ctx& c, const Items& L, const double* part, int nc, double* Y, int64_t ldy) {
     if (!L.ncomb) return;
     // k_combine2 wins when rows have few partials (C4's A^T*Y: 11 per row,
     // 11.2 -> 6.0 ms per run) and loses with many (C1: 49 per row, 0.45 ->
@@ -664,23 +684,23 @@ void combine(Ctx& c, const ItemList& L, const double* part, int nc, double* Y, i
         const unsigned g = unsigned(L.ncomb);
         auto go = [&](auto k1, auto k2, auto k3, auto k4) {
             switch ((nc + 63) / 64) {
-                case 1: k1<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
-                case 2: k2<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
-                case 3: k3<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
-                default: k4<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy); break;
+                case 1: k1<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb, part, nc, Y, ldy); break;
+                case 2: k2<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb, part, nc, Y, ldy); break;
+                case 3: k3<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb, part, nc, Y, ldy); break;
+                default: k4<<<g, kCombWarps * 32, 0, c.stream>>>(L.comb, part, nc, Y, ldy); break;
             }
         };
         go(k_combine2<1>, k_combine2<2>, k_combine2<3>, k_combine2<4>);
         FB_LAUNCH_CHECK();
         return;
     }
-    k_combine<<<unsigned(L.ncomb), kCombWarps * 32, 0, c.stream>>>(L.comb.get(), part, nc, Y, ldy);
+    k_combine<<<unsigned(L.ncomb), kCombWarps * 32, 0, c.stream>>>(L.comb, part, nc, Y, ldy);
     FB_LAUNCH_CHECK();
 }
 
 // One slice of <= 256 columns over the work list L (rows with skip[r] left
 // out), then the fixed-order combine of its long rows.
-void spmm_list(Ctx& c, const DCsr& A, const ItemList& L, const uint8_t* skip, const double* X, int64_t ldx,
+void spmm_list(Ctx& c, const DCsr& A, const Items& L, const uint8_t* skip, const double* X, int64_t ldx,
                int nc, double* Y, int64_t ldy, double* part) {
     const bool v2 = (nc % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
                     (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
@@ -750,7 +770,7 @@ void spmm_sx(Ctx& c, DCsr& A, const double* X, int64_t ldx, int64_t ncols, doubl
                                                              A.L.items.get(), A.L.nitems, X + c0, ldx, w, Y + c0,
                                                              ldy, part.get(), A.rank_ids.get(), H, counter);
         FB_LAUNCH_CHECK();
-        combine(c, A.L, part.get(), w, Y + c0, ldy);
+        combine(c, Items(A.L, true), part.get(), w, Y + c0, ldy);
     }
 }
 
@@ -769,7 +789,7 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
     for (int64_t off = 0; off < ncols; off += 256) {
         const int nc = int(std::min<int64_t>(256, ncols - off));
         if (A.L.nslots && part.n < size_t(A.L.nslots) * nc) part.alloc(size_t(A.L.nslots) * nc, c.stream);
-        spmm_list(c, A, A.L, nullptr, X + off, ldx, nc, Y + off, ldy, part.get());
+        spmm_list(c, A, Items(A.L, true), nullptr, X + off, ldx, nc, Y + off, ldy, part.get());
     }
 }
 
@@ -834,7 +854,7 @@ void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, c
             c.stream = c.aux;
             {
                 Prof pd(c, "spmm_AtY_cold", 0, 0);
-                spmm_list(c, T, P.cold, P.skip.get(), Y + off, ncols, nc, Z + off, ncols,
+                spmm_list(c, T, Items(P.cold, false), P.skip.get(), Y + off, ncols, nc, Z + off, ncols,
                           part.get() + size_t(P.hot.nslots) * size_t(nc));
             }
             c.stream = s0;
@@ -842,15 +862,114 @@ void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, c
         }
         {
             Prof pc(c, "spmm_AtY_pcombine", 0, 0);
-            combine(c, P.hot, part.get(), nc, Z + off, ncols);
+            combine(c, Items(P.hot, false), part.get(), nc, Z + off, ncols);
         }
         if (conc) {
             FB_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
             continue;
         }
         Prof pd(c, "spmm_AtY_cold", 0, 0);
-        spmm_list(c, T, P.cold, P.skip.get(), Y + off, ncols, nc, Z + off, ncols, part.get());
+        spmm_list(c, T, Items(P.cold, false), P.skip.get(), Y + off, ncols, nc, Z + off, ncols, part.get());
     }
+}
+
+// ---- products with the sharded sum overlapped -----------------
+namespace {
+
+// Hands finished row chunks of a row-major output (ld = ncols) to the
+// collective on Ctx::comm_stream; finish() makes the main stream wait for the
+// last sum.
+struct ChunkReducer {
+    Ctx& c;
+    double* out;
+    int64_t ld;
+    std::vector<cudaEvent_t> evs;
+    ChunkReducer(Ctx& ctx, double* o, int64_t l) : c(ctx), out(o), ld(l) {
+        if (!c.comm_stream) FB_CUDA(cudaStreamCreateWithFlags(&c.comm_stream, cudaStreamNonBlocking));
+    }
+    void rows(int64_t r0, int64_t r1) {
+        if (r1 <= r0) return;
+        cudaEvent_t ev;
+        FB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        evs.push_back(ev);
+        FB_CUDA(cudaEventRecord(ev, c.stream));
+        FB_CUDA(cudaStreamWaitEvent(c.comm_stream, ev, 0));
+        c.coll->allreduce_sum(c, out + r0 * ld, (r1 - r0) * ld, c.comm_stream);
+    }
+    void finish() {
+        cudaEvent_t ev;
+        FB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        evs.push_back(ev);
+        FB_CUDA(cudaEventRecord(ev, c.comm_stream));
+        FB_CUDA(cudaStreamWaitEvent(c.stream, ev, 0));
+    }
+    ~ChunkReducer() {
+        for (auto e : evs) cudaEventDestroy(e);  // (destroying a pending event is allowed)
+    }
+};
+
+}  // namespace
+
+void spmm_device_reduced(Ctx& c, const DCsr& A, const double* X, int64_t ncols, double* Y, const char* tag) {
+    if (c.world <= 1 || ncols > 256 || A.L.cut_row.size() < 2 || A.rows == 0) {
+        spmm_device(c, A, X, ncols, ncols, Y, ncols, tag);
+        allreduce_sum(c, Y, A.rows * ncols);
+        return;
+    }
+    const double bytes = 12.0 * A.nnz + 8.0 * (A.rows + 1) + 8.0 * ncols * (A.cols + A.rows);
+    ChunkReducer red(c, Y, ncols);
+    {
+        Prof prof(c, tag, bytes, 2.0 * A.nnz * ncols);  // (the sums overlap this bracket)
+        ensure_hint(c, const_cast<DCsr&>(A), ncols);
+        DBuf<double> part;
+        if (A.L.nslots) part.alloc(size_t(A.L.nslots) * ncols, c.stream);
+        const int nchunks = int(A.L.cut_row.size()) - 1;
+        for (int k = 0; k < nchunks; ++k) {
+            spmm_list(c, A, Items(A.L, true, k), nullptr, X, ncols, int(ncols), Y, ncols, part.get());
+            red.rows(A.L.cut_row[size_t(k)], A.L.cut_row[size_t(k) + 1]);
+        }
+    }
+    red.finish();
+}
+
+void spmm_t_device_reduced(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, const char* tag) {
+    int64_t pr = 0, cap = 0;
+    const bool pan = panel_rows_for(T, ncols, pr, cap);
+    if (pan) ensure_panels(c, T, pr, cap);
+    const ItemList& L = (pan && T.pan.nhot) ? T.pan.cold : T.L;
+    if (c.world <= 1 || ncols > 256 || L.cut_row.size() < 2 || T.rows == 0) {
+        spmm_t_device(c, T, Y, ncols, Z, tag);
+        allreduce_sum(c, Z, T.rows * ncols);
+        return;
+    }
+    const int nc = int(ncols);
+    ChunkReducer red(c, Z, ncols);
+    const int nchunks = int(L.cut_row.size()) - 1;
+    {
+        Prof prof(c, tag, 12.0 * T.nnz + 8.0 * (T.rows + 1) + 8.0 * ncols * (T.cols + T.rows), 2.0 * T.nnz * ncols);
+        if (pan && T.pan.nhot) {
+            // the hot rows (panel chunks + their combine) first, whole; then the
+            // cold rows chunk by chunk: chunk k completes rows [cut k, cut k+1)
+            const PanelPlan& P = T.pan;
+            DBuf<double>& part = const_cast<PanelPlan&>(P).part;
+            const size_t slots = size_t(std::max(P.hot.nslots, P.cold.nslots));
+            if (part.n < slots * size_t(nc)) part.alloc(slots * size_t(nc), c.stream);
+            launch_panels(c, T, Y, ncols, part.get(), nc);
+            combine(c, Items(P.hot, false), part.get(), nc, Z, ncols);
+            for (int k = 0; k < nchunks; ++k) {
+                spmm_list(c, T, Items(P.cold, false, k), P.skip.get(), Y, ncols, nc, Z, ncols, part.get());
+                red.rows(L.cut_row[size_t(k)], L.cut_row[size_t(k) + 1]);
+            }
+        } else {
+            DBuf<double> part;
+            if (T.L.nslots) part.alloc(size_t(T.L.nslots) * nc, c.stream);
+            for (int k = 0; k < nchunks; ++k) {
+                spmm_list(c, T, Items(T.L, true, k), nullptr, Y, ncols, nc, Z, ncols, part.get());
+                red.rows(L.cut_row[size_t(k)], L.cut_row[size_t(k) + 1]);
+            }
+        }
+    }
+    red.finish();
 }
 
 }  // namespace fb
