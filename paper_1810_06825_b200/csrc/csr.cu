@@ -123,11 +123,16 @@ __global__ void k_item_counts(const int64_t* __restrict__ rp, int64_t m, int64_t
 
 // chunk cuts of an item list (ItemList::cut_*): for k = 1..kCuts-1 the row r
 // of item k nitems / kCuts and the item / combine offsets of that row
-__global__ void k_item_cuts(const WorkItem* __restrict__ items, int64_t nitems, const int32_t* __restrict__ o_items,
-                            const int32_t* __restrict__ o_comb, int64_t* __restrict__ out) {
+// chunk cuts at rows k m / kCuts: a function of the row count alone, so every
+// rank of a sharded run (same output rows, its own items) cuts its reduced
+// output identically. The first item of chunk k is the first item starting
+// at or after its row (o_items counts the items of the rows before it); an
+// item straddling the cut (a group of short rows) finishes in chunk k - 1.
+__global__ void k_item_cuts(int64_t m, const int32_t* __restrict__ o_items, const int32_t* __restrict__ o_comb,
+                            int64_t* __restrict__ out) {
     const int k = threadIdx.x;
     if (k < 1 || k >= kCuts) return;
-    const int32_t r = items[int64_t(k) * nitems / kCuts].r0;
+    const int64_t r = int64_t(k) * m / kCuts;
     out[3 * k] = r;
     out[3 * k + 1] = o_items[r];
     out[3 * k + 2] = o_comb[r];
@@ -205,20 +210,19 @@ void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_
     k_item_write<<<grid_for(c, m), 256, 0, c.stream>>>(A.rowptr.get(), m, ch, oi, os, oc, L.items.get(),
                                                         L.comb.get(), skip);
     FB_LAUNCH_CHECK();
-    // chunk cuts: the rows of items k nitems / kCuts, moved back to the first
-    // item of their row; one small gather, one read
+    // chunk cuts (k_item_cuts); one small gather, one read
     L.cut_row.assign(1, 0);
     L.cut_item.assign(1, 0);
     L.cut_comb.assign(1, 0);
-    if (L.nitems > 0) {
+    {
         DBuf<int64_t> cv(3 * kCuts, c.stream);
-        k_item_cuts<<<1, 32, 0, c.stream>>>(L.items.get(), L.nitems, oi, oc, cv.get());
+        k_item_cuts<<<1, 32, 0, c.stream>>>(m, oi, oc, cv.get());
         FB_LAUNCH_CHECK();
         int64_t h[3 * kCuts];
         FB_CUDA(cudaMemcpyAsync(h, cv.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
         FB_CUDA(cudaStreamSynchronize(c.stream));
         for (int k = 1; k < kCuts; ++k)
-            if (h[3 * k] > L.cut_row.back() && h[3 * k + 1] > L.cut_item.back()) {
+            if (h[3 * k] > L.cut_row.back()) {  // (rows only: the same cuts on every rank)
                 L.cut_row.push_back(h[3 * k]);
                 L.cut_item.push_back(h[3 * k + 1]);
                 L.cut_comb.push_back(h[3 * k + 2]);

@@ -14,17 +14,16 @@
 // pairs, an exclusive scan gives every segment its output offset, and (2)
 // regenerates the segment and writes its normals. The arithmetic of every
 // accepted pair is the host's, operation for operation, in IEEE round-to-
-// nearest without contraction; log(r2) is evaluated correctly rounded. glibc's
-// log is not correctly rounded in ~0.08% of inputs (its bound is 0.52 ulp), so
-// those normals differ from libstdc++'s by a few ulp; accept/reject decisions
-// (r2 alone) and hence the stream positions are always identical.
+// nearest without contraction, and log(r2) is glibc's log restated operation
+// for operation (glibc_log.cuh: the FMA build the host's ifunc selects), so
+// every normal is bitwise equal to libstdc++'s.
 #include <cub/cub.cuh>
 
 #include <cmath>
 #include <map>
 #include <mutex>
 
-#include "crlog.cuh"
+#include "glibc_log.cuh"
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -224,7 +223,7 @@ __device__ __forceinline__ void emit_win(double* __restrict__ out, int64_t p, do
 // normals of the accepted attempts, written at their stream positions
 __global__ void __launch_bounds__(PT, 5)
 k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restrict__ off,
-       double* __restrict__ out, int64_t count, const crlog::LogEntry* __restrict__ logtab, Window win) {
+       double* __restrict__ out, int64_t count, Window win) {
     // round e of the chunk = attempts b CHUNK + e PT + [0, PT) (coalesced
     // loads); the stream position of an accepted attempt = accepted attempts
     // of the earlier rounds + of the lower lanes of its round: one block scan
@@ -258,7 +257,7 @@ k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restri
             // mult = sqrt(-2 log(r2) / r2); y*mult first, then the saved
             // x*mult; each passes through `ret * stddev + mean` with (1, 0)
             // (random.tcc).
-            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, crlog::fast_log(rs[e], logtab)), rs[e]));
+            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, glibc_log::log_polar(rs[e])), rs[e]));
             const double a = __dadd_rn(__dmul_rn(__dmul_rn(ys[e], mult), 1.0), 0.0);
             const double b = __dadd_rn(__dmul_rn(__dmul_rn(xs[e], mult), 1.0), 0.0);
             if (!win.ident) {
@@ -288,22 +287,6 @@ struct PolyCache {
 PolyCache& cache() {
     static PolyCache c;
     return c;
-}
-
-// table of the correctly rounded log's fast path, one copy per device
-const crlog::LogEntry* device_logtab(Ctx& c) {
-    static std::mutex mu;
-    static std::map<int, crlog::LogEntry*> tabs;
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = tabs.find(c.device);
-    if (it != tabs.end()) return it->second;
-    std::vector<crlog::LogEntry> h(crlog::kLogTab);
-    crlog::build_log_table(h.data());
-    crlog::LogEntry* d = nullptr;
-    FB_CUDA(cudaMalloc(&d, h.size() * sizeof(crlog::LogEntry)));
-    FB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(crlog::LogEntry), cudaMemcpyHostToDevice));
-    tabs[c.device] = d;
-    return d;
 }
 
 const uint32_t* device_polys(Ctx& c, int log2S, int& groups) {
@@ -369,7 +352,6 @@ void gaussian_stream_window(Ctx& c, uint64_t seed, int64_t count, int64_t period
         polys = device_polys(c, log2S, groups);
     }
     smem_optin(k_jump_level, size_t(kNibBytes));
-    const crlog::LogEntry* logtab = device_logtab(c);
     uint64_t s0[NN];
     mt64_seed_state(seed, s0);
     int64_t K = (2 * P + J - 1) / J;
@@ -425,7 +407,7 @@ void gaussian_stream_window(Ctx& c, uint64_t seed, int64_t count, int64_t period
         }
         {
             Prof pe(c, "omega_emit", 8.0 * nseg * J + 8.0 * count, 0.0);
-            k_emit<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, off.get(), out, count, logtab, win);
+            k_emit<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, off.get(), out, count, win);
             FB_LAUNCH_CHECK();
         }
         if (defer) {
