@@ -87,10 +87,16 @@ __global__ void k_lowrank_dense(const double* __restrict__ U, const double* __re
     }
 }
 
+// (A's ids may carry the A*X launch encodings: decoded through rank_ids)
 __global__ void k_scatter_dense(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                const double* __restrict__ val, int64_t m, double* __restrict__ R) {
+                                const double* __restrict__ val, int64_t m, const int32_t* __restrict__ rank_ids,
+                                double* __restrict__ R) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
-        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) R[i + int64_t(col[p] & kColMask) * m] = val[p];
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            const int32_t e = col[p];
+            const int32_t cc = (e & kColHot) ? rank_ids[e & kRankMask] : (e & kColMask);
+            R[i + int64_t(cc) * m] = val[p];
+        }
 }
 
 int vgrid(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>(4096, (n + 255) / 256))); }
@@ -178,7 +184,8 @@ double low_rank_error_device(Ctx& c, DMat& M, int64_t k, const double* U, const 
         DBuf<double> R(size_t(std::max<uint64_t>(entries, 1)), s);
         FB_CUDA(cudaMemsetAsync(R.get(), 0, R.bytes(), s));
         if (m) {
-            k_scatter_dense<<<vgrid(m), 256, 0, s>>>(M.A.rowptr.get(), M.A.col.get(), M.A.val.get(), m, R.get());
+            k_scatter_dense<<<vgrid(m), 256, 0, s>>>(M.A.rowptr.get(), M.A.col.get(), M.A.val.get(), m,
+                                                     M.A.rank_ids.get(), R.get());
             FB_LAUNCH_CHECK();
         }
         if (k && entries) {
