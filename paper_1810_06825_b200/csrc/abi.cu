@@ -715,7 +715,10 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
             // the panel plan of the run's A^T*Y width is built while the
             // values are still crossing PCIe
             const int64_t whint = (algo == FRPCA_ALGO_FRPCA || algo == FRPCA_ALGO_FRPCAT) ? cfg->k + cfg->oversample : 0;
-            dcsr_upload_build(*c, *M, rows, cols, nnz, row_ptr, col_idx, values, whint);
+            // frpca / frpcat: the first A*X starts on the values as they land
+            const char* pe = std::getenv("FRPCA_UPLOAD_PIPELINE");  // A/B knob
+            const bool pipe = whint > 0 && c->world == 1 && !(pe && pe[0] == '0');
+            dcsr_upload_build(*c, *M, rows, cols, nnz, row_ptr, col_idx, values, whint, pipe);
         } catch (...) {
             if (side_thread.joinable()) side_thread.join();
             throw;

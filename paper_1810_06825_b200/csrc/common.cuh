@@ -44,19 +44,107 @@ void count_launch();
         FB_CUDA(cudaGetLastError()); \
     } while (0)
 
-// Minimal owning device buffer (stream-ordered allocation).
+// Large device buffers are recycled per device instead of going back to the
+// stream-ordered pool. Measured at C3 (tools/e2e_ab.py, FRPCA_DEBUG_ALLOC):
+// re-taking a multi-GB block from the pool cost 10-600 ms of host time per
+// cudaMallocAsync while copies and kernels were in flight, although every
+// call of a repeated run asks for the same sizes. A released buffer of at
+// least kCacheMin bytes is parked with an event recorded on its last stream;
+// a later request of the same device takes the smallest parked buffer that
+// fits within 1/8 slack, after making its stream wait on that event (the
+// ordering the pool itself would provide). Parked buffers are freed when an
+// allocation fails (then retried) and beyond kCacheMax bytes.
+struct BufCache {
+    struct Entry {
+        void* p;
+        size_t bytes;
+        int dev;
+        cudaEvent_t ev;
+    };
+    static constexpr size_t kCacheMin = size_t(32) << 20;
+    static constexpr size_t kCacheMax = size_t(48) << 30;
+    static constexpr size_t kMinFree = size_t(20) << 30;  // device headroom kept for other allocators
+    std::mutex mu;
+    std::vector<Entry> parked;
+    size_t held = 0;
+    static BufCache& get() {
+        static BufCache* c = new BufCache;  // never destroyed (process exit order)
+        return *c;
+    }
+    static void drop(Entry& e) {
+        cudaEventSynchronize(e.ev);
+        cudaEventDestroy(e.ev);
+        cudaFree(e.p);
+    }
+    // a parked buffer of [bytes, bytes + bytes/8] on this device, or nullptr
+    void* take(size_t bytes, cudaStream_t s, size_t& cap) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+        std::lock_guard<std::mutex> lk(mu);
+        size_t best = parked.size();
+        for (size_t k = 0; k < parked.size(); ++k) {
+            const Entry& e = parked[k];
+            if (e.dev == dev && e.bytes >= bytes && e.bytes - bytes <= bytes / 8 &&
+                (best == parked.size() || e.bytes < parked[best].bytes))
+                best = k;
+        }
+        if (best == parked.size()) return nullptr;
+        Entry e = parked[best];
+        parked.erase(parked.begin() + long(best));
+        held -= e.bytes;
+        cudaStreamWaitEvent(s, e.ev, 0);
+        cudaEventDestroy(e.ev);
+        cap = e.bytes;
+        return e.p;
+    }
+    bool give(void* p, size_t bytes, cudaStream_t s) {
+        int dev = 0;
+        cudaEvent_t ev;
+        if (cudaGetDevice(&dev) != cudaSuccess) return false;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return false;
+        if (cudaEventRecord(ev, s) != cudaSuccess) {
+            cudaEventDestroy(ev);
+            return false;
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        parked.push_back({p, bytes, dev, ev});
+        held += bytes;
+        size_t fr = 0, tot = 0;
+        const bool low = cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr < kMinFree;
+        while ((held > kCacheMax || (low && held > bytes)) && parked.size() > 1) {
+            held -= parked.front().bytes;
+            drop(parked.front());
+            parked.erase(parked.begin());
+        }
+        return true;
+    }
+    void flush() {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto& e : parked) drop(e);
+        parked.clear();
+        held = 0;
+    }
+};
+
+// Minimal owning device buffer (stream-ordered allocation; large buffers
+// recycled through BufCache).
 template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
     cudaStream_t s = nullptr;
+    size_t cap = 0;  // bytes actually held (>= n * sizeof(T))
     DBuf() = default;
     DBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), cap(o.cap) { o.p = nullptr; o.n = 0; o.cap = 0; }
     DBuf& operator=(DBuf&& o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; s = o.s; cap = o.cap;
+            o.p = nullptr; o.n = 0; o.cap = 0;
+        }
         return *this;
     }
     ~DBuf() { release(); }
@@ -64,12 +152,31 @@ struct DBuf {
         release();
         s = stream;
         n = count;
-        if (count) FB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+        if (!count) return;
+        const size_t bytes = count * sizeof(T);
+        if (bytes >= BufCache::kCacheMin) {
+            if (void* q = BufCache::get().take(bytes, stream, cap)) {
+                p = static_cast<T*>(q);
+                return;
+            }
+        }
+        cap = bytes;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, stream);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            BufCache::get().flush();
+            e = cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, stream);
+        }
+        if (e != cudaSuccess) {
+            p = nullptr;
+            n = cap = 0;
+            FB_CUDA(e);
+        }
     }
     void release() noexcept {
-        if (p) cudaFreeAsync(p, s);
+        if (p && !(cap >= BufCache::kCacheMin && BufCache::get().give(p, cap, s))) cudaFreeAsync(p, s);
         p = nullptr;
-        n = 0;
+        n = cap = 0;
     }
     T* get() const { return p; }
     size_t bytes() const { return n * sizeof(T); }

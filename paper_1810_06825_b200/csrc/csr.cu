@@ -61,19 +61,29 @@ __global__ void k_iota(int32_t* __restrict__ x, int64_t n) {
 }
 
 // Transposed entries from the stable column sort: entry k of A^T is original
-// nonzero perm[k]; its column id in A^T is the original row id.
-__global__ void k_gather_transpose_cols(const int32_t* __restrict__ perm, const int32_t* __restrict__ rowid,
-                                        int64_t nnz, int32_t* __restrict__ tcol) {
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz;
-         k += int64_t(gridDim.x) * blockDim.x)
-        tcol[k] = rowid[perm[k]];
-}
-
-__global__ void k_gather_transpose_vals(const int32_t* __restrict__ perm, const double* __restrict__ val,
-                                        int64_t nnz, double* __restrict__ tval) {
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nnz;
-         k += int64_t(gridDim.x) * blockDim.x)
-        tval[k] = val[perm[k]];
+// nonzero perm[k]; its column id in A^T is the original row id, its value the
+// original value. Random gathers: eight independent loads in flight per
+// thread (one per 32-byte sector), so the kernel is not bound by a single
+// load's latency.
+template <class T>
+__global__ void __launch_bounds__(256)
+k_gather_perm(const int32_t* __restrict__ perm, const T* __restrict__ src, int64_t n, T* __restrict__ dst) {
+    constexpr int U = 8;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x * U;
+    for (int64_t k0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * U; k0 < n; k0 += stride) {
+        if (k0 + U <= n) {
+            const int4 a = __ldcs(reinterpret_cast<const int4*>(perm + k0));
+            const int4 b = __ldcs(reinterpret_cast<const int4*>(perm + k0 + 4));
+            const int idx[U] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            T v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = __ldg(src + idx[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) __stcs(dst + k0 + u, v[u]);
+        } else {
+            for (int64_t k = k0; k < n; ++k) dst[k] = src[perm[k]];
+        }
+    }
 }
 
 // t_rowptr[c] = lower_bound(sorted_keys, c), c in [0, n].
@@ -304,8 +314,21 @@ const char* kValidateMsg[3] = {
 
 }  // namespace
 
+// pipelined (frpca_run_csr): the values cross PCIe in kValChunks chunks on the
+// copy stream and the call returns without waiting for them; A.pend / M.At.pend
+// (PendingValues) tell the first product what to wait for.
+constexpr int kValChunks = 8;
+
+void consume_pending(Ctx& c, DCsr& A) {
+    if (!A.pend) return;
+    if (!A.pend->ev.empty()) FB_CUDA(cudaStreamWaitEvent(c.stream, A.pend->ev.back(), 0));
+    if (A.pend->all) FB_CUDA(cudaStreamWaitEvent(c.stream, A.pend->all, 0));
+    A.pend.reset();
+}
+
 void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
-                       const int64_t* h_rp, const int64_t* h_col, const double* h_val, int64_t width_hint) {
+                       const int64_t* h_rp, const int64_t* h_col, const double* h_val, int64_t width_hint,
+                       bool pipelined) {
     // O(1) checks of validate() (sparse_matrix.hpp:126-130), same messages.
     require(rows >= 0 && cols >= 0, "csr: negative dimension");
     require(nnz >= 0, "csr: col_idx/values length mismatch");
@@ -327,6 +350,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     // the values are first needed by the transpose's gather: they cross PCIe
     // on the copy stream while the ids are validated and sorted
     cudaEvent_t ev_ids = nullptr, ev_val = nullptr;
+    std::shared_ptr<PendingValues> pv;
     if (nnz) {
         FB_CUDA(cudaMemcpyAsync(col64.get(), h_col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
         if (!c.copy) FB_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
@@ -334,7 +358,21 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         FB_CUDA(cudaEventCreateWithFlags(&ev_val, cudaEventDisableTiming));
         FB_CUDA(cudaEventRecord(ev_ids, s));
         FB_CUDA(cudaStreamWaitEvent(c.copy, ev_ids, 0));
-        FB_CUDA(cudaMemcpyAsync(A.val.get(), h_val, sizeof(double) * nnz, cudaMemcpyHostToDevice, c.copy));
+        if (pipelined) {
+            pv = std::make_shared<PendingValues>();
+            const int64_t V = (nnz + kValChunks - 1) / kValChunks;
+            for (int64_t v0 = 0; v0 < nnz; v0 += V) {
+                const int64_t v1 = std::min(nnz, v0 + V);
+                FB_CUDA(cudaMemcpyAsync(A.val.get() + v0, h_val + v0, sizeof(double) * (v1 - v0),
+                                        cudaMemcpyHostToDevice, c.copy));
+                cudaEvent_t e;
+                FB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                pv->ev.push_back(e);
+                FB_CUDA(cudaEventRecord(e, c.copy));
+            }
+        } else {
+            FB_CUDA(cudaMemcpyAsync(A.val.get(), h_val, sizeof(double) * nnz, cudaMemcpyHostToDevice, c.copy));
+        }
         FB_CUDA(cudaEventRecord(ev_val, c.copy));
     }
     struct EvGuard {
@@ -348,6 +386,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         }
     } evg{ev_ids, ev_val, c.copy};
     ph.reset(new Prof(c, "upload_validate", 0, 0));
+    std::unique_ptr<Prof> pv0(new Prof(c, "upload_v_rowptr", 0, 0));
     DBuf<unsigned long long> err(2, s);
     FB_CUDA(cudaMemsetAsync(err.get(), 0xff, err.bytes(), s));
     if (rows) {
@@ -363,6 +402,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         nnz_valid = std::min<int64_t>(tmp, nnz);
     }
     // row id of every nonzero (mark + inclusive max-scan)
+    pv0.reset(new Prof(c, "upload_v_rowid", 0, 0));
     DBuf<int32_t> rowid(size_t(nnz), s);
     if (nnz) {
         DBuf<int32_t> mark(size_t(nnz), s);
@@ -377,6 +417,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         DBuf<unsigned char> tmp(tb, s);
         FB_CUDA(cub::DeviceScan::InclusiveScan(tmp.get(), tb, mark.get(), rowid.get(), cub::Max(),
                                                nnz, s));
+        pv0.reset(new Prof(c, "upload_v_cols", 0, 0));
         if (nnz_valid > 0) {
             k_check_cols<<<grid_for(c, nnz_valid), 256, 0, s>>>(
                 A.rowptr.get(), rowid.get(), col64.get(), nnz_valid, cols, A.col.get(), err.get() + 1);
@@ -384,6 +425,7 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         }
     }
     const unsigned long long key = read_scalar(c, err.get() + 1);
+    pv0.reset();
     if (key != kNoError) {
         const int kind = (key & 1ull) ? 1 : 2;
         throw InvalidArgument(kValidateMsg[kind]);
@@ -404,8 +446,10 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     // gathered last.
     DBuf<int32_t> perm_out;
     if (nnz) {
+        std::unique_ptr<Prof> pt(new Prof(c, "upload_t_alloc", 0, 0));
         DBuf<int32_t> keys_out(size_t(nnz), s), perm_in(size_t(nnz), s);
         perm_out.alloc(size_t(nnz), s);
+        pt.reset(new Prof(c, "upload_t_sort", 0, 0));
         k_iota<<<grid_for(c, nnz), 256, 0, s>>>(perm_in.get(), nnz);
         FB_LAUNCH_CHECK();
         int end_bit = 1;
@@ -416,7 +460,8 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         DBuf<unsigned char> tmp(tb, s);
         FB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, A.col.get(), keys_out.get(),
                                                 perm_in.get(), perm_out.get(), nnz, 0, end_bit, s));
-        k_gather_transpose_cols<<<grid_for(c, nnz), 256, 0, s>>>(perm_out.get(), rowid.get(), nnz, T.col.get());
+        pt.reset(new Prof(c, "upload_t_gather", 0, 0));
+        k_gather_perm<int32_t><<<grid_for(c, (nnz + 7) / 8), 256, 0, s>>>(perm_out.get(), rowid.get(), nnz, T.col.get());
         FB_LAUNCH_CHECK();
         k_rowptr_from_sorted<<<grid_for(c, cols + 1), 256, 0, s>>>(keys_out.get(), nnz, cols,
                                                                     T.rowptr.get());
@@ -433,10 +478,38 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         int64_t pr = 0, cap = 0;
         if (panel_rows_for(T, width_hint, pr, cap)) ensure_panels(c, T, pr, cap);
     }
+    if (nnz && pv) {
+        // A^T's values are gathered on the copy stream behind the last chunk;
+        // the first A*X starts on the chunks as they land (PendingValues)
+        ph.reset();
+        cudaEvent_t ev_perm;
+        FB_CUDA(cudaEventCreateWithFlags(&ev_perm, cudaEventDisableTiming));
+        FB_CUDA(cudaEventRecord(ev_perm, s));
+        FB_CUDA(cudaStreamWaitEvent(c.copy, ev_perm, 0));
+        FB_CUDA(cudaEventDestroy(ev_perm));
+        k_gather_perm<double><<<grid_for(c, (nnz + 7) / 8), 256, 0, c.copy>>>(perm_out.get(), A.val.get(), nnz,
+                                                                             T.val.get());
+        FB_LAUNCH_CHECK();
+        FB_CUDA(cudaEventCreateWithFlags(&pv->all, cudaEventDisableTiming));
+        FB_CUDA(cudaEventRecord(pv->all, c.copy));
+        pv->perm = std::move(perm_out);
+        // item chunk k of A's list reads the values up to row_ptr[cut_row[k + 1]]
+        const int64_t V = (nnz + kValChunks - 1) / kValChunks;
+        for (size_t k = 0; k + 1 < A.L.cut_row.size(); ++k) {
+            const int64_t e = h_rp[A.L.cut_row[k + 1]];
+            pv->need.push_back(int(e > 0 ? (e - 1) / V : 0));
+        }
+        A.pend = pv;
+        T.pend = pv;
+        FB_CUDA(cudaEventDestroy(ev_val));  // (the recorded work stays queued; the guard must not wait for it)
+        ev_val = nullptr;
+        FB_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
     if (nnz) {
         ph.reset(new Prof(c, "upload_values", 0, 0));
         FB_CUDA(cudaStreamWaitEvent(s, ev_val, 0));
-        k_gather_transpose_vals<<<grid_for(c, nnz), 256, 0, s>>>(perm_out.get(), A.val.get(), nnz, T.val.get());
+        k_gather_perm<double><<<grid_for(c, (nnz + 7) / 8), 256, 0, s>>>(perm_out.get(), A.val.get(), nnz, T.val.get());
         FB_LAUNCH_CHECK();
     }
     perm_out.release();
@@ -475,48 +548,57 @@ __device__ __forceinline__ int64_t lower_bound(const int32_t* __restrict__ col, 
     return lo;
 }
 
-// Walks hot row h segment by segment (one non-empty panel each). WRITE = false:
-// chunk counts per (panel, row) and per row; WRITE = true: the items (at the
-// panel-major positions) and the row's combine entry.
+// One thread per (panel b, hot row h): the entries of h in panel b are
+// [q_b, q_(b+1)) with q_b = lower_bound(row h, b * pr) (T's entries ascend
+// within a row), cut into chunks of pch entries. WRITE = false: the chunk
+// count k(b, h), stored panel-major (item positions) and row-major (slot
+// numbering: a row's partials in panel order). WRITE = true: the k items at
+// their panel-major positions with their row-major slots. Balanced over
+// (panel, row) pairs: the longest hot row (5.3M entries at C3) no longer
+// serialises on one thread.
 template <bool WRITE>
-__global__ void k_panel_walk(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                             const int32_t* __restrict__ hot, int64_t nhot, int64_t pr, int64_t pch,
-                             int32_t* __restrict__ cnt, int32_t* __restrict__ rowslots,
-                             const int32_t* __restrict__ itempos, const int32_t* __restrict__ slotbase,
-                             WorkItem* __restrict__ items, Combine* __restrict__ comb) {
+__global__ void k_panel_cells(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const int32_t* __restrict__ hot, int64_t nhot, int64_t npan, int64_t pr, int64_t pch,
+                              int32_t* __restrict__ cnt_pm, int32_t* __restrict__ cnt_rm,
+                              const int32_t* __restrict__ itempos, const int32_t* __restrict__ slotpos,
+                              WorkItem* __restrict__ items) {
+    const int64_t total = npan * nhot;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = t / nhot, h = t - b * nhot;  // consecutive threads: consecutive rows
+        const int32_t r = hot[h];
+        const int64_t p0 = rp[r], p1 = rp[r + 1];
+        const int64_t q0 = lower_bound(col, p0, p1, b * pr);
+        const int64_t q1 = lower_bound(col, q0, p1, (b + 1) * pr);
+        const int32_t k = int32_t((q1 - q0 + pch - 1) / pch);
+        if (!WRITE) {
+            cnt_pm[t] = k;
+            cnt_rm[h * npan + b] = k;
+            continue;
+        }
+        const int32_t o = itempos[t], sl = slotpos[h * npan + b];
+        for (int32_t u = 0; u < k; ++u) {
+            WorkItem w;
+            w.p0 = q0 + int64_t(u) * pch;
+            w.p1 = min(q1, q0 + int64_t(u + 1) * pch);
+            w.r0 = r;
+            w.r1 = -(sl + u) - 1;
+            items[o + u] = w;
+        }
+    }
+}
+
+// combine entry of hot row h: its slots [slotpos(h, 0), slotpos(h + 1, 0))
+__global__ void k_panel_comb(const int32_t* __restrict__ hot, int64_t nhot, int64_t npan,
+                             const int32_t* __restrict__ slotpos, Combine* __restrict__ comb) {
     for (int64_t h = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; h < nhot;
          h += int64_t(gridDim.x) * blockDim.x) {
-        const int32_t r = hot[h];
-        int64_t p = rp[r];
-        const int64_t e = rp[r + 1];
-        int32_t slot = WRITE ? slotbase[h] : 0;
-        while (p < e) {
-            const int64_t pan = col[p] / pr;
-            const int64_t q = lower_bound(col, p, e, (pan + 1) * pr);
-            const int32_t k = int32_t((q - p + pch - 1) / pch);
-            if (WRITE) {
-                const int32_t o = itempos[pan * nhot + h];
-                for (int32_t t = 0; t < k; ++t) {
-                    WorkItem w;
-                    w.p0 = p + int64_t(t) * pch;
-                    w.p1 = min(q, p + int64_t(t + 1) * pch);
-                    w.r0 = r;
-                    w.r1 = -(slot + t) - 1;
-                    items[o + t] = w;
-                }
-            } else {
-                cnt[pan * nhot + h] = k;
-            }
-            slot += k;
-            p = q;
-        }
-        if (WRITE) {
-            Combine cb;
-            cb.row = r; cb.s0 = slotbase[h]; cb.s1 = slot; cb.pad = 0;
-            comb[h] = cb;
-        } else {
-            rowslots[h] = slot;
-        }
+        Combine cb;
+        cb.row = hot[h];
+        cb.s0 = slotpos[h * npan];
+        cb.s1 = slotpos[(h + 1) * npan];
+        cb.pad = 0;
+        comb[h] = cb;
     }
 }
 
@@ -542,7 +624,7 @@ void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap) {
     DBuf<int32_t> flag(size_t(n) + 1, s), pos(size_t(n) + 1, s);
     P.skip.alloc(size_t(n), s);
     int64_t thot = 3 * npan, nhot = 0, nitems = 0;
-    DBuf<int32_t> hot, cnt, rowslots, itempos, slotbase;
+    DBuf<int32_t> hot, cnt_pm, cnt_rm, itempos, slotpos;
     for (;;) {
         FB_CUDA(cudaMemsetAsync(flag.get(), 0, flag.bytes(), s));
         k_hot_flags<<<grid_for(c, n), 256, 0, s>>>(T.rowptr.get(), n, thot, P.skip.get(), flag.get());
@@ -561,39 +643,39 @@ void ensure_panels(Ctx& c, DCsr& T, int64_t pr, int64_t slot_cap) {
         hot.alloc(size_t(nhot), s);
         k_hot_list<<<grid_for(c, n), 256, 0, s>>>(flag.get(), pos.get(), n, hot.get());
         FB_LAUNCH_CHECK();
-        cnt.alloc(size_t(npan * nhot) + 1, s);
-        rowslots.alloc(size_t(nhot) + 1, s);
-        FB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-        FB_CUDA(cudaMemsetAsync(rowslots.get(), 0, rowslots.bytes(), s));
-        k_panel_walk<false><<<grid_for(c, nhot, 128), 128, 0, s>>>(T.rowptr.get(), T.col.get(), hot.get(), nhot,
-                                                                   pr, pch, cnt.get(), rowslots.get(), nullptr,
-                                                                   nullptr, nullptr, nullptr);
+        // the +1 entries stay 0: the scans below then end on the totals
+        cnt_pm.alloc(size_t(npan * nhot) + 1, s);
+        cnt_rm.alloc(size_t(npan * nhot) + 1, s);
+        FB_CUDA(cudaMemsetAsync(cnt_pm.get() + npan * nhot, 0, sizeof(int32_t), s));
+        FB_CUDA(cudaMemsetAsync(cnt_rm.get() + npan * nhot, 0, sizeof(int32_t), s));
+        k_panel_cells<false><<<grid_for(c, npan * nhot), 256, 0, s>>>(T.rowptr.get(), T.col.get(), hot.get(), nhot,
+                                                                      npan, pr, pch, cnt_pm.get(), cnt_rm.get(),
+                                                                      nullptr, nullptr, nullptr);
         FB_LAUNCH_CHECK();
         // 64-bit total first: the int32 scans below need it < 2^31
         DBuf<int64_t> tot(1, s);
         size_t tb2 = 0;
-        FB_CUDA(cub::DeviceReduce::Sum(nullptr, tb2, rowslots.get(), tot.get(), nhot, s));
+        FB_CUDA(cub::DeviceReduce::Sum(nullptr, tb2, cnt_pm.get(), tot.get(), npan * nhot, s));
         DBuf<unsigned char> tmp2(tb2, s);
-        FB_CUDA(cub::DeviceReduce::Sum(tmp2.get(), tb2, rowslots.get(), tot.get(), nhot, s));
+        FB_CUDA(cub::DeviceReduce::Sum(tmp2.get(), tb2, cnt_pm.get(), tot.get(), npan * nhot, s));
         nitems = read_scalar(c, tot.get());
         if (nitems <= slot_cap && nitems < (int64_t(1) << 30)) break;
         thot *= 2;
     }
     itempos.alloc(size_t(npan * nhot) + 1, s);
-    slotbase.alloc(size_t(nhot) + 1, s);
+    slotpos.alloc(size_t(npan * nhot) + 1, s);
     size_t tb = 0;
-    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), itempos.get(), npan * nhot + 1, s));
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt_pm.get(), itempos.get(), npan * nhot + 1, s));
     DBuf<unsigned char> tmp(tb, s);
-    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), itempos.get(), npan * nhot + 1, s));
-    tb = 0;
-    FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, rowslots.get(), slotbase.get(), nhot + 1, s));
-    tmp.alloc(tb, s);
-    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, rowslots.get(), slotbase.get(), nhot + 1, s));
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt_pm.get(), itempos.get(), npan * nhot + 1, s));
+    FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt_rm.get(), slotpos.get(), npan * nhot + 1, s));
     P.hot.items.alloc(size_t(nitems), s);
     P.hot.comb.alloc(size_t(nhot), s);
-    k_panel_walk<true><<<grid_for(c, nhot, 128), 128, 0, s>>>(T.rowptr.get(), T.col.get(), hot.get(), nhot, pr,
-                                                              pch, nullptr, nullptr, itempos.get(), slotbase.get(),
-                                                              P.hot.items.get(), P.hot.comb.get());
+    k_panel_cells<true><<<grid_for(c, npan * nhot), 256, 0, s>>>(T.rowptr.get(), T.col.get(), hot.get(), nhot, npan,
+                                                                 pr, pch, nullptr, nullptr, itempos.get(),
+                                                                 slotpos.get(), P.hot.items.get());
+    FB_LAUNCH_CHECK();
+    k_panel_comb<<<grid_for(c, nhot), 256, 0, s>>>(hot.get(), nhot, npan, slotpos.get(), P.hot.comb.get());
     FB_LAUNCH_CHECK();
     P.hot.nitems = P.hot.nslots = nitems;
     P.hot.ncomb = nhot;

@@ -66,6 +66,28 @@ struct PanelPlan {
     DBuf<double> part;   // chunk partials, kept with the plan (grown on demand)
 };
 
+// Values of a CSR still crossing PCIe (frpca_run_csr's pipelined upload,
+// csr.cu dcsr_upload_build): the copy stream records ev[j] when values chunk j
+// has landed; item chunk k of A's work list (ItemList::cut_*) needs chunk
+// need[k]. `all` follows the last chunk and the gather of A^T's values (on the
+// copy stream, from `perm`). The first product over the matrix consumes it
+// (spmm.cu): A*X chunk by chunk as the values land, A^T*Y after `all`.
+struct PendingValues {
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> need;
+    cudaEvent_t all = nullptr;
+    DBuf<int32_t> perm;
+    PendingValues() = default;
+    PendingValues(const PendingValues&) = delete;
+    PendingValues& operator=(const PendingValues&) = delete;
+    ~PendingValues() {
+        // never free the gather's source or a buffer the copy stream still writes
+        if (all) cudaEventSynchronize(all);
+        for (auto e : ev) cudaEventDestroy(e);
+        if (all) cudaEventDestroy(all);
+    }
+};
+
 // Device CSR: int64 row_ptr (8 B/row), int32 col ids, fp64 values (12 B/nnz).
 struct DCsr {
     int64_t rows = 0, cols = 0, nnz = 0;
@@ -82,7 +104,11 @@ struct DCsr {
     DBuf<int32_t> rank_of, rank_ids;
     int64_t hint_h = 0, sx_h = 0;
     PanelPlan pan;  // on A^T only
+    // last member, so it is destroyed (and waited for) before the buffers
+    std::shared_ptr<PendingValues> pend;
 };
+// waits (on c.stream) for every pending value of A and drops the record
+void consume_pending(Ctx& c, DCsr& A);
 constexpr int32_t kColMask = 0x7fffffff;  // id under the L2-hint sign bit
 constexpr int32_t kColHot = 0x40000000;   // shared-memory-staged column: kColHot | rank
 constexpr int32_t kRankMask = 0x3fffffff;
@@ -172,7 +198,7 @@ struct DMat {
 // width_hint > 0: the A^T*Y panel plan for that width is built at load too
 void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
                        const int64_t* h_rowptr, const int64_t* h_col, const double* h_val,
-                       int64_t width_hint = 0);
+                       int64_t width_hint = 0, bool pipelined = false);
 void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v);
 // work list of A's rows (rows with skip[r] != 0 left out), chunk size ch
 void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_t ch);

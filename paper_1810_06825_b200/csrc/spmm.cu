@@ -783,8 +783,23 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
     const double bytes = 12.0 * A.nnz + 8.0 * (A.rows + 1) + 8.0 * ncols * (A.cols + A.rows);
     const double flops = 2.0 * A.nnz * ncols;
     Prof prof(c, tag, bytes, flops);
-    if (use_sx(c, A, ncols)) return spmm_sx(c, const_cast<DCsr&>(A), X, ldx, ncols, Y, ldy);
-    ensure_hint(c, const_cast<DCsr&>(A), std::min<int64_t>(ncols, 256));
+    DCsr& Am = const_cast<DCsr&>(A);
+    if (Am.pend && !Am.pend->need.empty() && ncols <= 256 && !use_sx(c, A, ncols)) {
+        // the values are still landing (pipelined upload): item chunk k starts
+        // as soon as the values of its rows are on the device
+        std::shared_ptr<PendingValues> pv = std::move(Am.pend);
+        ensure_hint(c, Am, ncols);
+        DBuf<double> part;
+        if (A.L.nslots) part.alloc(size_t(A.L.nslots) * ncols, c.stream);
+        for (size_t k = 0; k + 1 < A.L.cut_row.size(); ++k) {
+            FB_CUDA(cudaStreamWaitEvent(c.stream, pv->ev[size_t(pv->need[k])], 0));
+            spmm_list(c, A, Items(A.L, true, int(k)), nullptr, X, ldx, int(ncols), Y, ldy, part.get());
+        }
+        return;
+    }
+    consume_pending(c, Am);
+    if (use_sx(c, A, ncols)) return spmm_sx(c, Am, X, ldx, ncols, Y, ldy);
+    ensure_hint(c, Am, std::min<int64_t>(ncols, 256));
     DBuf<double> part;
     for (int64_t off = 0; off < ncols; off += 256) {
         const int nc = int(std::min<int64_t>(256, ncols - off));
@@ -810,6 +825,7 @@ bool panel_rows_for(const DCsr& T, int64_t ncols, int64_t& pr, int64_t& cap) {
 
 void spmm_t_device(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, const char* tag) {
     if (T.rows == 0 || ncols == 0) return;
+    consume_pending(c, T);
     const int64_t w = std::min<int64_t>(ncols, 256);
     int64_t pr = 0, cap = 0;
     const bool use = panel_rows_for(T, ncols, pr, cap);
@@ -911,6 +927,7 @@ struct ChunkReducer {
 }  // namespace
 
 void spmm_device_reduced(Ctx& c, const DCsr& A, const double* X, int64_t ncols, double* Y, const char* tag) {
+    consume_pending(c, const_cast<DCsr&>(A));
     if (c.world <= 1 || ncols > 256 || A.L.cut_row.size() < 2 || A.rows == 0) {
         spmm_device(c, A, X, ncols, ncols, Y, ncols, tag);
         allreduce_sum(c, Y, A.rows * ncols);
@@ -933,6 +950,7 @@ void spmm_device_reduced(Ctx& c, const DCsr& A, const double* X, int64_t ncols, 
 }
 
 void spmm_t_device_reduced(Ctx& c, DCsr& T, const double* Y, int64_t ncols, double* Z, const char* tag) {
+    consume_pending(c, T);
     int64_t pr = 0, cap = 0;
     const bool pan = panel_rows_for(T, ncols, pr, cap);
     if (pan) ensure_panels(c, T, pr, cap);
