@@ -297,6 +297,11 @@ int frpca_ctx_destroy(frpca_ctx* c) {
             cudaStreamDestroy(c->side->stream);
             c->side.reset();
         }
+        if (c->tside) {
+            cudaStreamSynchronize(c->tside->stream);
+            cudaStreamDestroy(c->tside->stream);
+            c->tside.reset();
+        }
         c->omega_raw.release();  // stream-ordered frees before the stream goes
         c->dflag.release();
         c->wcount.release();

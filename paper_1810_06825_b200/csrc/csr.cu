@@ -286,9 +286,8 @@ __global__ void k_encode_cols(int32_t* __restrict__ col, int64_t nnz, const int3
 
 // Popularity rank of every column of A (counts = row lengths of T), kept for
 // the L2 hints of A*X.
-void build_ranks(Ctx& c, DCsr& A, const DCsr& T) {
-    const int64_t n = A.cols;
-    if (n == 0 || A.nnz == 0) return;
+void build_ranks(Ctx& c, int64_t n, const DCsr& T, DBuf<int32_t>& rank_of, DBuf<int32_t>& rank_ids) {
+    if (n == 0 || T.nnz == 0) return;
     cudaStream_t s = c.stream;
     DBuf<int32_t> cnt(size_t(n), s), ids(size_t(n), s), cnt_s(size_t(n), s), ids_s(size_t(n), s);
     k_col_counts<<<grid_for(c, n), 256, 0, s>>>(T.rowptr.get(), n, cnt.get(), ids.get());
@@ -299,11 +298,54 @@ void build_ranks(Ctx& c, DCsr& A, const DCsr& T) {
     DBuf<unsigned char> tmp(tb, s);
     FB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), tb, cnt.get(), cnt_s.get(), ids.get(),
                                                       ids_s.get(), n, 0, 32, s));
-    A.rank_of.alloc(size_t(n), s);
-    k_rank_all<<<grid_for(c, n), 256, 0, s>>>(ids_s.get(), n, A.rank_of.get());
+    rank_of.alloc(size_t(n), s);
+    k_rank_all<<<grid_for(c, n), 256, 0, s>>>(ids_s.get(), n, rank_of.get());
     FB_LAUNCH_CHECK();
-    A.rank_ids = std::move(ids_s);
-    A.hint_h = A.sx_h = 0;
+    rank_ids = std::move(ids_s);
+}
+
+// Structure of A^T (stable radix sort by column keeps ascending rows, the
+// order spmm_transpose accumulates in, sparse_matrix.hpp:229-237): T.col,
+// T.rowptr and the sort permutation (entry k of A^T is nonzero perm[k] of A),
+// whose gather of the values comes last (they may still be crossing PCIe).
+void transpose_structure(Ctx& c, const DCsr& A, DCsr& T, const int32_t* rowid, DBuf<int32_t>& perm_out) {
+    cudaStream_t s = c.stream;
+    const int64_t nnz = A.nnz, cols = A.cols;
+    if (!nnz) {
+        FB_CUDA(cudaMemsetAsync(T.rowptr.get(), 0, T.rowptr.bytes(), s));
+        return;
+    }
+    std::unique_ptr<Prof> pt(new Prof(c, "upload_t_sort", 0, 0));
+    DBuf<int32_t> keys_out(size_t(nnz), s), perm_in(size_t(nnz), s);
+    perm_out.alloc(size_t(nnz), s);
+    k_iota<<<grid_for(c, nnz), 256, 0, s>>>(perm_in.get(), nnz);
+    FB_LAUNCH_CHECK();
+    int end_bit = 1;
+    while (end_bit < 31 && (int64_t(1) << end_bit) <= cols) ++end_bit;
+    size_t tb = 0;
+    FB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, A.col.get(), keys_out.get(), perm_in.get(),
+                                            perm_out.get(), nnz, 0, end_bit, s));
+    DBuf<unsigned char> tmp(tb, s);
+    FB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, A.col.get(), keys_out.get(), perm_in.get(),
+                                            perm_out.get(), nnz, 0, end_bit, s));
+    pt.reset(new Prof(c, "upload_t_gather", 0, 0));
+    k_gather_perm<int32_t><<<grid_for(c, (nnz + 7) / 8), 256, 0, s>>>(perm_out.get(), rowid, nnz, T.col.get());
+    FB_LAUNCH_CHECK();
+    k_rowptr_from_sorted<<<grid_for(c, cols + 1), 256, 0, s>>>(keys_out.get(), nnz, cols, T.rowptr.get());
+    FB_LAUNCH_CHECK();
+}
+
+// The builder of a pipelined upload: its own stream, driven from the
+// builder thread (PendingValues::builder)
+Ctx& builder_ctx(Ctx& c) {
+    if (!c.tside) {
+        auto b = std::make_unique<Ctx>();
+        b->device = c.device;
+        b->num_sms = c.num_sms;
+        FB_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+        c.tside = std::move(b);
+    }
+    return *c.tside;
 }
 
 const char* kValidateMsg[3] = {
@@ -319,11 +361,24 @@ const char* kValidateMsg[3] = {
 // (PendingValues) tell the first product what to wait for.
 constexpr int kValChunks = 8;
 
+void PendingValues::join() {
+    if (joined) return;
+    joined = true;
+    if (builder.joinable()) builder.join();
+    if (a && rank_of.n) {
+        a->rank_of = std::move(rank_of);
+        a->rank_ids = std::move(rank_ids);
+        a->hint_h = a->sx_h = 0;
+    }
+    if (err) std::rethrow_exception(err);
+}
+
 void consume_pending(Ctx& c, DCsr& A) {
     if (!A.pend) return;
-    if (!A.pend->ev.empty()) FB_CUDA(cudaStreamWaitEvent(c.stream, A.pend->ev.back(), 0));
-    if (A.pend->all) FB_CUDA(cudaStreamWaitEvent(c.stream, A.pend->all, 0));
-    A.pend.reset();
+    std::shared_ptr<PendingValues> pv = std::move(A.pend);
+    pv->join();  // (the builder has recorded `all` once it is joined)
+    if (!pv->ev.empty()) FB_CUDA(cudaStreamWaitEvent(c.stream, pv->ev.back(), 0));
+    if (pv->all) FB_CUDA(cudaStreamWaitEvent(c.stream, pv->all, 0));
 }
 
 void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
@@ -432,79 +487,75 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     }
     if (m_valid < rows) throw InvalidArgument(kValidateMsg[0]);
     col64.release();
-    ph.reset(new Prof(c, "upload_transpose", 0, 0));
-
-    // ---- transposed CSR (stable radix sort by column keeps ascending rows,
-    // the order spmm_transpose accumulates in, sparse_matrix.hpp:229-237)
     DCsr& T = M.At;
     T.rows = cols; T.cols = rows; T.nnz = nnz;
     T.rowptr.alloc(size_t(cols + 1), s);
     T.col.alloc(size_t(nnz), s);
     T.val.alloc(size_t(nnz), s);
-    // Everything up to the work lists and the A^T*Y panel plan needs only
-    // the structure; the values (still crossing PCIe on the copy stream) are
-    // gathered last.
-    DBuf<int32_t> perm_out;
-    if (nnz) {
-        std::unique_ptr<Prof> pt(new Prof(c, "upload_t_alloc", 0, 0));
-        DBuf<int32_t> keys_out(size_t(nnz), s), perm_in(size_t(nnz), s);
-        perm_out.alloc(size_t(nnz), s);
-        pt.reset(new Prof(c, "upload_t_sort", 0, 0));
-        k_iota<<<grid_for(c, nnz), 256, 0, s>>>(perm_in.get(), nnz);
-        FB_LAUNCH_CHECK();
-        int end_bit = 1;
-        while (end_bit < 31 && (int64_t(1) << end_bit) <= cols) ++end_bit;
-        size_t tb = 0;
-        FB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, A.col.get(), keys_out.get(),
-                                                perm_in.get(), perm_out.get(), nnz, 0, end_bit, s));
-        DBuf<unsigned char> tmp(tb, s);
-        FB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, A.col.get(), keys_out.get(),
-                                                perm_in.get(), perm_out.get(), nnz, 0, end_bit, s));
-        pt.reset(new Prof(c, "upload_t_gather", 0, 0));
-        k_gather_perm<int32_t><<<grid_for(c, (nnz + 7) / 8), 256, 0, s>>>(perm_out.get(), rowid.get(), nnz, T.col.get());
-        FB_LAUNCH_CHECK();
-        k_rowptr_from_sorted<<<grid_for(c, cols + 1), 256, 0, s>>>(keys_out.get(), nnz, cols,
-                                                                    T.rowptr.get());
-        FB_LAUNCH_CHECK();
-    } else {
-        FB_CUDA(cudaMemsetAsync(T.rowptr.get(), 0, T.rowptr.bytes(), s));
-    }
-    rowid.release();
-    ph.reset(new Prof(c, "upload_items", 0, 0));
-    build_ranks(c, A, T);
-    build_items(c, A, nullptr, A.L, default_chunk(c, A));
-    build_items(c, T, nullptr, T.L, default_chunk(c, T));
-    if (width_hint > 0) {  // the panel plan of the A^T*Y the caller is about to run
-        int64_t pr = 0, cap = 0;
-        if (panel_rows_for(T, width_hint, pr, cap)) ensure_panels(c, T, pr, cap);
-    }
     if (nnz && pv) {
-        // A^T's values are gathered on the copy stream behind the last chunk;
-        // the first A*X starts on the chunks as they land (PendingValues)
-        ph.reset();
-        cudaEvent_t ev_perm;
-        FB_CUDA(cudaEventCreateWithFlags(&ev_perm, cudaEventDisableTiming));
-        FB_CUDA(cudaEventRecord(ev_perm, s));
-        FB_CUDA(cudaStreamWaitEvent(c.copy, ev_perm, 0));
-        FB_CUDA(cudaEventDestroy(ev_perm));
-        k_gather_perm<double><<<grid_for(c, (nnz + 7) / 8), 256, 0, c.copy>>>(perm_out.get(), A.val.get(), nnz,
-                                                                             T.val.get());
-        FB_LAUNCH_CHECK();
-        FB_CUDA(cudaEventCreateWithFlags(&pv->all, cudaEventDisableTiming));
-        FB_CUDA(cudaEventRecord(pv->all, c.copy));
-        pv->perm = std::move(perm_out);
-        // item chunk k of A's list reads the values up to row_ptr[cut_row[k + 1]]
+        // Pipelined: A's work list now, so the first A*X can start on the
+        // value chunks as they land; the structure of A^T, the column ranks,
+        // A^T's work list and panel plan and the gather of A^T's values are
+        // built beside it by the builder thread on its own stream, joined by
+        // the first A^T*Y (consume_pending).
+        ph.reset(new Prof(c, "upload_items", 0, 0));
+        build_items(c, A, nullptr, A.L, default_chunk(c, A));
         const int64_t V = (nnz + kValChunks - 1) / kValChunks;
         for (size_t k = 0; k + 1 < A.L.cut_row.size(); ++k) {
             const int64_t e = h_rp[A.L.cut_row[k + 1]];
             pv->need.push_back(int(e > 0 ? (e - 1) / V : 0));
         }
+        ph.reset();
+        Ctx& b = builder_ctx(c);
+        cudaEvent_t ev_ready;
+        FB_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+        FB_CUDA(cudaEventRecord(ev_ready, s));
+        FB_CUDA(cudaEventCreateWithFlags(&pv->all, cudaEventDisableTiming));
+        pv->a = &A;
+        pv->rowid = std::move(rowid);
+        PendingValues* P = pv.get();
+        const cudaEvent_t last = pv->ev.back();
+        P->builder = std::thread([&b, &A, &T, P, ev_ready, last, width_hint] {
+            try {
+                FB_CUDA(cudaSetDevice(b.device));
+                FB_CUDA(cudaStreamWaitEvent(b.stream, ev_ready, 0));
+                cudaEventDestroy(ev_ready);
+                DBuf<int32_t> perm;
+                transpose_structure(b, A, T, P->rowid.get(), perm);
+                P->rowid.release();
+                build_ranks(b, A.cols, T, P->rank_of, P->rank_ids);
+                build_items(b, T, nullptr, T.L, default_chunk(b, T));
+                if (width_hint > 0) {
+                    int64_t pr = 0, cap = 0;
+                    if (panel_rows_for(T, width_hint, pr, cap)) ensure_panels(b, T, pr, cap);
+                }
+                FB_CUDA(cudaStreamWaitEvent(b.stream, last, 0));
+                k_gather_perm<double><<<grid_for(b, (A.nnz + 7) / 8), 256, 0, b.stream>>>(perm.get(), A.val.get(),
+                                                                                        A.nnz, T.val.get());
+                FB_LAUNCH_CHECK();
+            } catch (...) {
+                P->err = std::current_exception();
+            }
+            cudaEventRecord(P->all, b.stream);
+        });
         A.pend = pv;
         T.pend = pv;
         FB_CUDA(cudaEventDestroy(ev_val));  // (the recorded work stays queued; the guard must not wait for it)
         ev_val = nullptr;
-        FB_CUDA(cudaStreamSynchronize(s));
         return;
+    }
+    ph.reset(new Prof(c, "upload_transpose", 0, 0));
+    DBuf<int32_t> perm_out;
+    transpose_structure(c, A, T, rowid.get(), perm_out);
+    rowid.release();
+    ph.reset(new Prof(c, "upload_items", 0, 0));
+    build_ranks(c, A.cols, T, A.rank_of, A.rank_ids);
+    A.hint_h = A.sx_h = 0;
+    build_items(c, A, nullptr, A.L, default_chunk(c, A));
+    build_items(c, T, nullptr, T.L, default_chunk(c, T));
+    if (width_hint > 0) {  // the panel plan of the A^T*Y the caller is about to run
+        int64_t pr = 0, cap = 0;
+        if (panel_rows_for(T, width_hint, pr, cap)) ensure_panels(c, T, pr, cap);
     }
     if (nnz) {
         ph.reset(new Prof(c, "upload_values", 0, 0));

@@ -8,6 +8,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -69,19 +70,29 @@ struct PanelPlan {
 // Values of a CSR still crossing PCIe (frpca_run_csr's pipelined upload,
 // csr.cu dcsr_upload_build): the copy stream records ev[j] when values chunk j
 // has landed; item chunk k of A's work list (ItemList::cut_*) needs chunk
-// need[k]. `all` follows the last chunk and the gather of A^T's values (on the
-// copy stream, from `perm`). The first product over the matrix consumes it
-// (spmm.cu): A*X chunk by chunk as the values land, A^T*Y after `all`.
+// need[k]. Meanwhile the builder thread builds A^T (structure, work list,
+// panel plan, then its values behind the last chunk) and A's column ranks on
+// its own stream and records `all`. The first product over the matrix
+// consumes it (spmm.cu): A*X chunk by chunk as the values land; anything else
+// joins the builder and waits for `all` (consume_pending).
+struct DCsr;
 struct PendingValues {
     std::vector<cudaEvent_t> ev;
     std::vector<int> need;
     cudaEvent_t all = nullptr;
-    DBuf<int32_t> perm;
+    std::thread builder;
+    std::exception_ptr err;
+    bool joined = false;
+    DCsr* a = nullptr;                  // receives the ranks at the join
+    DBuf<int32_t> rowid;                // the builder's gather source
+    DBuf<int32_t> rank_of, rank_ids;    // A's column ranks, built by the builder
     PendingValues() = default;
     PendingValues(const PendingValues&) = delete;
     PendingValues& operator=(const PendingValues&) = delete;
+    void join();  // joins the builder, installs the ranks, rethrows its error
     ~PendingValues() {
-        // never free the gather's source or a buffer the copy stream still writes
+        // never free a buffer the builder or the copy stream still uses
+        if (builder.joinable()) builder.join();
         if (all) cudaEventSynchronize(all);
         for (auto e : ev) cudaEventDestroy(e);
         if (all) cudaEventDestroy(all);
@@ -136,6 +147,7 @@ struct Ctx {
     bool checked = false;         // inside with_checks: deferred errors will be read
     DBuf<uint64_t> omega_raw;  // raw-word buffer of the Omega generator, kept (grown on demand)
     std::unique_ptr<Ctx> side;  // second stream for work overlapped with the upload (frpca_run_csr)
+    std::unique_ptr<Ctx> tside;  // builder of A^T beside the first A*X (pipelined upload)
     cudaStream_t copy = nullptr;  // device->host copies of results overlapped with the output GEMMs
     // sharded runs: the allreduce of a product's finished row chunks runs here
     // while the next chunks are computed (spmm.cu *_reduced)
@@ -192,6 +204,14 @@ struct DMat {
     int64_t offset = 0;            // first global row (row shard) or column (col shard)
     int col_shard = 0;
     std::atomic<uint64_t> passes{0};
+    DMat() = default;
+    ~DMat() {
+        // the builder of a pipelined upload writes into At: finish it first
+        std::shared_ptr<PendingValues> p = A.pend ? A.pend : At.pend;
+        A.pend.reset();
+        At.pend.reset();
+        p.reset();
+    }
 };
 
 // ---- csr.cu
