@@ -181,6 +181,13 @@ int frpca_gaussian_matrix(frpca_ctx* ctx, int64_t rows, int64_t cols, uint64_t s
  * (out[(p / period) (w1 - w0) + p mod period - w0]). */
 int frpca_gaussian_window(frpca_ctx* ctx, int64_t count, int64_t period, int64_t w0, int64_t w1, uint64_t seed,
                           double* out);
+/* The same window in the layout the products gather from: rows [w0, w1) of
+ * the column-major stream as a row-major (w1 - w0) x ceil(count / period)
+ * matrix (out[(p mod period - w0) ceil(count / period) + p / period]); positions
+ * >= count are not written. Replaces gaussian_matrix + transpose for the
+ * row-major sketch panels (randsvd.hpp:246-247, :298-299). */
+int frpca_gaussian_window_rows(frpca_ctx* ctx, int64_t count, int64_t period, int64_t w0, int64_t w1,
+                               uint64_t seed, double* out);
 /* lu_basis (dense_kernels.hpp:50-116): X = P^T L of M (m x l, m >= l). */
 int frpca_lu_basis(frpca_ctx* ctx, int64_t m, int64_t l, const double* M, double* X);
 /* orth (dense_kernels.hpp:30-48): Q (m x l, column-major) of the Householder

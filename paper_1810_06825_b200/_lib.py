@@ -73,6 +73,7 @@ SIGNATURES = {
     "frpca_spmm": (C.c_int, [_vp, _vp, C.c_int, _vp, _i64, _i64, _vp]),
     "frpca_gaussian_matrix": (C.c_int, [_vp, _i64, _i64, _u64, _vp]),
     "frpca_gaussian_window": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _vp]),
+    "frpca_gaussian_window_rows": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _vp]),
     "frpca_lu_basis": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
     "frpca_orth": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
     "frpca_eig_svd": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),

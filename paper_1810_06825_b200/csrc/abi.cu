@@ -472,6 +472,22 @@ int frpca_gaussian_window(frpca_ctx* c, int64_t count, int64_t period, int64_t w
     });
 }
 
+int frpca_gaussian_window_rows(frpca_ctx* c, int64_t count, int64_t period, int64_t w0, int64_t w1, uint64_t seed,
+                               double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        require(count >= 1 && period >= 1 && 0 <= w0 && w0 < w1 && w1 <= period, "gaussian_window: bad window");
+        std::lock_guard<std::mutex> lk(c->mu);
+        FB_CUDA(cudaSetDevice(c->device));
+        const int64_t n = (w1 - w0) * ((count + period - 1) / period);
+        DBuf<double> d(size_t(n), c->stream);
+        FB_CUDA(cudaMemcpyAsync(d.get(), out, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        with_checks(*c, [&] { gaussian_stream_window(*c, seed, count, period, w0, w1, d.get(), true); });
+        FB_CUDA(cudaMemcpyAsync(out, d.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        FB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
 int frpca_lu_basis(frpca_ctx* c, int64_t m, int64_t l, const double* Mh, double* X) {
     return guarded([&] {
         check_ctx(c);
@@ -686,6 +702,7 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
             }
         }
         DBuf<double>* pre = nullptr;
+        bool pre_rm = false;
         std::exception_ptr side_err;
         std::thread side_thread;
         if (ok) {
@@ -700,11 +717,14 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
             Ctx* side = c->side.get();
             const uint64_t seed = mix_seed(cfg->seed, 0xA11CEull);
             const int64_t count = orow * ocol;
-            side_thread = std::thread([side, seed, count, &pre, &side_err] {
+            // frpca and odd-q frpcat read the sketch row-major: generated so
+            const bool rm = algo == FRPCA_ALGO_FRPCA || (algo == FRPCA_ALGO_FRPCAT && q % 2 == 1);
+            pre_rm = rm;
+            side_thread = std::thread([side, seed, count, orow, rm, &pre, &side_err] {
                 try {
                     FB_CUDA(cudaSetDevice(side->device));
                     pre = &side->slot(0, size_t(count));  // kept: swapped with the run's slot
-                    gaussian_stream_device(*side, seed, count, pre->get());
+                    gaussian_stream_window(*side, seed, count, orow, 0, orow, pre->get(), rm);
                     FB_CUDA(cudaStreamSynchronize(side->stream));
                 } catch (...) {
                     side_err = std::current_exception();
@@ -738,6 +758,7 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
         a.U = U; a.S = S; a.V = V; a.basis = basis;
         a.device_io = (cfg->flags & FRPCA_FLAG_DEVICE_IO) != 0;
         a.pre = ok ? pre : nullptr;
+        a.pre_rowmajor = pre_rm;
         if (dispatched) *dispatched = algo;
         require(algo == FRPCA_ALGO_FRPCA || algo == FRPCA_ALGO_FRPCAT || algo == FRPCA_ALGO_BASIC_RPCA ||
                     algo == FRPCA_ALGO_BASIC_RPCAT,

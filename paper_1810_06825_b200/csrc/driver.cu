@@ -178,7 +178,7 @@ static void sketch_cols(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, in
 // stream when frpca_run_csr overlapped it with the upload, else generated now.
 static void sketch_into(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, DBuf<double>& dst) {
     const size_t count = size_t(rows) * size_t(cols);
-    if (a.pre && a.pre->get() && a.pre->n >= count && !a.omega) {
+    if (a.pre && !a.pre_rowmajor && a.pre->get() && a.pre->n >= count && !a.omega) {
         cudaStream_t ps = a.pre->s;
         std::swap(dst, *a.pre);  // both buffers stay allocated (workspace slots)
         dst.s = c.stream;
@@ -187,6 +187,32 @@ static void sketch_into(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, DB
     }
     if (dst.n < count) dst.alloc(count, c.stream);
     sketch_stream(c, a, rows, cols, dst.get());
+}
+
+// Rows [r0, r1) of Omega (rows x cols, column-major stream order) as the
+// row-major (r1 - r0) x cols panel the products gather from: generated
+// straight into that layout (rng.cu k_place_rm), or the pre-generated one of
+// frpca_run_csr; an injected or host-generated sketch is transposed.
+static void sketch_rowmajor(Ctx& c, const RunArgs& a, int64_t rows, int64_t cols, int64_t r0, int64_t r1,
+                            DBuf<double>& dst) {
+    const int64_t nr = r1 - r0;
+    const size_t count = size_t(nr) * size_t(cols);
+    if (a.pre && a.pre_rowmajor && a.pre->get() && a.pre->n >= count && !a.omega && nr == rows) {
+        cudaStream_t ps = a.pre->s;
+        std::swap(dst, *a.pre);  // both buffers stay allocated (workspace slots)
+        dst.s = c.stream;
+        a.pre->s = ps;
+        return;
+    }
+    if (dst.n < count) dst.alloc(count, c.stream);
+    if (a.omega || (a.cfg.flags & FRPCA_FLAG_HOST_OMEGA)) {
+        DBuf<double> t(count, c.stream);
+        sketch_rows(c, a, rows, cols, r0, r1, t.get());   // nr x cols column-major
+        transpose_device(c, t.get(), cols, nr, dst.get());
+        return;
+    }
+    const uint64_t seed = mix_seed(a.cfg.seed, 0xA11CEull);
+    gaussian_stream_window(c, seed, (cols - 1) * rows + r1, rows, r0, r1, dst.get(), /*rowmajor=*/true);
 }
 
 static void check_common(const frpca_config& cfg) {  // randsvd.hpp:78-81
@@ -323,9 +349,7 @@ void run_frpcat(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
             std::swap(Q, Z);
         }
     } else {
-        DBuf<double>& om = c.slot(3, 0);
-        sketch_into(c, a, n, l, om);                      // n x l column-major
-        transpose_device(c, om.get(), l, n, Q.get());     // -> row-major n x l
+        sketch_rowmajor(c, a, n, l, 0, n, Q);             // Q = Omega, row-major n x l
     }
     T.mark(1);
 
@@ -387,15 +411,9 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
     StageTimer T(S);
     T.mark(0);
     if (q % 2 == 0) {
-        // Omega: gcols x l column-major; this rank needs rows [offset, offset+n)
-        DBuf<double>& om = c.slot(3, 0);
-        if (M.offset == 0 && n == M.gcols) {
-            sketch_into(c, a, M.gcols, l, om);
-        } else {
-            if (om.n < size_t(n * l)) om.alloc(size_t(n * l), S);
-            sketch_rows(c, a, M.gcols, l, M.offset, M.offset + n, om.get());   // this rank's rows only
-        }
-        transpose_device(c, om.get(), l, n, bufN.get());
+        // Omega: gcols x l column-major; this rank needs rows [offset, offset+n),
+        // row-major
+        sketch_rowmajor(c, a, M.gcols, l, M.offset, M.offset + n, bufN);
         spmm_pass_reduced(c, M, false, bufN.get(), l, Y.get());  // A Omega, m x l, summed over ranks
         if (q > 2) {
             lu_basis_device(c, Y.get(), m, l);
@@ -404,9 +422,7 @@ void run_frpca(Ctx& c, DMat& M, const RunArgs& a, frpca_stats* st) {
             eig_svd_U(c, Y.get(), m, l, Q.get());
         }
     } else {
-        DBuf<double>& om = c.slot(3, 0);
-        sketch_into(c, a, m, l, om);
-        transpose_device(c, om.get(), l, m, Q.get());
+        sketch_rowmajor(c, a, m, l, 0, m, Q);              // Q = Omega, row-major m x l
     }
     T.mark(1);
 

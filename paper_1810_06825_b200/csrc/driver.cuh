@@ -19,6 +19,7 @@ struct RunArgs {
     // first sketch_into of the call; a repeated call (run_algorithm's retry)
     // regenerates it
     DBuf<double>* pre = nullptr;
+    bool pre_rowmajor = false;  // `pre` holds the row-major (transposed) layout
 };
 
 // eig_svd pipeline state: Gram -> (allreduce) -> syevd (B becomes V) -> rank check.

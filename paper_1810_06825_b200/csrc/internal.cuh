@@ -295,7 +295,10 @@ void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out);
 // the positions p < count of the same stream with (p mod P) in [w0, w1), into
 // out[(p / P) (w1 - w0) + (p mod P - w0)]: a rank's slice of the sketch
 // (randsvd.hpp:246-247 sharded; only that slice is written)
-void gaussian_stream_window(Ctx& c, uint64_t seed, int64_t count, int64_t P, int64_t w0, int64_t w1, double* out);
+// rowmajor: the window's rows as a row-major (w1 - w0) x ceil(count / P) matrix
+// (the transposed layout the products gather from) instead of column-major
+void gaussian_stream_window(Ctx& c, uint64_t seed, int64_t count, int64_t P, int64_t w0, int64_t w1, double* out,
+                            bool rowmajor = false);
 void gaussian_stream_host(uint64_t seed, int64_t count, double* out);
 
 }  // namespace fb

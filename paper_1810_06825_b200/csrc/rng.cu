@@ -134,38 +134,6 @@ k_jump_level(uint64_t* __restrict__ states, const uint32_t* __restrict__ polys, 
     if (tid < NN) states[size_t(k) * NN + tid] = (cur ? R1 : ext)[tid];
 }
 
-// Raw stream of a segment: 156 new words per step, one barrier per step. The
-// words live in a ring of 4 x 156: step s reads its window at ring offset
-// (s mod 4) 156 ([b, b + 312)) and writes the new words at [b + 312, b + 468)
-// (mod 624), so no window copy; the tempered outputs go straight to global
-// memory (coalesced). 160 threads: the last 4 only keep the barrier count.
-constexpr int GT = 160;
-constexpr int kGenPerSm = 6;  // segments per SM the host plans for (5 warps each)
-__global__ void __launch_bounds__(GT)
-k_gen(const uint64_t* __restrict__ states, int64_t seg0, int64_t steps, uint64_t* __restrict__ raw) {
-    constexpr int RING = 4 * MM;
-    __shared__ uint64_t X[RING];
-    const int tid = threadIdx.x;
-    const int64_t seg = seg0 + blockIdx.x;
-    for (int i = tid; i < NN; i += GT) X[i] = states[seg * NN + i];
-    __syncthreads();
-    uint64_t* dst = raw + int64_t(blockIdx.x) * steps * MM + tid;
-    int b = 0;
-    for (int64_t st = 0; st < steps; ++st) {
-        if (tid < MM) {
-            const int i0 = b + tid;
-            const int i1 = i0 + 1 < RING ? i0 + 1 : i0 + 1 - RING;
-            const int i2 = i0 + MM < RING ? i0 + MM : i0 + MM - RING;
-            const int io = i0 + 2 * MM < RING ? i0 + 2 * MM : i0 + 2 * MM - RING;
-            const uint64_t nw = mt_next(X[i0], X[i1], X[i2]);
-            X[io] = nw;
-            dst[st * MM] = temper(nw);
-        }
-        b = b + MM < RING ? b + MM : 0;
-        __syncthreads();
-    }
-}
-
 // polar attempt on raw words (w0, w1): x = 2u1 - 1, y = 2u2 - 1, r2 = x^2 + y^2
 __device__ __forceinline__ bool attempt(uint64_t w0, uint64_t w1, double& x, double& y, double& r2) {
     x = __dsub_rn(__dmul_rn(2.0, canonical(w0)), 1.0);
@@ -174,109 +142,179 @@ __device__ __forceinline__ bool attempt(uint64_t w0, uint64_t w1, double& x, dou
     return !(r2 > 1.0 || r2 == 0.0);
 }
 
-constexpr int PT = 256;      // threads per chunk CTA
-constexpr int PPT = 4;       // attempts per thread
-constexpr int CHUNK = PT * PPT;
-
-// accepted attempts per chunk of CHUNK consecutive attempts
-__global__ void __launch_bounds__(PT)
-k_count(const uint64_t* __restrict__ raw, int64_t npairs, int64_t* __restrict__ cnt) {
-    __shared__ int red[PT / 32];
-    // chunk b = attempts [b CHUNK, (b + 1) CHUNK), lane-interleaved (coalesced)
-    const int64_t p0 = int64_t(blockIdx.x) * CHUNK + threadIdx.x;
-    int c = 0;
-    #pragma unroll
-    for (int e = 0; e < PPT; ++e) {
-        const int64_t q = p0 + int64_t(e) * PT;
-        if (q < npairs) {
-            const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(raw + 2 * q);
-            double x, y, r2;
-            c += attempt(w.x, w.y, x, y, r2) ? 1 : 0;
-        }
-    }
-    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int t = 0;
-        for (int w = 0; w < PT / 32; ++w) t += red[w];
-        cnt[blockIdx.x] = t;
-    }
+// the two normals of an accepted attempt: mult = sqrt(-2 log(r2) / r2);
+// y*mult first, then the saved x*mult, each through `ret * stddev + mean`
+// with (1, 0) (random.tcc)
+__device__ __forceinline__ void polar_pair(double x, double y, double r2, double& a, double& b) {
+    const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, glibc_log::log_polar(r2)), r2));
+    a = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), 1.0), 0.0);
+    b = __dadd_rn(__dmul_rn(__dmul_rn(x, mult), 1.0), 0.0);
 }
 
-// A window of the stream: positions p < count with (p mod P) in [w0, w1) go
-// to out[(p / P) (w1 - w0) + (p mod P - w0)] -- a rank's rows of a
-// column-major sketch (P = rows), or a contiguous slice (P = count).
+// Phase 1, one CTA per segment (seg0 + blockIdx.x): the raw stream, 156 new
+// words per step from a ring of 4 x 156 words (step s reads [b, b + 312) and
+// writes [b + 312, b + 468) mod 624, b = 156 (s mod 4)), in rounds of four
+// steps. After a round the ring holds its 624 words, word w at (312 + w) mod
+// 624: 312 polar attempts (threads t < 156 take attempts t and t + 156),
+// whose normals go, in stream order, to the segment's staging slots
+// stage[seg J + i]; cnt[seg] = normals of the segment. Nothing but the
+// normals reaches global memory (no raw-word buffer).
+constexpr int GT = 160;
+constexpr int kGenPerSm = 9;  // segments per SM the host plans for (5 warps each; 9 fit by registers)
+__global__ void __launch_bounds__(GT)
+k_gen_polar(const uint64_t* __restrict__ states, int64_t seg0, int64_t steps, int64_t J,
+            double* __restrict__ stage, int64_t* __restrict__ cnt) {
+    constexpr int RING = 4 * MM;
+    using Scan = cub::BlockScan<unsigned, GT>;
+    __shared__ uint64_t X[RING];
+    __shared__ typename Scan::TempStorage tmp;
+    const int tid = threadIdx.x;
+    const int64_t seg = seg0 + blockIdx.x;
+    for (int i = tid; i < NN; i += GT) X[i] = states[seg * NN + i];
+    double* out = stage + seg * J;
+    int64_t pairs = 0;  // accepted attempts so far (block-uniform)
+    for (int64_t r = 0; r < steps; r += 4) {
+        __syncthreads();  // (the previous round's ring reads are done)
+#pragma unroll
+        for (int st = 0; st < 4; ++st) {
+            if (tid < MM) {
+                const int i0 = st * MM + tid;
+                const int i1 = i0 + 1 < RING ? i0 + 1 : i0 + 1 - RING;
+                const int i2 = i0 + MM < RING ? i0 + MM : i0 + MM - RING;
+                const int io = i0 + 2 * MM < RING ? i0 + 2 * MM : i0 + 2 * MM - RING;
+                X[io] = mt_next(X[i0], X[i1], X[i2]);
+            }
+            __syncthreads();
+        }
+        bool ok0 = false, ok1 = false;
+        double x0 = 0, y0 = 0, r0 = 0, x1 = 0, y1 = 0, r1 = 0;
+        if (tid < MM) {
+            // attempt t: words 2t, 2t + 1 at ring 312 + 2t (+1); attempt t + 156:
+            // words 312 + 2t (+1) at ring 2t (+1)
+            ok0 = attempt(temper(X[2 * MM + 2 * tid]), temper(X[2 * MM + 2 * tid + 1]), x0, y0, r0);
+            ok1 = attempt(temper(X[2 * tid]), temper(X[2 * tid + 1]), x1, y1, r1);
+        }
+        unsigned pre = 0, tot = 0;
+        Scan(tmp).ExclusiveSum((ok0 ? 1u : 0u) | ((ok1 ? 1u : 0u) << 16), pre, tot);
+        const int64_t first = int64_t(tot & 0xffffu);
+        if (ok0) {
+            double a, b;
+            polar_pair(x0, y0, r0, a, b);
+            const int64_t o = 2 * (pairs + int64_t(pre & 0xffffu));
+            out[o] = a;
+            out[o + 1] = b;
+        }
+        if (ok1) {
+            double a, b;
+            polar_pair(x1, y1, r1, a, b);
+            const int64_t o = 2 * (pairs + first + int64_t(pre >> 16));
+            out[o] = a;
+            out[o + 1] = b;
+        }
+        pairs += first + int64_t(tot >> 16);
+    }
+    if (tid == 0) cnt[seg] = 2 * pairs;
+}
+
+// A window of the stream: positions p < count with (p mod P) in [w0, w1).
+// Column-major: out[(p / P) (w1 - w0) + (p mod P - w0)] (a rank's rows of a
+// column-major sketch; P = count: a contiguous slice). Row-major (k_place_rm):
+// out[(p mod P - w0) ncols + p / P], the transposed layout the products read.
 struct Window {
     int64_t P, w0, w1;
     bool ident;  // the whole stream, out[p]
 };
 
-__device__ __forceinline__ void emit_win(double* __restrict__ out, int64_t p, double v, int64_t count,
-                                         const Window& w) {
-    if (p >= count) return;
-    const int64_t q = p / w.P, r = p - q * w.P;
-    if (r < w.w0 || r >= w.w1) return;
-    out[q * (w.w1 - w.w0) + (r - w.w0)] = v;
+// Phase 2, column-major window: segment s0 + blockIdx.x's normals to their
+// stream positions (positions in [plo, phi) only)
+__global__ void __launch_bounds__(256)
+k_place(const double* __restrict__ stage, int64_t J, const int64_t* __restrict__ off,
+        const int64_t* __restrict__ cnt, int64_t s0, int64_t plo, int64_t phi, Window w, double* __restrict__ out) {
+    const int64_t seg = s0 + blockIdx.x;
+    const int64_t base = off[seg], n = cnt[seg];
+    const double* src = stage + seg * J;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int64_t p = base + i;
+        if (p < plo || p >= phi) continue;
+        const double v = __ldcs(src + i);
+        if (w.ident) {
+            __stcs(out + p, v);
+            continue;
+        }
+        const int64_t q = p / w.P, r = p - q * w.P;
+        if (r >= w.w0 && r < w.w1) __stcs(out + q * (w.w1 - w.w0) + (r - w.w0), v);
+    }
 }
 
-// normals of the accepted attempts, written at their stream positions
-__global__ void __launch_bounds__(PT, 5)
-k_emit(const uint64_t* __restrict__ raw, int64_t npairs, const int64_t* __restrict__ off,
-       double* __restrict__ out, int64_t count, Window win) {
-    // round e of the chunk = attempts b CHUNK + e PT + [0, PT) (coalesced
-    // loads); the stream position of an accepted attempt = accepted attempts
-    // of the earlier rounds + of the lower lanes of its round: one block scan
-    // of the per-round flags packed in 16-bit fields
-    using Scan = cub::BlockScan<unsigned long long, PT>;
-    __shared__ typename Scan::TempStorage tmp;
-    const int64_t base = off[blockIdx.x];
-    if (2 * base >= count) return;
-    const int64_t p0 = int64_t(blockIdx.x) * CHUNK + threadIdx.x;
-    double xs[PPT], ys[PPT], rs[PPT];
-    bool ok[PPT];
-    unsigned long long flags = 0;
-    #pragma unroll
-    for (int e = 0; e < PPT; ++e) {
-        const int64_t q = p0 + int64_t(e) * PT;
-        ok[e] = false;
-        if (q < npairs) {
-            const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(raw + 2 * q);
-            ok[e] = attempt(w.x, w.y, xs[e], ys[e], rs[e]);
-        }
-        flags |= (ok[e] ? 1ull : 0ull) << (16 * e);
+// Segment lookup of the row-major placement: seg_at[b] = the segment holding
+// stream position b * kBucket (segments hold thousands of normals, so a
+// position's segment is seg_at[p / kBucket] or one of the next few).
+constexpr int64_t kBucket = 1024;
+__global__ void k_seg_buckets(const int64_t* __restrict__ off, int64_t nseg, int64_t nbuck,
+                              int32_t* __restrict__ seg_at) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nseg; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b0 = (off[k] + kBucket - 1) / kBucket;
+        const int64_t b1 = min(nbuck, (off[k + 1] + kBucket - 1) / kBucket);
+        for (int64_t b = b0; b < b1; ++b) seg_at[b] = int32_t(k);
     }
-    unsigned long long pre = 0, tot = 0;
-    Scan(tmp).ExclusiveSum(flags, pre, tot);
-    const bool vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    int64_t rb = base;
-    #pragma unroll
-    for (int e = 0; e < PPT; ++e) {
-        if (ok[e]) {
-            const int64_t idx = 2 * (rb + int64_t((pre >> (16 * e)) & 0xffffull));
-            // mult = sqrt(-2 log(r2) / r2); y*mult first, then the saved
-            // x*mult; each passes through `ret * stddev + mean` with (1, 0)
-            // (random.tcc).
-            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, glibc_log::log_polar(rs[e])), rs[e]));
-            const double a = __dadd_rn(__dmul_rn(__dmul_rn(ys[e], mult), 1.0), 0.0);
-            const double b = __dadd_rn(__dmul_rn(__dmul_rn(xs[e], mult), 1.0), 0.0);
-            if (!win.ident) {
-                emit_win(out, idx, a, count, win);
-                emit_win(out, idx + 1, b, count, win);
-            } else if (vec && idx + 1 < count) {
-                __stcs(reinterpret_cast<double2*>(out + idx), make_double2(a, b));
-            } else {
-                if (idx < count) out[idx] = a;
-                if (idx + 1 < count) out[idx + 1] = b;
+}
+
+__device__ __forceinline__ int64_t seg_of(const int64_t* __restrict__ off, const int32_t* __restrict__ seg_at,
+                                          int64_t nseg, int64_t p) {
+    int64_t k = seg_at[p / kBucket];
+    while (k + 1 < nseg && off[k + 1] <= p) ++k;
+    return k;
+}
+
+// Phase 2, row-major window: a 128-row x 32-column tile of the output per
+// CTA. Column q's rows r0..r0+127 are the stream run q P + r: read from the
+// staging (one or two segments) into shared memory, 16 independent loads in
+// flight per thread, then written as 256-byte row segments. Positions
+// outside [plo, phi) are left to another batch.
+constexpr int kTR = 128, kTC = 32;
+__global__ void __launch_bounds__(256)
+k_place_rm(const double* __restrict__ stage, int64_t J, const int64_t* __restrict__ off,
+           const int32_t* __restrict__ seg_at, int64_t nseg, int64_t plo, int64_t phi, int64_t P, int64_t w0,
+           int64_t w1, int64_t ncols, double* __restrict__ out) {
+    __shared__ double tile[kTC][kTR + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // column blocks vary fastest across CTAs, so the CTAs in flight complete
+    // whole output rows (full lines merge in L2 before they reach DRAM)
+    const int64_t ncb = (ncols + kTC - 1) / kTC;
+    const int64_t r0 = w0 + int64_t(blockIdx.x / ncb) * kTR, q0 = int64_t(blockIdx.x % ncb) * kTC;
+    double v[kTC / 8][kTR / 32];
+#pragma unroll
+    for (int j = 0; j < kTC / 8; ++j) {
+        const int64_t q = q0 + warp + 8 * j;
+#pragma unroll
+        for (int h = 0; h < kTR / 32; ++h) {
+            const int rr = lane + 32 * h;
+            const int64_t p = q * P + r0 + rr;
+            v[j][h] = 0.0;
+            if (q < ncols && r0 + rr < w1 && p >= plo && p < phi) {
+                const int64_t k = seg_of(off, seg_at, nseg, p);
+                v[j][h] = __ldcs(stage + k * J + (p - off[k]));
             }
         }
-        rb += int64_t((tot >> (16 * e)) & 0xffffull);
+    }
+#pragma unroll
+    for (int j = 0; j < kTC / 8; ++j)
+#pragma unroll
+        for (int h = 0; h < kTR / 32; ++h) tile[warp + 8 * j][lane + 32 * h] = v[j][h];
+    __syncthreads();
+    const int64_t q = q0 + lane;
+    for (int rr = warp; rr < kTR; rr += 8) {
+        const int64_t r = r0 + rr;
+        if (r >= w1 || q >= ncols) continue;
+        const int64_t p = q * P + r;
+        if (p < plo || p >= phi) continue;
+        __stcs(out + (r - w0) * ncols + q, tile[lane][rr]);
     }
 }
 
 // single-batch Omega: the shortfall check of the host loop, on the device
-__global__ void k_check_short(const int64_t* __restrict__ pairs, int64_t count, int* __restrict__ flag) {
-    if (2 * pairs[0] < count) atomicCAS(flag, 0, kErrOmegaShort);
+__global__ void k_check_short(const int64_t* __restrict__ total, int64_t count, int* __restrict__ flag) {
+    if (total[0] < count) atomicCAS(flag, 0, kErrOmegaShort);
 }
 
 struct PolyCache {
@@ -324,21 +362,21 @@ void jump_states(Ctx& c, uint64_t* states, const uint32_t* polys, int groups, in
 }  // namespace
 
 void gaussian_stream_device(Ctx& c, uint64_t seed, int64_t count, double* out) {
-    gaussian_stream_window(c, seed, count, count, 0, count, out);
+    gaussian_stream_window(c, seed, count, count, 0, count, out, false);
 }
 
 void gaussian_stream_window(Ctx& c, uint64_t seed, int64_t count, int64_t period, int64_t w0, int64_t w1,
-                            double* out) {
+                            double* out, bool rowmajor) {
     if (count <= 0) return;
     const Window win{period, w0, w1, period >= count && w0 == 0 && w1 >= count};
+    const int64_t ncols = (count + period - 1) / period;  // columns of the (row-major) window
     Prof prof(c, "omega_total", 8.0 * double(count) * double(w1 - w0) / double(period), 0.0);
     cudaStream_t s = c.stream;
     // attempts needed with margin: accepted ~ Bin(P, pi/4), need 2*acc >= count
     const double half = 0.5 * double(count);
     const int64_t P = int64_t(half / (M_PI / 4.0) + 8.0 * std::sqrt(half / (M_PI / 4.0)) + 64.0);
     // segments of J = 156 * 2^e words: the fewest that still fill the
-    // generator (one CTA per segment, kGenPerSm per SM), capped so
-    // that a batch of <= 2^30 raw words holds >= that many segments
+    // generator (one CTA per segment, kGenPerSm per SM), at most 2^12 steps
     const int64_t fill = int64_t(c.num_sms) * kGenPerSm;
     int log2S = 6;
     while (log2S < 12 && (2 * P + (int64_t(MM) << log2S) - 1) / (int64_t(MM) << log2S) > fill) ++log2S;
@@ -354,71 +392,67 @@ void gaussian_stream_window(Ctx& c, uint64_t seed, int64_t count, int64_t period
     smem_optin(k_jump_level, size_t(kNibBytes));
     uint64_t s0[NN];
     mt64_seed_state(seed, s0);
+    // one batch of K segments covers the stream (shortfall probability
+    // ~1e-15): the deferred check re-runs the call with omega_sync, whose
+    // host check regenerates with the 2K + 1 segments of the jump table
     int64_t K = (2 * P + J - 1) / J;
-    // room for 2K + 1 segments so that the rare shortfall extends in place
     const int64_t Kmax = 2 * K + 1;
     require(Kmax <= (int64_t(1) << (4 * kJumpLevels)), "gaussian_matrix: stream too long for the jump table");
-    DBuf<uint64_t> states(size_t(Kmax) * NN, s);
+    const bool defer = c.checked && !c.omega_sync;
+    DBuf<uint64_t> states(size_t(defer ? K : Kmax) * NN, s);
     {
         Prof pj(c, "omega_jump", 0.0, 0.0);
         FB_CUDA(cudaMemcpyAsync(states.get(), s0, sizeof(s0), cudaMemcpyHostToDevice, s));
         jump_states(c, states.get(), polys, groups, 1, K);
     }
-    // batches of segments: raw words -> per-chunk counts -> scan -> normals
-    const int64_t seg_per_batch = std::max<int64_t>(1, (int64_t(1) << 30) / J);
-    DBuf<uint64_t>& raw = c.omega_raw;  // kept on the context (see DESIGN: pool remaps)
-    {
-        Prof pa(c, "omega_alloc", 0.0, 0.0);
-        const size_t need = size_t(std::min(K, seg_per_batch) * J);
-        if (raw.n < need) raw.alloc(need, s);
-    }
-    int64_t pairs_done = 0;  // accepted attempts emitted so far
-    // one batch covers the stream (every BASELINE config): no host round trip,
-    // the shortfall test is deferred (err_check re-runs the call with
-    // omega_sync); otherwise the batches are checked on the host
-    const bool defer = c.checked && !c.omega_sync && K <= seg_per_batch;
-    for (int64_t seg0 = 0; 2 * pairs_done < count; seg0 += seg_per_batch) {
-        if (seg0 >= K) {
-            // shortfall (probability ~ 1e-15): extend the jump table to Kmax
-            require(seg0 < Kmax, "gaussian_matrix: device stream generation did not converge");
-            jump_states(c, states.get(), polys, groups, K, Kmax);
-            K = Kmax;
-        }
-        const int64_t nseg = std::min(seg_per_batch, K - seg0);
-        const int64_t npairs = nseg * J / 2;
-        const int64_t nchunks = (npairs + CHUNK - 1) / CHUNK;
+    for (int attempt_no = 0;; ++attempt_no) {
+        // staging: J normals per segment at most (every attempt accepted)
+        DBuf<uint64_t>& stage = c.omega_raw;  // kept on the context
+        if (stage.n < size_t(K * J)) stage.alloc(size_t(K * J), s);
+        double* st = reinterpret_cast<double*>(stage.get());
+        DBuf<int64_t> cnt(size_t(K) + 1, s), off(size_t(K) + 1, s);
         {
-            Prof pg(c, "omega_gen", 8.0 * nseg * J, 0.0);
-            k_gen<<<unsigned(nseg), GT, 0, s>>>(states.get(), seg0, steps, raw.get());
-            FB_LAUNCH_CHECK();
-        }
-        DBuf<int64_t> cnt(size_t(nchunks) + 1, s), off(size_t(nchunks) + 1, s);
-        {
-            Prof pc(c, "omega_count", 8.0 * nseg * J, 0.0);
-            FB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-            k_count<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, cnt.get());
+            Prof pg(c, "omega_gen", 8.0 * double(count), 0.0);
+            FB_CUDA(cudaMemsetAsync(cnt.get() + K, 0, sizeof(int64_t), s));
+            k_gen_polar<<<unsigned(K), GT, 0, s>>>(states.get(), 0, steps, J, st, cnt.get());
             FB_LAUNCH_CHECK();
             size_t tb = 0;
-            FB_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tb, cnt.get(), off.get(), cub::Sum(),
-                                                   pairs_done, nchunks + 1, s));
+            FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), off.get(), K + 1, s));
             DBuf<unsigned char> tmp(tb, s);
-            FB_CUDA(cub::DeviceScan::ExclusiveScan(tmp.get(), tb, cnt.get(), off.get(), cub::Sum(),
-                                                   pairs_done, nchunks + 1, s));
+            FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), off.get(), K + 1, s));
         }
-        {
-            Prof pe(c, "omega_emit", 8.0 * nseg * J + 8.0 * count, 0.0);
-            k_emit<<<unsigned(nchunks), PT, 0, s>>>(raw.get(), npairs, off.get(), out, count, win);
-            FB_LAUNCH_CHECK();
-        }
+        // FRPCA_TEST_OMEGA_SHORT: tests force the shortfall -> re-run path
+        const bool force = std::getenv("FRPCA_TEST_OMEGA_SHORT") != nullptr;
         if (defer) {
-            // FRPCA_TEST_OMEGA_SHORT: tests force the shortfall -> re-run path
-            const bool force = std::getenv("FRPCA_TEST_OMEGA_SHORT") != nullptr;
-            k_check_short<<<1, 1, 0, s>>>(off.get() + nchunks, force ? INT64_MAX : count, err_flag(c));
+            k_check_short<<<1, 1, 0, s>>>(off.get() + K, force ? INT64_MAX : count, err_flag(c));
             FB_LAUNCH_CHECK();
-            break;
+        } else {
+            int64_t total = 0;
+            FB_CUDA(cudaMemcpyAsync(&total, off.get() + K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            FB_CUDA(cudaStreamSynchronize(s));
+            if (total < count || (force && attempt_no == 0)) {
+                // shortfall: the whole stream again over the longer jump table
+                require(K < Kmax, "gaussian_matrix: device stream generation did not converge");
+                jump_states(c, states.get(), polys, groups, K, Kmax);
+                K = Kmax;
+                continue;
+            }
         }
-        FB_CUDA(cudaMemcpyAsync(&pairs_done, off.get() + nchunks, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        FB_CUDA(cudaStreamSynchronize(s));
+        Prof pe(c, "omega_place", 8.0 * double(count) * double(w1 - w0) / double(period) * 2.0, 0.0);
+        if (rowmajor) {
+            const int64_t nbuck = (count + kBucket - 1) / kBucket;
+            DBuf<int32_t> seg_at(size_t(nbuck), s);
+            FB_CUDA(cudaMemsetAsync(seg_at.get(), 0, seg_at.bytes(), s));  // (a deferred shortfall leaves a tail)
+            k_seg_buckets<<<unsigned((K + 255) / 256), 256, 0, s>>>(off.get(), K, nbuck, seg_at.get());
+            FB_LAUNCH_CHECK();
+            const int64_t ntiles = (w1 - w0 + kTR - 1) / kTR * ((ncols + kTC - 1) / kTC);
+            require(ntiles < (int64_t(1) << 31), "gaussian_matrix: window too large");
+            k_place_rm<<<unsigned(ntiles), 256, 0, s>>>(st, J, off.get(), seg_at.get(), K, 0, count, period, w0, w1, ncols, out);
+        } else {
+            k_place<<<unsigned(K), 256, 0, s>>>(st, J, off.get(), cnt.get(), 0, 0, count, win, out);
+        }
+        FB_LAUNCH_CHECK();
+        break;
     }
 }
 

@@ -145,7 +145,8 @@ def test_group_rejects_nccl_on_one_device(fb):
 
 
 @pytest.mark.parametrize("rows,cols,r0,r1", [(1000, 7, 0, 1000), (1000, 7, 250, 600), (5000, 40, 4999, 5000),
-                                             (3, 100000, 1, 2), (20000, 12, 0, 1)])
+                                             (3, 100000, 1, 2), (20000, 12, 0, 1), (300000, 40, 0, 300000),
+                                             (300000, 41, 12345, 200001)])
 def test_sketch_window_is_the_stream_slice(fb, ctx, rows, cols, r0, r1):
     """A rank's slice of the sketch (rows [r0, r1) of a column-major rows x
     cols Omega, or a contiguous run) is bitwise the corresponding part of the
@@ -158,6 +159,10 @@ def test_sketch_window_is_the_stream_slice(fb, ctx, rows, cols, r0, r1):
     win = np.empty((r1 - r0) * cols)
     _lib.check(L.frpca_gaussian_window(ctx._h, rows * cols, rows, r0, r1, seed, win.ctypes.data))
     assert np.array_equal(win.reshape(cols, r1 - r0).T, full[r0:r1])
+    # the same rows, row-major (the layout the products read; rng.cu k_place_rm)
+    rm = np.full((r1 - r0) * cols, np.nan)
+    _lib.check(L.frpca_gaussian_window_rows(ctx._h, (cols - 1) * rows + r1, rows, r0, r1, seed, rm.ctypes.data))
+    assert np.array_equal(rm.reshape(r1 - r0, cols), full[r0:r1])
     # a contiguous run of columns [1, cols - 1), generated only up to its end
     run = np.empty((cols - 2) * rows) if cols > 2 else None
     if run is not None:
