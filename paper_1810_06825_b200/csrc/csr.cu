@@ -54,10 +54,22 @@ __global__ void k_check_cols(const int64_t* __restrict__ rp, const int32_t* __re
     }
 }
 
-__global__ void k_iota(int32_t* __restrict__ x, int64_t n) {
+// sort payload of nonzero i: (row id << 32) | i
+__global__ void k_pack_rows(const int32_t* __restrict__ rowid, int64_t n, uint64_t* __restrict__ pay) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
-        x[i] = int32_t(i);
+        pay[i] = (uint64_t(uint32_t(rowid[i])) << 32) | uint64_t(uint32_t(i));
+}
+
+// sorted payload -> A^T's column ids (the row ids) and the permutation
+__global__ void k_unpack_rows(const uint64_t* __restrict__ pay, int64_t n, int32_t* __restrict__ tcol,
+                              int32_t* __restrict__ perm) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t v = pay[k];
+        tcol[k] = int32_t(v >> 32);
+        perm[k] = int32_t(uint32_t(v));
+    }
 }
 
 // Transposed entries from the stable column sort: entry k of A^T is original
@@ -315,21 +327,25 @@ void transpose_structure(Ctx& c, const DCsr& A, DCsr& T, const int32_t* rowid, D
         FB_CUDA(cudaMemsetAsync(T.rowptr.get(), 0, T.rowptr.bytes(), s));
         return;
     }
+    // the sort carries (row id << 32 | nonzero index): A^T's column ids come
+    // out of the sort directly, no random gather of the row ids
     std::unique_ptr<Prof> pt(new Prof(c, "upload_t_sort", 0, 0));
-    DBuf<int32_t> keys_out(size_t(nnz), s), perm_in(size_t(nnz), s);
-    perm_out.alloc(size_t(nnz), s);
-    k_iota<<<grid_for(c, nnz), 256, 0, s>>>(perm_in.get(), nnz);
+    DBuf<int32_t> keys_out(size_t(nnz), s);
+    DBuf<uint64_t> pay_in(size_t(nnz), s), pay_out(size_t(nnz), s);
+    k_pack_rows<<<grid_for(c, nnz), 256, 0, s>>>(rowid, nnz, pay_in.get());
     FB_LAUNCH_CHECK();
     int end_bit = 1;
     while (end_bit < 31 && (int64_t(1) << end_bit) <= cols) ++end_bit;
     size_t tb = 0;
-    FB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, A.col.get(), keys_out.get(), perm_in.get(),
-                                            perm_out.get(), nnz, 0, end_bit, s));
+    FB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, A.col.get(), keys_out.get(), pay_in.get(),
+                                            pay_out.get(), nnz, 0, end_bit, s));
     DBuf<unsigned char> tmp(tb, s);
-    FB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, A.col.get(), keys_out.get(), perm_in.get(),
-                                            perm_out.get(), nnz, 0, end_bit, s));
-    pt.reset(new Prof(c, "upload_t_gather", 0, 0));
-    k_gather_perm<int32_t><<<grid_for(c, (nnz + 7) / 8), 256, 0, s>>>(perm_out.get(), rowid, nnz, T.col.get());
+    FB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, A.col.get(), keys_out.get(), pay_in.get(),
+                                            pay_out.get(), nnz, 0, end_bit, s));
+    pay_in.release();
+    pt.reset(new Prof(c, "upload_t_unpack", 0, 0));
+    perm_out.alloc(size_t(nnz), s);
+    k_unpack_rows<<<grid_for(c, nnz), 256, 0, s>>>(pay_out.get(), nnz, T.col.get(), perm_out.get());
     FB_LAUNCH_CHECK();
     k_rowptr_from_sorted<<<grid_for(c, cols + 1), 256, 0, s>>>(keys_out.get(), nnz, cols, T.rowptr.get());
     FB_LAUNCH_CHECK();
