@@ -291,18 +291,18 @@ int frpca_ctx_destroy(frpca_ctx* c) {
         for (auto& b : c->slots) b.release();
         if (c->side) {
             for (auto& b : c->side->slots) b.release();
-            c->side->omega_raw.release();
+            c->side->omega_stage.release();
             c->side->dflag.release();
             cudaStreamSynchronize(c->side->stream);
             cudaStreamDestroy(c->side->stream);
             c->side.reset();
         }
+        c->omega_stage.release();  // stream-ordered frees before the stream goes
         if (c->tside) {
             cudaStreamSynchronize(c->tside->stream);
             cudaStreamDestroy(c->tside->stream);
             c->tside.reset();
         }
-        c->omega_raw.release();  // stream-ordered frees before the stream goes
         c->dflag.release();
         c->wcount.release();
         if (c->copy) {

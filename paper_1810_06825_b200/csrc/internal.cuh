@@ -145,7 +145,7 @@ struct Ctx {
     bool force_cusolver = false;  // re-run after the small eigensolver did not converge
     bool omega_sync = false;      // Omega batches checked on the host (re-run after a shortfall; side stream)
     bool checked = false;         // inside with_checks: deferred errors will be read
-    DBuf<uint64_t> omega_raw;  // raw-word buffer of the Omega generator, kept (grown on demand)
+    DBuf<double> omega_stage;  // normals staging of the Omega generator, kept (grown on demand)
     std::unique_ptr<Ctx> side;  // second stream for work overlapped with the upload (frpca_run_csr)
     std::unique_ptr<Ctx> tside;  // builder of A^T beside the first A*X (pipelined upload)
     cudaStream_t copy = nullptr;  // device->host copies of results overlapped with the output GEMMs

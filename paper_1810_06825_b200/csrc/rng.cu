@@ -171,7 +171,7 @@ k_gen_polar(const uint64_t* __restrict__ states, int64_t seg0, int64_t steps, in
     const int tid = threadIdx.x;
     const int64_t seg = seg0 + blockIdx.x;
     for (int i = tid; i < NN; i += GT) X[i] = states[seg * NN + i];
-    double* out = stage + seg * J;
+    double* out = stage + int64_t(blockIdx.x) * J;  // the batch's staging starts at segment seg0
     int64_t pairs = 0;  // accepted attempts so far (block-uniform)
     for (int64_t r = 0; r < steps; r += 4) {
         __syncthreads();  // (the previous round's ring reads are done)
@@ -229,13 +229,13 @@ struct Window {
 // stream positions (positions in [plo, phi) only)
 __global__ void __launch_bounds__(256)
 k_place(const double* __restrict__ stage, int64_t J, const int64_t* __restrict__ off,
-        const int64_t* __restrict__ cnt, int64_t s0, int64_t plo, int64_t phi, Window w, double* __restrict__ out) {
+        const int64_t* __restrict__ cnt, int64_t s0, int64_t count, Window w, double* __restrict__ out) {
     const int64_t seg = s0 + blockIdx.x;
     const int64_t base = off[seg], n = cnt[seg];
-    const double* src = stage + seg * J;
+    const double* src = stage + int64_t(blockIdx.x) * J;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const int64_t p = base + i;
-        if (p < plo || p >= phi) continue;
+        if (p >= count) break;
         const double v = __ldcs(src + i);
         if (w.ident) {
             __stcs(out + p, v);
@@ -250,9 +250,9 @@ k_place(const double* __restrict__ stage, int64_t J, const int64_t* __restrict__
 // stream position b * kBucket (segments hold thousands of normals, so a
 // position's segment is seg_at[p / kBucket] or one of the next few).
 constexpr int64_t kBucket = 1024;
-__global__ void k_seg_buckets(const int64_t* __restrict__ off, int64_t nseg, int64_t nbuck,
+__global__ void k_seg_buckets(const int64_t* __restrict__ off, int64_t s0, int64_t s1, int64_t nbuck,
                               int32_t* __restrict__ seg_at) {
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nseg; k += int64_t(gridDim.x) * blockDim.x) {
+    for (int64_t k = s0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < s1; k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t b0 = (off[k] + kBucket - 1) / kBucket;
         const int64_t b1 = min(nbuck, (off[k + 1] + kBucket - 1) / kBucket);
         for (int64_t b = b0; b < b1; ++b) seg_at[b] = int32_t(k);
@@ -274,14 +274,21 @@ __device__ __forceinline__ int64_t seg_of(const int64_t* __restrict__ off, const
 constexpr int kTR = 128, kTC = 32;
 __global__ void __launch_bounds__(256)
 k_place_rm(const double* __restrict__ stage, int64_t J, const int64_t* __restrict__ off,
-           const int32_t* __restrict__ seg_at, int64_t nseg, int64_t plo, int64_t phi, int64_t P, int64_t w0,
-           int64_t w1, int64_t ncols, double* __restrict__ out) {
+           const int32_t* __restrict__ seg_at, int64_t s0, int64_t s1, int64_t count, int64_t P, int64_t w0,
+           int64_t w1, int64_t ncols, int64_t ncb_launch, double* __restrict__ out) {
     __shared__ double tile[kTC][kTR + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // column blocks vary fastest across CTAs, so the CTAs in flight complete
     // whole output rows (full lines merge in L2 before they reach DRAM)
+    // this batch's stream positions: segments [s0, s1); its columns start at
+    // block plo / P / kTC, and ncb_launch column blocks cover any batch
+    const int64_t plo = off[s0], phi = min(off[s1], count);
     const int64_t ncb = (ncols + kTC - 1) / kTC;
-    const int64_t r0 = w0 + int64_t(blockIdx.x / ncb) * kTR, q0 = int64_t(blockIdx.x % ncb) * kTC;
+    const int64_t cb = (plo / P) / kTC + int64_t(blockIdx.x % ncb_launch);
+    if (cb >= ncb) return;
+    const int64_t r0 = w0 + int64_t(blockIdx.x / ncb_launch) * kTR, q0 = cb * kTC;
+    const int64_t qlast = min(q0 + kTC, ncols) - 1;
+    if (q0 * P + r0 >= phi || qlast * P + min(r0 + kTR, w1) - 1 < plo) return;  // tile outside the batch
     double v[kTC / 8][kTR / 32];
 #pragma unroll
     for (int j = 0; j < kTC / 8; ++j) {
@@ -292,8 +299,8 @@ k_place_rm(const double* __restrict__ stage, int64_t J, const int64_t* __restric
             const int64_t p = q * P + r0 + rr;
             v[j][h] = 0.0;
             if (q < ncols && r0 + rr < w1 && p >= plo && p < phi) {
-                const int64_t k = seg_of(off, seg_at, nseg, p);
-                v[j][h] = __ldcs(stage + k * J + (p - off[k]));
+                const int64_t k = seg_of(off, seg_at, s1, p);
+                v[j][h] = __ldcs(stage + (k - s0) * J + (p - off[k]));
             }
         }
     }
@@ -405,54 +412,81 @@ void gaussian_stream_window(Ctx& c, uint64_t seed, int64_t count, int64_t period
         FB_CUDA(cudaMemcpyAsync(states.get(), s0, sizeof(s0), cudaMemcpyHostToDevice, s));
         jump_states(c, states.get(), polys, groups, 1, K);
     }
+    // Staging: J normals per segment at most, kept on the context (Ctx::
+    // omega_stage: re-taking a 41 GB block per call stalls on pool re-maps)
+    // and grown only while 24 GB of device memory stay free; beyond that the
+    // segments go in batches. One batch is faster for the row-major placement
+    // (the CTAs in flight complete whole output rows; a batch covers only
+    // some columns): C4 16.7 ms vs 24.4 ms in 5 batches.
+    DBuf<double>& stage = c.omega_stage;
+    {
+        const size_t need = sizeof(double) * size_t(K) * size_t(J);
+        if (stage.bytes() < need) {
+            size_t fr = 0, tot = 0;
+            FB_CUDA(cudaMemGetInfo(&fr, &tot));
+            const size_t head = size_t(24) << 30, have = stage.bytes();
+            const size_t room = fr + have > head ? fr + have - head : 0;
+            const size_t want = std::min(need, std::max(room, size_t(2) << 30));
+            if (want > have) {
+                stage.release();
+                stage.alloc(std::max<size_t>(J, want / sizeof(double)), s);
+            }
+        }
+    }
+    const int64_t spb = std::max<int64_t>(1, int64_t(stage.n / size_t(J)));
+    const int64_t nbuck = (count + kBucket - 1) / kBucket;
     for (int attempt_no = 0;; ++attempt_no) {
-        // staging: J normals per segment at most (every attempt accepted)
-        DBuf<uint64_t>& stage = c.omega_raw;  // kept on the context
-        if (stage.n < size_t(K * J)) stage.alloc(size_t(K * J), s);
-        double* st = reinterpret_cast<double*>(stage.get());
         DBuf<int64_t> cnt(size_t(K) + 1, s), off(size_t(K) + 1, s);
-        {
-            Prof pg(c, "omega_gen", 8.0 * double(count), 0.0);
-            FB_CUDA(cudaMemsetAsync(cnt.get() + K, 0, sizeof(int64_t), s));
-            k_gen_polar<<<unsigned(K), GT, 0, s>>>(states.get(), 0, steps, J, st, cnt.get());
+        FB_CUDA(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+        DBuf<int32_t> seg_at;
+        if (rowmajor) {
+            seg_at.alloc(size_t(nbuck), s);
+            FB_CUDA(cudaMemsetAsync(seg_at.get(), 0, seg_at.bytes(), s));  // (a deferred shortfall leaves a tail)
+        }
+        size_t tb = 0;
+        FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), off.get(), K + 1, s));
+        DBuf<unsigned char> tmp(tb, s);
+        for (int64_t s0 = 0; s0 < K; s0 += spb) {
+            const int64_t s1 = std::min(K, s0 + spb);
+            {
+                Prof pg(c, "omega_gen", 8.0 * double(count) * double(s1 - s0) / double(K), 0.0);
+                k_gen_polar<<<unsigned(s1 - s0), GT, 0, s>>>(states.get(), s0, steps, J, stage.get(), cnt.get());
+                FB_LAUNCH_CHECK();
+                // offsets of segments [0, s1] (cnt past s1 is still 0)
+                FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), off.get(), s1 + 1, s));
+            }
+            Prof pe(c, "omega_place", 16.0 * double(count) * double(w1 - w0) / double(period) * double(s1 - s0) / double(K),
+                    0.0);
+            if (rowmajor) {
+                k_seg_buckets<<<unsigned((s1 - s0 + 255) / 256), 256, 0, s>>>(off.get(), s0, s1, nbuck, seg_at.get());
+                FB_LAUNCH_CHECK();
+                // a batch holds at most (s1 - s0) J normals: the column blocks it can touch
+                const int64_t ncb = (ncols + kTC - 1) / kTC;
+                const int64_t ncb_launch = K <= spb ? ncb : std::min(ncb, ((s1 - s0) * J / period + 1) / kTC + 2);
+                const int64_t ntiles = (w1 - w0 + kTR - 1) / kTR * ncb_launch;
+                require(ntiles < (int64_t(1) << 31), "gaussian_matrix: window too large");
+                k_place_rm<<<unsigned(ntiles), 256, 0, s>>>(stage.get(), J, off.get(), seg_at.get(), s0, s1, count,
+                                                            period, w0, w1, ncols, ncb_launch, out);
+            } else {
+                k_place<<<unsigned(s1 - s0), 256, 0, s>>>(stage.get(), J, off.get(), cnt.get(), s0, count, win, out);
+            }
             FB_LAUNCH_CHECK();
-            size_t tb = 0;
-            FB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), off.get(), K + 1, s));
-            DBuf<unsigned char> tmp(tb, s);
-            FB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), off.get(), K + 1, s));
         }
         // FRPCA_TEST_OMEGA_SHORT: tests force the shortfall -> re-run path
         const bool force = std::getenv("FRPCA_TEST_OMEGA_SHORT") != nullptr;
         if (defer) {
             k_check_short<<<1, 1, 0, s>>>(off.get() + K, force ? INT64_MAX : count, err_flag(c));
             FB_LAUNCH_CHECK();
-        } else {
-            int64_t total = 0;
-            FB_CUDA(cudaMemcpyAsync(&total, off.get() + K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-            FB_CUDA(cudaStreamSynchronize(s));
-            if (total < count || (force && attempt_no == 0)) {
-                // shortfall: the whole stream again over the longer jump table
-                require(K < Kmax, "gaussian_matrix: device stream generation did not converge");
-                jump_states(c, states.get(), polys, groups, K, Kmax);
-                K = Kmax;
-                continue;
-            }
+            break;
         }
-        Prof pe(c, "omega_place", 8.0 * double(count) * double(w1 - w0) / double(period) * 2.0, 0.0);
-        if (rowmajor) {
-            const int64_t nbuck = (count + kBucket - 1) / kBucket;
-            DBuf<int32_t> seg_at(size_t(nbuck), s);
-            FB_CUDA(cudaMemsetAsync(seg_at.get(), 0, seg_at.bytes(), s));  // (a deferred shortfall leaves a tail)
-            k_seg_buckets<<<unsigned((K + 255) / 256), 256, 0, s>>>(off.get(), K, nbuck, seg_at.get());
-            FB_LAUNCH_CHECK();
-            const int64_t ntiles = (w1 - w0 + kTR - 1) / kTR * ((ncols + kTC - 1) / kTC);
-            require(ntiles < (int64_t(1) << 31), "gaussian_matrix: window too large");
-            k_place_rm<<<unsigned(ntiles), 256, 0, s>>>(st, J, off.get(), seg_at.get(), K, 0, count, period, w0, w1, ncols, out);
-        } else {
-            k_place<<<unsigned(K), 256, 0, s>>>(st, J, off.get(), cnt.get(), 0, 0, count, win, out);
-        }
-        FB_LAUNCH_CHECK();
-        break;
+        int64_t total = 0;
+        FB_CUDA(cudaMemcpyAsync(&total, off.get() + K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        FB_CUDA(cudaStreamSynchronize(s));
+        if (total >= count && !(force && attempt_no == 0)) break;
+        // shortfall: the whole stream again over the longer jump table
+        require(K < Kmax, "gaussian_matrix: device stream generation did not converge");
+        jump_states(c, states.get(), polys, groups, K, Kmax);
+        K = Kmax;
     }
 }
 
