@@ -1,3 +1,4 @@
+#include <chrono>
 // extern "C" boundary (include/frpca_b200.h). Exceptions never cross it:
 // each entry point maps fb::InvalidArgument -> 2, fb::NumericalError -> 4,
 // CUDA/NCCL/cuSOLVER failures -> 5 and keeps the message for
@@ -668,6 +669,16 @@ int frpca_run(frpca_ctx* c, frpca_dmat* M, int algorithm, const frpca_config* cf
 // One-shot run from a host CSR: upload + run + release, with the sketch (which
 // depends only on the seed and the shape) generated on a second stream by a
 // second host thread while the CSR is uploaded and the device transpose built.
+// FRPCA_DEBUG_E2E: host timestamps of frpca_run_csr's phases (diagnostic)
+static void dbg_mark(const char* what, bool start = false) {
+    static const bool on = std::getenv("FRPCA_DEBUG_E2E") != nullptr;
+    if (!on) return;
+    static thread_local std::chrono::steady_clock::time_point t0;
+    const auto now = std::chrono::steady_clock::now();
+    if (start) t0 = now;
+    std::fprintf(stderr, "[e2e] %8.2f ms %s\n", std::chrono::duration<double, std::milli>(now - t0).count(), what);
+}
+
 int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
                   const int64_t* col_idx, const double* values, int algorithm, const frpca_config* cfg,
                   const double* omega, int64_t omega_rows, int64_t omega_cols, double* U, double* S, double* V,
@@ -677,6 +688,7 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
         require(cfg != nullptr, "frpca_run: null argument");
         std::lock_guard<std::mutex> lk(c->mu);
         FB_CUDA(cudaSetDevice(c->device));
+        dbg_mark("start", true);
         int algo = algorithm;
         if (algo == FRPCA_ALGO_AUTO) algo = (rows < cols) ? FRPCA_ALGO_FRPCA : FRPCA_ALGO_FRPCAT;
         // shape of the sketch each algorithm draws (randsvd.hpp:110, :150, :239, :291)
@@ -748,7 +760,9 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
             if (side_thread.joinable()) side_thread.join();
             throw;
         }
+        dbg_mark("upload returned");
         if (side_thread.joinable()) side_thread.join();
+        dbg_mark("side joined");
         if (side_err) std::rethrow_exception(side_err);
         RunArgs a;
         a.cfg = *cfg;
@@ -764,7 +778,9 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
                     algo == FRPCA_ALGO_BASIC_RPCAT,
                 "frpca_run: unknown algorithm");
         run_algorithm(*c, *M, a, stats, algo);
+        dbg_mark("run returned");
         FB_CUDA(cudaStreamSynchronize(c->stream));
+        dbg_mark("synced");
     });
 }
 

@@ -52,8 +52,9 @@ void count_launch();
 // least kCacheMin bytes is parked with an event recorded on its last stream;
 // a later request of the same device takes the smallest parked buffer that
 // fits within 1/8 slack, after making its stream wait on that event (the
-// ordering the pool itself would provide). Parked buffers are freed when an
-// allocation fails (then retried) and beyond kCacheMax bytes.
+// ordering the pool itself would provide). Parked buffers go back to the
+// pool when an allocation fails (then retried), beyond kCacheMax bytes, or
+// when the device has less than kMinFree bytes free.
 struct BufCache {
     struct Entry {
         void* p;
@@ -62,7 +63,7 @@ struct BufCache {
         cudaEvent_t ev;
     };
     static constexpr size_t kCacheMin = size_t(32) << 20;
-    static constexpr size_t kCacheMax = size_t(48) << 30;
+    static constexpr size_t kCacheMax = size_t(128) << 30;
     static constexpr size_t kMinFree = size_t(20) << 30;  // device headroom kept for other allocators
     std::mutex mu;
     std::vector<Entry> parked;
@@ -71,10 +72,11 @@ struct BufCache {
         static BufCache* c = new BufCache;  // never destroyed (process exit order)
         return *c;
     }
+    // back to the stream-ordered pool (no unmap: the pool keeps its memory)
     static void drop(Entry& e) {
         cudaEventSynchronize(e.ev);
         cudaEventDestroy(e.ev);
-        cudaFree(e.p);
+        cudaFreeAsync(e.p, cudaStreamPerThread);
     }
     // a parked buffer of [bytes, bytes + bytes/8] on this device, or nullptr
     void* take(size_t bytes, cudaStream_t s, size_t& cap) {
@@ -123,6 +125,7 @@ struct BufCache {
         for (auto& e : parked) drop(e);
         parked.clear();
         held = 0;
+        cudaStreamSynchronize(cudaStreamPerThread);  // the pool can hand the memory out again
     }
 };
 

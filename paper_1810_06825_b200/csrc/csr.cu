@@ -4,7 +4,9 @@
 // load-balanced SpMM work lists of both.
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -191,6 +193,26 @@ __global__ void k_item_write(const int64_t* __restrict__ rp, int64_t m, int64_t 
     }
 }
 
+// n elements of d into the context's mapped host words (read_scalar)
+template <class T>
+__global__ void k_put(const T* __restrict__ src, int n, T* __restrict__ dst) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+uint64_t* mapped_slots(Ctx& c, int n) {
+    constexpr int kSlots = 64;
+    if (n > kSlots) throw CudaError("mapped_slots: too many words");
+    if (!c.mapped.h) {
+        void* h = nullptr;
+        FB_CUDA(cudaHostAlloc(&h, sizeof(uint64_t) * kSlots, cudaHostAllocMapped));
+        c.mapped.h = static_cast<uint64_t*>(h);
+        void* d = nullptr;
+        FB_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+        c.mapped.d = static_cast<uint64_t*>(d);
+    }
+    return c.mapped.h;
+}
+
 int grid_for(const Ctx& c, int64_t n, int threads = 256) {
     const int64_t want = (n + threads - 1) / threads;
     const int64_t cap = int64_t(c.num_sms) * 32;
@@ -199,9 +221,13 @@ int grid_for(const Ctx& c, int64_t n, int threads = 256) {
 
 template <class T>
 T read_scalar(Ctx& c, const T* d) {
-    T h;
-    FB_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+    static_assert(sizeof(T) <= sizeof(uint64_t), "scalar read-back");
+    uint64_t* slot = mapped_slots(c, 1);
+    k_put<T><<<1, 32, 0, c.stream>>>(d, 1, reinterpret_cast<T*>(c.mapped.d));
+    FB_LAUNCH_CHECK();
     FB_CUDA(cudaStreamSynchronize(c.stream));
+    T h;
+    std::memcpy(&h, slot, sizeof(T));
     return h;
 }
 
@@ -240,9 +266,12 @@ void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_
         DBuf<int64_t> cv(3 * kCuts, c.stream);
         k_item_cuts<<<1, 32, 0, c.stream>>>(m, oi, oc, cv.get());
         FB_LAUNCH_CHECK();
-        int64_t h[3 * kCuts];
-        FB_CUDA(cudaMemcpyAsync(h, cv.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+        uint64_t* slots = mapped_slots(c, 3 * kCuts);
+        k_put<int64_t><<<1, 32, 0, c.stream>>>(cv.get(), 3 * kCuts, reinterpret_cast<int64_t*>(c.mapped.d));
+        FB_LAUNCH_CHECK();
         FB_CUDA(cudaStreamSynchronize(c.stream));
+        int64_t h[3 * kCuts];
+        std::memcpy(h, slots, sizeof(h));
         for (int k = 1; k < kCuts; ++k)
             if (h[3 * k] > L.cut_row.back()) {  // (rows only: the same cuts on every rank)
                 L.cut_row.push_back(h[3 * k]);
@@ -358,7 +387,11 @@ Ctx& builder_ctx(Ctx& c) {
         auto b = std::make_unique<Ctx>();
         b->device = c.device;
         b->num_sms = c.num_sms;
-        FB_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+        // highest priority: its short kernels go ahead of the first A*X's
+        // blocks, so the join at the first A^T*Y does not wait on them
+        int lo = 0, hi = 0;
+        FB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FB_CUDA(cudaStreamCreateWithPriority(&b->stream, cudaStreamNonBlocking, hi));
         c.tside = std::move(b);
     }
     return *c.tside;
@@ -380,7 +413,12 @@ constexpr int kValChunks = 8;
 void PendingValues::join() {
     if (joined) return;
     joined = true;
+    static const bool dbg = std::getenv("FRPCA_DEBUG_E2E") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     if (builder.joinable()) builder.join();
+    if (dbg)
+        std::fprintf(stderr, "[e2e] builder join waited %.2f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     if (a && rank_of.n) {
         a->rank_of = std::move(rank_of);
         a->rank_ids = std::move(rank_ids);
@@ -942,5 +980,7 @@ void download_csr(Ctx& c, const DCsr& A, int64_t* rp, int64_t* ci, double* v) {
         ci[i] = (e & kColHot) ? ids[size_t(e & kRankMask)] : (e & kColMask);
     }
 }
+
+int64_t read_i64(Ctx& c, const int64_t* d) { return read_scalar(c, d); }
 
 }  // namespace fb

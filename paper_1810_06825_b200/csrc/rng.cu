@@ -479,9 +479,7 @@ void gaussian_stream_window(Ctx& c, uint64_t seed, int64_t count, int64_t period
             FB_LAUNCH_CHECK();
             break;
         }
-        int64_t total = 0;
-        FB_CUDA(cudaMemcpyAsync(&total, off.get() + K, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        FB_CUDA(cudaStreamSynchronize(s));
+        const int64_t total = read_i64(c, off.get() + K);
         if (total >= count && !(force && attempt_no == 0)) break;
         // shortfall: the whole stream again over the longer jump table
         require(K < Kmax, "gaussian_matrix: device stream generation did not converge");

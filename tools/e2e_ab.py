@@ -59,12 +59,34 @@ def unsetenv(v):
 
 times = {v: [] for v in variants}
 S0 = None
+per_call = os.environ.get("E2E_PER_CALL_PROFILE") == "1"
+
+
+def profile_rows():
+    cnt = C.c_int()
+    _lib.check(L.frpca_profile_count(ctx._h, C.byref(cnt)))
+    rows = {}
+    for i in range(cnt.value):
+        nm = C.c_char_p(); la = C.c_int64(); ms = C.c_double(); by = C.c_double(); fl = C.c_double()
+        _lib.check(L.frpca_profile_get(ctx._h, i, C.byref(nm), C.byref(la), C.byref(ms), C.byref(by), C.byref(fl)))
+        rows[nm.value.decode()] = round(ms.value, 1)
+    return rows
+
+
 for r in range(reps + 1):
     for v in variants:
         setenv(v)
+        if per_call:
+            _lib.check(L.frpca_profile_reset(ctx._h))
+            _lib.check(L.frpca_profile_enable(ctx._h, 1))
         t0 = time.perf_counter()
         run_csr()
         t = (time.perf_counter() - t0) * 1e3
+        if per_call:
+            _lib.check(L.frpca_profile_enable(ctx._h, 0))
+            rows = profile_rows()
+            top = dict(sorted(rows.items(), key=lambda x: -x[1])[:8])
+            print(f"  profile {v} call {r}: {top}", file=sys.stderr, flush=True)
         S = np.ctypeslib.as_array(C.cast(pS, C.POINTER(C.c_double)), shape=(k,)).copy()
         if S0 is None:
             S0 = S
