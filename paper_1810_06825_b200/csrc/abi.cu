@@ -689,6 +689,7 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
         std::lock_guard<std::mutex> lk(c->mu);
         FB_CUDA(cudaSetDevice(c->device));
         dbg_mark("start", true);
+        const size_t p0 = c->pending.size();
         int algo = algorithm;
         if (algo == FRPCA_ALGO_AUTO) algo = (rows < cols) ? FRPCA_ALGO_FRPCA : FRPCA_ALGO_FRPCAT;
         // shape of the sketch each algorithm draws (randsvd.hpp:110, :150, :239, :291)
@@ -781,6 +782,26 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
         dbg_mark("run returned");
         FB_CUDA(cudaStreamSynchronize(c->stream));
         dbg_mark("synced");
+        // FRPCA_DEBUG_TIMELINE (with profiling on): the call's event brackets on
+        // the main stream, start / end relative to the first one (diagnostic)
+        static const bool tl = std::getenv("FRPCA_DEBUG_TIMELINE") != nullptr;
+        if (tl && c->prof && c->pending.size() > p0) {
+            const cudaEvent_t base = c->pending[p0].a;
+            for (size_t i = p0; i < c->pending.size(); ++i) {
+                float t0 = 0.f, t1 = 0.f;
+                cudaEventElapsedTime(&t0, base, c->pending[i].a);
+                cudaEventElapsedTime(&t1, base, c->pending[i].b);
+                std::fprintf(stderr, "[timeline] %9.2f %9.2f %s\n", t0, t1, c->pending[i].name.c_str());
+            }
+            if (c->tside)
+                for (size_t i = c->tside->tl_mark; i < c->tside->pending.size(); ++i) {
+                    float t0 = 0.f, t1 = 0.f;
+                    cudaEventElapsedTime(&t0, base, c->tside->pending[i].a);
+                    cudaEventElapsedTime(&t1, base, c->tside->pending[i].b);
+                    std::fprintf(stderr, "[timeline] %9.2f %9.2f   builder: %s\n", t0, t1,
+                                 c->tside->pending[i].name.c_str());
+                }
+        }
     });
 }
 

@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -164,7 +166,13 @@ struct DBuf {
             }
         }
         cap = bytes;
+        static const bool dbg = std::getenv("FRPCA_DEBUG_E2E") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, stream);
+        if (dbg) {
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (ms > 2.0) std::fprintf(stderr, "[e2e] cudaMallocAsync %.1f MB took %.1f ms\n", bytes / 1e6, ms);
+        }
         if (e == cudaErrorMemoryAllocation) {
             cudaGetLastError();
             BufCache::get().flush();

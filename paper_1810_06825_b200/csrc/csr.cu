@@ -222,10 +222,19 @@ int grid_for(const Ctx& c, int64_t n, int threads = 256) {
 template <class T>
 T read_scalar(Ctx& c, const T* d) {
     static_assert(sizeof(T) <= sizeof(uint64_t), "scalar read-back");
+    static const bool dbg = std::getenv("FRPCA_DEBUG_E2E") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     uint64_t* slot = mapped_slots(c, 1);
     k_put<T><<<1, 32, 0, c.stream>>>(d, 1, reinterpret_cast<T*>(c.mapped.d));
     FB_LAUNCH_CHECK();
+    const auto t1 = std::chrono::steady_clock::now();
     FB_CUDA(cudaStreamSynchronize(c.stream));
+    if (dbg) {
+        const auto t2 = std::chrono::steady_clock::now();
+        const double a = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        const double b = std::chrono::duration<double, std::milli>(t2 - t1).count();
+        if (a + b > 5.0) std::fprintf(stderr, "[e2e] read_scalar: launch %.2f ms, sync %.2f ms\n", a, b);
+    }
     T h;
     std::memcpy(&h, slot, sizeof(T));
     return h;
@@ -547,11 +556,17 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
     T.col.alloc(size_t(nnz), s);
     T.val.alloc(size_t(nnz), s);
     if (nnz && pv) {
-        // Pipelined: A's work list now, so the first A*X can start on the
-        // value chunks as they land; the structure of A^T, the column ranks,
-        // A^T's work list and panel plan and the gather of A^T's values are
-        // built beside it by the builder thread on its own stream, joined by
-        // the first A^T*Y (consume_pending).
+        // Pipelined: A^T's structure (the radix sort) and A's work list now,
+        // while the values cross PCIe; the first A*X then starts on the value
+        // chunks as they land. The column ranks, A^T's work list and panel
+        // plan and the gather of A^T's values are built beside it by the
+        // builder thread on its own stream, joined by the first A^T*Y
+        // (consume_pending). (With the sort on the builder, its kernels
+        // waited for the persistent A*X blocks of each chunk to drain: sort
+        // 10 -> 32 ms, first A*X done at 169 instead of ~125 ms at C3.)
+        ph.reset(new Prof(c, "upload_transpose", 0, 0));
+        transpose_structure(c, A, T, rowid.get(), pv->perm);
+        rowid.release();
         ph.reset(new Prof(c, "upload_items", 0, 0));
         build_items(c, A, nullptr, A.L, default_chunk(c, A));
         const int64_t V = (nnz + kValChunks - 1) / kValChunks;
@@ -561,12 +576,13 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
         }
         ph.reset();
         Ctx& b = builder_ctx(c);
+        b.prof = c.prof;  // (its brackets join the call's timeline, FRPCA_DEBUG_TIMELINE)
+        b.tl_mark = b.pending.size();
         cudaEvent_t ev_ready;
         FB_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
         FB_CUDA(cudaEventRecord(ev_ready, s));
         FB_CUDA(cudaEventCreateWithFlags(&pv->all, cudaEventDisableTiming));
         pv->a = &A;
-        pv->rowid = std::move(rowid);
         PendingValues* P = pv.get();
         const cudaEvent_t last = pv->ev.back();
         P->builder = std::thread([&b, &A, &T, P, ev_ready, last, width_hint] {
@@ -574,9 +590,6 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
                 FB_CUDA(cudaSetDevice(b.device));
                 FB_CUDA(cudaStreamWaitEvent(b.stream, ev_ready, 0));
                 cudaEventDestroy(ev_ready);
-                DBuf<int32_t> perm;
-                transpose_structure(b, A, T, P->rowid.get(), perm);
-                P->rowid.release();
                 build_ranks(b, A.cols, T, P->rank_of, P->rank_ids);
                 build_items(b, T, nullptr, T.L, default_chunk(b, T));
                 if (width_hint > 0) {
@@ -584,8 +597,9 @@ void dcsr_upload_build(Ctx& c, DMat& M, int64_t rows, int64_t cols, int64_t nnz,
                     if (panel_rows_for(T, width_hint, pr, cap)) ensure_panels(b, T, pr, cap);
                 }
                 FB_CUDA(cudaStreamWaitEvent(b.stream, last, 0));
-                k_gather_perm<double><<<grid_for(b, (A.nnz + 7) / 8), 256, 0, b.stream>>>(perm.get(), A.val.get(),
+                k_gather_perm<double><<<grid_for(b, (A.nnz + 7) / 8), 256, 0, b.stream>>>(P->perm.get(), A.val.get(),
                                                                                         A.nnz, T.val.get());
+                P->perm.release();
                 FB_LAUNCH_CHECK();
             } catch (...) {
                 P->err = std::current_exception();

@@ -308,7 +308,10 @@ static void output_products(Ctx& c, const RunArgs& a, int64_t l, int64_t k, OutP
         FB_CUDA(cudaMemcpy2DAsync(big.user + r0, sizeof(double) * ldu, big.dev + r0, sizeof(double) * R,
                                   sizeof(double) * (r1 - r0), size_t(k), cudaMemcpyDeviceToHost, c.copy));
     }
-    fence(c.copy, S);  // the run's final synchronisation covers the copies
+    {
+        Prof pw(c, "out_d2h_tail", 0.0, 0.0);  // the copies still running after the last GEMM
+        fence(c.copy, S);  // the run's final synchronisation covers the copies
+    }
     FB_CUDA(cudaStreamSynchronize(S));
     for (auto ev : evs) cudaEventDestroy(ev);
 }

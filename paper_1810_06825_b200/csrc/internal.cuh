@@ -84,7 +84,7 @@ struct PendingValues {
     std::exception_ptr err;
     bool joined = false;
     DCsr* a = nullptr;                  // receives the ranks at the join
-    DBuf<int32_t> rowid;                // the builder's gather source
+    DBuf<int32_t> perm;                 // A^T entry k = nonzero perm[k] of A (the values gather)
     DBuf<int32_t> rank_of, rank_ids;    // A's column ranks, built by the builder
     PendingValues() = default;
     PendingValues(const PendingValues&) = delete;
@@ -193,6 +193,7 @@ struct Ctx {
 
     // profiling: events around each launch, folded into per-kernel aggregates
     bool prof = false;
+    size_t tl_mark = 0;  // first bracket of the current call (timeline diagnostics)
     struct Pending {
         std::string name;
         cudaEvent_t a, b;
