@@ -782,6 +782,8 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
         dbg_mark("run returned");
         FB_CUDA(cudaStreamSynchronize(c->stream));
         dbg_mark("synced");
+        M.reset();
+        dbg_mark("matrix released");
         // FRPCA_DEBUG_TIMELINE (with profiling on): the call's event brackets on
         // the main stream, start / end relative to the first one (diagnostic)
         static const bool tl = std::getenv("FRPCA_DEBUG_TIMELINE") != nullptr;

@@ -70,6 +70,7 @@ struct BufCache {
     std::mutex mu;
     std::vector<Entry> parked;
     size_t held = 0;
+    std::chrono::steady_clock::time_point last_check{};
     static BufCache& get() {
         static BufCache* c = new BufCache;  // never destroyed (process exit order)
         return *c;
@@ -102,6 +103,22 @@ struct BufCache {
         return e.p;
     }
     bool give(void* p, size_t bytes, cudaStream_t s) {
+        static const bool dbg = std::getenv("FRPCA_DEBUG_E2E") != nullptr;
+        const auto g0 = std::chrono::steady_clock::now();
+        struct Report {
+            bool on;
+            std::chrono::steady_clock::time_point t0;
+            size_t bytes;
+            int drops = 0;
+            bool checked = false;
+            ~Report() {
+                if (!on) return;
+                const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                if (ms > 2.0)
+                    std::fprintf(stderr, "[e2e] park %.1f MB took %.1f ms (mem check %d, drops %d)\n", bytes / 1e6, ms,
+                                 int(checked), drops);
+            }
+        } rep{dbg, g0, bytes};
         int dev = 0;
         cudaEvent_t ev;
         if (cudaGetDevice(&dev) != cudaSuccess) return false;
@@ -113,12 +130,21 @@ struct BufCache {
         std::lock_guard<std::mutex> lk(mu);
         parked.push_back({p, bytes, dev, ev});
         held += bytes;
-        size_t fr = 0, tot = 0;
-        const bool low = cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr < kMinFree;
+        // device headroom, checked at most every 2 s (cudaMemGetInfo stalled a
+        // release for ~40 ms now and then, measured inside frpca_run_csr)
+        bool low = false;
+        const auto now = std::chrono::steady_clock::now();
+        if (now - last_check > std::chrono::seconds(2)) {
+            last_check = now;
+            size_t fr = 0, tot = 0;
+            low = cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr < kMinFree;
+            rep.checked = true;
+        }
         while ((held > kCacheMax || (low && held > bytes)) && parked.size() > 1) {
             held -= parked.front().bytes;
             drop(parked.front());
             parked.erase(parked.begin());
+            ++rep.drops;
         }
         return true;
     }
