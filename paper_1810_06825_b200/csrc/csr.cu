@@ -400,7 +400,8 @@ Ctx& builder_ctx(Ctx& c) {
         // blocks, so the join at the first A^T*Y does not wait on them
         int lo = 0, hi = 0;
         FB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        FB_CUDA(cudaStreamCreateWithPriority(&b->stream, cudaStreamNonBlocking, hi));
+        const char* e = std::getenv("FRPCA_BUILDER_PRIO");  // A/B: "lo" = the default priority
+        FB_CUDA(cudaStreamCreateWithPriority(&b->stream, cudaStreamNonBlocking, (e && e[0] == 'l') ? lo : hi));
         c.tside = std::move(b);
     }
     return *c.tside;

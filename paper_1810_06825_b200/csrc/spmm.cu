@@ -791,10 +791,28 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
         ensure_hint(c, Am, ncols);
         DBuf<double> part;
         if (A.L.nslots) part.alloc(size_t(A.L.nslots) * ncols, c.stream);
+        // Item chunks alternate between the main and the aux stream (their
+        // own work counters; disjoint output rows and partial slots), so a
+        // chunk's blocks fill the SMs the previous chunk's tail frees (an
+        // item of a long row runs for milliseconds); the main stream joins.
+        if (!c.aux) {
+            FB_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
+            FB_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+            FB_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+        }
+        const cudaStream_t s0 = c.stream;
+        const bool alt = env_double("FRPCA_PIPE_ALT", 1.0) != 0.0;
+        FB_CUDA(cudaEventRecord(c.ev_fork, s0));
+        FB_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
         for (size_t k = 0; k + 1 < A.L.cut_row.size(); ++k) {
+            c.stream = (alt && (k & 1)) ? c.aux : s0;
             FB_CUDA(cudaStreamWaitEvent(c.stream, pv->ev[size_t(pv->need[k])], 0));
             spmm_list(c, A, Items(A.L, true, int(k)), nullptr, X, ldx, int(ncols), Y, ldy, part.get());
         }
+        c.stream = s0;
+        FB_CUDA(cudaEventRecord(c.ev_join, c.aux));
+        FB_CUDA(cudaStreamWaitEvent(s0, c.ev_join, 0));
+        part.s = s0;  // (freed behind the join)
         return;
     }
     consume_pending(c, Am);
