@@ -396,12 +396,14 @@ Ctx& builder_ctx(Ctx& c) {
         auto b = std::make_unique<Ctx>();
         b->device = c.device;
         b->num_sms = c.num_sms;
-        // highest priority: its short kernels go ahead of the first A*X's
-        // blocks, so the join at the first A^T*Y does not wait on them
+        // default (lowest) priority: the run's own kernels (the first A*X, the
+        // LU of an even-q frpca) go first and the builder fills the gaps
+        // (C4 e2e: the LU took 15.5 instead of 2.9 ms behind top-priority
+        // builder kernels); FRPCA_BUILDER_PRIO=hi for the A/B
         int lo = 0, hi = 0;
         FB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        const char* e = std::getenv("FRPCA_BUILDER_PRIO");  // A/B: "lo" = the default priority
-        FB_CUDA(cudaStreamCreateWithPriority(&b->stream, cudaStreamNonBlocking, (e && e[0] == 'l') ? lo : hi));
+        const char* e = std::getenv("FRPCA_BUILDER_PRIO");
+        FB_CUDA(cudaStreamCreateWithPriority(&b->stream, cudaStreamNonBlocking, (e && e[0] == 'h') ? hi : lo));
         c.tside = std::move(b);
     }
     return *c.tside;

@@ -945,12 +945,12 @@ struct ChunkReducer {
 }  // namespace
 
 void spmm_device_reduced(Ctx& c, const DCsr& A, const double* X, int64_t ncols, double* Y, const char* tag) {
-    consume_pending(c, const_cast<DCsr&>(A));
     if (c.world <= 1 || ncols > 256 || A.L.cut_row.size() < 2 || A.rows == 0) {
-        spmm_device(c, A, X, ncols, ncols, Y, ncols, tag);
+        spmm_device(c, A, X, ncols, ncols, Y, ncols, tag);  // (starts on the values as they land)
         allreduce_sum(c, Y, A.rows * ncols);
         return;
     }
+    consume_pending(c, const_cast<DCsr&>(A));
     const double bytes = 12.0 * A.nnz + 8.0 * (A.rows + 1) + 8.0 * ncols * (A.cols + A.rows);
     ChunkReducer red(c, Y, ncols);
     {
