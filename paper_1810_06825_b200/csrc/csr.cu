@@ -242,6 +242,53 @@ T read_scalar(Ctx& c, const T* d) {
 
 }  // namespace
 
+// item weight: nonzeros + rows (the chunk of a long row, or a group of short rows)
+__global__ void k_item_weights(const int64_t* __restrict__ rp, const WorkItem* __restrict__ items, int64_t n,
+                               int64_t* __restrict__ w, int32_t* __restrict__ idx) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const WorkItem it = items[i];
+        w[i] = it.r1 >= 0 ? (rp[it.r1] - rp[it.r0]) + (it.r1 - it.r0) : (it.p1 - it.p0) + 1;
+        idx[i] = int32_t(i);
+    }
+}
+
+__global__ void k_item_gather(const WorkItem* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                              WorkItem* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+// Within each chunk of the list (ItemList::cut_item), the heaviest items
+// first: warps take items from a global counter, so the last ones handed out
+// are the lightest and the launch's tail is short. Which warp runs an item
+// does not enter any sum (results bitwise unchanged). FRPCA_ITEM_ORDER=0 keeps
+// row order.
+void order_items_heaviest_first(Ctx& c, const DCsr& A, ItemList& L) {
+    const char* e = std::getenv("FRPCA_ITEM_ORDER");
+    if ((e && e[0] == '0') || L.nitems < 2) return;
+    cudaStream_t s = c.stream;
+    const int64_t n = L.nitems;
+    DBuf<int64_t> w(size_t(n), s), w2(size_t(n), s);
+    DBuf<int32_t> idx(size_t(n), s), idx2(size_t(n), s);
+    k_item_weights<<<grid_for(c, n), 256, 0, s>>>(A.rowptr.get(), L.items.get(), n, w.get(), idx.get());
+    FB_LAUNCH_CHECK();
+    std::vector<int32_t> hoff(L.cut_item.begin(), L.cut_item.end());
+    DBuf<int32_t> doff(hoff.size(), s);
+    FB_CUDA(cudaMemcpyAsync(doff.get(), hoff.data(), sizeof(int32_t) * hoff.size(), cudaMemcpyHostToDevice, s));
+    const int nseg = int(hoff.size()) - 1;
+    size_t tb = 0;
+    FB_CUDA(cub::DeviceSegmentedSort::StableSortPairsDescending(nullptr, tb, w.get(), w2.get(), idx.get(), idx2.get(),
+                                                                n, nseg, doff.get(), doff.get() + 1, s));
+    DBuf<unsigned char> tmp(tb, s);
+    FB_CUDA(cub::DeviceSegmentedSort::StableSortPairsDescending(tmp.get(), tb, w.get(), w2.get(), idx.get(),
+                                                                idx2.get(), n, nseg, doff.get(), doff.get() + 1, s));
+    DBuf<WorkItem> out(size_t(n), s);
+    k_item_gather<<<grid_for(c, n), 256, 0, s>>>(L.items.get(), idx2.get(), n, out.get());
+    FB_LAUNCH_CHECK();
+    L.items = std::move(out);
+    FB_CUDA(cudaStreamSynchronize(s));  // (hoff is host memory read by the copy)
+}
+
 void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_t ch) {
     const int64_t m = A.rows;
     L.nitems = L.ncomb = L.nslots = 0;
@@ -291,6 +338,7 @@ void build_items(Ctx& c, const DCsr& A, const uint8_t* skip, ItemList& L, int64_
     L.cut_row.push_back(m);
     L.cut_item.push_back(L.nitems);
     L.cut_comb.push_back(L.ncomb);
+    order_items_heaviest_first(c, A, L);
 }
 
 namespace {
