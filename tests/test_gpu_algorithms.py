@@ -201,6 +201,67 @@ def test_run_csr_equals_upload_and_run(fb, orc, algo, shape, q):
     assert np.array_equal(r1.S, r2.S) and np.array_equal(r1.U, r2.U) and np.array_equal(r1.V, r2.V)
 
 
+def _raw_run_csr(fb, m, n, rp, ci, va, algo, k=8, s=4, q=3):
+    """frpca_run_csr straight through the C ABI (no host-side validation on
+    the way): the pipelined upload's own checks are what is tested."""
+    import ctypes as C
+    from paper_1810_06825_b200 import _lib
+    ctx = fb.default_context()
+    U, S, V = np.empty(m * k), np.empty(k), np.empty(n * k)
+    c = fb.PcaConfig(k=k, oversample=s, passes=q, seed=5).to_c()
+    _lib.check(_lib.load().frpca_run_csr(ctx._h, m, n, int(rp[-1]), rp.ctypes.data, ci.ctypes.data, va.ctypes.data,
+                                         algo, C.byref(c), None, 0, 0, U.ctypes.data, S.ctypes.data,
+                                         V.ctypes.data, None, None, None))
+    return S
+
+
+@pytest.mark.parametrize("algo", [1, 0])
+@pytest.mark.parametrize("bad,msg", [("col_range", "csr: column index out of range"),
+                                     ("col_order", "csr: column indices must be strictly increasing within a row"),
+                                     ("rowptr", "csr: row_ptr must be non-decreasing")])
+def test_run_csr_invalid_input_pipelined(fb, orc, algo, bad, msg):
+    """The pipelined upload of frpca_run_csr (values in chunks, A^T built by
+    a builder thread beside the first A*X) reports an invalid CSR with the
+    reference's message (sparse_matrix.hpp:125-142) before any product, and
+    the context stays usable: the next call equals upload + run bitwise."""
+    shape = (20000, 4000) if algo == 1 else (4000, 20000)
+    oA = powerlaw_csr(orc, shape[0], shape[1], 300000, 43, a_row=1.5, a_col=1.1)
+    rp, ci, va = (np.ascontiguousarray(x) for x in oA.arrays())
+    ci = ci.astype(np.int64).copy()
+    rp = rp.astype(np.int64).copy()
+    m, n = shape
+    lens = np.diff(rp)
+    r = int(np.nonzero(lens >= 3)[0][len(np.nonzero(lens >= 3)[0]) // 2])
+    if bad == "col_range":
+        ci[rp[r] + 1] = n
+    elif bad == "col_order":
+        ci[rp[r]], ci[rp[r] + 1] = ci[rp[r] + 1], ci[rp[r]]
+    else:
+        rp[r + 1] = rp[r] - 1 if rp[r] > 0 else rp[r + 2] + 1
+    with pytest.raises(ValueError, match=msg):
+        _raw_run_csr(fb, m, n, rp, ci, va.astype(np.float64), algo)
+    rp0, ci0, va0 = (np.ascontiguousarray(x) for x in oA.arrays())
+    S1 = _raw_run_csr(fb, m, n, rp0.astype(np.int64), ci0.astype(np.int64), va0.astype(np.float64), algo)
+    f = fb.frpcat if algo == 1 else fb.frpca
+    r2 = f(to_fb(fb, oA), fb.PcaConfig(k=8, oversample=4, passes=3, seed=5))
+    assert np.array_equal(S1, r2.S)
+
+
+def test_run_csr_repeated_shapes_reuse_buffers(fb, orc):
+    """Large device buffers are recycled between calls (common.cuh BufCache):
+    alternating shapes and algorithms through frpca_run_csr still give
+    bitwise the results of a fresh upload + run."""
+    cases = [(1, (30000, 5000), 600000, 3), (0, (5000, 30000), 600000, 4), (1, (30000, 5000), 600000, 3),
+             (1, (40000, 6000), 900000, 4), (0, (5000, 30000), 600000, 4)]
+    for algo, shape, nnz, q in cases:
+        oA = powerlaw_csr(orc, shape[0], shape[1], nnz, 47 + q, a_row=1.5, a_col=1.1)
+        A = to_fb(fb, oA)
+        c = fb.PcaConfig(k=16, oversample=8, passes=q, seed=3)
+        r1, _ = fb.run_csr(A, c, fb.PcaAlgorithm(algo))
+        r2 = (fb.frpcat if algo == 1 else fb.frpca)(to_fb(fb, oA), c)
+        assert np.array_equal(r1.S, r2.S) and np.array_equal(r1.U, r2.U) and np.array_equal(r1.V, r2.V)
+
+
 def test_run_csr_errors(fb, orc):
     A = to_fb(fb, orc.Csr.random_sparse(50, 40, 0.2, 3))
     with pytest.raises(ValueError, match="frpca: requires rows <= cols"):
