@@ -641,6 +641,28 @@ int frpca_eig_svd(frpca_ctx* c, int64_t m, int64_t n, const double* Ah, double* 
     });
 }
 
+// FRPCA_DEBUG_TIMELINE (with profiling on): the call's event brackets on the
+// main stream (and the upload builder's), start / end relative to the first
+// one (diagnostic)
+static void print_timeline(Ctx& c, size_t p0) {
+    static const bool tl = std::getenv("FRPCA_DEBUG_TIMELINE") != nullptr;
+    if (!tl || !c.prof || c.pending.size() <= p0) return;
+    const cudaEvent_t base = c.pending[p0].a;
+    for (size_t i = p0; i < c.pending.size(); ++i) {
+        float t0 = 0.f, t1 = 0.f;
+        cudaEventElapsedTime(&t0, base, c.pending[i].a);
+        cudaEventElapsedTime(&t1, base, c.pending[i].b);
+        std::fprintf(stderr, "[timeline] %9.2f %9.2f %s\n", t0, t1, c.pending[i].name.c_str());
+    }
+    if (c.tside)
+        for (size_t i = c.tside->tl_mark; i < c.tside->pending.size(); ++i) {
+            float t0 = 0.f, t1 = 0.f;
+            cudaEventElapsedTime(&t0, base, c.tside->pending[i].a);
+            cudaEventElapsedTime(&t1, base, c.tside->pending[i].b);
+            std::fprintf(stderr, "[timeline] %9.2f %9.2f   builder: %s\n", t0, t1, c.tside->pending[i].name.c_str());
+        }
+}
+
 int frpca_run(frpca_ctx* c, frpca_dmat* M, int algorithm, const frpca_config* cfg, const double* omega,
               int64_t omega_rows, int64_t omega_cols, double* U, double* S, double* V, double* basis,
               frpca_stats* stats, int* dispatched) {
@@ -662,7 +684,9 @@ int frpca_run(frpca_ctx* c, frpca_dmat* M, int algorithm, const frpca_config* cf
                     algo == FRPCA_ALGO_BASIC_RPCAT,
                 "frpca_run: unknown algorithm");
         if (dispatched) *dispatched = algo;
+        const size_t p0 = c->pending.size();
         run_algorithm(*c, *M, a, stats, algo);
+        print_timeline(*c, p0);
     });
 }
 
@@ -784,26 +808,7 @@ int frpca_run_csr(frpca_ctx* c, int64_t rows, int64_t cols, int64_t nnz, const i
         dbg_mark("synced");
         M.reset();
         dbg_mark("matrix released");
-        // FRPCA_DEBUG_TIMELINE (with profiling on): the call's event brackets on
-        // the main stream, start / end relative to the first one (diagnostic)
-        static const bool tl = std::getenv("FRPCA_DEBUG_TIMELINE") != nullptr;
-        if (tl && c->prof && c->pending.size() > p0) {
-            const cudaEvent_t base = c->pending[p0].a;
-            for (size_t i = p0; i < c->pending.size(); ++i) {
-                float t0 = 0.f, t1 = 0.f;
-                cudaEventElapsedTime(&t0, base, c->pending[i].a);
-                cudaEventElapsedTime(&t1, base, c->pending[i].b);
-                std::fprintf(stderr, "[timeline] %9.2f %9.2f %s\n", t0, t1, c->pending[i].name.c_str());
-            }
-            if (c->tside)
-                for (size_t i = c->tside->tl_mark; i < c->tside->pending.size(); ++i) {
-                    float t0 = 0.f, t1 = 0.f;
-                    cudaEventElapsedTime(&t0, base, c->tside->pending[i].a);
-                    cudaEventElapsedTime(&t1, base, c->tside->pending[i].b);
-                    std::fprintf(stderr, "[timeline] %9.2f %9.2f   builder: %s\n", t0, t1,
-                                 c->tside->pending[i].name.c_str());
-                }
-        }
+        print_timeline(*c, p0);
     });
 }
 
