@@ -57,6 +57,18 @@ void count_launch();
 // ordering the pool itself would provide). Parked buffers go back to the
 // pool when an allocation fails (then retried), beyond kCacheMax bytes, or
 // when the device has less than kMinFree bytes free.
+// current device switched for a scope (restored on exit)
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 struct BufCache {
     struct Entry {
         void* p;
@@ -77,6 +89,7 @@ struct BufCache {
     }
     // back to the stream-ordered pool (no unmap: the pool keeps its memory)
     static void drop(Entry& e) {
+        DeviceScope ds(e.dev);  // (the buffer's device, whatever the caller's)
         cudaEventSynchronize(e.ev);
         cudaEventDestroy(e.ev);
         cudaFreeAsync(e.p, cudaStreamPerThread);
@@ -102,7 +115,7 @@ struct BufCache {
         cap = e.bytes;
         return e.p;
     }
-    bool give(void* p, size_t bytes, cudaStream_t s) {
+    bool give(void* p, size_t bytes, cudaStream_t s, int dev) {
         static const bool dbg = std::getenv("FRPCA_DEBUG_E2E") != nullptr;
         const auto g0 = std::chrono::steady_clock::now();
         struct Report {
@@ -119,11 +132,14 @@ struct BufCache {
                                  int(checked), drops);
             }
         } rep{dbg, g0, bytes};
-        int dev = 0;
+        DeviceScope ds(dev);  // the event belongs to the buffer's device (its last stream's)
         cudaEvent_t ev;
-        if (cudaGetDevice(&dev) != cudaSuccess) return false;
-        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return false;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
         if (cudaEventRecord(ev, s) != cudaSuccess) {
+            cudaGetLastError();  // (not left for a later launch check)
             cudaEventDestroy(ev);
             return false;
         }
@@ -140,11 +156,20 @@ struct BufCache {
             low = cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr < kMinFree;
             rep.checked = true;
         }
-        while ((held > kCacheMax || (low && held > bytes)) && parked.size() > 1) {
-            held -= parked.front().bytes;
-            drop(parked.front());
-            parked.erase(parked.begin());
-            ++rep.drops;
+        // oldest first: beyond the cap any device's, when this device is short
+        // of memory this device's
+        for (size_t k = 0; k + 1 < parked.size();) {
+            const bool over = held > kCacheMax;
+            const bool mine_low = low && parked[k].dev == dev && held > bytes;
+            if (!over && !(low && held > bytes)) break;
+            if (over || mine_low) {
+                held -= parked[k].bytes;
+                drop(parked[k]);
+                parked.erase(parked.begin() + long(k));
+                ++rep.drops;
+            } else {
+                ++k;
+            }
         }
         return true;
     }
@@ -165,15 +190,16 @@ struct DBuf {
     size_t n = 0;
     cudaStream_t s = nullptr;
     size_t cap = 0;  // bytes actually held (>= n * sizeof(T))
+    int dev = 0;     // device of the allocation
     DBuf() = default;
     DBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), cap(o.cap) { o.p = nullptr; o.n = 0; o.cap = 0; }
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), cap(o.cap), dev(o.dev) { o.p = nullptr; o.n = 0; o.cap = 0; }
     DBuf& operator=(DBuf&& o) noexcept {
         if (this != &o) {
             release();
-            p = o.p; n = o.n; s = o.s; cap = o.cap;
+            p = o.p; n = o.n; s = o.s; cap = o.cap; dev = o.dev;
             o.p = nullptr; o.n = 0; o.cap = 0;
         }
         return *this;
@@ -184,6 +210,7 @@ struct DBuf {
         s = stream;
         n = count;
         if (!count) return;
+        cudaGetDevice(&dev);
         const size_t bytes = count * sizeof(T);
         if (bytes >= BufCache::kCacheMin) {
             if (void* q = BufCache::get().take(bytes, stream, cap)) {
@@ -211,7 +238,7 @@ struct DBuf {
         }
     }
     void release() noexcept {
-        if (p && !(cap >= BufCache::kCacheMin && BufCache::get().give(p, cap, s))) cudaFreeAsync(p, s);
+        if (p && !(cap >= BufCache::kCacheMin && BufCache::get().give(p, cap, s, dev))) cudaFreeAsync(p, s);
         p = nullptr;
         n = cap = 0;
     }
