@@ -615,7 +615,7 @@ int frpca_orth(frpca_ctx* c, int64_t m, int64_t l, const double* Mh, double* Q) 
         FB_CUDA(cudaSetDevice(c->device));
         DBuf<double> W(size_t(m * l), c->stream);
         upload_colmajor(*c, Mh, m, l, m, W.get());
-        orth_device(*c, W.get(), m, l);
+        with_checks(*c, [&] { orth_device(*c, W.get(), m, l); });
         download_colmajor(*c, W.get(), m, l, Q);
     });
 }

@@ -598,6 +598,7 @@ void err_check(Ctx& c) {
     if (h == kErrLuPivot) throw NumericalError("lu_basis: zero pivot, input is rank-deficient");  // :81
     if (h == kErrEigRank) throw NumericalError("eig_svd: input does not have full numerical column rank");
     if (h == kErrEigFail) throw NumericalError("eig_svd: eigendecomposition failed to converge");  // :160-161
+    if (h == kErrOrthRank) throw NumericalError("orth: numerically rank-deficient input");  // :43-44
     if (h == kErrEigNoConv) {
         const char* mode = std::getenv("FRPCA_EIG");
         if (mode && std::strcmp(mode, "strict") == 0)

@@ -281,7 +281,8 @@ double maxabs_device(Ctx& c, const double* x, int64_t n);
 void maxabs_device_async(Ctx& c, const double* x, int64_t n, unsigned long long* out);
 
 // ---- deferred errors (driver.cu)
-constexpr int kErrLuPivot = 1, kErrEigRank = 2, kErrEigNoConv = 3, kErrOmegaShort = 4, kErrEigFail = 5;
+constexpr int kErrLuPivot = 1, kErrEigRank = 2, kErrEigNoConv = 3, kErrOmegaShort = 4, kErrEigFail = 5,
+              kErrOrthRank = 6;
 int* err_flag(Ctx& c);
 void err_reset(Ctx& c);
 // waits for the stream; throws the first recorded error (NumericalError with

@@ -61,6 +61,53 @@ def test_orth_vs_oracle(fb, orc, m, l):
     # same Householder sign convention as the reference: Q itself agrees
     assert np.abs(Q - Qo).max() < 1e-10
 
+
+# the hand-written Householder kernel (csrc/orth.cu): panels of 16 columns,
+# thread-per-column chunks of 256, one CTA per 64+ rows; shapes around every
+# one of those boundaries, against the oracle entry by entry
+@pytest.mark.parametrize("m,l", [(1, 1), (2, 1), (17, 16), (17, 17), (33, 32), (40, 31), (63, 1), (64, 48), (65, 33),
+                                 (129, 100), (600, 257), (700, 300), (1000, 513), (9473, 40), (20000, 272),
+                                 (400000, 64)])
+def test_orth_shapes(fb, orc, m, l):
+    M = orc.gaussian_matrix(m, l, 3 * m + l)
+    Q = fb.orth(M)
+    assert orthonormality(Q) < 1e-12
+    assert np.abs(Q - orc.orth(M)).max() < 1e-10
+
+
+def test_orth_deterministic_and_scaled(fb, orc):
+    M = orc.gaussian_matrix(30000, 96, 5)
+    Q1, Q2 = fb.orth(M), fb.orth(M)
+    assert np.array_equal(Q1, Q2)  # fixed-order reductions
+    # column scales over 8 decades (inside the reference's scale-dependent rank check)
+    sc = np.logspace(-4, 4, 96)
+    Qs = fb.orth(M * sc)
+    assert orthonormality(Qs) < 1e-12
+    assert np.abs(Qs - orc.orth(M * sc)).max() < 1e-10
+
+
+def test_orth_zero_tail_column(fb, orc):
+    # a column whose entries below the diagonal are exactly zero takes Eigen's
+    # tau = 0 branch (beta = c0, no reflection), :makeHouseholderInPlace
+    M = orc.gaussian_matrix(50, 4, 9)
+    M[1:, 0] = 0.0
+    Q = fb.orth(M)
+    assert np.abs(Q - orc.orth(M)).max() < 1e-12
+    M2 = np.zeros((6, 2))
+    M2[0, 0] = -2.0
+    M2[1, 1] = 3.0
+    assert np.abs(fb.orth(M2) - orc.orth(M2)).max() == 0.0
+
+
+def test_orth_rank_deficient_late_column(fb, orc):
+    # dependence only shows in the last panel; the context stays usable
+    M = orc.gaussian_matrix(3000, 40, 2)
+    M[:, 37] = M[:, 3] - 2.0 * M[:, 20]
+    with pytest.raises(fb.NumericalError, match="orth: numerically rank-deficient input"):
+        fb.orth(M)
+    G = orc.gaussian_matrix(3000, 40, 2)
+    assert np.abs(fb.orth(G) - orc.orth(G)).max() < 1e-10
+
 # --------------------------------------------------------------- baselines
 
 
