@@ -29,7 +29,8 @@ struct RunArgs {
 struct EigWork {
     DBuf<double> B, D;
     int64_t l = 0;
-    void run(Ctx& c, const double* W, int64_t r, int64_t n, bool row_sharded);
+    // keep_gram (n x n, optional): a copy of the Gram matrix before syevd overwrites it
+    void run(Ctx& c, const double* W, int64_t r, int64_t n, bool row_sharded, double* keep_gram = nullptr);
     void factor(Ctx& c, int s, int k, int ncols, bool rev, bool scale, double* M);
     void singular_values(Ctx& c, int s, int k, bool rev, double* S);
 };

@@ -18,20 +18,25 @@ __global__ void k_info_to_flag(const int* __restrict__ info, int* __restrict__ f
 
 void syevd_device(Ctx& c, double* B, int64_t n, double* d_D, bool final_step) {
     Prof prof(c, "syevd", 8.0 * n * n * 2, 4.0 / 3.0 * n * n * n);
-    // Per role:
-    //  - the final eig_svd (only its top-k pairs reach the output): the
-    //    library's own solver (syev.cu), faster than syevd at l = 200;
+    // The library's own solver (syev.cu) serves both roles by default:
+    //  - the final eig_svd (only its top-k pairs reach the output): faster
+    //    than syevd at l = 200;
     //  - the power iteration's eig_svd, whose basis Q = Z V S^-1 carries every
-    //    pair, the small ones amplified by S^-1: cuSOLVER syevd, whose small
-    //    eigenvalues are more accurate (tools/syev_accuracy.py); with it the GPU
-    //    result at C2 is closer to the long-double arbiter than the oracle on
-    //    sigma and both subspaces (profiles/r2_parity_C2_arbiter.json).
+    //    pair, the small ones amplified by S^-1. Either tridiagonal solver
+    //    resolves them to eps*lambda_max only (cuSOLVER syevd: Q^T Q - I up to
+    //    2e-4 on a panel graded over 1e12, the library's solver 1e-7, the
+    //    oracle's Jacobi 5e-9; tools/probe/eig_loop_orth.py), so eig_svd_U
+    //    (driver.cu) removes the defect with an l x l correction of the
+    //    rescale factor. With it a randomised sweep (tools/fuzz_parity.py,
+    //    520 cases, profiles/r2_fuzz_eig_loop.json) stays within 1.7x the
+    //    oracle's distance from the long-double arbiter, and C2 is 3x closer
+    //    to the arbiter than the oracle on both subspaces. DESIGN.md §3.
     // FRPCA_EIG_LOOP / FRPCA_EIG_FINAL (cusolver | small), then FRPCA_EIG
     // (cusolver | strict), override. A non-converged small solve is reported
     // by err_check, which re-runs the call with cuSOLVER (or fails when strict).
     const char* mode = std::getenv(final_step ? "FRPCA_EIG_FINAL" : "FRPCA_EIG_LOOP");
     if (!mode || !*mode) mode = std::getenv("FRPCA_EIG");
-    const bool cus = (mode && *mode) ? std::strcmp(mode, "cusolver") == 0 : !final_step;
+    const bool cus = (mode && *mode) ? std::strcmp(mode, "cusolver") == 0 : false;
     if (!cus) {
         if (syev_small(c, B, n, d_D)) return;
     }

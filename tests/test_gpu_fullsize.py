@@ -4,11 +4,14 @@ case), C1, C2, C3 (the bench workload, 12.9M x 324k, 400M nnz) and C4 (frpca,
 200k x 20M, 400M nnz; the oracle takes ~4 min on 16 threads) at full size. Bars: top-k sigma within 1e-10 relative, ||UU^T - U'U'^T||_2 and
 ||VV^T - V'V'^T||_2 within 1e-8, q passes.
 
-C2 (Poisson counts, l = 150, q = 5) sits below those bars for ANY fp64
-evaluation: the oracle itself is ~3e-10 / ~2e-8 from the same algorithm in
-80-bit long double (oracle/arbiter.cpp). There the bar is that the GPU result
-is at least as close to the long-double arbiter as the oracle is, on sigma and
-on both subspaces (the arbiter criterion)."""
+C2 (Poisson counts, l = 150, q = 5) sits below the sigma bar for ANY fp64
+evaluation: the oracle itself is 3.5e-10 / 6.7e-9 / 7.9e-9 from the same
+algorithm in 80-bit long double (oracle/arbiter.cpp), 4.4e-10 / 1.25e-8 /
+1.30e-8 with the reference's own eigensolver class (tridiagonal QL,
+FRPCA_ORACLE_EIG=ql). There the bar is that the GPU result is at least as
+close to the long-double arbiter as the oracle is, on sigma and on both
+subspaces (the arbiter criterion; measured 2.4e-10 / 2.1e-9 /
+2.6e-9, profiles/r2_parity_C2_arbiter_refined.json)."""
 import os
 import sys
 
@@ -38,3 +41,22 @@ def test_fullsize_parity_c2_arbiter(fb, orc):
     if not r["pass_direct"]:
         for key in ("sigma_rel", "subspace_U", "subspace_V"):
             assert a["gpu_vs_arbiter"][key] <= a["oracle_vs_arbiter"][key], (key, a)
+
+
+def test_fuzz_sweep(fb, orc):
+    """tools/fuzz_parity.py: 150 random cases (every kernel entry point, the
+    fast and the baseline algorithms; uniform and power-law sparsity, empty
+    and very long rows, values over many orders of magnitude, k up to 150)
+    against the oracle at the north_star bars; fast runs above the direct bars
+    (ill-conditioned q-pass products) must stay within 4x the oracle's own
+    distance from the long-double arbiter, the oracle evaluated with either of
+    its eigensolvers (measured worst ratio over 520 cases: 1.7)."""
+    import json
+    import subprocess
+    tool = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "fuzz_parity.py")
+    p = subprocess.run([sys.executable, tool, "--cases", "150", "--seed", "7", "--kmax", "150", "--smax", "80"],
+                       capture_output=True, text=True)
+    rep = json.loads(p.stdout.strip().splitlines()[-1])
+    print(rep["worst"], rep["counts"])
+    assert rep["failures"] == [], rep["failures"]
+    assert p.returncode == 0

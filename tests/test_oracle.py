@@ -235,6 +235,28 @@ def test_eig_svd_vs_jacobi(orc):  # test_dense_kernels.cpp:159-165
     assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-10
 
 
+def test_eig_svd_ql_variant(orc, monkeypatch):
+    # FRPCA_ORACLE_EIG=ql: the tridiagonal-QL evaluation (the reference's own
+    # solver class, oracle.cpp eig_sym_lower_ql) agrees with the Jacobi default
+    # on a well-conditioned panel and meets the same known answers; on a graded
+    # panel its small singular values are of absolute accuracy only
+    A = orc.gaussian_matrix(300, 40, 23)
+    Uj, Sj, Vj = orc.eig_svd(A)
+    G = orc.gaussian_matrix(400, 40, 5) * np.exp(-np.arange(40) / 5.0)
+    _, Sgj, _ = orc.eig_svd(G)
+    monkeypatch.setenv("FRPCA_ORACLE_EIG", "ql")
+    U, S, V = orc.eig_svd(A)
+    assert np.max(np.abs(S - Sj) / Sj) < 1e-13
+    assert np.all(np.diff(S) >= 0)
+    assert orthonormality(U) < 1e-12 and orthonormality(V) < 1e-13
+    assert np.linalg.norm(A - (U * S) @ V.T) / np.linalg.norm(A) < 1e-13
+    _, S3, _ = orc.eig_svd(np.eye(3))
+    assert np.abs(S3 - 1).max() < 1e-14
+    _, Sg, _ = orc.eig_svd(G)
+    rel = np.abs(Sg - Sgj) / Sgj
+    assert rel[-1] < 1e-14 and rel.max() < 1e-16 * (Sgj[-1] / Sgj[0]) ** 2 * 100
+
+
 def test_eig_svd_rank_deficient(orc):  # test_dense_kernels.cpp:167-172
     A = orc.gaussian_matrix(5, 3, 1)
     A[:, 2] = A[:, 0] + A[:, 1]

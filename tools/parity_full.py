@@ -70,8 +70,19 @@ def run(name: str, threads: int | None = None, scale: float = 1.0, floor: bool =
         dist = lambda U, S, V: {"sigma_rel": sigma_rel(S, a["S"]), "subspace_U": subspace_dist(a["U"], U),
                                 "subspace_V": subspace_dist(a["V"], V)}
         g, c = dist(r.U, r.S, r.V), dist(o["U"], o["S"], o["V"])
-        arb = {"gpu_vs_arbiter": g, "oracle_vs_arbiter": c,
+        # the oracle again with the reference's own eigensolver class
+        # (Householder tridiagonalisation + implicit QL, oracle.cpp
+        # eig_sym_lower_ql) in place of the Jacobi default
+        os.environ["FRPCA_ORACLE_EIG"] = "ql"
+        try:
+            oq = oracle.pca(oracle.Csr.create(m, n, rp, ci, va), algo_o, cfg.k, cfg.s, cfg.q, seed=0)
+        finally:
+            del os.environ["FRPCA_ORACLE_EIG"]
+        cq = dist(oq["U"], oq["S"], oq["V"])
+        del oq
+        arb = {"gpu_vs_arbiter": g, "oracle_vs_arbiter": c, "oracle_ql_vs_arbiter": cq,
                "gpu_no_worse": bool(all(g[k] <= c[k] for k in g)),
+               "gpu_within_oracle_solvers": bool(all(g[k] <= max(c[k], cq[k]) for k in g)),
                "oracle_fma_vs_arbiter": dist(o2["U"], o2["S"], o2["V"]) if o2 is not None else None,
                "seconds": round(time.time() - t0, 1),
                "what": "oracle/arbiter.cpp: the same algorithm in 80-bit long double, same CSR and Omega"}
