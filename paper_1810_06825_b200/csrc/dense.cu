@@ -1188,7 +1188,9 @@ void gemm_device(Ctx& c, const double* W, int64_t r, int64_t K, const double* M,
             const int64_t nc = std::min<int64_t>(PCOLS, N - c0);
             double* Cc = col_major_out ? C + c0 * ldc : C + c0;
             const int ntiles = int((nc + 7) / 8);
-            const int WC = ntiles <= 8 ? 1 : 2;
+            // a warp holds at most 7 column tiles (<4, 7>): 8 tiles (57-64 columns)
+            // go to two column groups of 4, not to one group of 8
+            const int WC = ntiles <= 7 ? 1 : 2;
             const int nt = (ntiles + WC - 1) / WC;
             const char* ge = std::getenv("FRPCA_GEMM_CPASYNC");  // A/B and tests
             const bool tma = !(ge && *ge == '1');

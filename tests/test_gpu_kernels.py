@@ -6,7 +6,7 @@ inputs (FMA vs separate mul/add is the only difference in a row's sum)."""
 import numpy as np
 import pytest
 
-from metrics import SPMM_TOL, orth, orthonormality, projector_gap_dense, rel_fro, subspace_dist
+from metrics import SPMM_TOL, orth, orthonormality, projector_gap_dense, rel_fro, sigma_rel, subspace_dist
 
 pytestmark = pytest.mark.gpu
 
@@ -506,6 +506,36 @@ def test_gram4_bulk_copies_equal_gram3(fb, orc, monkeypatch, m, n):
     r2 = fb.eig_svd(A)
     for x, y in zip(r1, r2):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("kernel", ["tma", "cpasync"])
+def test_rescale_gemm_every_width(fb, orc, monkeypatch, kernel):
+    """eig_svd of a 4100-row panel at every width 1..232: the persistent
+    rescale GEMM (r >= 4096) splits the output columns into chunks of <= 104
+    and each chunk's 8-column tiles over one or two warp groups of <= 7 tiles.
+    Found by the randomised sweep: a chunk of exactly 8 tiles (57-64 columns,
+    i.e. l or k in 57..64 and 161..168) went to one group and lost its last
+    tile."""
+    if kernel == "cpasync":
+        monkeypatch.setenv("FRPCA_GEMM_CPASYNC", "1")
+    G = orc.gaussian_matrix(4100, 232, 77)
+    for n in range(1, 233):
+        A = np.ascontiguousarray(G[:, :n])
+        U, S, V = fb.eig_svd(A)
+        assert np.abs((U * S) @ V.T - A).max() <= 1e-10, n
+        assert orthonormality(U) <= 1e-10, n
+
+
+@pytest.mark.parametrize("k,s", [(57, 0), (60, 10), (64, 0), (50, 10), (63, 100), (100, 62)])
+def test_run_outputs_at_eight_tile_widths(fb, orc, k, s):
+    # the column-major k-of-l outputs of a run (U: 6000 rows) at those widths
+    oA = powerlaw_csr(orc, 6000, 400, 150000, 3)
+    A = to_fb(fb, oA)
+    r = fb.frpcat(A, fb.PcaConfig(k=k, oversample=s, passes=3, seed=2))
+    o = orc.pca(oA, orc.FRPCAT, k, s, seed=2, passes=3)
+    assert sigma_rel(r.S, o["S"]) <= 1e-10
+    assert subspace_dist(o["U"], r.U) <= 1e-8 and subspace_dist(o["V"], r.V) <= 1e-8
+    assert np.abs(np.abs(np.sum(r.U * o["U"], axis=0)) - 1).max() <= 1e-8
 
 
 @pytest.mark.parametrize("m,n", [(4096, 16), (5000, 40), (70001, 150), (123457, 200), (4100, 208)])
