@@ -118,6 +118,14 @@ def main():
                 note("spmm_transpose", rel_fro(fb.spmm_transpose(A, Y), orc.spmm_transpose(oA, Y)), 1e-12, case)
             elif kind in ("pca", "basic"):
                 m, n = int(rng.integers(8, 3000)), int(rng.integers(8, 3000))
+                # a third of the cases are long in one dimension: the dense
+                # kernels switch to their persistent variants at 4096 rows
+                stretch = int(rng.integers(0, 3))
+                if stretch == 0:
+                    if rng.random() < 0.5:
+                        m = int(rng.integers(4096, 14000))
+                    else:
+                        n = int(rng.integers(4096, 14000))
                 lmax = min(m, n)
                 k = int(rng.integers(1, max(2, min(lmax, a.kmax))))
                 s = int(rng.integers(0, max(1, min(lmax - k, a.smax)) + 1))
@@ -192,7 +200,10 @@ def main():
                     noisy.append({"case": case, "gpu_vs_oracle": d, "gpu_vs_arbiter": g, "oracle_vs_arbiter": c,
                                   "oracle_ql_vs_arbiter": cq})
                     for key in g:
-                        note("arbiter_ratio_" + key, g[key] / max(c[key], cq[key], bars[key] * 1e-3), 4.0, case)
+                        if d[key] <= bars[key]:  # this metric meets its direct bar
+                            note(kind + "_" + key, d[key], bars[key], case)
+                        else:
+                            note("arbiter_ratio_" + key, g[key] / max(c[key], cq[key], bars[key] * 1e-3), 4.0, case)
                 else:
                     for key in d:
                         note(kind + "_" + key, d[key], bars[key], case)
