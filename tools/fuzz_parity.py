@@ -69,6 +69,19 @@ def random_csr(rng, m, n):
     return orc.Csr.create(m, n, rp, c.astype(np.int64), v)
 
 
+def big_csr(rng, m, n, nnz):
+    """Large case, vectorised: uniform rows, Zipf columns over a permutation, a few long rows."""
+    r = rng.integers(0, m, nnz)
+    r[: nnz // 20] = rng.integers(0, 3)  # three long rows (chunked + combined)
+    c = rng.permutation(n)[np.minimum(rng.zipf(1.2, nnz), n) - 1]
+    key = np.unique(r.astype(np.int64) * n + c)
+    r, c = key // n, key % n
+    v = rng.standard_normal(r.size)
+    rp = np.zeros(m + 1, dtype=np.int64)
+    np.add.at(rp, r + 1, 1)
+    return orc.Csr.create(m, n, np.cumsum(rp), c.astype(np.int64), v)
+
+
 def to_fb(oA):
     rp, ci, va = oA.arrays()
     return fb.SparseMatrixCsr(oA.rows, oA.cols, rp, ci, va)
@@ -107,7 +120,13 @@ def main():
             if kind == "spmm":
                 m, n = int(rng.integers(1, 4000)), int(rng.integers(1, 3000))
                 w = int(rng.choice([1, 2, 3, 7, 31, 32, 33, 64, 100, 129, 200, 256, 257, 300]))
-                oA = random_csr(rng, m, n)
+                if rng.random() < 0.2:
+                    # large enough for the L2 hints of A*X and the panel plan of A^T*Y
+                    m, n = int(rng.integers(60000, 400000)), int(rng.integers(20000, 120000))
+                    w = int(rng.choice([64, 150, 200, 256]))
+                    oA = big_csr(rng, m, n, int(rng.integers(1, 5) * 1000000))
+                else:
+                    oA = random_csr(rng, m, n)
                 A = to_fb(oA)
                 case.update(m=m, n=n, w=w)
                 X = rng.standard_normal((n, w))
@@ -209,6 +228,8 @@ def main():
                         note(kind + "_" + key, d[key], bars[key], case)
             else:
                 m = int(rng.integers(1, 6000))
+                if rng.random() < 0.2:
+                    m = int(rng.integers(6000, 300000))  # the global-panel LU, split Grams
                 l = int(rng.integers(1, min(max(m // 2, 1), 300) + 1))  # well-conditioned Gaussian panels
                 case.update(m=m, l=l)
                 M = rng.standard_normal((m, l))
