@@ -801,7 +801,15 @@ void spmm_device(Ctx& c, const DCsr& A, const double* X, int64_t ldx, int64_t nc
             FB_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
         }
         const cudaStream_t s0 = c.stream;
-        const bool alt = env_double("FRPCA_PIPE_ALT", 1.0) != 0.0;
+        // (only where a chunk is ONE launch over its own partial slots: the
+        // scalar path of an odd or unaligned width runs slices of <= 128
+        // columns that re-use the partial buffer at another stride, so two
+        // chunks in flight on two streams overwrote each other's partials --
+        // odd l > 128 through frpca_run_csr, found by the randomised sweep)
+        const bool one_launch = ncols <= 128 || (ncols % 2 == 0 && ldx % 2 == 0 && ldy % 2 == 0 &&
+                                                 reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+                                                 reinterpret_cast<uintptr_t>(Y) % 16 == 0);
+        const bool alt = env_double("FRPCA_PIPE_ALT", 1.0) != 0.0 && one_launch;
         FB_CUDA(cudaEventRecord(c.ev_fork, s0));
         FB_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
         for (size_t k = 0; k + 1 < A.L.cut_row.size(); ++k) {

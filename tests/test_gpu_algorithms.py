@@ -201,6 +201,40 @@ def test_run_csr_equals_upload_and_run(fb, orc, algo, shape, q):
     assert np.array_equal(r1.S, r2.S) and np.array_equal(r1.U, r2.U) and np.array_equal(r1.V, r2.V)
 
 
+@pytest.mark.parametrize("k,s", [(135, 14), (129, 0), (140, 9), (100, 31), (200, 33), (64, 63), (150, 0)])
+@pytest.mark.parametrize("algo,shape,q", [(1, (1067, 551), 4), (1, (1067, 551), 2), (1, (1067, 551), 3),
+                                          (0, (600, 2400), 4), (0, (600, 2400), 3)])
+def test_run_csr_odd_widths(fb, orc, algo, shape, q, k, s):
+    """The pipelined one-shot call at odd sketch widths past 128 columns: the
+    scalar SpMM path runs in slices of <= 128 columns that re-use the partial
+    buffer, so its item chunks must not alternate between two streams (found
+    by the randomised sweep: sigma off by 7e-3 at l = 149, even q). Long rows
+    (chunked, combined) and several item chunks; bitwise equal to upload + run."""
+    m, n = shape
+    oA = powerlaw_csr(orc, m, n, 60000, 19, a_row=1.3, a_col=1.1)
+    A = to_fb(fb, oA)
+    c = fb.PcaConfig(k=k, oversample=s, passes=q, seed=5)
+    f = {0: fb.frpca, 1: fb.frpcat}[algo]
+    r2 = f(to_fb(fb, oA), c)
+    for _ in range(3):
+        r1, _ = fb.run_csr(A, c, fb.PcaAlgorithm(algo))
+        assert np.array_equal(r1.S, r2.S) and np.array_equal(r1.U, r2.U) and np.array_equal(r1.V, r2.V)
+
+
+def test_run_csr_sweep_case(fb):
+    """The sweep's own reproducer of that defect (tests/golden/run_csr/: case 77 of
+    `tools/fuzz_parity.py --seed 52 --kinds pca --kmax 170 --smax 80 --dump`,
+    1067 x 551, l = 149, q = 4)."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "run_csr", "case_52_77.npz"))
+    m, n, k, s, q, seed = (int(z[x]) for x in ("m", "n", "k", "s", "q", "seed"))
+    A = fb.SparseMatrixCsr(m, n, z["rp"], z["ci"], z["va"])
+    c = fb.PcaConfig(k=k, oversample=s, passes=q, seed=seed)
+    r2 = fb.frpcat(A, c)
+    r1, _ = fb.run_csr(A, c, fb.PcaAlgorithm.Frpcat)
+    assert np.array_equal(r1.S, r2.S) and np.array_equal(r1.U, r2.U) and np.array_equal(r1.V, r2.V)
+
+
 def _raw_run_csr(fb, m, n, rp, ci, va, algo, k=8, s=4, q=3):
     """frpca_run_csr straight through the C ABI (no host-side validation on
     the way): the pipelined upload's own checks are what is tested."""

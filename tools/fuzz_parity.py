@@ -95,6 +95,7 @@ def main():
     ap.add_argument("--kmax", type=int, default=60)
     ap.add_argument("--smax", type=int, default=40)
     ap.add_argument("--only", type=int, nargs="*", help="evaluate only these case numbers (same draws)")
+    ap.add_argument("--dump", default="", help="directory: save the CSR and parameters of the evaluated pca cases")
     a = ap.parse_args()
     orc.build()
     rng = np.random.default_rng(a.seed)
@@ -168,6 +169,10 @@ def main():
                 if skip:
                     continue
                 case.update(m=m, n=n, k=k, s=s, q=q, algo=int(algo), seed=seed)
+                if a.dump and kind == "pca":
+                    rp_, ci_, va_ = oA.arrays()
+                    np.savez(os.path.join(a.dump, "case_%d_%d.npz" % (a.seed, it)), rp=rp_, ci=ci_, va=va_, m=m, n=n,
+                             k=k, s=s, q=q, seed=seed, algo=int(algo))
                 try:
                     o = orc.pca(oA, algo, k, s, seed=seed, **kw)
                 except (orc.NumericalError, ValueError) as e:
@@ -178,6 +183,31 @@ def main():
                         counts["rejected_by_both"] = counts.get("rejected_by_both", 0) + 1
                     continue
                 r = f(A, cfg)
+                if kind == "pca":
+                    # the one-shot call from host buffers (frpca_run_csr: upload
+                    # pipelined with the sketch and the first product) must be
+                    # the same computation as upload + run
+                    r1, _ = fb.run_csr(A, cfg, fb.PcaAlgorithm.Frpca if algo == orc.FRPCA else fb.PcaAlgorithm.Frpcat)
+                    same = np.array_equal(r1.S, r.S) and np.array_equal(r1.U, r.U) and np.array_equal(r1.V, r.V)
+                    if not same:
+                        case["run_csr_vs_upload_run"] = {"sigma": sigma_rel(r1.S, r.S), "U": subspace_dist(r.U, r1.U),
+                                                         "V": subspace_dist(r.V, r1.V)}
+                    note("run_csr_differs_from_upload_run", 0.0 if same else 1.0, 0.0, case)
+                    if it % 4 == 0:
+                        # the sharded drivers through the loopback group (2 or 3
+                        # ranks on this device) against the unsharded run
+                        world = 2 + (it // 4) % 2
+                        g = fb.Group([0] * world)
+                        try:
+                            rg, _ = g.run(A, cfg, fb.PcaAlgorithm.Frpca if algo == orc.FRPCA else fb.PcaAlgorithm.Frpcat)
+                        finally:
+                            g.close()
+                        counts["sharded"] = counts.get("sharded", 0) + 1
+                        sharded = {"S": rg.S, "U": rg.U, "V": rg.V}
+                else:
+                    sharded = None
+                if kind != "pca" or it % 4 != 0:
+                    sharded = None
                 # the bars hold where the k-th singular value is separated from
                 # round-off: a numerically rank-deficient case is compared on
                 # its well-conditioned leading part only
@@ -218,6 +248,14 @@ def main():
                         del os.environ["FRPCA_ORACLE_EIG"]
                     noisy.append({"case": case, "gpu_vs_oracle": d, "gpu_vs_arbiter": g, "oracle_vs_arbiter": c,
                                   "oracle_ql_vs_arbiter": cq})
+                    if sharded is not None:
+                        gs, ds = dist(sharded, arb), dist(sharded, o)
+                        for key in gs:
+                            if ds[key] <= bars[key]:
+                                note("sharded_" + key, ds[key], bars[key], case)
+                            else:
+                                note("sharded_arbiter_ratio_" + key,
+                                     gs[key] / max(c[key], cq[key], bars[key] * 1e-3), 4.0, case)
                     for key in g:
                         if d[key] <= bars[key]:  # this metric meets its direct bar
                             note(kind + "_" + key, d[key], bars[key], case)
@@ -226,6 +264,20 @@ def main():
                 else:
                     for key in d:
                         note(kind + "_" + key, d[key], bars[key], case)
+                    if sharded is not None:
+                        ds = dist(sharded, o)
+                        if any(ds[key] > bars[key] for key in ds):
+                            # a different split of the same sums: judged like the unsharded run
+                            rp, ci, va = oA.arrays()
+                            arb = orc.arbiter_pca(m, n, rp, ci, va, algo, k, s, q, seed=seed)
+                            gs, c = dist(sharded, arb), dist(o, arb)
+                            noisy.append({"case": case, "sharded_vs_oracle": ds, "sharded_vs_arbiter": gs,
+                                          "oracle_vs_arbiter": c})
+                        for key in ds:
+                            if ds[key] <= bars[key]:
+                                note("sharded_" + key, ds[key], bars[key], case)
+                            else:
+                                note("sharded_arbiter_ratio_" + key, gs[key] / max(c[key], bars[key] * 1e-3), 4.0, case)
             else:
                 m = int(rng.integers(1, 6000))
                 if rng.random() < 0.2:
