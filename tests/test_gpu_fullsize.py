@@ -44,17 +44,19 @@ def test_fullsize_parity_c2_arbiter(fb, orc):
 
 
 def test_fuzz_sweep(fb, orc):
-    """tools/fuzz_parity.py: 150 random cases (every kernel entry point, the
-    fast and the baseline algorithms; uniform and power-law sparsity, empty
-    and very long rows, values over many orders of magnitude, k up to 150)
-    against the oracle at the north_star bars; fast runs above the direct bars
+    """tools/fuzz_parity.py: 210 random cases (every kernel entry point, the
+    fast and the baseline algorithms, the one-shot frpca_run_csr bitwise against
+    upload + run, 2- and 3-rank loopback groups, the load step and the
+    validation metrics; uniform and power-law sparsity, empty and very long
+    rows, values over many orders of magnitude, shapes stretched past 4096 rows
+    or columns, k up to 150) against the oracle at the north_star bars; fast runs above the direct bars
     (ill-conditioned q-pass products) must stay within 4x the oracle's own
     distance from the long-double arbiter, the oracle evaluated with either of
     its eigensolvers (measured worst ratio over 520 cases: 1.7)."""
     import json
     import subprocess
     tool = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "fuzz_parity.py")
-    p = subprocess.run([sys.executable, tool, "--cases", "150", "--seed", "7", "--kmax", "150", "--smax", "80"],
+    p = subprocess.run([sys.executable, tool, "--cases", "210", "--seed", "7", "--kmax", "150", "--smax", "80"],
                        capture_output=True, text=True)
     rep = json.loads(p.stdout.strip().splitlines()[-1])
     print(rep["worst"], rep["counts"])

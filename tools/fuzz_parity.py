@@ -91,7 +91,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=150)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--kinds", default="spmm,pca,pca,dense,basic", help="case kinds, dealt round-robin")
+    ap.add_argument("--kinds", default="spmm,pca,pca,dense,basic,load,valid", help="case kinds, dealt round-robin")
     ap.add_argument("--kmax", type=int, default=60)
     ap.add_argument("--smax", type=int, default=40)
     ap.add_argument("--only", type=int, nargs="*", help="evaluate only these case numbers (same draws)")
@@ -278,6 +278,77 @@ def main():
                                 note("sharded_" + key, ds[key], bars[key], case)
                             else:
                                 note("sharded_arbiter_ratio_" + key, gs[key] / max(c[key], bars[key] * 1e-3), 4.0, case)
+            elif kind == "load":
+                # from_triplets on the device (<= 2 entries per coordinate, exact
+                # zeros dropped) and the Matrix Market writer/reader round trip
+                m, n = int(rng.integers(1, 3000)), int(rng.integers(1, 3000))
+                nt = int(rng.integers(0, 60000))
+                r = rng.integers(0, m, nt)
+                c = rng.integers(0, n, nt)
+                key = np.unique(r.astype(np.int64) * n + c)
+                r, c = key // n, key % n
+                v = rng.standard_normal(r.size)
+                dup = rng.random(r.size) < 0.2          # a second entry at the same coordinate
+                cancel = rng.random(r.size) < 0.3       # ... a third of which cancel exactly
+                r2, c2 = r[dup], c[dup]
+                v2 = np.where(cancel[dup], -v[dup], rng.standard_normal(int(dup.sum())))
+                order = rng.permutation(r.size + r2.size)
+                tr = np.concatenate([r, r2])[order]
+                tc = np.concatenate([c, c2])[order]
+                tv = np.concatenate([v, v2])[order]
+                case.update(m=m, n=n, triplets=int(tr.size))
+                if skip:
+                    continue
+                oA = orc.Csr.from_triplets(m, n, list(zip(tr.tolist(), tc.tolist(), tv.tolist())))
+                orp, oci, ova = oA.arrays()
+                for dev in (False, True):
+                    A = fb.SparseMatrixCsr.from_triplets(m, n, (tr, tc, tv), device=dev)
+                    same = (np.array_equal(A.rowPtr(), orp) and np.array_equal(A.colIdx(), oci)
+                            and np.array_equal(A.values(), ova))
+                    note("from_triplets_device" if dev else "from_triplets_host", 0.0 if same else 1.0, 0.0, case)
+                import tempfile
+                with tempfile.TemporaryDirectory() as td:
+                    path = os.path.join(td, "a.mtx")
+                    fb.write_matrix_market(path, A)
+                    B = fb.load_matrix_market(path)
+                    same = (B.rows() == m and B.cols() == n and np.array_equal(B.rowPtr(), orp)
+                            and np.array_equal(B.colIdx(), oci) and np.array_equal(B.values(), ova))
+                    note("matrix_market_round_trip", 0.0 if same else 1.0, 0.0, case)
+            elif kind == "valid":
+                # validation metrics on the GPU against the oracle's (validation.hpp:125-332)
+                m, n = int(rng.integers(20, 1500)), int(rng.integers(20, 1500))
+                oA = random_csr(rng, m, n)
+                A = to_fb(oA)
+                k = int(rng.integers(1, min(m, n, 40)))
+                seed = int(rng.integers(0, 1 << 30))
+                case.update(m=m, n=n, k=k, seed=seed)
+                if skip:
+                    continue
+                algo = orc.FRPCA if m <= n else orc.FRPCAT
+                try:
+                    o = orc.pca(oA, algo, k, min(5, min(m, n) - k), seed=seed, passes=3)
+                except (orc.NumericalError, ValueError):
+                    continue
+                res = fb.SvdResult(o["U"], o["S"], o["V"])
+                for norm, name in ((fb.ErrorNorm.Frobenius, "fro"), (fb.ErrorNorm.Spectral, "spec")):
+                    e_o = orc.low_rank_error(oA, o["U"], o["S"], o["V"], int(norm))
+                    e_g = fb.low_rank_error(A, res, norm)
+                    note("low_rank_error_" + name, abs(e_g - e_o) / max(e_o, 1e-300), 1e-6 if name == "spec" else 1e-9, case)
+                    e_g2 = fb.low_rank_error(A, res, norm, entry_limit=1)   # the matrix-free / cross-term path
+                    note("low_rank_error_" + name + "_matrix_free", abs(e_g2 - e_o) / max(e_o, 1e-300),
+                         1e-6 if name == "spec" else 1e-7, case)
+                P = np.linalg.qr(rng.standard_normal((m, k)))[0]
+                note("pc_correlation", np.abs(fb.pc_correlation(o["U"], P) - orc.pc_correlation(o["U"], P)).max(), 1e-12, case)
+                def guarded(f):  # the reference rejects a basis that is not orthonormal within 1e-8
+                    try:
+                        return f(o["U"], P)
+                    except ValueError as e:
+                        return str(e)
+                pg, po = guarded(fb.projector_distance), guarded(orc.projector_distance)
+                if isinstance(pg, str) or isinstance(po, str):
+                    note("projector_distance_rejection_differs", 0.0 if pg == po else 1.0, 0.0, case)
+                else:
+                    note("projector_distance", abs(pg - po), 1e-9, case)
             else:
                 m = int(rng.integers(1, 6000))
                 if rng.random() < 0.2:
