@@ -94,6 +94,7 @@ def main():
     ap.add_argument("--kinds", default="spmm,pca,pca,dense,basic,load,valid", help="case kinds, dealt round-robin")
     ap.add_argument("--kmax", type=int, default=60)
     ap.add_argument("--smax", type=int, default=40)
+    ap.add_argument("--qmax", type=int, default=7, help="largest pass count q of the fast algorithms")
     ap.add_argument("--only", type=int, nargs="*", help="evaluate only these case numbers (same draws)")
     ap.add_argument("--dump", default="", help="directory: save the CSR and parameters of the evaluated pca cases")
     a = ap.parse_args()
@@ -150,7 +151,7 @@ def main():
                 k = int(rng.integers(1, max(2, min(lmax, a.kmax))))
                 s = int(rng.integers(0, max(1, min(lmax - k, a.smax)) + 1))
                 s = min(s, lmax - k)
-                q = int(rng.integers(2, 8)) if kind == "pca" else int(rng.integers(0, 3))
+                q = int(rng.integers(2, a.qmax + 1)) if kind == "pca" else int(rng.integers(0, 3))
                 oA = random_csr(rng, m, n)
                 A = to_fb(oA)
                 seed = int(rng.integers(0, 1 << 30))
